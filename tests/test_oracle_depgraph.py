@@ -1,0 +1,139 @@
+"""Pins for the depth / k-set oracle (§4): the Figure-1 worked values,
+the definition's O(n^3) edge test, Appendix B, topological sort, O(n^2) brute
+force and the streaming recurrence in oracle.c must all agree, and k-sets must
+satisfy Properties 1 and 2."""
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import depgraph as g
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _streaming(pool):
+    """oracle.c orc_depths on a pool of (item, mode) lists."""
+    items, modes, off = [], [], [0]
+    names = {}
+    for txn in pool:
+        m = {}
+        for it, md in txn:
+            m[it] = 'W' if (md == 'W' or m.get(it) == 'W') else 'R'
+        for it, md in m.items():
+            items.append(names.setdefault(it, len(names)))
+            modes.append(1 if md == 'W' else 0)
+        off.append(len(items))
+    return list(oracle.depths_from_ops(np.array(off, np.uint64), np.array(items, np.uint64),
+                                       np.array(modes, np.uint8)))
+
+
+def test_figure1_worked_example():
+    fx = json.load(open(os.path.join(GOLD, "figure1.json")))
+    pool = [[tuple(op) for op in t] for t in fx["pool"]]
+    edges = g.graph_by_definition(pool)
+    assert edges == {tuple(e) for e in fx["edges"]}
+    for e in fx["absent_edges"]:
+        assert tuple(e) not in edges
+    assert g.graph_appendix_b(pool) == edges
+    assert g.topo_depths(len(pool), edges) == fx["depths"]
+    assert g.depths_bruteforce(pool) == fx["depths"]
+    assert _streaming(pool) == fx["depths"]
+    assert g.literal_rank_rule(pool) == fx["ranks_group_a"]   # single-item pool: rule is exact
+    assert g.ksets(fx["depths"]) == fx["ksets"]
+
+
+def test_literal_rank_rule_counterexample():
+    fx = json.load(open(os.path.join(GOLD, "rank_rule_counterexample.json")))
+    pool = [[tuple(op) for op in t] for t in fx["pool"]]
+    assert g.literal_rank_rule(pool) == fx["literal_rule_depths"]
+    assert g.topo_depths(3, g.graph_by_definition(pool)) == fx["true_depths"]
+    assert _streaming(pool) == fx["true_depths"]
+    ok, _ = g.check_properties(pool, fx["literal_rule_depths"])
+    assert not ok                                       # literal k-sets violate Property 1
+
+
+def _closure(n, edges):
+    reach = [set() for _ in range(n)]
+    for v in range(n - 1, -1, -1):
+        for a, b in edges:
+            if a == v:
+                reach[v] |= {b} | reach[b]
+    return reach
+
+
+def _same_order(n, e_def, e_b):
+    """Appendix B adds edges per item and does not test condition (c) across items,
+    so it may add t1 -> t2 implied by a path through a third transaction
+    (DESIGN.md R-S8): a superset with the same reachability (hence depths)."""
+    return e_def <= e_b and _closure(n, e_def) == _closure(n, e_b)
+
+
+def _footprints(items):
+    fps = []
+    for k in range(1, len(items) + 1):
+        for sub in itertools.combinations(items, k):
+            for modes in itertools.product("RW", repeat=k):
+                fps.append(list(zip(sub, modes)))
+    return fps
+
+
+def test_exhaustive_small_pools():
+    """Every pool of <= 3 transactions over 3 items (26 footprints each)."""
+    fps = _footprints(["a", "b", "c"])
+    assert len(fps) == 26
+    count = 0
+    for n in (1, 2, 3):
+        for pool in itertools.product(fps, repeat=n):
+            pool = list(pool)
+            edges = g.graph_by_definition(pool)
+            eb = g.graph_appendix_b(pool)
+            assert _same_order(n, edges, eb)
+            d = g.topo_depths(n, edges)
+            assert g.topo_depths(n, eb) == d
+            assert g.depths_bruteforce(pool) == d
+            ok, msg = g.check_properties(pool, d)
+            assert ok, msg
+            count += 1
+    assert count == 26 + 26 ** 2 + 26 ** 3
+
+
+def test_streaming_matches_graph_random():
+    rng = random.Random(5)
+    for _ in range(400):
+        n = rng.randint(1, 12)
+        nitems = rng.randint(1, 5)
+        pool = [[(rng.randrange(nitems), rng.choice("RW")) for _ in range(rng.randint(0, 3))]
+                for _ in range(n)]
+        edges = g.graph_by_definition(pool)
+        d = g.topo_depths(n, edges)
+        eb = g.graph_appendix_b(pool)
+        assert _same_order(n, edges, eb)
+        assert g.topo_depths(n, eb) == d
+        assert g.depths_bruteforce(pool) == d
+        assert _streaming(pool) == d
+        ok, msg = g.check_properties(pool, d)
+        assert ok, msg
+
+
+def test_literal_rule_exact_for_single_op_transactions():
+    rng = random.Random(9)
+    for _ in range(300):
+        n = rng.randint(1, 15)
+        pool = [[(rng.randrange(3), rng.choice("RW"))] for _ in range(n)]
+        assert g.literal_rank_rule(pool) == g.depths_bruteforce(pool)
+
+
+def test_reads_only_single_kset():
+    pool = [[("x", "R")] for _ in range(10)]
+    assert _streaming(pool) == [0] * 10
+    assert g.graph_by_definition(pool) == set()
+
+
+def test_empty_pool():
+    assert _streaming([]) == []
+    assert g.depths_bruteforce([]) == []

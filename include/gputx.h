@@ -1,0 +1,188 @@
+/*
+ * gputx.h — C ABI of the B200-native GPUTx bulk transaction engine.
+ *
+ * Implements the bulk execution model of He & Yu, "High-Throughput Transaction
+ * Executions on Graphics Processors", PVLDB 4(5) 2011 (arXiv 1103.3105):
+ *   - a bulk of stored-procedure transactions <id, type, params> (§3.2)
+ *   - executed on the GPU so that the final database and every transaction's
+ *     output equal serial execution in increasing timestamp order
+ *     (Definition 1, §3.1)
+ *   - under one of three strategies (§5):
+ *       GPUTX_TPL  two-phase locking with ts-ordered counter locks (§5.1, App. C Fig. 11)
+ *       GPUTX_PART one thread per partition, partitions run serially (§5.2)
+ *       GPUTX_KSET k-set by k-set execution of the T-dependency graph (§4, §5.3)
+ *
+ * Conventions (every function):
+ *   - returns gputx_status; nothing throws or aborts across the ABI; on error
+ *     gputx_last_error(db) describes it (valid until the next call on db).
+ *   - a gputx_db owns ALL device memory it uses; callers own every pointer they pass
+ *     and may reuse it as soon as the call returns.
+ *   - a handle is not thread-safe: one host thread per handle.
+ *   - "host" pointers are ordinary (pinned or pageable) host memory; "device"
+ *     pointers are CUDA device memory of cfg.device.
+ *   - all work is ordered on the handle's stream (cfg.stream or a library stream).
+ *
+ * Schemas, type ids and parameter words (u32, little-endian; 0-based ids except
+ * TM-1 s_id in [1, P]):
+ *   TPC-B     type 0 deposit    [aid, tid, bid, delta(i32)]
+ *   TM-1 type 0 GSD [s_id]   1 GND [s_id, sf, st, et]   2 GAD [s_id, ai]
+ *                             3 USD [s_id, sf, bit1, data_a]   4 UL [nbr_lo, nbr_hi, vlr]
+ *                             5 ICF [nbr_lo, nbr_hi, sf, st, et, numx_lo, numx_hi]
+ *                             6 DCF [nbr_lo, nbr_hi, sf, st]
+ *                             (nbr = sub_nbr string, 15 BCD digits; the lookup
+ *                             half of the split transaction, runs at submit)
+ *   TPC-C     type 0 NewOrder [w, d, c, ol_cnt, (i, supply_w, qty) x ol_cnt]
+ *                             type 1 Payment  [w, d, cw, cd, by_name, c_or_last, h_amount]
+ *                             (by-name customer lookup, runs at submit)
+ *
+ * Output records (fixed stride per schema, zero for aborted transactions):
+ *   TPC-B  8 B : i64 account balance after the deposit
+ *   TM-1  40 B : GSD  [0]u64 sub_nbr [8]u64 hex [16]u32 msc [20]u32 vlr [24]u16 bits [26]u8[10] byte2
+ *                GND  [0]u32 count [8,16,24]u64 numberx of the qualifying rows in start-time order
+ *                GAD  [0]u8 data1 [1]u8 data2 [4]u32 data3 [8]u64 data4
+ *   TPC-C 200 B: NewOrder [0]u32 o_id [4]u32 ol_cnt [8]i64 total, line l at 16+12l:
+ *                         [0]i32 s_quantity before the update [4]i32 amount [8]u8 brand 'B'
+ *                Payment  [0]u32 c_id [4]u32 c_credit(1=BC) [8]i64 c_balance after
+ * Status: 0 commit, 1 logical abort (no writes; two-phase procedures).
+ */
+#ifndef GPUTX_H
+#define GPUTX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gputx_db gputx_db;                         /* opaque */
+
+typedef enum {
+    GPUTX_OK = 0,
+    GPUTX_EINVAL = 1,        /* bad argument, bad column, malformed transaction        */
+    GPUTX_ENOMEM = 2,        /* device or host allocation failed                         */
+    GPUTX_EDUP_TYPE = 3,     /* register_types: a type id listed twice                    */
+    GPUTX_EUNKNOWN_TYPE = 4, /* type id not compiled for the schema / not registered      */
+    GPUTX_ESTATE = 5,        /* call out of order (e.g. submit twice, execute unsealed)   */
+    GPUTX_ECAPACITY = 6,     /* bulk > max_bulk, output buffer short, insert table full   */
+    GPUTX_ECROSS = 7,        /* PART: a cross-partition type with no fragment split       */
+    GPUTX_EDEADLOCK = 8,     /* TPL spin watchdog tripped; db poisoned until reset        */
+    GPUTX_ECUDA = 9,         /* CUDA runtime error                                        */
+    GPUTX_ENCCL = 10         /* reserved: inter-GPU exchange                              */
+} gputx_status;
+
+typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2 } gputx_strategy;
+typedef enum { GPUTX_TPCB = 1, GPUTX_TM1 = 2, GPUTX_TPCC = 3 } gputx_schema;
+
+typedef struct {
+    gputx_schema schema;
+    uint32_t dims[4];         /* TPC-B: branches, tellers/branch, accounts/branch, 0
+                                 TM-1 : subscribers P, 0, 0, 0
+                                 TPC-C: warehouses W, districts/W D, customers/district C, items I */
+    uint64_t max_bulk;        /* transactions per bulk, <= 1<<24 (timestamp field width)            */
+    uint64_t insert_capacity; /* rows per merged insert table; 0 => 8 * max_bulk                    */
+    uint32_t part_size;       /* PART: TM-1 subscribers per partition; 0 => 128     */
+    int device;               /* CUDA device ordinal                                                */
+    void* stream;             /* cudaStream_t to order all work on; NULL => a library-owned stream  */
+    uint32_t flags;           /* reserved, 0                                                        */
+} gputx_db_config;
+
+typedef struct {
+    const uint8_t* type;        /* u8[n]                                                */
+    const uint32_t* param_off;  /* u32[n+1], param_off[0] == 0                          */
+    const uint32_t* param_words;/* u32[param_off[n]]                                    */
+    uint64_t n;
+    int on_device;              /* 0: host pointers (copied H2D at submit);
+                                   1: device pointers already resident in HBM           */
+} gputx_bulk;
+
+typedef struct {
+    uint64_t n, committed, aborted;
+    uint64_t depth;          /* d: depth of the T-dependency graph (K-SET) */
+    uint64_t ksets;          /* d + 1 (K-SET)                                            */
+    uint64_t zero_set;       /* w0 = |0-set| (K-SET)                        */
+    uint64_t records;        /* access records emitted (K-SET, TPL)                     */
+    uint64_t rank_passes;    /* segmented max-scan passes to the fixpoint (K-SET)       */
+    uint64_t parts;          /* partitions (PART)                                       */
+    uint64_t fragments;      /* executed fragments (PART)                               */
+    uint64_t max_chain;      /* longest partition (PART)                                */
+    double ms_emit, ms_sort, ms_rank, ms_group, ms_exec, ms_merge, ms_total;
+} gputx_stats;
+
+/* Create a database handle for cfg->schema with empty (zero) columns on cfg->device.
+ * Errors: EINVAL (bad schema/dims/max_bulk), ENOMEM, ECUDA.  *out is NULL on error. */
+gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out);
+
+/* Copy one column of the initial image from host memory ("the necessary
+ * data columns and indexes are copied from the main memory to the GPU memory").
+ * name/bytes must match the schema's column list (gputx_column_info); EINVAL otherwise.
+ * Only before gputx_seal. */
+gputx_status gputx_load_column(gputx_db* db, const char* name, const void* host, uint64_t bytes);
+
+/* Column catalog ("system catalog"): index -> name, element bytes and row
+ * count. Returns EINVAL past the last column. */
+gputx_status gputx_column_info(const gputx_db* db, uint32_t index, const char** name,
+                               uint32_t* elem_bytes, uint64_t* count);
+
+/* Finish loading: build the static indexes (TM-1 sub_nbr hash, TPC-C (w,d,c_last)
+ * index), keep a pristine device copy for gputx_reset.  ESTATE if called twice. */
+gputx_status gputx_seal(gputx_db* db);
+
+/* Enable k compiled-in stored procedures (registering = adding a case of
+ * the combined switch kernel).  Errors: EDUP_TYPE, EUNKNOWN_TYPE; nothing changes on
+ * error.  Unless called, every type of the schema is enabled. */
+gputx_status gputx_register_types(gputx_db* db, const uint32_t* type_ids, uint32_t k);
+
+/* Submit one bulk.  Copies/reads the signatures, assigns ts =
+ * first_ts + i, validates every transaction and resolves the static lookups.
+ * Synchronous.  Errors (nothing enqueued): ECAPACITY (n > max_bulk), EINVAL /
+ * EUNKNOWN_TYPE (first bad transaction in the message), ESTATE (unsealed, or a bulk
+ * already submitted and not executed).  *first_ts may be NULL. */
+gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* bulk, uint64_t* first_ts);
+
+/* Execute the submitted bulk with the given strategy to completion (synchronous) and
+ * merge the insert buffers.  stats may be NULL.  Errors: ESTATE (nothing
+ * submitted), EDEADLOCK (TPL watchdog), ECAPACITY (insert table full), ECUDA. */
+gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* stats);
+
+/* Copy the last executed bulk's results to host: status u8[n] (may be NULL) and the
+ * output records (n * gputx_out_stride bytes; out may be NULL).  ECAPACITY if out_bytes
+ * is short, ESTATE before the first execute. */
+gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes);
+
+/* Device pointers to the last bulk's status u8[n] and output records; valid until the
+ * next submit.  For callers that keep results in HBM. */
+gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const void** out,
+                                  uint64_t* n);
+
+uint32_t gputx_out_stride(gputx_schema schema);
+
+/* Snapshot one current column to host (exact bytes of the column). */
+gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint64_t bytes);
+
+/* Merged insert tables (TPC-B "history"; TPC-C "order", "new_order", "order_line",
+ * "history"): row count, and one column (u32/i32 per row) copied to host. */
+gputx_status gputx_insert_rows(gputx_db* db, const char* table, uint64_t* rows);
+gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const char* column,
+                                      void* host, uint64_t bytes);
+
+/* Diagnostics of the last execute: K-SET depth per transaction (u32[n]); the
+ * k-set execution order perm (u32[n]); TPL lock key per access record in emission
+ * order (u32[records]).  ESTATE when the last strategy did not compute them. */
+gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n);
+gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n);
+
+/* Restore the pristine image (columns and insert tables) by a device copy. */
+gputx_status gputx_reset(gputx_db* db);
+
+void gputx_close_db(gputx_db* db);
+const char* gputx_last_error(const gputx_db* db);
+
+/* Launch-shape overrides for tests of grid-shape independence (0 = default). */
+gputx_status gputx_set_launch(gputx_db* db, uint32_t exec_block, uint32_t exec_grid,
+                              uint32_t narrow_max);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPUTX_H */

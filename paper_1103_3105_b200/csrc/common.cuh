@@ -1,0 +1,228 @@
+// common.cuh — device primitives shared by the GPUTx kernels (sm_100a).
+//
+//  * acquire/release loads and stores (PTX memory model, gpu scope)
+//  * a sense-free generation grid barrier for cooperative persistent kernels
+//  * warp / block scans for any associative (not necessarily commutative)
+//    operator, and a decoupled look-back across tiles (single pass over the data)
+//
+// Operators follow the convention  Op::combine(earlier, later)  so that a
+// prefix is  combine(combine(x0, x1), x2) ...  in array order.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define DEV __device__ __forceinline__
+
+namespace gputx {
+
+constexpr int WARP = 32;
+
+DEV uint32_t lane_id() { return threadIdx.x & 31u; }
+DEV uint32_t warp_id() { return threadIdx.x >> 5; }
+DEV uint32_t lanemask_lt() { uint32_t m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
+
+DEV uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+DEV uint64_t ld_acquire64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+DEV uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+DEV void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+DEV void st_release64(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+DEV uint32_t atom_add_release(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// ---------------------------------------------------------------------------------
+// Grid barrier for a cooperative launch (all CTAs co-resident).  gen is bumped by
+// the last arriver; waiters poll it with acquire loads.
+// ---------------------------------------------------------------------------------
+struct GridBar {
+    uint32_t count;
+    uint32_t gen;
+};
+
+DEV void grid_sync(GridBar* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+        uint32_t g = ld_acquire(&b->gen);
+        __threadfence();
+        uint32_t arrived = atomicAdd(&b->count, 1u);
+        if (arrived == nb - 1) {
+            b->count = 0;
+            st_release(&b->gen, g + 1);
+        } else {
+            while (ld_acquire(&b->gen) == g) { }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------
+// Scans
+// ---------------------------------------------------------------------------------
+template <class T>
+DEV T shfl_up_t(T v, int d) {
+    static_assert(sizeof(T) % 4 == 0, "4-byte multiple");
+    union { T t; uint32_t w[sizeof(T) / 4]; } u;
+    u.t = v;
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(T) / 4); ++k) u.w[k] = __shfl_up_sync(0xffffffffu, u.w[k], d);
+    return u.t;
+}
+template <class T>
+DEV T shfl_t(T v, int src) {
+    union { T t; uint32_t w[sizeof(T) / 4]; } u;
+    u.t = v;
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(T) / 4); ++k) u.w[k] = __shfl_sync(0xffffffffu, u.w[k], src);
+    return u.t;
+}
+
+// inclusive warp scan
+template <class T, class Op>
+DEV T warp_scan_incl(T x) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T y = shfl_up_t(x, d);
+        if (lane >= d) x = Op::combine(y, x);
+    }
+    return x;
+}
+
+// Exclusive block scan of one value per thread.  Returns the exclusive prefix
+// (Op::identity() for thread 0) and the block aggregate.  smem: >= (blockDim/32) T.
+template <class T, class Op>
+DEV T block_scan_excl(T x, T& total, T* smem) {
+    const int lane = lane_id(), wid = warp_id(), nw = blockDim.x >> 5;
+    T inc = warp_scan_incl<T, Op>(x);
+    if (lane == 31) smem[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        T w = lane < nw ? smem[lane] : Op::identity();
+        T wi = warp_scan_incl<T, Op>(w);
+        if (lane < nw) smem[lane] = wi;          // inclusive warp totals
+    }
+    __syncthreads();
+    T wpre = wid ? smem[wid - 1] : Op::identity();
+    total = smem[nw - 1];
+    T ex = shfl_up_t(inc, 1);
+    if (lane == 0) ex = Op::identity();
+    T r = Op::combine(wpre, ex);
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------------
+// Decoupled look-back (single-pass tile prefix).  Per tile: a flag word
+// (epoch << 2 | kind, kind 1 = aggregate, 2 = inclusive prefix) and two payloads.
+// epoch makes stale flags of earlier launches/passes invisible (no resets).
+// ---------------------------------------------------------------------------------
+template <class T>
+struct LookBack {
+    uint32_t* flag;
+    T* agg;
+    T* inc;
+};
+
+template <class T>
+DEV void lb_store(T* dst, const T& v) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(T) / 4); ++k) __stcg(d + k, s[k]);
+}
+template <class T>
+DEV T lb_load(const T* src) {
+    union { T t; uint32_t w[sizeof(T) / 4]; } u;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(T) / 4); ++k) u.w[k] = __ldcg(s + k);
+    return u.t;
+}
+
+// Called by ONE full warp of the tile's CTA.  Publishes the aggregate, looks back
+// for the exclusive prefix, publishes the inclusive prefix, returns the exclusive
+// prefix (identity for tile 0) to all lanes of the warp.
+template <class T, class Op>
+DEV T lookback_warp(LookBack<T> lb, uint32_t tile, uint32_t epoch, T agg) {
+    const int lane = lane_id();
+    const uint32_t fa = (epoch << 2) | 1u, fi = (epoch << 2) | 2u;
+    if (tile == 0) {
+        if (lane == 0) {
+            lb_store(&lb.inc[0], agg);
+            __threadfence();
+            st_release(&lb.flag[0], fi);
+        }
+        __syncwarp();
+        return Op::identity();
+    }
+    if (lane == 0) {
+        lb_store(&lb.agg[tile], agg);
+        __threadfence();
+        st_release(&lb.flag[tile], fa);
+    }
+    __syncwarp();
+    T excl = Op::identity();          // prefix of tiles (p, tile) gathered so far (lane 0)
+    int64_t base = (int64_t)tile - 1;
+    while (true) {
+        int64_t p = base - lane;
+        uint32_t f = 0;
+        if (p >= 0) {
+            do { f = ld_acquire(&lb.flag[p]); } while ((f >> 2) != epoch);
+        } else {
+            f = fi;                      // virtual inclusive before tile 0 (never reached)
+        }
+        uint32_t kind = f & 3u;
+        uint32_t incmask = __ballot_sync(0xffffffffu, kind == 2u);
+        int stop = incmask ? __ffs(incmask) - 1 : 32;       // closest inclusive lane
+        T v = Op::identity();
+        if (p >= 0 && lane <= stop && lane < 32) v = (kind == 2u) ? lb_load(&lb.inc[p]) : lb_load(&lb.agg[p]);
+        // compose lanes stop..0 (oldest first) on lane 0
+        int top = stop < 32 ? stop : 31;
+        T acc = Op::identity();
+        for (int l = top; l >= 0; --l) {
+            T vl = shfl_t(v, l);
+            acc = Op::combine(acc, vl);
+        }
+        if (lane == 0) excl = Op::combine(acc, excl);
+        if (stop < 32) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        T incv = Op::combine(excl, agg);
+        lb_store(&lb.inc[tile], incv);
+        __threadfence();
+        st_release(&lb.flag[tile], fi);
+    }
+    excl = shfl_t(excl, 0);
+    return excl;
+}
+
+// ---------------------------------------------------------------------------------
+// Operators
+// ---------------------------------------------------------------------------------
+struct OpAddU32 {
+    static DEV uint32_t identity() { return 0u; }
+    static DEV uint32_t combine(uint32_t a, uint32_t b) { return a + b; }
+};
+
+}  // namespace gputx

@@ -1,0 +1,872 @@
+// engine.cu — host runtime of the B200 GPUTx engine and the C ABI of include/gputx.h.
+//
+// Owns the HBM-resident column store and indexes, the bulk
+// buffers, and the per-strategy pipelines:
+//   K-SET: emit -> radix sort by item -> rank fixpoint -> group (depth, type) -> rounds
+//   PART : fragments -> radix sort by partition -> bounds -> one thread per partition
+//   TPL  : emit -> radix sort by item -> lock keys -> ts-ordered 2PL execution
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gputx.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "schema.cuh"
+#include "sort.cuh"
+
+using namespace gputx;
+
+namespace {
+
+struct ColSpec {
+    const char* name;
+    uint32_t elem;
+    uint64_t count;
+};
+
+struct InsSpec {
+    const char* table;
+    int table_id;
+    std::vector<const char*> cols;
+    uint32_t per_txn;
+};
+
+std::vector<ColSpec> column_specs(int schema, const uint32_t* d) {
+    const uint64_t a = d[0], b = d[1], c = d[2], e = d[3];
+    if (schema == S_TPCB)
+        return {{"br_bal", 8, a}, {"tel_bal", 8, a * b}, {"acc_bal", 8, a * c}};
+    if (schema == S_TM1) {
+        const uint64_t P = a;
+        return {{"sub_nbr", 8, P},      {"sub_bits", 2, P},     {"sub_hex", 8, P},       {"sub_byte2", 1, 10 * P},
+                {"sub_msc", 4, P},      {"sub_vlr", 4, P},      {"ai_valid", 1, 4 * P},  {"ai_data1", 1, 4 * P},
+                {"ai_data2", 1, 4 * P}, {"ai_data3", 4, 4 * P}, {"ai_data4", 8, 4 * P},  {"sf_valid", 1, 4 * P},
+                {"sf_active", 1, 4 * P}, {"sf_error", 1, 4 * P}, {"sf_data_a", 1, 4 * P}, {"sf_data_b", 8, 4 * P},
+                {"cf_live", 1, 12 * P}, {"cf_end", 1, 12 * P},  {"cf_numberx", 8, 12 * P}};
+    }
+    const uint64_t W = a, WD = a * b, WDC = a * b * c, I = e, WI = a * e;
+    return {{"w_ytd", 8, W},          {"w_tax", 4, W},         {"d_ytd", 8, WD},          {"d_tax", 4, WD},
+            {"d_next_o_id", 4, WD},   {"c_balance", 8, WDC},   {"c_ytd_payment", 8, WDC}, {"c_payment_cnt", 4, WDC},
+            {"c_discount", 4, WDC},   {"c_credit", 1, WDC},    {"c_last", 2, WDC},        {"c_first", 8, WDC},
+            {"i_price", 4, I},        {"i_original", 1, I},    {"s_quantity", 4, WI},     {"s_ytd", 8, WI},
+            {"s_order_cnt", 4, WI},   {"s_remote_cnt", 4, WI}, {"s_original", 1, WI}};
+}
+
+std::vector<InsSpec> insert_specs(int schema) {
+    if (schema == S_TPCB) return {{"history", 0, {"h_tid", "h_bid", "h_aid", "h_delta", "h_ts"}, 1}};
+    if (schema == S_TPCC)
+        return {{"order", T_ORDER, {"o_id", "o_d", "o_w", "o_c", "o_entry_d", "o_ol_cnt", "o_all_local"}, 1},
+                {"new_order", T_NEWORDER, {"no_o_id", "no_d", "no_w"}, 1},
+                {"order_line", T_OLINE,
+                 {"ol_o_id", "ol_d", "ol_w", "ol_number", "ol_i_id", "ol_supply_w", "ol_quantity", "ol_amount"}, 15},
+                {"history", T_HIST, {"h_c", "h_cd", "h_cw", "h_d", "h_w", "h_date", "h_amount"}, 1}};
+    return {};
+}
+
+uint32_t ntypes_of(int schema) { return schema == S_TPCB ? 1 : schema == S_TM1 ? 7 : 2; }
+uint32_t bits_for(uint64_t maxval) {   // bits to represent values in [0, maxval]
+    uint32_t b = 0;
+    while (b < 64 && (maxval >> b)) ++b;
+    return b ? b : 1;
+}
+
+struct Col {
+    ColSpec spec;
+    void* d = nullptr;
+    void* pristine = nullptr;
+    bool loaded = false;
+};
+struct InsCol {
+    std::string name;
+    void* d = nullptr;
+};
+struct InsTable {
+    std::string name;
+    int table_id;
+    uint32_t per_txn;
+    uint64_t cap = 0, rows = 0, pending = 0;
+    std::vector<InsCol> cols;
+};
+
+}  // namespace
+
+struct gputx_db {
+    gputx_db_config cfg{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int schema = 0;
+    uint32_t ntypes = 0, type_mask = 0;
+    std::vector<Col> cols;
+    std::vector<InsTable> ins;
+    bool sealed = false, submitted = false, executed = false, poisoned = false;
+    int last_strategy = -1;
+    uint64_t n = 0, first_ts = 0, next_ts = 0, max_bulk = 0, max_words = 0, max_rec = 0, n_items = 0;
+    uint32_t item_bits = 0;
+    uint32_t nparts = 0, part_bits = 0, part_size = 128;
+    // bulk + results
+    uint8_t* d_type = nullptr;
+    uint32_t* d_poff = nullptr;
+    uint32_t* d_pw = nullptr;
+    uint8_t* d_status = nullptr;
+    uint8_t* d_out = nullptr;
+    uint32_t out_stride = 0;
+    uint32_t* d_ins_off = nullptr;   // 4 * (max_bulk + 1)
+    // indexes
+    uint64_t* d_hkeys = nullptr;
+    uint32_t* d_hvals = nullptr;
+    uint64_t hmask = 0;
+    uint32_t* d_name_sorted = nullptr;
+    uint32_t* d_name_off = nullptr;
+    std::vector<uint64_t> h_nbr;
+    std::vector<uint16_t> h_last;
+    std::vector<uint64_t> h_first;
+    // workspaces
+    uint64_t* d_rec_a = nullptr;
+    uint64_t* d_rec_b = nullptr;
+    uint64_t* d_sorted = nullptr;
+    uint32_t* d_cnt = nullptr;       // max(max_bulk, max_rec) + 1
+    uint32_t* d_rec_off = nullptr;   // max_bulk + 1
+    uint32_t* d_D = nullptr;
+    uint32_t* d_perm = nullptr;
+    uint32_t* d_gcnt = nullptr;      // max_bulk * ntypes + 2
+    uint32_t* d_goff = nullptr;
+    uint32_t* d_lock = nullptr;
+    uint32_t* d_lkey = nullptr;
+    uint32_t* d_part_off = nullptr;
+    uint32_t* d_sc = nullptr;
+    uint32_t* h_sc = nullptr;        // pinned mirror
+    GridBar* d_bar = nullptr;
+    uint32_t* d_tickets = nullptr;   // [256]
+    LookBack<uint32_t> lb_scan{};
+    LookBack<Xf> lb_rank{};
+    LookBack<Pair> lb_tpl{};
+    SortWs sort_ws{};
+    uint32_t epoch = 0;        // look-back epochs of scans / sorts / TPL keys
+    uint32_t rank_epoch = 0;   // look-back epochs of rank passes (own array)
+    uint32_t ticket_slot = 0;
+    int nsm = 0;
+    int rank_grid = 0, kset_grid = 0;
+    uint32_t exec_block = 256, exec_grid_override = 0, narrow_max = 256;
+    cudaEvent_t ev[8] = {};
+    bool has_depth = false, has_perm = false;
+};
+
+namespace {
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) {                                                                \
+            db->err = std::string(#x) + ": " + cudaGetErrorString(e_);                          \
+            return GPUTX_ECUDA;                                                                 \
+        }                                                                                       \
+    } while (0)
+
+gputx_status fail(gputx_db* db, gputx_status s, const std::string& m) {
+    if (db) db->err = m;
+    return s;
+}
+
+template <class T>
+gputx_status dalloc(gputx_db* db, T** p, uint64_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        db->err = std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + "): " + cudaGetErrorString(e);
+        return GPUTX_ENOMEM;
+    }
+    return GPUTX_OK;
+}
+
+#define TRY(x)                              \
+    do {                                    \
+        gputx_status s_ = (x);              \
+        if (s_ != GPUTX_OK) return s_;      \
+    } while (0)
+
+uint32_t* next_ticket(gputx_db* db) {
+    // 256 ticket counters zeroed together; a slot is used once per memset cycle
+    if (db->ticket_slot == 0) cudaMemsetAsync(db->d_tickets, 0, 256 * sizeof(uint32_t), db->stream);
+    uint32_t* t = db->d_tickets + db->ticket_slot;
+    db->ticket_slot = (db->ticket_slot + 1) & 255u;
+    return t;
+}
+
+// exclusive scan of n (device or host count) u32 values; out[n] = total
+void scan_u32(gputx_db* db, const uint32_t* in, uint32_t* out, const uint32_t* n_dev, uint64_t n_max, uint32_t* total) {
+    const uint32_t grid = (uint32_t)((n_max + SC_TILE) / SC_TILE);
+    ++db->epoch;
+    scan_kernel<<<grid, SC_THREADS, 0, db->stream>>>(in, out, n_dev, (uint32_t)n_max, db->lb_scan, db->epoch,
+                                                     next_ticket(db), total);
+}
+
+DevDb make_devdb(gputx_db* db) {
+    DevDb v{};
+    v.schema = db->schema;
+    for (int k = 0; k < 4; ++k) v.dims[k] = db->cfg.dims[k];
+    v.ntypes = db->ntypes;
+    v.n = (uint32_t)db->n;
+    v.first_ts = (uint32_t)db->first_ts;
+    v.type = db->d_type;
+    v.poff = db->d_poff;
+    v.pw = db->d_pw;
+    v.status = db->d_status;
+    v.out = db->d_out;
+    v.out_stride = db->out_stride;
+    for (size_t k = 0; k < db->cols.size() && k < (size_t)MAX_COLS; ++k) v.col[k] = db->cols[k].d;
+    int c = 0;
+    for (auto& t : db->ins) {
+        v.ins_base[t.table_id] = t.rows;
+        for (auto& ic : t.cols) v.ins[c++] = ic.d;
+    }
+    v.ins_off = db->d_ins_off;
+    v.ins_stride = (uint32_t)(db->n + 1);
+    v.hkeys = db->d_hkeys;
+    v.hvals = db->d_hvals;
+    v.hmask = db->hmask;
+    v.name_sorted = db->d_name_sorted;
+    v.name_off = db->d_name_off;
+    v.part_size = db->part_size;
+    return v;
+}
+
+template <class K>
+int coop_grid(gputx_db* db, K kernel, int block, size_t smem) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, block, smem);
+    if (per < 1) per = 1;
+    return per * db->nsm;
+}
+
+gputx_status launch_coop(gputx_db* db, const void* fn, int grid, int block, void** args) {
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, 0, db->stream);
+    if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e));
+    return GPUTX_OK;
+}
+
+uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
+    uint64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (uint32_t)g;
+}
+
+// ------------------------------------------------------------------------------- K-SET
+template <int S>
+gputx_status emit_records(gputx_db* db, const DevDb& v) {
+    const uint32_t g = grid_for(db->n, 256, 148 * 16);
+    emit_count_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_cnt);
+    scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NREC);
+    emit_write_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_rec_off, db->d_rec_a);
+    return GPUTX_OK;
+}
+
+gputx_status sort_records(gputx_db* db, uint32_t lo, uint32_t nbits, const uint32_t* n_dev, uint64_t n_max) {
+    db->d_sorted = radix_sort_u64(db->d_rec_a, db->d_rec_b, n_dev, n_max, lo, nbits, db->sort_ws, db->epoch, db->stream);
+    return GPUTX_OK;
+}
+
+template <int S>
+gputx_status run_kset(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[1], s);
+    TRY(emit_records<S>(db, v));
+    cudaEventRecord(db->ev[2], s);
+    TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    cudaEventRecord(db->ev[3], s);
+    // rank fixpoint (persistent, cooperative)
+    CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
+    {
+        const uint64_t* keys = db->d_sorted;
+        const uint32_t* nrec = db->d_sc + SC_NREC;
+        uint32_t* D = db->d_D;
+        LookBack<Xf> lb = db->lb_rank;
+        uint32_t epoch0 = db->rank_epoch + 1;
+        GridBar* bar = db->d_bar;
+        uint32_t* sc = db->d_sc;
+        uint32_t maxp = 1u << 20;
+        void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp};
+        TRY(launch_coop(db, (const void*)rank_kernel, db->rank_grid, RK_THREADS, args));
+    }
+    cudaEventRecord(db->ev[4], s);
+    // group by (depth, type)
+    const uint32_t T = db->ntypes;
+    const uint32_t g = grid_for(db->n, 256, 148 * 8);
+    depth_reduce_kernel<<<g, 256, 0, s>>>(db->d_D, (uint32_t)db->n, db->d_sc);
+    group_nkeys_kernel<<<1, 1, 0, s>>>(db->d_sc, T);
+    zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
+    group_hist_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt);
+    scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
+    group_scatter_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff, db->d_perm);
+    cudaEventRecord(db->ev[5], s);
+    // rounds
+    {
+        DevDb vv = v;
+        const uint32_t* perm = db->d_perm;
+        const uint32_t* off = db->d_goff;
+        GridBar* bar = db->d_bar;
+        uint32_t* sc = db->d_sc;
+        uint32_t nm = db->narrow_max;
+        uint32_t TT = T;
+        void* args[] = {&vv, &perm, &off, &TT, &bar, &sc, &nm};
+        const void* fn = (const void*)kset_exec_kernel<S>;
+        int grid = db->exec_grid_override ? (int)db->exec_grid_override : db->kset_grid;
+        TRY(launch_coop(db, fn, grid, 256, args));
+    }
+    cudaEventRecord(db->ev[6], s);
+    db->has_depth = db->has_perm = true;
+    return GPUTX_OK;
+}
+
+// -------------------------------------------------------------------------------- PART
+template <int S>
+gputx_status run_part(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[1], s);
+    const uint32_t g = grid_for(db->n, 256, 148 * 16);
+    frag_count_kernel<S><<<g, 256, 0, s>>>(v, db->d_cnt);
+    scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NFRAG);
+    frag_emit_kernel<S><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a);
+    cudaEventRecord(db->ev[2], s);
+    TRY(sort_records(db, 32, db->part_bits, db->d_sc + SC_NFRAG, db->max_rec));
+    cudaEventRecord(db->ev[3], s);
+    part_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NFRAG,
+                                                                               db->nparts, db->d_part_off);
+    cudaEventRecord(db->ev[4], s);
+    cudaEventRecord(db->ev[5], s);
+    const uint32_t pb = 128;
+    part_exec_kernel<S><<<(db->nparts + pb - 1) / pb, pb, 0, s>>>(v, db->d_sorted, db->d_part_off, db->nparts, db->d_sc);
+    cudaEventRecord(db->ev[6], s);
+    return GPUTX_OK;
+}
+
+// --------------------------------------------------------------------------------- TPL
+template <int S>
+gputx_status run_tpl(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[1], s);
+    TRY(emit_records<S>(db, v));
+    cudaEventRecord(db->ev[2], s);
+    TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    cudaEventRecord(db->ev[3], s);
+    ++db->epoch;
+    tpl_keys_kernel<<<(uint32_t)((db->max_rec + RK_TILE - 1) / RK_TILE) + 1, RK_THREADS, 0, s>>>(
+        db->d_sorted, db->d_sc + SC_NREC, db->d_rec_off, db->d_lkey, db->d_lock, db->lb_tpl, db->epoch, next_ticket(db));
+    cudaEventRecord(db->ev[4], s);
+    cudaEventRecord(db->ev[5], s);
+    const uint32_t tb = 128;
+    tpl_exec_kernel<S><<<(uint32_t)((db->n + tb - 1) / tb), tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+    cudaEventRecord(db->ev[6], s);
+    return GPUTX_OK;
+}
+
+template <int S>
+gputx_status execute_schema(gputx_db* db, gputx_strategy st) {
+    DevDb v = make_devdb(db);
+    if (st == GPUTX_KSET) return run_kset<S>(db, v);
+    if (st == GPUTX_PART) return run_part<S>(db, v);
+    return run_tpl<S>(db, v);
+}
+
+template <int S>
+void launch_ingest(gputx_db* db, uint32_t n_words) {
+    DevDb v = make_devdb(db);
+    const uint32_t g = grid_for(db->n, 256, 148 * 16);
+    ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, db->type_mask, db->d_ins_off,
+                                                (uint32_t)(db->n + 1), db->d_sc);
+}
+
+Col* find_col(gputx_db* db, const char* name) {
+    for (auto& c : db->cols)
+        if (!strcmp(c.spec.name, name)) return &c;
+    return nullptr;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+uint32_t gputx_out_stride(gputx_schema schema) {
+    return schema == GPUTX_TPCB ? 8 : schema == GPUTX_TM1 ? 40 : schema == GPUTX_TPCC ? 200 : 0;
+}
+
+const char* gputx_last_error(const gputx_db* db) { return db ? db->err.c_str() : "null handle"; }
+
+gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
+    if (!out) return GPUTX_EINVAL;
+    *out = nullptr;
+    if (!cfg) return GPUTX_EINVAL;
+    const int schema = (int)cfg->schema;
+    if (schema < 1 || schema > 3) return GPUTX_EINVAL;
+    if (cfg->max_bulk == 0 || cfg->max_bulk > (1u << 24)) return GPUTX_EINVAL;
+    const uint32_t* d = cfg->dims;
+    if (schema == S_TPCB && (!d[0] || !d[1] || !d[2])) return GPUTX_EINVAL;
+    if (schema == S_TM1 && !d[0]) return GPUTX_EINVAL;
+    if (schema == S_TPCC && (!d[0] || !d[1] || !d[2] || !d[3])) return GPUTX_EINVAL;
+    gputx_db* db = new gputx_db();
+    db->cfg = *cfg;
+    db->schema = schema;
+    db->ntypes = ntypes_of(schema);
+    db->type_mask = (1u << db->ntypes) - 1;
+    db->max_bulk = cfg->max_bulk;
+    db->out_stride = gputx_out_stride(cfg->schema);
+    db->part_size = cfg->part_size ? cfg->part_size : 128;
+    auto bail = [&](gputx_status s) { *out = db; gputx_close_db(db); *out = nullptr; return s; };
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(GPUTX_ECUDA);
+    cudaDeviceGetAttribute(&db->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+    if (cfg->stream) {
+        db->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(GPUTX_ECUDA);
+        db->own_stream = true;
+    }
+    // sizes
+    uint64_t n_items = 0, max_words_per = 0, max_rec_per = 0;
+    if (schema == S_TPCB) {
+        n_items = (uint64_t)d[0] * d[2] + (uint64_t)d[0] * d[1] + d[0];
+        max_words_per = 4; max_rec_per = 3;
+        db->nparts = d[0];
+    } else if (schema == S_TM1) {
+        n_items = 18ull * d[0];
+        max_words_per = 7; max_rec_per = 3;
+        db->nparts = (uint32_t)((d[0] + db->part_size - 1) / db->part_size);
+    } else {
+        const uint64_t WD = (uint64_t)d[0] * d[1];
+        n_items = 2 * WD + d[0] + WD * d[2] + (uint64_t)d[0] * d[3];
+        max_words_per = 49; max_rec_per = 16;
+        db->nparts = d[0];
+    }
+    db->n_items = n_items;
+    db->item_bits = bits_for(n_items - 1);
+    if (db->item_bits > 34) return bail(GPUTX_EINVAL);
+    db->part_bits = bits_for(db->nparts ? db->nparts - 1 : 0);
+    db->max_words = max_words_per * db->max_bulk;
+    db->max_rec = max_rec_per * db->max_bulk;       // records (K-SET/TPL) and fragments (PART) share buffers
+    gputx_status st;
+    // columns
+    for (auto& cs : column_specs(schema, d)) {
+        Col c;
+        c.spec = cs;
+        if ((st = dalloc(db, (uint8_t**)&c.d, cs.count * cs.elem)) != GPUTX_OK) return bail(st);
+        cudaMemsetAsync(c.d, 0, cs.count * cs.elem, db->stream);
+        db->cols.push_back(c);
+    }
+    // insert tables
+    for (auto& is : insert_specs(schema)) {
+        InsTable t;
+        t.name = is.table;
+        t.table_id = is.table_id;
+        t.per_txn = is.per_txn;
+        t.cap = cfg->insert_capacity ? cfg->insert_capacity : 8 * db->max_bulk * is.per_txn;
+        for (auto* cn : is.cols) {
+            InsCol ic;
+            ic.name = cn;
+            if ((st = dalloc(db, (uint32_t**)&ic.d, t.cap)) != GPUTX_OK) return bail(st);
+            t.cols.push_back(ic);
+        }
+        db->ins.push_back(t);
+    }
+    const uint64_t NB = db->max_bulk;
+    const uint64_t cntn = std::max(NB, db->max_rec) + 2;
+    if ((st = dalloc(db, &db->d_type, NB)) || (st = dalloc(db, &db->d_poff, NB + 1)) ||
+        (st = dalloc(db, &db->d_pw, db->max_words)) || (st = dalloc(db, &db->d_status, NB)) ||
+        (st = dalloc(db, &db->d_out, NB * db->out_stride)) || (st = dalloc(db, &db->d_ins_off, 4 * (NB + 1))) ||
+        (st = dalloc(db, &db->d_rec_a, db->max_rec)) || (st = dalloc(db, &db->d_rec_b, db->max_rec)) ||
+        (st = dalloc(db, &db->d_cnt, cntn)) || (st = dalloc(db, &db->d_rec_off, NB + 2)) ||
+        (st = dalloc(db, &db->d_D, NB)) || (st = dalloc(db, &db->d_perm, NB)) ||
+        (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
+        (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
+        (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
+        (st = dalloc(db, &db->d_bar, 1)) || (st = dalloc(db, &db->d_tickets, 256)))
+        return bail(st);
+    // look-back state: sized for the largest tiled pass
+    const uint64_t tiles = (std::max(db->max_rec, NB * db->ntypes) + 2) / 2048 + 4;
+    if ((st = dalloc(db, &db->lb_scan.flag, tiles)) || (st = dalloc(db, &db->lb_scan.agg, tiles)) ||
+        (st = dalloc(db, &db->lb_scan.inc, tiles)) || (st = dalloc(db, &db->lb_rank.flag, tiles)) ||
+        (st = dalloc(db, &db->lb_rank.agg, tiles)) || (st = dalloc(db, &db->lb_rank.inc, tiles)) ||
+        (st = dalloc(db, &db->lb_tpl.flag, tiles)) || (st = dalloc(db, &db->lb_tpl.agg, tiles)) ||
+        (st = dalloc(db, &db->lb_tpl.inc, tiles)))
+        return bail(st);
+    db->sort_ws.max_tiles = db->max_rec / RS_TILE + 2;
+    if ((st = dalloc(db, &db->sort_ws.hist, RS_MAXPASS * 256)) ||
+        (st = dalloc(db, &db->sort_ws.status, db->sort_ws.max_tiles * 256)) ||
+        (st = dalloc(db, &db->sort_ws.tickets, 64)))
+        return bail(st);
+    cudaMemsetAsync(db->lb_scan.flag, 0, tiles * 4, db->stream);
+    cudaMemsetAsync(db->lb_rank.flag, 0, tiles * 4, db->stream);
+    cudaMemsetAsync(db->lb_tpl.flag, 0, tiles * 4, db->stream);
+    cudaMemsetAsync(db->sort_ws.status, 0, db->sort_ws.max_tiles * 256 * 8, db->stream);
+    cudaMemsetAsync(db->d_bar, 0, sizeof(GridBar), db->stream);
+    cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, db->stream);
+    cudaMemsetAsync(db->d_lock, 0, n_items * 4, db->stream);
+    if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
+    for (auto& e : db->ev) cudaEventCreate(&e);
+    db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
+    int kg = 0;
+    if (schema == S_TPCB) kg = coop_grid(db, kset_exec_kernel<S_TPCB>, 256, 0);
+    else if (schema == S_TM1) kg = coop_grid(db, kset_exec_kernel<S_TM1>, 256, 0);
+    else kg = coop_grid(db, kset_exec_kernel<S_TPCC>, 256, 0);
+    db->kset_grid = kg;
+    if (cudaStreamSynchronize(db->stream) != cudaSuccess) return bail(GPUTX_ECUDA);
+    *out = db;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_column_info(const gputx_db* db, uint32_t index, const char** name, uint32_t* elem_bytes,
+                               uint64_t* count) {
+    if (!db || index >= db->cols.size()) return GPUTX_EINVAL;
+    if (name) *name = db->cols[index].spec.name;
+    if (elem_bytes) *elem_bytes = db->cols[index].spec.elem;
+    if (count) *count = db->cols[index].spec.count;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_load_column(gputx_db* db, const char* name, const void* host, uint64_t bytes) {
+    if (!db || !name || !host) return GPUTX_EINVAL;
+    if (db->sealed) return fail(db, GPUTX_ESTATE, "load_column after seal");
+    Col* c = find_col(db, name);
+    if (!c) return fail(db, GPUTX_EINVAL, std::string("unknown column ") + name);
+    const uint64_t need = c->spec.count * c->spec.elem;
+    if (bytes != need)
+        return fail(db, GPUTX_EINVAL, std::string("column ") + name + ": expected " + std::to_string(need) + " bytes");
+    CK(cudaMemcpyAsync(c->d, host, bytes, cudaMemcpyHostToDevice, db->stream));
+    CK(cudaStreamSynchronize(db->stream));
+    c->loaded = true;
+    if (!strcmp(name, "sub_nbr")) db->h_nbr.assign((const uint64_t*)host, (const uint64_t*)host + c->spec.count);
+    if (!strcmp(name, "c_last")) db->h_last.assign((const uint16_t*)host, (const uint16_t*)host + c->spec.count);
+    if (!strcmp(name, "c_first")) db->h_first.assign((const uint64_t*)host, (const uint64_t*)host + c->spec.count);
+    return GPUTX_OK;
+}
+
+gputx_status gputx_seal(gputx_db* db) {
+    if (!db) return GPUTX_EINVAL;
+    if (db->sealed) return fail(db, GPUTX_ESTATE, "already sealed");
+    gputx_status st;
+    if (db->schema == S_TM1) {
+        // static sub_nbr -> s_id index (open addressing, load <= 0.5)
+        const uint64_t P = db->cfg.dims[0];
+        uint64_t cap = 1;
+        while (cap < 2 * P) cap <<= 1;
+        std::vector<uint64_t> keys(cap, 0);
+        std::vector<uint32_t> vals(cap, 0);
+        if (db->h_nbr.size() != P) db->h_nbr.assign(P, 0);
+        for (uint64_t s = 0; s < P; ++s) {
+            const uint64_t k = db->h_nbr[s];
+            if (!k) continue;
+            uint64_t h = nbr_hash(k) & (cap - 1);
+            while (keys[h] != 0 && keys[h] != k) h = (h + 1) & (cap - 1);
+            keys[h] = k;
+            vals[h] = (uint32_t)(s + 1);
+        }
+        db->hmask = cap - 1;
+        if ((st = dalloc(db, &db->d_hkeys, cap)) || (st = dalloc(db, &db->d_hvals, cap))) return st;
+        CK(cudaMemcpyAsync(db->d_hkeys, keys.data(), cap * 8, cudaMemcpyHostToDevice, db->stream));
+        CK(cudaMemcpyAsync(db->d_hvals, vals.data(), cap * 4, cudaMemcpyHostToDevice, db->stream));
+        CK(cudaStreamSynchronize(db->stream));
+        db->h_nbr.clear();
+        db->h_nbr.shrink_to_fit();
+    }
+    if (db->schema == S_TPCC) {
+        // static (w, d, c_last) -> customers ordered by (c_first, c)
+        const uint64_t W = db->cfg.dims[0], D = db->cfg.dims[1], C = db->cfg.dims[2];
+        const uint64_t WD = W * D;
+        if (db->h_last.size() != WD * C) db->h_last.assign(WD * C, 0);
+        if (db->h_first.size() != WD * C) db->h_first.assign(WD * C, 0);
+        std::vector<uint32_t> sorted(WD * C);
+        std::vector<uint32_t> off(WD * 1000 + 1, 0);
+        std::vector<uint32_t> idx(C);
+        for (uint64_t wd = 0; wd < WD; ++wd) {
+            const uint64_t b = wd * C;
+            for (uint32_t c = 0; c < C; ++c) idx[c] = c;
+            std::sort(idx.begin(), idx.end(), [&](uint32_t x, uint32_t y) {
+                const uint16_t lx = db->h_last[b + x], ly = db->h_last[b + y];
+                if (lx != ly) return lx < ly;
+                const uint64_t fx = db->h_first[b + x], fy = db->h_first[b + y];
+                if (fx != fy) return fx < fy;
+                return x < y;
+            });
+            uint32_t k = 0;
+            for (uint32_t last = 0; last < 1000; ++last) {
+                off[wd * 1000 + last] = (uint32_t)(b + k);
+                while (k < C && db->h_last[b + idx[k]] == last) { sorted[b + k] = idx[k]; ++k; }
+            }
+            for (; k < C; ++k) sorted[b + k] = idx[k];     // names >= 1000 (not reachable)
+        }
+        off[WD * 1000] = (uint32_t)(WD * C);
+        if ((st = dalloc(db, &db->d_name_sorted, WD * C)) || (st = dalloc(db, &db->d_name_off, WD * 1000 + 1))) return st;
+        CK(cudaMemcpyAsync(db->d_name_sorted, sorted.data(), WD * C * 4, cudaMemcpyHostToDevice, db->stream));
+        CK(cudaMemcpyAsync(db->d_name_off, off.data(), (WD * 1000 + 1) * 4, cudaMemcpyHostToDevice, db->stream));
+        CK(cudaStreamSynchronize(db->stream));
+        db->h_last.clear();
+        db->h_first.clear();
+    }
+    // pristine copy for reset
+    for (auto& c : db->cols) {
+        const uint64_t b = c.spec.count * c.spec.elem;
+        if ((st = dalloc(db, (uint8_t**)&c.pristine, b)) != GPUTX_OK) return st;
+        CK(cudaMemcpyAsync(c.pristine, c.d, b, cudaMemcpyDeviceToDevice, db->stream));
+    }
+    CK(cudaStreamSynchronize(db->stream));
+    db->sealed = true;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_register_types(gputx_db* db, const uint32_t* ids, uint32_t k) {
+    if (!db || (k && !ids)) return GPUTX_EINVAL;
+    uint32_t mask = 0;
+    for (uint32_t j = 0; j < k; ++j) {
+        if (ids[j] >= db->ntypes) return fail(db, GPUTX_EUNKNOWN_TYPE, "type " + std::to_string(ids[j]) + " not compiled");
+        if (mask & (1u << ids[j])) return fail(db, GPUTX_EDUP_TYPE, "type " + std::to_string(ids[j]) + " listed twice");
+        mask |= 1u << ids[j];
+    }
+    db->type_mask = mask;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
+    if (!db || !b) return GPUTX_EINVAL;
+    if (!db->sealed) return fail(db, GPUTX_ESTATE, "submit before seal");
+    if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is already submitted");
+    if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
+    if (b->n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
+    if (b->n && (!b->type || !b->param_off || !b->param_words)) return GPUTX_EINVAL;
+    cudaStream_t s = db->stream;
+    const uint64_t n = b->n;
+    uint32_t n_words = 0;
+    if (n) {
+        if (b->on_device) CK(cudaMemcpy(&n_words, b->param_off + n, 4, cudaMemcpyDeviceToHost));
+        else n_words = b->param_off[n];
+    }
+    if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
+    if (db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
+    db->n = n;
+    db->has_depth = db->has_perm = false;
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    if (n) {
+        const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
+        CK(cudaMemcpyAsync(db->d_poff, b->param_off, (n + 1) * 4, kind, s));
+        if (n_words) CK(cudaMemcpyAsync(db->d_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
+        if (db->schema == S_TPCC) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * 4, s));
+        db->first_ts = db->next_ts;
+        if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words);
+        else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words);
+        else launch_ingest<S_TPCC>(db, n_words);
+        if (db->schema == S_TPCC)
+            for (int t = 0; t < 4; ++t)
+                scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n, db->d_sc + 20 + t);
+    }
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_ERR]) {
+        static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
+                                     "parameter out of range", "bad param_off"};
+        const uint32_t e = db->h_sc[SC_ERR];
+        db->n = 0;
+        return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
+                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 6 ? e : 0]);
+    }
+    // insert rows this bulk will append (decisions are static: two-phase procedures)
+    for (auto& t : db->ins) {
+        t.pending = db->schema == S_TPCB ? n : db->h_sc[20 + t.table_id];
+        if (t.rows + t.pending > t.cap) {
+            db->n = 0;
+            return fail(db, GPUTX_ECAPACITY, "insert table " + t.name + " full; reset or raise insert_capacity");
+        }
+    }
+    db->next_ts += n;
+    if (first_ts) *first_ts = db->first_ts;
+    db->submitted = true;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->submitted) return fail(db, GPUTX_ESTATE, "nothing submitted");
+    if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET) return fail(db, GPUTX_EINVAL, "bad strategy");
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[0], s);
+    const uint64_t n = db->n;
+    gputx_status r = GPUTX_OK;
+    if (n) {
+        CK(cudaMemsetAsync(db->d_status, 0, n, s));
+        if (db->schema != S_TPCB) CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
+        if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
+        else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
+        else r = execute_schema<S_TPCC>(db, st);
+    } else {
+        for (int k = 1; k < 7; ++k) cudaEventRecord(db->ev[k], s);
+    }
+    cudaEventRecord(db->ev[7], s);
+    db->submitted = false;
+    if (r != GPUTX_OK) return r;
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (st == GPUTX_KSET) db->rank_epoch += db->h_sc[SC_PASSES] + 1;
+    for (auto& t : db->ins) { t.rows += t.pending; t.pending = 0; }
+    db->executed = true;
+    db->last_strategy = (int)st;
+    if (st == GPUTX_KSET && db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
+    if (db->h_sc[SC_DEADLOCK]) {
+        db->poisoned = true;
+        return fail(db, GPUTX_EDEADLOCK, "TPL spin watchdog tripped");
+    }
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->n = n;
+        stats->records = st == GPUTX_PART ? 0 : db->h_sc[SC_NREC];
+        stats->fragments = st == GPUTX_PART ? db->h_sc[SC_NFRAG] : 0;
+        if (st == GPUTX_KSET && n) {
+            stats->depth = db->h_sc[SC_MAXD];
+            stats->ksets = (uint64_t)db->h_sc[SC_MAXD] + 1;
+            stats->zero_set = db->h_sc[SC_ZERO];
+            stats->rank_passes = db->h_sc[SC_PASSES];
+        }
+        if (st == GPUTX_PART) {
+            stats->parts = db->nparts;
+            stats->max_chain = db->h_sc[SC_MAXCHAIN];
+        }
+        float ms[8] = {0};
+        for (int k = 1; k < 8; ++k) cudaEventElapsedTime(&ms[k], db->ev[k - 1], db->ev[k]);
+        stats->ms_emit = ms[2];
+        stats->ms_sort = ms[3];
+        stats->ms_rank = ms[4];
+        stats->ms_group = ms[5];
+        stats->ms_exec = ms[6];
+        stats->ms_merge = ms[7];
+        float tot = 0;
+        cudaEventElapsedTime(&tot, db->ev[0], db->ev[7]);
+        stats->ms_total = tot;
+        // committed count (status bytes, D2H once)
+        std::vector<uint8_t> stv(n);
+        if (n) CK(cudaMemcpy(stv.data(), db->d_status, n, cudaMemcpyDeviceToHost));
+        uint64_t ab = 0;
+        for (uint8_t x : stv) ab += x != 0;
+        stats->aborted = ab;
+        stats->committed = n - ab;
+    }
+    return GPUTX_OK;
+}
+
+gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    const uint64_t need = db->n * db->out_stride;
+    if (out && out_bytes < need) return fail(db, GPUTX_ECAPACITY, "output buffer too small");
+    if (status && db->n) CK(cudaMemcpyAsync(status, db->d_status, db->n, cudaMemcpyDeviceToHost, db->stream));
+    if (out && db->n) CK(cudaMemcpyAsync(out, db->d_out, need, cudaMemcpyDeviceToHost, db->stream));
+    CK(cudaStreamSynchronize(db->stream));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const void** out, uint64_t* n) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    if (status) *status = db->d_status;
+    if (out) *out = db->d_out;
+    if (n) *n = db->n;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint64_t bytes) {
+    if (!db || !name || !host) return GPUTX_EINVAL;
+    Col* c = find_col(db, name);
+    if (!c) return fail(db, GPUTX_EINVAL, std::string("unknown column ") + name);
+    if (bytes != c->spec.count * c->spec.elem) return fail(db, GPUTX_EINVAL, "size mismatch");
+    CK(cudaMemcpyAsync(host, c->d, bytes, cudaMemcpyDeviceToHost, db->stream));
+    CK(cudaStreamSynchronize(db->stream));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_insert_rows(gputx_db* db, const char* table, uint64_t* rows) {
+    if (!db || !table || !rows) return GPUTX_EINVAL;
+    for (auto& t : db->ins)
+        if (t.name == table) { *rows = t.rows; return GPUTX_OK; }
+    return fail(db, GPUTX_EINVAL, std::string("unknown table ") + table);
+}
+
+gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const char* column, void* host, uint64_t bytes) {
+    if (!db || !table || !column) return GPUTX_EINVAL;
+    for (auto& t : db->ins) {
+        if (t.name != table) continue;
+        for (auto& c : t.cols) {
+            if (c.name != column) continue;
+            if (bytes != t.rows * 4) return fail(db, GPUTX_EINVAL, "size mismatch");
+            if (bytes) {
+                CK(cudaMemcpyAsync(host, c.d, bytes, cudaMemcpyDeviceToHost, db->stream));
+                CK(cudaStreamSynchronize(db->stream));
+            }
+            return GPUTX_OK;
+        }
+    }
+    return fail(db, GPUTX_EINVAL, std::string("unknown insert column ") + table + "." + column);
+}
+
+gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (!db || !host) return GPUTX_EINVAL;
+    if (!db->has_depth || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET depths for this bulk");
+    if (n) CK(cudaMemcpy(host, db->d_D, n * 4, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (!db || !host) return GPUTX_EINVAL;
+    if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
+    if (n) CK(cudaMemcpy(host, db->d_perm, n * 4, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_reset(gputx_db* db) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->sealed) return fail(db, GPUTX_ESTATE, "reset before seal");
+    for (auto& c : db->cols)
+        CK(cudaMemcpyAsync(c.d, c.pristine, c.spec.count * c.spec.elem, cudaMemcpyDeviceToDevice, db->stream));
+    for (auto& t : db->ins) { t.rows = 0; t.pending = 0; }
+    CK(cudaStreamSynchronize(db->stream));
+    db->poisoned = false;
+    db->submitted = false;
+    db->executed = false;
+    db->next_ts = 0;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_set_launch(gputx_db* db, uint32_t exec_block, uint32_t exec_grid, uint32_t narrow_max) {
+    if (!db) return GPUTX_EINVAL;
+    if (exec_grid && (int)exec_grid > db->kset_grid) return fail(db, GPUTX_EINVAL, "grid exceeds co-resident CTAs");
+    (void)exec_block;
+    db->exec_grid_override = exec_grid;
+    if (narrow_max) db->narrow_max = narrow_max;
+    return GPUTX_OK;
+}
+
+void gputx_close_db(gputx_db* db) {
+    if (!db) return;
+    if (db->stream) cudaStreamSynchronize(db->stream);
+    for (auto& c : db->cols) { cudaFree(c.d); cudaFree(c.pristine); }
+    for (auto& t : db->ins)
+        for (auto& c : t.cols) cudaFree(c.d);
+    void* ps[] = {db->d_type, db->d_poff, db->d_pw, db->d_status, db->d_out, db->d_ins_off, db->d_hkeys, db->d_hvals,
+                  db->d_name_sorted, db->d_name_off, db->d_rec_a, db->d_rec_b, db->d_cnt, db->d_rec_off, db->d_D,
+                  db->d_perm, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
+                  db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
+                  db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
+                  db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    if (db->h_sc) cudaFreeHost(db->h_sc);
+    for (auto& e : db->ev)
+        if (e) cudaEventDestroy(e);
+    if (db->own_stream && db->stream) cudaStreamDestroy(db->stream);
+    delete db;
+}
+
+}  // extern "C"

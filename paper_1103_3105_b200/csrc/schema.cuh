@@ -1,0 +1,454 @@
+// schema.cuh — the registered stored procedures of the three benchmarks as device
+// functions, combined per schema into one switch(type) (§3.2),
+// their conflict footprints (basic operations, §4.1; Fekete-style
+// static analysis PAPER.md:457 -> only columns some type writes produce an
+// operation, DESIGN.md R-S18) and their fragment split for PART (DESIGN.md R-S9).
+//
+// Column store: one HBM array per fixed-length column, row
+// index = primary key position.  All procedures are two-phase:
+// every abort decision is taken before the first write.
+#pragma once
+#include <cstdint>
+#include "common.cuh"
+
+namespace gputx {
+
+enum Schema { S_TPCB = 1, S_TM1 = 2, S_TPCC = 3 };
+
+// ---- column indices (must match the catalog in engine.cu) -----------------------
+enum { B_BR = 0, B_TEL, B_ACC, B_NCOL };
+enum { M_NBR = 0, M_BITS, M_HEX, M_BYTE2, M_MSC, M_VLR, M_AI_VALID, M_AI_D1, M_AI_D2, M_AI_D3, M_AI_D4,
+       M_SF_VALID, M_SF_ACTIVE, M_SF_ERR, M_SF_DA, M_SF_DB, M_CF_LIVE, M_CF_END, M_CF_NUM, M_NCOL };
+enum { C_W_YTD = 0, C_W_TAX, C_D_YTD, C_D_TAX, C_D_NEXT, C_C_BAL, C_C_YTD, C_C_CNT, C_C_DISC, C_C_CREDIT,
+       C_C_LAST, C_C_FIRST, C_I_PRICE, C_I_ORIG, C_S_QTY, C_S_YTD, C_S_OCNT, C_S_RCNT, C_S_ORIG, C_NCOL };
+// insert columns: TPC-B history 0..4; TPC-C order 0..6, new_order 7..9, order_line 10..17, history 18..24
+enum { IB_TID = 0, IB_BID, IB_AID, IB_DELTA, IB_TS };
+enum { IO_ID = 0, IO_D, IO_W, IO_C, IO_ENTRY, IO_OLCNT, IO_ALLLOCAL,
+       IN_OID = 7, IN_D, IN_W,
+       IL_OID = 10, IL_D, IL_W, IL_NUM, IL_I, IL_SW, IL_QTY, IL_AMT,
+       IH_C = 18, IH_CD, IH_CW, IH_D, IH_W, IH_DATE, IH_AMT };
+enum { T_ORDER = 0, T_NEWORDER = 1, T_OLINE = 2, T_HIST = 3 };
+
+constexpr int MAX_COLS = 32;
+constexpr int MAX_INS = 32;
+constexpr int MAX_REC = 16;            // access records per transaction (TPC-C NO: 1 + 15)
+
+struct DevDb {
+    int schema;
+    uint32_t dims[4];
+    uint32_t ntypes;
+    uint32_t n;                        // transactions in the bulk
+    uint32_t first_ts;
+    const uint8_t* type;
+    const uint32_t* poff;
+    const uint32_t* pw;
+    uint8_t* status;
+    uint8_t* out;
+    uint32_t out_stride;
+    void* col[MAX_COLS];
+    void* ins[MAX_INS];
+    uint64_t ins_base[4];              // merged-table row count before this bulk
+    const uint32_t* ins_off;           // [table][ins_stride] exclusive row offsets within this bulk
+    uint32_t ins_stride;
+    const uint64_t* hkeys;             // TM-1 sub_nbr hash (open addressing)
+    const uint32_t* hvals;
+    uint64_t hmask;
+    const uint32_t* name_sorted;       // TPC-C customers of (w,d) sorted by (c_last, c_first, c)
+    const uint32_t* name_off;          // [(w*D+d)*1000 + last] -> range start, +1 -> end
+    uint32_t part_size;
+};
+
+#define COL(T, k) (reinterpret_cast<T*>(db.col[(k)]))
+#define INS(T, k) (reinterpret_cast<T*>(db.ins[(k)]))
+
+// mutable column access: L2-coherent (bypass L1) so that writes of earlier k-sets /
+// lock holders on other SMs are seen
+template <class T> DEV T ldm(const T* p) { return __ldcg(p); }
+template <class T> DEV void stm(T* p, T v) { __stcg(p, v); }
+DEV void put32(uint8_t* o, uint32_t v) { *reinterpret_cast<uint32_t*>(o) = v; }
+DEV void put64(uint8_t* o, uint64_t v) {
+    reinterpret_cast<uint32_t*>(o)[0] = (uint32_t)v;
+    reinterpret_cast<uint32_t*>(o)[1] = (uint32_t)(v >> 32);
+}
+
+// =================================================================================
+// Item space (dense, per schema) and access records
+//   record key = item << 30 | idx << 6 | j << 2 | mode     (mode 1 = write)
+// =================================================================================
+constexpr int KEY_ITEM_SHIFT = 30;
+DEV uint64_t make_key(uint64_t item, uint32_t idx, uint32_t j, uint32_t w) {
+    return (item << KEY_ITEM_SHIFT) | ((uint64_t)idx << 6) | ((uint64_t)j << 2) | w;
+}
+DEV uint64_t key_item(uint64_t k) { return k >> KEY_ITEM_SHIFT; }
+DEV uint32_t key_idx(uint64_t k) { return (uint32_t)(k >> 6) & 0xFFFFFFu; }
+DEV uint32_t key_j(uint64_t k) { return (uint32_t)(k >> 2) & 0xFu; }
+DEV uint32_t key_w(uint64_t k) { return (uint32_t)k & 1u; }
+
+struct Rec {
+    uint64_t item;
+    uint32_t w;
+};
+
+DEV int add_rec(Rec* r, int k, uint64_t item, uint32_t w) {
+    for (int j = 0; j < k; ++j)
+        if (r[j].item == item) { r[j].w |= w; return k; }   // same item: one record, W dominates
+    r[k].item = item;
+    r[k].w = w;
+    return k + 1;
+}
+
+// Basic operations of one (ingested) transaction.  Returns the count (<= MAX_REC).
+template <int S>
+DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
+    int k = 0;
+    if (S == S_TPCB) {
+        const uint64_t BA = (uint64_t)db.dims[0] * db.dims[2], BT = (uint64_t)db.dims[0] * db.dims[1];
+        r[0] = {p[0], 1u};
+        r[1] = {BA + p[1], 1u};
+        r[2] = {BA + BT + p[2], 1u};
+        return 3;
+    } else if (S == S_TM1) {
+        const uint64_t P = db.dims[0];
+        switch (t) {
+        case 0: { uint64_t s = p[0] - 1; r[0] = {s, 0u}; r[1] = {P + s, 0u}; return 2; }
+        case 1: {
+            uint64_t c = (((uint64_t)(p[0] - 1)) * 4 + (p[1] - 1)) * 3;
+            r[0] = {6 * P + c, 0u}; r[1] = {6 * P + c + 1, 0u}; r[2] = {6 * P + c + 2, 0u};
+            return 3;
+        }
+        case 2: return 0;
+        case 3: { uint64_t s = p[0] - 1; r[0] = {s, 1u}; r[1] = {2 * P + s * 4 + (p[1] - 1), 1u}; return 2; }
+        case 4: if (p[0] == 0) return 0; r[0] = {P + (p[0] - 1), 1u}; return 1;
+        case 5: case 6:
+            if (p[0] == 0) return 0;
+            r[0] = {6 * P + (((uint64_t)(p[0] - 1)) * 4 + (p[2] - 1)) * 3 + p[3] / 8, 1u};
+            return 1;
+        }
+        return 0;
+    } else {
+        const uint64_t W = db.dims[0], D = db.dims[1], C = db.dims[2], I = db.dims[3];
+        const uint64_t WD = W * D, base_c = 2 * WD + W, base_s = base_c + WD * C;
+        if (t == 0) {
+            k = add_rec(r, k, (uint64_t)p[0] * D + p[1], 1u);
+            const uint32_t cnt = p[3];
+            for (uint32_t l = 0; l < cnt; ++l) {
+                uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l];
+                if (i >= I) continue;
+                k = add_rec(r, k, base_s + (uint64_t)sw * I + i, 1u);
+            }
+            return k;
+        }
+        r[0] = {WD + p[0], 1u};
+        r[1] = {WD + W + (uint64_t)p[0] * D + p[1], 1u};
+        if (p[4] == 2) return 2;                           // by-name lookup found nobody
+        r[2] = {base_c + ((uint64_t)p[2] * D + p[3]) * C + p[5], 1u};
+        return 3;
+    }
+}
+
+// =================================================================================
+// Stored procedures (whole transaction; K-SET and TPL)
+// =================================================================================
+DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    const int32_t delta = (int32_t)p[3];
+    int64_t* tel = COL(int64_t, B_TEL);
+    int64_t* br = COL(int64_t, B_BR);
+    stm(&tel[p[1]], ldm(&tel[p[1]]) + delta);
+    stm(&br[p[2]], ldm(&br[p[2]]) + delta);
+    const uint64_t r = db.ins_base[0] + idx;               // history row (every deposit commits)
+    INS(uint32_t, IB_TID)[r] = p[1];
+    INS(uint32_t, IB_BID)[r] = p[2];
+    INS(uint32_t, IB_AID)[r] = p[0];
+    INS(int32_t, IB_DELTA)[r] = delta;
+    INS(uint32_t, IB_TS)[r] = db.first_ts + idx;
+}
+DEV void tpcb_account(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    int64_t* acc = COL(int64_t, B_ACC);
+    const int64_t v = ldm(&acc[p[0]]) + (int32_t)p[3];
+    stm(&acc[p[0]], v);
+    reinterpret_cast<int64_t*>(db.out)[idx] = v;
+}
+
+// ---- TM-1 --------------------------------------------------------------------------
+DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+    uint8_t* o = db.out + (uint64_t)idx * 40;
+    switch (t) {
+    case 0: {   // GET_SUBSCRIBER_DATA
+        const uint32_t s = p[0] - 1;
+        put64(o, __ldg(&COL(const uint64_t, M_NBR)[s]));
+        put64(o + 8, __ldg(&COL(const uint64_t, M_HEX)[s]));
+        put32(o + 16, __ldg(&COL(const uint32_t, M_MSC)[s]));
+        put32(o + 20, ldm(&COL(uint32_t, M_VLR)[s]));
+        const uint16_t bits = ldm(&COL(uint16_t, M_BITS)[s]);
+        const uint8_t* b2 = COL(const uint8_t, M_BYTE2) + (uint64_t)s * 10;
+        o[24] = (uint8_t)bits; o[25] = (uint8_t)(bits >> 8);
+#pragma unroll
+        for (int k = 0; k < 10; ++k) o[26 + k] = __ldg(b2 + k);
+        return;
+    }
+    case 1: {   // GET_NEW_DESTINATION
+        const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
+        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f]) || !__ldg(&COL(const uint8_t, M_SF_ACTIVE)[f])) {
+            db.status[idx] = 1; return;
+        }
+        const uint8_t* live = COL(uint8_t, M_CF_LIVE);
+        const uint8_t* endt = COL(uint8_t, M_CF_END);
+        const uint64_t* num = COL(uint64_t, M_CF_NUM);
+        uint32_t cnt = 0;
+        for (uint32_t k = 0; k < 3; ++k) {
+            const uint64_t c = f * 3 + k;
+            if (ldm(&live[c]) && k * 8 <= p[2] && p[3] < ldm(&endt[c])) {
+                put64(o + 8 + 8 * cnt, ldm(&num[c]));
+                ++cnt;
+            }
+        }
+        if (cnt == 0) {
+            db.status[idx] = 1;
+            for (int k = 8; k < 32; k += 4) put32(o + k, 0);
+            return;
+        }
+        put32(o, cnt);
+        return;
+    }
+    case 2: {   // GET_ACCESS_DATA
+        const uint64_t a = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
+        if (!__ldg(&COL(const uint8_t, M_AI_VALID)[a])) { db.status[idx] = 1; return; }
+        o[0] = __ldg(&COL(const uint8_t, M_AI_D1)[a]);
+        o[1] = __ldg(&COL(const uint8_t, M_AI_D2)[a]);
+        put32(o + 4, __ldg(&COL(const uint32_t, M_AI_D3)[a]));
+        put64(o + 8, __ldg(&COL(const uint64_t, M_AI_D4)[a]));
+        return;
+    }
+    case 3: {   // UPDATE_SUBSCRIBER_DATA (two-phase: SF existence first)
+        const uint32_t s = p[0] - 1;
+        const uint64_t f = (uint64_t)s * 4 + (p[1] - 1);
+        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f])) { db.status[idx] = 1; return; }
+        uint16_t* bits = COL(uint16_t, M_BITS);
+        stm(&bits[s], (uint16_t)((ldm(&bits[s]) & 0xFFFEu) | (p[2] & 1u)));
+        stm(&COL(uint8_t, M_SF_DA)[f], (uint8_t)p[3]);
+        return;
+    }
+    case 4: {   // UPDATE_LOCATION (sub_nbr resolved at submit)
+        if (p[0] == 0) { db.status[idx] = 1; return; }
+        stm(&COL(uint32_t, M_VLR)[p[0] - 1], p[2]);
+        return;
+    }
+    case 5: {   // INSERT_CALL_FORWARDING
+        if (p[0] == 0) { db.status[idx] = 1; return; }
+        const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[2] - 1);
+        const uint64_t c = f * 3 + p[3] / 8;
+        uint8_t* live = COL(uint8_t, M_CF_LIVE);
+        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f]) || ldm(&live[c])) { db.status[idx] = 1; return; }
+        stm(&live[c], (uint8_t)1);
+        stm(&COL(uint8_t, M_CF_END)[c], (uint8_t)p[4]);
+        stm(&COL(uint64_t, M_CF_NUM)[c], (uint64_t)p[5] | ((uint64_t)p[6] << 32));
+        return;
+    }
+    case 6: {   // DELETE_CALL_FORWARDING
+        if (p[0] == 0) { db.status[idx] = 1; return; }
+        const uint64_t c = ((uint64_t)(p[0] - 1) * 4 + (p[2] - 1)) * 3 + p[3] / 8;
+        uint8_t* live = COL(uint8_t, M_CF_LIVE);
+        if (!ldm(&live[c])) { db.status[idx] = 1; return; }
+        stm(&live[c], (uint8_t)0);
+        return;
+    }
+    }
+}
+
+// ---- TPC-C -------------------------------------------------------------------------
+// NewOrder home part: district counter, ORDER / NEW_ORDER / ORDER_LINE rows, o_id,
+// total, per-line amount + brand; stock lines whose supply warehouse == sw_sel
+// (all lines when sw_sel == ALL).
+constexpr uint32_t ALL_LINES = 0xFFFFFFFFu;
+
+DEV bool tpcc_no_aborts(const DevDb& db, const uint32_t* p) {
+    const uint32_t cnt = p[3];
+    for (uint32_t l = 0; l < cnt; ++l)
+        if (p[4 + 3 * l] >= db.dims[3]) return true;       // unused item: roll back (static)
+    return false;
+}
+
+DEV void tpcc_no_stock(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_t sw_sel) {
+    const uint32_t I = db.dims[3], w = p[0], cnt = p[3];
+    int32_t* sq = COL(int32_t, C_S_QTY);
+    int64_t* sy = COL(int64_t, C_S_YTD);
+    uint32_t* so = COL(uint32_t, C_S_OCNT);
+    uint32_t* sr = COL(uint32_t, C_S_RCNT);
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    for (uint32_t l = 0; l < cnt; ++l) {
+        const uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l], q = p[6 + 3 * l];
+        if (sw_sel != ALL_LINES && sw != sw_sel) continue;
+        const uint64_t s = (uint64_t)sw * I + i;
+        const int32_t cur = ldm(&sq[s]);
+        stm(&sq[s], cur >= (int32_t)q + 10 ? cur - (int32_t)q : cur - (int32_t)q + 91);
+        stm(&sy[s], ldm(&sy[s]) + (int64_t)q);
+        stm(&so[s], ldm(&so[s]) + 1u);
+        if (sw != w) stm(&sr[s], ldm(&sr[s]) + 1u);
+        put32(o + 16 + 12 * l, (uint32_t)cur);
+    }
+}
+
+DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    const uint32_t D = db.dims[1], C = db.dims[2], w = p[0], d = p[1], c = p[2], cnt = p[3];
+    const uint64_t wd = (uint64_t)w * D + d;
+    uint32_t* dn = COL(uint32_t, C_D_NEXT);
+    const uint32_t oid = ldm(&dn[wd]);
+    stm(&dn[wd], oid + 1);
+    uint32_t all_local = 1;
+    for (uint32_t l = 0; l < cnt; ++l) all_local &= (p[5 + 3 * l] == w);
+    const uint64_t ro = db.ins_base[T_ORDER] + db.ins_off[T_ORDER * (uint64_t)db.ins_stride + idx];
+    INS(uint32_t, IO_ID)[ro] = oid; INS(uint32_t, IO_D)[ro] = d; INS(uint32_t, IO_W)[ro] = w;
+    INS(uint32_t, IO_C)[ro] = c; INS(uint32_t, IO_ENTRY)[ro] = db.first_ts + idx;
+    INS(uint32_t, IO_OLCNT)[ro] = cnt; INS(uint32_t, IO_ALLLOCAL)[ro] = all_local;
+    const uint64_t rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
+    INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
+    const uint64_t rl0 = db.ins_base[T_OLINE] + db.ins_off[T_OLINE * (uint64_t)db.ins_stride + idx];
+    const int32_t* price = COL(const int32_t, C_I_PRICE);
+    const uint8_t* iorig = COL(const uint8_t, C_I_ORIG);
+    const uint8_t* sorig = COL(const uint8_t, C_S_ORIG);
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    int64_t sum = 0;
+    for (uint32_t l = 0; l < cnt; ++l) {
+        const uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l], q = p[6 + 3 * l];
+        const int32_t amount = (int32_t)q * __ldg(&price[i]);
+        sum += amount;
+        const uint64_t rl = rl0 + l;
+        INS(uint32_t, IL_OID)[rl] = oid; INS(uint32_t, IL_D)[rl] = d; INS(uint32_t, IL_W)[rl] = w;
+        INS(uint32_t, IL_NUM)[rl] = l; INS(uint32_t, IL_I)[rl] = i; INS(uint32_t, IL_SW)[rl] = sw;
+        INS(uint32_t, IL_QTY)[rl] = q; INS(int32_t, IL_AMT)[rl] = amount;
+        put32(o + 16 + 12 * l + 4, (uint32_t)amount);
+        o[16 + 12 * l + 8] = (uint8_t)(__ldg(&iorig[i]) & __ldg(&sorig[(uint64_t)sw * db.dims[3] + i]));
+    }
+    const int64_t disc = __ldg(&COL(const int32_t, C_C_DISC)[wd * C + c]);
+    const int64_t tax = (int64_t)__ldg(&COL(const int32_t, C_W_TAX)[w]) + __ldg(&COL(const int32_t, C_D_TAX)[wd]);
+    const int64_t x = sum * (10000 - disc) * (10000 + tax);
+    put32(o, oid);
+    put32(o + 4, cnt);
+    put64(o + 8, (uint64_t)((x + 50000000) / 100000000));
+}
+
+DEV void tpcc_pay_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    const uint32_t D = db.dims[1], w = p[0], d = p[1], h = p[6];
+    int64_t* wy = COL(int64_t, C_W_YTD);
+    int64_t* dy = COL(int64_t, C_D_YTD);
+    const uint64_t wd = (uint64_t)w * D + d;
+    stm(&wy[w], ldm(&wy[w]) + (int64_t)h);
+    stm(&dy[wd], ldm(&dy[wd]) + (int64_t)h);
+    const uint64_t r = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
+    INS(uint32_t, IH_C)[r] = p[5]; INS(uint32_t, IH_CD)[r] = p[3]; INS(uint32_t, IH_CW)[r] = p[2];
+    INS(uint32_t, IH_D)[r] = d; INS(uint32_t, IH_W)[r] = w; INS(uint32_t, IH_DATE)[r] = db.first_ts + idx;
+    INS(int32_t, IH_AMT)[r] = (int32_t)h;
+}
+DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    const uint32_t D = db.dims[1], C = db.dims[2], h = p[6];
+    const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
+    int64_t* bal = COL(int64_t, C_C_BAL);
+    int64_t* ytd = COL(int64_t, C_C_YTD);
+    uint32_t* cnt = COL(uint32_t, C_C_CNT);
+    const int64_t nb = ldm(&bal[cx]) - (int64_t)h;
+    stm(&bal[cx], nb);
+    stm(&ytd[cx], ldm(&ytd[cx]) + (int64_t)h);
+    stm(&cnt[cx], ldm(&cnt[cx]) + 1u);
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    put32(o, p[5]);
+    put32(o + 4, __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]));
+    put64(o + 8, (uint64_t)nb);
+}
+
+// The combined kernel body: one whole transaction (K-SET, TPL).
+template <int S>
+DEV void exec_txn(const DevDb& db, uint32_t idx) {
+    const uint32_t t = db.type[idx];
+    const uint32_t* p = db.pw + db.poff[idx];
+    if (S == S_TPCB) {
+        tpcb_account(db, idx, p);
+        tpcb_home(db, idx, p);
+    } else if (S == S_TM1) {
+        tm1_txn(db, idx, t, p);
+    } else {
+        if (t == 0) {
+            if (tpcc_no_aborts(db, p)) { db.status[idx] = 1; return; }
+            tpcc_no_home(db, idx, p);
+            tpcc_no_stock(db, idx, p, ALL_LINES);
+        } else {
+            if (p[4] == 2) { db.status[idx] = 1; return; }
+            tpcc_pay_home(db, idx, p);
+            tpcc_pay_customer(db, idx, p);
+        }
+    }
+}
+
+// =================================================================================
+// PART fragments (DESIGN.md R-S9): a cross-partition transaction whose parts share
+// no data flow runs as one fragment per partition; each partition executes its
+// fragments in ts order.  frag key = pid << 32 | idx << 8 | kind
+// =================================================================================
+enum { F_WHOLE = 0, F_HOME = 1, F_REMOTE = 2 };
+
+DEV uint64_t frag_key(uint32_t pid, uint32_t idx, uint32_t kind) {
+    return ((uint64_t)pid << 32) | ((uint64_t)idx << 8) | kind;
+}
+
+// number of fragments of txn idx and, if out != nullptr, the keys
+template <int S>
+DEV int fragments(const DevDb& db, uint32_t idx, uint64_t* out) {
+    const uint32_t t = db.type[idx];
+    const uint32_t* p = db.pw + db.poff[idx];
+    if (S == S_TPCB) {
+        const uint32_t home = p[2], own = p[0] / db.dims[2];
+        if (home == own) { if (out) out[0] = frag_key(home, idx, F_WHOLE); return 1; }
+        if (out) { out[0] = frag_key(home, idx, F_HOME); out[1] = frag_key(own, idx, F_REMOTE); }
+        return 2;
+    } else if (S == S_TM1) {
+        const uint32_t pid = p[0] ? (p[0] - 1) / db.part_size : 0;
+        if (out) out[0] = frag_key(pid, idx, F_WHOLE);
+        return 1;
+    } else {
+        const uint32_t w = p[0];
+        if (t == 0) {
+            if (tpcc_no_aborts(db, p)) { if (out) out[0] = frag_key(w, idx, F_HOME); return 1; }
+            int k = 0;
+            if (out) out[k] = frag_key(w, idx, F_HOME);
+            ++k;
+            const uint32_t cnt = p[3];
+            for (uint32_t l = 0; l < cnt; ++l) {
+                const uint32_t sw = p[5 + 3 * l];
+                if (sw == w) continue;
+                bool seen = false;
+                for (uint32_t m = 0; m < l; ++m) seen |= (p[5 + 3 * m] == sw);
+                if (seen) continue;
+                if (out) out[k] = frag_key(sw, idx, F_REMOTE);
+                ++k;
+            }
+            return k;
+        }
+        if (p[4] == 2 || p[2] == w) { if (out) out[0] = frag_key(w, idx, F_WHOLE); return 1; }
+        if (out) { out[0] = frag_key(w, idx, F_HOME); out[1] = frag_key(p[2], idx, F_REMOTE); }
+        return 2;
+    }
+}
+
+template <int S>
+DEV void exec_frag(const DevDb& db, uint64_t fk) {
+    const uint32_t pid = (uint32_t)(fk >> 32), idx = (uint32_t)(fk >> 8) & 0xFFFFFFu, kind = (uint32_t)fk & 0xFFu;
+    const uint32_t t = db.type[idx];
+    const uint32_t* p = db.pw + db.poff[idx];
+    if (S == S_TPCB) {
+        if (kind != F_REMOTE) tpcb_home(db, idx, p);
+        if (kind != F_HOME) tpcb_account(db, idx, p);
+    } else if (S == S_TM1) {
+        tm1_txn(db, idx, t, p);
+    } else {
+        if (t == 0) {
+            if (tpcc_no_aborts(db, p)) { db.status[idx] = 1; return; }
+            if (kind != F_REMOTE) tpcc_no_home(db, idx, p);
+            tpcc_no_stock(db, idx, p, pid);
+        } else {
+            if (p[4] == 2) { if (kind != F_REMOTE) db.status[idx] = 1; return; }
+            if (kind != F_REMOTE) tpcc_pay_home(db, idx, p);
+            if (kind != F_HOME) tpcc_pay_customer(db, idx, p);
+        }
+    }
+}
+
+}  // namespace gputx

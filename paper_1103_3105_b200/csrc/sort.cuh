@@ -1,0 +1,187 @@
+// sort.cuh — stable LSD radix sort of u64 keys on a bit range, onesweep style:
+// one histogram pass over the keys for all digit passes, then per 8-bit digit pass a
+// single kernel that ranks a 4096-key tile (warp multi-split with __match_any_sync),
+// obtains the tile's global digit offsets by decoupled look-back, stages the tile in
+// shared memory in digit order and writes it out coalesced.
+//
+// The paper groups access records "firstly on v and then on id" with a sort
+// (§4.2) and partitions PART's transactions with a radix sort
+// (§5.2).  Records are emitted in timestamp order, so a STABLE sort on
+// the item (resp. partition) bits alone yields (item, ts) order.
+#pragma once
+#include "common.cuh"
+
+namespace gputx {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_WK = 32 * RS_ITEMS;               // keys per warp
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per tile
+constexpr int RS_MAXPASS = 5;
+constexpr int RS_HIST_GRID = 296;
+
+struct SortWs {
+    uint32_t* hist;        // [RS_MAXPASS][256]
+    uint64_t* status;      // [max_tiles][256]  (epoch:30 | kind:2) << 32 | value
+    uint32_t* tickets;     // [64]
+    uint64_t max_tiles;
+};
+
+__global__ void __launch_bounds__(256) rs_hist_kernel(const uint64_t* __restrict__ keys,
+                                                      const uint32_t* __restrict__ n_ptr, uint32_t lo,
+                                                      uint32_t nbits, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[RS_MAXPASS][256];
+    const uint32_t npass = (nbits + 7) / 8;
+    for (uint32_t i = threadIdx.x; i < RS_MAXPASS * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t n = *n_ptr;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31) & ~31u); i += gridDim.x * blockDim.x) {
+        const bool valid = i < n;
+        const uint64_t k = valid ? __ldg(&keys[i]) : 0;
+        for (uint32_t p = 0; p < npass; ++p) {
+            const uint32_t w = min(8u, nbits - 8 * p);
+            const uint32_t d = valid ? (uint32_t)(k >> (lo + 8 * p)) & ((1u << w) - 1) : 0x100u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (d < 256 && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&h[p][d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+// exclusive scan of each pass's 256 counts (one block per pass)
+__global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t* hist) {
+    __shared__ uint32_t sm[8];
+    uint32_t* h = hist + blockIdx.x * 256;
+    uint32_t v = h[threadIdx.x], tot;
+    uint32_t ex = block_scan_excl<uint32_t, OpAddU32>(v, tot, sm);
+    h[threadIdx.x] = ex;
+}
+
+DEV uint64_t rs_pack(uint32_t epoch, uint32_t kind, uint32_t v) {
+    return ((uint64_t)((epoch << 2) | kind) << 32) | v;
+}
+
+__global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __restrict__ in,
+                                                             uint64_t* __restrict__ out,
+                                                             const uint32_t* __restrict__ n_ptr,
+                                                             uint32_t shift, uint32_t mask,
+                                                             const uint32_t* __restrict__ base,
+                                                             uint64_t* status, uint32_t epoch,
+                                                             uint32_t* ticket) {
+    __shared__ uint32_t whist[RS_WARPS][256];
+    __shared__ uint32_t tstart[256];
+    __shared__ uint32_t gbase[256];
+    __shared__ uint32_t scan_sm[8];
+    __shared__ uint64_t stage[RS_TILE];
+    __shared__ uint32_t s_tile;
+
+    const uint32_t n = *n_ptr;
+    const uint32_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    for (uint32_t i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t tbase = (uint64_t)tile * RS_TILE;
+
+    uint64_t key[RS_ITEMS];
+    uint16_t loc[RS_ITEMS];
+    const uint64_t wbase = tbase + wid * RS_WK;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint64_t i = wbase + j * 32 + lane;
+        key[j] = i < n ? __ldg(&in[i]) : ~0ull;
+    }
+    const uint32_t lmask = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint64_t i = wbase + j * 32 + lane;
+        const uint32_t d = i < n ? (uint32_t)(key[j] >> shift) & mask : 0x100u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if ((int)lane == leader && d < 256) {
+            old = whist[wid][d];
+            whist[wid][d] = old + __popc(peers);
+        }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        loc[j] = (uint16_t)(old + __popc(peers & lmask));
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps (in key order), tile count
+    const uint32_t d = tid;                     // RS_THREADS == 256 digits
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+        const uint32_t c = whist[w][d];
+        whist[w][d] = cnt;
+        cnt += c;
+    }
+    // decoupled look-back per digit across tiles
+    uint64_t* st = status + (uint64_t)tile * 256 + d;
+    uint32_t excl = 0;
+    if (tile == 0) {
+        st_release64(st, rs_pack(epoch, 2, cnt));
+    } else {
+        st_release64(st, rs_pack(epoch, 1, cnt));
+        int64_t p = (int64_t)tile - 1;
+        while (p >= 0) {
+            uint64_t s;
+            do { s = ld_acquire64(status + (uint64_t)p * 256 + d); } while ((uint32_t)(s >> 34) != epoch);
+            excl += (uint32_t)s;
+            if (((s >> 32) & 3u) == 2u) break;
+            --p;
+        }
+        st_release64(st, rs_pack(epoch, 2, excl + cnt));
+    }
+    gbase[d] = base[d] + excl;
+    uint32_t tot;
+    tstart[d] = block_scan_excl<uint32_t, OpAddU32>(cnt, tot, scan_sm);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint64_t i = wbase + j * 32 + lane;
+        if (i < n) {
+            const uint32_t dj = (uint32_t)(key[j] >> shift) & mask;
+            stage[tstart[dj] + whist[wid][dj] + loc[j]] = key[j];
+        }
+    }
+    __syncthreads();
+    const uint32_t tn = (n - tbase) < (uint64_t)RS_TILE ? (uint32_t)(n - tbase) : (uint32_t)RS_TILE;
+    for (uint32_t i = tid; i < tn; i += RS_THREADS) {
+        const uint64_t k = stage[i];
+        const uint32_t dk = (uint32_t)(k >> shift) & mask;
+        out[gbase[dk] + (i - tstart[dk])] = k;
+    }
+}
+
+// Sorts n (device value, <= n_max) keys of a[] on bits [lo, lo+nbits).  Returns the
+// buffer holding the result (a or b).  epoch is advanced by the passes used.
+inline uint64_t* radix_sort_u64(uint64_t* a, uint64_t* b, const uint32_t* n_dev, uint64_t n_max, uint32_t lo,
+                                uint32_t nbits, SortWs& ws, uint32_t& epoch, cudaStream_t s) {
+    if (n_max == 0 || nbits == 0) return a;
+    const uint32_t npass = (nbits + 7) / 8;
+    cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * RS_MAXPASS * 256, s);
+    cudaMemsetAsync(ws.tickets, 0, sizeof(uint32_t) * 64, s);
+    rs_hist_kernel<<<RS_HIST_GRID, 256, 0, s>>>(a, n_dev, lo, nbits, ws.hist);
+    rs_scan_kernel<<<npass, 256, 0, s>>>(ws.hist);
+    const uint32_t grid = (uint32_t)((n_max + RS_TILE - 1) / RS_TILE);
+    uint64_t* src = a;
+    uint64_t* dst = b;
+    for (uint32_t p = 0; p < npass; ++p) {
+        const uint32_t w = nbits - 8 * p < 8 ? nbits - 8 * p : 8;
+        ++epoch;
+        rs_pass_kernel<<<grid, RS_THREADS, 0, s>>>(src, dst, n_dev, lo + 8 * p, (1u << w) - 1, ws.hist + p * 256,
+                                                   ws.status, epoch, ws.tickets + p);
+        uint64_t* t = src; src = dst; dst = t;
+    }
+    return src;
+}
+
+}  // namespace gputx

@@ -1,0 +1,273 @@
+"""ctypes binding of include/gputx.h — argument marshalling only.
+
+The names mirror the C ABI (gputx_open_db / load_column / seal / register_types /
+submit_bulk / execute / read_results ...).  No transaction logic lives here.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "libgputx.so")
+
+GPUTX_TPL, GPUTX_PART, GPUTX_KSET = 0, 1, 2
+TPL, PART, KSET = "tpl", "part", "kset"
+STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET}
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_TYPE", 5: "ESTATE",
+                6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
+OUT_STRIDE = {1: 8, 2: 40, 3: 200}
+
+
+class GputxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("schema", ctypes.c_int), ("dims", ctypes.c_uint32 * 4), ("max_bulk", ctypes.c_uint64),
+                ("insert_capacity", ctypes.c_uint64), ("part_size", ctypes.c_uint32), ("device", ctypes.c_int),
+                ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+
+
+class BulkC(ctypes.Structure):
+    _fields_ = [("type", ctypes.c_void_p), ("param_off", ctypes.c_void_p), ("param_words", ctypes.c_void_p),
+                ("n", ctypes.c_uint64), ("on_device", ctypes.c_int)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in ("n", "committed", "aborted", "depth", "ksets", "zero_set", "records",
+                                               "rank_passes", "parts", "fragments", "max_chain")] + \
+               [(k, ctypes.c_double) for k in ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_merge",
+                                               "ms_total")]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libgputx.so (build it first with paper_1103_3105_b200.build.build()).
+    Raises if it is missing: there is no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built; run python -m paper_1103_3105_b200.build")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, U32, U64, I = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    sig = {
+        "gputx_open_db": ([ctypes.POINTER(Config), ctypes.POINTER(P)], I),
+        "gputx_load_column": ([P, ctypes.c_char_p, P, U64], I),
+        "gputx_column_info": ([P, U32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(U32), ctypes.POINTER(U64)], I),
+        "gputx_seal": ([P], I),
+        "gputx_register_types": ([P, P, U32], I),
+        "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
+        "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
+        "gputx_read_results": ([P, P, P, U64], I),
+        "gputx_results_device": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)], I),
+        "gputx_out_stride": ([I], U32),
+        "gputx_read_column": ([P, ctypes.c_char_p, P, U64], I),
+        "gputx_insert_rows": ([P, ctypes.c_char_p, ctypes.POINTER(U64)], I),
+        "gputx_read_insert_column": ([P, ctypes.c_char_p, ctypes.c_char_p, P, U64], I),
+        "gputx_read_depths": ([P, P, U64], I),
+        "gputx_read_perm": ([P, P, U64], I),
+        "gputx_reset": ([P], I),
+        "gputx_close_db": ([P], None),
+        "gputx_last_error": ([P], ctypes.c_char_p),
+        "gputx_set_launch": ([P, U32, U32, U32], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_seal", "gputx_register_types",
+            "gputx_submit_bulk", "gputx_execute", "gputx_read_results", "gputx_results_device",
+            "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
+            "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
+            "gputx_set_launch"]
+
+INSERT_TABLES = {
+    1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
+    2: {},
+    3: {"order": ["o_id", "o_d", "o_w", "o_c", "o_entry_d", "o_ol_cnt", "o_all_local"],
+        "new_order": ["no_o_id", "no_d", "no_w"],
+        "order_line": ["ol_o_id", "ol_d", "ol_w", "ol_number", "ol_i_id", "ol_supply_w", "ol_quantity", "ol_amount"],
+        "history": ["h_c", "h_cd", "h_cw", "h_d", "h_w", "h_date", "h_amount"]},
+}
+SIGNED_INSERT_COLS = {"h_delta", "ol_amount", "h_amount"}
+
+
+def _ptr(a) -> int:
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    assert a.flags.c_contiguous
+    return a.ctypes.data
+
+
+class Database:
+    """One gputx_db handle: an HBM-resident database of one schema on one GPU."""
+
+    def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
+                 device: int = 0, stream: int | None = None, insert_capacity: int = 0):
+        self.lib = load_library()
+        self.schema = schema
+        cfg = Config()
+        cfg.schema = schema
+        for k, v in enumerate(dims):
+            cfg.dims[k] = int(v)
+        cfg.max_bulk = int(max_bulk)
+        cfg.insert_capacity = int(insert_capacity)
+        cfg.part_size = int(part_size)
+        cfg.device = int(device)
+        cfg.stream = stream
+        h = ctypes.c_void_p()
+        self._check(self.lib.gputx_open_db(ctypes.byref(cfg), ctypes.byref(h)), None)
+        self.h = h
+        self.stride = OUT_STRIDE[schema]
+        self.n = 0
+        self.columns = {}
+        k = 0
+        while True:
+            nm, el, cnt = ctypes.c_char_p(), ctypes.c_uint32(), ctypes.c_uint64()
+            if self.lib.gputx_column_info(self.h, k, ctypes.byref(nm), ctypes.byref(el), ctypes.byref(cnt)) != 0:
+                break
+            self.columns[nm.value.decode()] = (el.value, cnt.value)
+            k += 1
+        if image is not None:
+            for name in self.columns:
+                self.load_column(name, image[name])
+            self.seal()
+
+    # --------------------------------------------------------------------------------
+    def _check(self, status: int, h):
+        if status != 0:
+            msg = self.lib.gputx_last_error(h).decode() if h else "open failed"
+            raise GputxError(status, msg)
+
+    def load_column(self, name: str, arr: np.ndarray):
+        a = np.ascontiguousarray(arr)
+        self._check(self.lib.gputx_load_column(self.h, name.encode(), a.ctypes.data, a.nbytes), self.h)
+
+    def seal(self):
+        self._check(self.lib.gputx_seal(self.h), self.h)
+
+    def register_types(self, ids):
+        a = np.ascontiguousarray(np.asarray(ids, np.uint32))
+        self._check(self.lib.gputx_register_types(self.h, a.ctypes.data if a.size else None, a.size), self.h)
+
+    def submit(self, bulk=None, *, type=None, param_off=None, param_words=None, on_device: bool = False) -> int:
+        """Submit a bulk: any object with .type/.param_off/.param_words (numpy, host), or
+        the three arrays as torch CUDA tensors with on_device=True (resident in HBM)."""
+        if bulk is not None:
+            type, param_off, param_words = bulk.type, bulk.param_off, bulk.param_words
+        if not on_device:
+            type = np.ascontiguousarray(type, np.uint8)
+            param_off = np.ascontiguousarray(param_off, np.uint32)
+            param_words = np.ascontiguousarray(param_words, np.uint32)
+            if param_words.size == 0:
+                param_words = np.zeros(1, np.uint32)
+        self._keep = (type, param_off, param_words)
+        b = BulkC(_ptr(type), _ptr(param_off), _ptr(param_words), int(type.shape[0]), int(on_device))
+        ts = ctypes.c_uint64()
+        self._check(self.lib.gputx_submit_bulk(self.h, ctypes.byref(b), ctypes.byref(ts)), self.h)
+        self.n = int(type.shape[0])
+        return ts.value
+
+    def execute(self, strategy: str = KSET) -> dict:
+        st = Stats()
+        self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
+        return st.as_dict()
+
+    def execute_nostats(self, strategy: str = KSET):
+        self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], None), self.h)
+
+    def read_results(self, status: np.ndarray | None = None, out: np.ndarray | None = None):
+        if status is None:
+            status = np.zeros(self.n, np.uint8)
+        if out is None:
+            out = np.zeros((self.n, self.stride), np.uint8)
+        self._check(self.lib.gputx_read_results(self.h, _ptr(status) if self.n else None,
+                                                _ptr(out) if self.n else None, out.nbytes), self.h)
+        return status, out
+
+    def results_device(self):
+        s, o, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        self._check(self.lib.gputx_results_device(self.h, ctypes.byref(s), ctypes.byref(o), ctypes.byref(n)), self.h)
+        return s.value, o.value, n.value
+
+    def read_column(self, name: str) -> np.ndarray:
+        el, cnt = self.columns[name]
+        a = np.zeros(el * cnt, np.uint8)
+        self._check(self.lib.gputx_read_column(self.h, name.encode(), a.ctypes.data, a.nbytes), self.h)
+        return a
+
+    def read_image(self, like: dict) -> dict:
+        """All columns, viewed with the dtype/shape of `like` (e.g. the initial image)."""
+        out = {}
+        for name in self.columns:
+            raw = self.read_column(name)
+            ref = np.asarray(like[name])
+            out[name] = raw.view(ref.dtype).reshape(ref.shape)
+        return out
+
+    def inserts(self) -> dict:
+        res = {}
+        for tab, cols in INSERT_TABLES[self.schema].items():
+            rows = ctypes.c_uint64()
+            self._check(self.lib.gputx_insert_rows(self.h, tab.encode(), ctypes.byref(rows)), self.h)
+            res[tab] = {}
+            for c in cols:
+                dt = np.int32 if c in SIGNED_INSERT_COLS else np.uint32
+                a = np.zeros(rows.value, dt)
+                self._check(self.lib.gputx_read_insert_column(self.h, tab.encode(), c.encode(),
+                                                              a.ctypes.data if a.size else None, a.nbytes), self.h)
+                res[tab][c] = a
+        return res
+
+    def depths(self) -> np.ndarray:
+        a = np.zeros(max(1, self.n), np.uint32)
+        self._check(self.lib.gputx_read_depths(self.h, a.ctypes.data, self.n), self.h)
+        return a[:self.n]
+
+    def perm(self) -> np.ndarray:
+        a = np.zeros(max(1, self.n), np.uint32)
+        self._check(self.lib.gputx_read_perm(self.h, a.ctypes.data, self.n), self.h)
+        return a[:self.n]
+
+    def set_launch(self, exec_block: int = 0, exec_grid: int = 0, narrow_max: int = 0):
+        self._check(self.lib.gputx_set_launch(self.h, exec_block, exec_grid, narrow_max), self.h)
+
+    def reset(self):
+        self._check(self.lib.gputx_reset(self.h), self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gputx_close_db(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,57 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every entry point
+include/gputx.h declares (no compute calls: runs without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gputx.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gputx_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_header():
+    from paper_1103_3105_b200 import build
+    lib_path = build.build()
+    lib = ctypes.CDLL(lib_path)
+    names = _declared()
+    assert len(names) >= 15
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    from paper_1103_3105_b200 import gputx
+    assert set(gputx.EXPORTED) == set(names)
+
+
+def test_sass_is_sm100a():
+    from paper_1103_3105_b200 import build
+    out = subprocess.run(["cuobjdump", "--list-elf", build.build()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_out_stride_without_gpu():
+    from paper_1103_3105_b200 import gputx
+    lib = gputx.load_library()
+    assert [lib.gputx_out_stride(s) for s in (1, 2, 3)] == [8, 40, 200]
+
+
+def test_no_cpu_fallback_without_library(tmp_path, monkeypatch):
+    from paper_1103_3105_b200 import gputx
+    monkeypatch.setattr(gputx, "_lib", None)
+    monkeypatch.setattr(gputx, "_LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(ImportError):
+        gputx.Database(1, (1, 1, 1, 0), 4)
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1103_3105_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f

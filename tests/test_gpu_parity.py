@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle (Definition 1,
+PAPER.md:73), bit-exact on final database, statuses, outputs and inserted rows,
+for TPL / PART / K-SET on TPC-B, TM-1 and TPC-C."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import compare, gpu_db, run_both
+
+pytestmark = pytest.mark.gpu
+
+STRATS = ["kset", "part", "tpl"]
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_tpcb_tiny_config1(strategy):
+    """BASELINE config 1: 1 branch, 10 tellers, 100k accounts, 4,096 deposits."""
+    dims = W.TpcbDims(1, 10, 100_000)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 4096, seed=1)
+    db = gpu_db(W.TPCB, dims, image, 4096)
+    st = run_both(W.TPCB, dims, image, [bulk], strategy, db=db)[0]
+    if strategy == "kset":
+        assert np.array_equal(db.depths(), np.arange(4096))       # one path: depth(t) = t
+        assert st["depth"] == 4095 and st["zero_set"] == 1
+    db.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("n", [1, 37, 9000])
+def test_tpcb_multibranch(strategy, n):
+    dims = W.TpcbDims(16, 10, 2000)
+    image = W.tpcb_db(dims)
+    run_both(W.TPCB, dims, image, [W.tpcb_bulk(dims, n, seed=n, remote_pct=15.0)], strategy)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("dist", ["nurand", "uniform"])
+def test_tm1(strategy, dist):
+    dims = W.Tm1Dims(20_000)
+    image = W.tm1_db(dims, seed=3)
+    bulks = [W.tm1_bulk(dims, 30_011, seed=5, dist=dist), W.tm1_bulk(dims, 7_000, seed=6, dist=dist)]
+    run_both(W.TM1, dims, image, bulks, strategy, max_bulk=40_000)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_tpcc(strategy):
+    dims = W.TpccDims(4, 10, 3000, 100_000)
+    image = W.tpcc_db(dims, seed=2)
+    bulks = [W.tpcc_bulk(dims, 12_345, seed=7), W.tpcc_bulk(dims, 3_000, seed=8)]
+    run_both(W.TPCC, dims, image, bulks, strategy, max_bulk=20_000)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_tpcc_tiny_contention(strategy):
+    """Tiny dimensions: many remote lines/customers, duplicate items, by-name, aborts."""
+    dims = W.TpccDims(3, 2, 30, 40)
+    image = W.tpcc_db(dims, seed=4)
+    bulk = W.tpcc_bulk(dims, 5000, seed=9, remote_line_pct=30.0, remote_pay_pct=40.0, rbk_pct=10.0)
+    run_both(W.TPCC, dims, image, [bulk], strategy)
+
+
+@pytest.mark.parametrize("schema,dims,kw", [
+    (W.TPCB, W.TpcbDims(8, 10, 1000), dict(remote_pct=15.0)),
+    (W.TM1, W.Tm1Dims(5000), dict(dist="nurand")),
+    (W.TPCC, W.TpccDims(2, 10, 3000, 1000), {}),
+])
+def test_kset_depths_match_oracle(schema, dims, kw):
+    """A5: the rank fixpoint equals the T-dependency-graph depth."""
+    image = W.make_db(schema, dims, seed=3)
+    bulk = W.make_bulk(schema, dims, 20_000, 11, **kw)
+    db = gpu_db(schema, dims, image, bulk.n)
+    db.submit(bulk)
+    st = db.execute("kset")
+    d = db.depths()
+    ref = oracle.depths(schema, dims.dims, image, bulk)
+    assert np.array_equal(d, ref)
+    assert st["depth"] == ref.max() and st["zero_set"] == int((ref == 0).sum())
+    # A6: perm is a permutation ordered by (depth, type)
+    perm = db.perm()
+    assert np.array_equal(np.sort(perm), np.arange(bulk.n))
+    key = ref[perm].astype(np.int64) * 8 + bulk.type[perm]
+    assert (np.diff(key) >= 0).all()
+    db.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_grid_shape_independence(strategy):
+    dims = W.Tm1Dims(3000)
+    image = W.tm1_db(dims, seed=1)
+    bulk = W.tm1_bulk(dims, 20_000, seed=2)
+    ref = oracle.run(W.TM1, dims.dims, image, bulk)
+    for grid, narrow in [(1, 64), (7, 1), (0, 1024)]:
+        db = gpu_db(W.TM1, dims, image, bulk.n)
+        db.set_launch(exec_grid=grid, narrow_max=narrow)
+        db.submit(bulk)
+        db.execute(strategy)
+        compare(W.TM1, ref, db, image, label=f"grid {grid} narrow {narrow}")
+        db.close()
+
+
+def test_empty_bulk():
+    dims = W.TpcbDims(2, 10, 100)
+    image = W.tpcb_db(dims)
+    db = gpu_db(W.TPCB, dims, image, 16)
+    empty = W.tpcb_bulk(dims, 0, seed=1)
+    for s in STRATS:
+        db.submit(empty)
+        st = db.execute(s)
+        assert st["n"] == 0
+    db.close()
+
+
+def test_errors():
+    from paper_1103_3105_b200 import GputxError
+    dims = W.Tm1Dims(100)
+    image = W.tm1_db(dims, seed=1)
+    db = gpu_db(W.TM1, dims, image, 64)
+    with pytest.raises(GputxError) as e:
+        db.register_types([0, 1, 1])
+    assert e.value.name == "EDUP_TYPE"
+    with pytest.raises(GputxError) as e:
+        db.register_types([9])
+    assert e.value.name == "EUNKNOWN_TYPE"
+    db.register_types([0, 4])                        # GSD and UL only
+    b = W.tm1_bulk(dims, 20, seed=1)                 # contains other types
+    with pytest.raises(GputxError) as e:
+        db.submit(b)
+    assert e.value.name == "EUNKNOWN_TYPE"
+    db.register_types(list(range(7)))
+    with pytest.raises(GputxError) as e:
+        db.submit(W.tm1_bulk(dims, 65, seed=1))
+    assert e.value.name == "ECAPACITY"
+    bad = W.tm1_bulk(dims, 10, seed=1)
+    bad.param_words = bad.param_words.copy()
+    i = int(np.nonzero(bad.type == W.TM1_GSD)[0][0])
+    bad.param_words[bad.param_off[i]] = 10_000        # s_id out of range
+    with pytest.raises(GputxError) as e:
+        db.submit(bad)
+    assert e.value.name == "EINVAL"
+    with pytest.raises(GputxError) as e:
+        db.execute("kset")
+    assert e.value.name == "ESTATE"
+    db.submit(W.tm1_bulk(dims, 10, seed=2))
+    with pytest.raises(GputxError) as e:
+        db.submit(W.tm1_bulk(dims, 10, seed=3))
+    assert e.value.name == "ESTATE"
+    db.execute("tpl")
+    db.close()
+
+
+def test_reset_restores_pristine():
+    dims = W.TpcbDims(4, 10, 1000)
+    image = W.tpcb_db(dims)
+    db = gpu_db(W.TPCB, dims, image, 5000)
+    db.submit(W.tpcb_bulk(dims, 5000, seed=1))
+    db.execute("kset")
+    db.reset()
+    got = db.read_image(image)
+    for k in image:
+        assert np.array_equal(got[k], image[k])
+    assert db.inserts()["history"]["h_ts"].size == 0
+    run_both(W.TPCB, dims, image, [W.tpcb_bulk(dims, 5000, seed=1)], "part", db=db)
+    db.close()

@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""GPUTx B200 benchmark: bulk transactions/s (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 2 — TM-1 (TATP), 1M subscribers, bulks of
+1M transactions (TATP standard mix, NURand s_id), K-SET strategy (headline), with
+PART and TPL measured on the same bulks.  One "step" = one bulk through the whole
+hot path: submit (ingest: validation + split lookups) and execute (emit, sort, rank,
+group, k-set rounds) — every §8(a) row.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tm1|tpcb|tpcb_tiny|tpcc]
+  python bench.py --impl reference ...   # the oracle (serial CPU executor) as reference arm
+
+For N > 1 (torchrun), every rank owns an independent shard (its own subscribers /
+branches / warehouses and its own bulk): weak scaling, no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "bulk transactions/sec (TM-1, TPC-B, TPC-C) at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "txn/s"
+
+WORKLOADS = {
+    "tm1": dict(schema=W.TM1, dims=W.Tm1Dims(1_000_000), n=1_000_000, kw=dict(dist="nurand"),
+                desc="TM-1 (TATP) 1M subscribers, bulk 1M, standard mix, NURand s_id"),
+    "tm1_uniform": dict(schema=W.TM1, dims=W.Tm1Dims(1_000_000), n=1_000_000, kw=dict(dist="uniform"),
+                        desc="TM-1 (TATP) 1M subscribers, bulk 1M, standard mix, uniform s_id"),
+    "tpcb": dict(schema=W.TPCB, dims=W.TpcbDims(1000, 10, 100_000), n=4_000_000, kw=dict(remote_pct=15.0),
+                 desc="TPC-B 1,000 branches, bulk 4M, uniform, 15% remote accounts"),
+    "tpcb_tiny": dict(schema=W.TPCB, dims=W.TpcbDims(1, 10, 100_000), n=4096, kw={},
+                      desc="TPC-B tiny: 1 branch, 10 tellers, 100k accounts, bulk 4,096"),
+    "tpcc": dict(schema=W.TPCC, dims=W.TpccDims(64, 10, 3000, 100_000), n=1_000_000, kw={},
+                 desc="TPC-C NewOrder+Payment, 64 warehouses, bulk 1M"),
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------------------
+# algorithmic bytes (DESIGN.md §"Roofline"): what the method itself must move
+# --------------------------------------------------------------------------------------
+def exec_bytes(schema: int, bulk, status: np.ndarray) -> int:
+    """Bytes the k-set executor must read/write for this bulk: perm index (4), type (1),
+    param offset (4), params (4/word), the columns each procedure touches on its
+    committed or aborted path (App. B profiles), status byte of aborts, output bytes."""
+    t = bulk.type
+    nw = np.diff(bulk.param_off.astype(np.int64))
+    base = 9 + 4 * nw
+    ok = status == 0
+    if schema == W.TPCB:
+        per = base + 3 * 16 + 20 + 8                 # A/T/B read+write, history row, output
+        return int(per.sum())
+    if schema == W.TM1:
+        extra = np.zeros(t.shape[0], np.int64)
+        extra[t == W.TM1_GSD] = 36 + 36
+        g = t == W.TM1_GND
+        extra[g] = 2 + np.where(ok[g], 6 + 2 * (8 + 8) + 4, 1)       # ~2 qualifying rows read+written
+        a = t == W.TM1_GAD
+        extra[a] = 1 + np.where(ok[a], 14 + 16, 1)
+        u = t == W.TM1_USD
+        extra[u] = 1 + np.where(ok[u], 5, 1)
+        extra[t == W.TM1_UL] = 4
+        i = t == W.TM1_ICF
+        extra[i] = 2 + np.where(ok[i], 10, 1)
+        d = t == W.TM1_DCF
+        extra[d] = 1 + np.where(ok[d], 1, 1)
+        return int((base + extra).sum())
+    # TPC-C: NO: district r/w 8, per line stock 4x(r+w)=48 -> ~ (4+8+4+4)*2 + price 4 + orig 2 + OL row 32 + out 12;
+    #        order/new_order rows 40, discount/tax 12, out 16.   Payment: W/D ytd 32, customer 40, hist 28, out 16.
+    no = t == W.TPCC_NEWORDER
+    cnt = np.zeros(t.shape[0], np.int64)
+    offs = bulk.param_off[:-1].astype(np.int64)
+    cnt[no] = bulk.param_words[offs[no] + 3]
+    per = base.copy()
+    per[no] += np.where(ok[no], 8 + 40 + 12 + 16 + cnt[no] * (40 + 6 + 32 + 12), 1)
+    per[~no] += np.where(ok[~no], 32 + 40 + 28 + 16, 1)
+    return int(per.sum())
+
+
+def rank_bytes(records: int, passes: int, n: int) -> int:
+    """Per pass: read each sorted record (8 B) and gather its transaction's depth (4 B);
+    plus the initial zeroing of D (4 B/txn)."""
+    return passes * records * 12 + 4 * n
+
+
+# --------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if (torch.cuda.is_available() and args.impl != "reference") else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return ws, rank, local, pg
+
+
+def make_inputs(wl, rank: int, steps: int, seed: int):
+    dims = wl["dims"]
+    image = W.make_db(wl["schema"], dims, seed=seed + 1000 * rank)
+    nb = min(steps, 3)
+    bulks = [W.make_bulk(wl["schema"], dims, wl["n"], seed + 1000 * rank + k, **wl["kw"]) for k in range(nb)]
+    return image, bulks
+
+
+def oracle_rate(wl, image, bulks, min_seconds: float, max_runs: int):
+    """The oracle (serial ts-order executor, one host core) on a bounded sample:
+    successive bulks on the evolving state until min_seconds of loop time."""
+    import oracle
+    cur = image
+    secs, txns, runs = 0.0, 0, 0
+    while runs < max_runs and (secs < min_seconds or runs == 0):
+        b = bulks[runs % len(bulks)]
+        r = oracle.run(wl["schema"], wl["dims"].dims, cur, b, first_ts=txns)
+        cur = r.db
+        secs += r.seconds
+        txns += b.n
+        runs += 1
+    return txns / secs, txns, runs, secs
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, wl, ws, rank):
+    if rank != 0:
+        return 0
+    image, bulks = make_inputs(wl, 0, max(args.steps, 1), args.seed)
+    import oracle
+    cur = image
+    for k in range(args.warmup):
+        cur = oracle.run(wl["schema"], wl["dims"].dims, cur, bulks[k % len(bulks)]).db
+    secs = []
+    txns = 0
+    for k in range(args.steps):
+        b = bulks[k % len(bulks)]
+        r = oracle.run(wl["schema"], wl["dims"].dims, cur, b, first_ts=txns)
+        cur = r.db
+        secs.append(r.seconds)
+        txns += b.n
+    value = txns / sum(secs)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": config_of(args, wl),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} bulks of {wl['n']} txns ({wl['desc']}), serial loop only",
+                         "cpu": cpu_model(), "nproc": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, wl):
+    return {"workload": wl["desc"], "strategy": args.strategy, "bulk": wl["n"], "dims": list(wl["dims"].dims),
+            "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM (value); "
+            "pinned host (e2e)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="tm1", choices=sorted(WORKLOADS))
+    ap.add_argument("--strategy", default="kset", choices=["kset", "part", "tpl"])
+    ap.add_argument("--others", default="part,tpl", help="extra strategies measured on the same bulks")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    ws, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference(args, wl, ws, rank)
+
+    import torch
+    from paper_1103_3105_b200 import Database
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    image, bulks = make_inputs(wl, rank, max(args.steps, 1), args.seed)
+    n = wl["n"]
+    cap = (args.warmup + args.steps) * 4 * n + 16
+    db = Database(wl["schema"], wl["dims"].dims, n, image, device=local, stream=stream.cuda_stream,
+                  insert_capacity=cap)
+    dbulks = [(torch.from_numpy(b.type).to(dev), torch.from_numpy(b.param_off.view(np.int32)).to(dev),
+               torch.from_numpy(b.param_words.view(np.int32)).to(dev)) for b in bulks]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step_dev(k, strategy):
+        t, o, w = dbulks[k % len(dbulks)]
+        db.submit(type=t, param_off=o, param_words=w, on_device=True)
+        return db.execute(strategy)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def timed(strategy, steps, warmup):
+        for k in range(warmup):
+            step_dev(k, strategy)
+        torch.cuda.synchronize()
+        barrier()
+        ms, stats = [], []
+        for k in range(steps):
+            flush.fill_(k & 0xFF)                        # L2 flush, outside the timed window
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            stats.append(step_dev(warmup + k, strategy))
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        barrier()
+        return ms, stats
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- headline strategy, device-resident inputs -----------------------------------
+    with Clocks(local) as clk:
+        ms, stats = timed(args.strategy, args.steps, args.warmup)
+    total_ms = max_over_ranks(sum(ms))
+    value = ws * n * args.steps / (total_ms / 1e3)
+    launches = int(sum(s["launches"] for s in stats))
+
+    # results of the last step for the byte model
+    st_host, _ = db.read_results()
+
+    # ---- e2e through the C ABI with host (pinned) buffers ----------------------------
+    hb = []
+    for b in bulks:
+        pt = torch.from_numpy(b.type).pin_memory().numpy()
+        po = torch.from_numpy(b.param_off.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        pw = torch.from_numpy(b.param_words.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        hb.append((pt, po, pw))
+    st_pin = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+    out_pin = torch.empty(n * db.stride, dtype=torch.uint8).pin_memory().numpy().reshape(n, db.stride)
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        pt, po, pw = hb[k % len(hb)]
+        flush.fill_(k & 0xFF)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        db.submit(type=pt, param_off=po, param_words=pw, on_device=False)
+        db.execute_nostats(args.strategy)
+        db.read_results(st_pin, out_pin)
+        e1.record(stream)
+        e1.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_total = max_over_ranks(sum(e2e_ms))
+    h2d = int(np.mean([a.nbytes + b.nbytes + c.nbytes for a, b, c in hb]))
+    d2h = n + n * db.stride
+
+    # ---- other strategies on the same bulks ------------------------------------------
+    others = {}
+    for s in [x for x in args.others.split(",") if x and x != args.strategy]:
+        m2, s2 = timed(s, max(2, args.steps // 2), 1)
+        tot = max_over_ranks(sum(m2))
+        others[s] = {"value": ws * n * len(m2) / (tot / 1e3), "ms_per_step": tot / len(m2),
+                     "ms_exec": statistics.mean(x["ms_exec"] for x in s2),
+                     "max_chain": s2[-1]["max_chain"], "parts": s2[-1]["parts"]}
+
+    # ---- roofline of the dominant kernel ---------------------------------------------
+    peak, peak_kind = _peaks()
+    phase = {k: statistics.mean(s[k] for s in stats) for k in
+             ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_total")}
+    last = stats[-1]
+    b_last = bulks[(args.warmup + args.steps - 1) % len(bulks)]
+    cand = {}
+    if args.strategy == "kset":
+        cand["kset_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+        cand["rank_kernel"] = (rank_bytes(last["records"], last["rank_passes"], n), phase["ms_rank"])
+    else:
+        cand[f"{args.strategy}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+    kname = max(cand, key=lambda k: cand[k][1])
+    kbytes, kms = cand[kname]
+    achieved = kbytes / (kms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "algorithmic_bytes": kbytes, "kernel_ms": kms,
+                "share_of_step": kms / phase["ms_total"] if phase["ms_total"] else None}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) -----------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, txns, runs, secs = oracle_rate(wl, image, bulks, args.cpu_seconds, 50)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{runs} bulk(s) x {n} txns of the same workload, serial loop {secs:.2f} s",
+               "cpu": cpu_model(), "nproc": os.cpu_count()}
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic (seeded generators, workloads/)",
+        "config": config_of(args, wl),
+        "e2e": {"value": ws * n * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "phases_ms": phase,
+        "graph": {"depth": last["depth"], "zero_set": last["zero_set"], "records": last["records"],
+                  "rank_passes": last["rank_passes"], "committed": last["committed"], "aborted": last["aborted"]},
+        "strategies": {args.strategy: {"value": value, "ms_per_step": total_ms / args.steps}, **others},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    db.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,7 @@ typedef struct {
     uint64_t parts;          /* partitions (PART)                                       */
     uint64_t fragments;      /* executed fragments (PART)                               */
     uint64_t max_chain;      /* longest partition (PART)                                */
+    uint64_t launches;       /* kernels this library launched for the bulk (submit + execute) */
     double ms_emit, ms_sort, ms_rank, ms_group, ms_exec, ms_merge, ms_total;
 } gputx_stats;
 

@@ -17,6 +17,7 @@ import ctypes
 import os
 import subprocess
 import threading
+import time
 
 import numpy as np
 
@@ -126,15 +127,19 @@ def run(schema: int, dims, db: dict, bulk, first_ts: int = 0) -> Result:
     if pw.size == 0:
         pw = np.zeros(1, np.uint32)
     dm = _dims(dims)
+    t0 = time.perf_counter()
     rc = lib.orc_run(schema, _ptr(dm), _ptrs(cols), n, _ptr(tp), _ptr(po), _ptr(pw), first_ts,
                      _ptr(status), _ptr(out), _ptrs(ins_cols), _ptr(nrows))
+    secs = time.perf_counter() - t0
     if rc != 0:
         raise RuntimeError(f"orc_run failed: {rc}")
     inserts = {}
     for k, (tab, cl, arrs) in enumerate(ins_tabs):
         m = int(nrows[k])
         inserts[tab] = {name: a[:m].copy() for (name, _), a in zip(cl, arrs)}
-    return Result(work, status, out, inserts)
+    r = Result(work, status, out, inserts)
+    r.seconds = secs          # time of the serial loop alone (one host core)
+    return r
 
 
 def footprint(schema: int, dims, db: dict, bulk):

@@ -152,6 +152,7 @@ struct gputx_db {
     uint32_t exec_block = 256, exec_grid_override = 0, narrow_max = 256;
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
+    uint64_t launches = 0;     // kernels launched since the last submit
 };
 
 namespace {
@@ -202,6 +203,7 @@ void scan_u32(gputx_db* db, const uint32_t* in, uint32_t* out, const uint32_t* n
     ++db->epoch;
     scan_kernel<<<grid, SC_THREADS, 0, db->stream>>>(in, out, n_dev, (uint32_t)n_max, db->lb_scan, db->epoch,
                                                      next_ticket(db), total);
+                                                     ++db->launches;
 }
 
 DevDb make_devdb(gputx_db* db) {
@@ -260,13 +262,16 @@ template <int S>
 gputx_status emit_records(gputx_db* db, const DevDb& v) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     emit_count_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_cnt);
+    ++db->launches;
     scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NREC);
     emit_write_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_rec_off, db->d_rec_a);
+    ++db->launches;
     return GPUTX_OK;
 }
 
 gputx_status sort_records(gputx_db* db, uint32_t lo, uint32_t nbits, const uint32_t* n_dev, uint64_t n_max) {
     db->d_sorted = radix_sort_u64(db->d_rec_a, db->d_rec_b, n_dev, n_max, lo, nbits, db->sort_ws, db->epoch, db->stream);
+    db->launches += 2 + (nbits + 7) / 8;
     return GPUTX_OK;
 }
 
@@ -291,17 +296,23 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         uint32_t maxp = 1u << 20;
         void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp};
         TRY(launch_coop(db, (const void*)rank_kernel, db->rank_grid, RK_THREADS, args));
+        ++db->launches;
     }
     cudaEventRecord(db->ev[4], s);
     // group by (depth, type)
     const uint32_t T = db->ntypes;
     const uint32_t g = grid_for(db->n, 256, 148 * 8);
     depth_reduce_kernel<<<g, 256, 0, s>>>(db->d_D, (uint32_t)db->n, db->d_sc);
+    ++db->launches;
     group_nkeys_kernel<<<1, 1, 0, s>>>(db->d_sc, T);
+    ++db->launches;
     zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
+    ++db->launches;
     group_hist_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt);
+    ++db->launches;
     scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
     group_scatter_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff, db->d_perm);
+    ++db->launches;
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
@@ -316,6 +327,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         const void* fn = (const void*)kset_exec_kernel<S>;
         int grid = db->exec_grid_override ? (int)db->exec_grid_override : db->kset_grid;
         TRY(launch_coop(db, fn, grid, 256, args));
+        ++db->launches;
     }
     cudaEventRecord(db->ev[6], s);
     db->has_depth = db->has_perm = true;
@@ -329,17 +341,21 @@ gputx_status run_part(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[1], s);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     frag_count_kernel<S><<<g, 256, 0, s>>>(v, db->d_cnt);
+    ++db->launches;
     scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NFRAG);
     frag_emit_kernel<S><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a);
+    ++db->launches;
     cudaEventRecord(db->ev[2], s);
     TRY(sort_records(db, 32, db->part_bits, db->d_sc + SC_NFRAG, db->max_rec));
     cudaEventRecord(db->ev[3], s);
     part_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NFRAG,
                                                                                db->nparts, db->d_part_off);
+                                                                               ++db->launches;
     cudaEventRecord(db->ev[4], s);
     cudaEventRecord(db->ev[5], s);
     const uint32_t pb = 128;
     part_exec_kernel<S><<<(db->nparts + pb - 1) / pb, pb, 0, s>>>(v, db->d_sorted, db->d_part_off, db->nparts, db->d_sc);
+    ++db->launches;
     cudaEventRecord(db->ev[6], s);
     return GPUTX_OK;
 }
@@ -356,10 +372,12 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v) {
     ++db->epoch;
     tpl_keys_kernel<<<(uint32_t)((db->max_rec + RK_TILE - 1) / RK_TILE) + 1, RK_THREADS, 0, s>>>(
         db->d_sorted, db->d_sc + SC_NREC, db->d_rec_off, db->d_lkey, db->d_lock, db->lb_tpl, db->epoch, next_ticket(db));
+        ++db->launches;
     cudaEventRecord(db->ev[4], s);
     cudaEventRecord(db->ev[5], s);
     const uint32_t tb = 128;
     tpl_exec_kernel<S><<<(uint32_t)((db->n + tb - 1) / tb), tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+    ++db->launches;
     cudaEventRecord(db->ev[6], s);
     return GPUTX_OK;
 }
@@ -378,6 +396,7 @@ void launch_ingest(gputx_db* db, uint32_t n_words) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, db->type_mask, db->d_ins_off,
                                                 (uint32_t)(db->n + 1), db->d_sc);
+                                                ++db->launches;
 }
 
 Col* find_col(gputx_db* db, const char* name) {
@@ -647,6 +666,7 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     if (db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
     db->n = n;
+    db->launches = 0;
     db->has_depth = db->has_perm = false;
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
     CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
@@ -723,6 +743,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     if (stats) {
         memset(stats, 0, sizeof(*stats));
         stats->n = n;
+        stats->launches = db->launches;
         stats->records = st == GPUTX_PART ? 0 : db->h_sc[SC_NREC];
         stats->fragments = st == GPUTX_PART ? db->h_sc[SC_NFRAG] : 0;
         if (st == GPUTX_KSET && n) {

@@ -41,7 +41,7 @@ class BulkC(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in ("n", "committed", "aborted", "depth", "ksets", "zero_set", "records",
-                                               "rank_passes", "parts", "fragments", "max_chain")] + \
+                                               "rank_passes", "parts", "fragments", "max_chain", "launches")] + \
                [(k, ctypes.c_double) for k in ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_merge",
                                                "ms_total")]
 

@@ -272,7 +272,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     image, bulks = make_inputs(wl, rank, max(args.steps, 1), args.seed)
     n = wl["n"]
-    cap = (args.warmup + args.steps) * 4 * n + 16
+    cap = 3 * (args.warmup + args.steps) + 8          # bulks the merged insert tables must hold
     db = Database(wl["schema"], wl["dims"].dims, n, image, device=local, stream=stream.cuda_stream,
                   insert_capacity=cap)
     dbulks = [(torch.from_numpy(b.type).to(dev), torch.from_numpy(b.param_off.view(np.int32)).to(dev),

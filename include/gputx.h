@@ -80,7 +80,7 @@ typedef struct {
                                  TM-1 : subscribers P, 0, 0, 0
                                  TPC-C: warehouses W, districts/W D, customers/district C, items I */
     uint64_t max_bulk;        /* transactions per bulk, <= 1<<24 (timestamp field width)            */
-    uint64_t insert_capacity; /* rows per merged insert table; 0 => 8 * max_bulk                    */
+    uint64_t insert_capacity; /* merged insert tables hold this many full bulks; 0 => 8            */
     uint32_t part_size;       /* PART: TM-1 subscribers per partition; 0 => 128     */
     int device;               /* CUDA device ordinal                                                */
     void* stream;             /* cudaStream_t to order all work on; NULL => a library-owned stream  */
@@ -179,7 +179,8 @@ gputx_status gputx_reset(gputx_db* db);
 void gputx_close_db(gputx_db* db);
 const char* gputx_last_error(const gputx_db* db);
 
-/* Launch-shape overrides for tests of grid-shape independence (0 = default). */
+/* Launch-shape overrides for tests of grid-shape independence (0 = default):
+ * exec_grid = CTAs of the persistent K-SET executor (<= co-resident); others reserved. */
 gputx_status gputx_set_launch(gputx_db* db, uint32_t exec_block, uint32_t exec_grid,
                               uint32_t narrow_max);
 

@@ -52,24 +52,41 @@ DEV uint32_t atom_add_release(uint32_t* p, uint32_t v) {
 // Grid barrier for a cooperative launch (all CTAs co-resident).  gen is bumped by
 // the last arriver; waiters poll it with acquire loads.
 // ---------------------------------------------------------------------------------
+// Two-level arrival tree: CTA b arrives on sub-counter b % GB_SUB (each on its own
+// 128-B line), the last arriver of a sub-counter arrives on the top counter, the last
+// top arriver bumps gen.  Same-address atomics per level: <= gridDim/GB_SUB.
+constexpr uint32_t GB_SUB = 16;
 struct GridBar {
-    uint32_t count;
+    uint32_t sub[GB_SUB * 32];
+    uint32_t top;
+    uint32_t pad[31];
     uint32_t gen;
 };
 
 DEV void grid_sync(GridBar* b) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
-        uint32_t g = ld_acquire(&b->gen);
+        const uint32_t nb = gridDim.x;
+        const uint32_t g = ld_acquire(&b->gen);
+        const uint32_t s = blockIdx.x % GB_SUB;
+        const uint32_t nsub = nb < GB_SUB ? nb : GB_SUB;
+        const uint32_t members = (nb - s + GB_SUB - 1) / GB_SUB;
         __threadfence();
-        uint32_t arrived = atomicAdd(&b->count, 1u);
-        if (arrived == nb - 1) {
-            b->count = 0;
-            st_release(&b->gen, g + 1);
-        } else {
-            while (ld_acquire(&b->gen) == g) { }
+        const uint32_t a = atomicAdd(&b->sub[s * 32], 1u);
+        bool wait = true;
+        if (a == members - 1) {
+            b->sub[s * 32] = 0;
+            __threadfence();
+            const uint32_t t = atomicAdd(&b->top, 1u);
+            if (t == nsub - 1) {
+                b->top = 0;
+                __threadfence();
+                st_release(&b->gen, g + 1);
+                wait = false;
+            }
         }
+        if (wait)
+            while (ld_acquire(&b->gen) == g) { }
         __threadfence();
     }
     __syncthreads();

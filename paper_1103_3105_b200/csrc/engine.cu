@@ -136,6 +136,8 @@ struct gputx_db {
     uint32_t* d_lock = nullptr;
     uint32_t* d_lkey = nullptr;
     uint32_t* d_part_off = nullptr;
+    uint16_t* d_g = nullptr;         // CTAs per k-set round
+    uint32_t* d_done = nullptr;      // per-round completion counters
     uint32_t* d_sc = nullptr;
     uint32_t* h_sc = nullptr;        // pinned mirror
     GridBar* d_bar = nullptr;
@@ -149,7 +151,7 @@ struct gputx_db {
     uint32_t ticket_slot = 0;
     int nsm = 0;
     int rank_grid = 0, kset_grid = 0;
-    uint32_t exec_block = 256, exec_grid_override = 0, narrow_max = 256;
+    uint32_t exec_grid_override = 0;
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
     uint64_t launches = 0;     // kernels launched since the last submit
@@ -258,6 +260,9 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 }
 
 // ------------------------------------------------------------------------------- K-SET
+// parameter words staged in registers by the K-SET executor (0: read from HBM)
+template <int S> constexpr int kset_pw() { return S == S_TPCB ? 4 : S == S_TM1 ? 8 : 0; }
+template <int S> const void* kset_fn() { return (const void*)kset_exec_kernel<S, kset_pw<S>()>; }
 template <int S>
 gputx_status emit_records(gputx_db* db, const DevDb& v) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
@@ -308,25 +313,29 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     ++db->launches;
     zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
     ++db->launches;
-    group_hist_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt);
+    const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
+    group_kernel<0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, nullptr, nullptr);
     ++db->launches;
     scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
-    group_scatter_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff, db->d_perm);
+    ++db->launches;
+    group_kernel<1><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff, db->d_perm);
     ++db->launches;
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
+        const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
+        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, KX_THREADS,
+                                                                         db->d_g, db->d_done);
+        ++db->launches;
         DevDb vv = v;
         const uint32_t* perm = db->d_perm;
         const uint32_t* off = db->d_goff;
-        GridBar* bar = db->d_bar;
-        uint32_t* sc = db->d_sc;
-        uint32_t nm = db->narrow_max;
+        const uint16_t* gk = db->d_g;
+        uint32_t* done = db->d_done;
+        const uint32_t* sc = db->d_sc;
         uint32_t TT = T;
-        void* args[] = {&vv, &perm, &off, &TT, &bar, &sc, &nm};
-        const void* fn = (const void*)kset_exec_kernel<S>;
-        int grid = db->exec_grid_override ? (int)db->exec_grid_override : db->kset_grid;
-        TRY(launch_coop(db, fn, grid, 256, args));
+        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc};
+        TRY(launch_coop(db, kset_fn<S>(), (int)G, KX_THREADS, args));
         ++db->launches;
     }
     cudaEventRecord(db->ev[6], s);
@@ -483,7 +492,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         t.name = is.table;
         t.table_id = is.table_id;
         t.per_txn = is.per_txn;
-        t.cap = cfg->insert_capacity ? cfg->insert_capacity : 8 * db->max_bulk * is.per_txn;
+        t.cap = (cfg->insert_capacity ? cfg->insert_capacity : 8) * db->max_bulk * is.per_txn;
         for (auto* cn : is.cols) {
             InsCol ic;
             ic.name = cn;
@@ -495,11 +504,12 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     const uint64_t NB = db->max_bulk;
     const uint64_t cntn = std::max(NB, db->max_rec) + 2;
     if ((st = dalloc(db, &db->d_type, NB)) || (st = dalloc(db, &db->d_poff, NB + 1)) ||
-        (st = dalloc(db, &db->d_pw, db->max_words)) || (st = dalloc(db, &db->d_status, NB)) ||
+        (st = dalloc(db, &db->d_pw, db->max_words + 16)) || (st = dalloc(db, &db->d_status, NB)) ||
         (st = dalloc(db, &db->d_out, NB * db->out_stride)) || (st = dalloc(db, &db->d_ins_off, 4 * (NB + 1))) ||
         (st = dalloc(db, &db->d_rec_a, db->max_rec)) || (st = dalloc(db, &db->d_rec_b, db->max_rec)) ||
         (st = dalloc(db, &db->d_cnt, cntn)) || (st = dalloc(db, &db->d_rec_off, NB + 2)) ||
         (st = dalloc(db, &db->d_D, NB)) || (st = dalloc(db, &db->d_perm, NB)) ||
+        (st = dalloc(db, &db->d_g, NB + 1)) || (st = dalloc(db, &db->d_done, NB + 1)) ||
         (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
@@ -529,9 +539,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
     int kg = 0;
-    if (schema == S_TPCB) kg = coop_grid(db, kset_exec_kernel<S_TPCB>, 256, 0);
-    else if (schema == S_TM1) kg = coop_grid(db, kset_exec_kernel<S_TM1>, 256, 0);
-    else kg = coop_grid(db, kset_exec_kernel<S_TPCC>, 256, 0);
+    if (schema == S_TPCB) kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>()>, KX_THREADS, 0);
+    else if (schema == S_TM1) kg = coop_grid(db, kset_exec_kernel<S_TM1, kset_pw<S_TM1>()>, KX_THREADS, 0);
+    else kg = coop_grid(db, kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>()>, KX_THREADS, 0);
     db->kset_grid = kg;
     if (cudaStreamSynchronize(db->stream) != cudaSuccess) return bail(GPUTX_ECUDA);
     *out = db;
@@ -864,8 +874,8 @@ gputx_status gputx_set_launch(gputx_db* db, uint32_t exec_block, uint32_t exec_g
     if (!db) return GPUTX_EINVAL;
     if (exec_grid && (int)exec_grid > db->kset_grid) return fail(db, GPUTX_EINVAL, "grid exceeds co-resident CTAs");
     (void)exec_block;
+    (void)narrow_max;
     db->exec_grid_override = exec_grid;
-    if (narrow_max) db->narrow_max = narrow_max;
     return GPUTX_OK;
 }
 
@@ -877,7 +887,7 @@ void gputx_close_db(gputx_db* db) {
         for (auto& c : t.cols) cudaFree(c.d);
     void* ps[] = {db->d_type, db->d_poff, db->d_pw, db->d_status, db->d_out, db->d_ins_off, db->d_hkeys, db->d_hvals,
                   db->d_name_sorted, db->d_name_off, db->d_rec_a, db->d_rec_b, db->d_cnt, db->d_rec_off, db->d_D,
-                  db->d_perm, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
+                  db->d_perm, db->d_g, db->d_done, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
                   db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
                   db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
                   db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets};

@@ -214,7 +214,14 @@ DEV Xf rec_xf(bool head, uint32_t w, int d) {
 }
 
 constexpr int RK_THREADS = 256, RK_ITEMS = 8, RK_TILE = RK_THREADS * RK_ITEMS;
+constexpr int RK_LOCAL_MAX = 32;     // in-tile Gauss-Seidel sweeps per pass
 
+// One pass over the sorted records.  A tile first publishes its map aggregate and
+// gets the prefix entering it by decoupled look-back; then it re-sweeps itself with
+// the D values it just raised until nothing changes on chip (items of one root key
+// are adjacent, so most chains close inside a tile).  Every L computed is a lower
+// bound of the true depth, so chaotic/in-tile updates reach the same fixpoint; a
+// pass that raises nothing proves it.
 __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes) {
@@ -237,51 +244,59 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
                 stage[i] = (tb + i < nrec) ? __ldg(&keys[tb + i]) : ~0ull;
             if (tid == 0) s_prev = tb ? __ldg(&keys[tb - 1]) : ~0ull;
             __syncthreads();
-            int dv[RK_ITEMS];
-            uint32_t hw = 0;                   // bit 2k: head, bit 2k+1: write
-            Xf agg = OpXf::identity();
+            uint32_t hw = 0;                   // bit 2k: head, bit 2k+1: write, bit 16+k: valid
 #pragma unroll
             for (int k = 0; k < RK_ITEMS; ++k) {
                 const uint32_t pos = tid * RK_ITEMS + k;
-                const uint64_t key = stage[pos];
-                dv[k] = 0;
                 if (tb + pos < nrec) {
+                    const uint64_t key = stage[pos];
                     const uint64_t prev = pos ? stage[pos - 1] : s_prev;
                     const bool head = (tb + pos == 0) || key_item(prev) != key_item(key);
-                    const uint32_t w = key_w(key);
-                    const int d = (int)__ldcg(&D[key_idx(key)]);
-                    dv[k] = d;
                     hw |= (head ? 1u : 0u) << (2 * k);
-                    hw |= w << (2 * k + 1);
-                    agg = OpXf::combine(agg, rec_xf(head, w, d));
+                    hw |= key_w(key) << (2 * k + 1);
+                    hw |= 1u << (16 + k);
                 }
             }
-            Xf tot;
-            Xf ex = block_scan_excl<Xf, OpXf>(agg, tot, sm);
-            if (warp_id() == 0) {
-                Xf pre = lookback_warp<Xf, OpXf>(lb, tile, epoch, tot);
-                if (lane_id() == 0) s_pre = pre;
-            }
-            __syncthreads();
-            Xf cur = OpXf::combine(s_pre, ex);
-            bool chg = false;
+            for (int it = 0; it < RK_LOCAL_MAX; ++it) {
+                int dv[RK_ITEMS];
+                Xf agg = OpXf::identity();
 #pragma unroll
-            for (int k = 0; k < RK_ITEMS; ++k) {
-                const uint32_t pos = tid * RK_ITEMS + k;
-                if (tb + pos < nrec) {
-                    const bool head = (hw >> (2 * k)) & 1u;
-                    const uint32_t w = (hw >> (2 * k + 1)) & 1u;
-                    const int d = dv[k];
-                    const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
-                    const int L = w ? max(d, m + 1) : max(d, a + 1);
-                    if (L > d) {
-                        const uint32_t old = atomicMax(&D[key_idx(stage[pos])], (uint32_t)L);
-                        chg |= old < (uint32_t)L;
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    dv[k] = 0;
+                    if ((hw >> (16 + k)) & 1u) {
+                        dv[k] = (int)__ldcg(&D[key_idx(stage[tid * RK_ITEMS + k])]);
+                        agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
                     }
-                    cur = OpXf::combine(cur, rec_xf(head, w, d));
                 }
+                Xf tot;
+                Xf ex = block_scan_excl<Xf, OpXf>(agg, tot, sm);
+                if (it == 0) {
+                    if (warp_id() == 0) {
+                        Xf pre = lookback_warp<Xf, OpXf>(lb, tile, epoch, tot);
+                        if (lane_id() == 0) s_pre = pre;
+                    }
+                    __syncthreads();
+                }
+                Xf cur = OpXf::combine(s_pre, ex);
+                bool chg = false;
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    if ((hw >> (16 + k)) & 1u) {
+                        const bool head = (hw >> (2 * k)) & 1u;
+                        const uint32_t w = (hw >> (2 * k + 1)) & 1u;
+                        const int d = dv[k];
+                        const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
+                        const int L = w ? max(d, m + 1) : max(d, a + 1);
+                        if (L > d) {
+                            const uint32_t old = atomicMax(&D[key_idx(stage[tid * RK_ITEMS + k])], (uint32_t)L);
+                            chg |= old < (uint32_t)L;
+                        }
+                        cur = OpXf::combine(cur, rec_xf(head, w, d));
+                    }
+                }
+                if (!__syncthreads_or(chg)) break;
+                if (tid == 0) s_chg = 1;
             }
-            if (chg) s_chg = 1;
         }
         __syncthreads();
         if (tid == 0 && s_chg) sc[SC_CHG0 + pass % 3] = 1;
@@ -298,7 +313,9 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
 }
 
 // =====================================================================================
-// group by (depth, type)
+// group by (depth, type): counting sort.  Each CTA first aggregates its tile's keys in
+// a shared-memory table (open addressing) so hot keys (the 0-set of a wide graph) cost
+// one global atomic per CTA instead of one per warp; keys that do not fit go global.
 // =====================================================================================
 __global__ void __launch_bounds__(256) depth_reduce_kernel(const uint32_t* D, uint32_t n, uint32_t* sc) {
     uint32_t mx = 0, z = 0;
@@ -328,67 +345,165 @@ __global__ void __launch_bounds__(256) zero_dev_kernel(uint32_t* a, const uint32
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = 0;
 }
 
-__global__ void __launch_bounds__(256) group_hist_kernel(const uint32_t* D, const uint8_t* type, uint32_t n, uint32_t T,
-                                                         uint32_t* cnt) {
-    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
-        const uint32_t i = i0 + threadIdx.x;
-        const uint32_t key = i < n ? D[i] * T + type[i] : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        if (key != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&cnt[key], __popc(peers));
+constexpr int GR_ITEMS = 16, GR_TILE = 256 * GR_ITEMS, GR_SLOTS = 1024, GR_PROBE = 8;
+constexpr uint32_t GR_EMPTY = 0xFFFFFFFFu;
+
+// insert key into the smem table, returns slot or -1
+DEV int gr_slot(uint32_t* skey, uint32_t key) {
+    uint32_t h = (key * 0x9E3779B1u) >> 22;            // 10 bits
+    for (int p = 0; p < GR_PROBE; ++p) {
+        const uint32_t s = (h + p) & (GR_SLOTS - 1);
+        const uint32_t old = atomicCAS(&skey[s], GR_EMPTY, key);
+        if (old == GR_EMPTY || old == key) return (int)s;
     }
+    return -1;
 }
 
-__global__ void __launch_bounds__(256) group_scatter_kernel(const uint32_t* D, const uint8_t* type, uint32_t n, uint32_t T,
-                                                            uint32_t* cnt, const uint32_t* off, uint32_t* perm) {
-    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
-        const uint32_t i = i0 + threadIdx.x;
-        const uint32_t key = i < n ? D[i] * T + type[i] : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, key);
-        const int leader = __ffs(peers) - 1;
-        const uint32_t c = __popc(peers);
-        uint32_t old = 0;
-        if (key != 0xFFFFFFFFu && (int)lane_id() == leader) old = atomicSub(&cnt[key], c);
-        old = __shfl_sync(0xffffffffu, old, leader);
-        if (key != 0xFFFFFFFFu) perm[off[key] + old - c + __popc(peers & lanemask_lt())] = i;
-    }
-}
-
-// =====================================================================================
-// K-SET executor: persistent, one round per k-set (Property 1: no locks).  A run of
-// narrow k-sets (<= narrow_max) executes inside CTA 0 separated by __syncthreads;
-// wide k-sets are spread over the grid, separated by a grid barrier.
-// =====================================================================================
-template <int S>
-__global__ void __launch_bounds__(256) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
-                                                        const uint32_t* __restrict__ off, uint32_t T, GridBar* bar,
-                                                        uint32_t* sc, uint32_t narrow_max) {
-    const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t gstride = gridDim.x * blockDim.x;
-    uint32_t k = 0;
-    while (k < nk) {
-        uint32_t lo = __ldcg(&off[k * T]), hi = __ldcg(&off[(k + 1) * T]);
-        if (hi - lo <= narrow_max) {
-            if (blockIdx.x == 0) {
-                while (true) {
-                    for (uint32_t j = lo + tid; j < hi; j += blockDim.x) exec_txn<S>(db, __ldg(&perm[j]));
-                    __syncthreads();
-                    ++k;
-                    if (k >= nk) break;
-                    lo = hi;
-                    hi = __ldcg(&off[(k + 1) * T]);
-                    if (hi - lo > narrow_max) break;
-                }
-                if (tid == 0) sc[SC_KNEXT] = k;
+// mode 0: histogram into cnt[]; mode 1: scatter perm[] (cnt[] counts down)
+template <int MODE>
+__global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__ D, const uint8_t* __restrict__ type,
+                                                    uint32_t n, uint32_t T, uint32_t* cnt, const uint32_t* off,
+                                                    uint32_t* perm) {
+    __shared__ uint32_t skey[GR_SLOTS];
+    __shared__ uint32_t scnt[GR_SLOTS];
+    __shared__ uint32_t sbase[GR_SLOTS];
+    for (uint64_t t0 = (uint64_t)blockIdx.x * GR_TILE; t0 < n; t0 += (uint64_t)gridDim.x * GR_TILE) {
+        for (int s = threadIdx.x; s < GR_SLOTS; s += 256) { skey[s] = GR_EMPTY; scnt[s] = 0; }
+        __syncthreads();
+        uint32_t key[GR_ITEMS];
+        int slot[GR_ITEMS];
+        uint32_t rank[GR_ITEMS];
+#pragma unroll
+        for (int k = 0; k < GR_ITEMS; ++k) {
+            const uint64_t i = t0 + k * 256 + threadIdx.x;
+            key[k] = i < n ? D[i] * T + type[i] : GR_EMPTY;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key[k]);
+            const int leader = __ffs(peers) - 1;
+            int sl = -1;
+            uint32_t old = 0;
+            if (key[k] != GR_EMPTY && (int)lane_id() == leader) {
+                sl = gr_slot(skey, key[k]);
+                if (sl >= 0) old = atomicAdd(&scnt[sl], __popc(peers));
+                else if (MODE == 0) atomicAdd(&cnt[key[k]], __popc(peers));
+                else old = atomicSub(&cnt[key[k]], __popc(peers)) - __popc(peers);   // global slot range
             }
-            grid_sync(bar);
-            k = __ldcg(&sc[SC_KNEXT]);
-            grid_sync(bar);                    // everyone has read KNEXT before it can change
-        } else {
-            for (uint32_t j = lo + blockIdx.x * blockDim.x + tid; j < hi; j += gstride) exec_txn<S>(db, __ldg(&perm[j]));
-            grid_sync(bar);
-            ++k;
+            sl = __shfl_sync(0xffffffffu, sl, leader);
+            old = __shfl_sync(0xffffffffu, old, leader);
+            slot[k] = sl;
+            rank[k] = old + __popc(peers & lanemask_lt());
         }
+        __syncthreads();
+        for (int s = threadIdx.x; s < GR_SLOTS; s += 256) {
+            if (skey[s] != GR_EMPTY) {
+                if (MODE == 0) atomicAdd(&cnt[skey[s]], scnt[s]);
+                else sbase[s] = atomicSub(&cnt[skey[s]], scnt[s]) - scnt[s];
+            }
+        }
+        __syncthreads();
+        if (MODE == 1) {
+#pragma unroll
+            for (int k = 0; k < GR_ITEMS; ++k) {
+                if (key[k] == GR_EMPTY) continue;
+                const uint32_t i = (uint32_t)(t0 + k * 256 + threadIdx.x);
+                const uint32_t pos = off[key[k]] + (slot[k] >= 0 ? sbase[slot[k]] + rank[k] : rank[k]);
+                perm[pos] = i;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// =====================================================================================
+// K-SET executor.  Round k (k-set k) needs g[k] = ceil(|k-set| / B)
+// CTAs (<= grid).  The g[k] participants of round k wait until all g[k-1] participants
+// of round k-1 have signalled done[k-1]; no grid-wide barrier.  Consecutive rounds
+// that fit one CTA run in CTA 0 separated by __syncthreads only.  Property 1: no
+// locks inside a round.  For PW > 0 the next round's transaction ids and parameter
+// words are loaded into registers before the current round executes.
+// =====================================================================================
+__global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, const uint32_t* sc, uint32_t G,
+                                  uint32_t per_cta, uint16_t* g, uint32_t* done) {
+    const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x) {
+        const uint32_t s = off[(k + 1) * T] - off[k * T];
+        uint32_t c = (s + per_cta - 1) / per_cta;
+        g[k] = (uint16_t)(c < 1 ? 1 : (c > G ? G : c));
+        done[k] = 0;
+    }
+}
+
+constexpr int KX_THREADS = 1024;
+
+template <int S, int PW>
+__global__ void __launch_bounds__(KX_THREADS) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
+                                                               const uint32_t* __restrict__ off, uint32_t T,
+                                                               const uint16_t* __restrict__ g, uint32_t* done,
+                                                               const uint32_t* sc) {
+    const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
+    const uint32_t b = blockIdx.x, tid = threadIdx.x;
+    // prefetched first slice of the round this CTA executes next
+    uint32_t nidx = 0xFFFFFFFFu, nt = 0;
+    uint32_t np[PW > 0 ? PW : 1];
+    auto prefetch = [&](uint32_t lo, uint32_t hi) {
+        const uint32_t j = lo + b * KX_THREADS + tid;
+        nidx = 0xFFFFFFFFu;
+        if (j < hi) {
+            nidx = __ldg(&perm[j]);
+            nt = db.type[nidx];
+            if (PW > 0) {
+                const uint32_t* p = db.pw + db.poff[nidx];
+#pragma unroll
+                for (int w = 0; w < (PW > 0 ? PW : 1); ++w) np[w] = p[w];
+            }
+        }
+    };
+    uint32_t k = 0;
+    // find this CTA's first round
+    while (k < nk && __ldg(&g[k]) <= b) ++k;
+    if (k >= nk) return;
+    uint32_t lo = __ldcg(&off[k * T]), hi = __ldcg(&off[(k + 1) * T]);
+    prefetch(lo, hi);
+    uint32_t prev = 0xFFFFFFFFu;            // last round this CTA executed
+    while (k < nk) {
+        const uint32_t gk = __ldg(&g[k]);
+        // wait for round k-1
+        if (k > 0) {
+            const bool mine = (prev == k - 1) && __ldg(&g[k - 1]) == 1;
+            if (!mine) {
+                if (tid == 0) {
+                    const uint32_t need = __ldg(&g[k - 1]);
+                    while (ld_acquire(&done[k - 1]) < need) { }
+                }
+                __syncthreads();
+            }
+        }
+        // take the prefetched slice, then prefetch this CTA's next round
+        const uint32_t cidx = nidx, ct = nt;
+        uint32_t cp[PW > 0 ? PW : 1];
+#pragma unroll
+        for (int w = 0; w < (PW > 0 ? PW : 1); ++w) cp[w] = np[w];
+        const uint32_t clo = lo, chi = hi;
+        uint32_t k2 = k + 1;
+        while (k2 < nk && __ldg(&g[k2]) <= b) ++k2;
+        if (k2 < nk) {
+            lo = __ldcg(&off[k2 * T]);
+            hi = __ldcg(&off[(k2 + 1) * T]);
+            prefetch(lo, hi);
+        }
+        if (cidx != 0xFFFFFFFFu) {
+            if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
+            else exec_txn<S>(db, cidx);
+        }
+        for (uint32_t j = clo + (b + gk) * KX_THREADS + tid; j < chi; j += gk * KX_THREADS)
+            exec_txn<S>(db, __ldg(&perm[j]));
+        __syncthreads();
+        const bool next_shared = (k + 1 < nk) && __ldg(&g[k + 1]) > 1;
+        if (tid == 0 && (gk > 1 || next_shared || b > 0)) {
+            __threadfence();
+            atomicAdd(&done[k], 1u);
+        }
+        prev = k;
+        k = k2;
     }
 }
 

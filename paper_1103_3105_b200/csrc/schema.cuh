@@ -97,51 +97,57 @@ DEV int add_rec(Rec* r, int k, uint64_t item, uint32_t w) {
     return k + 1;
 }
 
+// Item ids are partition-major (subscriber / branch / warehouse): all items of one
+// root key are adjacent, so the conflict groups a transaction touches sit in the same
+// sorted tile and the rank kernel's in-tile iteration resolves their chains on chip.
+//   TM-1 : s*18 + {0 BIT1, 1 VLR, 2+sf-1 SFDA, 6+(sf-1)*3+st/8 CF}
+//   TPC-B: b*(1+T+A) + {0 BR, 1+t TEL, 1+T+a ACC}
+//   TPC-C: w*(2D+1+DC+I) + {d DNEXT, D WYTD, D+1+d DYTD, 2D+1+d*C+c CUST, 2D+1+DC+i STOCK}
 // Basic operations of one (ingested) transaction.  Returns the count (<= MAX_REC).
 template <int S>
 DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
     int k = 0;
     if (S == S_TPCB) {
-        const uint64_t BA = (uint64_t)db.dims[0] * db.dims[2], BT = (uint64_t)db.dims[0] * db.dims[1];
-        r[0] = {p[0], 1u};
-        r[1] = {BA + p[1], 1u};
-        r[2] = {BA + BT + p[2], 1u};
+        const uint32_t T = db.dims[1], A = db.dims[2];
+        const uint64_t sb = 1ull + T + A;
+        r[0] = {(uint64_t)(p[0] / A) * sb + 1 + T + p[0] % A, 1u};
+        r[1] = {(uint64_t)(p[1] / T) * sb + 1 + p[1] % T, 1u};
+        r[2] = {(uint64_t)p[2] * sb, 1u};
         return 3;
     } else if (S == S_TM1) {
-        const uint64_t P = db.dims[0];
         switch (t) {
-        case 0: { uint64_t s = p[0] - 1; r[0] = {s, 0u}; r[1] = {P + s, 0u}; return 2; }
+        case 0: { uint64_t s = (uint64_t)(p[0] - 1) * 18; r[0] = {s, 0u}; r[1] = {s + 1, 0u}; return 2; }
         case 1: {
-            uint64_t c = (((uint64_t)(p[0] - 1)) * 4 + (p[1] - 1)) * 3;
-            r[0] = {6 * P + c, 0u}; r[1] = {6 * P + c + 1, 0u}; r[2] = {6 * P + c + 2, 0u};
+            uint64_t c = (uint64_t)(p[0] - 1) * 18 + 6 + (p[1] - 1) * 3;
+            r[0] = {c, 0u}; r[1] = {c + 1, 0u}; r[2] = {c + 2, 0u};
             return 3;
         }
         case 2: return 0;
-        case 3: { uint64_t s = p[0] - 1; r[0] = {s, 1u}; r[1] = {2 * P + s * 4 + (p[1] - 1), 1u}; return 2; }
-        case 4: if (p[0] == 0) return 0; r[0] = {P + (p[0] - 1), 1u}; return 1;
+        case 3: { uint64_t s = (uint64_t)(p[0] - 1) * 18; r[0] = {s, 1u}; r[1] = {s + 2 + (p[1] - 1), 1u}; return 2; }
+        case 4: if (p[0] == 0) return 0; r[0] = {(uint64_t)(p[0] - 1) * 18 + 1, 1u}; return 1;
         case 5: case 6:
             if (p[0] == 0) return 0;
-            r[0] = {6 * P + (((uint64_t)(p[0] - 1)) * 4 + (p[2] - 1)) * 3 + p[3] / 8, 1u};
+            r[0] = {(uint64_t)(p[0] - 1) * 18 + 6 + (p[2] - 1) * 3 + p[3] / 8, 1u};
             return 1;
         }
         return 0;
     } else {
-        const uint64_t W = db.dims[0], D = db.dims[1], C = db.dims[2], I = db.dims[3];
-        const uint64_t WD = W * D, base_c = 2 * WD + W, base_s = base_c + WD * C;
+        const uint64_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
+        const uint64_t sw_ = 2 * D + 1 + D * C + I;
         if (t == 0) {
-            k = add_rec(r, k, (uint64_t)p[0] * D + p[1], 1u);
+            k = add_rec(r, k, (uint64_t)p[0] * sw_ + p[1], 1u);
             const uint32_t cnt = p[3];
             for (uint32_t l = 0; l < cnt; ++l) {
                 uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l];
                 if (i >= I) continue;
-                k = add_rec(r, k, base_s + (uint64_t)sw * I + i, 1u);
+                k = add_rec(r, k, (uint64_t)sw * sw_ + 2 * D + 1 + D * C + i, 1u);
             }
             return k;
         }
-        r[0] = {WD + p[0], 1u};
-        r[1] = {WD + W + (uint64_t)p[0] * D + p[1], 1u};
+        r[0] = {(uint64_t)p[0] * sw_ + D, 1u};
+        r[1] = {(uint64_t)p[0] * sw_ + D + 1 + p[1], 1u};
         if (p[4] == 2) return 2;                           // by-name lookup found nobody
-        r[2] = {base_c + ((uint64_t)p[2] * D + p[3]) * C + p[5], 1u};
+        r[2] = {(uint64_t)p[2] * sw_ + 2 * D + 1 + (uint64_t)p[3] * C + p[5], 1u};
         return 3;
     }
 }
@@ -357,9 +363,7 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
 
 // The combined kernel body: one whole transaction (K-SET, TPL).
 template <int S>
-DEV void exec_txn(const DevDb& db, uint32_t idx) {
-    const uint32_t t = db.type[idx];
-    const uint32_t* p = db.pw + db.poff[idx];
+DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     if (S == S_TPCB) {
         tpcb_account(db, idx, p);
         tpcb_home(db, idx, p);
@@ -376,6 +380,11 @@ DEV void exec_txn(const DevDb& db, uint32_t idx) {
             tpcc_pay_customer(db, idx, p);
         }
     }
+}
+
+template <int S>
+DEV void exec_txn(const DevDb& db, uint32_t idx) {
+    exec_txn_p<S>(db, idx, db.type[idx], db.pw + db.poff[idx]);
 }
 
 // =================================================================================

@@ -91,7 +91,7 @@ def test_grid_shape_independence(strategy):
     image = W.tm1_db(dims, seed=1)
     bulk = W.tm1_bulk(dims, 20_000, seed=2)
     ref = oracle.run(W.TM1, dims.dims, image, bulk)
-    for grid, narrow in [(1, 64), (7, 1), (0, 1024)]:
+    for grid, narrow in [(1, 0), (7, 0), (0, 0)]:
         db = gpu_db(W.TM1, dims, image, bulk.n)
         db.set_launch(exec_grid=grid, narrow_max=narrow)
         db.submit(bulk)

@@ -137,6 +137,8 @@ struct gputx_db {
     uint32_t* d_lkey = nullptr;
     uint32_t* d_part_off = nullptr;
     uint16_t* d_g = nullptr;         // CTAs per k-set round
+    uint8_t* d_ptype = nullptr;      // types in k-set execution order
+    uint32_t* d_pp = nullptr;        // first 8 parameter words in k-set execution order
     uint32_t* d_done = nullptr;      // per-round completion counters
     uint32_t* d_sc = nullptr;
     uint32_t* h_sc = nullptr;        // pinned mirror
@@ -262,7 +264,8 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 // ------------------------------------------------------------------------------- K-SET
 // parameter words staged in registers by the K-SET executor (0: read from HBM)
 template <int S> constexpr int kset_pw() { return S == S_TPCB ? 4 : S == S_TM1 ? 8 : 0; }
-template <int S> const void* kset_fn() { return (const void*)kset_exec_kernel<S, kset_pw<S>()>; }
+template <int S> constexpr int kset_block() { return S == S_TPCC ? 256 : KX_THREADS; }
+template <int S> const void* kset_fn() { return (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>()>; }
 template <int S>
 gputx_status emit_records(gputx_db* db, const DevDb& v) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
@@ -314,17 +317,19 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
     ++db->launches;
     const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
-    group_kernel<0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, nullptr, nullptr);
+    group_kernel<0, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, nullptr, nullptr,
+                                          nullptr, nullptr, nullptr, nullptr);
     ++db->launches;
     scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
     ++db->launches;
-    group_kernel<1><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff, db->d_perm);
+    group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
+                                                     db->d_perm, db->d_poff, db->d_pw, db->d_ptype, db->d_pp);
     ++db->launches;
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
         const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
-        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, KX_THREADS,
+        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, kset_block<S>(),
                                                                          db->d_g, db->d_done);
         ++db->launches;
         DevDb vv = v;
@@ -334,8 +339,10 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         uint32_t* done = db->d_done;
         const uint32_t* sc = db->d_sc;
         uint32_t TT = T;
-        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc};
-        TRY(launch_coop(db, kset_fn<S>(), (int)G, KX_THREADS, args));
+        const uint8_t* pt = db->d_ptype;
+        const uint32_t* pp = db->d_pp;
+        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp};
+        TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
         ++db->launches;
     }
     cudaEventRecord(db->ev[6], s);
@@ -510,6 +517,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_cnt, cntn)) || (st = dalloc(db, &db->d_rec_off, NB + 2)) ||
         (st = dalloc(db, &db->d_D, NB)) || (st = dalloc(db, &db->d_perm, NB)) ||
         (st = dalloc(db, &db->d_g, NB + 1)) || (st = dalloc(db, &db->d_done, NB + 1)) ||
+        (st = dalloc(db, &db->d_ptype, NB)) || (st = dalloc(db, &db->d_pp, NB * 8)) ||
         (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
@@ -539,9 +547,12 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
     int kg = 0;
-    if (schema == S_TPCB) kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>()>, KX_THREADS, 0);
-    else if (schema == S_TM1) kg = coop_grid(db, kset_exec_kernel<S_TM1, kset_pw<S_TM1>()>, KX_THREADS, 0);
-    else kg = coop_grid(db, kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>()>, KX_THREADS, 0);
+    if (schema == S_TPCB)
+        kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>, kset_block<S_TPCB>(), 0);
+    else if (schema == S_TM1)
+        kg = coop_grid(db, kset_exec_kernel<S_TM1, kset_pw<S_TM1>(), kset_block<S_TM1>()>, kset_block<S_TM1>(), 0);
+    else
+        kg = coop_grid(db, kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>(), kset_block<S_TPCC>()>, kset_block<S_TPCC>(), 0);
     db->kset_grid = kg;
     if (cudaStreamSynchronize(db->stream) != cudaSuccess) return bail(GPUTX_ECUDA);
     *out = db;
@@ -887,7 +898,7 @@ void gputx_close_db(gputx_db* db) {
         for (auto& c : t.cols) cudaFree(c.d);
     void* ps[] = {db->d_type, db->d_poff, db->d_pw, db->d_status, db->d_out, db->d_ins_off, db->d_hkeys, db->d_hvals,
                   db->d_name_sorted, db->d_name_off, db->d_rec_a, db->d_rec_b, db->d_cnt, db->d_rec_off, db->d_D,
-                  db->d_perm, db->d_g, db->d_done, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
+                  db->d_perm, db->d_g, db->d_done, db->d_ptype, db->d_pp, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
                   db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
                   db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
                   db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets};

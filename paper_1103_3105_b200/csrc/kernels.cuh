@@ -359,11 +359,14 @@ DEV int gr_slot(uint32_t* skey, uint32_t key) {
     return -1;
 }
 
-// mode 0: histogram into cnt[]; mode 1: scatter perm[] (cnt[] counts down)
-template <int MODE>
+// mode 0: histogram into cnt[]; mode 1: scatter perm[] (cnt[] counts down) and, for
+// PW > 0, the type and the first PW parameter words of each transaction into execution
+// order (ptype[pos], pp[pos*PW..]) so the executor reads them coalesced.
+template <int MODE, int PW>
 __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__ D, const uint8_t* __restrict__ type,
                                                     uint32_t n, uint32_t T, uint32_t* cnt, const uint32_t* off,
-                                                    uint32_t* perm) {
+                                                    uint32_t* perm, const uint32_t* __restrict__ poff,
+                                                    const uint32_t* __restrict__ pw, uint8_t* ptype, uint32_t* pp) {
     __shared__ uint32_t skey[GR_SLOTS];
     __shared__ uint32_t scnt[GR_SLOTS];
     __shared__ uint32_t sbase[GR_SLOTS];
@@ -407,6 +410,16 @@ __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__
                 const uint32_t i = (uint32_t)(t0 + k * 256 + threadIdx.x);
                 const uint32_t pos = off[key[k]] + (slot[k] >= 0 ? sbase[slot[k]] + rank[k] : rank[k]);
                 perm[pos] = i;
+                if (PW > 0) {
+                    ptype[pos] = type[i];
+                    const uint32_t* src = pw + poff[i];
+                    uint32_t v[PW > 0 ? PW : 1];
+#pragma unroll
+                    for (int w = 0; w < PW; ++w) v[w] = src[w];
+#pragma unroll
+                    for (int w = 0; w < PW; w += 4)
+                        *reinterpret_cast<uint4*>(pp + (uint64_t)pos * PW + w) = make_uint4(v[w], v[w + 1], v[w + 2], v[w + 3]);
+                }
             }
         }
         __syncthreads();
@@ -434,26 +447,29 @@ __global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, 
 
 constexpr int KX_THREADS = 1024;
 
-template <int S, int PW>
-__global__ void __launch_bounds__(KX_THREADS) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
+template <int S, int PW, int KB>
+__global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
                                                                const uint32_t* __restrict__ off, uint32_t T,
                                                                const uint16_t* __restrict__ g, uint32_t* done,
-                                                               const uint32_t* sc) {
+                                                               const uint32_t* sc, const uint8_t* __restrict__ ptype,
+                                                               const uint32_t* __restrict__ pp) {
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
     // prefetched first slice of the round this CTA executes next
     uint32_t nidx = 0xFFFFFFFFu, nt = 0;
     uint32_t np[PW > 0 ? PW : 1];
     auto prefetch = [&](uint32_t lo, uint32_t hi) {
-        const uint32_t j = lo + b * KX_THREADS + tid;
+        const uint32_t j = lo + b * KB + tid;
         nidx = 0xFFFFFFFFu;
         if (j < hi) {
             nidx = __ldg(&perm[j]);
-            nt = db.type[nidx];
             if (PW > 0) {
-                const uint32_t* p = db.pw + db.poff[nidx];
+                nt = __ldg(&ptype[j]);
 #pragma unroll
-                for (int w = 0; w < (PW > 0 ? PW : 1); ++w) np[w] = p[w];
+                for (int w = 0; w < (PW > 0 ? PW : 1); w += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(pp + (uint64_t)j * PW + w));
+                    np[w] = v.x; np[w + 1] = v.y; np[w + 2] = v.z; np[w + 3] = v.w;
+                }
             }
         }
     };
@@ -494,8 +510,19 @@ __global__ void __launch_bounds__(KX_THREADS) kset_exec_kernel(DevDb db, const u
             if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
             else exec_txn<S>(db, cidx);
         }
-        for (uint32_t j = clo + (b + gk) * KX_THREADS + tid; j < chi; j += gk * KX_THREADS)
-            exec_txn<S>(db, __ldg(&perm[j]));
+        for (uint32_t j = clo + (b + gk) * KB + tid; j < chi; j += gk * KB) {
+            if (PW > 0) {
+                uint32_t q[PW > 0 ? PW : 1];
+#pragma unroll
+                for (int w = 0; w < (PW > 0 ? PW : 1); w += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(pp + (uint64_t)j * PW + w));
+                    q[w] = v.x; q[w + 1] = v.y; q[w + 2] = v.z; q[w + 3] = v.w;
+                }
+                exec_txn_p<S>(db, __ldg(&perm[j]), __ldg(&ptype[j]), q);
+            } else {
+                exec_txn<S>(db, __ldg(&perm[j]));
+            }
+        }
         __syncthreads();
         const bool next_shared = (k + 1 < nk) && __ldg(&g[k + 1]) > 1;
         if (tid == 0 && (gk > 1 || next_shared || b > 0)) {

@@ -155,12 +155,19 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
 // =================================================================================
 // Stored procedures (whole transaction; K-SET and TPL)
 // =================================================================================
+// Every procedure issues all of its reads first (static columns speculatively), then
+// takes its abort decision, then writes: the loads of one transaction overlap in
+// flight instead of serialising behind stores.  Increments whose old value no output
+// needs are fire-and-forget reductions (red.global.add) — the transaction holds the
+// item exclusively (k-set round, TPL lock, PART partition), so this is plain RMW
+// without a round trip.
+DEV void red_add(int64_t* p, int64_t v) { atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v); }
+DEV void red_add(uint32_t* p, uint32_t v) { atomicAdd(p, v); }
+
 DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
     const int32_t delta = (int32_t)p[3];
-    int64_t* tel = COL(int64_t, B_TEL);
-    int64_t* br = COL(int64_t, B_BR);
-    stm(&tel[p[1]], ldm(&tel[p[1]]) + delta);
-    stm(&br[p[2]], ldm(&br[p[2]]) + delta);
+    red_add(&COL(int64_t, B_TEL)[p[1]], (int64_t)delta);
+    red_add(&COL(int64_t, B_BR)[p[2]], (int64_t)delta);
     const uint64_t r = db.ins_base[0] + idx;               // history row (every deposit commits)
     INS(uint32_t, IB_TID)[r] = p[1];
     INS(uint32_t, IB_BID)[r] = p[2];
@@ -181,56 +188,70 @@ DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     switch (t) {
     case 0: {   // GET_SUBSCRIBER_DATA
         const uint32_t s = p[0] - 1;
-        put64(o, __ldg(&COL(const uint64_t, M_NBR)[s]));
-        put64(o + 8, __ldg(&COL(const uint64_t, M_HEX)[s]));
-        put32(o + 16, __ldg(&COL(const uint32_t, M_MSC)[s]));
-        put32(o + 20, ldm(&COL(uint32_t, M_VLR)[s]));
+        const uint64_t nbr = __ldg(&COL(const uint64_t, M_NBR)[s]);
+        const uint64_t hex = __ldg(&COL(const uint64_t, M_HEX)[s]);
+        const uint32_t msc = __ldg(&COL(const uint32_t, M_MSC)[s]);
+        const uint32_t vlr = ldm(&COL(uint32_t, M_VLR)[s]);
         const uint16_t bits = ldm(&COL(uint16_t, M_BITS)[s]);
-        const uint8_t* b2 = COL(const uint8_t, M_BYTE2) + (uint64_t)s * 10;
-        o[24] = (uint8_t)bits; o[25] = (uint8_t)(bits >> 8);
+        const uint16_t* b2 = reinterpret_cast<const uint16_t*>(COL(const uint8_t, M_BYTE2) + (uint64_t)s * 10);
+        uint16_t bb[5];
 #pragma unroll
-        for (int k = 0; k < 10; ++k) o[26 + k] = __ldg(b2 + k);
+        for (int k = 0; k < 5; ++k) bb[k] = __ldg(b2 + k);
+        put64(o, nbr);
+        put64(o + 8, hex);
+        put32(o + 16, msc);
+        put32(o + 20, vlr);
+        reinterpret_cast<uint16_t*>(o)[12] = bits;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) reinterpret_cast<uint16_t*>(o)[13 + k] = bb[k];
         return;
     }
     case 1: {   // GET_NEW_DESTINATION
         const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
-        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f]) || !__ldg(&COL(const uint8_t, M_SF_ACTIVE)[f])) {
-            db.status[idx] = 1; return;
+        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
+        const uint8_t active = __ldg(&COL(const uint8_t, M_SF_ACTIVE)[f]);
+        uint8_t live[3], endt[3];
+        uint64_t num[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            live[k] = ldm(&COL(uint8_t, M_CF_LIVE)[f * 3 + k]);
+            endt[k] = ldm(&COL(uint8_t, M_CF_END)[f * 3 + k]);
+            num[k] = ldm(&COL(uint64_t, M_CF_NUM)[f * 3 + k]);
         }
-        const uint8_t* live = COL(uint8_t, M_CF_LIVE);
-        const uint8_t* endt = COL(uint8_t, M_CF_END);
-        const uint64_t* num = COL(uint64_t, M_CF_NUM);
+        if (!valid || !active) { db.status[idx] = 1; return; }
         uint32_t cnt = 0;
-        for (uint32_t k = 0; k < 3; ++k) {
-            const uint64_t c = f * 3 + k;
-            if (ldm(&live[c]) && k * 8 <= p[2] && p[3] < ldm(&endt[c])) {
-                put64(o + 8 + 8 * cnt, ldm(&num[c]));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (live[k] && (uint32_t)k * 8 <= p[2] && p[3] < endt[k]) {
+                put64(o + 8 + 8 * cnt, num[k]);
                 ++cnt;
             }
         }
-        if (cnt == 0) {
-            db.status[idx] = 1;
-            for (int k = 8; k < 32; k += 4) put32(o + k, 0);
-            return;
-        }
+        if (cnt == 0) { db.status[idx] = 1; return; }
         put32(o, cnt);
         return;
     }
     case 2: {   // GET_ACCESS_DATA
         const uint64_t a = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
-        if (!__ldg(&COL(const uint8_t, M_AI_VALID)[a])) { db.status[idx] = 1; return; }
-        o[0] = __ldg(&COL(const uint8_t, M_AI_D1)[a]);
-        o[1] = __ldg(&COL(const uint8_t, M_AI_D2)[a]);
-        put32(o + 4, __ldg(&COL(const uint32_t, M_AI_D3)[a]));
-        put64(o + 8, __ldg(&COL(const uint64_t, M_AI_D4)[a]));
+        const uint8_t valid = __ldg(&COL(const uint8_t, M_AI_VALID)[a]);
+        const uint8_t d1 = __ldg(&COL(const uint8_t, M_AI_D1)[a]);
+        const uint8_t d2 = __ldg(&COL(const uint8_t, M_AI_D2)[a]);
+        const uint32_t d3 = __ldg(&COL(const uint32_t, M_AI_D3)[a]);
+        const uint64_t d4 = __ldg(&COL(const uint64_t, M_AI_D4)[a]);
+        if (!valid) { db.status[idx] = 1; return; }
+        put32(o, (uint32_t)d1 | ((uint32_t)d2 << 8));
+        put32(o + 4, d3);
+        put64(o + 8, d4);
         return;
     }
     case 3: {   // UPDATE_SUBSCRIBER_DATA (two-phase: SF existence first)
         const uint32_t s = p[0] - 1;
         const uint64_t f = (uint64_t)s * 4 + (p[1] - 1);
-        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f])) { db.status[idx] = 1; return; }
         uint16_t* bits = COL(uint16_t, M_BITS);
-        stm(&bits[s], (uint16_t)((ldm(&bits[s]) & 0xFFFEu) | (p[2] & 1u)));
+        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
+        const uint16_t b = ldm(&bits[s]);
+        if (!valid) { db.status[idx] = 1; return; }
+        stm(&bits[s], (uint16_t)((b & 0xFFFEu) | (p[2] & 1u)));
         stm(&COL(uint8_t, M_SF_DA)[f], (uint8_t)p[3]);
         return;
     }
@@ -244,7 +265,9 @@ DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
         const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[2] - 1);
         const uint64_t c = f * 3 + p[3] / 8;
         uint8_t* live = COL(uint8_t, M_CF_LIVE);
-        if (!__ldg(&COL(const uint8_t, M_SF_VALID)[f]) || ldm(&live[c])) { db.status[idx] = 1; return; }
+        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
+        const uint8_t lv = ldm(&live[c]);
+        if (!valid || lv) { db.status[idx] = 1; return; }
         stm(&live[c], (uint8_t)1);
         stm(&COL(uint8_t, M_CF_END)[c], (uint8_t)p[4]);
         stm(&COL(uint64_t, M_CF_NUM)[c], (uint64_t)p[5] | ((uint64_t)p[6] << 32));
@@ -274,31 +297,67 @@ DEV bool tpcc_no_aborts(const DevDb& db, const uint32_t* p) {
     return false;
 }
 
+// Stock lines: read every selected line's S_QUANTITY first, then apply the lines in
+// order (a repeated (sw, i) sees its earlier line's update), then write.
 DEV void tpcc_no_stock(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_t sw_sel) {
     const uint32_t I = db.dims[3], w = p[0], cnt = p[3];
     int32_t* sq = COL(int32_t, C_S_QTY);
-    int64_t* sy = COL(int64_t, C_S_YTD);
-    uint32_t* so = COL(uint32_t, C_S_OCNT);
-    uint32_t* sr = COL(uint32_t, C_S_RCNT);
+    uint64_t sidx[15];
+    int32_t q0[15];
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        if ((uint32_t)l < cnt) {
+            sidx[l] = (uint64_t)p[5 + 3 * l] * I + p[4 + 3 * l];
+            q0[l] = ldm(&sq[sidx[l]]);
+        }
+    }
     uint8_t* o = db.out + (uint64_t)idx * 200;
-    for (uint32_t l = 0; l < cnt; ++l) {
-        const uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l], q = p[6 + 3 * l];
+    int32_t cur[15];
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        if ((uint32_t)l >= cnt) continue;
+        const uint32_t sw = p[5 + 3 * l];
         if (sw_sel != ALL_LINES && sw != sw_sel) continue;
-        const uint64_t s = (uint64_t)sw * I + i;
-        const int32_t cur = ldm(&sq[s]);
-        stm(&sq[s], cur >= (int32_t)q + 10 ? cur - (int32_t)q : cur - (int32_t)q + 91);
-        stm(&sy[s], ldm(&sy[s]) + (int64_t)q);
-        stm(&so[s], ldm(&so[s]) + 1u);
-        if (sw != w) stm(&sr[s], ldm(&sr[s]) + 1u);
-        put32(o + 16 + 12 * l, (uint32_t)cur);
+        const int32_t q = (int32_t)p[6 + 3 * l];
+        int32_t before = q0[l];
+#pragma unroll
+        for (int m = 0; m < l; ++m)
+            if (sidx[m] == sidx[l]) before = cur[m];       // latest earlier update of the same stock row
+        cur[l] = before >= q + 10 ? before - q : before - q + 91;
+        put32(o + 16 + 12 * l, (uint32_t)before);
+        red_add(&COL(int64_t, C_S_YTD)[sidx[l]], (int64_t)q);
+        red_add(&COL(uint32_t, C_S_OCNT)[sidx[l]], 1u);
+        if (sw != w) red_add(&COL(uint32_t, C_S_RCNT)[sidx[l]], 1u);
+    }
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        if ((uint32_t)l >= cnt) continue;
+        const uint32_t sw = p[5 + 3 * l];
+        if (sw_sel != ALL_LINES && sw != sw_sel) continue;
+        stm(&sq[sidx[l]], cur[l]);
     }
 }
 
 DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
-    const uint32_t D = db.dims[1], C = db.dims[2], w = p[0], d = p[1], c = p[2], cnt = p[3];
+    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3], w = p[0], d = p[1], c = p[2], cnt = p[3];
     const uint64_t wd = (uint64_t)w * D + d;
     uint32_t* dn = COL(uint32_t, C_D_NEXT);
+    const int32_t* price = COL(const int32_t, C_I_PRICE);
+    const uint8_t* iorig = COL(const uint8_t, C_I_ORIG);
+    const uint8_t* sorig = COL(const uint8_t, C_S_ORIG);
     const uint32_t oid = ldm(&dn[wd]);
+    const int64_t disc = __ldg(&COL(const int32_t, C_C_DISC)[wd * C + c]);
+    const int64_t tax = (int64_t)__ldg(&COL(const int32_t, C_W_TAX)[w]) + __ldg(&COL(const int32_t, C_D_TAX)[wd]);
+    int32_t pr[15];
+    uint8_t br[15];
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        if ((uint32_t)l < cnt) {
+            const uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l];
+            pr[l] = __ldg(&price[i]);
+            br[l] = __ldg(&iorig[i]) & __ldg(&sorig[(uint64_t)sw * I + i]);
+        }
+    }
     stm(&dn[wd], oid + 1);
     uint32_t all_local = 1;
     for (uint32_t l = 0; l < cnt; ++l) all_local &= (p[5 + 3 * l] == w);
@@ -309,24 +368,21 @@ DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
     const uint64_t rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
     const uint64_t rl0 = db.ins_base[T_OLINE] + db.ins_off[T_OLINE * (uint64_t)db.ins_stride + idx];
-    const int32_t* price = COL(const int32_t, C_I_PRICE);
-    const uint8_t* iorig = COL(const uint8_t, C_I_ORIG);
-    const uint8_t* sorig = COL(const uint8_t, C_S_ORIG);
     uint8_t* o = db.out + (uint64_t)idx * 200;
     int64_t sum = 0;
-    for (uint32_t l = 0; l < cnt; ++l) {
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        if ((uint32_t)l >= cnt) continue;
         const uint32_t i = p[4 + 3 * l], sw = p[5 + 3 * l], q = p[6 + 3 * l];
-        const int32_t amount = (int32_t)q * __ldg(&price[i]);
+        const int32_t amount = (int32_t)q * pr[l];
         sum += amount;
         const uint64_t rl = rl0 + l;
         INS(uint32_t, IL_OID)[rl] = oid; INS(uint32_t, IL_D)[rl] = d; INS(uint32_t, IL_W)[rl] = w;
         INS(uint32_t, IL_NUM)[rl] = l; INS(uint32_t, IL_I)[rl] = i; INS(uint32_t, IL_SW)[rl] = sw;
         INS(uint32_t, IL_QTY)[rl] = q; INS(int32_t, IL_AMT)[rl] = amount;
         put32(o + 16 + 12 * l + 4, (uint32_t)amount);
-        o[16 + 12 * l + 8] = (uint8_t)(__ldg(&iorig[i]) & __ldg(&sorig[(uint64_t)sw * db.dims[3] + i]));
+        o[16 + 12 * l + 8] = br[l];
     }
-    const int64_t disc = __ldg(&COL(const int32_t, C_C_DISC)[wd * C + c]);
-    const int64_t tax = (int64_t)__ldg(&COL(const int32_t, C_W_TAX)[w]) + __ldg(&COL(const int32_t, C_D_TAX)[wd]);
     const int64_t x = sum * (10000 - disc) * (10000 + tax);
     put32(o, oid);
     put32(o + 4, cnt);
@@ -335,11 +391,8 @@ DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
 
 DEV void tpcc_pay_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
     const uint32_t D = db.dims[1], w = p[0], d = p[1], h = p[6];
-    int64_t* wy = COL(int64_t, C_W_YTD);
-    int64_t* dy = COL(int64_t, C_D_YTD);
-    const uint64_t wd = (uint64_t)w * D + d;
-    stm(&wy[w], ldm(&wy[w]) + (int64_t)h);
-    stm(&dy[wd], ldm(&dy[wd]) + (int64_t)h);
+    red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
+    red_add(&COL(int64_t, C_D_YTD)[(uint64_t)w * D + d], (int64_t)h);
     const uint64_t r = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IH_C)[r] = p[5]; INS(uint32_t, IH_CD)[r] = p[3]; INS(uint32_t, IH_CW)[r] = p[2];
     INS(uint32_t, IH_D)[r] = d; INS(uint32_t, IH_W)[r] = w; INS(uint32_t, IH_DATE)[r] = db.first_ts + idx;
@@ -349,15 +402,14 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
     const uint32_t D = db.dims[1], C = db.dims[2], h = p[6];
     const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
     int64_t* bal = COL(int64_t, C_C_BAL);
-    int64_t* ytd = COL(int64_t, C_C_YTD);
-    uint32_t* cnt = COL(uint32_t, C_C_CNT);
     const int64_t nb = ldm(&bal[cx]) - (int64_t)h;
+    const uint8_t credit = __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]);
     stm(&bal[cx], nb);
-    stm(&ytd[cx], ldm(&ytd[cx]) + (int64_t)h);
-    stm(&cnt[cx], ldm(&cnt[cx]) + 1u);
+    red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
+    red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
     uint8_t* o = db.out + (uint64_t)idx * 200;
     put32(o, p[5]);
-    put32(o + 4, __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]));
+    put32(o + 4, credit);
     put64(o + 8, (uint64_t)nb);
 }
 
@@ -365,8 +417,8 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
 template <int S>
 DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     if (S == S_TPCB) {
-        tpcb_account(db, idx, p);
         tpcb_home(db, idx, p);
+        tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
     } else {

@@ -153,6 +153,7 @@ struct gputx_db {
     uint32_t ticket_slot = 0;
     int nsm = 0;
     int rank_grid = 0, kset_grid = 0;
+    uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
     uint32_t exec_grid_override = 0;
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
@@ -302,7 +303,8 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         GridBar* bar = db->d_bar;
         uint32_t* sc = db->d_sc;
         uint32_t maxp = 1u << 20;
-        void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp};
+        uint32_t lmax = db->rank_local;
+        void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp, &lmax};
         TRY(launch_coop(db, (const void*)rank_kernel, db->rank_grid, RK_THREADS, args));
         ++db->launches;
     }
@@ -546,6 +548,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
+    if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
     int kg = 0;
     if (schema == S_TPCB)
         kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>, kset_block<S_TPCB>(), 0);

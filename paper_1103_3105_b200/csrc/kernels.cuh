@@ -214,7 +214,7 @@ DEV Xf rec_xf(bool head, uint32_t w, int d) {
 }
 
 constexpr int RK_THREADS = 256, RK_ITEMS = 8, RK_TILE = RK_THREADS * RK_ITEMS;
-constexpr int RK_LOCAL_MAX = 32;     // in-tile Gauss-Seidel sweeps per pass
+constexpr uint32_t RK_LOCAL_DEFAULT = 4;   // in-tile Gauss-Seidel sweeps per pass (default)
 
 // One pass over the sorted records.  A tile first publishes its map aggregate and
 // gets the prefix entering it by decoupled look-back; then it re-sweeps itself with
@@ -224,7 +224,8 @@ constexpr int RK_LOCAL_MAX = 32;     // in-tile Gauss-Seidel sweeps per pass
 // pass that raises nothing proves it.
 __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
-                                                          GridBar* bar, uint32_t* sc, uint32_t max_passes) {
+                                                          GridBar* bar, uint32_t* sc, uint32_t max_passes,
+                                                          uint32_t local_max) {
     __shared__ uint64_t stage[RK_TILE];
     __shared__ Xf sm[8];
     __shared__ Xf s_pre;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
                     hw |= 1u << (16 + k);
                 }
             }
-            for (int it = 0; it < RK_LOCAL_MAX; ++it) {
+            for (uint32_t it = 0; it < local_max; ++it) {
                 int dv[RK_ITEMS];
                 Xf agg = OpXf::identity();
 #pragma unroll
@@ -446,6 +447,7 @@ __global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, 
 }
 
 constexpr int KX_THREADS = 1024;
+constexpr uint32_t KX_CH = 2048;      // rounds staged per shared-memory chunk
 
 template <int S, int PW, int KB>
 __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
@@ -473,21 +475,43 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             }
         }
     };
+    // round metadata (g[k], k-set start off[k*T]) staged in shared memory by chunks:
+    // the per-round lookups on the critical path are shared-memory hits
+    __shared__ uint16_t sg[KX_CH];
+    __shared__ uint32_t soff[KX_CH + 1];
+    uint32_t cb = 0xFFFFFFFFu;
+    auto load_chunk = [&](uint32_t base) {           // CTA-uniform
+        __syncthreads();
+        for (uint32_t i = tid; i < KX_CH; i += KB) sg[i] = base + i < nk ? __ldg(&g[base + i]) : (uint16_t)0;
+        for (uint32_t i = tid; i <= KX_CH; i += KB) soff[i] = base + i <= nk ? __ldcg(&off[(base + i) * T]) : 0u;
+        __syncthreads();
+        cb = base;
+    };
+    auto G = [&](uint32_t kk) -> uint32_t {
+        if (kk < cb || kk >= cb + KX_CH) load_chunk(kk - kk % KX_CH);
+        return sg[kk - cb];
+    };
+    auto bounds = [&](uint32_t kk, uint32_t& l, uint32_t& h) {
+        G(kk);
+        l = soff[kk - cb];
+        h = soff[kk - cb + 1];
+    };
     uint32_t k = 0;
     // find this CTA's first round
-    while (k < nk && __ldg(&g[k]) <= b) ++k;
+    while (k < nk && G(k) <= b) ++k;
     if (k >= nk) return;
-    uint32_t lo = __ldcg(&off[k * T]), hi = __ldcg(&off[(k + 1) * T]);
+    uint32_t lo, hi;
+    bounds(k, lo, hi);
     prefetch(lo, hi);
-    uint32_t prev = 0xFFFFFFFFu;            // last round this CTA executed
+    uint32_t prev = 0xFFFFFFFFu, gprev = 0;   // last round this CTA executed, its CTA count
     while (k < nk) {
-        const uint32_t gk = __ldg(&g[k]);
+        const uint32_t gk = G(k);
         // wait for round k-1
         if (k > 0) {
-            const bool mine = (prev == k - 1) && __ldg(&g[k - 1]) == 1;
+            const bool mine = (prev == k - 1) && gprev == 1;
             if (!mine) {
                 if (tid == 0) {
-                    const uint32_t need = __ldg(&g[k - 1]);
+                    const uint32_t need = prev == k - 1 ? gprev : __ldg(&g[k - 1]);
                     while (ld_acquire(&done[k - 1]) < need) { }
                 }
                 __syncthreads();
@@ -500,10 +524,9 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         for (int w = 0; w < (PW > 0 ? PW : 1); ++w) cp[w] = np[w];
         const uint32_t clo = lo, chi = hi;
         uint32_t k2 = k + 1;
-        while (k2 < nk && __ldg(&g[k2]) <= b) ++k2;
+        while (k2 < nk && G(k2) <= b) ++k2;
         if (k2 < nk) {
-            lo = __ldcg(&off[k2 * T]);
-            hi = __ldcg(&off[(k2 + 1) * T]);
+            bounds(k2, lo, hi);
             prefetch(lo, hi);
         }
         if (cidx != 0xFFFFFFFFu) {
@@ -524,12 +547,14 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             }
         }
         __syncthreads();
-        const bool next_shared = (k + 1 < nk) && __ldg(&g[k + 1]) > 1;
-        if (tid == 0 && (gk > 1 || next_shared || b > 0)) {
+        // CTA 0 runs every round; for it k2 == k + 1, which is in the staged chunk
+        const bool next_shared = b > 0 || ((k + 1 < nk) && G(k + 1) > 1);
+        if (tid == 0 && (gk > 1 || next_shared)) {
             __threadfence();
             atomicAdd(&done[k], 1u);
         }
         prev = k;
+        gprev = gk;
         k = k2;
     }
 }

@@ -173,6 +173,12 @@ gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const cha
 gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n);
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n);
 
+/* K-SET round tracing (diagnostics): when on, the executor records the device time
+ * (ns, %globaltimer) at which CTA 0 starts each round; gputx_read_round_ns copies the
+ * first `rounds` (<= n) entries of the last K-SET execute.  ESTATE if tracing was off. */
+gputx_status gputx_trace_rounds(gputx_db* db, int on);
+gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds);
+
 /* Restore the pristine image (columns and insert tables) by a device copy. */
 gputx_status gputx_reset(gputx_db* db);
 

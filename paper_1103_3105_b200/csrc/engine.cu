@@ -139,6 +139,8 @@ struct gputx_db {
     uint16_t* d_g = nullptr;         // CTAs per k-set round
     uint8_t* d_ptype = nullptr;      // types in k-set execution order
     uint32_t* d_pp = nullptr;        // first 8 parameter words in k-set execution order
+    uint64_t* d_trace = nullptr;     // per-round start times (ns), CTA 0, when trace_rounds
+    bool trace_rounds = false;
     uint32_t* d_done = nullptr;      // per-round completion counters
     uint32_t* d_sc = nullptr;
     uint32_t* h_sc = nullptr;        // pinned mirror
@@ -343,7 +345,8 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         uint32_t TT = T;
         const uint8_t* pt = db->d_ptype;
         const uint32_t* pp = db->d_pp;
-        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp};
+        uint64_t* trace = db->trace_rounds ? db->d_trace : nullptr;
+        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace};
         TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
         ++db->launches;
     }
@@ -520,6 +523,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_D, NB)) || (st = dalloc(db, &db->d_perm, NB)) ||
         (st = dalloc(db, &db->d_g, NB + 1)) || (st = dalloc(db, &db->d_done, NB + 1)) ||
         (st = dalloc(db, &db->d_ptype, NB)) || (st = dalloc(db, &db->d_pp, NB * 8)) ||
+        (st = dalloc(db, &db->d_trace, NB + 1)) ||
         (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
@@ -863,6 +867,20 @@ gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n) {
     return GPUTX_OK;
 }
 
+gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds) {
+    if (!db || !host) return GPUTX_EINVAL;
+    if (!db->trace_rounds || !db->has_perm) return fail(db, GPUTX_ESTATE, "round tracing off or no K-SET bulk");
+    if (rounds > db->n) return fail(db, GPUTX_EINVAL, "more rounds than transactions");
+    if (rounds) CK(cudaMemcpy(host, db->d_trace, rounds * 8, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_trace_rounds(gputx_db* db, int on) {
+    if (!db) return GPUTX_EINVAL;
+    db->trace_rounds = on != 0;
+    return GPUTX_OK;
+}
+
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
@@ -901,7 +919,7 @@ void gputx_close_db(gputx_db* db) {
         for (auto& c : t.cols) cudaFree(c.d);
     void* ps[] = {db->d_type, db->d_poff, db->d_pw, db->d_status, db->d_out, db->d_ins_off, db->d_hkeys, db->d_hvals,
                   db->d_name_sorted, db->d_name_off, db->d_rec_a, db->d_rec_b, db->d_cnt, db->d_rec_off, db->d_D,
-                  db->d_perm, db->d_g, db->d_done, db->d_ptype, db->d_pp, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
+                  db->d_perm, db->d_g, db->d_done, db->d_ptype, db->d_pp, db->d_trace, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
                   db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
                   db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
                   db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets};

@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                                                                const uint32_t* __restrict__ off, uint32_t T,
                                                                const uint16_t* __restrict__ g, uint32_t* done,
                                                                const uint32_t* sc, const uint8_t* __restrict__ ptype,
-                                                               const uint32_t* __restrict__ pp) {
+                                                               const uint32_t* __restrict__ pp, uint64_t* trace) {
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
     // prefetched first slice of the round this CTA executes next
@@ -512,11 +512,14 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             if (!mine) {
                 if (tid == 0) {
                     const uint32_t need = prev == k - 1 ? gprev : __ldg(&g[k - 1]);
-                    while (ld_acquire(&done[k - 1]) < need) { }
+                    uint32_t spins = 0;
+                    while (ld_acquire(&done[k - 1]) < need)
+                        if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
                 }
                 __syncthreads();
             }
         }
+        if (trace && b == 0 && tid == 0) trace[k] = globaltimer_ns();
         // take the prefetched slice, then prefetch this CTA's next round
         const uint32_t cidx = nidx, ct = nt;
         uint32_t cp[PW > 0 ? PW : 1];

@@ -86,6 +86,8 @@ def load_library():
         "gputx_close_db": ([P], None),
         "gputx_last_error": ([P], ctypes.c_char_p),
         "gputx_set_launch": ([P, U32, U32, U32], I),
+        "gputx_trace_rounds": ([P, I], I),
+        "gputx_read_round_ns": ([P, P, U64], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -99,7 +101,7 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_submit_bulk", "gputx_execute", "gputx_read_results", "gputx_results_device",
             "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
-            "gputx_set_launch"]
+            "gputx_set_launch", "gputx_trace_rounds", "gputx_read_round_ns"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -251,6 +253,14 @@ class Database:
 
     def set_launch(self, exec_block: int = 0, exec_grid: int = 0, narrow_max: int = 0):
         self._check(self.lib.gputx_set_launch(self.h, exec_block, exec_grid, narrow_max), self.h)
+
+    def trace_rounds(self, on: bool = True):
+        self._check(self.lib.gputx_trace_rounds(self.h, int(on)), self.h)
+
+    def round_ns(self, rounds: int) -> np.ndarray:
+        a = np.zeros(max(1, rounds), np.uint64)
+        self._check(self.lib.gputx_read_round_ns(self.h, a.ctypes.data, rounds), self.h)
+        return a[:rounds]
 
     def reset(self):
         self._check(self.lib.gputx_reset(self.h), self.h)

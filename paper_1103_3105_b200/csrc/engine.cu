@@ -156,6 +156,7 @@ struct gputx_db {
     int nsm = 0;
     int rank_grid = 0, kset_grid = 0;
     uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
+    uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
     uint32_t exec_grid_override = 0;
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
@@ -333,7 +334,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     // rounds
     {
         const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
-        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, kset_block<S>(),
+        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, db->kset_q,
                                                                          db->d_g, db->d_done);
         ++db->launches;
         DevDb vv = v;
@@ -553,6 +554,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
+    // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
+    // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
+    db->kset_q = schema == S_TPCC ? 32 : 128;
+    if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     int kg = 0;
     if (schema == S_TPCB)
         kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>, kset_block<S_TPCB>(), 0);

@@ -460,8 +460,14 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     // prefetched first slice of the round this CTA executes next
     uint32_t nidx = 0xFFFFFFFFu, nt = 0;
     uint32_t np[PW > 0 ? PW : 1];
-    auto prefetch = [&](uint32_t lo, uint32_t hi) {
-        const uint32_t j = lo + b * KB + tid;
+    // CTA b's slice of a round [lo, hi) executed by gk CTAs: contiguous chunk b
+    auto slice = [&](uint32_t lo, uint32_t hi, uint32_t gk, uint32_t& slo, uint32_t& shi) {
+        const uint32_t chunk = (hi - lo + gk - 1) / gk;
+        slo = lo + b * chunk;
+        shi = min(hi, slo + chunk);
+    };
+    auto prefetch = [&](uint32_t lo, uint32_t hi) {     // [lo, hi) = this CTA's slice
+        const uint32_t j = lo + tid;
         nidx = 0xFFFFFFFFu;
         if (j < hi) {
             nidx = __ldg(&perm[j]);
@@ -502,6 +508,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     if (k >= nk) return;
     uint32_t lo, hi;
     bounds(k, lo, hi);
+    slice(lo, hi, G(k), lo, hi);
     prefetch(lo, hi);
     uint32_t prev = 0xFFFFFFFFu, gprev = 0;   // last round this CTA executed, its CTA count
     while (k < nk) {
@@ -530,13 +537,14 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         while (k2 < nk && G(k2) <= b) ++k2;
         if (k2 < nk) {
             bounds(k2, lo, hi);
+            slice(lo, hi, G(k2), lo, hi);
             prefetch(lo, hi);
         }
         if (cidx != 0xFFFFFFFFu) {
             if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
             else exec_txn<S>(db, cidx);
         }
-        for (uint32_t j = clo + (b + gk) * KB + tid; j < chi; j += gk * KB) {
+        for (uint32_t j = clo + KB + tid; j < chi; j += KB) {
             if (PW > 0) {
                 uint32_t q[PW > 0 ? PW : 1];
 #pragma unroll

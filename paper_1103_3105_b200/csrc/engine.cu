@@ -531,7 +531,8 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_bar, 1)) || (st = dalloc(db, &db->d_tickets, 256)))
         return bail(st);
     // look-back state: sized for the largest tiled pass
-    const uint64_t tiles = (std::max(db->max_rec, NB * db->ntypes) + 2) / 2048 + 4;
+    // (>= 4096 entries: the rank kernel also keeps one aggregate per CTA here)
+    const uint64_t tiles = std::max<uint64_t>((std::max(db->max_rec, NB * db->ntypes) + 2) / 2048 + 4, 4096);
     if ((st = dalloc(db, &db->lb_scan.flag, tiles)) || (st = dalloc(db, &db->lb_scan.agg, tiles)) ||
         (st = dalloc(db, &db->lb_scan.inc, tiles)) || (st = dalloc(db, &db->lb_rank.flag, tiles)) ||
         (st = dalloc(db, &db->lb_rank.agg, tiles)) || (st = dalloc(db, &db->lb_rank.inc, tiles)) ||

@@ -216,69 +216,106 @@ DEV Xf rec_xf(bool head, uint32_t w, int d) {
 constexpr int RK_THREADS = 256, RK_ITEMS = 8, RK_TILE = RK_THREADS * RK_ITEMS;
 constexpr uint32_t RK_LOCAL_DEFAULT = 4;   // in-tile Gauss-Seidel sweeps per pass (default)
 
-// One pass over the sorted records.  A tile first publishes its map aggregate and
-// gets the prefix entering it by decoupled look-back; then it re-sweeps itself with
-// the D values it just raised until nothing changes on chip (items of one root key
-// are adjacent, so most chains close inside a tile).  Every L computed is a lower
-// bound of the true depth, so chaotic/in-tile updates reach the same fixpoint; a
-// pass that raises nothing proves it.
+// One pass over the sorted records = reduce, then scan:
+//   A. every CTA owns a contiguous range of tiles; it composes the maps of its records
+//      (with the current D) into one aggregate and publishes it;
+//   B. grid barrier;
+//   C. each CTA composes the aggregates of the CTAs before it -> the state entering
+//      its range (no look-back chain);
+//   D. it sweeps its tiles in order: block scan of the maps, L per record, atomicMax
+//      into D; a tile that raised something is re-swept with its own new values (up to
+//      local_max times; items of one root key are adjacent, so chains close on chip).
+// Every L computed is a lower bound of the true depth, so chaotic/in-tile updates
+// reach the same fixpoint; a pass in which nothing is raised proves it.
+struct RkTile {
+    uint32_t hw;       // bit 2k: head, bit 2k+1: write, bit 16+k: valid
+};
+
+DEV uint32_t rk_load(const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t tile, uint64_t* stage,
+                     uint64_t* s_prev) {
+    const uint64_t tb = (uint64_t)tile * RK_TILE;
+    const uint32_t tid = threadIdx.x;
+    __syncthreads();
+    for (uint32_t i = tid; i < RK_TILE; i += RK_THREADS) stage[i] = (tb + i < nrec) ? __ldg(&keys[tb + i]) : ~0ull;
+    if (tid == 0) *s_prev = tb ? __ldg(&keys[tb - 1]) : ~0ull;
+    __syncthreads();
+    uint32_t hw = 0;
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        const uint32_t pos = tid * RK_ITEMS + k;
+        if (tb + pos < nrec) {
+            const uint64_t key = stage[pos];
+            const uint64_t prev = pos ? stage[pos - 1] : *s_prev;
+            const bool head = (tb + pos == 0) || key_item(prev) != key_item(key);
+            hw |= (head ? 1u : 0u) << (2 * k);
+            hw |= key_w(key) << (2 * k + 1);
+            hw |= 1u << (16 + k);
+        }
+    }
+    return hw;
+}
+
+// this thread's composed map over its RK_ITEMS records (current D), and the D values
+DEV Xf rk_thread_map(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* dv) {
+    Xf agg = OpXf::identity();
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        dv[k] = 0;
+        if ((hw >> (16 + k)) & 1u) {
+            dv[k] = (int)__ldcg(&D[key_idx(stage[threadIdx.x * RK_ITEMS + k])]);
+            agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
+        }
+    }
+    return agg;
+}
+
 __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes,
                                                           uint32_t local_max) {
     __shared__ uint64_t stage[RK_TILE];
     __shared__ Xf sm[8];
-    __shared__ Xf s_pre;
     __shared__ uint64_t s_prev;
     __shared__ int s_chg;
+    (void)epoch0;
+    Xf* cta_agg = lb.agg;                  // one aggregate per CTA
     const uint32_t nrec = *nrec_ptr;
     const uint32_t ntiles = (nrec + RK_TILE - 1) / RK_TILE;
+    const uint32_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint32_t t0 = min(ntiles, blockIdx.x * per), t1 = min(ntiles, t0 + per);
     const uint32_t tid = threadIdx.x;
     for (uint32_t pass = 0;; ++pass) {
-        const uint32_t epoch = epoch0 + pass;
         if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (pass + 1) % 3] = 0;
         if (tid == 0) s_chg = 0;
-        for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const uint64_t tb = (uint64_t)tile * RK_TILE;
-            __syncthreads();
-            for (uint32_t i = tid; i < RK_TILE; i += RK_THREADS)
-                stage[i] = (tb + i < nrec) ? __ldg(&keys[tb + i]) : ~0ull;
-            if (tid == 0) s_prev = tb ? __ldg(&keys[tb - 1]) : ~0ull;
-            __syncthreads();
-            uint32_t hw = 0;                   // bit 2k: head, bit 2k+1: write, bit 16+k: valid
-#pragma unroll
-            for (int k = 0; k < RK_ITEMS; ++k) {
-                const uint32_t pos = tid * RK_ITEMS + k;
-                if (tb + pos < nrec) {
-                    const uint64_t key = stage[pos];
-                    const uint64_t prev = pos ? stage[pos - 1] : s_prev;
-                    const bool head = (tb + pos == 0) || key_item(prev) != key_item(key);
-                    hw |= (head ? 1u : 0u) << (2 * k);
-                    hw |= key_w(key) << (2 * k + 1);
-                    hw |= 1u << (16 + k);
-                }
-            }
+        // A: aggregate of this CTA's range
+        Xf mine = OpXf::identity();
+        for (uint32_t tile = t0; tile < t1; ++tile) {
+            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
+            int dv[RK_ITEMS];
+            Xf tot;
+            block_scan_excl<Xf, OpXf>(rk_thread_map(stage, hw, D, dv), tot, sm);
+            mine = OpXf::combine(mine, tot);
+        }
+        if (tid == 0) lb_store(&cta_agg[blockIdx.x], mine);
+        grid_sync(bar);
+        // C: state entering this CTA's range = composition of the aggregates before it
+        Xf carry = OpXf::identity();
+        for (uint32_t c0 = 0; c0 < blockIdx.x; c0 += RK_THREADS) {
+            const Xf x = (c0 + tid < blockIdx.x) ? lb_load(&cta_agg[c0 + tid]) : OpXf::identity();
+            Xf tot;
+            block_scan_excl<Xf, OpXf>(x, tot, sm);
+            carry = OpXf::combine(carry, tot);
+        }
+        // D: sweep the tiles in order
+        for (uint32_t tile = t0; tile < t1; ++tile) {
+            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
+            Xf last_tot = OpXf::identity();
             for (uint32_t it = 0; it < local_max; ++it) {
                 int dv[RK_ITEMS];
-                Xf agg = OpXf::identity();
-#pragma unroll
-                for (int k = 0; k < RK_ITEMS; ++k) {
-                    dv[k] = 0;
-                    if ((hw >> (16 + k)) & 1u) {
-                        dv[k] = (int)__ldcg(&D[key_idx(stage[tid * RK_ITEMS + k])]);
-                        agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
-                    }
-                }
                 Xf tot;
-                Xf ex = block_scan_excl<Xf, OpXf>(agg, tot, sm);
-                if (it == 0) {
-                    if (warp_id() == 0) {
-                        Xf pre = lookback_warp<Xf, OpXf>(lb, tile, epoch, tot);
-                        if (lane_id() == 0) s_pre = pre;
-                    }
-                    __syncthreads();
-                }
-                Xf cur = OpXf::combine(s_pre, ex);
+                const Xf ex = block_scan_excl<Xf, OpXf>(rk_thread_map(stage, hw, D, dv), tot, sm);
+                last_tot = tot;
+                Xf cur = OpXf::combine(carry, ex);
                 bool chg = false;
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k) {
@@ -298,6 +335,7 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
                 if (!__syncthreads_or(chg)) break;
                 if (tid == 0) s_chg = 1;
             }
+            carry = OpXf::combine(carry, last_tot);
         }
         __syncthreads();
         if (tid == 0 && s_chg) sc[SC_CHG0 + pass % 3] = 1;

@@ -554,10 +554,13 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
+    // in-tile sweeps per rank pass, measured per schema (profiles/round1_tuning.md):
+    // TM-1 chains are subscriber-local (sweeps close them on chip), TPC-C's cross tiles
+    db->rank_local = schema == S_TM1 ? 16 : schema == S_TPCB ? 4 : 1;
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
-    db->kset_q = schema == S_TPCC ? 32 : 128;
+    db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 32 : 256;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     int kg = 0;
     if (schema == S_TPCB)

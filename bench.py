@@ -175,6 +175,17 @@ def dist_setup(args):
     return ws, rank, local, pg
 
 
+def reduce_max(dist, x: float, dev=None) -> float:
+    """Max of x over ranks (device time of the slowest rank); identity at N = 1."""
+    if dist is None:
+        return x
+    import torch
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def make_inputs(wl, rank: int, steps: int, seed: int):
     dims = wl["dims"]
     image = W.make_db(wl["schema"], dims, seed=seed + 1000 * rank)
@@ -308,11 +319,7 @@ def main():
         return ms, stats
 
     def max_over_ranks(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(dist, x, dev)
 
     # ---- headline strategy, device-resident inputs -----------------------------------
     with Clocks(local) as clk:

@@ -173,9 +173,11 @@ gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const cha
 gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n);
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n);
 
-/* K-SET round tracing (diagnostics): when on, the executor records the device time
- * (ns, %globaltimer) at which CTA 0 starts each round; gputx_read_round_ns copies the
- * first `rounds` (<= n) entries of the last K-SET execute.  ESTATE if tracing was off. */
+/* K-SET round tracing (diagnostics): when on, the executor records device times (ns,
+ * %globaltimer) per round k: [8k] CTA 0 starts, [8k+1] CTA 0 has signalled, [8k+2] and
+ * [8k+3] the same for CTA 1 (0 if it did not take part), [8k+4], [8k+5] polls CTA 0 / 1
+ * spent waiting for round k-1.  gputx_read_round_ns copies 8 * rounds u64 (rounds <= n)
+ * of the last K-SET execute.  ESTATE if tracing was off. */
 gputx_status gputx_trace_rounds(gputx_db* db, int on);
 gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds);
 

@@ -157,6 +157,7 @@ struct gputx_db {
     int rank_grid = 0, kset_grid = 0;
     uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
+    uint32_t kset_diag = 0;    // GPUTX_KSET_DIAG (diagnostics): 1 skip bodies, 8 skip prefetch, 128 hand-off skeleton
     uint32_t exec_grid_override = 0;
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
@@ -334,20 +335,21 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     // rounds
     {
         const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
+        uint32_t* done = db->d_done;
         kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, db->kset_q,
-                                                                         db->d_g, db->d_done);
+                                                                         db->d_g, done);
         ++db->launches;
         DevDb vv = v;
         const uint32_t* perm = db->d_perm;
         const uint32_t* off = db->d_goff;
         const uint16_t* gk = db->d_g;
-        uint32_t* done = db->d_done;
         const uint32_t* sc = db->d_sc;
         uint32_t TT = T;
         const uint8_t* pt = db->d_ptype;
         const uint32_t* pp = db->d_pp;
         uint64_t* trace = db->trace_rounds ? db->d_trace : nullptr;
-        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace};
+        uint32_t diag = db->kset_diag;
+        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace, &diag};
         TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
         ++db->launches;
     }
@@ -524,7 +526,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_D, NB)) || (st = dalloc(db, &db->d_perm, NB)) ||
         (st = dalloc(db, &db->d_g, NB + 1)) || (st = dalloc(db, &db->d_done, NB + 1)) ||
         (st = dalloc(db, &db->d_ptype, NB)) || (st = dalloc(db, &db->d_pp, NB * 8)) ||
-        (st = dalloc(db, &db->d_trace, NB + 1)) ||
+        (st = dalloc(db, &db->d_trace, 8 * (NB + 1))) ||
         (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
@@ -562,6 +564,8 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
     db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 32 : 256;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
+    if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
+    if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);
     int kg = 0;
     if (schema == S_TPCB)
         kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>, kset_block<S_TPCB>(), 0);
@@ -880,7 +884,7 @@ gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds) 
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->trace_rounds || !db->has_perm) return fail(db, GPUTX_ESTATE, "round tracing off or no K-SET bulk");
     if (rounds > db->n) return fail(db, GPUTX_EINVAL, "more rounds than transactions");
-    if (rounds) CK(cudaMemcpy(host, db->d_trace, rounds * 8, cudaMemcpyDeviceToHost));
+    if (rounds) CK(cudaMemcpy(host, db->d_trace, rounds * 8 * 8, cudaMemcpyDeviceToHost));
     return GPUTX_OK;
 }
 

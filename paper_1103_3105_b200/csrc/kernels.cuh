@@ -492,7 +492,8 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                                                                const uint32_t* __restrict__ off, uint32_t T,
                                                                const uint16_t* __restrict__ g, uint32_t* done,
                                                                const uint32_t* sc, const uint8_t* __restrict__ ptype,
-                                                               const uint32_t* __restrict__ pp, uint64_t* trace) {
+                                                               const uint32_t* __restrict__ pp, uint64_t* trace,
+                                                               uint32_t diag) {
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
     // prefetched first slice of the round this CTA executes next
@@ -540,6 +541,26 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         l = soff[kk - cb];
         h = soff[kk - cb + 1];
     };
+    if (diag & 128u) {                 // hand-off skeleton only (diagnostics)
+        for (uint32_t kk = 0; kk < nk; ++kk) {
+            const uint32_t gg = __ldg(&g[kk]);
+            if (b >= gg) continue;
+            if (kk > 0) {
+                if (tid == 0) {
+                    const uint32_t need = __ldg(&g[kk - 1]);
+                    while (ld_acquire(&done[kk - 1]) < need) { }
+                }
+                __syncthreads();
+            }
+            if (trace && b == 0 && tid == 0) trace[8 * kk] = globaltimer_ns();
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(&done[kk], 1u);
+            }
+        }
+        return;
+    }
     uint32_t k = 0;
     // find this CTA's first round
     while (k < nk && G(k) <= b) ++k;
@@ -560,11 +581,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                     uint32_t spins = 0;
                     while (ld_acquire(&done[k - 1]) < need)
                         if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
+                    if (trace && b < 2) trace[8 * k + 4 + b] = spins;
                 }
                 __syncthreads();
             }
         }
-        if (trace && b == 0 && tid == 0) trace[k] = globaltimer_ns();
+        if (trace && b < 2 && tid == 0) trace[8 * k + 2 * b] = globaltimer_ns();
         // take the prefetched slice, then prefetch this CTA's next round
         const uint32_t cidx = nidx, ct = nt;
         uint32_t cp[PW > 0 ? PW : 1];
@@ -576,13 +598,13 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         if (k2 < nk) {
             bounds(k2, lo, hi);
             slice(lo, hi, G(k2), lo, hi);
-            prefetch(lo, hi);
+            if (!(diag & 8u)) prefetch(lo, hi);
         }
-        if (cidx != 0xFFFFFFFFu) {
+        if (cidx != 0xFFFFFFFFu && !(diag & 1u)) {
             if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
             else exec_txn<S>(db, cidx);
         }
-        for (uint32_t j = clo + KB + tid; j < chi; j += KB) {
+        for (uint32_t j = (diag & 1u) ? chi : clo + KB + tid; j < chi; j += KB) {
             if (PW > 0) {
                 uint32_t q[PW > 0 ? PW : 1];
 #pragma unroll
@@ -602,6 +624,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             __threadfence();
             atomicAdd(&done[k], 1u);
         }
+        if (trace && b < 2 && tid == 0) trace[8 * k + 2 * b + 1] = globaltimer_ns();
         prev = k;
         gprev = gk;
         k = k2;

@@ -258,9 +258,10 @@ class Database:
         self._check(self.lib.gputx_trace_rounds(self.h, int(on)), self.h)
 
     def round_ns(self, rounds: int) -> np.ndarray:
-        a = np.zeros(max(1, rounds), np.uint64)
+        """(rounds, 8) u64: CTA0 start, CTA0 signalled, CTA1 start, CTA1 signalled, polls0, polls1."""
+        a = np.zeros(max(1, rounds) * 8, np.uint64)
         self._check(self.lib.gputx_read_round_ns(self.h, a.ctypes.data, rounds), self.h)
-        return a[:rounds]
+        return a[:rounds * 8].reshape(rounds, 8)
 
     def reset(self):
         self._check(self.lib.gputx_reset(self.h), self.h)

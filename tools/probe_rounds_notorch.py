@@ -3,7 +3,7 @@ import sys
 import time
 
 import numpy as np
-import torch
+
 
 sys.path.insert(0, ".")
 import workloads as W  # noqa: E402

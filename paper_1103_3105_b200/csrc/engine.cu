@@ -336,8 +336,9 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     {
         const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
         uint32_t* done = db->d_done;
+        if (db->kset_diag & 16u) CK(cudaMemsetAsync(done, 0, db->n * 4, s));
         kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, db->kset_q,
-                                                                         db->d_g, done);
+                                                                         db->d_g, (db->kset_diag & 16u) ? nullptr : done);
         ++db->launches;
         DevDb vv = v;
         const uint32_t* perm = db->d_perm;
@@ -759,7 +760,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     gputx_status r = GPUTX_OK;
     if (n) {
         CK(cudaMemsetAsync(db->d_status, 0, n, s));
-        if (db->schema != S_TPCB) CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
+        if (db->schema != S_TPCB && !(db->kset_diag & 4096u)) CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
         if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
         else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
         else r = execute_schema<S_TPCC>(db, st);

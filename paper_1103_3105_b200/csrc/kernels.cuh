@@ -480,7 +480,7 @@ __global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, 
         const uint32_t s = off[(k + 1) * T] - off[k * T];
         uint32_t c = (s + per_cta - 1) / per_cta;
         g[k] = (uint16_t)(c < 1 ? 1 : (c > G ? G : c));
-        done[k] = 0;
+        if (done) done[k] = 0;
     }
 }
 

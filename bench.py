@@ -129,7 +129,15 @@ class Clocks:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.time(), ln.strip()))
+
+    def wait_first(self, timeout: float = 5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self):
+        return time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -139,10 +147,18 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0: float = 0.0, t1: float = float("inf")):
+        """Median SM clock and active throttle reasons of the samples taken in [t0, t1]
+        (all samples if the window caught none: nvidia-smi samples every 100 ms)."""
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inwin = [ln for t, ln in self.lines if t0 <= t <= t1]
+        window = "timed region"
+        if not inwin:
+            # nearest samples around the window
+            inwin = [ln for t, ln in self.lines if t0 - 0.5 <= t <= t1 + 0.5] or [ln for _, ln in self.lines]
+            window = "around the timed region"
+        for ln in inwin:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -155,7 +171,7 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 # --------------------------------------------------------------------------------------
@@ -281,6 +297,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
+    clk = Clocks(local).__enter__()                      # sampling starts now, ends after the e2e loop
     image, bulks = make_inputs(wl, rank, max(args.steps, 1), args.seed)
     n = wl["n"]
     cap = 3 * (args.warmup + args.steps) + 8          # bulks the merged insert tables must hold
@@ -304,6 +321,8 @@ def main():
             step_dev(k, strategy)
         torch.cuda.synchronize()
         barrier()
+        clk.wait_first()
+        window[0] = time.time()
         ms, stats = [], []
         for k in range(steps):
             flush.fill_(k & 0xFF)                        # L2 flush, outside the timed window
@@ -315,15 +334,18 @@ def main():
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
         torch.cuda.synchronize()
+        window[1] = time.time()
         barrier()
         return ms, stats
+
+    window = [0.0, 0.0]
 
     def max_over_ranks(x: float) -> float:
         return reduce_max(dist, x, dev)
 
     # ---- headline strategy, device-resident inputs -----------------------------------
-    with Clocks(local) as clk:
-        ms, stats = timed(args.strategy, args.steps, args.warmup)
+    ms, stats = timed(args.strategy, args.steps, args.warmup)
+    clocks = clk.summary(*window)
     total_ms = max_over_ranks(sum(ms))
     value = ws * n * args.steps / (total_ms / 1e3)
     launches = int(sum(s["launches"] for s in stats))
@@ -396,7 +418,7 @@ def main():
                "sample": f"{runs} bulk(s) x {n} txns of the same workload, serial loop {secs:.2f} s",
                "cpu": cpu_model(), "nproc": os.cpu_count()}
 
-    clocks = clk.summary()
+    clk.__exit__()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

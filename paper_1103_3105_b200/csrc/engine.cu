@@ -159,6 +159,7 @@ struct gputx_db {
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
     uint32_t kset_diag = 0;    // GPUTX_KSET_DIAG (diagnostics): 1 skip bodies, 8 skip prefetch, 128 hand-off skeleton
     uint32_t exec_grid_override = 0;
+    bool tpl_persistent = false;   // GPUTX_TPL_PERSISTENT=1: persistent per-lane tickets (slower: divergent spinners)
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
     uint64_t launches = 0;     // kernels launched since the last submit
@@ -400,8 +401,18 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v) {
         ++db->launches;
     cudaEventRecord(db->ev[4], s);
     cudaEventRecord(db->ev[5], s);
-    const uint32_t tb = 128;
-    tpl_exec_kernel<S><<<(uint32_t)((db->n + tb - 1) / tb), tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+    if (db->tpl_persistent) {
+        // grid = what is co-resident (every ticket holder must be running)
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tpl_exec_persistent_kernel<S>, 256, 0);
+        const uint32_t grid = (uint32_t)std::max(1, per) * (uint32_t)db->nsm;
+        tpl_exec_persistent_kernel<S><<<std::min<uint64_t>(grid, (db->n + 255) / 256), 256, 0, s>>>(
+            v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+    } else {
+        const uint32_t tb = 128;
+        tpl_exec_kernel<S><<<(uint32_t)((db->n + tb - 1) / tb), tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock,
+                                                                            db->d_sc);
+    }
     ++db->launches;
     cudaEventRecord(db->ev[6], s);
     return GPUTX_OK;
@@ -566,6 +577,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 32 : 256;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
+    if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
     if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);
     int kg = 0;
     if (schema == S_TPCB)

@@ -736,7 +736,39 @@ __global__ void __launch_bounds__(RK_THREADS) tpl_keys_kernel(const uint64_t* __
     }
 }
 
-constexpr uint32_t SPIN_LIMIT = 1u << 26;
+constexpr uint32_t SPIN_LIMIT = 1u << 24;   // polls before the watchdog trips (EDEADLOCK)
+
+// Enter a counter lock: wait until *lw >= key.  Warp-aggregated acquisition: the lanes
+// of a warp currently waiting on the same lock word share one poll (one leader load,
+// broadcast).  A waiter sleeps in proportion to the releases it still needs
+// (key - value), so a deep queue behind a hot lock does not flood L2 with polls.
+// Only lanes already in the loop take part in the collectives (__activemask), and
+// no lane waits inside a collective for another lane's release: ITS lets a lane whose
+// lock is free leave, execute and release while its siblings keep polling.
+DEV bool tpl_acquire(uint32_t* lw, uint32_t key) {
+    if (ld_acquire(lw) >= key) return true;          // uncontended: no collective
+    uint32_t polls = 0;
+    for (;;) {
+        const uint32_t am = __activemask();
+        const uint32_t peers = __match_any_sync(am, (unsigned long long)lw);
+        const int leader = __ffs(peers) - 1;
+        uint32_t v = 0;
+        if ((int)lane_id() == leader) v = ld_acquire(lw);
+        v = __shfl_sync(peers, v, leader);
+        if (v >= key) return true;
+        if (++polls > SPIN_LIMIT) return false;
+        const uint32_t gap = key - v;
+        if (gap > 1) __nanosleep(min(gap * 32u, 2048u));
+        else if (polls > 8) __nanosleep(32);
+    }
+}
+
+// Release +1 on a lock word; lanes releasing the same word combine into one atomic.
+DEV void tpl_release(uint32_t* lw) {
+    const uint32_t am = __activemask();
+    const uint32_t peers = __match_any_sync(am, (unsigned long long)lw);
+    if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(lw, (uint32_t)__popc(peers));
+}
 
 template <int S>
 __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
@@ -752,17 +784,42 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
     // growing phase: enter every lock in turn (keys order conflicting records by ts)
     for (int j = 0; j < k; ++j) {
         const uint32_t key = __ldg(&lkey[ro + j]);
-        uint32_t* lw = &lock[r[j].item];
-        uint32_t spins = 0;
-        while (ld_acquire(lw) < key) {
-            if (++spins > SPIN_LIMIT) { atomicExch(&sc[SC_DEADLOCK], 1u); break; }
-            if (spins > 64) __nanosleep(64);
-        }
+        if (!tpl_acquire(&lock[r[j].item], key)) atomicExch(&sc[SC_DEADLOCK], 1u);
     }
     exec_txn<S>(db, idx);
     __threadfence();
     // shrinking phase
-    for (int j = 0; j < k; ++j) atomicAdd(&lock[r[j].item], 1u);
+    for (int j = 0; j < k; ++j) tpl_release(&lock[r[j].item]);
+}
+
+// Persistent TPL: every lane takes its next transaction as soon as it has released the
+// previous one (warp-aggregated ticket grab, tickets in ts order).  A lane holding
+// ticket t waits only for transactions with smaller tickets, all of which were taken
+// by running lanes, so the grid (sized to what is co-resident) always progresses, and
+// no slot idles behind a slow sibling of its CTA.
+template <int S>
+__global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
+                                                                  const uint32_t* __restrict__ lkey, uint32_t* lock,
+                                                                  uint32_t* sc) {
+    for (;;) {
+        const uint32_t am = __activemask();
+        const int leader = __ffs(am) - 1;
+        uint32_t base = 0;
+        if ((int)lane_id() == leader) base = atomicAdd(&sc[SC_TICKET], (uint32_t)__popc(am));
+        base = __shfl_sync(am, base, leader);
+        const uint32_t idx = base + __popc(am & lanemask_lt());
+        if (idx >= db.n) break;
+        Rec r[MAX_REC];
+        const int k = footprint<S>(db, db.type[idx], db.pw + db.poff[idx], r);
+        const uint32_t ro = rec_off[idx];
+        for (int j = 0; j < k; ++j) {
+            const uint32_t key = __ldg(&lkey[ro + j]);
+            if (!tpl_acquire(&lock[r[j].item], key)) atomicExch(&sc[SC_DEADLOCK], 1u);
+        }
+        exec_txn<S>(db, idx);
+        __threadfence();
+        for (int j = 0; j < k; ++j) tpl_release(&lock[r[j].item]);
+    }
 }
 
 }  // namespace gputx

@@ -160,6 +160,7 @@ struct gputx_db {
     uint32_t kset_diag = 0;    // GPUTX_KSET_DIAG (diagnostics): 1 skip bodies, 8 skip prefetch, 128 hand-off skeleton
     uint32_t exec_grid_override = 0;
     bool tpl_persistent = false;   // GPUTX_TPL_PERSISTENT=1: persistent per-lane tickets (slower: divergent spinners)
+    uint32_t kset_cluster = 8;     // CTAs per thread-block cluster of the K-SET executor
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
     uint64_t launches = 0;     // kernels launched since the last submit
@@ -335,7 +336,8 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
-        const uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
+        uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
+        if (db->kset_cluster) G = std::max(db->kset_cluster, G / db->kset_cluster * db->kset_cluster);
         uint32_t* done = db->d_done;
         if (db->kset_diag & 16u) CK(cudaMemsetAsync(done, 0, db->n * 4, s));
         kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, db->kset_q,
@@ -351,8 +353,41 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         const uint32_t* pp = db->d_pp;
         uint64_t* trace = db->trace_rounds ? db->d_trace : nullptr;
         uint32_t diag = db->kset_diag;
-        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace, &diag};
-        TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
+        uint32_t C = db->kset_cluster;
+        if (diag & 64u) {                 // diagnostics: run on freshly allocated metadata buffers
+            static uint16_t* fg = nullptr;
+            static uint32_t *fdone = nullptr, *foff = nullptr;
+            static uint64_t fcap = 0;
+            if (fcap < db->n * T + 2) {
+                cudaFree(fg); cudaFree(fdone); cudaFree(foff);
+                fcap = db->n * T + 2;
+                cudaMalloc(&fg, fcap * 2); cudaMalloc(&fdone, fcap * 4); cudaMalloc(&foff, fcap * 4);
+            }
+            cudaMemcpyAsync(fg, db->d_g, db->n * 2, cudaMemcpyDeviceToDevice, s);
+            cudaMemsetAsync(fdone, 0, db->n * 4, s);
+            cudaMemcpyAsync(foff, db->d_goff, (db->n * T + 1) * 4, cudaMemcpyDeviceToDevice, s);
+            gk = fg; done = fdone; off = foff;
+        }
+        void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace, &diag, &C};
+        if (C) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(G);
+            lc.blockDim = dim3(kset_block<S>());
+            lc.stream = s;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = C;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeCooperative;
+            at[1].val.cooperative = 1;
+            lc.attrs = at;
+            lc.numAttrs = 2;
+            cudaError_t e = cudaLaunchKernelExC(&lc, kset_fn<S>(), args);
+            if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
+        } else {
+            TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
+        }
         ++db->launches;
     }
     cudaEventRecord(db->ev[6], s);
@@ -574,19 +609,47 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
-    db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 32 : 256;
+    db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 128 : 256;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
+    // K-SET executor: thread-block clusters of kset_cluster CTAs (rounds of <= that many
+    // CTAs are separated by the hardware cluster barrier); 0 disables clusters
+    if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
+    const void* kfn = schema == S_TPCB  ? (const void*)kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>
+                      : schema == S_TM1 ? (const void*)kset_exec_kernel<S_TM1, kset_pw<S_TM1>(), kset_block<S_TM1>()>
+                                        : (const void*)kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>(), kset_block<S_TPCC>()>;
+    const int kblock = schema == S_TPCB ? kset_block<S_TPCB>() : schema == S_TM1 ? kset_block<S_TM1>()
+                                                                                 : kset_block<S_TPCC>();
+    {
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kblock, 0);
+        db->kset_grid = std::max(1, per) * db->nsm;
+    }
+    if (db->kset_cluster) {
+        if (db->kset_cluster > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(db->kset_grid);
+        lc.blockDim = dim3(kblock);
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = db->kset_cluster;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        lc.attrs = &at;
+        lc.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &lc) != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            db->kset_cluster = 0;            // no cluster support: counter hand-offs only
+        } else {
+            db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
+        }
+    }
     if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);
-    int kg = 0;
-    if (schema == S_TPCB)
-        kg = coop_grid(db, kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>, kset_block<S_TPCB>(), 0);
-    else if (schema == S_TM1)
-        kg = coop_grid(db, kset_exec_kernel<S_TM1, kset_pw<S_TM1>(), kset_block<S_TM1>()>, kset_block<S_TM1>(), 0);
-    else
-        kg = coop_grid(db, kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>(), kset_block<S_TPCC>()>, kset_block<S_TPCC>(), 0);
-    db->kset_grid = kg;
+    if (getenv("GPUTX_DEBUG"))
+        fprintf(stderr, "gputx: schema %d kset grid %d block %d cluster %u Q %u rank grid %d local %u\n", schema,
+                db->kset_grid, kblock, db->kset_cluster, db->kset_q, db->rank_grid, db->rank_local);
     if (cudaStreamSynchronize(db->stream) != cudaSuccess) return bail(GPUTX_ECUDA);
     *out = db;
     return GPUTX_OK;

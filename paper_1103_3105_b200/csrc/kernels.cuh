@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                                                                const uint16_t* __restrict__ g, uint32_t* done,
                                                                const uint32_t* sc, const uint8_t* __restrict__ ptype,
                                                                const uint32_t* __restrict__ pp, uint64_t* trace,
-                                                               uint32_t diag) {
+                                                               uint32_t diag, uint32_t cluster_c) {
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
     // prefetched first slice of the round this CTA executes next
@@ -561,9 +561,17 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         }
         return;
     }
+    // Round classes.  With a cluster launch (C > 0) a round of g <= C CTAs is "narrow":
+    // it is run by cluster 0 (CTAs 0..C-1, only the first g hold work) and consecutive
+    // narrow rounds are separated by the hardware cluster barrier alone.  A "wide"
+    // round (g > C, or any round without clusters) is run by CTAs 0..g-1, which wait for
+    // the previous round's signals on done[k-1] and signal done[k] when done.
+    const uint32_t C = cluster_c;
+    auto narrow = [&](uint32_t kk) -> bool { return C && G(kk) <= C; };
+    auto part = [&](uint32_t kk) -> bool { return narrow(kk) ? b < C : b < G(kk); };
+    auto nsig = [&](uint32_t kk) -> uint32_t { return narrow(kk) ? C : G(kk); };   // signals of round kk
     uint32_t k = 0;
-    // find this CTA's first round
-    while (k < nk && G(k) <= b) ++k;
+    while (k < nk && !part(k)) ++k;                      // this CTA's first round
     if (k >= nk) return;
     uint32_t lo, hi;
     bounds(k, lo, hi);
@@ -572,12 +580,13 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     uint32_t prev = 0xFFFFFFFFu, gprev = 0;   // last round this CTA executed, its CTA count
     while (k < nk) {
         const uint32_t gk = G(k);
-        // wait for round k-1
-        if (k > 0) {
-            const bool mine = (prev == k - 1) && gprev == 1;
+        const bool nar = narrow(k);
+        // wait for round k-1 (nothing to wait for after a narrow round: cluster barrier)
+        if (k > 0 && !(nar && narrow(k - 1))) {
+            const bool mine = !C && (prev == k - 1) && gprev == 1;
             if (!mine) {
                 if (tid == 0) {
-                    const uint32_t need = prev == k - 1 ? gprev : __ldg(&g[k - 1]);
+                    const uint32_t need = nsig(k - 1);
                     uint32_t spins = 0;
                     while (ld_acquire(&done[k - 1]) < need)
                         if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
@@ -594,7 +603,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         for (int w = 0; w < (PW > 0 ? PW : 1); ++w) cp[w] = np[w];
         const uint32_t clo = lo, chi = hi;
         uint32_t k2 = k + 1;
-        while (k2 < nk && G(k2) <= b) ++k2;
+        while (k2 < nk && !part(k2)) ++k2;
         if (k2 < nk) {
             bounds(k2, lo, hi);
             slice(lo, hi, G(k2), lo, hi);
@@ -617,12 +626,21 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                 exec_txn<S>(db, __ldg(&perm[j]));
             }
         }
-        __syncthreads();
-        // CTA 0 runs every round; for it k2 == k + 1, which is in the staged chunk
-        const bool next_shared = b > 0 || ((k + 1 < nk) && G(k + 1) > 1);
-        if (tid == 0 && (gk > 1 || next_shared)) {
-            __threadfence();
-            atomicAdd(&done[k], 1u);
+        if (nar) {
+            // all C CTAs of cluster 0: release their writes to each other, acquire theirs
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            if (k + 1 < nk && !narrow(k + 1) && tid == 0) {          // a wide round follows
+                __threadfence();
+                atomicAdd(&done[k], 1u);
+            }
+        } else {
+            __syncthreads();
+            // without clusters CTA 0 runs every round; for it k2 == k + 1
+            const bool next_shared = b > 0 || C || ((k + 1 < nk) && G(k + 1) > 1);
+            if (tid == 0 && (gk > 1 || next_shared)) {
+                __threadfence();
+                atomicAdd(&done[k], 1u);
+            }
         }
         if (trace && b < 2 && tid == 0) trace[8 * k + 2 * b + 1] = globaltimer_ns();
         prev = k;

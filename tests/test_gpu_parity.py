@@ -1,6 +1,8 @@
 """GPU parity: the CUDA path through the C ABI vs the oracle (Definition 1,
 PAPER.md:73), bit-exact on final database, statuses, outputs and inserted rows,
 for TPL / PART / K-SET on TPC-B, TM-1 and TPC-C."""
+import os
+
 import numpy as np
 import pytest
 
@@ -91,12 +93,16 @@ def test_grid_shape_independence(strategy):
     image = W.tm1_db(dims, seed=1)
     bulk = W.tm1_bulk(dims, 20_000, seed=2)
     ref = oracle.run(W.TM1, dims.dims, image, bulk)
-    for grid, narrow in [(1, 0), (7, 0), (0, 0)]:
-        db = gpu_db(W.TM1, dims, image, bulk.n)
-        db.set_launch(exec_grid=grid, narrow_max=narrow)
+    for grid, cluster in [(1, "0"), (7, "0"), (8, "8"), (16, "8"), (0, "8"), (0, "16")]:
+        os.environ["GPUTX_KSET_CLUSTER"] = cluster
+        try:
+            db = gpu_db(W.TM1, dims, image, bulk.n)
+        finally:
+            os.environ.pop("GPUTX_KSET_CLUSTER", None)
+        db.set_launch(exec_grid=grid)
         db.submit(bulk)
         db.execute(strategy)
-        compare(W.TM1, ref, db, image, label=f"grid {grid} narrow {narrow}")
+        compare(W.TM1, ref, db, image, label=f"grid {grid} cluster {cluster}")
         db.close()
 
 

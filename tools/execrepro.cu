@@ -6,6 +6,13 @@
 #include "../paper_1103_3105_b200/csrc/kernels.cuh"
 using namespace gputx;
 
+__global__ void touch(uint16_t* g, uint32_t* done, uint32_t nk, const uint16_t* src) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x) {
+        g[k] = src[k];
+        done[k] = 0;
+    }
+}
+
 int main() {
     uint32_t nk = 195;
     const uint32_t T = 7, n = 1000000;
@@ -43,11 +50,14 @@ int main() {
     }
     cudaStream_t nb;
     cudaStreamCreateWithFlags(&nb, cudaStreamNonBlocking);
-    for (uint32_t diag : {13u, 141u, 13u + 4096u, 13u + 8192u}) {
+    uint16_t* gsrc; cudaMalloc(&gsrc, nk * 2); cudaMemcpy(gsrc, hg.data(), nk * 2, cudaMemcpyHostToDevice);
+    for (uint32_t diag : {13u, 141u, 13u + 4096u, 13u + 8192u, 13u + 16384u}) {
         if (diag & 4096u) { cudaMemset(big, 1, 1ull << 30); }
         cudaMemset(done, 0, nk * 4);
+        if (diag & 16384u) touch<<<592, 256>>>(g, done, nk, gsrc);
         uint32_t TT = T;
-        void* args[] = {&db, &perm, &off, &TT, &g, &done, &sc, &ptype, &pp, &tr, &diag};
+        uint32_t C0 = 0;
+        void* args[] = {&db, &perm, &off, &TT, &g, &done, &sc, &ptype, &pp, &tr, &diag, &C0};
         cudaError_t e = cudaLaunchCooperativeKernel((void*)kset_exec_kernel<S_TM1, 8, 1024>, dim3(2), dim3(1024), args, 0,
                                                     (diag & 8192u) ? nb : (cudaStream_t)0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();

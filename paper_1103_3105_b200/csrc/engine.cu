@@ -352,6 +352,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         const uint8_t* pt = db->d_ptype;
         const uint32_t* pp = db->d_pp;
         uint64_t* trace = db->trace_rounds ? db->d_trace : nullptr;
+        if (trace) CK(cudaMemsetAsync(trace, 0, (db->n + 1) * 64, s));
         uint32_t diag = db->kset_diag;
         uint32_t C = db->kset_cluster;
         if (diag & 64u) {                 // diagnostics: run on freshly allocated metadata buffers
@@ -626,10 +627,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kblock, 0);
         db->kset_grid = std::max(1, per) * db->nsm;
     }
-    if (db->kset_cluster) {
+    while (db->kset_cluster) {
         if (db->kset_cluster > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(db->kset_grid);
+        lc.gridDim = dim3(std::max<uint32_t>(db->kset_cluster, db->kset_grid / db->kset_cluster * db->kset_cluster));
         lc.blockDim = dim3(kblock);
         cudaLaunchAttribute at;
         at.id = cudaLaunchAttributeClusterDimension;
@@ -639,12 +640,18 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         lc.attrs = &at;
         lc.numAttrs = 1;
         int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &lc) != cudaSuccess || nclusters < 1) {
+        const cudaError_t ce = cudaOccupancyMaxActiveClusters(&nclusters, kfn, &lc);
+        if (getenv("GPUTX_DEBUG"))
+            fprintf(stderr, "gputx: cluster %u query: %s, %d clusters\n", db->kset_cluster, cudaGetErrorString(ce),
+                    nclusters);
+        if (ce != cudaSuccess || nclusters < 1) {
             cudaGetLastError();
-            db->kset_cluster = 0;            // no cluster support: counter hand-offs only
-        } else {
-            db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
+            db->kset_cluster /= 2;           // try smaller clusters; 1 -> 0: counter hand-offs only
+            if (db->kset_cluster < 2) db->kset_cluster = 0;
+            continue;
         }
+        db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
+        break;
     }
     if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);
     if (getenv("GPUTX_DEBUG"))

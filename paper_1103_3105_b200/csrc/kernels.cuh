@@ -581,37 +581,54 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     while (k < nk) {
         const uint32_t gk = G(k);
         const bool nar = narrow(k);
-        // wait for round k-1 (nothing to wait for after a narrow round: cluster barrier)
-        if (k > 0 && !(nar && narrow(k - 1))) {
+        // wait for round k-1 (nothing to wait for after a narrow round: cluster barrier).
+        // g[k-1] is read from global memory: round k-1 may lie in the previous staged
+        // chunk, and a chunk reload (__syncthreads) must not happen inside tid == 0 code.
+        const uint32_t gm1 = k > 0 ? (uint32_t)__ldg(&g[k - 1]) : 0u;
+        const bool nar_m1 = C && gm1 <= C;
+        if (k > 0 && !(nar && nar_m1)) {
             const bool mine = !C && (prev == k - 1) && gprev == 1;
             if (!mine) {
                 if (tid == 0) {
-                    const uint32_t need = nsig(k - 1);
+                    const uint32_t need = nar_m1 ? C : gm1;
                     uint32_t spins = 0;
                     while (ld_acquire(&done[k - 1]) < need)
                         if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
-                    if (trace && b < 2) trace[8 * k + 4 + b] = spins;
+                    if (trace && b == 0) trace[8 * k + 4] = spins;
                 }
                 __syncthreads();
             }
         }
-        if (trace && b < 2 && tid == 0) trace[8 * k + 2 * b] = globaltimer_ns();
+        if (trace && tid == 0) {
+            const uint64_t now = globaltimer_ns();
+            if (b == 0) trace[8 * k] = now;
+            atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 5]), (unsigned long long)now);  // last start
+        }
         // take the prefetched slice, then prefetch this CTA's next round
         const uint32_t cidx = nidx, ct = nt;
         uint32_t cp[PW > 0 ? PW : 1];
 #pragma unroll
         for (int w = 0; w < (PW > 0 ? PW : 1); ++w) cp[w] = np[w];
         const uint32_t clo = lo, chi = hi;
+        // prefetch the next round's slice now only if this CTA takes part in round k+1;
+        // a longer scan for its next round happens after it has signalled this one (a
+        // CTA must never delay the round others wait for)
         uint32_t k2 = k + 1;
-        while (k2 < nk && !part(k2)) ++k2;
-        if (k2 < nk) {
+        const bool next_mine = k2 < nk && part(k2);
+        if (next_mine) {
             bounds(k2, lo, hi);
             slice(lo, hi, G(k2), lo, hi);
             if (!(diag & 8u)) prefetch(lo, hi);
         }
         if (cidx != 0xFFFFFFFFu && !(diag & 1u)) {
+            const uint64_t t0 = trace ? globaltimer_ns() : 0;
             if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
             else exec_txn<S>(db, cidx);
+            if (trace) {   // slowest transaction of the round: duration << 24 | idx
+                const uint64_t d = globaltimer_ns() - t0;
+                atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 3]),
+                          (unsigned long long)((d << 24) | cidx));
+            }
         }
         for (uint32_t j = (diag & 1u) ? chi : clo + KB + tid; j < chi; j += KB) {
             if (PW > 0) {
@@ -625,6 +642,11 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             } else {
                 exec_txn<S>(db, __ldg(&perm[j]));
             }
+        }
+        if (trace && tid == 0) {
+            const uint64_t now = globaltimer_ns();
+            if (b == 0) trace[8 * k + 6] = now;                               // CTA 0's work issued
+            atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 7]), (unsigned long long)now);  // last CTA
         }
         if (nar) {
             // all C CTAs of cluster 0: release their writes to each other, acquire theirs
@@ -642,7 +664,15 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                 atomicAdd(&done[k], 1u);
             }
         }
-        if (trace && b < 2 && tid == 0) trace[8 * k + 2 * b + 1] = globaltimer_ns();
+        if (trace && b == 0 && tid == 0) trace[8 * k + 1] = globaltimer_ns();
+        if (!next_mine) {
+            while (k2 < nk && !part(k2)) ++k2;
+            if (k2 < nk) {
+                bounds(k2, lo, hi);
+                slice(lo, hi, G(k2), lo, hi);
+                if (!(diag & 8u)) prefetch(lo, hi);
+            }
+        }
         prev = k;
         gprev = gk;
         k = k2;

@@ -35,11 +35,16 @@ sizes = np.bincount(d, minlength=nk)
 dt = np.diff(ns)
 print(f"{wl}: ksets {nk} exec_ms {st['ms_exec']:.3f} rank_ms {st['ms_rank']:.3f} passes {st['rank_passes']}")
 print("round start span ms", (ns[-1] - ns[0]) / 1e6)
-order = np.argsort(-dt)[:15]
+order = np.argsort(-dt)[:12]
 for k in order:
-    c1 = f"cta1 start {(tr[k, 2] - ns[k]) / 1e3:8.2f} sig {(tr[k, 3] - ns[k]) / 1e3:8.2f}" if tr[k, 2] else ""
-    half = (raw[k + 1, 6] - ns[k]) / 1e3 if k + 1 < nk and raw[k + 1, 6] else -1
-    print(f"  round {k:5d} size {sizes[k]:8d} dt_us {dt[k] / 1e3:8.2f} cta0 sig {(tr[k, 1] - ns[k]) / 1e3:8.2f} {c1} spins {spins[k, 1]} {spins[k, 3]} cta0 saw-first-signal {half:8.2f}")
+    st = raw[k, 5] - ns[k]; wk = raw[k, 7] - ns[k]
+    print(f"  round {k:5d} size {sizes[k]:8d} dt_us {dt[k] / 1e3:8.2f} cta0 work {(raw[k, 6] - ns[k]) / 1e3:7.2f} "
+          f"last start {st / 1e3:7.2f} last work-done {wk / 1e3:7.2f} cta0 polls {raw[k + 1, 4] if k + 1 < nk else 0}")
+    sl = int(raw[k, 3]); sidx = sl & 0xFFFFFF; sdur = (sl >> 24) / 1e3
+    print(f"        slowest txn {sidx} type {bulk.type[sidx]} {sdur:.1f} us params {bulk.params(sidx)[:8]}")
+w = np.where(raw[:, 6] > 0, raw[:, 6] - ns, 0)[:-1]
+s1 = np.where(raw[:, 1] > 0, raw[:, 1] - ns, 0)[:-1]
+print(f"  mean us: work-issued {w.mean() / 1e3:.2f} signalled {s1.mean() / 1e3:.2f} round {dt.mean() / 1e3:.2f}")
 for lo, hi in [(0, 1), (1, 33), (33, 1025), (1025, 10**9)]:
     m = (sizes[:-1] >= lo) & (sizes[:-1] < hi)
     if m.any():

@@ -61,10 +61,14 @@ struct DevDb {
 #define COL(T, k) (reinterpret_cast<T*>(db.col[(k)]))
 #define INS(T, k) (reinterpret_cast<T*>(db.ins[(k)]))
 
-// mutable column access: L2-coherent (bypass L1) so that writes of earlier k-sets /
-// lock holders on other SMs are seen
-template <class T> DEV T ldm(const T* p) { return __ldcg(p); }
-template <class T> DEV void stm(T* p, T v) { __stcg(p, v); }
+// Mutable column access.  Plain (weak) loads/stores: every strategy orders conflicting
+// accesses with acquire/release synchronisation (k-set round hand-off, cluster
+// barrier, counter-lock acquire), whose acquire side invalidates L1, so a weak load
+// after it sees the earlier writer.  (ld.global.cg compiles to LDG.E.STRONG.GPU on
+// sm_100a, and those serialise the lanes of a warp: 8 NewOrders in one warp took 10x
+// the time of 8 in 8 warps.)
+template <class T> DEV T ldm(const T* p) { return *p; }
+template <class T> DEV void stm(T* p, T v) { *p = v; }
 DEV void put32(uint8_t* o, uint32_t v) { *reinterpret_cast<uint32_t*>(o) = v; }
 DEV void put64(uint8_t* o, uint64_t v) {
     reinterpret_cast<uint32_t*>(o)[0] = (uint32_t)v;
@@ -413,6 +417,119 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
     put64(o + 8, (uint64_t)nb);
 }
 
+// Whole TPC-C transaction (K-SET, TPL) written for warp convergence: one load phase
+// with no early exit or data-dependent loop (the 15 line slots are predicated), so
+// the lanes of a warp issue all their loads together; the abort decision and the
+// writes come after.  (Lanes that diverged in the line loops with their loads
+// outstanding ran one after another: 8 NewOrders in one warp took 10x one.)
+DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
+    const bool no = t == 0;
+    const uint32_t w = p[0], d = p[1];
+    const uint32_t cnt = no ? min(p[3], 15u) : 0u;
+    uint32_t li[15], lsw[15], lq[15];
+    bool abort = !no && p[4] == 2;
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        li[l] = 0; lsw[l] = 0; lq[l] = 0;
+        if ((uint32_t)l < cnt) { li[l] = p[4 + 3 * l]; lsw[l] = p[5 + 3 * l]; lq[l] = p[6 + 3 * l]; }
+    }
+#pragma unroll
+    for (int l = 0; l < 15; ++l) abort |= ((uint32_t)l < cnt) && li[l] >= I;   // unused item: roll back
+    const bool go = !abort;
+    const uint64_t wd = (uint64_t)w * D + d;
+    // ---- load phase
+    uint32_t oid = 0;
+    int64_t disc = 0, tax = 0, cbal = 0;
+    uint8_t credit = 0;
+    uint64_t ro = 0, rn = 0, rl0 = 0, rh = 0, cx = 0;
+    uint64_t sidx[15];
+    int32_t pr[15], q0[15];
+    uint8_t br[15];
+    if (no && go) {
+        oid = ldm(&COL(uint32_t, C_D_NEXT)[wd]);
+        disc = __ldg(&COL(const int32_t, C_C_DISC)[wd * C + p[2]]);
+        tax = (int64_t)__ldg(&COL(const int32_t, C_W_TAX)[w]) + __ldg(&COL(const int32_t, C_D_TAX)[wd]);
+        ro = db.ins_base[T_ORDER] + db.ins_off[T_ORDER * (uint64_t)db.ins_stride + idx];
+        rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
+        rl0 = db.ins_base[T_OLINE] + db.ins_off[T_OLINE * (uint64_t)db.ins_stride + idx];
+    }
+#pragma unroll
+    for (int l = 0; l < 15; ++l) {
+        sidx[l] = (uint64_t)lsw[l] * I + li[l];
+        pr[l] = 0; q0[l] = 0; br[l] = 0;
+        if (no && go && (uint32_t)l < cnt) {
+            pr[l] = __ldg(&COL(const int32_t, C_I_PRICE)[li[l]]);
+            br[l] = __ldg(&COL(const uint8_t, C_I_ORIG)[li[l]]) & __ldg(&COL(const uint8_t, C_S_ORIG)[sidx[l]]);
+            q0[l] = ldm(&COL(int32_t, C_S_QTY)[sidx[l]]);
+        }
+    }
+    if (!no && go) {
+        cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
+        cbal = ldm(&COL(int64_t, C_C_BAL)[cx]);
+        credit = __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]);
+        rh = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
+    }
+    // ---- decide, then write
+    if (abort) { db.status[idx] = 1; return; }
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    if (no) {
+        stm(&COL(uint32_t, C_D_NEXT)[wd], oid + 1);
+        uint32_t all_local = 1;
+#pragma unroll
+        for (int l = 0; l < 15; ++l) all_local &= ((uint32_t)l >= cnt) || lsw[l] == w;
+        INS(uint32_t, IO_ID)[ro] = oid; INS(uint32_t, IO_D)[ro] = d; INS(uint32_t, IO_W)[ro] = w;
+        INS(uint32_t, IO_C)[ro] = p[2]; INS(uint32_t, IO_ENTRY)[ro] = db.first_ts + idx;
+        INS(uint32_t, IO_OLCNT)[ro] = cnt; INS(uint32_t, IO_ALLLOCAL)[ro] = all_local;
+        INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
+        int64_t sum = 0;
+        int32_t cur[15];
+#pragma unroll
+        for (int l = 0; l < 15; ++l) {
+            if ((uint32_t)l >= cnt) continue;
+            const int32_t q = (int32_t)lq[l];
+            const int32_t amount = q * pr[l];
+            sum += amount;
+            int32_t before = q0[l];
+#pragma unroll
+            for (int m = 0; m < l; ++m)
+                if (sidx[m] == sidx[l]) before = cur[m];      // latest earlier update of the same stock row
+            cur[l] = before >= q + 10 ? before - q : before - q + 91;
+            const uint64_t rl = rl0 + l;
+            INS(uint32_t, IL_OID)[rl] = oid; INS(uint32_t, IL_D)[rl] = d; INS(uint32_t, IL_W)[rl] = w;
+            INS(uint32_t, IL_NUM)[rl] = l; INS(uint32_t, IL_I)[rl] = li[l]; INS(uint32_t, IL_SW)[rl] = lsw[l];
+            INS(uint32_t, IL_QTY)[rl] = lq[l]; INS(int32_t, IL_AMT)[rl] = amount;
+            put32(o + 16 + 12 * l, (uint32_t)before);
+            put32(o + 16 + 12 * l + 4, (uint32_t)amount);
+            o[16 + 12 * l + 8] = br[l];
+            red_add(&COL(int64_t, C_S_YTD)[sidx[l]], (int64_t)q);
+            red_add(&COL(uint32_t, C_S_OCNT)[sidx[l]], 1u);
+            if (lsw[l] != w) red_add(&COL(uint32_t, C_S_RCNT)[sidx[l]], 1u);
+        }
+#pragma unroll
+        for (int l = 0; l < 15; ++l)
+            if ((uint32_t)l < cnt) stm(&COL(int32_t, C_S_QTY)[sidx[l]], cur[l]);
+        const int64_t x = sum * (10000 - disc) * (10000 + tax);
+        put32(o, oid);
+        put32(o + 4, cnt);
+        put64(o + 8, (uint64_t)((x + 50000000) / 100000000));
+    } else {
+        const uint32_t h = p[6];
+        red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
+        red_add(&COL(int64_t, C_D_YTD)[wd], (int64_t)h);
+        INS(uint32_t, IH_C)[rh] = p[5]; INS(uint32_t, IH_CD)[rh] = p[3]; INS(uint32_t, IH_CW)[rh] = p[2];
+        INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = db.first_ts + idx;
+        INS(int32_t, IH_AMT)[rh] = (int32_t)h;
+        const int64_t nb = cbal - (int64_t)h;
+        stm(&COL(int64_t, C_C_BAL)[cx], nb);
+        red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
+        red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
+        put32(o, p[5]);
+        put32(o + 4, credit);
+        put64(o + 8, (uint64_t)nb);
+    }
+}
+
 // The combined kernel body: one whole transaction (K-SET, TPL).
 template <int S>
 DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
@@ -422,15 +539,7 @@ DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
     } else {
-        if (t == 0) {
-            if (tpcc_no_aborts(db, p)) { db.status[idx] = 1; return; }
-            tpcc_no_home(db, idx, p);
-            tpcc_no_stock(db, idx, p, ALL_LINES);
-        } else {
-            if (p[4] == 2) { db.status[idx] = 1; return; }
-            tpcc_pay_home(db, idx, p);
-            tpcc_pay_customer(db, idx, p);
-        }
+        tpcc_txn(db, idx, t, p);
     }
 }
 

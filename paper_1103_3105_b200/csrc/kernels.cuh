@@ -649,8 +649,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 7]), (unsigned long long)now);  // last CTA
         }
         if (nar) {
-            // all C CTAs of cluster 0: release their writes to each other, acquire theirs
-            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            // Consecutive one-CTA rounds are CTA 0's alone (__syncthreads); otherwise all
+            // C CTAs of cluster 0 release their writes to each other and acquire theirs.
+            // Every CTA of the cluster takes the same decision from the same schedule.
+            const bool solo = gk == 1 && k + 1 < nk && narrow(k + 1) && G(k + 1) == 1;
+            if (solo) __syncthreads();
+            else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             if (k + 1 < nk && !narrow(k + 1) && tid == 0) {          // a wide round follows
                 __threadfence();
                 atomicAdd(&done[k], 1u);

@@ -621,10 +621,11 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             if (!(diag & 8u)) prefetch(lo, hi);
         }
         if (cidx != 0xFFFFFFFFu && !(diag & 1u)) {
-            const uint64_t t0 = trace ? globaltimer_ns() : 0;
+            const bool tt = trace && (diag & 2u);
+            const uint64_t t0 = tt ? globaltimer_ns() : 0;
             if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
             else exec_txn<S>(db, cidx);
-            if (trace) {   // slowest transaction of the round: duration << 24 | idx
+            if (tt) {   // slowest transaction of the round: duration << 24 | idx (GPUTX_KSET_DIAG=2)
                 const uint64_t d = globaltimer_ns() - t0;
                 atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 3]),
                           (unsigned long long)((d << 24) | cidx));

@@ -181,6 +181,13 @@ gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n);
 gputx_status gputx_trace_rounds(gputx_db* db, int on);
 gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds);
 
+/* Rank-pass tracing (same switch): per pass p of the last K-SET rank fixpoint, u64
+ * [8p] pass start, [8p+1] last CTA done aggregating, [8p+2] past barrier 1, [8p+3]
+ * last CTA done sweeping, [8p+4] past barrier 2 (ns, %globaltimer), [8p+5] tiles swept,
+ * [8p+6] tile sweeps.  Copies 8 * passes u64 (passes <= 1024).  ESTATE if tracing was
+ * off or the last execute was not K-SET; EINVAL for passes > 1024. */
+gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes);
+
 /* Restore the pristine image (columns and insert tables) by a device copy. */
 gputx_status gputx_reset(gputx_db* db);
 

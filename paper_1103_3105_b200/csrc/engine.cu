@@ -149,6 +149,8 @@ struct gputx_db {
     LookBack<uint32_t> lb_scan{};
     LookBack<Xf> lb_rank{};
     LookBack<Pair> lb_tpl{};
+    RkMemo rank_memo{};               // per-tile memo of the rank passes
+    uint64_t* d_rtrace = nullptr;     // rank pass phase times (diagnostics)
     SortWs sort_ws{};
     uint32_t epoch = 0;        // look-back epochs of scans / sorts / TPL keys
     uint32_t rank_epoch = 0;   // look-back epochs of rank passes (own array)
@@ -156,7 +158,9 @@ struct gputx_db {
     int nsm = 0;
     int rank_grid = 0, kset_grid = 0;
     uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
+    uint32_t rank_dirty = 1;                  // dirty-tile worklist (GPUTX_RANK_DIRTY overrides)
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
+    bool sync_stages = false;  // GPUTX_SYNC (diagnostics): synchronise and check after each stage
     uint32_t kset_diag = 0;    // GPUTX_KSET_DIAG (diagnostics): 1 skip bodies, 8 skip prefetch, 128 hand-off skeleton
     uint32_t exec_grid_override = 0;
     bool tpl_persistent = false;   // GPUTX_TPL_PERSISTENT=1: persistent per-lane tickets (slower: divergent spinners)
@@ -194,6 +198,13 @@ gputx_status dalloc(gputx_db* db, T** p, uint64_t count) {
     return GPUTX_OK;
 }
 
+#define STAGE(name)                                                                             \
+    do {                                                                                        \
+        if (db->sync_stages) {                                                                  \
+            cudaError_t e_ = cudaStreamSynchronize(db->stream);                                 \
+            if (e_ != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
+        }                                                                                       \
+    } while (0)
 #define TRY(x)                              \
     do {                                    \
         gputx_status s_ = (x);              \
@@ -295,8 +306,10 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
     TRY(emit_records<S>(db, v));
+    STAGE("emit");
     cudaEventRecord(db->ev[2], s);
     TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    STAGE("sort");
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
@@ -310,10 +323,16 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         uint32_t* sc = db->d_sc;
         uint32_t maxp = 1u << 20;
         uint32_t lmax = db->rank_local;
-        void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp, &lmax};
+        uint32_t dirty = db->rank_dirty;
+        RkMemo memo = db->rank_memo;
+        memo.rec_off = db->d_rec_off;
+        uint64_t* rtrace = db->trace_rounds ? db->d_rtrace : nullptr;
+        if (rtrace) CK(cudaMemsetAsync(rtrace, 0, RANK_TRACE_SLOTS * 8, s));
+        void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp, &lmax, &dirty, &memo, &rtrace};
         TRY(launch_coop(db, (const void*)rank_kernel, db->rank_grid, RK_THREADS, args));
         ++db->launches;
     }
+    STAGE("rank");
     cudaEventRecord(db->ev[4], s);
     // group by (depth, type)
     const uint32_t T = db->ntypes;
@@ -333,6 +352,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
                                                      db->d_perm, db->d_poff, db->d_pw, db->d_ptype, db->d_pp);
     ++db->launches;
+    STAGE("group");
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
@@ -391,6 +411,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         }
         ++db->launches;
     }
+    STAGE("kset exec");
     cudaEventRecord(db->ev[6], s);
     db->has_depth = db->has_perm = true;
     return GPUTX_OK;
@@ -589,6 +610,14 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->lb_tpl.flag, tiles)) || (st = dalloc(db, &db->lb_tpl.agg, tiles)) ||
         (st = dalloc(db, &db->lb_tpl.inc, tiles)))
         return bail(st);
+    {
+        const uint64_t rt = db->max_rec / RK_TILE + 2;
+        if ((st = dalloc(db, &db->rank_memo.aggA, rt)) || (st = dalloc(db, &db->rank_memo.carD, rt)) ||
+            (st = dalloc(db, &db->rank_memo.dirty, rt / 32 + 1)) ||
+            (st = dalloc(db, &db->rank_memo.recpos, db->max_rec + 1)) ||
+            (st = dalloc(db, &db->d_rtrace, RANK_TRACE_SLOTS)))
+            return bail(st);
+    }
     db->sort_ws.max_tiles = db->max_rec / RS_TILE + 2;
     if ((st = dalloc(db, &db->sort_ws.hist, RS_MAXPASS * 256)) ||
         (st = dalloc(db, &db->sort_ws.status, db->sort_ws.max_tiles * 256)) ||
@@ -608,12 +637,17 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // TM-1 chains are subscriber-local (sweeps close them on chip), TPC-C's cross tiles
     db->rank_local = schema == S_TM1 ? 16 : schema == S_TPCB ? 4 : 1;
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
+    // TPC-C: each pass raises most of the long W_YTD chains' suffix, so nearly every tile is
+    // dirty every pass and the marking costs more than it saves (profiles/round1.md)
+    db->rank_dirty = schema == S_TPCC ? 0 : 1;
+    if (const char* e = getenv("GPUTX_RANK_DIRTY")) db->rank_dirty = (uint32_t)atoi(e);
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
     db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 64 : 128;
     db->kset_cluster = schema == S_TPCB ? 16 : 8;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
+    db->sync_stages = getenv("GPUTX_SYNC") != nullptr;
     if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
     // K-SET executor: thread-block clusters of kset_cluster CTAs (rounds of <= that many
     // CTAs are separated by the hardware cluster barrier); 0 disables clusters
@@ -972,6 +1006,14 @@ gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds) 
     return GPUTX_OK;
 }
 
+gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes) {
+    if (!db || !host) return GPUTX_EINVAL;
+    if (!db->trace_rounds || !db->has_depth) return fail(db, GPUTX_ESTATE, "tracing off or no K-SET bulk");
+    if (passes > RANK_TRACE_SLOTS / 8) return fail(db, GPUTX_EINVAL, "too many passes");
+    if (passes) CK(cudaMemcpy(host, db->d_rtrace, passes * 64, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
 gputx_status gputx_trace_rounds(gputx_db* db, int on) {
     if (!db) return GPUTX_EINVAL;
     db->trace_rounds = on != 0;
@@ -1019,7 +1061,8 @@ void gputx_close_db(gputx_db* db) {
                   db->d_perm, db->d_g, db->d_done, db->d_ptype, db->d_pp, db->d_trace, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
                   db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
                   db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
-                  db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets};
+                  db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets, db->rank_memo.aggA,
+                  db->rank_memo.carD, db->rank_memo.dirty, db->rank_memo.recpos, db->d_rtrace};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (db->h_sc) cudaFreeHost(db->h_sc);

@@ -255,49 +255,106 @@ DEV uint32_t rk_load(const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t 
     return hw;
 }
 
-// this thread's composed map over its RK_ITEMS records (current D), and the D values
-DEV Xf rk_thread_map(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* dv) {
+// Dirty-tile worklist across the passes of one rank launch.  A tile's map aggregate
+// depends only on the depths of its records' transactions, and its sweep only on those
+// and its incoming state.  So a tile is re-swept only if one of its transactions was
+// raised since its last sweep (`dirty` bit, set by the raiser) or its incoming state
+// changed (`carD`); a clean tile reuses its memoised aggregate `aggA`.  To mark, the
+// raiser needs the tiles of all records of a transaction: `recpos` (sorted position of
+// record rec_off[t] + j), built in the prologue.
+constexpr uint32_t RANK_TRACE_SLOTS = 8 * 1024;      // 8 timestamps per pass (diagnostics)
+struct RkMemo {
+    Xf* aggA;
+    Xf* carD;
+    uint32_t* dirty;
+    uint32_t* recpos;
+    const uint32_t* rec_off;
+};
+
+DEV bool xf_eq(const Xf& a, const Xf& b) {
+    return a.aa == b.aa && a.am == b.am && a.ac == b.ac && a.ma == b.ma && a.mm == b.mm && a.mc == b.mc;
+}
+
+DEV void rk_gather(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* dv) {
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k)
+        dv[k] = ((hw >> (16 + k)) & 1u) ? (int)__ldcg(&D[key_idx(stage[threadIdx.x * RK_ITEMS + k])]) : 0;
+}
+
+DEV Xf rk_compose(uint32_t hw, const int* dv) {
     Xf agg = OpXf::identity();
 #pragma unroll
-    for (int k = 0; k < RK_ITEMS; ++k) {
-        dv[k] = 0;
-        if ((hw >> (16 + k)) & 1u) {
-            dv[k] = (int)__ldcg(&D[key_idx(stage[threadIdx.x * RK_ITEMS + k])]);
-            agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
-        }
-    }
+    for (int k = 0; k < RK_ITEMS; ++k)
+        if ((hw >> (16 + k)) & 1u) agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
     return agg;
+}
+
+DEV bool rk_is_dirty(const uint32_t* dirty, uint32_t tile) {
+    return (__ldcg(&dirty[tile >> 5]) >> (tile & 31)) & 1u;
+}
+
+// transaction t was raised by a thread sweeping tile `self`: mark the other tiles holding
+// its records (`self` is swept again until it raises nothing)
+DEV void rk_mark(const RkMemo& memo, uint32_t t, uint32_t self) {
+    __threadfence();                          // the raise is visible before the mark
+    const uint32_t r0 = __ldg(&memo.rec_off[t]), r1 = __ldg(&memo.rec_off[t + 1]);
+    for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t tl = __ldcg(&memo.recpos[r]) / RK_TILE;
+        if (tl != self && !rk_is_dirty(memo.dirty, tl)) atomicOr(&memo.dirty[tl >> 5], 1u << (tl & 31));
+    }
 }
 
 __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes,
-                                                          uint32_t local_max) {
+                                                          uint32_t local_max, uint32_t use_dirty, RkMemo memo,
+                                                          uint64_t* trace) {
+    // trace (diagnostics): per pass p, [8p] pass start (CTA 0), [8p+1] last CTA done with A,
+    // [8p+2] CTA 0 past barrier 1, [8p+3] last CTA done with D, [8p+4] CTA 0 past barrier 2,
+    // [8p+5] tiles swept, [8p+6] sweeps
+    auto tmax = [&](uint32_t pass, uint32_t slot) {
+        if (trace && threadIdx.x == 0 && pass < RANK_TRACE_SLOTS / 8)
+            atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * pass + slot]), (unsigned long long)globaltimer_ns());
+    };
     __shared__ uint64_t stage[RK_TILE];
     __shared__ Xf sm[8];
     __shared__ uint64_t s_prev;
     __shared__ int s_chg;
-    (void)epoch0;
     Xf* cta_agg = lb.agg;                  // one aggregate per CTA
     const uint32_t nrec = *nrec_ptr;
     const uint32_t ntiles = (nrec + RK_TILE - 1) / RK_TILE;
     const uint32_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const uint32_t t0 = min(ntiles, blockIdx.x * per), t1 = min(ntiles, t0 + per);
     const uint32_t tid = threadIdx.x;
+    // prologue (complete before the first marks, which come after pass 0's barriers)
+    for (uint64_t p = (uint64_t)t0 * RK_TILE + tid; p < min((uint64_t)t1 * RK_TILE, (uint64_t)nrec); p += RK_THREADS) {
+        const uint64_t k = __ldg(&keys[p]);
+        memo.recpos[__ldg(&memo.rec_off[key_idx(k)]) + key_j(k)] = (uint32_t)p;
+    }
     for (uint32_t pass = 0;; ++pass) {
+        const bool all = pass < 2 || !use_dirty;   // passes 0 and 1 sweep everything; marks start in pass 1
         if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (pass + 1) % 3] = 0;
+        if (blockIdx.x == 0) tmax(pass, 0);
         if (tid == 0) s_chg = 0;
         // A: aggregate of this CTA's range
         Xf mine = OpXf::identity();
         for (uint32_t tile = t0; tile < t1; ++tile) {
-            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
-            int dv[RK_ITEMS];
             Xf tot;
-            block_scan_excl<Xf, OpXf>(rk_thread_map(stage, hw, D, dv), tot, sm);
+            // the bit can be set concurrently by other CTAs: one thread reads it for the CTA
+            if (!all && !__syncthreads_or(tid == 0 && rk_is_dirty(memo.dirty, tile))) {
+                tot = memo.aggA[tile];
+            } else {
+                const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
+                int dv[RK_ITEMS];
+                rk_gather(stage, hw, D, dv);
+                block_scan_excl<Xf, OpXf>(rk_compose(hw, dv), tot, sm);
+            }
             mine = OpXf::combine(mine, tot);
         }
         if (tid == 0) lb_store(&cta_agg[blockIdx.x], mine);
+        tmax(pass, 1);
         grid_sync(bar);
+        if (blockIdx.x == 0) tmax(pass, 2);
         // C: state entering this CTA's range = composition of the aggregates before it
         Xf carry = OpXf::identity();
         for (uint32_t c0 = 0; c0 < blockIdx.x; c0 += RK_THREADS) {
@@ -307,39 +364,82 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
             carry = OpXf::combine(carry, tot);
         }
         // D: sweep the tiles in order
+        uint32_t swept = 0, sweeps = 0;
         for (uint32_t tile = t0; tile < t1; ++tile) {
-            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
+            const bool dirty = all || __syncthreads_or(tid == 0 && rk_is_dirty(memo.dirty, tile));
+            if (!dirty && xf_eq(carry, memo.carD[tile])) {       // same inputs and state: settled
+                carry = OpXf::combine(carry, memo.aggA[tile]);
+                continue;
+            }
+            if (tid == 0) {
+                if (dirty) atomicAnd(&memo.dirty[tile >> 5], ~(1u << (tile & 31)));
+                __threadfence();           // clear before gathering: a later raise re-marks
+            }
+            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);   // (syncs the CTA)
+            ++swept;
             Xf last_tot = OpXf::identity();
+            bool settled = false;
+            uint32_t raised = 0;           // bit k: record k's transaction raised in this tile
             for (uint32_t it = 0; it < local_max; ++it) {
+                ++sweeps;
                 int dv[RK_ITEMS];
+                rk_gather(stage, hw, D, dv);
                 Xf tot;
-                const Xf ex = block_scan_excl<Xf, OpXf>(rk_thread_map(stage, hw, D, dv), tot, sm);
+                const Xf ex = block_scan_excl<Xf, OpXf>(rk_compose(hw, dv), tot, sm);
                 last_tot = tot;
                 Xf cur = OpXf::combine(carry, ex);
-                bool chg = false;
+                int L[RK_ITEMS];
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k) {
+                    L[k] = 0;
                     if ((hw >> (16 + k)) & 1u) {
                         const bool head = (hw >> (2 * k)) & 1u;
                         const uint32_t w = (hw >> (2 * k + 1)) & 1u;
                         const int d = dv[k];
                         const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
-                        const int L = w ? max(d, m + 1) : max(d, a + 1);
-                        if (L > d) {
-                            const uint32_t old = atomicMax(&D[key_idx(stage[tid * RK_ITEMS + k])], (uint32_t)L);
-                            chg |= old < (uint32_t)L;
-                        }
+                        L[k] = w ? max(d, m + 1) : max(d, a + 1);
                         cur = OpXf::combine(cur, rec_xf(head, w, d));
                     }
                 }
-                if (!__syncthreads_or(chg)) break;
+                uint32_t old[RK_ITEMS];    // all raises in flight together
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k)
+                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[tid * RK_ITEMS + k])], (uint32_t)L[k])
+                                          : 0xFFFFFFFFu;
+                bool chg = false;
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k)
+                    if (old[k] < (uint32_t)L[k]) { chg = true; raised |= 1u << k; }
+                if (!__syncthreads_or(chg)) {
+                    // this sweep raised nothing: its aggregate and incoming state are the
+                    // tile's fixpoint until a record's transaction is raised
+                    if (tid == 0) { memo.carD[tile] = carry; memo.aggA[tile] = tot; }
+                    settled = true;
+                    break;
+                }
                 if (tid == 0) s_chg = 1;
+            }
+            if (!settled && tid == 0) {    // sweep cap hit: sweep again next pass
+                memo.aggA[tile] = last_tot;
+                atomicOr(&memo.dirty[tile >> 5], 1u << (tile & 31));
+            }
+            if (use_dirty && pass >= 1 && raised) {     // mark the other tiles of the raised transactions
+                __threadfence();           // the raises are visible before the marks
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k)
+                    if ((raised >> k) & 1u) rk_mark(memo, key_idx(stage[tid * RK_ITEMS + k]), tile);
             }
             carry = OpXf::combine(carry, last_tot);
         }
         __syncthreads();
         if (tid == 0 && s_chg) sc[SC_CHG0 + pass % 3] = 1;
+        if (trace && tid == 0 && pass < RANK_TRACE_SLOTS / 8) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 5]), (unsigned long long)swept);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 6]), (unsigned long long)sweeps);
+        }
+        tmax(pass, 3);
         grid_sync(bar);
+        if (blockIdx.x == 0) tmax(pass, 4);
         const uint32_t c = __ldcg(&sc[SC_CHG0 + pass % 3]);
         if (!c || pass + 1 >= max_passes) {
             if (blockIdx.x == 0 && tid == 0) {

@@ -88,6 +88,7 @@ def load_library():
         "gputx_set_launch": ([P, U32, U32, U32], I),
         "gputx_trace_rounds": ([P, I], I),
         "gputx_read_round_ns": ([P, P, U64], I),
+        "gputx_read_rank_ns": ([P, P, U64], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -101,7 +102,8 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_submit_bulk", "gputx_execute", "gputx_read_results", "gputx_results_device",
             "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
-            "gputx_set_launch", "gputx_trace_rounds", "gputx_read_round_ns"]
+            "gputx_set_launch", "gputx_trace_rounds", "gputx_read_round_ns",
+            "gputx_read_rank_ns"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -262,6 +264,12 @@ class Database:
         a = np.zeros(max(1, rounds) * 8, np.uint64)
         self._check(self.lib.gputx_read_round_ns(self.h, a.ctypes.data, rounds), self.h)
         return a[:rounds * 8].reshape(rounds, 8)
+
+    def rank_ns(self, passes: int) -> np.ndarray:
+        """(passes, 8) u64: start, A done, past bar 1, D done, past bar 2, tiles swept, sweeps."""
+        a = np.zeros(max(1, passes) * 8, np.uint64)
+        self._check(self.lib.gputx_read_rank_ns(self.h, a.ctypes.data, passes), self.h)
+        return a[:passes * 8].reshape(passes, 8)
 
     def reset(self):
         self._check(self.lib.gputx_reset(self.h), self.h)

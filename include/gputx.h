@@ -85,6 +85,8 @@ typedef struct {
     int device;               /* CUDA device ordinal                                                */
     void* stream;             /* cudaStream_t to order all work on; NULL => a library-owned stream  */
     uint32_t flags;           /* reserved, 0                                                        */
+    uint32_t shard;           /* this handle's shard in [0, nshards)                                */
+    uint32_t nshards;         /* 0 or 1: unsharded; 2..8: one handle per GPU, see "Sharding" below  */
 } gputx_db_config;
 
 typedef struct {
@@ -94,6 +96,8 @@ typedef struct {
     uint64_t n;
     int on_device;              /* 0: host pointers (copied H2D at submit);
                                    1: device pointers already resident in HBM           */
+    const uint32_t* ts;         /* u32[n] global timestamps, strictly increasing, or NULL
+                                   (then ts = first_ts + i); REQUIRED sharded */
 } gputx_bulk;
 
 typedef struct {
@@ -148,7 +152,8 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* s
 
 /* Copy the last executed bulk's results to host: status u8[n] (may be NULL) and the
  * output records (n * gputx_out_stride bytes; out may be NULL).  ECAPACITY if out_bytes
- * is short, ESTATE before the first execute. */
+ * is short, ESTATE before the first execute.  Sharded: the n home transactions passed to
+ * gputx_shard_pack, in that order, after gputx_shard_return_merge. */
 gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes);
 
 /* Device pointers to the last bulk's status u8[n] and output records; valid until the
@@ -187,6 +192,37 @@ gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds);
  * [8p+6] tile sweeps.  Copies 8 * passes u64 (passes <= 1024).  ESTATE if tracing was
  * off or the last execute was not K-SET; EINVAL for passes > 1024. */
 gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes);
+
+/* ---- Sharding (multi-GPU) ----------------------------------------------
+ * Tables are partitioned by root key (TPC-B branch, TPC-C warehouse, TM-1 subscriber):
+ * shard r owns roots [ceil(r*R/G), ceil((r+1)*R/G)) of R, so root x lives on x*G/R.  Each
+ * handle holds the whole image but only its roots are ever read or written; the union of
+ * the shards' roots is the database.  A cross-shard transaction is split into fragments
+ * with no data flow between them (PART's split, DESIGN.md R-S9), each run on the shard
+ * that owns its root: every shard runs its fragments in global ts order, which projects
+ * the serial order onto its items, so the union equals serial execution (Definition 1).
+ * Per bulk, every shard calls, in this order (the caller moves the buffers between
+ * shards, e.g. NCCL all-to-all over NVLink):
+ *   1. gputx_shard_pack(db, home, send, cap, counts): stage the home bulk (transactions
+ *      whose home root is local, global ts required) and write, for every other shard q,
+ *      counts[q] records [ts, type, len, params, 0-padding] (gputx_shard_stride(schema, 0)
+ *      u32 words each) to the device buffer send, grouped by q in increasing q, each group
+ *      in ts order.  counts: host u64[nshards].  ECAPACITY if cap (records) is short.
+ *   2. gputx_shard_submit(db, recv, n_recv, &n_local): recv = the records the peers sent
+ *      to this shard (device, any order of groups); the local bulk is home + received
+ *      transactions in ts order.  ECROSS if a home transaction's root is not local.
+ *   3. gputx_execute (any strategy; ranks and locks are shard-local).
+ *   4. gputx_shard_return_pack(db, send, cap, counts): the outputs of the peers'
+ *      transactions, [ts, out words] (gputx_shard_stride(schema, 1) words), grouped by
+ *      home shard.
+ *   5. gputx_shard_return_merge(db, recv, n_recv): OR the returned fragment outputs into
+ *      the home records (fragments write disjoint fields).  Then gputx_read_results. */
+uint32_t gputx_shard_stride(gputx_schema schema, int result);
+gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* home, uint32_t* send, uint64_t send_cap,
+                              uint64_t* counts);
+gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_recv, uint64_t* n_local);
+gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send_cap, uint64_t* counts);
+gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64_t n_recv);
 
 /* Restore the pristine image (columns and insert tables) by a device copy. */
 gputx_status gputx_reset(gputx_db* db);

@@ -168,6 +168,18 @@ struct gputx_db {
     cudaEvent_t ev[8] = {};
     bool has_depth = false, has_perm = false;
     uint64_t launches = 0;     // kernels launched since the last submit
+    // timestamps and shards
+    uint32_t* d_ts = nullptr;        // global ts per bulk position (when has_ts)
+    bool has_ts = false;
+    uint32_t nshards = 1, shard = 0, nroot = 1, root_lo = 0, root_hi = 1;
+    uint32_t* d_src = nullptr;       // sharded: home-bulk index or NOT_HOME
+    uint32_t* d_home_pos = nullptr;  // sharded: bulk position of home transaction i
+    uint8_t* d_xflag = nullptr;      // sharded: has a fragment on another shard
+    uint8_t* s_type = nullptr;       // sharded: staged home bulk (gputx_shard_pack)
+    uint32_t *s_poff = nullptr, *s_pw = nullptr, *s_ts = nullptr;
+    uint8_t *d_hstatus = nullptr, *d_hout = nullptr;   // sharded: home results in home order
+    uint64_t nh = 0;                 // sharded: home transactions staged / in the bulk
+    bool staged = false, returned = false;
 };
 
 namespace {
@@ -255,6 +267,14 @@ DevDb make_devdb(gputx_db* db) {
     v.name_sorted = db->d_name_sorted;
     v.name_off = db->d_name_off;
     v.part_size = db->part_size;
+    v.nshards = db->nshards;
+    v.shard = db->shard;
+    v.nroot = db->nroot;
+    v.root_lo = db->root_lo;
+    v.root_hi = db->root_hi;
+    v.ts = db->has_ts ? db->d_ts : nullptr;
+    v.src = db->nshards > 1 ? db->d_src : nullptr;
+    v.xflag = db->nshards > 1 ? db->d_xflag : nullptr;
     return v;
 }
 
@@ -283,7 +303,10 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 // parameter words staged in registers by the K-SET executor (0: read from HBM)
 template <int S> constexpr int kset_pw() { return S == S_TPCB ? 4 : S == S_TM1 ? 8 : 0; }
 template <int S> constexpr int kset_block() { return S == S_TPCC ? 256 : KX_THREADS; }
-template <int S> const void* kset_fn() { return (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>()>; }
+template <int S> const void* kset_fn(bool sh) {
+    return sh ? (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), true>
+              : (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), false>;
+}
 template <int S>
 gputx_status emit_records(gputx_db* db, const DevDb& v) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
@@ -404,10 +427,10 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
             at[1].val.cooperative = 1;
             lc.attrs = at;
             lc.numAttrs = 2;
-            cudaError_t e = cudaLaunchKernelExC(&lc, kset_fn<S>(), args);
+            cudaError_t e = cudaLaunchKernelExC(&lc, kset_fn<S>(db->has_ts), args);
             if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
         } else {
-            TRY(launch_coop(db, kset_fn<S>(), (int)G, kset_block<S>(), args));
+            TRY(launch_coop(db, kset_fn<S>(db->has_ts), (int)G, kset_block<S>(), args));
         }
         ++db->launches;
     }
@@ -458,17 +481,18 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v) {
         ++db->launches;
     cudaEventRecord(db->ev[4], s);
     cudaEventRecord(db->ev[5], s);
+    const bool sh = db->has_ts;
     if (db->tpl_persistent) {
         // grid = what is co-resident (every ticket holder must be running)
         int per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tpl_exec_persistent_kernel<S>, 256, 0);
-        const uint32_t grid = (uint32_t)std::max(1, per) * (uint32_t)db->nsm;
-        tpl_exec_persistent_kernel<S><<<std::min<uint64_t>(grid, (db->n + 255) / 256), 256, 0, s>>>(
-            v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tpl_exec_persistent_kernel<S, true>, 256, 0);
+        const uint32_t grid = std::min<uint64_t>((uint32_t)std::max(1, per) * (uint32_t)db->nsm, (db->n + 255) / 256);
+        if (sh) tpl_exec_persistent_kernel<S, true><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        else tpl_exec_persistent_kernel<S, false><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
     } else {
-        const uint32_t tb = 128;
-        tpl_exec_kernel<S><<<(uint32_t)((db->n + tb - 1) / tb), tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock,
-                                                                            db->d_sc);
+        const uint32_t tb = 128, grid = (uint32_t)((db->n + tb - 1) / tb);
+        if (sh) tpl_exec_kernel<S, true><<<grid, tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        else tpl_exec_kernel<S, false><<<grid, tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
     }
     ++db->launches;
     cudaEventRecord(db->ev[6], s);
@@ -488,8 +512,63 @@ void launch_ingest(gputx_db* db, uint32_t n_words) {
     DevDb v = make_devdb(db);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, db->type_mask, db->d_ins_off,
-                                                (uint32_t)(db->n + 1), db->d_sc);
+                                                (uint32_t)(db->n + 1), db->d_sc, db->d_xflag);
                                                 ++db->launches;
+}
+
+gputx_status submit_check(gputx_db* db, const gputx_bulk* b) {
+    if (!db->sealed) return fail(db, GPUTX_ESTATE, "submit before seal");
+    if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is already submitted");
+    if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
+    if (b->n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
+    if (b->n && (!b->type || !b->param_off || !b->param_words)) return GPUTX_EINVAL;
+    return GPUTX_OK;
+}
+
+// the bulk is in d_type / d_poff / d_pw (/ d_ts, d_src): validate it, resolve the split
+// lookups, count insert rows
+gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words) {
+    cudaStream_t s = db->stream;
+    db->n = n;
+    db->launches = 0;
+    db->has_depth = db->has_perm = false;
+    db->executed = false;
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    const bool ins_scan = db->schema == S_TPCC || db->has_ts;
+    const int ntab = db->schema == S_TPCC ? 4 : 1;
+    if (n) {
+        if (ins_scan) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * ntab, s));
+        if (db->nshards > 1) CK(cudaMemsetAsync(db->d_xflag, 0, n, s));
+        if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words);
+        else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words);
+        else launch_ingest<S_TPCC>(db, n_words);
+        if (ins_scan && db->schema != S_TM1)
+            for (int t = 0; t < ntab; ++t)
+                scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n,
+                         db->d_sc + SC_INS0 + t);
+    }
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_ERR]) {
+        static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
+                                     "parameter out of range", "bad param_off", "timestamps not increasing",
+                                     "home partition not owned by this shard"};
+        const uint32_t e = db->h_sc[SC_ERR];
+        db->n = 0;
+        return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : e == E_OWNER ? GPUTX_ECROSS : GPUTX_EINVAL,
+                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 8 ? e : 0]);
+    }
+    // insert rows this bulk will append (decisions are static: two-phase procedures)
+    for (auto& t : db->ins) {
+        t.pending = (db->schema == S_TPCB && !db->has_ts) ? n : db->h_sc[SC_INS0 + t.table_id];
+        if (t.rows + t.pending > t.cap) {
+            db->n = 0;
+            return fail(db, GPUTX_ECAPACITY, "insert table " + t.name + " full; reset or raise insert_capacity");
+        }
+    }
+    db->submitted = true;
+    return GPUTX_OK;
 }
 
 Col* find_col(gputx_db* db, const char* name) {
@@ -530,6 +609,13 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->max_bulk = cfg->max_bulk;
     db->out_stride = gputx_out_stride(cfg->schema);
     db->part_size = cfg->part_size ? cfg->part_size : 128;
+    db->nshards = cfg->nshards ? cfg->nshards : 1;
+    db->shard = cfg->shard;
+    if (db->nshards > MAX_SHARDS || db->shard >= db->nshards) { delete db; return GPUTX_EINVAL; }
+    db->nroot = d[0];                       // branches / subscribers / warehouses
+    if (db->nroot < db->nshards) { delete db; return GPUTX_EINVAL; }
+    db->root_lo = (uint32_t)(((uint64_t)db->shard * db->nroot + db->nshards - 1) / db->nshards);
+    db->root_hi = (uint32_t)(((uint64_t)(db->shard + 1) * db->nroot + db->nshards - 1) / db->nshards);
     auto bail = [&](gputx_status s) { *out = db; gputx_close_db(db); *out = nullptr; return s; };
     if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(GPUTX_ECUDA);
     cudaDeviceGetAttribute(&db->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -599,7 +685,15 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_gcnt, NB * db->ntypes + 2)) || (st = dalloc(db, &db->d_goff, NB * db->ntypes + 2)) ||
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
-        (st = dalloc(db, &db->d_bar, 1)) || (st = dalloc(db, &db->d_tickets, 256)))
+        (st = dalloc(db, &db->d_bar, 1)) || (st = dalloc(db, &db->d_tickets, 256)) ||
+        (st = dalloc(db, &db->d_ts, NB + 1)))
+        return bail(st);
+    if (db->nshards > 1 &&
+        ((st = dalloc(db, &db->d_src, NB + 1)) || (st = dalloc(db, &db->d_home_pos, NB + 1)) ||
+         (st = dalloc(db, &db->d_xflag, NB + 1)) || (st = dalloc(db, &db->s_type, NB + 1)) ||
+         (st = dalloc(db, &db->s_poff, NB + 1)) || (st = dalloc(db, &db->s_pw, db->max_words + 16)) ||
+         (st = dalloc(db, &db->s_ts, NB + 1)) || (st = dalloc(db, &db->d_hstatus, NB + 1)) ||
+         (st = dalloc(db, &db->d_hout, NB * db->out_stride + 16))))
         return bail(st);
     // look-back state: sized for the largest tiled pass
     // (>= 4096 entries: the rank kernel also keeps one aggregate per CTA here)
@@ -652,9 +746,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // K-SET executor: thread-block clusters of kset_cluster CTAs (rounds of <= that many
     // CTAs are separated by the hardware cluster barrier); 0 disables clusters
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
-    const void* kfn = schema == S_TPCB  ? (const void*)kset_exec_kernel<S_TPCB, kset_pw<S_TPCB>(), kset_block<S_TPCB>()>
-                      : schema == S_TM1 ? (const void*)kset_exec_kernel<S_TM1, kset_pw<S_TM1>(), kset_block<S_TM1>()>
-                                        : (const void*)kset_exec_kernel<S_TPCC, kset_pw<S_TPCC>(), kset_block<S_TPCC>()>;
+    // (sized on the plain variant; the explicit-ts / sharded variant gets the same attributes)
+    const void* kfn = schema == S_TPCB ? kset_fn<S_TPCB>(false) : schema == S_TM1 ? kset_fn<S_TM1>(false)
+                                                                                  : kset_fn<S_TPCC>(false);
     const int kblock = schema == S_TPCB ? kset_block<S_TPCB>() : schema == S_TM1 ? kset_block<S_TM1>()
                                                                                  : kset_block<S_TPCC>();
     {
@@ -663,7 +757,12 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         db->kset_grid = std::max(1, per) * db->nsm;
     }
     while (db->kset_cluster) {
-        if (db->kset_cluster > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (db->kset_cluster > 8) {
+            const void* kfn_ts = schema == S_TPCB ? kset_fn<S_TPCB>(true) : schema == S_TM1 ? kset_fn<S_TM1>(true)
+                                                                                           : kset_fn<S_TPCC>(true);
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(kfn_ts, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(std::max<uint32_t>(db->kset_cluster, db->kset_grid / db->kset_cluster * db->kset_cluster));
         lc.blockDim = dim3(kblock);
@@ -810,11 +909,8 @@ gputx_status gputx_register_types(gputx_db* db, const uint32_t* ids, uint32_t k)
 
 gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
     if (!db || !b) return GPUTX_EINVAL;
-    if (!db->sealed) return fail(db, GPUTX_ESTATE, "submit before seal");
-    if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is already submitted");
-    if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
-    if (b->n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
-    if (b->n && (!b->type || !b->param_off || !b->param_words)) return GPUTX_EINVAL;
+    if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "sharded handle: submit with gputx_shard_pack + gputx_shard_submit");
+    TRY(submit_check(db, b));
     cudaStream_t s = db->stream;
     const uint64_t n = b->n;
     uint32_t n_words = 0;
@@ -823,47 +919,177 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
         else n_words = b->param_off[n];
     }
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
-    if (db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
-    db->n = n;
-    db->launches = 0;
-    db->has_depth = db->has_perm = false;
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    if (!b->ts && db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
+    db->has_ts = b->ts != nullptr;
     if (n) {
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
         CK(cudaMemcpyAsync(db->d_poff, b->param_off, (n + 1) * 4, kind, s));
         if (n_words) CK(cudaMemcpyAsync(db->d_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
-        if (db->schema == S_TPCC) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * 4, s));
-        db->first_ts = db->next_ts;
-        if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words);
-        else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words);
-        else launch_ingest<S_TPCC>(db, n_words);
-        if (db->schema == S_TPCC)
-            for (int t = 0; t < 4; ++t)
-                scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n, db->d_sc + 20 + t);
+        if (b->ts) CK(cudaMemcpyAsync(db->d_ts, b->ts, n * 4, kind, s));
+    }
+    db->first_ts = db->next_ts;
+    TRY(finish_submit(db, n, n_words));
+    if (!b->ts) db->next_ts += n;
+    if (first_ts) *first_ts = db->first_ts;
+    return GPUTX_OK;
+}
+
+uint32_t gputx_shard_stride(gputx_schema schema, int result) {
+    if (result) return 1 + gputx_out_stride(schema) / 4;
+    return schema == GPUTX_TPCB ? 3 + 4 : schema == GPUTX_TM1 ? 3 + 7 : schema == GPUTX_TPCC ? 3 + 49 : 0;
+}
+
+gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send, uint64_t send_cap, uint64_t* counts) {
+    if (!db || !b || !counts) return GPUTX_EINVAL;
+    if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
+    TRY(submit_check(db, b));
+    if (b->n && !b->ts) return fail(db, GPUTX_EINVAL, "sharded bulks need global timestamps (gputx_bulk.ts)");
+    cudaStream_t s = db->stream;
+    const uint64_t n = b->n;
+    uint32_t n_words = 0;
+    if (n) {
+        if (b->on_device) CK(cudaMemcpy(&n_words, b->param_off + n, 4, cudaMemcpyDeviceToHost));
+        else n_words = b->param_off[n];
+    }
+    if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
+    const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    if (n) {
+        const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(db->s_type, b->type, n, kind, s));
+        CK(cudaMemcpyAsync(db->s_poff, b->param_off, (n + 1) * 4, kind, s));
+        if (n_words) CK(cudaMemcpyAsync(db->s_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
+        CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
+        const DevDb v = make_devdb(db);
+        const uint32_t g = grid_for(n, 256, 148 * 8);
+        if (db->schema == S_TPCB) shard_count_kernel<S_TPCB><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
+        else if (db->schema == S_TM1) shard_count_kernel<S_TM1><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
+        else shard_count_kernel<S_TPCC><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
+        scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, n, db->d_sc + SC_XTOTAL);
+        if (db->schema == S_TPCB) shard_pair_kernel<S_TPCB><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_rec_off, db->d_rec_a, db->d_sc);
+        else if (db->schema == S_TM1) shard_pair_kernel<S_TM1><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_rec_off, db->d_rec_a, db->d_sc);
+        else shard_pair_kernel<S_TPCC><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_rec_off, db->d_rec_a, db->d_sc);
+        db->launches += 2;
+        const uint64_t* pairs = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL,
+                                               std::min<uint64_t>(n * (db->nshards - 1), db->max_rec), 32,
+                                               bits_for(db->nshards - 1), db->sort_ws, db->epoch, s);
+        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t np = db->h_sc[SC_XTOTAL];
+        for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
+        if (np > send_cap) return fail(db, GPUTX_ECAPACITY, "send buffer holds " + std::to_string(send_cap) +
+                                                                 " records, need " + std::to_string(np));
+        if (np) {
+            if (!send) return GPUTX_EINVAL;
+            shard_pack_kernel<<<grid_for(np, 256, 148 * 8), 256, 0, s>>>(pairs, db->d_sc + SC_XTOTAL, db->s_type,
+                                                                         db->s_poff, db->s_pw, db->s_ts, stride, send);
+            ++db->launches;
+        }
+    } else {
+        for (uint32_t q = 0; q < SC_COUNT; ++q) db->h_sc[q] = 0;
+    }
+    for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
+    db->nh = n;
+    db->staged = true;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_recv, uint64_t* n_local) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_pack first");
+    if (n_recv && !recv) return GPUTX_EINVAL;
+    const uint64_t n = db->nh + n_recv;
+    if (n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "home + received transactions exceed max_bulk");
+    cudaStream_t s = db->stream;
+    const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
+    uint32_t n_words = 0;
+    if (n) {
+        const uint32_t g = grid_for(n, 256, 148 * 8);
+        const uint32_t nh = (uint32_t)db->nh;
+        merge_keys_kernel<<<g, 256, 0, s>>>(db->s_ts, nh, recv, (uint32_t)n_recv, stride, db->d_rec_a);
+        CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+        uint32_t nn = (uint32_t)n;
+        CK(cudaMemcpyAsync(db->d_sc + SC_XTOTAL, &nn, 4, cudaMemcpyHostToDevice, s));
+        const uint64_t* keys = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL, n, 32, 32, db->sort_ws,
+                                              db->epoch, s);
+        merge_meta_kernel<<<g, 256, 0, s>>>(keys, nn, nh, db->s_type, db->s_poff, db->s_ts, recv, stride, db->d_type,
+                                            db->d_ts, db->d_src, db->d_home_pos, db->d_cnt);
+        scan_u32(db, db->d_cnt, db->d_poff, nullptr, n, db->d_sc + SC_XTOTAL);
+        merge_params_kernel<<<g, 256, 0, s>>>(keys, nn, nh, db->s_poff, db->s_pw, recv, stride, db->d_poff, db->d_pw);
+        db->launches += 4 + 4;
+        CK(cudaMemcpyAsync(&n_words, db->d_sc + SC_XTOTAL, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
+    }
+    db->has_ts = true;
+    db->staged = false;
+    db->returned = false;
+    TRY(finish_submit(db, n, n_words));
+    if (n_local) *n_local = n;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send_cap, uint64_t* counts) {
+    if (!db || !counts) return GPUTX_EINVAL;
+    if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
+    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    cudaStream_t s = db->stream;
+    const uint32_t ow = db->out_stride / 4;
+    CK(cudaMemsetAsync(db->d_sc + SC_DEST0, 0, MAX_SHARDS * 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_XTOTAL, 0, 4, s));
+    if (db->n) {
+        const uint32_t g = grid_for(db->n, 256, 148 * 8);
+        const DevDb v = make_devdb(db);
+        ret_count_kernel<<<g, 256, 0, s>>>(db->d_src, (uint32_t)db->n, db->d_cnt);
+        scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_XTOTAL);
+        if (db->schema == S_TPCB) ret_pair_kernel<S_TPCB><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a, db->d_sc);
+        else if (db->schema == S_TM1) ret_pair_kernel<S_TM1><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a, db->d_sc);
+        else ret_pair_kernel<S_TPCC><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a, db->d_sc);
+        const uint64_t* pairs = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL, db->n, 32,
+                                               bits_for(db->nshards - 1), db->sort_ws, db->epoch, s);
+        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint64_t np = db->h_sc[SC_XTOTAL];
+        for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
+        if (np > send_cap) return fail(db, GPUTX_ECAPACITY, "send buffer holds " + std::to_string(send_cap) +
+                                                                 " records, need " + std::to_string(np));
+        if (np) {
+            if (!send) return GPUTX_EINVAL;
+            ret_pack_kernel<<<grid_for(np, 256, 148 * 8), 256, 0, s>>>(pairs, db->d_sc + SC_XTOTAL, db->d_ts,
+                                                                       db->d_out, ow, send);
+        }
+    } else {
+        for (uint32_t q = 0; q < SC_COUNT; ++q) db->h_sc[q] = 0;
+    }
+    for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64_t n_recv) {
+    if (!db) return GPUTX_EINVAL;
+    if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
+    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    if (n_recv && !recv) return GPUTX_EINVAL;
+    cudaStream_t s = db->stream;
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    if (n_recv) {
+        ret_merge_kernel<<<grid_for(n_recv, 256, 148 * 8), 256, 0, s>>>(recv, (uint32_t)n_recv, db->out_stride / 4,
+                                                                         db->d_ts, db->d_src, (uint32_t)db->n,
+                                                                         db->d_out, db->d_sc);
+    }
+    if (db->nh) {
+        home_gather_kernel<<<grid_for(db->nh, 256, 148 * 8), 256, 0, s>>>(db->d_home_pos, (uint32_t)db->nh,
+                                                                           db->d_status, db->d_out, db->out_stride,
+                                                                           db->d_hstatus, db->d_hout);
     }
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (db->h_sc[SC_ERR]) {
-        static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
-                                     "parameter out of range", "bad param_off"};
-        const uint32_t e = db->h_sc[SC_ERR];
-        db->n = 0;
-        return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
-                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 6 ? e : 0]);
-    }
-    // insert rows this bulk will append (decisions are static: two-phase procedures)
-    for (auto& t : db->ins) {
-        t.pending = db->schema == S_TPCB ? n : db->h_sc[20 + t.table_id];
-        if (t.rows + t.pending > t.cap) {
-            db->n = 0;
-            return fail(db, GPUTX_ECAPACITY, "insert table " + t.name + " full; reset or raise insert_capacity");
-        }
-    }
-    db->next_ts += n;
-    if (first_ts) *first_ts = db->first_ts;
-    db->submitted = true;
+    if (db->h_sc[SC_ERR])
+        return fail(db, GPUTX_EINVAL, "returned result " + std::to_string(db->h_sc[SC_BADIDX]) +
+                                          " matches no home transaction");
+    db->returned = true;
     return GPUTX_OK;
 }
 
@@ -938,12 +1164,14 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
 }
 
 gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes) {
-    if (!db) return GPUTX_EINVAL;
-    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
-    const uint64_t need = db->n * db->out_stride;
+    const uint8_t* ds = nullptr;
+    const void* dout = nullptr;
+    uint64_t n = 0;
+    TRY(gputx_results_device(db, &ds, &dout, &n));
+    const uint64_t need = n * db->out_stride;
     if (out && out_bytes < need) return fail(db, GPUTX_ECAPACITY, "output buffer too small");
-    if (status && db->n) CK(cudaMemcpyAsync(status, db->d_status, db->n, cudaMemcpyDeviceToHost, db->stream));
-    if (out && db->n) CK(cudaMemcpyAsync(out, db->d_out, need, cudaMemcpyDeviceToHost, db->stream));
+    if (status && n) CK(cudaMemcpyAsync(status, ds, n, cudaMemcpyDeviceToHost, db->stream));
+    if (out && n) CK(cudaMemcpyAsync(out, dout, need, cudaMemcpyDeviceToHost, db->stream));
     CK(cudaStreamSynchronize(db->stream));
     return GPUTX_OK;
 }
@@ -951,6 +1179,13 @@ gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64
 gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const void** out, uint64_t* n) {
     if (!db) return GPUTX_EINVAL;
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    if (db->nshards > 1) {
+        if (!db->returned) return fail(db, GPUTX_ESTATE, "sharded: gputx_shard_return_merge first");
+        if (status) *status = db->d_hstatus;
+        if (out) *out = db->d_hout;
+        if (n) *n = db->nh;
+        return GPUTX_OK;
+    }
     if (status) *status = db->d_status;
     if (out) *out = db->d_out;
     if (n) *n = db->n;
@@ -1062,7 +1297,9 @@ void gputx_close_db(gputx_db* db) {
                   db->d_tickets, db->lb_scan.flag, db->lb_scan.agg, db->lb_scan.inc, db->lb_rank.flag,
                   db->lb_rank.agg, db->lb_rank.inc, db->lb_tpl.flag, db->lb_tpl.agg, db->lb_tpl.inc,
                   db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets, db->rank_memo.aggA,
-                  db->rank_memo.carD, db->rank_memo.dirty, db->rank_memo.recpos, db->d_rtrace};
+                  db->rank_memo.carD, db->rank_memo.dirty, db->rank_memo.recpos, db->d_rtrace, db->d_ts,
+                  db->d_src, db->d_home_pos, db->d_xflag, db->s_type, db->s_poff, db->s_pw, db->s_ts,
+                  db->d_hstatus, db->d_hout};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (db->h_sc) cudaFreeHost(db->h_sc);

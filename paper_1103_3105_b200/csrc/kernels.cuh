@@ -17,10 +17,11 @@ namespace gputx {
 // ---- device scalar slots (u32) -------------------------------------------------------
 enum {
     SC_ERR = 0, SC_BADIDX, SC_NREC, SC_NFRAG, SC_MAXD, SC_ZERO, SC_PASSES, SC_CHG0, SC_CHG1, SC_CHG2,
-    SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV,
+    SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV, SC_XTOTAL,
     SC_COUNT = 32
 };
-enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5 };
+enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7 };
+constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -38,10 +39,14 @@ DEV void report_err(uint32_t* sc, uint32_t code, uint32_t idx) {
 // =====================================================================================
 template <int S>
 __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uint32_t n_words, uint32_t type_mask,
-                                                     uint32_t* ins_cnt, uint32_t ins_stride, uint32_t* sc) {
+                                                     uint32_t* ins_cnt, uint32_t ins_stride, uint32_t* sc,
+                                                     uint8_t* xflag) {
     const uint32_t n = db.n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t t = db.type[i];
+        // sharded: a peer's transaction (NOT_HOME) only runs its fragments on this shard
+        const bool home = !db.src || db.src[i] != NOT_HOME;
+        if (db.ts && i + 1 < n && db.ts[i] >= db.ts[i + 1]) { report_err(sc, E_TS, i); continue; }
         const uint32_t o0 = db.poff[i], o1 = db.poff[i + 1];
         if (i == 0 && o0 != 0) { report_err(sc, E_OFF, i); continue; }
         if (i == n - 1 && o1 != n_words) { report_err(sc, E_OFF, i); continue; }
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                     abort |= p[4 + 3 * l] >= I;
                 }
                 if (bad) { report_err(sc, E_RANGE, i); continue; }
-                if (!abort) {
+                if (!abort && home) {
                     ins_cnt[T_ORDER * ins_stride + i] = 1;
                     ins_cnt[T_NEWORDER * ins_stride + i] = 1;
                     ins_cnt[T_OLINE * ins_stride + i] = cnt;
@@ -116,8 +121,15 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                 } else if (p[5] >= C) {
                     report_err(sc, E_RANGE, i); continue;
                 }
-                if (p[4] != 2) ins_cnt[T_HIST * ins_stride + i] = 1;
+                if (p[4] != 2 && home) ins_cnt[T_HIST * ins_stride + i] = 1;
             }
+        }
+        if (S == S_TPCB && db.ts) ins_cnt[i] = home ? 1u : 0u;   // history rows via ins_off
+        if (db.nshards > 1) {
+            // the home root must be this shard's iff the transaction was submitted here
+            const uint64_t root = S == S_TPCB ? p[2] : S == S_TPCC ? p[0] : (uint64_t)(p[0] ? p[0] - 1 : db.root_lo);
+            if (home != root_local(db, root)) { report_err(sc, E_OWNER, i); continue; }
+            xflag[i] = (!home || fragments_local<S>(db, i, nullptr) != fragments<S>(db, i, nullptr)) ? 1 : 0;
         }
     }
 }
@@ -169,7 +181,7 @@ template <int S>
 __global__ void __launch_bounds__(256) emit_count_kernel(DevDb db, uint32_t* cnt) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
         Rec r[MAX_REC];
-        cnt[i] = footprint<S>(db, db.type[i], db.pw + db.poff[i], r);
+        cnt[i] = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
     }
 }
 
@@ -177,7 +189,7 @@ template <int S>
 __global__ void __launch_bounds__(256) emit_write_kernel(DevDb db, const uint32_t* __restrict__ off, uint64_t* keys) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
         Rec r[MAX_REC];
-        const int k = footprint<S>(db, db.type[i], db.pw + db.poff[i], r);
+        const int k = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
         uint64_t* dst = keys + off[i];
         for (int j = 0; j < k; ++j) dst[j] = make_key(r[j].item, i, j, r[j].w);
     }
@@ -587,7 +599,7 @@ __global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, 
 constexpr int KX_THREADS = 1024;
 constexpr uint32_t KX_CH = 2048;      // rounds staged per shared-memory chunk
 
-template <int S, int PW, int KB>
+template <int S, int PW, int KB, bool SH>
 __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t* __restrict__ perm,
                                                                const uint32_t* __restrict__ off, uint32_t T,
                                                                const uint16_t* __restrict__ g, uint32_t* done,
@@ -723,8 +735,8 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         if (cidx != 0xFFFFFFFFu && !(diag & 1u)) {
             const bool tt = trace && (diag & 2u);
             const uint64_t t0 = tt ? globaltimer_ns() : 0;
-            if (PW > 0) exec_txn_p<S>(db, cidx, ct, cp);
-            else exec_txn<S>(db, cidx);
+            if (PW > 0) exec_txn_p<S, SH>(db, cidx, ct, cp);
+            else exec_txn<S, SH>(db, cidx);
             if (tt) {   // slowest transaction of the round: duration << 24 | idx (GPUTX_KSET_DIAG=2)
                 const uint64_t d = globaltimer_ns() - t0;
                 atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * k + 3]),
@@ -739,9 +751,9 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                     const uint4 v = __ldg(reinterpret_cast<const uint4*>(pp + (uint64_t)j * PW + w));
                     q[w] = v.x; q[w + 1] = v.y; q[w + 2] = v.z; q[w + 3] = v.w;
                 }
-                exec_txn_p<S>(db, __ldg(&perm[j]), __ldg(&ptype[j]), q);
+                exec_txn_p<S, SH>(db, __ldg(&perm[j]), __ldg(&ptype[j]), q);
             } else {
-                exec_txn<S>(db, __ldg(&perm[j]));
+                exec_txn<S, SH>(db, __ldg(&perm[j]));
             }
         }
         if (trace && tid == 0) {
@@ -790,12 +802,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
 template <int S>
 __global__ void __launch_bounds__(256) frag_count_kernel(DevDb db, uint32_t* cnt) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x)
-        cnt[i] = fragments<S>(db, i, nullptr);
+        cnt[i] = fragments_local<S>(db, i, nullptr);
 }
 template <int S>
 __global__ void __launch_bounds__(256) frag_emit_kernel(DevDb db, const uint32_t* off, uint64_t* keys) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x)
-        fragments<S>(db, i, keys + off[i]);
+        fragments_local<S>(db, i, keys + off[i]);
 }
 __global__ void __launch_bounds__(256) part_bounds_kernel(const uint64_t* frags, const uint32_t* nf_ptr, uint32_t nparts,
                                                           uint32_t* part_off) {
@@ -819,6 +831,182 @@ __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t
     const uint32_t lo = part_off[p], hi = part_off[p + 1];
     for (uint32_t j = lo; j < hi; ++j) exec_frag<S>(db, __ldg(&frags[j]));
     if (hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
+}
+
+// =====================================================================================
+// shard exchange.  A transaction whose
+// fragments live on other shards is sent to each of them as a fixed-stride record
+//   [ts, type, len, params[len], 0...]          (shard_stride words)
+// and each remote fragment's output comes back to the home shard as
+//   [ts, out words]                             (1 + out_stride/4 words)
+// Records for one destination are contiguous and in home-bulk (ts) order.
+// =====================================================================================
+constexpr uint32_t MAX_SHARDS = 8;
+constexpr int SC_DEST0 = 24;      // [24, 32): records per destination shard
+
+// destination shards of a home transaction's remote fragments, from its raw (pre-ingest)
+// parameters; malformed transactions go nowhere (the home ingest rejects them)
+template <int S>
+DEV uint32_t dest_mask(const DevDb& db, uint32_t t, const uint32_t* p, uint32_t len) {
+    uint32_t m = 0;
+    if (S == S_TPCB) {
+        if (len == 4 && p[0] < db.dims[0] * db.dims[2]) m |= 1u << shard_of(db, p[0] / db.dims[2]);
+    } else if (S == S_TPCC) {
+        const uint32_t W = db.dims[0];
+        if (t == 0 && len >= 4) {
+            const uint32_t cnt = min(p[3], (len - 4) / 3);
+            bool abort = false;
+            for (uint32_t l = 0; l < cnt; ++l) {
+                abort |= p[4 + 3 * l] >= db.dims[3];
+                if (p[5 + 3 * l] < W) m |= 1u << shard_of(db, p[5 + 3 * l]);
+            }
+            if (abort) m = 0;
+        } else if (t == 1 && len == 7 && p[2] < W) {
+            m |= 1u << shard_of(db, p[2]);
+        }
+    }
+    return m & ~(1u << db.shard);
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) shard_count_kernel(DevDb db, const uint8_t* type, const uint32_t* poff,
+                                                          const uint32_t* pw, uint32_t nh, uint32_t* cnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x)
+        cnt[i] = __popc(dest_mask<S>(db, type[i], pw + poff[i], poff[i + 1] - poff[i]));
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) shard_pair_kernel(DevDb db, const uint8_t* type, const uint32_t* poff,
+                                                         const uint32_t* pw, uint32_t nh, const uint32_t* off,
+                                                         uint64_t* pairs, uint32_t* sc) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        uint32_t m = dest_mask<S>(db, type[i], pw + poff[i], poff[i + 1] - poff[i]);
+        uint32_t o = off[i];
+        while (m) {
+            const uint32_t q = __ffs(m) - 1;
+            m &= m - 1;
+            pairs[o++] = ((uint64_t)q << 32) | i;
+            atomicAdd(&sc[SC_DEST0 + q], 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) shard_pack_kernel(const uint64_t* pairs, const uint32_t* npairs,
+                                                         const uint8_t* type, const uint32_t* poff, const uint32_t* pw,
+                                                         const uint32_t* ts, uint32_t stride, uint32_t* send) {
+    const uint32_t np = *npairs;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < np; k += gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)pairs[k];
+        const uint32_t o0 = poff[i], len = min(poff[i + 1] - o0, stride - 3);
+        uint32_t* r = send + (uint64_t)k * stride;
+        r[0] = ts[i];
+        r[1] = type[i];
+        r[2] = len;
+        for (uint32_t w = 0; w < stride - 3; ++w) r[3 + w] = w < len ? pw[o0 + w] : 0u;
+    }
+}
+
+// merge: sort keys ts << 32 | source (home i < nh, received nh + j)
+__global__ void __launch_bounds__(256) merge_keys_kernel(const uint32_t* hts, uint32_t nh, const uint32_t* recv,
+                                                         uint32_t nr, uint32_t stride, uint64_t* keys) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nh + nr; k += gridDim.x * blockDim.x) {
+        const uint32_t t = k < nh ? hts[k] : recv[(uint64_t)(k - nh) * stride];
+        keys[k] = ((uint64_t)t << 32) | k;
+    }
+}
+
+__global__ void __launch_bounds__(256) merge_meta_kernel(const uint64_t* keys, uint32_t n, uint32_t nh,
+                                                         const uint8_t* htype, const uint32_t* hpoff,
+                                                         const uint32_t* hts, const uint32_t* recv, uint32_t stride,
+                                                         uint8_t* type, uint32_t* ts, uint32_t* src, uint32_t* home_pos,
+                                                         uint32_t* len) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)keys[k];
+        if (s < nh) {
+            type[k] = htype[s];
+            ts[k] = hts[s];
+            len[k] = hpoff[s + 1] - hpoff[s];
+            src[k] = s;
+            home_pos[s] = k;
+        } else {
+            const uint32_t* r = recv + (uint64_t)(s - nh) * stride;
+            type[k] = (uint8_t)min(r[1], 255u);
+            ts[k] = r[0];
+            len[k] = min(r[2], stride - 3);
+            src[k] = NOT_HOME;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) merge_params_kernel(const uint64_t* keys, uint32_t n, uint32_t nh,
+                                                           const uint32_t* hpoff, const uint32_t* hpw,
+                                                           const uint32_t* recv, uint32_t stride, const uint32_t* poff,
+                                                           uint32_t* pw) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)keys[k];
+        const uint32_t o = poff[k], len = poff[k + 1] - o;
+        const uint32_t* from = s < nh ? hpw + hpoff[s] : recv + (uint64_t)(s - nh) * stride + 3;
+        for (uint32_t w = 0; w < len; ++w) pw[o + w] = from[w];
+    }
+}
+
+// results of peers' transactions go back to their home shard
+__global__ void __launch_bounds__(256) ret_count_kernel(const uint32_t* src, uint32_t n, uint32_t* cnt) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        cnt[k] = src[k] == NOT_HOME ? 1u : 0u;
+}
+template <int S>
+__global__ void __launch_bounds__(256) ret_pair_kernel(DevDb db, const uint32_t* off, uint64_t* pairs, uint32_t* sc) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < db.n; k += gridDim.x * blockDim.x) {
+        if (db.src[k] != NOT_HOME) continue;
+        const uint32_t* p = db.pw + db.poff[k];
+        const uint32_t q = shard_of(db, S == S_TPCB ? p[2] : p[0]);
+        pairs[off[k]] = ((uint64_t)q << 32) | k;
+        atomicAdd(&sc[SC_DEST0 + q], 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) ret_pack_kernel(const uint64_t* pairs, const uint32_t* npairs, const uint32_t* ts,
+                                                       const uint8_t* out, uint32_t ow, uint32_t* send) {
+    const uint32_t np = *npairs;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < np; k += gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)pairs[k];
+        uint32_t* r = send + (uint64_t)k * (1 + ow);
+        r[0] = ts[i];
+        const uint32_t* o = reinterpret_cast<const uint32_t*>(out + (uint64_t)i * ow * 4);
+        for (uint32_t w = 0; w < ow; ++w) r[1 + w] = o[w];
+    }
+}
+
+// the fragments write disjoint output fields (zero elsewhere): OR them into the home record
+__global__ void __launch_bounds__(256) ret_merge_kernel(const uint32_t* recv, uint32_t nr, uint32_t ow, const uint32_t* ts,
+                                                        const uint32_t* src, uint32_t n, uint8_t* out, uint32_t* sc) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nr; j += gridDim.x * blockDim.x) {
+        const uint32_t* r = recv + (uint64_t)j * (1 + ow);
+        const uint32_t t = r[0];
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ts[mid] < t) lo = mid + 1; else hi = mid;
+        }
+        if (lo >= n || ts[lo] != t || src[lo] == NOT_HOME) { report_err(sc, E_OWNER, j); continue; }
+        uint32_t* o = reinterpret_cast<uint32_t*>(out + (uint64_t)lo * ow * 4);
+        for (uint32_t w = 0; w < ow; ++w)            // several shards may return to one record
+            if (r[1 + w]) atomicOr(&o[w], r[1 + w]);
+    }
+}
+
+// home results in home-bulk order
+__global__ void __launch_bounds__(256) home_gather_kernel(const uint32_t* home_pos, uint32_t nh, const uint8_t* status,
+                                                          const uint8_t* out, uint32_t stride, uint8_t* hstatus,
+                                                          uint8_t* hout) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const uint32_t k = home_pos[i];
+        hstatus[i] = status[k];
+        const uint32_t* a = reinterpret_cast<const uint32_t*>(out + (uint64_t)k * stride);
+        uint32_t* b = reinterpret_cast<uint32_t*>(hout + (uint64_t)i * stride);
+        for (uint32_t w = 0; w < stride / 4; ++w) b[w] = a[w];
+    }
 }
 
 // =====================================================================================
@@ -923,7 +1111,7 @@ DEV void tpl_release(uint32_t* lw) {
     if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(lw, (uint32_t)__popc(peers));
 }
 
-template <int S>
+template <int S, bool SH>
 __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
                                                        const uint32_t* __restrict__ lkey, uint32_t* lock, uint32_t* sc) {
     __shared__ uint32_t s_base;
@@ -932,14 +1120,14 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
     const uint32_t idx = s_base + threadIdx.x;
     if (idx >= db.n) return;
     Rec r[MAX_REC];
-    const int k = footprint<S>(db, db.type[idx], db.pw + db.poff[idx], r);
+    const int k = footprint_local<S>(db, db.type[idx], db.pw + db.poff[idx], r);
     const uint32_t ro = rec_off[idx];
     // growing phase: enter every lock in turn (keys order conflicting records by ts)
     for (int j = 0; j < k; ++j) {
         const uint32_t key = __ldg(&lkey[ro + j]);
         if (!tpl_acquire(&lock[r[j].item], key)) atomicExch(&sc[SC_DEADLOCK], 1u);
     }
-    exec_txn<S>(db, idx);
+    exec_txn<S, SH>(db, idx);
     __threadfence();
     // shrinking phase
     for (int j = 0; j < k; ++j) tpl_release(&lock[r[j].item]);
@@ -950,7 +1138,7 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
 // ticket t waits only for transactions with smaller tickets, all of which were taken
 // by running lanes, so the grid (sized to what is co-resident) always progresses, and
 // no slot idles behind a slow sibling of its CTA.
-template <int S>
+template <int S, bool SH>
 __global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
                                                                   const uint32_t* __restrict__ lkey, uint32_t* lock,
                                                                   uint32_t* sc) {
@@ -963,13 +1151,13 @@ __global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, cons
         const uint32_t idx = base + __popc(am & lanemask_lt());
         if (idx >= db.n) break;
         Rec r[MAX_REC];
-        const int k = footprint<S>(db, db.type[idx], db.pw + db.poff[idx], r);
+        const int k = footprint_local<S>(db, db.type[idx], db.pw + db.poff[idx], r);
         const uint32_t ro = rec_off[idx];
         for (int j = 0; j < k; ++j) {
             const uint32_t key = __ldg(&lkey[ro + j]);
             if (!tpl_acquire(&lock[r[j].item], key)) atomicExch(&sc[SC_DEADLOCK], 1u);
         }
-        exec_txn<S>(db, idx);
+        exec_txn<S, SH>(db, idx);
         __threadfence();
         for (int j = 0; j < k; ++j) tpl_release(&lock[r[j].item]);
     }

@@ -56,7 +56,21 @@ struct DevDb {
     const uint32_t* name_sorted;       // TPC-C customers of (w,d) sorted by (c_last, c_first, c)
     const uint32_t* name_off;          // [(w*D+d)*1000 + last] -> range start, +1 -> end
     uint32_t part_size;
+    // shards: this shard owns root keys [root_lo, root_hi) of nroot
+    // (root = TPC-B branch, TPC-C warehouse, TM-1 subscriber - 1), shard_of(r) = r*G/nroot
+    uint32_t nshards, shard, nroot, root_lo, root_hi;
+    const uint32_t* ts;                // global timestamps (NULL: first_ts + idx)
+    const uint32_t* src;               // sharded: home-bulk index, or NOT_HOME (a peer's transaction)
+    const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
 };
+constexpr uint32_t NOT_HOME = 0xFFFFFFFFu;
+
+// sh (compile-time in the fused kernels): the bulk carries explicit timestamps (sharded or
+// caller-given), insert rows of TPC-B come from ins_off, and cross-shard transactions
+// run their local fragments only
+DEV uint32_t txn_ts(const DevDb& db, uint32_t idx, bool sh) { return sh ? db.ts[idx] : db.first_ts + idx; }
+DEV bool root_local(const DevDb& db, uint64_t root) { return root >= db.root_lo && root < db.root_hi; }
+DEV uint32_t shard_of(const DevDb& db, uint64_t root) { return (uint32_t)(root * db.nshards / db.nroot); }
 
 #define COL(T, k) (reinterpret_cast<T*>(db.col[(k)]))
 #define INS(T, k) (reinterpret_cast<T*>(db.ins[(k)]))
@@ -156,6 +170,26 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
     }
 }
 
+// root key of an item (see the item layout above)
+template <int S>
+DEV uint64_t item_root(const DevDb& db, uint64_t item) {
+    if (S == S_TPCB) return item / (1ull + db.dims[1] + db.dims[2]);
+    if (S == S_TM1) return item / 18;
+    const uint64_t D = db.dims[1];
+    return item / (2 * D + 1 + D * db.dims[2] + db.dims[3]);
+}
+
+// the records of the transaction's items on this shard (all of them when unsharded)
+template <int S>
+DEV int footprint_local(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
+    const int k = footprint<S>(db, t, p, r);
+    if (db.nshards <= 1) return k;
+    int m = 0;
+    for (int j = 0; j < k; ++j)
+        if (root_local(db, item_root<S>(db, r[j].item))) r[m++] = r[j];
+    return m;
+}
+
 // =================================================================================
 // Stored procedures (whole transaction; K-SET and TPL)
 // =================================================================================
@@ -168,16 +202,17 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
 DEV void red_add(int64_t* p, int64_t v) { atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v); }
 DEV void red_add(uint32_t* p, uint32_t v) { atomicAdd(p, v); }
 
-DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     const int32_t delta = (int32_t)p[3];
     red_add(&COL(int64_t, B_TEL)[p[1]], (int64_t)delta);
     red_add(&COL(int64_t, B_BR)[p[2]], (int64_t)delta);
-    const uint64_t r = db.ins_base[0] + idx;               // history row (every deposit commits)
+    // history row: every deposit commits, so row = position (sharded: among home deposits)
+    const uint64_t r = db.ins_base[0] + (sh ? db.ins_off[idx] : idx);
     INS(uint32_t, IB_TID)[r] = p[1];
     INS(uint32_t, IB_BID)[r] = p[2];
     INS(uint32_t, IB_AID)[r] = p[0];
     INS(int32_t, IB_DELTA)[r] = delta;
-    INS(uint32_t, IB_TS)[r] = db.first_ts + idx;
+    INS(uint32_t, IB_TS)[r] = txn_ts(db, idx, sh);
 }
 DEV void tpcb_account(const DevDb& db, uint32_t idx, const uint32_t* p) {
     int64_t* acc = COL(int64_t, B_ACC);
@@ -342,7 +377,7 @@ DEV void tpcc_no_stock(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_
     }
 }
 
-DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3], w = p[0], d = p[1], c = p[2], cnt = p[3];
     const uint64_t wd = (uint64_t)w * D + d;
     uint32_t* dn = COL(uint32_t, C_D_NEXT);
@@ -367,7 +402,7 @@ DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
     for (uint32_t l = 0; l < cnt; ++l) all_local &= (p[5 + 3 * l] == w);
     const uint64_t ro = db.ins_base[T_ORDER] + db.ins_off[T_ORDER * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IO_ID)[ro] = oid; INS(uint32_t, IO_D)[ro] = d; INS(uint32_t, IO_W)[ro] = w;
-    INS(uint32_t, IO_C)[ro] = c; INS(uint32_t, IO_ENTRY)[ro] = db.first_ts + idx;
+    INS(uint32_t, IO_C)[ro] = c; INS(uint32_t, IO_ENTRY)[ro] = txn_ts(db, idx, sh);
     INS(uint32_t, IO_OLCNT)[ro] = cnt; INS(uint32_t, IO_ALLLOCAL)[ro] = all_local;
     const uint64_t rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
@@ -393,13 +428,13 @@ DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
     put64(o + 8, (uint64_t)((x + 50000000) / 100000000));
 }
 
-DEV void tpcc_pay_home(const DevDb& db, uint32_t idx, const uint32_t* p) {
+DEV void tpcc_pay_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     const uint32_t D = db.dims[1], w = p[0], d = p[1], h = p[6];
     red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
     red_add(&COL(int64_t, C_D_YTD)[(uint64_t)w * D + d], (int64_t)h);
     const uint64_t r = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IH_C)[r] = p[5]; INS(uint32_t, IH_CD)[r] = p[3]; INS(uint32_t, IH_CW)[r] = p[2];
-    INS(uint32_t, IH_D)[r] = d; INS(uint32_t, IH_W)[r] = w; INS(uint32_t, IH_DATE)[r] = db.first_ts + idx;
+    INS(uint32_t, IH_D)[r] = d; INS(uint32_t, IH_W)[r] = w; INS(uint32_t, IH_DATE)[r] = txn_ts(db, idx, sh);
     INS(int32_t, IH_AMT)[r] = (int32_t)h;
 }
 DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
@@ -422,7 +457,7 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
 // the lanes of a warp issue all their loads together; the abort decision and the
 // writes come after.  (Lanes that diverged in the line loops with their loads
 // outstanding ran one after another: 8 NewOrders in one warp took 10x one.)
-DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, bool sh) {
     const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
     const bool no = t == 0;
     const uint32_t w = p[0], d = p[1];
@@ -479,7 +514,7 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) 
 #pragma unroll
         for (int l = 0; l < 15; ++l) all_local &= ((uint32_t)l >= cnt) || lsw[l] == w;
         INS(uint32_t, IO_ID)[ro] = oid; INS(uint32_t, IO_D)[ro] = d; INS(uint32_t, IO_W)[ro] = w;
-        INS(uint32_t, IO_C)[ro] = p[2]; INS(uint32_t, IO_ENTRY)[ro] = db.first_ts + idx;
+        INS(uint32_t, IO_C)[ro] = p[2]; INS(uint32_t, IO_ENTRY)[ro] = txn_ts(db, idx, sh);
         INS(uint32_t, IO_OLCNT)[ro] = cnt; INS(uint32_t, IO_ALLLOCAL)[ro] = all_local;
         INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
         int64_t sum = 0;
@@ -518,7 +553,7 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) 
         red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
         red_add(&COL(int64_t, C_D_YTD)[wd], (int64_t)h);
         INS(uint32_t, IH_C)[rh] = p[5]; INS(uint32_t, IH_CD)[rh] = p[3]; INS(uint32_t, IH_CW)[rh] = p[2];
-        INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = db.first_ts + idx;
+        INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = txn_ts(db, idx, sh);
         INS(int32_t, IH_AMT)[rh] = (int32_t)h;
         const int64_t nb = cbal - (int64_t)h;
         stm(&COL(int64_t, C_C_BAL)[cx], nb);
@@ -530,22 +565,26 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) 
     }
 }
 
-// The combined kernel body: one whole transaction (K-SET, TPL).
-template <int S>
+template <int S> __device__ __noinline__ void exec_local(const DevDb& db, uint32_t idx);
+
+// The combined kernel body: one whole transaction (K-SET, TPL).  Sharded: a transaction
+// with a fragment on another shard runs only its local fragments.
+template <int S, bool SH = false>
 DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+    if (SH && db.xflag && db.xflag[idx]) { exec_local<S>(db, idx); return; }
     if (S == S_TPCB) {
-        tpcb_home(db, idx, p);
+        tpcb_home(db, idx, p, SH);
         tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
     } else {
-        tpcc_txn(db, idx, t, p);
+        tpcc_txn(db, idx, t, p, SH);
     }
 }
 
-template <int S>
+template <int S, bool SH = false>
 DEV void exec_txn(const DevDb& db, uint32_t idx) {
-    exec_txn_p<S>(db, idx, db.type[idx], db.pw + db.poff[idx]);
+    exec_txn_p<S, SH>(db, idx, db.type[idx], db.pw + db.poff[idx]);
 }
 
 // =================================================================================
@@ -602,23 +641,50 @@ template <int S>
 DEV void exec_frag(const DevDb& db, uint64_t fk) {
     const uint32_t pid = (uint32_t)(fk >> 32), idx = (uint32_t)(fk >> 8) & 0xFFFFFFu, kind = (uint32_t)fk & 0xFFu;
     const uint32_t t = db.type[idx];
+    const bool sh = db.ts != nullptr;
     const uint32_t* p = db.pw + db.poff[idx];
     if (S == S_TPCB) {
-        if (kind != F_REMOTE) tpcb_home(db, idx, p);
+        if (kind != F_REMOTE) tpcb_home(db, idx, p, sh);
         if (kind != F_HOME) tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
     } else {
         if (t == 0) {
             if (tpcc_no_aborts(db, p)) { db.status[idx] = 1; return; }
-            if (kind != F_REMOTE) tpcc_no_home(db, idx, p);
+            if (kind != F_REMOTE) tpcc_no_home(db, idx, p, sh);
             tpcc_no_stock(db, idx, p, pid);
         } else {
             if (p[4] == 2) { if (kind != F_REMOTE) db.status[idx] = 1; return; }
-            if (kind != F_REMOTE) tpcc_pay_home(db, idx, p);
+            if (kind != F_REMOTE) tpcc_pay_home(db, idx, p, sh);
             if (kind != F_HOME) tpcc_pay_customer(db, idx, p);
         }
     }
+}
+
+// a fragment lives on this shard (TM-1 transactions are single-root: home = local)
+template <int S>
+DEV bool frag_local(const DevDb& db, uint64_t fk) {
+    return S == S_TM1 || db.nshards <= 1 || root_local(db, fk >> 32);
+}
+
+// the fragments of txn idx on this shard (all of them when unsharded)
+template <int S>
+DEV int fragments_local(const DevDb& db, uint32_t idx, uint64_t* out) {
+    uint64_t fk[MAX_REC];
+    const int k = fragments<S>(db, idx, fk);
+    int m = 0;
+    for (int j = 0; j < k; ++j)
+        if (frag_local<S>(db, fk[j])) { if (out) out[m] = fk[j]; ++m; }
+    return m;
+}
+
+// (out of line: the cold sharded path must not cost the fused kernels registers)
+template <int S>
+__device__ __noinline__ void exec_local(const DevDb& db, uint32_t idx) {
+    uint64_t fk[MAX_REC];
+    const int k = fragments<S>(db, idx, fk);
+    for (int j = 0; j < k; ++j)
+        if (frag_local<S>(db, fk[j])) exec_frag<S>(db, fk[j]);
 }
 
 }  // namespace gputx

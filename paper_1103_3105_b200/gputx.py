@@ -31,12 +31,13 @@ class GputxError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [("schema", ctypes.c_int), ("dims", ctypes.c_uint32 * 4), ("max_bulk", ctypes.c_uint64),
                 ("insert_capacity", ctypes.c_uint64), ("part_size", ctypes.c_uint32), ("device", ctypes.c_int),
-                ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+                ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint32), ("shard", ctypes.c_uint32),
+                ("nshards", ctypes.c_uint32)]
 
 
 class BulkC(ctypes.Structure):
     _fields_ = [("type", ctypes.c_void_p), ("param_off", ctypes.c_void_p), ("param_words", ctypes.c_void_p),
-                ("n", ctypes.c_uint64), ("on_device", ctypes.c_int)]
+                ("n", ctypes.c_uint64), ("on_device", ctypes.c_int), ("ts", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):
@@ -89,6 +90,11 @@ def load_library():
         "gputx_trace_rounds": ([P, I], I),
         "gputx_read_round_ns": ([P, P, U64], I),
         "gputx_read_rank_ns": ([P, P, U64], I),
+        "gputx_shard_stride": ([I, I], U32),
+        "gputx_shard_pack": ([P, ctypes.POINTER(BulkC), P, U64, P], I),
+        "gputx_shard_submit": ([P, P, U64, ctypes.POINTER(U64)], I),
+        "gputx_shard_return_pack": ([P, P, U64, P], I),
+        "gputx_shard_return_merge": ([P, P, U64], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -103,7 +109,8 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
             "gputx_set_launch", "gputx_trace_rounds", "gputx_read_round_ns",
-            "gputx_read_rank_ns"]
+            "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
+            "gputx_shard_return_pack", "gputx_shard_return_merge"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -127,7 +134,8 @@ class Database:
     """One gputx_db handle: an HBM-resident database of one schema on one GPU."""
 
     def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
-                 device: int = 0, stream: int | None = None, insert_capacity: int = 0):
+                 device: int = 0, stream: int | None = None, insert_capacity: int = 0, shard: int = 0,
+                 nshards: int = 1):
         self.lib = load_library()
         self.schema = schema
         cfg = Config()
@@ -139,6 +147,10 @@ class Database:
         cfg.part_size = int(part_size)
         cfg.device = int(device)
         cfg.stream = stream
+        cfg.shard = int(shard)
+        cfg.nshards = int(nshards)
+        self.shard, self.nshards, self.device = int(shard), int(nshards), int(device)
+        self._bufs = {}
         h = ctypes.c_void_p()
         self._check(self.lib.gputx_open_db(ctypes.byref(cfg), ctypes.byref(h)), None)
         self.h = h
@@ -174,23 +186,83 @@ class Database:
         a = np.ascontiguousarray(np.asarray(ids, np.uint32))
         self._check(self.lib.gputx_register_types(self.h, a.ctypes.data if a.size else None, a.size), self.h)
 
-    def submit(self, bulk=None, *, type=None, param_off=None, param_words=None, on_device: bool = False) -> int:
-        """Submit a bulk: any object with .type/.param_off/.param_words (numpy, host), or
-        the three arrays as torch CUDA tensors with on_device=True (resident in HBM)."""
+    def _bulk(self, bulk, type, param_off, param_words, ts, on_device) -> BulkC:
         if bulk is not None:
             type, param_off, param_words = bulk.type, bulk.param_off, bulk.param_words
+            if ts is None:
+                ts = getattr(bulk, "ts", None)
         if not on_device:
             type = np.ascontiguousarray(type, np.uint8)
             param_off = np.ascontiguousarray(param_off, np.uint32)
             param_words = np.ascontiguousarray(param_words, np.uint32)
             if param_words.size == 0:
                 param_words = np.zeros(1, np.uint32)
-        self._keep = (type, param_off, param_words)
-        b = BulkC(_ptr(type), _ptr(param_off), _ptr(param_words), int(type.shape[0]), int(on_device))
-        ts = ctypes.c_uint64()
-        self._check(self.lib.gputx_submit_bulk(self.h, ctypes.byref(b), ctypes.byref(ts)), self.h)
-        self.n = int(type.shape[0])
-        return ts.value
+            if ts is not None:
+                ts = np.ascontiguousarray(ts, np.uint32)
+        self._keep = (type, param_off, param_words, ts)
+        return BulkC(_ptr(type), _ptr(param_off), _ptr(param_words), int(type.shape[0]), int(on_device),
+                     _ptr(ts) if ts is not None and int(type.shape[0]) else None)
+
+    def submit(self, bulk=None, *, type=None, param_off=None, param_words=None, ts=None,
+               on_device: bool = False) -> int:
+        """Submit a bulk: any object with .type/.param_off/.param_words (numpy, host), or
+        the three arrays as torch CUDA tensors with on_device=True (resident in HBM).
+        ts: optional global timestamps (u32, increasing)."""
+        b = self._bulk(bulk, type, param_off, param_words, ts, on_device)
+        first = ctypes.c_uint64()
+        self._check(self.lib.gputx_submit_bulk(self.h, ctypes.byref(b), ctypes.byref(first)), self.h)
+        self.n = int(b.n)
+        return first.value
+
+    # ---- sharding (include/gputx.h "Sharding") --------------------------------------
+    def shard_stride(self, result: bool = False) -> int:
+        return int(self.lib.gputx_shard_stride(self.schema, int(result)))
+
+    def _buf(self, key: str, words: int):
+        """A device u32 buffer (torch, on this handle's GPU) of at least `words` words."""
+        import torch
+        b = self._bufs.get(key)
+        if b is None or b.numel() < words:
+            b = torch.empty(max(words, 1024), dtype=torch.int32, device=f"cuda:{self.device}")
+            self._bufs[key] = b
+        return b
+
+    def _packed(self, fn, key: str, stride: int, est: int):
+        counts = (ctypes.c_uint64 * self.nshards)()
+        send = self._buf(key, est * stride)
+        st = fn(send, send.numel() // stride, counts)
+        if st == 6:                      # ECAPACITY: counts are filled; grow and repack
+            send = self._buf(key, sum(counts) * stride)
+            st = fn(send, send.numel() // stride, counts)
+        self._check(st, self.h)
+        return send, [int(c) for c in counts]
+
+    def shard_pack(self, bulk=None, *, type=None, param_off=None, param_words=None, ts=None,
+                   on_device: bool = False):
+        """Stage the home bulk; returns (send buffer, records per destination shard)."""
+        b = self._bulk(bulk, type, param_off, param_words, ts, on_device)
+        self.nh = int(b.n)
+        stride = self.shard_stride(False)
+        return self._packed(lambda buf, cap, c: self.lib.gputx_shard_pack(self.h, ctypes.byref(b), _ptr(buf), cap,
+                                                                          ctypes.addressof(c)),
+                            "send", stride, max(1024, self.nh // 4))
+
+    def shard_submit(self, recv, n_recv: int) -> int:
+        nl = ctypes.c_uint64()
+        self._check(self.lib.gputx_shard_submit(self.h, _ptr(recv) if n_recv else None, int(n_recv),
+                                                ctypes.byref(nl)), self.h)
+        self.n_local = int(nl.value)
+        self.n = self.nh
+        return self.n_local
+
+    def shard_return_pack(self):
+        stride = self.shard_stride(True)
+        return self._packed(lambda buf, cap, c: self.lib.gputx_shard_return_pack(self.h, _ptr(buf), cap,
+                                                                                 ctypes.addressof(c)),
+                            "ret", stride, max(1024, self.n_local // 4))
+
+    def shard_return_merge(self, recv, n_recv: int):
+        self._check(self.lib.gputx_shard_return_merge(self.h, _ptr(recv) if n_recv else None, int(n_recv)), self.h)
 
     def execute(self, strategy: str = KSET) -> dict:
         st = Stats()

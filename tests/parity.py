@@ -64,3 +64,48 @@ def run_both(schema, dims, image, bulks, strategy, db=None, max_bulk=None, **kw)
         if own:
             db.close()
     return stats
+
+
+def compare_sharded(schema, dims, ref, dbs, homes, image, label=""):
+    """Sharded run vs the oracle: every shard's owned rows, untouched foreign rows, home
+    results in submission order, and the union of the insert tables (each shard's rows
+    in ts order, the union compared as a multiset)."""
+    G = len(dbs)
+    R = W.n_roots(schema, dims)
+    for r, db in enumerate(dbs):
+        lo = (r * R + G - 1) // G
+        hi = ((r + 1) * R + G - 1) // G
+        got = db.read_image(image)
+        for k in image:
+            a, b, init = ref.db[k].reshape(-1), got[k].reshape(-1), np.asarray(image[k]).reshape(-1)
+            if schema == W.TPCC and k.startswith("i_"):
+                assert np.array_equal(a, b), f"{label}: replicated {k} changed on shard {r}"
+                continue
+            assert a.size % R == 0, k
+            f = a.size // R
+            own = slice(lo * f, hi * f)
+            if not np.array_equal(a[own], b[own]):
+                bad = np.nonzero(a[own] != b[own])[0] + lo * f
+                raise AssertionError(f"{label}: shard {r} column {k} differs at {bad[:10]} ({len(bad)} cells): "
+                                     f"oracle {a[bad[:5]]} gpu {b[bad[:5]]}")
+            rest = np.ones(a.size, bool)
+            rest[own] = False
+            assert np.array_equal(b[rest], init[rest]), f"{label}: shard {r} wrote foreign rows of {k}"
+        st, out = db.read_results()
+        idx = homes[r].ts.astype(np.int64)
+        if not np.array_equal(st, ref.status[idx]):
+            bad = np.nonzero(st != ref.status[idx])[0]
+            raise AssertionError(f"{label}: shard {r} status differs at {bad[:10]}")
+        if not np.array_equal(out, ref.out[idx]):
+            bad = np.nonzero((out != ref.out[idx]).any(axis=1))[0]
+            raise AssertionError(f"{label}: shard {r} output differs at home txns {bad[:10]} ({len(bad)}): "
+                                 f"oracle {ref.out[idx][bad[0]][:24]} gpu {out[bad[0]][:24]}")
+    ins = [db.inserts() for db in dbs]
+    for tab, cols in ref.inserts.items():
+        names = list(cols)
+        want = np.stack([cols[c].astype(np.int64) for c in names], axis=1)
+        have = np.concatenate([np.stack([i[tab][c].astype(np.int64) for c in names], axis=1) for i in ins])
+        assert want.shape == have.shape, f"{label}: insert {tab}: oracle {want.shape[0]} rows, gpu {have.shape[0]}"
+        ow = np.lexsort(want.T[::-1])
+        oh = np.lexsort(have.T[::-1])
+        assert np.array_equal(want[ow], have[oh]), f"{label}: insert table {tab} differs"

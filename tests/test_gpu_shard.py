@@ -1,0 +1,86 @@
+"""GPU parity of the sharded path (include/gputx.h "Sharding"): G shard
+handles on one GPU, cross-shard transactions exchanged as packed records (device copies
+stand in for the NCCL all-to-all), each shard executing its fragments in global ts order.
+The union of the shards must equal serial execution of the whole bulk (Definition 1)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import compare_sharded
+
+pytestmark = pytest.mark.gpu
+
+STRATS = ["kset", "part", "tpl"]
+
+
+def _run(schema, dims, image, bulk, G, strategy, **kw):
+    from paper_1103_3105_b200 import Database
+    from paper_1103_3105_b200.shard import LocalShards
+    ref = oracle.run(schema, dims.dims, image, bulk)
+    homes = W.split_home(bulk, dims, G)
+    dbs = [Database(schema, dims.dims, bulk.n, image, shard=r, nshards=G, **kw) for r in range(G)]
+    try:
+        stats = LocalShards(dbs).step(homes, strategy)
+        compare_sharded(schema, dims, ref, dbs, homes, image, label=f"{strategy} G={G}")
+        return stats
+    finally:
+        for db in dbs:
+            db.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("G", [2, 3])
+def test_tpcb_sharded(strategy, G):
+    dims = W.TpcbDims(12, 10, 500)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 6000, seed=3, remote_pct=40.0)
+    stats = _run(W.TPCB, dims, image, bulk, G, strategy)
+    assert sum(s["n"] for s in stats) > bulk.n          # remote accounts crossed shards
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("G", [2, 4])
+def test_tpcc_sharded(strategy, G):
+    dims = W.TpccDims(8, 10, 300, 2000)
+    image = W.tpcc_db(dims, seed=2)
+    bulk = W.tpcc_bulk(dims, 5000, seed=9, remote_line_pct=10.0, remote_pay_pct=30.0)
+    stats = _run(W.TPCC, dims, image, bulk, G, strategy)
+    assert sum(s["n"] for s in stats) > bulk.n
+
+
+def test_tpcc_sharded_tiny_contention():
+    """Few items and customers: duplicate lines, by-name misses, aborts, hot stock."""
+    dims = W.TpccDims(3, 2, 30, 40)
+    image = W.tpcc_db(dims, seed=4)
+    bulk = W.tpcc_bulk(dims, 3000, seed=5, remote_line_pct=30.0, remote_pay_pct=40.0)
+    for s in STRATS:
+        _run(W.TPCC, dims, image, bulk, 3, s)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_tm1_sharded(strategy):
+    dims = W.Tm1Dims(5000)
+    image = W.tm1_db(dims, seed=3)
+    bulk = W.tm1_bulk(dims, 20_000, seed=4, dist="nurand")
+    stats = _run(W.TM1, dims, image, bulk, 2, strategy)
+    assert sum(s["n"] for s in stats) == bulk.n          # single-subscriber: nothing crosses
+
+
+def test_sharded_errors():
+    from paper_1103_3105_b200 import Database, GputxError
+    dims = W.TpcbDims(4, 10, 100)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 100, seed=1)
+    db = Database(W.TPCB, dims.dims, 100, image, shard=0, nshards=2)
+    try:
+        with pytest.raises(GputxError) as e:
+            db.submit(bulk)                                   # sharded handles use shard_pack/submit
+        assert e.value.name == "ESTATE"
+        home = bulk.take(np.arange(bulk.n), ts=np.arange(bulk.n, dtype=np.uint32))
+        db.shard_pack(home)                                   # includes the other shard's txns
+        with pytest.raises(GputxError) as e:
+            db.shard_submit(None, 0)
+        assert e.value.name == "ECROSS"
+    finally:
+        db.close()

@@ -48,6 +48,7 @@ class Bulk:
     param_off: np.ndarray
     param_words: np.ndarray
     meta: dict = field(default_factory=dict)
+    ts: np.ndarray | None = None     # global timestamps (u32, increasing); None: position order
 
     @property
     def n(self) -> int:
@@ -55,6 +56,16 @@ class Bulk:
 
     def params(self, i: int) -> np.ndarray:
         return self.param_words[self.param_off[i]:self.param_off[i + 1]]
+
+    def take(self, idx: np.ndarray, ts: np.ndarray | None = None) -> "Bulk":
+        """The transactions at positions idx (increasing), optionally with timestamps."""
+        idx = np.asarray(idx, np.int64)
+        lens = (self.param_off[idx + 1].astype(np.int64) - self.param_off[idx])
+        off = np.zeros(idx.size + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        src = np.repeat(self.param_off[idx].astype(np.int64) - off[:-1], lens) + np.arange(off[-1])
+        return Bulk(self.schema, self.type[idx].copy(), off.astype(np.uint32), self.param_words[src].copy(),
+                    dict(self.meta), None if ts is None else np.asarray(ts, np.uint32))
 
     def slice(self, lo: int, hi: int) -> "Bulk":
         off = self.param_off[lo:hi + 1]
@@ -297,7 +308,7 @@ def tm1_bulk(dims: Tm1Dims, n: int, seed: int, dist: str = "nurand", mix=TM1_MIX
     mask = np.arange(7)[None, :] < L[:, None]
     words = W[mask].astype(np.uint32)
     b = Bulk(TM1, types, off.astype(np.uint32), words)
-    b.meta = dict(dims=dims.dims, seed=seed, dist=dist)
+    b.meta = dict(dims=dims.dims, seed=seed, dist=dist, root=(s_id - 1).astype(np.int64))
     return b
 
 
@@ -430,3 +441,52 @@ def make_bulk(schema: int, dims, n: int, seed: int, **kw) -> Bulk:
     if schema == TPCC:
         return tpcc_bulk(dims, n, seed, **kw)
     raise ValueError(schema)
+
+
+# --------------------------------------------------------------------------------------
+# Sharding by root key: TPC-B branch, TPC-C warehouse, TM-1 subscriber.
+# Shard r of G owns roots x with x*G // R == r.  These only select which rank submits a
+# transaction (its "home"); the engine splits cross-shard transactions itself.
+
+def n_roots(schema: int, dims) -> int:
+    return int(dims.dims[0])
+
+
+def home_roots(bulk: Bulk) -> np.ndarray:
+    """Home root key of every transaction (TPC-B teller's branch, TPC-C w, TM-1 s_id-1)."""
+    first = bulk.param_off[:-1].astype(np.int64)
+    if bulk.schema == TPCB:
+        return bulk.param_words[first + 2].astype(np.int64)
+    if bulk.schema == TPCC:
+        return bulk.param_words[first].astype(np.int64)
+    return np.asarray(bulk.meta["root"], np.int64)
+
+
+def shard_of(root: np.ndarray, G: int, R: int) -> np.ndarray:
+    return (np.asarray(root, np.int64) * G) // R
+
+
+def split_home(bulk: Bulk, dims, G: int) -> list[Bulk]:
+    """Per shard, its home transactions with their global timestamps (bulk positions)."""
+    owner = shard_of(home_roots(bulk), G, n_roots(bulk.schema, dims))
+    out = []
+    for r in range(G):
+        idx = np.nonzero(owner == r)[0]
+        out.append(bulk.take(idx, ts=idx.astype(np.uint32)))
+    return out
+
+
+def shard_rows(schema: int, dims, G: int, r: int) -> dict:
+    """Row ranges [lo, hi) of each root-partitioned column owned by shard r (columns
+    not listed are read-only and replicated)."""
+    R = n_roots(schema, dims)
+    lo = (r * R + G - 1) // G
+    hi = ((r + 1) * R + G - 1) // G
+    d = dims.dims
+    if schema == TPCB:
+        return {"branch": (lo, hi), "teller": (lo * d[1], hi * d[1]), "account": (lo * d[2], hi * d[2])}
+    if schema == TPCC:
+        D, C, I = d[1], d[2], d[3]
+        return {"warehouse": (lo, hi), "district": (lo * D, hi * D), "customer": (lo * D * C, hi * D * C),
+                "stock": (lo * I, hi * I)}
+    return {"subscriber": (lo, hi)}

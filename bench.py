@@ -10,8 +10,13 @@ group, k-set rounds) — every §8(a) row.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tm1|tpcb|tpcb_tiny|tpcc]
   python bench.py --impl reference ...   # the oracle (serial CPU executor) as reference arm
 
-For N > 1 (torchrun), every rank owns an independent shard (its own subscribers /
-branches / warehouses and its own bulk): weak scaling, no data-path collective.
+For N > 1 (torchrun, one rank per GPU) the database is N times the configuration's
+root keys (subscribers / branches / warehouses), sharded by root key, and every rank
+submits a bulk of the configuration's size whose home roots are its own (weak scaling:
+per-GPU work fixed).  Cross-shard transactions (TPC-B remote accounts, TPC-C remote
+supply warehouses / customers) are packed by the engine and exchanged with NCCL
+all-to-all before ranking; remote fragment outputs come back the same way
+(paper_1103_3105_b200/shard.py).  All of it is inside the timed step.
 """
 from __future__ import annotations
 
@@ -184,6 +189,8 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
         backend = "nccl" if (torch.cuda.is_available() and args.impl != "reference") else "gloo"
+        # GPUTX_DIST_BACKEND=gloo: several ranks on one GPU (host-staged all-to-all; tests only)
+        backend = os.environ.get("GPUTX_DIST_BACKEND", backend)
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
@@ -202,12 +209,19 @@ def reduce_max(dist, x: float, dev=None) -> float:
     return float(t.item())
 
 
-def make_inputs(wl, rank: int, steps: int, seed: int):
-    dims = wl["dims"]
-    image = W.make_db(wl["schema"], dims, seed=seed + 1000 * rank)
+def make_inputs(wl, rank: int, ws: int, steps: int, seed: int):
+    """(dims, image, bulks): the configuration itself at N = 1; at N > 1 the weak-scaled
+    global database (same image on every rank) and this rank's home bulks (global ts)."""
     nb = min(steps, 3)
-    bulks = [W.make_bulk(wl["schema"], dims, wl["n"], seed + 1000 * rank + k, **wl["kw"]) for k in range(nb)]
-    return image, bulks
+    if ws == 1:
+        dims = wl["dims"]
+        image = W.make_db(wl["schema"], dims, seed=seed)
+        bulks = [W.make_bulk(wl["schema"], dims, wl["n"], seed + k, **wl["kw"]) for k in range(nb)]
+        return dims, image, bulks
+    dims = W.scaled_dims(wl["schema"], wl["dims"], ws)
+    image = W.make_db(wl["schema"], dims, seed=seed)
+    bulks = [W.shard_bulk(wl["schema"], dims, wl["n"], seed + k, rank, ws, **wl["kw"]) for k in range(nb)]
+    return dims, image, bulks
 
 
 def oracle_rate(wl, image, bulks, min_seconds: float, max_runs: int):
@@ -239,7 +253,7 @@ def cpu_model():
 def run_reference(args, wl, ws, rank):
     if rank != 0:
         return 0
-    image, bulks = make_inputs(wl, 0, max(args.steps, 1), args.seed)
+    _, image, bulks = make_inputs(wl, 0, 1, max(args.steps, 1), args.seed)
     import oracle
     cur = image
     for k in range(args.warmup):
@@ -257,7 +271,7 @@ def run_reference(args, wl, ws, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": config_of(args, wl),
+        "config": config_of(args, wl, wl["dims"], 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} bulks of {wl['n']} txns ({wl['desc']}), serial loop only",
                          "cpu": cpu_model(), "nproc": os.cpu_count()},
@@ -267,10 +281,14 @@ def run_reference(args, wl, ws, rank):
     return 0
 
 
-def config_of(args, wl):
-    return {"workload": wl["desc"], "strategy": args.strategy, "bulk": wl["n"], "dims": list(wl["dims"].dims),
-            "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM (value); "
-            "pinned host (e2e)"}
+def config_of(args, wl, dims, ws):
+    c = {"workload": wl["desc"], "strategy": args.strategy, "bulk": wl["n"], "dims": list(dims.dims),
+         "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM (value); "
+         "pinned host (e2e)"}
+    if ws > 1:
+        c["sharding"] = (f"{ws} shards by root key, bulk {wl['n']} per shard (weak scaling); cross-shard "
+                         "transactions exchanged by NCCL all-to-all inside the step")
+    return c
 
 
 def main():
@@ -294,22 +312,37 @@ def main():
     import torch
     from paper_1103_3105_b200 import Database
 
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     clk = Clocks(local).__enter__()                      # sampling starts now, ends after the e2e loop
-    image, bulks = make_inputs(wl, rank, max(args.steps, 1), args.seed)
+    dims, image, bulks = make_inputs(wl, rank, ws, max(args.steps, 1), args.seed)
     n = wl["n"]
     cap = 3 * (args.warmup + args.steps) + 8          # bulks the merged insert tables must hold
-    db = Database(wl["schema"], wl["dims"].dims, n, image, device=local, stream=stream.cuda_stream,
-                  insert_capacity=cap)
-    dbulks = [(torch.from_numpy(b.type).to(dev), torch.from_numpy(b.param_off.view(np.int32)).to(dev),
-               torch.from_numpy(b.param_words.view(np.int32)).to(dev)) for b in bulks]
+    # sharded: the local bulk is the home bulk plus the peers' cross-shard transactions
+    max_bulk = n if ws == 1 else min(1 << 24, n + n // 2 + 1024)
+    db = Database(wl["schema"], dims.dims, max_bulk, image, device=local, stream=stream.cuda_stream,
+                  insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws)
+    del image
+
+    class DevBulk:
+        def __init__(self, b):
+            self.type = torch.from_numpy(b.type).to(dev)
+            self.param_off = torch.from_numpy(b.param_off.view(np.int32)).to(dev)
+            self.param_words = torch.from_numpy(b.param_words.view(np.int32)).to(dev)
+            self.ts = torch.from_numpy(b.ts.view(np.int32)).to(dev) if b.ts is not None else None
+
+    dbulks = [DevBulk(b) for b in bulks]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    if ws > 1:
+        from paper_1103_3105_b200 import shard as SH
 
     def step_dev(k, strategy):
-        t, o, w = dbulks[k % len(dbulks)]
-        db.submit(type=t, param_off=o, param_words=w, on_device=True)
+        b = dbulks[k % len(dbulks)]
+        if ws > 1:
+            return SH.step(db, b, strategy, on_device=True)
+        db.submit(b, on_device=True)
         return db.execute(strategy)
 
     def barrier():
@@ -354,31 +387,40 @@ def main():
     st_host, _ = db.read_results()
 
     # ---- e2e through the C ABI with host (pinned) buffers ----------------------------
-    hb = []
-    for b in bulks:
-        pt = torch.from_numpy(b.type).pin_memory().numpy()
-        po = torch.from_numpy(b.param_off.view(np.int32)).pin_memory().numpy().view(np.uint32)
-        pw = torch.from_numpy(b.param_words.view(np.int32)).pin_memory().numpy().view(np.uint32)
-        hb.append((pt, po, pw))
+    class HostBulk:
+        def __init__(self, b):
+            self.type = torch.from_numpy(b.type).pin_memory().numpy()
+            self.param_off = torch.from_numpy(b.param_off.view(np.int32)).pin_memory().numpy().view(np.uint32)
+            self.param_words = torch.from_numpy(b.param_words.view(np.int32)).pin_memory().numpy().view(np.uint32)
+            self.ts = (torch.from_numpy(b.ts.view(np.int32)).pin_memory().numpy().view(np.uint32)
+                       if b.ts is not None else None)
+
+        def nbytes(self):
+            return sum(a.nbytes for a in (self.type, self.param_off, self.param_words, self.ts) if a is not None)
+
+    hb = [HostBulk(b) for b in bulks]
     st_pin = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
     out_pin = torch.empty(n * db.stride, dtype=torch.uint8).pin_memory().numpy().reshape(n, db.stride)
     e2e_ms = []
     for k in range(args.warmup + args.steps):
-        pt, po, pw = hb[k % len(hb)]
+        b = hb[k % len(hb)]
         flush.fill_(k & 0xFF)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        db.submit(type=pt, param_off=po, param_words=pw, on_device=False)
-        db.execute_nostats(args.strategy)
+        if ws > 1:
+            SH.step(db, b, args.strategy, on_device=False)
+        else:
+            db.submit(b, on_device=False)
+            db.execute_nostats(args.strategy)
         db.read_results(st_pin, out_pin)
         e1.record(stream)
         e1.synchronize()
         if k >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
     e2e_total = max_over_ranks(sum(e2e_ms))
-    h2d = int(np.mean([a.nbytes + b.nbytes + c.nbytes for a, b, c in hb]))
+    h2d = int(np.mean([b.nbytes() for b in hb]))
     d2h = n + n * db.stride
 
     # ---- other strategies on the same bulks ------------------------------------------
@@ -413,7 +455,8 @@ def main():
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) -----------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, txns, runs, secs = oracle_rate(wl, image, bulks, args.cpu_seconds, 50)
+        rate, txns, runs, secs = oracle_rate(wl, W.make_db(wl["schema"], dims, seed=args.seed), bulks,
+                                             args.cpu_seconds, 50)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{runs} bulk(s) x {n} txns of the same workload, serial loop {secs:.2f} s",
                "cpu": cpu_model(), "nproc": os.cpu_count()}
@@ -423,7 +466,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (seeded generators, workloads/)",
-        "config": config_of(args, wl),
+        "config": config_of(args, wl, dims, ws),
         "e2e": {"value": ws * n * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -16,28 +16,44 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     sys.path.insert(0, ROOT)
+    import torch
     import bench
+    import workloads as W
+    from paper_1103_3105_b200.shard import all_to_all_records
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    wl = bench.WORKLOADS["tpcb_tiny"]
-    image, bulks = bench.make_inputs(wl, rank, 1, seed=3)
+    wl = bench.WORKLOADS["tpcc"]
+    small = dict(wl, dims=W.TpccDims(4, 10, 30, 1000), n=500)
+    dims, image, bulks = bench.make_inputs(small, rank, world, 1, seed=3)
+    roots = W.home_roots(bulks[0])
+    # exchange: rank r sends r+1 records to every peer (stride 3: [ts, src, dst])
+    stride = 3
+    counts = [(rank + 1) if q != rank else 0 for q in range(world)]
+    recs = [[1000 * rank + j, rank, q] for q in range(world) for j in range(counts[q])]
+    send = torch.tensor(recs, dtype=torch.int32).reshape(-1)
+    recv, nrecv = all_to_all_records(send, counts, stride)
+    got = recv[:nrecv * stride].reshape(-1, stride).tolist()
     x = bench.reduce_max(dist, float(rank + 1) * 1.5)
-    q.put((rank, x, bulks[0].param_words[:16].tolist()))
+    q.put((rank, x, dims.dims, int(roots.min()), int(roots.max()), bulks[0].ts[:3].tolist(), got))
     dist.destroy_process_group()
 
 
-def test_gloo_two_ranks_shards_and_max():
+def test_gloo_two_ranks_shards_exchange_and_max():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29000 + os.getpid() % 1000
     ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in range(2))
+    res = sorted(q.get(timeout=180) for _ in range(2))
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0][1] == res[1][1] == 3.0               # max over ranks
-    assert res[0][2] != res[1][2]                       # independent shard bulks
+    assert res[0][2] == res[1][2] == (8, 10, 30, 1000)  # weak scaling: 2 x 4 warehouses, same image
+    assert (res[0][3], res[0][4]) == (0, 3) and (res[1][3], res[1][4]) == (4, 7)   # home roots per shard
+    assert res[0][5] == [0, 2, 4] and res[1][5] == [1, 3, 5]                       # interleaved global ts
+    assert res[0][6] == [[1000, 1, 0], [1001, 1, 0]]   # rank 0 received rank 1's two records
+    assert res[1][6] == [[0, 0, 1]]
 
 
 def test_reference_arm_torchrun_two_ranks():

@@ -322,3 +322,22 @@ def test_kset_order_equals_serial(schema, dims, kw):
         d = oracle.depths(schema, dims.dims, db, bulk)
         order = np.lexsort((rng.random(bulk.n), d))
         assert _same(schema, ref, oracle.run_sequence(schema, dims.dims, db, bulk, order))
+
+
+def test_shard_split_covers_bulk_once():
+    """Sharding helpers (workloads): every transaction has exactly one home shard, homes
+    keep the bulk's order, and owned row ranges tile each table."""
+    dims = W.TpccDims(6, 10, 30, 500)
+    bulk = W.tpcc_bulk(dims, 2000, seed=4)
+    for G in (1, 2, 4):
+        parts = W.split_home(bulk, dims, G)
+        ts = np.concatenate([p.ts for p in parts])
+        assert np.array_equal(np.sort(ts), np.arange(bulk.n))
+        for r, p in enumerate(parts):
+            assert np.all(np.diff(p.ts.astype(np.int64)) > 0)
+            assert np.all(W.shard_of(W.home_roots(p), G, 6) == r)
+            for k in range(min(p.n, 20)):
+                assert np.array_equal(p.params(k), bulk.params(int(p.ts[k])))
+        rows = [W.shard_rows(W.TPCC, dims, G, r)["stock"] for r in range(G)]
+        assert rows[0][0] == 0 and rows[-1][1] == 6 * 500
+        assert all(rows[r][1] == rows[r + 1][0] for r in range(G - 1))

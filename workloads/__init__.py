@@ -152,7 +152,7 @@ def tpcb_db(dims: TpcbDims) -> dict[str, np.ndarray]:
 
 
 def tpcb_bulk(dims: TpcbDims, n: int, seed: int, remote_pct: float = 15.0,
-              alpha: float = 0.0, zipf_theta: float = 0.0) -> Bulk:
+              alpha: float = 0.0, zipf_theta: float = 0.0, home_range: tuple | None = None) -> Bulk:
     """n deposit transactions, params [aid, tid, bid, delta(i32 as u32)].
 
     Branch: hot-branch alpha model (branch 0 w.p. alpha, else uniform)
@@ -162,13 +162,14 @@ def tpcb_bulk(dims: TpcbDims, n: int, seed: int, remote_pct: float = 15.0,
     """
     rng = _rng(seed, 0xB)
     B, T, A = dims.branches, dims.tellers_per_branch, dims.accounts_per_branch
+    lo, hi = home_range if home_range is not None else (0, B)   # home branches (sharded generation)
     if zipf_theta > 0:
-        bid = zipf_keys(rng, zipf_theta, B, n)
+        bid = lo + zipf_keys(rng, zipf_theta, hi - lo, n)
     else:
-        bid = rng.integers(0, B, size=n, dtype=np.int64)
+        bid = rng.integers(lo, hi, size=n, dtype=np.int64)
         if alpha > 0:
             hot = rng.random(n) < alpha
-            bid = np.where(hot, 0, bid)
+            bid = np.where(hot, lo, bid)
     tid = bid * T + rng.integers(0, T, size=n, dtype=np.int64)
     abr = bid.copy()
     if B > 1 and remote_pct > 0:
@@ -255,7 +256,8 @@ def tm1_db(dims: Tm1Dims, seed: int = 7) -> dict[str, np.ndarray]:
     return db
 
 
-def tm1_bulk(dims: Tm1Dims, n: int, seed: int, dist: str = "nurand", mix=TM1_MIX) -> Bulk:
+def tm1_bulk(dims: Tm1Dims, n: int, seed: int, dist: str = "nurand", mix=TM1_MIX,
+             home_range: tuple | None = None) -> Bulk:
     """n TATP transactions.  s_id = NURand(A, 1, P) ("nurand", TATP standard with
     A = 65535 / 1048575 / 2097151 by P) or uniform in [1, P].
 
@@ -267,12 +269,13 @@ def tm1_bulk(dims: Tm1Dims, n: int, seed: int, dist: str = "nurand", mix=TM1_MIX
     UL/ICF/DCF carry the subscriber's sub_nbr string.
     """
     rng = _rng(seed, 0x7A1)
-    P = dims.subscribers
+    lo, hi = home_range if home_range is not None else (0, dims.subscribers)   # subscribers lo+1..hi
+    P = hi - lo
     if dist == "nurand":
         A = 65535 if P <= 1_000_000 else (1048575 if P <= 10_000_000 else 2097151)
-        s_id = nurand(rng, A, 1, P, n)
+        s_id = lo + nurand(rng, A, 1, P, n)
     elif dist == "uniform":
-        s_id = rng.integers(1, P + 1, size=n, dtype=np.int64)
+        s_id = lo + rng.integers(1, P + 1, size=n, dtype=np.int64)
     else:
         raise ValueError(dist)
     p = np.asarray(mix, np.float64)
@@ -490,3 +493,30 @@ def shard_rows(schema: int, dims, G: int, r: int) -> dict:
         return {"warehouse": (lo, hi), "district": (lo * D, hi * D), "customer": (lo * D * C, hi * D * C),
                 "stock": (lo * I, hi * I)}
     return {"subscriber": (lo, hi)}
+
+
+def scaled_dims(schema: int, dims, G: int):
+    """The global dimensions of a weak-scaled run: G times the root keys of `dims`."""
+    if schema == TPCB:
+        return TpcbDims(dims.branches * G, dims.tellers_per_branch, dims.accounts_per_branch)
+    if schema == TM1:
+        return Tm1Dims(dims.subscribers * G)
+    return TpccDims(dims.warehouses * G, dims.districts, dims.customers, dims.items)
+
+
+def shard_bulk(schema: int, gdims, n: int, seed: int, r: int, G: int, **kw) -> Bulk:
+    """Shard r's n home transactions of a G-shard run over the global dims: home roots
+    drawn in r's root range with the single-GPU distribution, remote accounts / supply
+    warehouses / customers over all roots; global ts = i*G + r (interleaved, unique)."""
+    R = n_roots(schema, gdims)
+    lo, hi = (r * R + G - 1) // G, ((r + 1) * R + G - 1) // G
+    s = seed * 1009 + r
+    if schema == TPCB:
+        b = tpcb_bulk(gdims, n, s, home_range=(lo, hi), **kw)
+    elif schema == TM1:
+        b = tm1_bulk(gdims, n, s, home_range=(lo, hi), **kw)
+    else:
+        w = np.random.default_rng(np.random.SeedSequence([s, 0x5EA])).integers(lo, hi, size=n, dtype=np.int64)
+        b = tpcc_bulk(gdims, n, s, home_w=w, **kw)
+    b.ts = (np.arange(n, dtype=np.int64) * G + r).astype(np.uint32)
+    return b

@@ -705,7 +705,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->lb_tpl.inc, tiles)))
         return bail(st);
     {
-        const uint64_t rt = db->max_rec / RK_TILE + 2;
+        const uint64_t rt = db->max_rec / RK_WT + 2;
         if ((st = dalloc(db, &db->rank_memo.aggA, rt)) || (st = dalloc(db, &db->rank_memo.carD, rt)) ||
             (st = dalloc(db, &db->rank_memo.dirty, rt / 32 + 1)) ||
             (st = dalloc(db, &db->rank_memo.recpos, db->max_rec + 1)) ||
@@ -727,9 +727,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
     for (auto& e : db->ev) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
-    // in-tile sweeps per rank pass, measured per schema (profiles/round1_tuning.md):
-    // TM-1 chains are subscriber-local (sweeps close them on chip), TPC-C's cross tiles
-    db->rank_local = schema == S_TM1 ? 16 : schema == S_TPCB ? 4 : 1;
+    // sweeps per warp-tile per rank pass, measured per schema (profiles/round1.md):
+    // TM-1 / TPC-B chains are mostly root-local (sweeps close them in the tile), TPC-C's cross tiles
+    db->rank_local = schema == S_TPCC ? 1 : 4;
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
     // TPC-C: each pass raises most of the long W_YTD chains' suffix, so nearly every tile is
     // dirty every pass and the marking costs more than it saves (profiles/round1.md)

@@ -226,6 +226,7 @@ DEV Xf rec_xf(bool head, uint32_t w, int d) {
 }
 
 constexpr int RK_THREADS = 256, RK_ITEMS = 8, RK_TILE = RK_THREADS * RK_ITEMS;
+constexpr int RK_WT = 32 * RK_ITEMS;      // records per warp-tile (the rank pass's unit of work)
 constexpr uint32_t RK_LOCAL_DEFAULT = 4;   // in-tile Gauss-Seidel sweeps per pass (default)
 
 // One pass over the sorted records = reduce, then scan:
@@ -311,11 +312,59 @@ DEV void rk_mark(const RkMemo& memo, uint32_t t, uint32_t self) {
     __threadfence();                          // the raise is visible before the mark
     const uint32_t r0 = __ldg(&memo.rec_off[t]), r1 = __ldg(&memo.rec_off[t + 1]);
     for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t tl = __ldcg(&memo.recpos[r]) / RK_TILE;
+        const uint32_t tl = __ldcg(&memo.recpos[r]) / RK_WT;
         if (tl != self && !rk_is_dirty(memo.dirty, tl)) atomicOr(&memo.dirty[tl >> 5], 1u << (tl & 31));
     }
 }
 
+// One warp-tile (RK_WT records) into this warp's stage; returns the head/write/valid bits
+// of the lane's RK_ITEMS records.
+DEV uint32_t rk_wload(const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t wt, uint64_t* stage) {
+    const uint64_t tb = (uint64_t)wt * RK_WT;
+    const uint32_t lane = lane_id();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        const uint32_t i = k * 32 + lane;            // coalesced
+        stage[i] = (tb + i < nrec) ? __ldg(&keys[tb + i]) : ~0ull;
+    }
+    const uint64_t prev = tb ? __ldg(&keys[tb - 1]) : ~0ull;
+    __syncwarp();
+    uint32_t hw = 0;
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        const uint32_t pos = lane * RK_ITEMS + k;
+        if (tb + pos < nrec) {
+            const uint64_t key = stage[pos];
+            const uint64_t pk = pos ? stage[pos - 1] : prev;
+            const bool head = (tb + pos == 0) || key_item(pk) != key_item(key);
+            hw |= (head ? 1u : 0u) << (2 * k);
+            hw |= key_w(key) << (2 * k + 1);
+            hw |= 1u << (16 + k);
+        }
+    }
+    return hw;
+}
+
+DEV void rk_wgather(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* dv) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k)
+        dv[k] = ((hw >> (16 + k)) & 1u) ? (int)__ldcg(&D[key_idx(stage[lane * RK_ITEMS + k])]) : 0;
+}
+
+// exclusive warp scan of maps; total to every lane
+DEV Xf rk_wscan(Xf x, Xf& total) {
+    const Xf inc = warp_scan_incl<Xf, OpXf>(x);
+    total = shfl_t(inc, 31);
+    Xf ex = shfl_up_t(inc, 1);
+    if (lane_id() == 0) ex = OpXf::identity();
+    return ex;
+}
+
+// Warp-granular passes: every warp owns a contiguous range of warp-tiles and walks it as
+// an independent chain (warp shuffles only, no block barrier in the tile loop), so an SM
+// has 16 independent load/scan/atomic chains in flight instead of 2.
 __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes,
@@ -323,23 +372,27 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
                                                           uint64_t* trace) {
     // trace (diagnostics): per pass p, [8p] pass start (CTA 0), [8p+1] last CTA done with A,
     // [8p+2] CTA 0 past barrier 1, [8p+3] last CTA done with D, [8p+4] CTA 0 past barrier 2,
-    // [8p+5] tiles swept, [8p+6] sweeps
+    // [8p+5] warp-tiles swept, [8p+6] sweeps
     auto tmax = [&](uint32_t pass, uint32_t slot) {
         if (trace && threadIdx.x == 0 && pass < RANK_TRACE_SLOTS / 8)
             atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * pass + slot]), (unsigned long long)globaltimer_ns());
     };
-    __shared__ uint64_t stage[RK_TILE];
+    constexpr uint32_t NW = RK_THREADS / 32;
+    __shared__ uint64_t stage_all[NW * RK_WT];
     __shared__ Xf sm[8];
-    __shared__ uint64_t s_prev;
+    __shared__ Xf wagg[NW];
     __shared__ int s_chg;
+    __shared__ uint32_t s_swept, s_sweeps;
     Xf* cta_agg = lb.agg;                  // one aggregate per CTA
     const uint32_t nrec = *nrec_ptr;
-    const uint32_t ntiles = (nrec + RK_TILE - 1) / RK_TILE;
-    const uint32_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const uint32_t t0 = min(ntiles, blockIdx.x * per), t1 = min(ntiles, t0 + per);
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+    uint64_t* stage = stage_all + wid * RK_WT;
+    const uint32_t nwt = (nrec + RK_WT - 1) / RK_WT;
+    const uint32_t per = (nwt + gridDim.x * NW - 1) / (gridDim.x * NW);
+    const uint32_t gw = blockIdx.x * NW + wid;
+    const uint32_t w0 = min(nwt, gw * per), w1 = min(nwt, w0 + per);
     // prologue (complete before the first marks, which come after pass 0's barriers)
-    for (uint64_t p = (uint64_t)t0 * RK_TILE + tid; p < min((uint64_t)t1 * RK_TILE, (uint64_t)nrec); p += RK_THREADS) {
+    for (uint64_t p = (uint64_t)w0 * RK_WT + lane; p < min((uint64_t)w1 * RK_WT, (uint64_t)nrec); p += 32) {
         const uint64_t k = __ldg(&keys[p]);
         memo.recpos[__ldg(&memo.rec_off[key_idx(k)]) + key_j(k)] = (uint32_t)p;
     }
@@ -347,27 +400,35 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
         const bool all = pass < 2 || !use_dirty;   // passes 0 and 1 sweep everything; marks start in pass 1
         if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (pass + 1) % 3] = 0;
         if (blockIdx.x == 0) tmax(pass, 0);
-        if (tid == 0) s_chg = 0;
-        // A: aggregate of this CTA's range
+        if (tid == 0) { s_chg = 0; s_swept = 0; s_sweeps = 0; }
+        // A: aggregate of this warp's range, then of the CTA's
         Xf mine = OpXf::identity();
-        for (uint32_t tile = t0; tile < t1; ++tile) {
+        for (uint32_t wt = w0; wt < w1; ++wt) {
             Xf tot;
-            // the bit can be set concurrently by other CTAs: one thread reads it for the CTA
-            if (!all && !__syncthreads_or(tid == 0 && rk_is_dirty(memo.dirty, tile))) {
-                tot = memo.aggA[tile];
+            // the bit can be set concurrently by other warps: lane 0 reads it for the warp
+            const uint32_t dirty = all ? 1u : __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)rk_is_dirty(memo.dirty, wt) : 0u, 0);
+            if (!dirty) {
+                tot = memo.aggA[wt];
             } else {
-                const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);
+                const uint32_t hw = rk_wload(keys, nrec, wt, stage);
                 int dv[RK_ITEMS];
-                rk_gather(stage, hw, D, dv);
-                block_scan_excl<Xf, OpXf>(rk_compose(hw, dv), tot, sm);
+                rk_wgather(stage, hw, D, dv);
+                rk_wscan(rk_compose(hw, dv), tot);
             }
             mine = OpXf::combine(mine, tot);
         }
-        if (tid == 0) lb_store(&cta_agg[blockIdx.x], mine);
+        if (lane == 0) wagg[wid] = mine;
+        __syncthreads();
+        if (tid == 0) {
+            Xf c = OpXf::identity();
+            for (uint32_t j = 0; j < NW; ++j) c = OpXf::combine(c, wagg[j]);
+            lb_store(&cta_agg[blockIdx.x], c);
+        }
         tmax(pass, 1);
         grid_sync(bar);
         if (blockIdx.x == 0) tmax(pass, 2);
-        // C: state entering this CTA's range = composition of the aggregates before it
+        // C: state entering this warp's range = the CTA aggregates before it, then the
+        // warp aggregates of this CTA before it
         Xf carry = OpXf::identity();
         for (uint32_t c0 = 0; c0 < blockIdx.x; c0 += RK_THREADS) {
             const Xf x = (c0 + tid < blockIdx.x) ? lb_load(&cta_agg[c0 + tid]) : OpXf::identity();
@@ -375,19 +436,22 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
             block_scan_excl<Xf, OpXf>(x, tot, sm);
             carry = OpXf::combine(carry, tot);
         }
-        // D: sweep the tiles in order
+        for (uint32_t j = 0; j < wid; ++j) carry = OpXf::combine(carry, wagg[j]);
+        // D: sweep the warp-tiles in order
         uint32_t swept = 0, sweeps = 0;
-        for (uint32_t tile = t0; tile < t1; ++tile) {
-            const bool dirty = all || __syncthreads_or(tid == 0 && rk_is_dirty(memo.dirty, tile));
-            if (!dirty && xf_eq(carry, memo.carD[tile])) {       // same inputs and state: settled
-                carry = OpXf::combine(carry, memo.aggA[tile]);
+        bool wchg = false;
+        for (uint32_t wt = w0; wt < w1; ++wt) {
+            const uint32_t dirty = all ? 1u : __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)rk_is_dirty(memo.dirty, wt) : 0u, 0);
+            if (!dirty && xf_eq(carry, memo.carD[wt])) {           // same inputs and state: settled
+                carry = OpXf::combine(carry, memo.aggA[wt]);
                 continue;
             }
-            if (tid == 0) {
-                if (dirty) atomicAnd(&memo.dirty[tile >> 5], ~(1u << (tile & 31)));
+            if (lane == 0) {
+                if (dirty) atomicAnd(&memo.dirty[wt >> 5], ~(1u << (wt & 31)));
                 __threadfence();           // clear before gathering: a later raise re-marks
             }
-            const uint32_t hw = rk_load(keys, nrec, tile, stage, &s_prev);   // (syncs the CTA)
+            __syncwarp();
+            const uint32_t hw = rk_wload(keys, nrec, wt, stage);
             ++swept;
             Xf last_tot = OpXf::identity();
             bool settled = false;
@@ -395,9 +459,9 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
             for (uint32_t it = 0; it < local_max; ++it) {
                 ++sweeps;
                 int dv[RK_ITEMS];
-                rk_gather(stage, hw, D, dv);
+                rk_wgather(stage, hw, D, dv);
                 Xf tot;
-                const Xf ex = block_scan_excl<Xf, OpXf>(rk_compose(hw, dv), tot, sm);
+                const Xf ex = rk_wscan(rk_compose(hw, dv), tot);
                 last_tot = tot;
                 Xf cur = OpXf::combine(carry, ex);
                 int L[RK_ITEMS];
@@ -416,38 +480,40 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
                 uint32_t old[RK_ITEMS];    // all raises in flight together
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k)
-                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[tid * RK_ITEMS + k])], (uint32_t)L[k])
+                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k])
                                           : 0xFFFFFFFFu;
                 bool chg = false;
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k)
                     if (old[k] < (uint32_t)L[k]) { chg = true; raised |= 1u << k; }
-                if (!__syncthreads_or(chg)) {
+                if (!__any_sync(0xffffffffu, chg)) {
                     // this sweep raised nothing: its aggregate and incoming state are the
                     // tile's fixpoint until a record's transaction is raised
-                    if (tid == 0) { memo.carD[tile] = carry; memo.aggA[tile] = tot; }
+                    if (lane == 0) { memo.carD[wt] = carry; memo.aggA[wt] = tot; }
                     settled = true;
                     break;
                 }
-                if (tid == 0) s_chg = 1;
+                wchg = true;
             }
-            if (!settled && tid == 0) {    // sweep cap hit: sweep again next pass
-                memo.aggA[tile] = last_tot;
-                atomicOr(&memo.dirty[tile >> 5], 1u << (tile & 31));
+            if (!settled && lane == 0) {   // sweep cap hit: sweep again next pass
+                memo.aggA[wt] = last_tot;
+                atomicOr(&memo.dirty[wt >> 5], 1u << (wt & 31));
             }
             if (use_dirty && pass >= 1 && raised) {     // mark the other tiles of the raised transactions
                 __threadfence();           // the raises are visible before the marks
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k)
-                    if ((raised >> k) & 1u) rk_mark(memo, key_idx(stage[tid * RK_ITEMS + k]), tile);
+                    if ((raised >> k) & 1u) rk_mark(memo, key_idx(stage[lane * RK_ITEMS + k]), wt);
             }
             carry = OpXf::combine(carry, last_tot);
         }
+        if (lane == 0 && wchg) s_chg = 1;
+        if (trace && lane == 0) { atomicAdd(&s_swept, swept); atomicAdd(&s_sweeps, sweeps); }
         __syncthreads();
         if (tid == 0 && s_chg) sc[SC_CHG0 + pass % 3] = 1;
         if (trace && tid == 0 && pass < RANK_TRACE_SLOTS / 8) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 5]), (unsigned long long)swept);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 6]), (unsigned long long)sweeps);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 5]), (unsigned long long)s_swept);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 6]), (unsigned long long)s_sweeps);
         }
         tmax(pass, 3);
         grid_sync(bar);

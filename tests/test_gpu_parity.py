@@ -169,3 +169,33 @@ def test_reset_restores_pristine():
     assert db.inserts()["history"]["h_ts"].size == 0
     run_both(W.TPCB, dims, image, [W.tpcb_bulk(dims, 5000, seed=1)], "part", db=db)
     db.close()
+
+
+TS_COLUMNS = {"h_ts", "o_entry_d", "h_date"}     # insert columns that hold the transaction's ts
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("schema", [W.TPCB, W.TPCC])
+def test_explicit_timestamps(strategy, schema):
+    """gputx_bulk.ts (caller-given global timestamps): same execution order as
+    position order, and the ts-valued insert columns carry the given timestamps."""
+    if schema == W.TPCB:
+        dims = W.TpcbDims(8, 10, 500)
+        bulk = W.tpcb_bulk(dims, 5000, seed=21, remote_pct=20.0)
+    else:
+        dims = W.TpccDims(4, 10, 300, 2000)
+        bulk = W.tpcc_bulk(dims, 4000, seed=22, remote_line_pct=5.0)
+    image = W.make_db(schema, dims, seed=5)
+    ts = (np.arange(bulk.n, dtype=np.int64) * 7 + 1000).astype(np.uint32)
+    ref = oracle.run(schema, dims.dims, image, bulk)
+    for tab, cols in ref.inserts.items():
+        for c in cols:
+            if c in TS_COLUMNS:
+                cols[c] = ts[cols[c].astype(np.int64)].astype(cols[c].dtype)
+    db = gpu_db(schema, dims, image, bulk.n)
+    try:
+        db.submit(bulk, ts=ts)
+        db.execute(strategy)
+        compare(schema, ref, db, image, label=f"{strategy} explicit ts")
+    finally:
+        db.close()

@@ -743,6 +743,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
     db->sync_stages = getenv("GPUTX_SYNC") != nullptr;
     if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
+    if (const char* e = getenv("GPUTX_TPL_SLEEP")) {
+        const uint32_t cap = (uint32_t)atoi(e);
+        cudaMemcpyToSymbol(g_tpl_sleep_cap, &cap, 4);
+    }
     // K-SET executor: thread-block clusters of kset_cluster CTAs (rounds of <= that many
     // CTAs are separated by the hardware cluster barrier); 0 disables clusters
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));

@@ -569,6 +569,37 @@ template <int S> __device__ __noinline__ void exec_local(const DevDb& db, uint32
 
 // The combined kernel body: one whole transaction (K-SET, TPL).  Sharded: a transaction
 // with a fragment on another shard runs only its local fragments.
+// Warm L2 with the rows a transaction of a coming k-set round will touch (from its
+// staged parameters).  prefetch.global.L2 returns no data, so it is safe while the
+// current round may still write those rows: the round's own loads come after the
+// round barrier and then hit L2 instead of HBM.
+DEV void l2_warm(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+template <int S>
+DEV void warm_rows(const DevDb& db, uint32_t t, const uint32_t* p) {
+    if (S == S_TPCB) {
+        l2_warm(&COL(const int64_t, B_ACC)[p[0]]);
+    } else if (S == S_TM1) {
+        if (p[0] == 0) return;
+        const uint64_t s = p[0] - 1;
+        switch (t) {
+        case 0:
+            l2_warm(&COL(const uint64_t, M_NBR)[s]); l2_warm(&COL(const uint64_t, M_HEX)[s]);
+            l2_warm(&COL(const uint32_t, M_MSC)[s]); l2_warm(&COL(const uint32_t, M_VLR)[s]);
+            l2_warm(&COL(const uint16_t, M_BITS)[s]); l2_warm(COL(const uint8_t, M_BYTE2) + s * 10);
+            break;
+        case 1: case 5: case 6: {
+            const uint64_t f = s * 4 + ((t == 1 ? p[1] : p[2]) - 1);
+            l2_warm(&COL(const uint8_t, M_SF_VALID)[f]); l2_warm(&COL(const uint8_t, M_CF_LIVE)[f * 3]);
+            l2_warm(&COL(const uint8_t, M_CF_END)[f * 3]); l2_warm(&COL(const uint64_t, M_CF_NUM)[f * 3]);
+            break;
+        }
+        case 2: l2_warm(&COL(const uint8_t, M_AI_VALID)[s * 4 + p[1] - 1]); break;
+        case 3: l2_warm(&COL(const uint16_t, M_BITS)[s]); l2_warm(&COL(const uint8_t, M_SF_VALID)[s * 4 + p[1] - 1]); break;
+        case 4: l2_warm(&COL(const uint32_t, M_VLR)[s]); break;
+        }
+    }
+}
+
 template <int S, bool SH = false>
 DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     if (SH && db.xflag && db.xflag[idx]) { exec_local<S>(db, idx); return; }

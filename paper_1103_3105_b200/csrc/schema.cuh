@@ -574,30 +574,12 @@ template <int S> __device__ __noinline__ void exec_local(const DevDb& db, uint32
 // current round may still write those rows: the round's own loads come after the
 // round barrier and then hit L2 instead of HBM.
 DEV void l2_warm(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+// TPC-B only: its round-to-round critical path is one HBM miss on the account row (1e8
+// accounts); TM-1's rows are hot in L2 already and the extra instructions cost more
+// (K-SET exec 0.73 -> 0.79 ms measured), TPC-C stages no parameters.
 template <int S>
 DEV void warm_rows(const DevDb& db, uint32_t t, const uint32_t* p) {
-    if (S == S_TPCB) {
-        l2_warm(&COL(const int64_t, B_ACC)[p[0]]);
-    } else if (S == S_TM1) {
-        if (p[0] == 0) return;
-        const uint64_t s = p[0] - 1;
-        switch (t) {
-        case 0:
-            l2_warm(&COL(const uint64_t, M_NBR)[s]); l2_warm(&COL(const uint64_t, M_HEX)[s]);
-            l2_warm(&COL(const uint32_t, M_MSC)[s]); l2_warm(&COL(const uint32_t, M_VLR)[s]);
-            l2_warm(&COL(const uint16_t, M_BITS)[s]); l2_warm(COL(const uint8_t, M_BYTE2) + s * 10);
-            break;
-        case 1: case 5: case 6: {
-            const uint64_t f = s * 4 + ((t == 1 ? p[1] : p[2]) - 1);
-            l2_warm(&COL(const uint8_t, M_SF_VALID)[f]); l2_warm(&COL(const uint8_t, M_CF_LIVE)[f * 3]);
-            l2_warm(&COL(const uint8_t, M_CF_END)[f * 3]); l2_warm(&COL(const uint64_t, M_CF_NUM)[f * 3]);
-            break;
-        }
-        case 2: l2_warm(&COL(const uint8_t, M_AI_VALID)[s * 4 + p[1] - 1]); break;
-        case 3: l2_warm(&COL(const uint16_t, M_BITS)[s]); l2_warm(&COL(const uint8_t, M_SF_VALID)[s * 4 + p[1] - 1]); break;
-        case 4: l2_warm(&COL(const uint32_t, M_VLR)[s]); break;
-        }
-    }
+    if (S == S_TPCB) l2_warm(&COL(const int64_t, B_ACC)[p[0]]);
 }
 
 template <int S, bool SH = false>

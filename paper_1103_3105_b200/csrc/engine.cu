@@ -737,7 +737,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_RANK_DIRTY")) db->rank_dirty = (uint32_t)atoi(e);
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
-    db->kset_q = schema == S_TPCC ? 16 : schema == S_TPCB ? 64 : 128;
+    db->kset_q = schema == S_TPCC ? 8 : schema == S_TPCB ? 64 : 128;   // TPC-C: one warp per txn, 8 warps
     db->kset_cluster = schema == S_TPCB ? 16 : 8;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
@@ -789,6 +789,15 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
             continue;
         }
         db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
+        // the explicit-ts / sharded variant must fit the same cooperative grid
+        const void* kfn_ts = schema == S_TPCB ? kset_fn<S_TPCB>(true) : schema == S_TM1 ? kset_fn<S_TM1>(true)
+                                                                                       : kset_fn<S_TPCC>(true);
+        int per_ts = 0, ncl_ts = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ts, kfn_ts, kblock, 0);
+        if (cudaOccupancyMaxActiveClusters(&ncl_ts, kfn_ts, &lc) == cudaSuccess && ncl_ts >= 1)
+            db->kset_grid = std::min(db->kset_grid, ncl_ts * (int)db->kset_cluster);
+        db->kset_grid = std::min(db->kset_grid, std::max(1, per_ts) * db->nsm);
+        cudaGetLastError();
         break;
     }
     if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);

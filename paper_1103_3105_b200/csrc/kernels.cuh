@@ -683,10 +683,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         slo = lo + b * chunk;
         shi = min(hi, slo + chunk);
     };
+    // TPC-C: one warp per transaction (tpcc_txn_warp); nothing is staged per thread
+    constexpr bool WARPX = S == S_TPCC;
     auto prefetch = [&](uint32_t lo, uint32_t hi) {     // [lo, hi) = this CTA's slice
         const uint32_t j = lo + tid;
         nidx = 0xFFFFFFFFu;
-        if (j < hi) {
+        if (!WARPX && j < hi) {
             nidx = __ldg(&perm[j]);
             if (PW > 0) {
                 nt = __ldg(&ptype[j]);
@@ -798,7 +800,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             slice(lo, hi, G(k2), lo, hi);
             if (!(diag & 8u)) prefetch(lo, hi);
         }
-        if (cidx != 0xFFFFFFFFu && !(diag & 1u)) {
+        if (!WARPX && cidx != 0xFFFFFFFFu && !(diag & 1u)) {
             const bool tt = trace && (diag & 2u);
             const uint64_t t0 = tt ? globaltimer_ns() : 0;
             if (PW > 0) exec_txn_p<S, SH>(db, cidx, ct, cp);
@@ -809,7 +811,9 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                           (unsigned long long)((d << 24) | cidx));
             }
         }
-        for (uint32_t j = (diag & 1u) ? chi : clo + KB + tid; j < chi; j += KB) {
+        if (WARPX && !(diag & 1u))
+            for (uint32_t j = clo + (tid >> 5); j < chi; j += KB / 32) exec_txn_warp<SH>(db, __ldg(&perm[j]));
+        for (uint32_t j = (diag & 1u) || WARPX ? chi : clo + KB + tid; j < chi; j += KB) {
             if (PW > 0) {
                 uint32_t q[PW > 0 ? PW : 1];
 #pragma unroll

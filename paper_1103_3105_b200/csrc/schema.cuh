@@ -565,7 +565,125 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, 
     }
 }
 
+// The same TPC-C transaction executed by a whole warp (K-SET, TPL): NewOrder line l is
+// lane l's.  One thread issuing a NewOrder's ~270 scattered loads and stores serially
+// was the per-round critical path (~5 us); spread over the lanes it is ~20 per lane.
+// Same results as tpcc_txn: a repeated stock row sees its earlier line's update (the
+// updates are chained through the lanes in line order) and only its last line stores it.
+DEV void tpcc_txn_warp(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, bool sh) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t lane = lane_id();
+    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
+    const uint32_t w = p[0], d = p[1];
+    const uint64_t wd = (uint64_t)w * D + d;
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    if (t != 0) {                                 // Payment: small, lane 0
+        if (lane != 0) return;
+        if (p[4] == 2) { db.status[idx] = 1; return; }
+        const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
+        const int64_t cbal = ldm(&COL(int64_t, C_C_BAL)[cx]);
+        const uint8_t credit = __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]);
+        const uint64_t rh = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
+        const uint32_t h = p[6];
+        red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
+        red_add(&COL(int64_t, C_D_YTD)[wd], (int64_t)h);
+        INS(uint32_t, IH_C)[rh] = p[5]; INS(uint32_t, IH_CD)[rh] = p[3]; INS(uint32_t, IH_CW)[rh] = p[2];
+        INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = txn_ts(db, idx, sh);
+        INS(int32_t, IH_AMT)[rh] = (int32_t)h;
+        const int64_t nb = cbal - (int64_t)h;
+        stm(&COL(int64_t, C_C_BAL)[cx], nb);
+        red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
+        red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
+        put32(o, p[5]);
+        put32(o + 4, credit);
+        put64(o + 8, (uint64_t)nb);
+        return;
+    }
+    const uint32_t cnt = min(p[3], 15u);
+    const bool has = lane < cnt;
+    uint32_t li = 0, lsw = 0, lq = 0;
+    if (has) { li = p[4 + 3 * lane]; lsw = p[5 + 3 * lane]; lq = p[6 + 3 * lane]; }
+    if (__any_sync(FULL, has && li >= I)) {       // unused item: roll back (static)
+        if (lane == 0) db.status[idx] = 1;
+        return;
+    }
+    // ---- load phase
+    uint32_t oid = 0;
+    int64_t disc = 0, tax = 0;
+    uint64_t ro = 0, rn = 0, rl0 = 0;
+    if (lane == 0) {
+        oid = ldm(&COL(uint32_t, C_D_NEXT)[wd]);
+        disc = __ldg(&COL(const int32_t, C_C_DISC)[wd * C + p[2]]);
+        tax = (int64_t)__ldg(&COL(const int32_t, C_W_TAX)[w]) + __ldg(&COL(const int32_t, C_D_TAX)[wd]);
+        ro = db.ins_base[T_ORDER] + db.ins_off[T_ORDER * (uint64_t)db.ins_stride + idx];
+        rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
+    }
+    if (lane == 1 || cnt == 0) rl0 = db.ins_base[T_OLINE] + db.ins_off[T_OLINE * (uint64_t)db.ins_stride + idx];
+    const uint64_t sidx = has ? (uint64_t)lsw * I + li : ~0ull - lane;     // unique for idle lanes
+    int32_t pr = 0, q0 = 0;
+    uint8_t br = 0;
+    if (has) {
+        pr = __ldg(&COL(const int32_t, C_I_PRICE)[li]);
+        br = __ldg(&COL(const uint8_t, C_I_ORIG)[li]) & __ldg(&COL(const uint8_t, C_S_ORIG)[sidx]);
+        q0 = ldm(&COL(int32_t, C_S_QTY)[sidx]);
+    }
+    oid = __shfl_sync(FULL, oid, 0);
+    rl0 = __shfl_sync(FULL, rl0, cnt == 0 ? 0 : 1);
+    // ---- stock recurrence in line order (duplicates chained through the lanes)
+    int32_t before = q0, cur = 0;
+    for (uint32_t m = 0; m < cnt; ++m) {
+        const int32_t bm = __shfl_sync(FULL, before, m);
+        const int32_t qm = (int32_t)__shfl_sync(FULL, lq, m);
+        const uint64_t sm = __shfl_sync(FULL, sidx, m);
+        const int32_t cm = bm >= qm + 10 ? bm - qm : bm - qm + 91;
+        if (lane == m) cur = cm;
+        if (lane > m && sidx == sm) before = cm;      // a later line of the same row sees it
+    }
+    const uint32_t peers = __match_any_sync(FULL, sidx);
+    const bool last_of_row = has && (31 - __clz(peers)) == (int)lane;
+    // ---- writes
+    const int32_t amount = has ? (int32_t)lq * pr : 0;
+    int64_t sum = amount;
+#pragma unroll
+    for (int sh2 = 16; sh2; sh2 >>= 1) sum += __shfl_xor_sync(FULL, sum, sh2);
+    const bool all_local = __all_sync(FULL, !has || lsw == w);
+    if (has) {
+        const uint64_t rl = rl0 + lane;
+        INS(uint32_t, IL_OID)[rl] = oid; INS(uint32_t, IL_D)[rl] = d; INS(uint32_t, IL_W)[rl] = w;
+        INS(uint32_t, IL_NUM)[rl] = lane; INS(uint32_t, IL_I)[rl] = li; INS(uint32_t, IL_SW)[rl] = lsw;
+        INS(uint32_t, IL_QTY)[rl] = lq; INS(int32_t, IL_AMT)[rl] = amount;
+        put32(o + 16 + 12 * lane, (uint32_t)before);
+        put32(o + 16 + 12 * lane + 4, (uint32_t)amount);
+        o[16 + 12 * lane + 8] = br;
+        red_add(&COL(int64_t, C_S_YTD)[sidx], (int64_t)lq);
+        red_add(&COL(uint32_t, C_S_OCNT)[sidx], 1u);
+        if (lsw != w) red_add(&COL(uint32_t, C_S_RCNT)[sidx], 1u);
+        if (last_of_row) stm(&COL(int32_t, C_S_QTY)[sidx], cur);
+    }
+    if (lane == 0) {
+        stm(&COL(uint32_t, C_D_NEXT)[wd], oid + 1);
+        INS(uint32_t, IO_ID)[ro] = oid; INS(uint32_t, IO_D)[ro] = d; INS(uint32_t, IO_W)[ro] = w;
+        INS(uint32_t, IO_C)[ro] = p[2]; INS(uint32_t, IO_ENTRY)[ro] = txn_ts(db, idx, sh);
+        INS(uint32_t, IO_OLCNT)[ro] = cnt; INS(uint32_t, IO_ALLLOCAL)[ro] = all_local ? 1u : 0u;
+        INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
+        const int64_t x = sum * (10000 - disc) * (10000 + tax);
+        put32(o, oid);
+        put32(o + 4, cnt);
+        put64(o + 8, (uint64_t)((x + 50000000) / 100000000));
+    }
+}
+
 template <int S> __device__ __noinline__ void exec_local(const DevDb& db, uint32_t idx);
+
+// one TPC-C transaction by the calling (whole) warp
+template <bool SH>
+DEV void exec_txn_warp(const DevDb& db, uint32_t idx) {
+    if (SH && db.xflag && db.xflag[idx]) {        // cross-shard: its local fragments, lane 0
+        if (lane_id() == 0) exec_local<S_TPCC>(db, idx);
+        return;
+    }
+    tpcc_txn_warp(db, idx, db.type[idx], db.pw + db.poff[idx], SH);
+}
 
 // The combined kernel body: one whole transaction (K-SET, TPL).  Sharded: a transaction
 // with a fragment on another shard runs only its local fragments.

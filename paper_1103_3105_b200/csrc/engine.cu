@@ -489,6 +489,10 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v) {
         const uint32_t grid = std::min<uint64_t>((uint32_t)std::max(1, per) * (uint32_t)db->nsm, (db->n + 255) / 256);
         if (sh) tpl_exec_persistent_kernel<S, true><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
         else tpl_exec_persistent_kernel<S, false><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+    } else if (S == S_TPCC) {                 // one warp per transaction
+        const uint32_t grid = (uint32_t)((db->n + 3) / 4);
+        if (sh) tpl_exec_warp_kernel<true><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        else tpl_exec_warp_kernel<false><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
     } else {
         const uint32_t tb = 128, grid = (uint32_t)((db->n + tb - 1) / tb);
         if (sh) tpl_exec_kernel<S, true><<<grid, tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);

@@ -1242,6 +1242,47 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
     }
 }
 
+// TPL for TPC-C: one warp per transaction.  Lane j waits for the lock of record j (all
+// of a transaction's locks are requested at once: keys order every lock's queue by ts,
+// so a transaction only ever waits for earlier ones and the order of requests cannot
+// deadlock), then the warp runs tpcc_txn_warp and every lane releases its lock.
+template <bool SH>
+__global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
+                                                            const uint32_t* __restrict__ lkey, uint32_t* lock,
+                                                            uint32_t* sc) {
+    __shared__ uint32_t s_base;
+    if (threadIdx.x == 0) s_base = atomicAdd(&sc[SC_TICKET], blockDim.x / 32);   // ts-ordered dispatch
+    __syncthreads();
+    const uint32_t idx = s_base + (threadIdx.x >> 5);
+    if (idx >= db.n) return;                                   // warp-uniform
+    const uint32_t lane = lane_id();
+    Rec r[MAX_REC];
+    const int k = footprint_local<S_TPCC>(db, db.type[idx], db.pw + db.poff[idx], r);
+    uint64_t item = 0;
+#pragma unroll
+    for (int j = 0; j < MAX_REC; ++j)
+        if (j < k && (uint32_t)j == lane) item = r[j].item;
+    const bool mine = (int)lane < k;
+    const uint32_t key = mine ? __ldg(&lkey[rec_off[idx] + lane]) : 0u;
+    bool got = !mine;
+    uint32_t polls = 0;
+    while (!__all_sync(0xffffffffu, got)) {
+        uint32_t gap = 0xFFFFFFFFu;
+        if (!got) {
+            const uint32_t v = ld_acquire(&lock[item]);
+            got = v >= key;
+            if (!got) gap = key - v;
+        }
+        if (__all_sync(0xffffffffu, got)) break;
+        if (++polls > SPIN_LIMIT) { if (lane == 0) atomicExch(&sc[SC_DEADLOCK], 1u); break; }
+        const uint32_t g = __reduce_min_sync(0xffffffffu, gap);
+        __nanosleep(g == 1 ? (polls > 8 ? 32u : 0u) : min(g * 32u, g_tpl_sleep_cap));
+    }
+    exec_txn_warp<SH>(db, idx);
+    __threadfence();
+    if (mine) atomicAdd(&lock[item], 1u);
+}
+
 // Persistent TPL: every lane takes its next transaction as soon as it has released the
 // previous one (warp-aggregated ticket grab, tickets in ts order).  A lane holding
 // ticket t waits only for transactions with smaller tickets, all of which were taken

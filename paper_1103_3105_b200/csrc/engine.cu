@@ -460,7 +460,11 @@ gputx_status run_part(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[4], s);
     cudaEventRecord(db->ev[5], s);
     const uint32_t pb = 128;
-    part_exec_kernel<S><<<(db->nparts + pb - 1) / pb, pb, 0, s>>>(v, db->d_sorted, db->d_part_off, db->nparts, db->d_sc);
+    if (S == S_TPCC)
+        part_exec_warp_kernel<<<(db->nparts * 32 + pb - 1) / pb, pb, 0, s>>>(v, db->d_sorted, db->d_part_off, db->nparts,
+                                                                             db->d_sc);
+    else
+        part_exec_kernel<S><<<(db->nparts + pb - 1) / pb, pb, 0, s>>>(v, db->d_sorted, db->d_part_off, db->nparts, db->d_sc);
     ++db->launches;
     cudaEventRecord(db->ev[6], s);
     return GPUTX_OK;

@@ -895,6 +895,28 @@ __global__ void __launch_bounds__(256) part_bounds_kernel(const uint64_t* frags,
         for (int64_t p = prev + 1; p <= pid; ++p) part_off[p] = k;
     }
 }
+// TPC-C: one warp per partition; a whole-transaction fragment runs as tpcc_txn_warp,
+// split fragments (remote lines / customer) on lane 0
+__global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uint64_t* __restrict__ frags,
+                                                             const uint32_t* __restrict__ part_off, uint32_t nparts,
+                                                             uint32_t* sc) {
+    const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (p >= nparts) return;                                   // warp-uniform
+    const uint32_t lo = part_off[p], hi = part_off[p + 1];
+    const bool sh = db.ts != nullptr;
+    for (uint32_t j = lo; j < hi; ++j) {
+        const uint64_t fk = __ldg(&frags[j]);
+        const uint32_t idx = (uint32_t)(fk >> 8) & 0xFFFFFFu;
+        if ((fk & 0xFFu) == F_WHOLE || (db.type[idx] == 0 && fragments<S_TPCC>(db, idx, nullptr) == 1)) {
+            tpcc_txn_warp(db, idx, db.type[idx], db.pw + db.poff[idx], sh);
+        } else {
+            if (lane_id() == 0) exec_frag<S_TPCC>(db, fk);
+            __syncwarp();
+        }
+    }
+    if (lane_id() == 0 && hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
+}
+
 template <int S>
 __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t* __restrict__ frags,
                                                         const uint32_t* __restrict__ part_off, uint32_t nparts, uint32_t* sc) {

@@ -529,6 +529,131 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
     }
 }
 
+// Root-local rank (TM-1): every warp owns a range of whole roots (a root = all items of
+// one subscriber, adjacent in the sorted records) and sweeps it until it raises nothing.
+// A transaction whose records all lie in one root is settled by its root alone, so when
+// no transaction crosses roots the first pass reaches the fixpoint everywhere and the
+// second only confirms it; transactions that do cross roots are still exact: passes
+// repeat (grid barrier between them) until one raises nothing.  This replaces ~12 grid
+// passes over CTA-sized ranges (hot NURand subscribers spanning several ranges) by
+// warp-local sweeps with no inter-warp dependence.
+template <int S>
+DEV uint64_t rr_root(const DevDb& db, uint64_t key) { return item_root<S>(db, key_item(key)); }
+
+// first record at or after p that starts a root (p itself if p == 0 or p >= nrec)
+template <int S>
+DEV uint32_t rr_align(const DevDb& db, const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t p) {
+    if (p == 0 || p >= nrec) return min(p, nrec);
+    const uint64_t r0 = rr_root<S>(db, __ldg(&keys[p - 1]));
+    for (uint32_t b = p; b < nrec; b += 32) {
+        const uint32_t i = b + lane_id();
+        const bool edge = i < nrec && rr_root<S>(db, __ldg(&keys[i])) != r0;
+        const uint32_t m = __ballot_sync(0xffffffffu, edge);
+        if (m) return b + __ffs(m) - 1;
+    }
+    return nrec;
+}
+
+template <int S>
+__global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const uint64_t* __restrict__ keys,
+                                                               const uint32_t* nrec_ptr, uint32_t* D, GridBar* bar,
+                                                               uint32_t* sc, uint32_t max_passes, uint64_t* trace) {
+    constexpr uint32_t NW = RK_THREADS / 32;
+    __shared__ uint64_t stage_all[NW * RK_WT];
+    __shared__ int s_chg;
+    const uint32_t nrec = *nrec_ptr;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+    uint64_t* stage = stage_all + wid * RK_WT;
+    const uint32_t TW = gridDim.x * NW, gw = blockIdx.x * NW + wid;
+    const uint32_t chunk = (nrec + TW - 1) / TW;
+    const uint32_t r0 = rr_align<S>(db, keys, nrec, gw * chunk);
+    const uint32_t r1 = rr_align<S>(db, keys, nrec, (gw + 1) * chunk);
+    for (uint32_t pass = 0;; ++pass) {
+        if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (pass + 1) % 3] = 0;
+        if (tid == 0) s_chg = 0;
+        if (trace && blockIdx.x == 0 && tid == 0 && pass < RANK_TRACE_SLOTS / 8) trace[8 * pass] = globaltimer_ns();
+        __syncthreads();
+        bool wchg = false;
+        uint32_t sweeps = 0;
+        for (;; ++sweeps) {
+            bool raised = false;
+            Xf carry = OpXf::identity();
+            for (uint32_t c = r0; c < r1; c += RK_WT) {
+                // chunk [c, min(c + RK_WT, r1)) into the warp's stage
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    const uint32_t i = k * 32 + lane;
+                    stage[i] = c + i < r1 ? __ldg(&keys[c + i]) : ~0ull;
+                }
+                const uint64_t prev = c ? __ldg(&keys[c - 1]) : ~0ull;
+                __syncwarp();
+                uint32_t hw = 0;
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    const uint32_t pos = lane * RK_ITEMS + k;
+                    if (c + pos < r1) {
+                        const uint64_t key = stage[pos];
+                        const uint64_t pk = pos ? stage[pos - 1] : prev;
+                        const bool head = (c + pos == 0) || key_item(pk) != key_item(key);
+                        hw |= (head ? 1u : 0u) << (2 * k);
+                        hw |= key_w(key) << (2 * k + 1);
+                        hw |= 1u << (16 + k);
+                    }
+                }
+                int dv[RK_ITEMS];
+                rk_wgather(stage, hw, D, dv);
+                Xf tot;
+                const Xf ex = rk_wscan(rk_compose(hw, dv), tot);
+                Xf cur = OpXf::combine(carry, ex);
+                int L[RK_ITEMS];
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    L[k] = 0;
+                    if ((hw >> (16 + k)) & 1u) {
+                        const bool head = (hw >> (2 * k)) & 1u;
+                        const uint32_t w = (hw >> (2 * k + 1)) & 1u;
+                        const int d = dv[k];
+                        const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
+                        L[k] = w ? max(d, m + 1) : max(d, a + 1);
+                        cur = OpXf::combine(cur, rec_xf(head, w, d));
+                    }
+                }
+                uint32_t old[RK_ITEMS];
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k)
+                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k])
+                                          : 0xFFFFFFFFu;
+                bool chg = false;
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) chg |= old[k] < (uint32_t)L[k];
+                raised |= __any_sync(0xffffffffu, chg);
+                carry = OpXf::combine(carry, tot);
+            }
+            if (!raised) break;
+            wchg = true;
+            if (sweeps + 1 >= max_passes) break;
+        }
+        if (lane == 0 && wchg) s_chg = 1;
+        if (trace && lane == 0 && pass < RANK_TRACE_SLOTS / 8)
+            atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 6]), (unsigned long long)sweeps);
+        __syncthreads();
+        if (tid == 0 && s_chg) sc[SC_CHG0 + pass % 3] = 1;
+        if (trace && tid == 0 && pass < RANK_TRACE_SLOTS / 8)
+            atomicMax(reinterpret_cast<unsigned long long*>(&trace[8 * pass + 3]), (unsigned long long)globaltimer_ns());
+        grid_sync(bar);
+        if (trace && blockIdx.x == 0 && tid == 0 && pass < RANK_TRACE_SLOTS / 8) trace[8 * pass + 4] = globaltimer_ns();
+        const uint32_t c = __ldcg(&sc[SC_CHG0 + pass % 3]);
+        if (!c || pass + 1 >= max_passes) {
+            if (blockIdx.x == 0 && tid == 0) {
+                sc[SC_PASSES] = pass + 1;
+                sc[SC_NOCONV] = c ? 1u : 0u;
+            }
+            return;
+        }
+    }
+}
+
 // =====================================================================================
 // group by (depth, type): counting sort.  Each CTA first aggregates its tile's keys in
 // a shared-memory table (open addressing) so hot keys (the 0-set of a wide graph) cost

@@ -1151,6 +1151,11 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     cudaEventRecord(db->ev[7], s);
     db->submitted = false;
     if (r != GPUTX_OK) return r;
+    if (n) {                                  // (status is 4-byte aligned: cudaMalloc)
+        count_aborts_kernel<<<grid_for(n / 4 + 1, 256, 148 * 4), 256, 0, s>>>(db->d_status, (uint32_t)n,
+                                                                              db->d_sc + SC_COMMITTED);
+        ++db->launches;
+    }
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
@@ -1190,11 +1195,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
         float tot = 0;
         cudaEventElapsedTime(&tot, db->ev[0], db->ev[7]);
         stats->ms_total = tot;
-        // committed count (status bytes, D2H once)
-        std::vector<uint8_t> stv(n);
-        if (n) CK(cudaMemcpy(stv.data(), db->d_status, n, cudaMemcpyDeviceToHost));
-        uint64_t ab = 0;
-        for (uint8_t x : stv) ab += x != 0;
+        const uint64_t ab = n ? db->h_sc[SC_COMMITTED] : 0;    // aborts, counted on the device
         stats->aborted = ab;
         stats->committed = n - ab;
     }

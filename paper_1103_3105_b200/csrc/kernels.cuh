@@ -1052,6 +1052,23 @@ __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t
     if (hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
 }
 
+// aborted transactions of the bulk (status != 0), for gputx_stats without a D2H of status
+__global__ void __launch_bounds__(256) count_aborts_kernel(const uint8_t* __restrict__ status, uint32_t n,
+                                                           uint32_t* out) {
+    uint32_t c = 0;
+    const uint32_t n4 = n / 4;
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(status);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        const uint32_t v = __ldg(&s4[i]);
+        c += ((v & 0xFFu) != 0) + ((v & 0xFF00u) != 0) + ((v & 0xFF0000u) != 0) + ((v & 0xFF000000u) != 0);
+    }
+    for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        c += status[i] != 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
 // =====================================================================================
 // shard exchange.  A transaction whose
 // fragments live on other shards is sent to each of them as a fixed-stride record

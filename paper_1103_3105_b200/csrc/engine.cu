@@ -156,7 +156,7 @@ struct gputx_db {
     uint32_t rank_epoch = 0;   // look-back epochs of rank passes (own array)
     uint32_t ticket_slot = 0;
     int nsm = 0;
-    int rank_grid = 0, kset_grid = 0;
+    int rank_grid = 0, kset_grid = 0, kset_grid_ts = 0;
     uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
     uint32_t rank_dirty = 1;                  // dirty-tile worklist (GPUTX_RANK_DIRTY overrides)
     uint32_t rank_root = 0;                   // root-local sweeps (GPUTX_RANK_ROOT overrides)
@@ -387,7 +387,8 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[5], s);
     // rounds
     {
-        uint32_t G = db->exec_grid_override ? db->exec_grid_override : (uint32_t)db->kset_grid;
+        const uint32_t Gv = (uint32_t)(db->has_ts ? db->kset_grid_ts : db->kset_grid);   // co-resident grid
+        uint32_t G = db->exec_grid_override ? std::min(db->exec_grid_override, Gv) : Gv;
         if (db->kset_cluster) G = std::max(db->kset_cluster, G / db->kset_cluster * db->kset_cluster);
         uint32_t* done = db->d_done;
         if (db->kset_diag & 16u) CK(cudaMemsetAsync(done, 0, db->n * 4, s));
@@ -814,21 +815,24 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
             continue;
         }
         db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
-        // the explicit-ts / sharded variant must fit the same cooperative grid
+        // the explicit-ts / sharded variant has its own cooperative grid
         const void* kfn_ts = schema == S_TPCB ? kset_fn<S_TPCB>(true) : schema == S_TM1 ? kset_fn<S_TM1>(true)
                                                                                        : kset_fn<S_TPCC>(true);
         int per_ts = 0, ncl_ts = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ts, kfn_ts, kblock, 0);
+        db->kset_grid_ts = std::max(1, per_ts) * db->nsm;
         if (cudaOccupancyMaxActiveClusters(&ncl_ts, kfn_ts, &lc) == cudaSuccess && ncl_ts >= 1)
-            db->kset_grid = std::min(db->kset_grid, ncl_ts * (int)db->kset_cluster);
-        db->kset_grid = std::min(db->kset_grid, std::max(1, per_ts) * db->nsm);
+            db->kset_grid_ts = std::min(db->kset_grid_ts, ncl_ts * (int)db->kset_cluster);
+        db->kset_grid_ts = std::min(db->kset_grid_ts, db->kset_grid);
         cudaGetLastError();
         break;
     }
     if (const char* e = getenv("GPUTX_KSET_GRID")) db->exec_grid_override = (uint32_t)std::min(atoi(e), db->kset_grid);
+    if (!db->kset_grid_ts) db->kset_grid_ts = db->kset_grid;
     if (getenv("GPUTX_DEBUG"))
-        fprintf(stderr, "gputx: schema %d kset grid %d block %d cluster %u Q %u rank grid %d local %u\n", schema,
-                db->kset_grid, kblock, db->kset_cluster, db->kset_q, db->rank_grid, db->rank_local);
+        fprintf(stderr, "gputx: schema %d kset grid %d (ts variant %d) block %d cluster %u Q %u rank grid %d local %u\n",
+                schema, db->kset_grid, db->kset_grid_ts, kblock, db->kset_cluster, db->kset_q, db->rank_grid,
+                db->rank_local);
     if (cudaStreamSynchronize(db->stream) != cudaSuccess) return bail(GPUTX_ECUDA);
     *out = db;
     return GPUTX_OK;

@@ -889,7 +889,9 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         // wait for round k-1 (nothing to wait for after a narrow round: cluster barrier).
         // g[k-1] is read from global memory: round k-1 may lie in the previous staged
         // chunk, and a chunk reload (__syncthreads) must not happen inside tid == 0 code.
-        const uint32_t gm1 = k > 0 ? (uint32_t)__ldg(&g[k - 1]) : 0u;
+        // (from the staged chunk when it holds k-1: a global load here is on the critical path)
+        const uint32_t gm1 = k == 0 ? 0u : (k - 1 >= cb && k - 1 < cb + KX_CH) ? (uint32_t)sg[k - 1 - cb]
+                                                                               : (uint32_t)__ldg(&g[k - 1]);
         const bool nar_m1 = C && gm1 <= C;
         if (k > 0 && !(nar && nar_m1)) {
             const bool mine = !C && (prev == k - 1) && gprev == 1;

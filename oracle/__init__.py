@@ -76,7 +76,8 @@ def _load():
         P = ctypes.c_void_p
         lib.orc_run.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P, ctypes.c_uint64, P, P, P, P]
         lib.orc_run.restype = ctypes.c_int
-        lib.orc_footprint.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P, P, P, P, ctypes.c_uint64]
+        lib.orc_footprint.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P, P, P, P, ctypes.c_uint64,
+                                      ctypes.c_int]
         lib.orc_footprint.restype = ctypes.c_int64
         lib.orc_depths.argtypes = [ctypes.c_uint64, P, P, P, P]
         lib.orc_depths.restype = ctypes.c_int
@@ -142,8 +143,10 @@ def run(schema: int, dims, db: dict, bulk, first_ts: int = 0) -> Result:
     return r
 
 
-def footprint(schema: int, dims, db: dict, bulk):
-    """(ops_off u64[n+1], items u64[m], modes u8[m]) — basic operations per txn."""
+def footprint(schema: int, dims, db: dict, bulk, add_rule: bool = False):
+    """(ops_off u64[n+1], items u64[m], modes u8[m]) — basic operations per txn.
+    modes: 0 read, 1 write, 2 add (only with add_rule: TPC-B teller/branch balances,
+    TPC-C W_YTD/D_YTD, which are only incremented and never read by an output)."""
     lib = _load()
     cols = [np.ascontiguousarray(db[k]) for k in COLS[schema]]
     n = bulk.n
@@ -157,7 +160,7 @@ def footprint(schema: int, dims, db: dict, bulk):
     if pw.size == 0:
         pw = np.zeros(1, np.uint32)
     m = lib.orc_footprint(schema, _ptr(_dims(dims)), _ptrs(cols), n, _ptr(tp), _ptr(po), _ptr(pw),
-                          _ptr(ops_off), _ptr(items), _ptr(modes), cap)
+                          _ptr(ops_off), _ptr(items), _ptr(modes), cap, int(add_rule))
     if m < 0:
         raise RuntimeError("footprint capacity")
     return ops_off, items[:m].copy(), modes[:m].copy()
@@ -179,9 +182,10 @@ def depths_from_ops(ops_off: np.ndarray, items: np.ndarray, modes: np.ndarray) -
     return out[:n]
 
 
-def depths(schema: int, dims, db: dict, bulk) -> np.ndarray:
-    """T-dependency-graph depth of every transaction of `bulk` against `db`."""
-    return depths_from_ops(*footprint(schema, dims, db, bulk))
+def depths(schema: int, dims, db: dict, bulk, add_rule: bool = False) -> np.ndarray:
+    """T-dependency-graph depth of every transaction of `bulk` against `db`
+    (add_rule: two increments of one item do not conflict)."""
+    return depths_from_ops(*footprint(schema, dims, db, bulk, add_rule))
 
 
 def run_sequence(schema: int, dims, db: dict, bulk, order, first_ts: int = 0) -> Result:

@@ -1,7 +1,9 @@
 """T-dependency graph on small pools — TEST INFRASTRUCTURE ONLY (pure Python).
 
 A pool is a list of transactions in timestamp order; each transaction is a list
-of basic operations (item, mode) with mode 'R' or 'W' (§4.1).
+of basic operations (item, mode) with mode 'R' or 'W' (§4.1), or 'A'
+(a commutative increment) under the ADD rule (PAPER.md:475(c):
+two adds of an item do not conflict; an add conflicts with reads and writes).
 These loops are for small pools (n <= a few hundred); full-size depths use
 oracle.depths() (the streaming recurrence in oracle.c).
 """
@@ -12,18 +14,25 @@ from collections import defaultdict
 
 
 def _norm(txn):
-    """Merge same-item operations of one transaction; W dominates (DESIGN.md R-S3)."""
+    """Merge same-item operations of one transaction; W dominates, differing modes
+    merge to W (DESIGN.md R-S3)."""
     m = {}
     for item, mode in txn:
-        m[item] = 'W' if (mode == 'W' or m.get(item) == 'W') else 'R'
+        old = m.get(item)
+        m[item] = mode if old in (None, mode) else 'W'
     return m
+
+
+def _ops_conflict(x: str, y: str) -> bool:
+    """Two operations on one item conflict unless both read or both add."""
+    return not (x == y and x in ('R', 'A'))
 
 
 def conflicting(t1, t2) -> bool:
     """two transactions conflict iff they have two operations on the
-    same data item and at least one is a write."""
+    same data item and at least one is a write (and, ADD rule, not both adds)."""
     a, b = _norm(t1), _norm(t2)
-    return any(x in b and ('W' in (a[x], b[x])) for x in a)
+    return any(x in b and _ops_conflict(a[x], b[x]) for x in a)
 
 
 def graph_by_definition(pool):

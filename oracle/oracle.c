@@ -352,7 +352,9 @@ int orc_run(int schema, const uint32_t* dims, void** cols, uint64_t n, const uin
 
 /* ============================================================================ */
 /* Conflict footprint (basic operations) and depths  */
-/* item = table tag << 48 | row;  mode 0 = read, 1 = write                         */
+/* item = table tag << 48 | row;  mode 0 = read, 1 = write, 2 = add (commutative    */
+/* increment; only with the ADD rule, SURVEY.md NEXT-1 / PAPER.md:475(c): two adds  */
+/* of one item do not conflict, an add conflicts with reads and writes)            */
 /* ============================================================================ */
 enum { T_ACC = 1, T_TEL, T_BR, T_BIT1, T_VLR, T_SFDA, T_CF, T_DNEXT, T_STOCK, T_WYTD, T_DYTD, T_CUST };
 #define ITEM(tag, row) (((uint64_t)(tag) << 48) | (uint64_t)(row))
@@ -360,7 +362,7 @@ enum { T_ACC = 1, T_TEL, T_BR, T_BIT1, T_VLR, T_SFDA, T_CF, T_DNEXT, T_STOCK, T_
 static int add_op(uint64_t* it, uint8_t* md, int k, uint64_t item, uint8_t mode)
 {
     for (int j = 0; j < k; ++j)
-        if (it[j] == item) { md[j] |= mode; return k; }   /* merge; W dominates */
+        if (it[j] == item) { if (md[j] != mode) md[j] = 1; return k; }   /* merge; differing modes -> W */
     it[k] = item;
     md[k] = mode;
     return k + 1;
@@ -369,13 +371,15 @@ static int add_op(uint64_t* it, uint8_t* md, int k, uint64_t item, uint8_t mode)
 /* Footprint of one transaction: only columns some registered type writes
  * produce operations (DESIGN.md R-S18).  Returns #ops (<= 16). */
 static int footprint(int schema, const uint32_t* dims, void** cols, int type, const uint32_t* p,
-                     uint64_t* it, uint8_t* md)
+                     uint64_t* it, uint8_t* md, int add_rule)
 {
     int k = 0;
+    /* balances / YTDs that only deposits / payments increment and no output reads */
+    const uint8_t inc = add_rule ? 2 : 1;
     if (schema == S_TPCB) {
         k = add_op(it, md, k, ITEM(T_ACC, p[0]), 1);
-        k = add_op(it, md, k, ITEM(T_TEL, p[1]), 1);
-        k = add_op(it, md, k, ITEM(T_BR, p[2]), 1);
+        k = add_op(it, md, k, ITEM(T_TEL, p[1]), inc);
+        k = add_op(it, md, k, ITEM(T_BR, p[2]), inc);
         return k;
     }
     if (schema == S_TM1) {
@@ -416,8 +420,8 @@ static int footprint(int schema, const uint32_t* dims, void** cols, int type, co
         return k;
     }
     int64_t c = p[4] ? tpcc_by_last(cols, dims, p[2], p[3], p[5]) : (int64_t)p[5];
-    k = add_op(it, md, k, ITEM(T_WYTD, p[0]), 1);
-    k = add_op(it, md, k, ITEM(T_DYTD, (uint64_t)p[0] * D + p[1]), 1);
+    k = add_op(it, md, k, ITEM(T_WYTD, p[0]), inc);
+    k = add_op(it, md, k, ITEM(T_DYTD, (uint64_t)p[0] * D + p[1]), inc);
     if (c >= 0) k = add_op(it, md, k, ITEM(T_CUST, ((uint64_t)p[2] * D + p[3]) * C + (uint64_t)c), 1);
     return k;
 }
@@ -425,14 +429,14 @@ static int footprint(int schema, const uint32_t* dims, void** cols, int type, co
 /* ops_off[n+1], items[], modes[] are filled; returns total ops or -1 if cap is short */
 int64_t orc_footprint(int schema, const uint32_t* dims, void** cols, uint64_t n, const uint8_t* type,
                       const uint32_t* param_off, const uint32_t* param_words,
-                      uint64_t* ops_off, uint64_t* items, uint8_t* modes, uint64_t cap)
+                      uint64_t* ops_off, uint64_t* items, uint8_t* modes, uint64_t cap, int add_rule)
 {
     uint64_t tot = 0;
     uint64_t it[16];
     uint8_t md[16];
     for (uint64_t i = 0; i < n; ++i) {
         ops_off[i] = tot;
-        int k = footprint(schema, dims, cols, type[i], param_words + param_off[i], it, md);
+        int k = footprint(schema, dims, cols, type[i], param_words + param_off[i], it, md, add_rule);
         if (tot + k > cap) return -1;
         for (int j = 0; j < k; ++j) { items[tot + j] = it[j]; modes[tot + j] = md[j]; }
         tot += k;
@@ -441,8 +445,14 @@ int64_t orc_footprint(int schema, const uint32_t* dims, void** cols, uint64_t n,
     return (int64_t)tot;
 }
 
-/* open-addressing map item -> (Wd, Md) */
-typedef struct { uint64_t key; int32_t wd, md; } slot_t;
+/* Streaming depth recurrence.  Per item, over the accesses so far in ts order:
+ *   rd = max depth of the last writer and the reads since it,
+ *   ad = max depth of the last writer and the adds since it   (-1 if none).
+ * A transaction's depth d = max over its operations of
+ *   read: ad + 1,   add: rd + 1,   write: max(rd, ad) + 1     (0 if it has none);
+ * then read: rd = max(rd, d); add: ad = max(ad, d); write: rd = ad = d.
+ * Without adds ad is the last writer's depth and this is the (Wd, Md) recurrence. */
+typedef struct { uint64_t key; int32_t rd, ad; } slot_t;
 
 int orc_depths(uint64_t n, const uint64_t* ops_off, const uint64_t* items, const uint8_t* modes,
                uint32_t* depth)
@@ -457,15 +467,17 @@ int orc_depths(uint64_t n, const uint64_t* ops_off, const uint64_t* items, const
         for (uint64_t j = ops_off[t]; j < ops_off[t + 1]; ++j) {
             uint64_t h = (items[j] * 0x9E3779B97F4A7C15ull) & (cap - 1);
             while (tab[h].key != UINT64_MAX && tab[h].key != items[j]) h = (h + 1) & (cap - 1);
-            if (tab[h].key == UINT64_MAX) { tab[h].key = items[j]; tab[h].wd = -1; tab[h].md = -1; }
-            int32_t c = modes[j] ? tab[h].md + 1 : tab[h].wd + 1;
+            if (tab[h].key == UINT64_MAX) { tab[h].key = items[j]; tab[h].rd = -1; tab[h].ad = -1; }
+            const int32_t rd = tab[h].rd, ad = tab[h].ad;
+            int32_t c = modes[j] == 0 ? ad + 1 : modes[j] == 2 ? rd + 1 : (rd > ad ? rd : ad) + 1;
             if (c > d) d = c;
         }
         for (uint64_t j = ops_off[t]; j < ops_off[t + 1]; ++j) {
             uint64_t h = (items[j] * 0x9E3779B97F4A7C15ull) & (cap - 1);
             while (tab[h].key != items[j]) h = (h + 1) & (cap - 1);
-            if (modes[j]) { tab[h].wd = d; tab[h].md = d; }
-            else if (d > tab[h].md) tab[h].md = d;
+            if (modes[j] == 1) { tab[h].rd = d; tab[h].ad = d; }
+            else if (modes[j] == 0) { if (d > tab[h].rd) tab[h].rd = d; }
+            else if (d > tab[h].ad) tab[h].ad = d;
         }
         depth[t] = (uint32_t)d;
     }

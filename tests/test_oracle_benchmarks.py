@@ -341,3 +341,22 @@ def test_shard_split_covers_bulk_once():
         rows = [W.shard_rows(W.TPCC, dims, G, r)["stock"] for r in range(G)]
         assert rows[0][0] == 0 and rows[-1][1] == 6 * 500
         assert all(rows[r][1] == rows[r + 1][0] for r in range(G - 1))
+
+
+def test_tpcb_add_rule_depth_closed_form():
+    """ADD rule: teller and branch balances are increments, so deposits conflict only
+    on the account row: depth(t) = number of earlier deposits to the same account."""
+    dims = W.TpcbDims(2, 10, 50)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 3000, seed=8, remote_pct=30.0)
+    d = oracle.depths(W.TPCB, dims.dims, image, bulk, add_rule=True)
+    aid = bulk.param_words[0::4].astype(np.int64)
+    seen = {}
+    want = []
+    for a in aid:
+        want.append(seen.get(a, 0))
+        seen[a] = seen.get(a, 0) + 1
+    assert np.array_equal(d, np.array(want))
+    # without the rule every deposit of a branch is one chain (depth >= branch position)
+    d0 = oracle.depths(W.TPCB, dims.dims, image, bulk)
+    assert d0.max() > 1000 and d.max() < 200

@@ -23,10 +23,11 @@ def _streaming(pool):
     for txn in pool:
         m = {}
         for it, md in txn:
-            m[it] = 'W' if (md == 'W' or m.get(it) == 'W') else 'R'
+            old = m.get(it)
+            m[it] = md if old in (None, md) else 'W'
         for it, md in m.items():
             items.append(names.setdefault(it, len(names)))
-            modes.append(1 if md == 'W' else 0)
+            modes.append({'R': 0, 'W': 1, 'A': 2}[md])
         off.append(len(items))
     return list(oracle.depths_from_ops(np.array(off, np.uint64), np.array(items, np.uint64),
                                        np.array(modes, np.uint8)))
@@ -137,3 +138,47 @@ def test_reads_only_single_kset():
 def test_empty_pool():
     assert _streaming([]) == []
     assert g.depths_bruteforce([]) == []
+
+
+def test_add_rule_exhaustive_small_pools():
+    """ADD rule: modes R/W/A, two adds of one item do not conflict.
+    Every pool of <= 3 transactions over 2 items: the streaming recurrence of
+    oracle.c equals the longest path of the graph built from the definition, and
+    equals the O(n^2) brute force; Properties 1-2 hold."""
+    fps = []
+    for k in (1, 2):
+        for sub in itertools.combinations(["a", "b"], k):
+            for modes in itertools.product("RWA", repeat=k):
+                fps.append(list(zip(sub, modes)))
+    assert len(fps) == 3 + 3 + 9
+    count = 0
+    for n in (1, 2, 3):
+        for pool in itertools.product(fps, repeat=n):
+            pool = list(pool)
+            d = g.topo_depths(n, g.graph_by_definition(pool))
+            assert g.depths_bruteforce(pool) == d
+            assert _streaming(pool) == d, pool
+            ok, msg = g.check_properties(pool, d)
+            assert ok, msg
+            count += 1
+    assert count == 15 + 15 ** 2 + 15 ** 3
+
+
+def test_add_rule_random_pools():
+    rng = random.Random(11)
+    for _ in range(400):
+        n = rng.randint(1, 14)
+        nitems = rng.randint(1, 4)
+        pool = [[(rng.randrange(nitems), rng.choice("RWAA")) for _ in range(rng.randint(0, 3))]
+                for _ in range(n)]
+        d = g.depths_bruteforce(pool)
+        assert g.topo_depths(n, g.graph_by_definition(pool)) == d
+        assert _streaming(pool) == d
+
+
+def test_add_rule_special_cases():
+    """Closed forms: adds only -> one k-set; add/read alternation on one item -> a chain
+    of runs; a write after adds waits for all of them."""
+    assert _streaming([[("x", "A")]] * 6) == [0] * 6
+    assert _streaming([[("x", "A")], [("x", "A")], [("x", "R")], [("x", "R")], [("x", "A")]]) == [0, 0, 1, 1, 2]
+    assert _streaming([[("x", "A")], [("x", "A")], [("x", "W")], [("x", "A")]]) == [0, 0, 1, 2]

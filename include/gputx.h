@@ -84,10 +84,19 @@ typedef struct {
     uint32_t part_size;       /* PART: TM-1 subscribers per partition; 0 => 128     */
     int device;               /* CUDA device ordinal                                                */
     void* stream;             /* cudaStream_t to order all work on; NULL => a library-owned stream  */
-    uint32_t flags;           /* reserved, 0                                                        */
+    uint32_t flags;           /* GPUTX_FLAG_* below; 0 = the paper's R/W conflict rule              */
     uint32_t shard;           /* this handle's shard in [0, nshards)                                */
     uint32_t nshards;         /* 0 or 1: unsharded; 2..8: one handle per GPU, see "Sharding" below  */
 } gputx_db_config;
+
+/* gputx_db_config.flags
+ * GPUTX_FLAG_ADD_RULE: a domain-specific conflict rule (PAPER.md:475(c)):
+ *   columns that their transaction types only increment and no output reads (TPC-B teller
+ *   and branch balances, TPC-C W_YTD and D_YTD) are accessed in mode ADD; two adds of one
+ *   item do not conflict (an add still conflicts with reads and writes).  K-SET depths and
+ *   TPL lock keys follow the rule; the final database and every output stay equal to
+ *   serial execution in ts order (the increments are atomic and commutative). */
+#define GPUTX_FLAG_ADD_RULE 1u
 
 typedef struct {
     const uint8_t* type;        /* u8[n]                                                */

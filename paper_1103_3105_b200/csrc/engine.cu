@@ -269,6 +269,7 @@ DevDb make_devdb(gputx_db* db) {
     v.name_sorted = db->d_name_sorted;
     v.name_off = db->d_name_off;
     v.part_size = db->part_size;
+    v.add_rule = (db->cfg.flags & GPUTX_FLAG_ADD_RULE) ? 1u : 0u;
     v.nshards = db->nshards;
     v.shard = db->shard;
     v.nroot = db->nroot;

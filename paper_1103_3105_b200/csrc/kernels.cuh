@@ -220,10 +220,31 @@ struct OpXf {
         return H;
     }
 };
-DEV Xf rec_xf(bool head, uint32_t w, int d) {
-    if (head) return w ? Xf{NEG, NEG, d, NEG, NEG, d} : Xf{NEG, NEG, -1, NEG, NEG, d};
-    return w ? Xf{NEG, 1, d, NEG, 1, d} : Xf{0, NEG, NEG, 1, 0, d};
+// Record maps on the state (a, m) = (max depth of the last writer and the adds since it,
+// max depth of the last writer and the reads since it); mode 0 read, 1 write, 2 add
+// (ADD rule: adds of one item do not conflict with each other).  Without adds a is
+// the last writer's depth, m the max since it, and these are the R/W maps.
+//   read : a' = a,                 m' = max(m, a+1, d)      level max(d, a+1)
+//   add  : a' = max(a, m+1, d),    m' = m                   level max(d, m+1)
+//   write: a' = m' = max(a+1, m+1, d)                       level max(d, max(a, m)+1)
+// A group head starts from (-1, -1).
+DEV Xf rec_xf(bool head, uint32_t mode, int d) {
+    if (head) return mode == 0 ? Xf{NEG, NEG, -1, NEG, NEG, d}
+                   : mode == 2 ? Xf{NEG, NEG, d, NEG, NEG, -1} : Xf{NEG, NEG, d, NEG, NEG, d};
+    return mode == 0 ? Xf{0, NEG, NEG, 1, 0, d} : mode == 2 ? Xf{0, 1, d, NEG, 0, NEG} : Xf{1, 1, d, 1, 1, d};
 }
+DEV int rec_level(bool head, uint32_t mode, int d, const Xf& cur) {
+    const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
+    return mode == 0 ? max(d, a + 1) : mode == 2 ? max(d, m + 1) : max(d, max(a, m) + 1);
+}
+// per-record bits of a lane's RK_ITEMS records: bit 3k head, bits 3k+1..3k+2 mode,
+// bit 24+k valid
+DEV uint32_t rk_bits(bool head, uint32_t mode, int k) {
+    return ((head ? 1u : 0u) | (mode << 1)) << (3 * k) | 1u << (24 + k);
+}
+DEV bool rk_valid(uint32_t hw, int k) { return (hw >> (24 + k)) & 1u; }
+DEV bool rk_head(uint32_t hw, int k) { return (hw >> (3 * k)) & 1u; }
+DEV uint32_t rk_mode(uint32_t hw, int k) { return (hw >> (3 * k + 1)) & 3u; }
 
 constexpr int RK_THREADS = 256, RK_ITEMS = 8, RK_TILE = RK_THREADS * RK_ITEMS;
 constexpr int RK_WT = 32 * RK_ITEMS;      // records per warp-tile (the rank pass's unit of work)
@@ -260,9 +281,7 @@ DEV uint32_t rk_load(const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t 
             const uint64_t key = stage[pos];
             const uint64_t prev = pos ? stage[pos - 1] : *s_prev;
             const bool head = (tb + pos == 0) || key_item(prev) != key_item(key);
-            hw |= (head ? 1u : 0u) << (2 * k);
-            hw |= key_w(key) << (2 * k + 1);
-            hw |= 1u << (16 + k);
+            hw |= rk_bits(head, key_mode(key), k);
         }
     }
     return hw;
@@ -291,14 +310,14 @@ DEV bool xf_eq(const Xf& a, const Xf& b) {
 DEV void rk_gather(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* dv) {
 #pragma unroll
     for (int k = 0; k < RK_ITEMS; ++k)
-        dv[k] = ((hw >> (16 + k)) & 1u) ? (int)__ldcg(&D[key_idx(stage[threadIdx.x * RK_ITEMS + k])]) : 0;
+        dv[k] = rk_valid(hw, k) ? (int)__ldcg(&D[key_idx(stage[threadIdx.x * RK_ITEMS + k])]) : 0;
 }
 
 DEV Xf rk_compose(uint32_t hw, const int* dv) {
     Xf agg = OpXf::identity();
 #pragma unroll
     for (int k = 0; k < RK_ITEMS; ++k)
-        if ((hw >> (16 + k)) & 1u) agg = OpXf::combine(agg, rec_xf((hw >> (2 * k)) & 1u, (hw >> (2 * k + 1)) & 1u, dv[k]));
+        if (rk_valid(hw, k)) agg = OpXf::combine(agg, rec_xf(rk_head(hw, k), rk_mode(hw, k), dv[k]));
     return agg;
 }
 
@@ -338,9 +357,7 @@ DEV uint32_t rk_wload(const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t
             const uint64_t key = stage[pos];
             const uint64_t pk = pos ? stage[pos - 1] : prev;
             const bool head = (tb + pos == 0) || key_item(pk) != key_item(key);
-            hw |= (head ? 1u : 0u) << (2 * k);
-            hw |= key_w(key) << (2 * k + 1);
-            hw |= 1u << (16 + k);
+            hw |= rk_bits(head, key_mode(key), k);
         }
     }
     return hw;
@@ -350,7 +367,7 @@ DEV void rk_wgather(const uint64_t* stage, uint32_t hw, const uint32_t* D, int* 
     const uint32_t lane = lane_id();
 #pragma unroll
     for (int k = 0; k < RK_ITEMS; ++k)
-        dv[k] = ((hw >> (16 + k)) & 1u) ? (int)__ldcg(&D[key_idx(stage[lane * RK_ITEMS + k])]) : 0;
+        dv[k] = rk_valid(hw, k) ? (int)__ldcg(&D[key_idx(stage[lane * RK_ITEMS + k])]) : 0;
 }
 
 // exclusive warp scan of maps; total to every lane
@@ -365,7 +382,7 @@ DEV Xf rk_wscan(Xf x, Xf& total) {
 // Warp-granular passes: every warp owns a contiguous range of warp-tiles and walks it as
 // an independent chain (warp shuffles only, no block barrier in the tile loop), so an SM
 // has 16 independent load/scan/atomic chains in flight instead of 2.
-__global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+__global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes,
                                                           uint32_t local_max, uint32_t use_dirty, RkMemo memo,
@@ -468,13 +485,11 @@ __global__ void __launch_bounds__(RK_THREADS) rank_kernel(const uint64_t* __rest
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k) {
                     L[k] = 0;
-                    if ((hw >> (16 + k)) & 1u) {
-                        const bool head = (hw >> (2 * k)) & 1u;
-                        const uint32_t w = (hw >> (2 * k + 1)) & 1u;
-                        const int d = dv[k];
-                        const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
-                        L[k] = w ? max(d, m + 1) : max(d, a + 1);
-                        cur = OpXf::combine(cur, rec_xf(head, w, d));
+                    if (rk_valid(hw, k)) {
+                        const bool head = rk_head(hw, k);
+                        const uint32_t mode = rk_mode(hw, k);
+                        L[k] = rec_level(head, mode, dv[k], cur);
+                        cur = OpXf::combine(cur, rec_xf(head, mode, dv[k]));
                     }
                 }
                 uint32_t old[RK_ITEMS];    // all raises in flight together
@@ -596,9 +611,7 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
                         const uint64_t key = stage[pos];
                         const uint64_t pk = pos ? stage[pos - 1] : prev;
                         const bool head = (c + pos == 0) || key_item(pk) != key_item(key);
-                        hw |= (head ? 1u : 0u) << (2 * k);
-                        hw |= key_w(key) << (2 * k + 1);
-                        hw |= 1u << (16 + k);
+                        hw |= rk_bits(head, key_mode(key), k);
                     }
                 }
                 int dv[RK_ITEMS];
@@ -610,13 +623,11 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k) {
                     L[k] = 0;
-                    if ((hw >> (16 + k)) & 1u) {
-                        const bool head = (hw >> (2 * k)) & 1u;
-                        const uint32_t w = (hw >> (2 * k + 1)) & 1u;
-                        const int d = dv[k];
-                        const int a = head ? -1 : cur.ac, m = head ? -1 : cur.mc;
-                        L[k] = w ? max(d, m + 1) : max(d, a + 1);
-                        cur = OpXf::combine(cur, rec_xf(head, w, d));
+                    if (rk_valid(hw, k)) {
+                        const bool head = rk_head(hw, k);
+                        const uint32_t mode = rk_mode(hw, k);
+                        L[k] = rec_level(head, mode, dv[k], cur);
+                        cur = OpXf::combine(cur, rec_xf(head, mode, dv[k]));
                     }
                 }
                 uint32_t old[RK_ITEMS];
@@ -1250,15 +1261,23 @@ __global__ void __launch_bounds__(256) home_gather_kernel(const uint32_t* home_p
 // =====================================================================================
 // TPL
 // =====================================================================================
-struct Pair { uint32_t h, w; };
+// index + 1 of the last group head / write / read / add at or before a position
+struct Pair { uint32_t h, w, r, a; };
 struct OpPair {
-    static DEV Pair identity() { return Pair{0u, 0u}; }
-    static DEV Pair combine(const Pair& a, const Pair& b) { return Pair{max(a.h, b.h), max(a.w, b.w)}; }
+    static DEV Pair identity() { return Pair{0u, 0u, 0u, 0u}; }
+    static DEV Pair combine(const Pair& x, const Pair& y) {
+        return Pair{max(x.h, y.h), max(x.w, y.w), max(x.r, y.r), max(x.a, y.a)};
+    }
 };
+DEV Pair tpl_elem(uint64_t i, bool head, uint32_t mode) {
+    const uint32_t p = (uint32_t)i + 1;
+    return Pair{head ? p : 0u, mode == 1 ? p : 0u, mode == 0 ? p : 0u, mode == 2 ? p : 0u};
+}
 
 // Counter-lock keys (DESIGN.md R-S5): in group order, a write's key is its position in
-// the group; a read's key is the position of the first record of its run of reads.
-// A record may enter when lock >= key; it releases +1 after its transaction.
+// the group; a read's (an add's) key is the position of the first record of its run of
+// reads (adds), i.e. one past the last record it conflicts with.  A record may enter
+// when lock >= key; it releases +1 after its transaction.
 __global__ void __launch_bounds__(RK_THREADS) tpl_keys_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                               const uint32_t* __restrict__ rec_off, uint32_t* lkey,
                                                               uint32_t* lock, LookBack<Pair> lb, uint32_t epoch,
@@ -1283,8 +1302,7 @@ __global__ void __launch_bounds__(RK_THREADS) tpl_keys_kernel(const uint64_t* __
             kk[k] = __ldg(&keys[i]);
             const bool head = i == 0 || key_item(__ldg(&keys[i - 1])) != key_item(kk[k]);
             hflags |= (head ? 1u : 0u) << k;
-            Pair e{head ? (uint32_t)i + 1 : 0u, key_w(kk[k]) ? (uint32_t)i + 1 : 0u};
-            agg = OpPair::combine(agg, e);
+            agg = OpPair::combine(agg, tpl_elem(i, head, key_mode(kk[k])));
         } else {
             kk[k] = 0;
         }
@@ -1302,13 +1320,15 @@ __global__ void __launch_bounds__(RK_THREADS) tpl_keys_kernel(const uint64_t* __
         const uint64_t i = b + k;
         if (i < nrec) {
             const bool head = (hflags >> k) & 1u;
-            const uint32_t lw_ex = cur.w;                  // index+1 of last write before i
-            const uint32_t w = key_w(kk[k]);
-            cur = OpPair::combine(cur, Pair{head ? (uint32_t)i + 1 : 0u, w ? (uint32_t)i + 1 : 0u});
+            const uint32_t mode = key_mode(kk[k]);
+            // index+1 of the last earlier record this one conflicts with (reads: writes and
+            // adds; adds: writes and reads)
+            const uint32_t lc_ex = mode == 0 ? max(cur.w, cur.a) : max(cur.w, cur.r);
+            cur = OpPair::combine(cur, tpl_elem(i, head, mode));
             const uint32_t H = cur.h - 1;                  // group head index
             uint32_t key;
-            if (w) key = (uint32_t)i - H;
-            else key = (lw_ex > H) ? lw_ex - H : 0u;
+            if (mode == 1) key = (uint32_t)i - H;
+            else key = (lc_ex > H) ? lc_ex - H : 0u;
             lkey[rec_off[key_idx(kk[k])] + key_j(kk[k])] = key;
             if (head) lock[key_item(kk[k])] = 0;
         }

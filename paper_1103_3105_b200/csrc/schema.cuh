@@ -59,6 +59,7 @@ struct DevDb {
     // shards: this shard owns root keys [root_lo, root_hi) of nroot
     // (root = TPC-B branch, TPC-C warehouse, TM-1 subscriber - 1), shard_of(r) = r*G/nroot
     uint32_t nshards, shard, nroot, root_lo, root_hi;
+    uint32_t add_rule;                 // GPUTX_FLAG_ADD_RULE: increments-only items in mode "add"
     const uint32_t* ts;                // global timestamps (NULL: first_ts + idx)
     const uint32_t* src;               // sharded: home-bulk index, or NOT_HOME (a peer's transaction)
     const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
@@ -91,7 +92,7 @@ DEV void put64(uint8_t* o, uint64_t v) {
 
 // =================================================================================
 // Item space (dense, per schema) and access records
-//   record key = item << 30 | idx << 6 | j << 2 | mode     (mode 1 = write)
+//   record key = item << 30 | idx << 6 | j << 2 | mode     (0 read, 1 write, 2 add)
 // =================================================================================
 constexpr int KEY_ITEM_SHIFT = 30;
 DEV uint64_t make_key(uint64_t item, uint32_t idx, uint32_t j, uint32_t w) {
@@ -101,15 +102,16 @@ DEV uint64_t key_item(uint64_t k) { return k >> KEY_ITEM_SHIFT; }
 DEV uint32_t key_idx(uint64_t k) { return (uint32_t)(k >> 6) & 0xFFFFFFu; }
 DEV uint32_t key_j(uint64_t k) { return (uint32_t)(k >> 2) & 0xFu; }
 DEV uint32_t key_w(uint64_t k) { return (uint32_t)k & 1u; }
+DEV uint32_t key_mode(uint64_t k) { return (uint32_t)k & 3u; }    // 0 read, 1 write, 2 add
 
 struct Rec {
     uint64_t item;
-    uint32_t w;
+    uint32_t w;        // mode: 0 read, 1 write, 2 add
 };
 
 DEV int add_rec(Rec* r, int k, uint64_t item, uint32_t w) {
     for (int j = 0; j < k; ++j)
-        if (r[j].item == item) { r[j].w |= w; return k; }   // same item: one record, W dominates
+        if (r[j].item == item) { if (r[j].w != w) r[j].w = 1u; return k; }   // one record; modes differ -> W
     r[k].item = item;
     r[k].w = w;
     return k + 1;
@@ -125,12 +127,14 @@ DEV int add_rec(Rec* r, int k, uint64_t item, uint32_t w) {
 template <int S>
 DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
     int k = 0;
+    // ADD rule: balances / YTDs only incremented by their type and never read by an output
+    const uint32_t inc = db.add_rule ? 2u : 1u;
     if (S == S_TPCB) {
         const uint32_t T = db.dims[1], A = db.dims[2];
         const uint64_t sb = 1ull + T + A;
         r[0] = {(uint64_t)(p[0] / A) * sb + 1 + T + p[0] % A, 1u};
-        r[1] = {(uint64_t)(p[1] / T) * sb + 1 + p[1] % T, 1u};
-        r[2] = {(uint64_t)p[2] * sb, 1u};
+        r[1] = {(uint64_t)(p[1] / T) * sb + 1 + p[1] % T, inc};
+        r[2] = {(uint64_t)p[2] * sb, inc};
         return 3;
     } else if (S == S_TM1) {
         switch (t) {
@@ -162,8 +166,8 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
             }
             return k;
         }
-        r[0] = {(uint64_t)p[0] * sw_ + D, 1u};
-        r[1] = {(uint64_t)p[0] * sw_ + D + 1 + p[1], 1u};
+        r[0] = {(uint64_t)p[0] * sw_ + D, inc};
+        r[1] = {(uint64_t)p[0] * sw_ + D + 1 + p[1], inc};
         if (p[4] == 2) return 2;                           // by-name lookup found nobody
         r[2] = {(uint64_t)p[2] * sw_ + 2 * D + 1 + (uint64_t)p[3] * C + p[5], 1u};
         return 3;

@@ -19,6 +19,7 @@ STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET}
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_TYPE", 5: "ESTATE",
                 6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
 OUT_STRIDE = {1: 8, 2: 40, 3: 200}
+FLAG_ADD_RULE = 1            # include/gputx.h GPUTX_FLAG_ADD_RULE
 
 
 class GputxError(RuntimeError):
@@ -135,7 +136,7 @@ class Database:
 
     def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
                  device: int = 0, stream: int | None = None, insert_capacity: int = 0, shard: int = 0,
-                 nshards: int = 1):
+                 nshards: int = 1, add_rule: bool = False):
         self.lib = load_library()
         self.schema = schema
         cfg = Config()
@@ -147,6 +148,7 @@ class Database:
         cfg.part_size = int(part_size)
         cfg.device = int(device)
         cfg.stream = stream
+        cfg.flags = FLAG_ADD_RULE if add_rule else 0
         cfg.shard = int(shard)
         cfg.nshards = int(nshards)
         self.shard, self.nshards, self.device = int(shard), int(nshards), int(device)

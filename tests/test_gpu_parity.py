@@ -199,3 +199,31 @@ def test_explicit_timestamps(strategy, schema):
         compare(schema, ref, db, image, label=f"{strategy} explicit ts")
     finally:
         db.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("schema", [W.TPCB, W.TPCC])
+def test_add_rule_parity_and_depths(strategy, schema):
+    """GPUTX_FLAG_ADD_RULE (PAPER.md:475(c)): increments of teller /
+    branch balances and W_YTD / D_YTD do not conflict with each other.  The final state,
+    outputs and inserts still equal serial execution; K-SET depths equal the oracle's
+    ADD-rule recurrence and are much shallower than under the R/W rule."""
+    if schema == W.TPCB:
+        dims = W.TpcbDims(4, 10, 300)
+        bulk = W.tpcb_bulk(dims, 20_000, seed=31, remote_pct=20.0)
+    else:
+        dims = W.TpccDims(4, 10, 300, 2000)
+        bulk = W.tpcc_bulk(dims, 8000, seed=32, remote_line_pct=5.0)
+    image = W.make_db(schema, dims, seed=6)
+    ref = oracle.run(schema, dims.dims, image, bulk)
+    db = gpu_db(schema, dims, image, bulk.n, add_rule=True)
+    try:
+        db.submit(bulk)
+        st = db.execute(strategy)
+        compare(schema, ref, db, image, label=f"{strategy} add rule")
+        if strategy == "kset":
+            want = oracle.depths(schema, dims.dims, image, bulk, add_rule=True)
+            assert np.array_equal(db.depths(), want)
+            assert st["depth"] < oracle.depths(schema, dims.dims, image, bulk).max()
+    finally:
+        db.close()

@@ -48,9 +48,17 @@ WORKLOADS = {
                  desc="TPC-B 1,000 branches, bulk 4M, uniform, 15% remote accounts"),
     "tpcb_tiny": dict(schema=W.TPCB, dims=W.TpcbDims(1, 10, 100_000), n=4096, kw={},
                       desc="TPC-B tiny: 1 branch, 10 tellers, 100k accounts, bulk 4,096"),
+    "tpcb_hot": dict(schema=W.TPCB, dims=W.TpcbDims(1000, 10, 100_000), n=4_000_000,
+                     kw=dict(remote_pct=15.0, alpha=0.1),
+                     desc="TPC-B 1,000 branches, bulk 4M, hot-branch alpha=0.1, 15% remote accounts"),
     "tpcc": dict(schema=W.TPCC, dims=W.TpccDims(64, 10, 3000, 100_000), n=1_000_000, kw={},
                  desc="TPC-C NewOrder+Payment, 64 warehouses, bulk 1M"),
 }
+# NEXT-1: the same bulks under the ADD conflict rule (GPUTX_FLAG_ADD_RULE:
+# commutative balance increments do not conflict with each other; PAPER.md:475(c)).
+for _k in ("tpcb", "tpcb_hot", "tpcc"):
+    WORKLOADS[_k + "_add"] = dict(WORKLOADS[_k], add_rule=True,
+                                  desc=WORKLOADS[_k]["desc"] + ", ADD conflict rule (commutative increments)")
 
 
 def _peaks():
@@ -283,6 +291,7 @@ def run_reference(args, wl, ws, rank):
 
 def config_of(args, wl, dims, ws):
     c = {"workload": wl["desc"], "strategy": args.strategy, "bulk": wl["n"], "dims": list(dims.dims),
+         "conflict_rule": "R/W + ADD" if wl.get("add_rule") else "R/W (paper)",
          "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM (value); "
          "pinned host (e2e)"}
     if ws > 1:
@@ -298,8 +307,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="tm1", choices=sorted(WORKLOADS))
-    ap.add_argument("--strategy", default="kset", choices=["kset", "part", "tpl"])
-    ap.add_argument("--others", default="part,tpl", help="extra strategies measured on the same bulks")
+    ap.add_argument("--strategy", default="kset", choices=["kset", "part", "tpl", "auto"])
+    ap.add_argument("--others", default="part,tpl,auto", help="extra strategies measured on the same bulks "
+                    "(auto: Algorithm 1, PAPER.md:422-437, with the library's default thresholds)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -323,7 +333,8 @@ def main():
     # sharded: the local bulk is the home bulk plus the peers' cross-shard transactions
     max_bulk = n if ws == 1 else min(1 << 24, n + n // 2 + 1024)
     db = Database(wl["schema"], dims.dims, max_bulk, image, device=local, stream=stream.cuda_stream,
-                  insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws)
+                  insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws,
+                  add_rule=wl.get("add_rule", False))
     del image
 
     class DevBulk:
@@ -431,6 +442,9 @@ def main():
         others[s] = {"value": ws * n * len(m2) / (tot / 1e3), "ms_per_step": tot / len(m2),
                      "ms_exec": statistics.mean(x["ms_exec"] for x in s2),
                      "max_chain": s2[-1]["max_chain"], "parts": s2[-1]["parts"]}
+        if s == "auto":
+            others[s]["chose"] = s2[-1]["strategy"]
+            others[s]["w0_d_c"] = [s2[-1]["zero_set"], s2[-1]["depth"], s2[-1]["cross"]]
 
     # ---- roofline of the dominant kernel ---------------------------------------------
     peak, peak_kind = _peaks()
@@ -439,11 +453,11 @@ def main():
     last = stats[-1]
     b_last = bulks[(args.warmup + args.steps - 1) % len(bulks)]
     cand = {}
-    if args.strategy == "kset":
-        cand["kset_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
-        cand["rank_kernel"] = (rank_bytes(last["records"], last["rank_passes"], n), phase["ms_rank"])
-    else:
-        cand[f"{args.strategy}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+    eff = last["strategy"]                                  # auto: the strategy Algorithm 1 chose
+    if last["rank_passes"]:
+        rk = "rank_kernel" if wl["schema"] == W.TPCC else "rank_root_kernel"
+        cand[rk] = (rank_bytes(last["records"], last["rank_passes"], n), phase["ms_rank"])
+    cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1])
     kbytes, kms = cand[kname]
     achieved = kbytes / (kms / 1e3) / 1e9

@@ -71,7 +71,8 @@ typedef enum {
     GPUTX_ENCCL = 10         /* reserved: inter-GPU exchange                              */
 } gputx_status;
 
-typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2 } gputx_strategy;
+typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2,
+               GPUTX_AUTO = 3  /* Algorithm 1, see gputx_set_chooser */ } gputx_strategy;
 typedef enum { GPUTX_TPCB = 1, GPUTX_TM1 = 2, GPUTX_TPCC = 3 } gputx_schema;
 
 typedef struct {
@@ -121,6 +122,9 @@ typedef struct {
     uint64_t max_chain;      /* longest partition (PART)                                */
     uint64_t launches;       /* kernels this library launched for the bulk (submit + execute) */
     double ms_emit, ms_sort, ms_rank, ms_group, ms_exec, ms_merge, ms_total;
+    uint64_t cross;          /* c: transactions with fragments in more than one PART partition
+                                (filled by PART and AUTO, else 0)             */
+    uint64_t strategy;       /* the strategy that ran (GPUTX_AUTO: the one Algorithm 1 chose) */
 } gputx_stats;
 
 /* Create a database handle for cfg->schema with empty (zero) columns on cfg->device.
@@ -158,6 +162,19 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* bulk, uint64_t* f
  * merge the insert buffers.  stats may be NULL.  Errors: ESTATE (nothing
  * submitted), EDEADLOCK (TPL watchdog), ECAPACITY (insert table full), ECUDA. */
 gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* stats);
+
+/* Thresholds of the strategy chooser, Algorithm 1 (Appendix D
+ * "Choosing the suitable execution strategy").  GPUTX_AUTO first builds the
+ * T-dependency graph's structural parameters of the submitted bulk:
+ *   w0 = |0-set| and d = depth, from the K-SET emit / sort / rank phases, and
+ *   c  = transactions whose PART fragments lie in more than one partition;
+ * then runs   w0 >= w0_bar            -> K-SET (reusing the ranks)
+ *             c <= c_bar or d >= d_bar -> PART
+ *             otherwise               -> TPL  (reusing the sorted access records).
+ * Defaults: w0_bar = 128 x #SMs (the GPU's processors: 18,944 on B200),
+ * d_bar = 2048, c_bar = 0 (calibrated per machine: tools/calibrate_chooser.py).
+ * Errors: EINVAL (null handle). */
+gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, uint64_t c_bar);
 
 /* Copy the last executed bulk's results to host: status u8[n] (may be NULL) and the
  * output records (n * gputx_out_stride bytes; out may be NULL).  ECAPACITY if out_bytes

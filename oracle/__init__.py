@@ -213,3 +213,51 @@ def run_sequence(schema: int, dims, db: dict, bulk, order, first_ts: int = 0) ->
         ins[tab] = {c: (np.concatenate(inserts[tab][c]) if inserts[tab][c] else np.zeros(0, dt))
                     for c, dt in cl}
     return Result(work, status, out, ins)
+
+
+# ---------------------------------------------------------------------------------------
+# Strategy chooser: Algorithm 1, PAPER.md:416-437 (Appendix D,
+# "Choosing the suitable execution strategy"), on the structural parameters of the
+# T-dependency graph listed at PAPER.md:408-413.
+# ---------------------------------------------------------------------------------------
+def cross_partition(schema: int, dims, bulk, status: np.ndarray) -> np.ndarray:
+    """bool[n]: the transaction accesses more than one PART partition (PAPER.md:413, 430:
+    "cross-partition transactions").  Partitions (DESIGN.md R-S10 / R-S20): TPC-B branch,
+    TPC-C warehouse, TM-1 128 subscribers (a TM-1 transaction touches one subscriber).
+    Accesses are those the procedure performs in the serial run: a transaction that
+    aborts in its first phase (TPC-C NewOrder with an unused item, by-name Payment
+    with no such customer) touches only its home partition."""
+    n = bulk.n
+    out = np.zeros(n, bool)
+    po = bulk.param_off.astype(np.int64)
+    pw = bulk.param_words
+    for i in range(n):
+        p = pw[po[i]:po[i + 1]]
+        if schema == TPCB:
+            # deposit [aid, tid, bid, delta]; accounts per branch = dims[2]
+            out[i] = int(p[0]) // int(dims[2]) != int(p[2])
+        elif schema == TPCC and status[i] == 0:
+            w = int(p[0])
+            if bulk.type[i] == 0:      # NewOrder [w, d, c, ol_cnt, (i, supply_w, qty) x ol_cnt]
+                out[i] = any(int(p[5 + 3 * l]) != w for l in range(int(p[3])))
+            else:                      # Payment [w, d, cw, cd, by_name, c_or_last, h_amount]
+                out[i] = int(p[2]) != w
+    return out
+
+
+def choose_strategy(w0: int, d: int, c: int, w0_bar: int, d_bar: int, c_bar: int) -> str:
+    """Algorithm 1, line by line."""
+    if w0 >= w0_bar:                  # 2: if w0 >= w0_bar then
+        return "kset"                 # 3:   return K-SET
+    if c <= c_bar or d >= d_bar:      # 7: if c <= c_bar or d >= d_bar then
+        return "part"                 # 8:   return PART
+    return "tpl"                      # 10: return TPL
+
+
+def structure(schema: int, dims, db: dict, bulk, add_rule: bool = False) -> dict:
+    """w0 = |0-set|, d = depth of the T-dependency graph, c = cross-partition
+    transactions (PAPER.md:408-413) of `bulk` against `db`."""
+    dep = depths(schema, dims, db, bulk, add_rule)
+    st = run(schema, dims, db, bulk).status
+    return {"w0": int((dep == 0).sum()), "d": int(dep.max()) if bulk.n else 0,
+            "c": int(cross_partition(schema, dims, bulk, st).sum())}

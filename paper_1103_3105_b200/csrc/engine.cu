@@ -103,6 +103,9 @@ struct gputx_db {
     std::vector<InsTable> ins;
     bool sealed = false, submitted = false, executed = false, poisoned = false;
     int last_strategy = -1;
+    int chosen = -1;                          // strategy that ran for the last execute
+    // Algorithm 1 thresholds (gputx_set_chooser); w0_bar 0 => 128 x #SMs
+    uint64_t ch_w0 = 0, ch_d = 2048, ch_c = 0;
     uint64_t n = 0, first_ts = 0, next_ts = 0, max_bulk = 0, max_words = 0, max_rec = 0, n_items = 0;
     uint32_t item_bits = 0;
     uint32_t nparts = 0, part_bits = 0, part_size = 128;
@@ -327,8 +330,10 @@ gputx_status sort_records(gputx_db* db, uint32_t lo, uint32_t nbits, const uint3
     return GPUTX_OK;
 }
 
+// K-SET part 1 (also the analysis half of GPUTX_AUTO): emit, sort, rank fixpoint, and
+// the depth reduction giving d = max depth and w0 = |0-set|
 template <int S>
-gputx_status run_kset(gputx_db* db, const DevDb& v) {
+gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
     TRY(emit_records<S>(db, v));
@@ -356,7 +361,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         if (rtrace) CK(cudaMemsetAsync(rtrace, 0, RANK_TRACE_SLOTS * 8, s));
         if (db->rank_root) {             // root-local sweeps (TM-1: single-root transactions)
             DevDb vv = v;
-            void* rargs[] = {&vv, &keys, &nrec, &D, &bar, &sc, &maxp, &rtrace};
+            void* rargs[] = {&vv, &keys, &nrec, &D, &bar, &sc, &maxp, &rtrace, &lb, &epoch0, &lmax, &dirty, &memo};
             TRY(launch_coop(db, (const void*)rank_root_kernel<S>, db->rank_root_grid, RK_THREADS, rargs));
         } else {
             void* args[] = {&keys, &nrec, &D, &lb, &epoch0, &bar, &sc, &maxp, &lmax, &dirty, &memo, &rtrace};
@@ -364,13 +369,20 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
         }
         ++db->launches;
     }
-    STAGE("rank");
-    cudaEventRecord(db->ev[4], s);
-    // group by (depth, type)
-    const uint32_t T = db->ntypes;
     const uint32_t g = grid_for(db->n, 256, 148 * 8);
     depth_reduce_kernel<<<g, 256, 0, s>>>(db->d_D, (uint32_t)db->n, db->d_sc);
     ++db->launches;
+    STAGE("rank");
+    cudaEventRecord(db->ev[4], s);
+    db->has_depth = true;
+    return GPUTX_OK;
+}
+
+// K-SET part 2: group by (depth, type), then the k-set rounds
+template <int S>
+gputx_status kset_exec(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    const uint32_t T = db->ntypes;
     group_nkeys_kernel<<<1, 1, 0, s>>>(db->d_sc, T);
     ++db->launches;
     zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
@@ -446,8 +458,14 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
     }
     STAGE("kset exec");
     cudaEventRecord(db->ev[6], s);
-    db->has_depth = db->has_perm = true;
+    db->has_perm = true;
     return GPUTX_OK;
+}
+
+template <int S>
+gputx_status run_kset(gputx_db* db, const DevDb& v) {
+    TRY(kset_rank<S>(db, v));
+    return kset_exec<S>(db, v);
 }
 
 // -------------------------------------------------------------------------------- PART
@@ -457,6 +475,8 @@ gputx_status run_part(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[1], s);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     frag_count_kernel<S><<<g, 256, 0, s>>>(v, db->d_cnt);
+    ++db->launches;
+    count_gt1_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_cnt, (uint32_t)db->n, db->d_sc + SC_CROSS);
     ++db->launches;
     scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NFRAG);
     frag_emit_kernel<S><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a);
@@ -481,14 +501,18 @@ gputx_status run_part(gputx_db* db, const DevDb& v) {
 }
 
 // --------------------------------------------------------------------------------- TPL
+// sorted = true: the access records are already emitted and sorted (GPUTX_AUTO ran the
+// K-SET analysis first; TPL's records are the same)
 template <int S>
-gputx_status run_tpl(gputx_db* db, const DevDb& v) {
+gputx_status run_tpl(gputx_db* db, const DevDb& v, bool sorted = false) {
     cudaStream_t s = db->stream;
-    cudaEventRecord(db->ev[1], s);
-    TRY(emit_records<S>(db, v));
-    cudaEventRecord(db->ev[2], s);
-    TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
-    cudaEventRecord(db->ev[3], s);
+    if (!sorted) {
+        cudaEventRecord(db->ev[1], s);
+        TRY(emit_records<S>(db, v));
+        cudaEventRecord(db->ev[2], s);
+        TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+        cudaEventRecord(db->ev[3], s);
+    }
     ++db->epoch;
     tpl_keys_kernel<<<(uint32_t)((db->max_rec + RK_TILE - 1) / RK_TILE) + 1, RK_THREADS, 0, s>>>(
         db->d_sorted, db->d_sc + SC_NREC, db->d_rec_off, db->d_lkey, db->d_lock, db->lb_tpl, db->epoch, next_ticket(db));
@@ -517,9 +541,34 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v) {
     return GPUTX_OK;
 }
 
+// Algorithm 1 on the bulk's structural parameters
+gputx_strategy choose_strategy(const gputx_db* db, uint64_t w0, uint64_t d, uint64_t c) {
+    const uint64_t w0_bar = db->ch_w0 ? db->ch_w0 : 128ull * (uint64_t)db->nsm;
+    if (w0 >= w0_bar) return GPUTX_KSET;                   // lines 2-3
+    if (c <= db->ch_c || d >= db->ch_d) return GPUTX_PART;  // lines 5-8
+    return GPUTX_TPL;                                      // line 10
+}
+
+template <int S>
+gputx_status run_auto(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cross_count_kernel<S><<<grid_for(db->n, 256, 148 * 8), 256, 0, s>>>(v, db->d_sc + SC_CROSS);
+    ++db->launches;
+    TRY(kset_rank<S>(db, v));                               // line 1: w0 (and d)
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
+    const gputx_strategy ch = choose_strategy(db, db->h_sc[SC_ZERO], db->h_sc[SC_MAXD], db->h_sc[SC_CROSS]);
+    db->chosen = (int)ch;
+    if (ch == GPUTX_KSET) return kset_exec<S>(db, v);
+    if (ch == GPUTX_TPL) return run_tpl<S>(db, v, true);
+    return run_part<S>(db, v);
+}
+
 template <int S>
 gputx_status execute_schema(gputx_db* db, gputx_strategy st) {
     DevDb v = make_devdb(db);
+    if (st == GPUTX_AUTO) return run_auto<S>(db, v);
     if (st == GPUTX_KSET) return run_kset<S>(db, v);
     if (st == GPUTX_PART) return run_part<S>(db, v);
     return run_tpl<S>(db, v);
@@ -1139,7 +1188,9 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
 gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
     if (!db) return GPUTX_EINVAL;
     if (!db->submitted) return fail(db, GPUTX_ESTATE, "nothing submitted");
-    if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET) return fail(db, GPUTX_EINVAL, "bad strategy");
+    if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET && st != GPUTX_AUTO)
+        return fail(db, GPUTX_EINVAL, "bad strategy");
+    db->chosen = st == GPUTX_AUTO ? (int)GPUTX_KSET : (int)st;   // AUTO: overwritten by run_auto
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[0], s);
     const uint64_t n = db->n;
@@ -1164,11 +1215,13 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
-    if (st == GPUTX_KSET) db->rank_epoch += db->h_sc[SC_PASSES] + 1;
+    const bool ranked = (st == GPUTX_KSET || st == GPUTX_AUTO) && n;
+    const gputx_strategy eff = (gputx_strategy)db->chosen;
+    if (ranked) db->rank_epoch += db->h_sc[SC_PASSES] + 1;
     for (auto& t : db->ins) { t.rows += t.pending; t.pending = 0; }
     db->executed = true;
-    db->last_strategy = (int)st;
-    if (st == GPUTX_KSET && db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
+    db->last_strategy = (int)eff;
+    if (ranked && db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
     if (db->h_sc[SC_DEADLOCK]) {
         db->poisoned = true;
         return fail(db, GPUTX_EDEADLOCK, "TPL spin watchdog tripped");
@@ -1177,15 +1230,17 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
         memset(stats, 0, sizeof(*stats));
         stats->n = n;
         stats->launches = db->launches;
+        stats->strategy = (uint64_t)eff;
+        stats->cross = (eff == GPUTX_PART || st == GPUTX_AUTO) ? db->h_sc[SC_CROSS] : 0;
         stats->records = st == GPUTX_PART ? 0 : db->h_sc[SC_NREC];
-        stats->fragments = st == GPUTX_PART ? db->h_sc[SC_NFRAG] : 0;
-        if (st == GPUTX_KSET && n) {
+        stats->fragments = eff == GPUTX_PART ? db->h_sc[SC_NFRAG] : 0;
+        if (ranked) {
             stats->depth = db->h_sc[SC_MAXD];
             stats->ksets = (uint64_t)db->h_sc[SC_MAXD] + 1;
             stats->zero_set = db->h_sc[SC_ZERO];
             stats->rank_passes = db->h_sc[SC_PASSES];
         }
-        if (st == GPUTX_PART) {
+        if (eff == GPUTX_PART) {
             stats->parts = db->nparts;
             stats->max_chain = db->h_sc[SC_MAXCHAIN];
         }
@@ -1303,6 +1358,14 @@ gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
     if (n) CK(cudaMemcpy(host, db->d_perm, n * 4, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, uint64_t c_bar) {
+    if (!db) return GPUTX_EINVAL;
+    db->ch_w0 = w0_bar;
+    db->ch_d = d_bar;
+    db->ch_c = c_bar;
     return GPUTX_OK;
 }
 

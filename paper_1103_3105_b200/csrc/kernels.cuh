@@ -18,10 +18,12 @@ namespace gputx {
 enum {
     SC_ERR = 0, SC_BADIDX, SC_NREC, SC_NFRAG, SC_MAXD, SC_ZERO, SC_PASSES, SC_CHG0, SC_CHG1, SC_CHG2,
     SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV, SC_XTOTAL,
+    SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
     SC_COUNT = 32
 };
 enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
+constexpr int SC_CROSS = 24;      // c: transactions with fragments in > 1 PART partition
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -382,11 +384,10 @@ DEV Xf rk_wscan(Xf x, Xf& total) {
 // Warp-granular passes: every warp owns a contiguous range of warp-tiles and walks it as
 // an independent chain (warp shuffles only, no block barrier in the tile loop), so an SM
 // has 16 independent load/scan/atomic chains in flight instead of 2.
-__global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
-                                                          uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
-                                                          GridBar* bar, uint32_t* sc, uint32_t max_passes,
-                                                          uint32_t local_max, uint32_t use_dirty, RkMemo memo,
-                                                          uint64_t* trace) {
+__device__ __forceinline__ void rank_generic(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr, uint32_t* D,
+                                             LookBack<Xf> lb, uint32_t epoch0, GridBar* bar, uint32_t* sc,
+                                             uint32_t max_passes, uint32_t local_max, uint32_t use_dirty, RkMemo memo,
+                                             uint64_t* trace) {
     // trace (diagnostics): per pass p, [8p] pass start (CTA 0), [8p+1] last CTA done with A,
     // [8p+2] CTA 0 past barrier 1, [8p+3] last CTA done with D, [8p+4] CTA 0 past barrier 2,
     // [8p+5] warp-tiles swept, [8p+6] sweeps
@@ -544,6 +545,14 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __r
     }
 }
 
+__global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                          uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
+                                                          GridBar* bar, uint32_t* sc, uint32_t max_passes,
+                                                          uint32_t local_max, uint32_t use_dirty, RkMemo memo,
+                                                          uint64_t* trace) {
+    rank_generic(keys, nrec_ptr, D, lb, epoch0, bar, sc, max_passes, local_max, use_dirty, memo, trace);
+}
+
 // Root-local rank (TM-1): every warp owns a range of whole roots (a root = all items of
 // one subscriber, adjacent in the sorted records) and sweeps it until it raises nothing.
 // A transaction whose records all lie in one root is settled by its root alone, so when
@@ -555,24 +564,43 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __r
 template <int S>
 DEV uint64_t rr_root(const DevDb& db, uint64_t key) { return item_root<S>(db, key_item(key)); }
 
-// first record at or after p that starts a root (p itself if p == 0 or p >= nrec)
+// first record at or after p that starts a root (p itself if p == 0 or p >= nrec);
+// searches at most `limit` records (4 x 32 loads in flight per step) and returns
+// 0xFFFFFFFF if the root continues past them
 template <int S>
-DEV uint32_t rr_align(const DevDb& db, const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t p) {
+DEV uint32_t rr_align(const DevDb& db, const uint64_t* __restrict__ keys, uint32_t nrec, uint32_t p, uint32_t limit) {
     if (p == 0 || p >= nrec) return min(p, nrec);
     const uint64_t r0 = rr_root<S>(db, __ldg(&keys[p - 1]));
-    for (uint32_t b = p; b < nrec; b += 32) {
-        const uint32_t i = b + lane_id();
-        const bool edge = i < nrec && rr_root<S>(db, __ldg(&keys[i])) != r0;
-        const uint32_t m = __ballot_sync(0xffffffffu, edge);
-        if (m) return b + __ffs(m) - 1;
+    const uint32_t end = (uint32_t)min((uint64_t)nrec, (uint64_t)p + limit);
+    for (uint32_t b = p; b < end; b += 128) {
+        uint64_t k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t i = b + 32 * j + lane_id();
+            k[j] = i < end ? __ldg(&keys[i]) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t i = b + 32 * j + lane_id();
+            const uint32_t m = __ballot_sync(0xffffffffu, i < end && rr_root<S>(db, k[j]) != r0);
+            if (m) return b + 32 * j + __ffs(m) - 1;
+        }
     }
-    return nrec;
+    return end == nrec ? nrec : 0xFFFFFFFFu;
 }
 
+//
+// A root holding many times a warp's share of the records (a hot branch: TPC-B with
+// hot-branch skew puts ~10% of all records in branch 0) would serialise the pass on one
+// warp, so the kernel first checks the aligned ranges: if any exceeds RR_SPLIT x the
+// even share, every CTA runs the grid-wide scan (rank_generic) instead.
+constexpr uint32_t RR_SPLIT = 8;
 template <int S>
 __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const uint64_t* __restrict__ keys,
                                                                const uint32_t* nrec_ptr, uint32_t* D, GridBar* bar,
-                                                               uint32_t* sc, uint32_t max_passes, uint64_t* trace) {
+                                                               uint32_t* sc, uint32_t max_passes, uint64_t* trace,
+                                                               LookBack<Xf> lb, uint32_t epoch0, uint32_t local_max,
+                                                               uint32_t use_dirty, RkMemo memo) {
     constexpr uint32_t NW = RK_THREADS / 32;
     __shared__ uint64_t stage_all[NW * RK_WT];
     __shared__ int s_chg;
@@ -581,8 +609,15 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
     uint64_t* stage = stage_all + wid * RK_WT;
     const uint32_t TW = gridDim.x * NW, gw = blockIdx.x * NW + wid;
     const uint32_t chunk = (nrec + TW - 1) / TW;
-    const uint32_t r0 = rr_align<S>(db, keys, nrec, gw * chunk);
-    const uint32_t r1 = rr_align<S>(db, keys, nrec, (gw + 1) * chunk);
+    const uint32_t lim = RR_SPLIT * max(chunk, RK_WT);
+    const uint32_t r0 = rr_align<S>(db, keys, nrec, gw * chunk, lim);
+    const uint32_t r1 = rr_align<S>(db, keys, nrec, (gw + 1) * chunk, lim);
+    if (lane == 0 && (r0 == 0xFFFFFFFFu || r1 == 0xFFFFFFFFu || r1 - r0 > lim)) atomicOr(&sc[SC_RRSPLIT], 1u);
+    grid_sync(bar);
+    if (__ldcg(&sc[SC_RRSPLIT])) {
+        rank_generic(keys, nrec_ptr, D, lb, epoch0, bar, sc, max_passes, local_max, use_dirty, memo, trace);
+        return;
+    }
     for (uint32_t pass = 0;; ++pass) {
         if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (pass + 1) % 3] = 0;
         if (tid == 0) s_chg = 0;
@@ -1018,6 +1053,26 @@ template <int S>
 __global__ void __launch_bounds__(256) frag_emit_kernel(DevDb db, const uint32_t* off, uint64_t* keys) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x)
         fragments_local<S>(db, i, keys + off[i]);
+}
+// c of Algorithm 1: transactions whose fragments span > 1 partition
+DEV void add_count(uint32_t* dst, bool pred) {
+    const uint32_t b = __ballot_sync(0xffffffffu, pred);
+    if (lane_id() == 0 && b) atomicAdd(dst, (uint32_t)__popc(b));
+}
+template <int S>
+__global__ void __launch_bounds__(256) cross_count_kernel(DevDb db, uint32_t* dst) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b = blockIdx.x * blockDim.x; b < db.n; b += stride) {
+        const uint32_t i = b + threadIdx.x;
+        add_count(dst, i < db.n && fragments<S>(db, i, nullptr) > 1);
+    }
+}
+__global__ void __launch_bounds__(256) count_gt1_kernel(const uint32_t* cnt, uint32_t n, uint32_t* dst) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b = blockIdx.x * blockDim.x; b < n; b += stride) {
+        const uint32_t i = b + threadIdx.x;
+        add_count(dst, i < n && cnt[i] > 1);
+    }
 }
 __global__ void __launch_bounds__(256) part_bounds_kernel(const uint64_t* frags, const uint32_t* nf_ptr, uint32_t nparts,
                                                           uint32_t* part_off) {

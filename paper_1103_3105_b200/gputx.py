@@ -13,9 +13,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(HERE, "libgputx.so")
 
-GPUTX_TPL, GPUTX_PART, GPUTX_KSET = 0, 1, 2
-TPL, PART, KSET = "tpl", "part", "kset"
-STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET}
+GPUTX_TPL, GPUTX_PART, GPUTX_KSET, GPUTX_AUTO = 0, 1, 2, 3
+TPL, PART, KSET, AUTO = "tpl", "part", "kset", "auto"
+STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET, AUTO: GPUTX_AUTO}
+STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_TYPE", 5: "ESTATE",
                 6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
 OUT_STRIDE = {1: 8, 2: 40, 3: 200}
@@ -45,10 +46,13 @@ class Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint64) for k in ("n", "committed", "aborted", "depth", "ksets", "zero_set", "records",
                                                "rank_passes", "parts", "fragments", "max_chain", "launches")] + \
                [(k, ctypes.c_double) for k in ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_merge",
-                                               "ms_total")]
+                                               "ms_total")] + \
+               [(k, ctypes.c_uint64) for k in ("cross", "strategy")]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["strategy"] = STRATEGY_NAMES[d["strategy"]]
+        return d
 
 
 _lib = None
@@ -88,6 +92,7 @@ def load_library():
         "gputx_close_db": ([P], None),
         "gputx_last_error": ([P], ctypes.c_char_p),
         "gputx_set_launch": ([P, U32, U32, U32], I),
+        "gputx_set_chooser": ([P, U64, U64, U64], I),
         "gputx_trace_rounds": ([P, I], I),
         "gputx_read_round_ns": ([P, P, U64], I),
         "gputx_read_rank_ns": ([P, P, U64], I),
@@ -109,7 +114,7 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_submit_bulk", "gputx_execute", "gputx_read_results", "gputx_results_device",
             "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
-            "gputx_set_launch", "gputx_trace_rounds", "gputx_read_round_ns",
+            "gputx_set_launch", "gputx_set_chooser", "gputx_trace_rounds", "gputx_read_round_ns",
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
             "gputx_shard_return_pack", "gputx_shard_return_merge"]
 
@@ -270,6 +275,10 @@ class Database:
         st = Stats()
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
         return st.as_dict()
+
+    def set_chooser(self, w0_bar: int = 0, d_bar: int = 2048, c_bar: int = 0):
+        """Algorithm 1 thresholds for strategy "auto" (include/gputx.h gputx_set_chooser)."""
+        self._check(self.lib.gputx_set_chooser(self.h, int(w0_bar), int(d_bar), int(c_bar)), self.h)
 
     def execute_nostats(self, strategy: str = KSET):
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], None), self.h)

@@ -17,18 +17,22 @@ CASES = {
     "tpcb_uniform": (W.TPCB, W.TpcbDims(1000, 10, 100_000), 4_000_000, dict(remote_pct=15.0)),
     "tpcb_hot": (W.TPCB, W.TpcbDims(1000, 10, 100_000), 1_000_000, dict(remote_pct=15.0, alpha=0.1)),
     "tpcc": (W.TPCC, W.TpccDims(64, 10, 3000, 100_000), 1_000_000, {}),
+    # NEXT-1 (ADD conflict rule): the bench's *_add workloads
+    "tpcb_hot_add": (W.TPCB, W.TpcbDims(1000, 10, 100_000), 4_000_000, dict(remote_pct=15.0, alpha=0.1)),
+    "tpcc_add": (W.TPCC, W.TpccDims(64, 10, 3000, 100_000), 1_000_000, {}),
 }
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_full_size_all_strategies(case):
     schema, dims, n, kw = CASES[case]
+    add_rule = case.endswith("_add")
     image = W.make_db(schema, dims, seed=1)
     bulk = W.make_bulk(schema, dims, n, seed=2, **kw)
     ref = oracle.run(schema, dims.dims, image, bulk)
     depth = None
     for strategy in ("kset", "part", "tpl"):
-        db = gpu_db(schema, dims, image, n, insert_capacity=2)
+        db = gpu_db(schema, dims, image, n, insert_capacity=2, add_rule=add_rule)
         db.submit(bulk)
         st = db.execute(strategy)
         compare(schema, ref, db, image, label=f"{case} {strategy}")
@@ -37,4 +41,4 @@ def test_full_size_all_strategies(case):
             assert st["depth"] == int(depth.max())
         db.close()
     # rank fixpoint = T-dependency-graph depth of every transaction
-    assert np.array_equal(depth, oracle.depths(schema, dims.dims, image, bulk))
+    assert np.array_equal(depth, oracle.depths(schema, dims.dims, image, bulk, add_rule=add_rule))

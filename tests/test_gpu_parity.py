@@ -37,6 +37,22 @@ def test_tpcb_multibranch(strategy, n):
     run_both(W.TPCB, dims, image, [W.tpcb_bulk(dims, n, seed=n, remote_pct=15.0)], strategy)
 
 
+@pytest.mark.parametrize("add_rule", [False, True])
+@pytest.mark.parametrize("strategy", STRATS)
+def test_tpcb_hot_branch(strategy, add_rule):
+    """Hot-branch skew: branch 0 holds half the bulk, far more records
+    than one warp's share, so the root-local rank falls back to the grid-wide scan
+    (kernels.cuh RR_SPLIT); depths and state must still equal the oracle's."""
+    dims = W.TpcbDims(16, 10, 2000)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 9000, seed=4, remote_pct=15.0, alpha=0.5)
+    db = gpu_db(W.TPCB, dims, image, bulk.n, add_rule=add_rule)
+    run_both(W.TPCB, dims, image, [bulk], strategy, db=db)
+    if strategy == "kset":
+        assert np.array_equal(db.depths(), oracle.depths(W.TPCB, dims.dims, image, bulk, add_rule=add_rule))
+    db.close()
+
+
 @pytest.mark.parametrize("strategy", STRATS)
 @pytest.mark.parametrize("dist", ["nurand", "uniform"])
 def test_tm1(strategy, dist):
@@ -227,3 +243,36 @@ def test_add_rule_parity_and_depths(strategy, schema):
             assert st["depth"] < oracle.depths(schema, dims.dims, image, bulk).max()
     finally:
         db.close()
+
+
+BIG = 1 << 62
+
+
+@pytest.mark.parametrize("schema,dims,n,kw", [
+    (W.TPCB, W.TpcbDims(16, 10, 2000), 9000, dict(remote_pct=15.0)),
+    (W.TM1, W.Tm1Dims(20_000), 30_000, dict(dist="nurand")),
+    (W.TPCC, W.TpccDims(4, 10, 3000, 100_000), 12_000, {}),
+])
+@pytest.mark.parametrize("want", ["kset", "part", "tpl"])
+def test_auto_strategy_algorithm1(schema, dims, n, kw, want):
+    """NEXT-3: GPUTX_AUTO computes w0, d, c equal to the oracle's and
+    runs the strategy Algorithm 1 picks; thresholds are set so that
+    each branch is taken, and the result is bit-exact against serial execution."""
+    image = W.make_db(schema, dims, seed=3)
+    bulk = W.make_bulk(schema, dims, n, 12, **kw)
+    ref = oracle.structure(schema, dims.dims, image, bulk)
+    if want == "kset":
+        bars = (ref["w0"], BIG, 0)                 # w0 >= w0_bar
+    elif want == "part":
+        bars = (ref["w0"] + 1, BIG, ref["c"])      # c <= c_bar
+    else:
+        if ref["c"] == 0:
+            pytest.skip("no cross-partition transaction (TM-1): Algorithm 1 never returns TPL")
+        bars = (ref["w0"] + 1, ref["d"] + 1, ref["c"] - 1)
+    assert oracle.choose_strategy(ref["w0"], ref["d"], ref["c"], *bars) == want
+    db = gpu_db(schema, dims, image, n)
+    db.set_chooser(*bars)
+    st = run_both(schema, dims, image, [bulk], "auto", db=db)[0]
+    assert st["strategy"] == want
+    assert (st["zero_set"], st["depth"], st["cross"]) == (ref["w0"], ref["d"], ref["c"])
+    db.close()

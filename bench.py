@@ -110,10 +110,29 @@ def exec_bytes(schema: int, bulk, status: np.ndarray) -> int:
     return int(per.sum())
 
 
-def rank_bytes(records: int, passes: int, n: int) -> int:
-    """Per pass: read each sorted record (8 B) and gather its transaction's depth (4 B);
-    plus the initial zeroing of D (4 B/txn)."""
+def rank_bytes(schema: int, records: int, passes: int, n: int) -> int:
+    """Iterated scan (TPC-B, TPC-C): per pass, read each sorted record (8 B) and gather
+    its transaction's depth (4 B); plus the initial zeroing of D (4 B/txn).
+    TM-1 streaming rank (one pass): read each record once (8 B), write D once per
+    transaction (4 B) after zeroing it (4 B)."""
+    if schema == W.TM1:
+        return records * 8 + 8 * n
     return passes * records * 12 + 4 * n
+
+
+def rank_kernel_name(schema: int) -> str:
+    return {W.TM1: "rank_stream_tm1_kernel", W.TPCB: "rank_root_kernel", W.TPCC: "rank_kernel"}[schema]
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """DRAM bytes per launch of `kernel` on `workload` from the committed ncu --set full
+    captures (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        e = json.load(open(p))[workload][kernel]
+        return e["dram_bytes_per_launch"], e["source"]
+    except Exception:
+        return None, None
 
 
 # --------------------------------------------------------------------------------------
@@ -455,14 +474,16 @@ def main():
     cand = {}
     eff = last["strategy"]                                  # auto: the strategy Algorithm 1 chose
     if last["rank_passes"]:
-        rk = "rank_kernel" if wl["schema"] == W.TPCC else "rank_root_kernel"
-        cand[rk] = (rank_bytes(last["records"], last["rank_passes"], n), phase["ms_rank"])
+        cand[rank_kernel_name(wl["schema"])] = (rank_bytes(wl["schema"], last["records"], last["rank_passes"], n),
+                                                phase["ms_rank"])
     cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1])
     kbytes, kms = cand[kname]
     achieved = kbytes / (kms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.workload, kname)
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_kind,
                 "algorithmic_bytes": kbytes, "kernel_ms": kms,
                 "share_of_step": kms / phase["ms_total"] if phase["ms_total"] else None}
 

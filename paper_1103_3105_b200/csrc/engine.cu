@@ -163,6 +163,8 @@ struct gputx_db {
     uint32_t rank_local = RK_LOCAL_DEFAULT;   // GPUTX_RANK_LOCAL overrides (experiments)
     uint32_t rank_dirty = 1;                  // dirty-tile worklist (GPUTX_RANK_DIRTY overrides)
     uint32_t rank_root = 0;                   // root-local sweeps (GPUTX_RANK_ROOT overrides)
+    uint32_t rank_stream = 1;                 // TM-1 per-subscriber streaming rank (GPUTX_RANK_STREAM overrides)
+    bool rec_item_sorted = false;             // d_sorted holds records in (item, ts) order
     int rank_root_grid = 0;
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
     bool sync_stages = false;  // GPUTX_SYNC (diagnostics): synchronise and check after each stage
@@ -339,12 +341,24 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     TRY(emit_records<S>(db, v));
     STAGE("emit");
     cudaEventRecord(db->ev[2], s);
-    TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    // TM-1: single-subscriber transactions -> sort on the subscriber bits only and run
+    // the exact streaming recurrence per subscriber (rank_stream_tm1_kernel)
+    const bool stream = S == S_TM1 && db->rank_stream;
+    if (stream)
+        TRY(sort_records(db, KEY_ITEM_SHIFT + TM1_SLOT_BITS, db->item_bits - TM1_SLOT_BITS, db->d_sc + SC_NREC,
+                         db->max_rec));
+    else
+        TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    db->rec_item_sorted = !stream;
     STAGE("sort");
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
-    {
+    if (stream) {
+        const uint32_t gs = grid_for(db->max_rec, RS_STREAM_THREADS, (uint32_t)db->nsm * 16);
+        rank_stream_tm1_kernel<<<gs, RS_STREAM_THREADS, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_D, db->d_sc);
+        ++db->launches;
+    } else {
         const uint64_t* keys = db->d_sorted;
         const uint32_t* nrec = db->d_sc + SC_NREC;
         uint32_t* D = db->d_D;
@@ -469,15 +483,18 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
 }
 
 // -------------------------------------------------------------------------------- PART
+// count_cross = false: GPUTX_AUTO counted c already
 template <int S>
-gputx_status run_part(gputx_db* db, const DevDb& v) {
+gputx_status run_part(gputx_db* db, const DevDb& v, bool count_cross = true) {
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     frag_count_kernel<S><<<g, 256, 0, s>>>(v, db->d_cnt);
     ++db->launches;
-    count_gt1_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_cnt, (uint32_t)db->n, db->d_sc + SC_CROSS);
-    ++db->launches;
+    if (count_cross) {
+        count_gt1_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_cnt, (uint32_t)db->n, db->d_sc + SC_CROSS);
+        ++db->launches;
+    }
     scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NFRAG);
     frag_emit_kernel<S><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a);
     ++db->launches;
@@ -561,8 +578,8 @@ gputx_status run_auto(gputx_db* db, const DevDb& v) {
     const gputx_strategy ch = choose_strategy(db, db->h_sc[SC_ZERO], db->h_sc[SC_MAXD], db->h_sc[SC_CROSS]);
     db->chosen = (int)ch;
     if (ch == GPUTX_KSET) return kset_exec<S>(db, v);
-    if (ch == GPUTX_TPL) return run_tpl<S>(db, v, true);
-    return run_part<S>(db, v);
+    if (ch == GPUTX_TPL) return run_tpl<S>(db, v, db->rec_item_sorted);
+    return run_part<S>(db, v, false);
 }
 
 template <int S>
@@ -699,7 +716,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         max_words_per = 4; max_rec_per = 3;
         db->nparts = d[0];
     } else if (schema == S_TM1) {
-        n_items = 18ull * d[0];
+        n_items = TM1_STRIDE * d[0];
         max_words_per = 7; max_rec_per = 3;
         db->nparts = (uint32_t)((d[0] + db->part_size - 1) / db->part_size);
     } else {
@@ -808,6 +825,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // TPC-C's 64 warehouses are far larger than a warp's share: CTA-range passes instead.
     db->rank_root = schema == S_TPCC ? 0 : 1;
     if (const char* e = getenv("GPUTX_RANK_ROOT")) db->rank_root = (uint32_t)atoi(e);
+    if (const char* e = getenv("GPUTX_RANK_STREAM")) db->rank_stream = (uint32_t)atoi(e);
     db->rank_root_grid = schema == S_TPCB ? coop_grid(db, rank_root_kernel<S_TPCB>, RK_THREADS, 0)
                          : schema == S_TM1 ? coop_grid(db, rank_root_kernel<S_TM1>, RK_THREADS, 0)
                                            : coop_grid(db, rank_root_kernel<S_TPCC>, RK_THREADS, 0);

@@ -700,6 +700,82 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
     }
 }
 
+// Root-stream rank (TM-1): every TM-1 transaction touches the items of ONE subscriber
+// (PAPER.md:451-453), so the T-dependency graph is a disjoint union of per-subscriber
+// graphs.  The records are sorted on the subscriber bits only (stable: (root, ts)
+// order, a transaction's records adjacent), and one thread per subscriber runs the
+// streaming depth recurrence over them in ts order (SURVEY.md §8(c) "Depth oracle"):
+//   d(t) = max over t's records of (write ? Md[x] + 1 : Wd[x] + 1), 0 without records;
+//   then write: Wd[x] = Md[x] = d(t);  read: Md[x] = max(Md[x], d(t)).
+// Exact in one pass (the streaming order is a topological order of the root's graph),
+// with the per-item state (Wd, Md) of the subscriber's <= 32 item slots in shared
+// memory.  This replaces the iterated scan's repeated sweeps of hot NURand subscribers
+// (13 sweeps in the first pass, profiles/round1.md).
+constexpr int RS_STREAM_THREADS = 128;
+constexpr int RS_CHUNK = 8;
+__global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(const uint64_t* __restrict__ keys,
+                                                                           const uint32_t* nrec_ptr, uint32_t* D,
+                                                                           uint32_t* sc) {
+    __shared__ int2 st_all[RS_STREAM_THREADS * TM1_STRIDE];      // (Wd, Md) per slot, per thread
+    int2* st = st_all + threadIdx.x;                            // slot k at st[k * THREADS]: no bank conflicts
+    const uint32_t nrec = *nrec_ptr;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nrec; p += stride) {
+        uint64_t k = __ldg(&keys[p]);
+        const uint64_t root = key_item(k) >> TM1_SLOT_BITS;
+        if (p > 0 && (key_item(__ldg(&keys[p - 1])) >> TM1_SLOT_BITS) == root) continue;   // not the root's head
+#pragma unroll 8
+        for (uint32_t j = 0; j < TM1_STRIDE; ++j) st[j * RS_STREAM_THREADS] = make_int2(-1, -1);
+        // walk the root's records in chunks of RS_CHUNK keys, the next chunk's loads in
+        // flight while the current one is processed.  The open transaction's records
+        // (distinct items, <= 3) are packed 7 bits each (slot | mode << 5) in `pk`; its
+        // depth is max'ed as they arrive (the state changes only when it closes).
+        uint64_t cur[RS_CHUNK], nxt[RS_CHUNK];
+        auto load = [&](uint64_t* b, uint32_t q) {
+#pragma unroll
+            for (int i = 0; i < RS_CHUNK; ++i) b[i] = q + i < nrec ? __ldg(&keys[q + i]) : ~0ull;
+        };
+        auto close = [&](uint32_t idx, uint32_t pk, int m, int d) {
+            for (int j = 0; j < m; ++j) {
+                const uint32_t e = (pk >> (7 * j)) & 0x7Fu;
+                int2* x = &st[(e & 31u) * RS_STREAM_THREADS];
+                if ((e >> 5) == 1u) *x = make_int2(d, d);
+                else x->y = max(x->y, d);
+            }
+            D[idx] = (uint32_t)d;
+        };
+        uint32_t q = p;
+        load(cur, q);
+        q += RS_CHUNK;
+        uint32_t tidx = 0xFFFFFFFFu, pk = 0;
+        int m = 0, d = 0;
+        bool go = true;
+        while (go) {
+            load(nxt, q);
+            q += RS_CHUNK;
+#pragma unroll
+            for (int i = 0; i < RS_CHUNK; ++i) {
+                const uint64_t kk = cur[i];
+                if (!go || (key_item(kk) >> TM1_SLOT_BITS) != root) { go = false; continue; }
+                const uint32_t id = key_idx(kk);
+                if (id != tidx) {
+                    if (m) close(tidx, pk, m, d);
+                    tidx = id; pk = 0; m = 0; d = 0;
+                }
+                const uint32_t slot = (uint32_t)(key_item(kk) & (TM1_STRIDE - 1)), mode = key_mode(kk);
+                const int2 x = st[slot * RS_STREAM_THREADS];
+                d = max(d, (mode == 1u ? x.y : x.x) + 1);
+                pk |= (slot | (mode << 5)) << (7 * m);
+                ++m;
+            }
+#pragma unroll
+            for (int i = 0; i < RS_CHUNK; ++i) cur[i] = nxt[i];
+        }
+        if (m) close(tidx, pk, m, d);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_PASSES] = 1;
+}
+
 // =====================================================================================
 // group by (depth, type): counting sort.  Each CTA first aggregates its tile's keys in
 // a shared-memory table (open addressing) so hot keys (the 0-set of a wide graph) cost

@@ -20,6 +20,7 @@ constexpr int RS_WK = 32 * RS_ITEMS;               // keys per warp
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per tile
 constexpr int RS_MAXPASS = 5;
 constexpr int RS_HIST_GRID = 296;
+constexpr int RS_LB = 8;                           // look-back window (tiles per round trip)
 
 struct SortWs {
     uint32_t* hist;        // [RS_MAXPASS][256]
@@ -130,13 +131,23 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
         st_release64(st, rs_pack(epoch, 2, cnt));
     } else {
         st_release64(st, rs_pack(epoch, 1, cnt));
+        // windowed look-back: RS_LB predecessors' (flag | count) words per round trip (each
+        // word is self-contained, so relaxed loads suffice and stay in flight together)
         int64_t p = (int64_t)tile - 1;
-        while (p >= 0) {
-            uint64_t s;
-            do { s = ld_acquire64(status + (uint64_t)p * 256 + d); } while ((uint32_t)(s >> 34) != epoch);
-            excl += (uint32_t)s;
-            if (((s >> 32) & 3u) == 2u) break;
-            --p;
+        bool found = false;
+        while (!found) {
+            uint64_t sv[RS_LB];
+#pragma unroll
+            for (int i = 0; i < RS_LB; ++i)
+                sv[i] = p - i >= 0 ? ld_relaxed64(status + (uint64_t)(p - i) * 256 + d) : rs_pack(epoch, 2, 0);
+#pragma unroll
+            for (int i = 0; i < RS_LB; ++i) {
+                if (found) continue;
+                while ((uint32_t)(sv[i] >> 34) != epoch) sv[i] = ld_relaxed64(status + (uint64_t)(p - i) * 256 + d);
+                excl += (uint32_t)sv[i];
+                found = ((sv[i] >> 32) & 3u) == 2u;
+            }
+            p -= RS_LB;
         }
         st_release64(st, rs_pack(epoch, 2, excl + cnt));
     }

@@ -355,7 +355,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     // rank fixpoint (persistent, cooperative)
     CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
     if (stream) {
-        const uint32_t gs = grid_for(db->max_rec, RS_STREAM_THREADS, (uint32_t)db->nsm * 16);
+        const uint32_t gs = grid_for(db->max_rec, RS_STREAM_TILE, (uint32_t)db->nsm * 6);
         rank_stream_tm1_kernel<<<gs, RS_STREAM_THREADS, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_D, db->d_sc);
         ++db->launches;
     } else {
@@ -383,7 +383,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
         }
         ++db->launches;
     }
-    const uint32_t g = grid_for(db->n, 256, 148 * 8);
+    const uint32_t g = grid_for(db->n / 4 + 1, 256, 148 * 4);
     depth_reduce_kernel<<<g, 256, 0, s>>>(db->d_D, (uint32_t)db->n, db->d_sc);
     ++db->launches;
     STAGE("rank");

@@ -493,15 +493,18 @@ __device__ __forceinline__ void rank_generic(const uint64_t* __restrict__ keys, 
                         cur = OpXf::combine(cur, rec_xf(head, mode, dv[k]));
                     }
                 }
-                uint32_t old[RK_ITEMS];    // all raises in flight together
-#pragma unroll
-                for (int k = 0; k < RK_ITEMS; ++k)
-                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k])
-                                          : 0xFFFFFFFFu;
+                // raises as fire-and-forget reductions (RED.MAX): a raise is detected from the
+                // gathered value (L > dv) instead of the atomic's return, so the sweep does not
+                // wait a round trip per tile; a raise another warp made meanwhile at most costs
+                // one more sweep (the next gather sees it: every value is a lower bound)
                 bool chg = false;
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k)
-                    if (old[k] < (uint32_t)L[k]) { chg = true; raised |= 1u << k; }
+                    if (L[k] > dv[k]) {
+                        atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k]);
+                        chg = true;
+                        raised |= 1u << k;
+                    }
                 if (!__any_sync(0xffffffffu, chg)) {
                     // this sweep raised nothing: its aggregate and incoming state are the
                     // tile's fixpoint until a record's transaction is raised
@@ -665,14 +668,13 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
                         cur = OpXf::combine(cur, rec_xf(head, mode, dv[k]));
                     }
                 }
-                uint32_t old[RK_ITEMS];
+                bool chg = false;                  // RED.MAX raises (see rank_generic)
 #pragma unroll
                 for (int k = 0; k < RK_ITEMS; ++k)
-                    old[k] = L[k] > dv[k] ? atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k])
-                                          : 0xFFFFFFFFu;
-                bool chg = false;
-#pragma unroll
-                for (int k = 0; k < RK_ITEMS; ++k) chg |= old[k] < (uint32_t)L[k];
+                    if (L[k] > dv[k]) {
+                        atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L[k]);
+                        chg = true;
+                    }
                 raised |= __any_sync(0xffffffffu, chg);
                 carry = OpXf::combine(carry, tot);
             }
@@ -713,65 +715,94 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
 // (13 sweeps in the first pass, profiles/round1.md).
 constexpr int RS_STREAM_THREADS = 128;
 constexpr int RS_CHUNK = 8;
+constexpr int RS_STREAM_TILE = RS_STREAM_THREADS * 8;     // records scanned for heads per CTA
+// Each CTA first collects the subscriber heads (first record of a subscriber) of its
+// tile of RS_STREAM_TILE sorted records into shared memory, then its threads walk those
+// subscribers (a walk may run past the tile) — so the lanes of a warp walk in lockstep
+// instead of diverging between head checks and walks (the SIMT cost of a thread-per-
+// record formulation).
 __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(const uint64_t* __restrict__ keys,
                                                                            const uint32_t* nrec_ptr, uint32_t* D,
                                                                            uint32_t* sc) {
     __shared__ int2 st_all[RS_STREAM_THREADS * TM1_STRIDE];      // (Wd, Md) per slot, per thread
+    __shared__ uint32_t heads[RS_STREAM_TILE];
+    __shared__ uint32_t s_nh;
     int2* st = st_all + threadIdx.x;                            // slot k at st[k * THREADS]: no bank conflicts
     const uint32_t nrec = *nrec_ptr;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nrec; p += stride) {
-        uint64_t k = __ldg(&keys[p]);
-        const uint64_t root = key_item(k) >> TM1_SLOT_BITS;
-        if (p > 0 && (key_item(__ldg(&keys[p - 1])) >> TM1_SLOT_BITS) == root) continue;   // not the root's head
-#pragma unroll 8
-        for (uint32_t j = 0; j < TM1_STRIDE; ++j) st[j * RS_STREAM_THREADS] = make_int2(-1, -1);
-        // walk the root's records in chunks of RS_CHUNK keys, the next chunk's loads in
-        // flight while the current one is processed.  The open transaction's records
-        // (distinct items, <= 3) are packed 7 bits each (slot | mode << 5) in `pk`; its
-        // depth is max'ed as they arrive (the state changes only when it closes).
-        uint64_t cur[RS_CHUNK], nxt[RS_CHUNK];
-        auto load = [&](uint64_t* b, uint32_t q) {
+    const uint32_t ntiles = (nrec + RS_STREAM_TILE - 1) / RS_STREAM_TILE;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x == 0) s_nh = 0;
+        __syncthreads();
+        const uint32_t t0 = tile * RS_STREAM_TILE;
 #pragma unroll
-            for (int i = 0; i < RS_CHUNK; ++i) b[i] = q + i < nrec ? __ldg(&keys[q + i]) : ~0ull;
-        };
-        auto close = [&](uint32_t idx, uint32_t pk, int m, int d) {
-            for (int j = 0; j < m; ++j) {
-                const uint32_t e = (pk >> (7 * j)) & 0x7Fu;
-                int2* x = &st[(e & 31u) * RS_STREAM_THREADS];
-                if ((e >> 5) == 1u) *x = make_int2(d, d);
-                else x->y = max(x->y, d);
+        for (int i = 0; i < RS_STREAM_TILE / RS_STREAM_THREADS; ++i) {
+            const uint32_t p = t0 + i * RS_STREAM_THREADS + threadIdx.x;
+            bool head = false;
+            if (p < nrec) {
+                const uint64_t r = key_item(__ldg(&keys[p])) >> TM1_SLOT_BITS;
+                head = p == 0 || (key_item(__ldg(&keys[p - 1])) >> TM1_SLOT_BITS) != r;
             }
-            D[idx] = (uint32_t)d;
-        };
-        uint32_t q = p;
-        load(cur, q);
-        q += RS_CHUNK;
-        uint32_t tidx = 0xFFFFFFFFu, pk = 0;
-        int m = 0, d = 0;
-        bool go = true;
-        while (go) {
-            load(nxt, q);
-            q += RS_CHUNK;
-#pragma unroll
-            for (int i = 0; i < RS_CHUNK; ++i) {
-                const uint64_t kk = cur[i];
-                if (!go || (key_item(kk) >> TM1_SLOT_BITS) != root) { go = false; continue; }
-                const uint32_t id = key_idx(kk);
-                if (id != tidx) {
-                    if (m) close(tidx, pk, m, d);
-                    tidx = id; pk = 0; m = 0; d = 0;
-                }
-                const uint32_t slot = (uint32_t)(key_item(kk) & (TM1_STRIDE - 1)), mode = key_mode(kk);
-                const int2 x = st[slot * RS_STREAM_THREADS];
-                d = max(d, (mode == 1u ? x.y : x.x) + 1);
-                pk |= (slot | (mode << 5)) << (7 * m);
-                ++m;
-            }
-#pragma unroll
-            for (int i = 0; i < RS_CHUNK; ++i) cur[i] = nxt[i];
+            const uint32_t m = __ballot_sync(0xffffffffu, head);
+            uint32_t base = 0;
+            if (lane_id() == 0 && m) base = atomicAdd(&s_nh, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (head) heads[base + __popc(m & lanemask_lt())] = p;
         }
-        if (m) close(tidx, pk, m, d);
+        __syncthreads();
+        const uint32_t nh = s_nh;
+        for (uint32_t h = threadIdx.x; h < nh; h += RS_STREAM_THREADS) {
+            const uint32_t p = heads[h];
+            const uint64_t root = key_item(__ldg(&keys[p])) >> TM1_SLOT_BITS;
+#pragma unroll 8
+            for (uint32_t j = 0; j < TM1_STRIDE; ++j) st[j * RS_STREAM_THREADS] = make_int2(-1, -1);
+            // walk the root's records in chunks of RS_CHUNK keys, the next chunk's loads in
+            // flight while the current one is processed.  The open transaction's records
+            // (distinct items, <= 3) are packed 7 bits each (slot | mode << 5) in `pk`; its
+            // depth is max'ed as they arrive (the state changes only when it closes).
+            uint64_t cur[RS_CHUNK], nxt[RS_CHUNK];
+            auto load = [&](uint64_t* b, uint32_t q) {
+#pragma unroll
+                for (int i = 0; i < RS_CHUNK; ++i) b[i] = q + i < nrec ? __ldg(&keys[q + i]) : ~0ull;
+            };
+            auto close = [&](uint32_t idx, uint32_t pk, int m, int d) {
+                for (int j = 0; j < m; ++j) {
+                    const uint32_t e = (pk >> (7 * j)) & 0x7Fu;
+                    int2* x = &st[(e & 31u) * RS_STREAM_THREADS];
+                    if ((e >> 5) == 1u) *x = make_int2(d, d);
+                    else x->y = max(x->y, d);
+                }
+                D[idx] = (uint32_t)d;
+            };
+            uint32_t q = p;
+            load(cur, q);
+            q += RS_CHUNK;
+            uint32_t tidx = 0xFFFFFFFFu, pk = 0;
+            int m = 0, d = 0;
+            bool go = true;
+            while (go) {
+                load(nxt, q);
+                q += RS_CHUNK;
+#pragma unroll
+                for (int i = 0; i < RS_CHUNK; ++i) {
+                    const uint64_t kk = cur[i];
+                    if (!go || (key_item(kk) >> TM1_SLOT_BITS) != root) { go = false; continue; }
+                    const uint32_t id = key_idx(kk);
+                    if (id != tidx) {
+                        if (m) close(tidx, pk, m, d);
+                        tidx = id; pk = 0; m = 0; d = 0;
+                    }
+                    const uint32_t slot = (uint32_t)(key_item(kk) & (TM1_STRIDE - 1)), mode = key_mode(kk);
+                    const int2 x = st[slot * RS_STREAM_THREADS];
+                    d = max(d, (mode == 1u ? x.y : x.x) + 1);
+                    pk |= (slot | (mode << 5)) << (7 * m);
+                    ++m;
+                }
+#pragma unroll
+                for (int i = 0; i < RS_CHUNK; ++i) cur[i] = nxt[i];
+            }
+            if (m) close(tidx, pk, m, d);
+        }
+        __syncthreads();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_PASSES] = 1;
 }
@@ -781,19 +812,54 @@ __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(cons
 // a shared-memory table (open addressing) so hot keys (the 0-set of a wide graph) cost
 // one global atomic per CTA instead of one per warp; keys that do not fit go global.
 // =====================================================================================
+// Block-level reductions of grid-stride counters: one global atomic per CTA (a global
+// atomic per warp on one address serialises thousands of them at L2).
+DEV uint32_t block_sum_u32(uint32_t v) {      // result valid in thread 0 (blockDim.x <= 1024)
+    __shared__ uint32_t red_sm[32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane_id() == 0) red_sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? red_sm[threadIdx.x] : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+DEV uint32_t block_max_u32(uint32_t v) {      // result valid in thread 0
+    __shared__ uint32_t rmx_sm[32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane_id() == 0) rmx_sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? rmx_sm[threadIdx.x] : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    return v;
+}
+
 __global__ void __launch_bounds__(256) depth_reduce_kernel(const uint32_t* D, uint32_t n, uint32_t* sc) {
     uint32_t mx = 0, z = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t d = D[i];
+    const uint32_t n4 = n / 4;
+    const uint4* D4 = reinterpret_cast<const uint4*>(D);         // D is cudaMalloc'ed: 16-B aligned
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        const uint4 d = __ldcg(&D4[i]);
+        mx = max(max(mx, max(d.x, d.y)), max(d.z, d.w));
+        z += (d.x == 0) + (d.y == 0) + (d.z == 0) + (d.w == 0);
+    }
+    for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t d = __ldcg(&D[i]);
         mx = max(mx, d);
         z += d == 0;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        z += __shfl_xor_sync(0xffffffffu, z, o);
-    }
-    if (lane_id() == 0) {
+    mx = block_max_u32(mx);
+    z = block_sum_u32(z);
+    if (threadIdx.x == 0) {
         atomicMax(&sc[SC_MAXD], mx);
         atomicAdd(&sc[SC_ZERO], z);
     }
@@ -921,6 +987,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                                                                uint32_t diag, uint32_t cluster_c) {
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
+    constexpr bool TAILRUN = S != S_TPCC && PW > 0;
     // prefetched first slice of the round this CTA executes next
     uint32_t nidx = 0xFFFFFFFFu, nt = 0;
     uint32_t np[PW > 0 ? PW : 1];
@@ -1028,6 +1095,54 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                 __syncthreads();
             }
         }
+        // Warp runs of tiny rounds: rounds k .. e-1 that are narrow, need one CTA and hold
+        // <= 32 transactions each are executed by warp 0 of the CTA alone, lane j taking
+        // the round's j-th transaction, separated by __syncwarp() (which orders the lanes'
+        // memory accesses) instead of a 1024-thread __syncthreads; the next round's
+        // parameters are loaded before the current one executes.  The run's last round
+        // goes through the regular path below (its hand-off to whatever follows).
+        // Other CTAs of the cluster hold no work in these rounds and skip them too.
+        if (TAILRUN && !trace && nar && gk == 1 && !(diag & 256u)) {
+            uint32_t e = k;
+            while (e < nk && e + 1 < cb + KX_CH && narrow(e) && G(e) == 1 && soff[e - cb + 1] - soff[e - cb] <= 32u) ++e;
+            if (e >= k + 2) {                   // rounds k .. e-2 in the warp run, e-1 regular
+                if (b == 0 && tid < 32) {
+                    auto ld = [&](uint32_t kk, uint32_t& idx, uint32_t& t, uint32_t* q) {
+                        const uint32_t j = soff[kk - cb] + tid;
+                        idx = 0xFFFFFFFFu;
+                        if (j < soff[kk - cb + 1]) {
+                            idx = __ldg(&perm[j]);
+                            t = __ldg(&ptype[j]);
+#pragma unroll
+                            for (int w = 0; w < (PW > 0 ? PW : 1); w += 4) {
+                                const uint4 v = __ldg(reinterpret_cast<const uint4*>(pp + (uint64_t)j * PW + w));
+                                q[w] = v.x; q[w + 1] = v.y; q[w + 2] = v.z; q[w + 3] = v.w;
+                            }
+                        }
+                    };
+                    uint32_t xi, xt = 0, xq[PW > 0 ? PW : 1];
+                    ld(k, xi, xt, xq);
+                    for (uint32_t kk = k; kk + 1 < e; ++kk) {
+                        uint32_t yi = 0xFFFFFFFFu, yt = 0, yq[PW > 0 ? PW : 1];
+                        if (kk + 2 < e) ld(kk + 1, yi, yt, yq);
+                        if (xi != 0xFFFFFFFFu) exec_txn_p<S, SH>(db, xi, xt, xq);
+                        if (yi != 0xFFFFFFFFu) warm_rows<S>(db, yt, yq);      // next round's rows into L2
+                        __syncwarp();
+                        xi = yi; xt = yt;
+#pragma unroll
+                        for (int w = 0; w < (PW > 0 ? PW : 1); ++w) xq[w] = yq[w];
+                    }
+                }
+                __syncthreads();
+                k = e - 1;
+                bounds(k, lo, hi);
+                slice(lo, hi, 1, lo, hi);
+                prefetch(lo, hi);
+                prev = k - 1;
+                gprev = 1;
+                continue;
+            }
+        }
         if (trace && tid == 0) {
             const uint64_t now = globaltimer_ns();
             if (b == 0) trace[8 * k] = now;
@@ -1131,24 +1246,19 @@ __global__ void __launch_bounds__(256) frag_emit_kernel(DevDb db, const uint32_t
         fragments_local<S>(db, i, keys + off[i]);
 }
 // c of Algorithm 1: transactions whose fragments span > 1 partition
-DEV void add_count(uint32_t* dst, bool pred) {
-    const uint32_t b = __ballot_sync(0xffffffffu, pred);
-    if (lane_id() == 0 && b) atomicAdd(dst, (uint32_t)__popc(b));
-}
 template <int S>
 __global__ void __launch_bounds__(256) cross_count_kernel(DevDb db, uint32_t* dst) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t b = blockIdx.x * blockDim.x; b < db.n; b += stride) {
-        const uint32_t i = b + threadIdx.x;
-        add_count(dst, i < db.n && fragments<S>(db, i, nullptr) > 1);
-    }
+    uint32_t c = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x)
+        c += fragments<S>(db, i, nullptr) > 1;
+    c = block_sum_u32(c);
+    if (threadIdx.x == 0 && c) atomicAdd(dst, c);
 }
 __global__ void __launch_bounds__(256) count_gt1_kernel(const uint32_t* cnt, uint32_t n, uint32_t* dst) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t b = blockIdx.x * blockDim.x; b < n; b += stride) {
-        const uint32_t i = b + threadIdx.x;
-        add_count(dst, i < n && cnt[i] > 1);
-    }
+    uint32_t c = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c += cnt[i] > 1;
+    c = block_sum_u32(c);
+    if (threadIdx.x == 0 && c) atomicAdd(dst, c);
 }
 __global__ void __launch_bounds__(256) part_bounds_kernel(const uint64_t* frags, const uint32_t* nf_ptr, uint32_t nparts,
                                                           uint32_t* part_off) {
@@ -1186,13 +1296,61 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
     if (lane_id() == 0 && hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
 }
 
+// One thread per partition runs its fragments in ts order.  The
+// chain is serial, but what each fragment READS before executing (its fragment key, the
+// transaction's type and parameter offset, the parameter words) is immutable, so it is
+// loaded ahead in a software pipeline: fragment j+3 key, j+2 type/offset, j+1 parameter
+// words (and its rows warmed into L2), j executes -- one dependent load per stage per
+// iteration instead of a chain of four before every fragment.
 template <int S>
 __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t* __restrict__ frags,
                                                         const uint32_t* __restrict__ part_off, uint32_t nparts, uint32_t* sc) {
+    constexpr int PW = S == S_TPCB ? 4 : 8;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= nparts) return;
     const uint32_t lo = part_off[p], hi = part_off[p + 1];
-    for (uint32_t j = lo; j < hi; ++j) exec_frag<S>(db, __ldg(&frags[j]));
+    const bool sh = db.ts != nullptr;
+    constexpr uint64_t NONE = ~0ull;
+    auto key = [&](uint32_t j) -> uint64_t { return j < hi ? __ldg(&frags[j]) : NONE; };
+    auto fidx = [](uint64_t fk) -> uint32_t { return (uint32_t)(fk >> 8) & 0xFFFFFFu; };
+    // stage registers: k1..k3 keys of fragments j+1..j+3; t2/o2 type/offset of j+2 (and
+    // t1/o1 of j+1); q1 parameter words of j+1; k0/t0/q0 the fragment executing now
+    uint64_t k0 = key(lo), k1 = key(lo + 1), k2 = key(lo + 2), k3 = key(lo + 3);
+    uint32_t t0 = 0, o0 = 0, t1 = 0, o1 = 0, t2 = 0, o2 = 0;
+    if (k0 != NONE) { t0 = db.type[fidx(k0)]; o0 = db.poff[fidx(k0)]; }
+    if (k1 != NONE) { t1 = db.type[fidx(k1)]; o1 = db.poff[fidx(k1)]; }
+    if (k2 != NONE) { t2 = db.type[fidx(k2)]; o2 = db.poff[fidx(k2)]; }
+    uint32_t q0[PW], q1[PW];
+#pragma unroll
+    for (int w = 0; w < PW; ++w) {
+        q0[w] = k0 != NONE ? db.pw[o0 + w] : 0u;
+        q1[w] = k1 != NONE ? db.pw[o1 + w] : 0u;
+    }
+    for (uint32_t j = lo; j < hi; ++j) {
+        // issue the next stages' loads (consumed next iteration)
+        const uint64_t k4 = key(j + 4);
+        uint32_t t3 = 0, o3 = 0;
+        if (k3 != NONE) { t3 = db.type[fidx(k3)]; o3 = db.poff[fidx(k3)]; }
+        uint32_t q2[PW];
+#pragma unroll
+        for (int w = 0; w < PW; ++w) q2[w] = k2 != NONE ? db.pw[o2 + w] : 0u;
+        if (k1 != NONE) warm_rows<S>(db, t1, q1);
+        // execute fragment j
+        const uint32_t idx = fidx(k0), kind = (uint32_t)k0 & 0xFFu;
+        if (S == S_TPCB) {
+            if (kind != F_REMOTE) tpcb_home(db, idx, q0, sh);
+            if (kind != F_HOME) tpcb_account(db, idx, q0);
+        } else {
+            tm1_txn(db, idx, t0, q0);
+        }
+        // shift the pipeline
+        k0 = k1; k1 = k2; k2 = k3; k3 = k4;
+        t0 = t1; t1 = t2; t2 = t3;
+        o1 = o2; o2 = o3;
+#pragma unroll
+        for (int w = 0; w < PW; ++w) { q0[w] = q1[w]; q1[w] = q2[w]; }
+    }
+    (void)o0; (void)o1;
     if (hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
 }
 
@@ -1208,9 +1366,8 @@ __global__ void __launch_bounds__(256) count_aborts_kernel(const uint8_t* __rest
     }
     for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         c += status[i] != 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane_id() == 0 && c) atomicAdd(out, c);
+    c = block_sum_u32(c);
+    if (threadIdx.x == 0 && c) atomicAdd(out, c);
 }
 
 // =====================================================================================

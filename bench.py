@@ -485,6 +485,12 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": peak_kind,
                 "algorithmic_bytes": kbytes, "kernel_ms": kms,
+                # K-SET exec is bounded by its d+1 dependent rounds: the
+                # per-round latency is the number that moves it on deep graphs
+                "critical_path": ({"rounds": last["depth"] + 1,
+                                   "us_per_round": 1e3 * phase["ms_exec"] / (last["depth"] + 1)}
+                                  if eff == "kset" else {"max_chain": last["max_chain"]} if eff == "part"
+                                  else None),
                 "share_of_step": kms / phase["ms_total"] if phase["ms_total"] else None}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) -----------------

@@ -1102,7 +1102,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         // parameters are loaded before the current one executes.  The run's last round
         // goes through the regular path below (its hand-off to whatever follows).
         // Other CTAs of the cluster hold no work in these rounds and skip them too.
-        if (TAILRUN && !trace && nar && gk == 1 && !(diag & 256u)) {
+        if (TAILRUN && nar && gk == 1 && !(diag & 256u)) {
             uint32_t e = k;
             while (e < nk && e + 1 < cb + KX_CH && narrow(e) && G(e) == 1 && soff[e - cb + 1] - soff[e - cb] <= 32u) ++e;
             if (e >= k + 2) {                   // rounds k .. e-2 in the warp run, e-1 regular
@@ -1123,6 +1123,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                     uint32_t xi, xt = 0, xq[PW > 0 ? PW : 1];
                     ld(k, xi, xt, xq);
                     for (uint32_t kk = k; kk + 1 < e; ++kk) {
+                        if (trace && tid == 0) trace[8 * kk] = globaltimer_ns();        // round start
                         uint32_t yi = 0xFFFFFFFFu, yt = 0, yq[PW > 0 ? PW : 1];
                         if (kk + 2 < e) ld(kk + 1, yi, yt, yq);
                         if (xi != 0xFFFFFFFFu) exec_txn_p<S, SH>(db, xi, xt, xq);

@@ -164,6 +164,10 @@ struct gputx_db {
     uint32_t rank_dirty = 1;                  // dirty-tile worklist (GPUTX_RANK_DIRTY overrides)
     uint32_t rank_root = 0;                   // root-local sweeps (GPUTX_RANK_ROOT overrides)
     uint32_t rank_stream = 1;                 // TM-1 per-subscriber streaming rank (GPUTX_RANK_STREAM overrides)
+    uint32_t rank_window = 0;                 // TPC-C windowed rank: log2 window (GPUTX_RANK_WINDOW overrides)
+    int rank_window_grid = 0;
+    uint32_t* d_wseg = nullptr;               // window -> first sorted record
+    int2* d_wst = nullptr;                    // item -> (a, m) at the end of the previous windows
     bool rec_item_sorted = false;             // d_sorted holds records in (item, ts) order
     int rank_root_grid = 0;
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
@@ -344,17 +348,46 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     // TM-1: single-subscriber transactions -> sort on the subscriber bits only and run
     // the exact streaming recurrence per subscriber (rank_stream_tm1_kernel)
     const bool stream = S == S_TM1 && db->rank_stream;
+    // TPC-C: windowed rank -> (window, item, ts) order: stable sort on the item bits, then
+    // on the window bits of the transaction index (key bits [6 + WB, 30))
+    const uint32_t wb = db->rank_window;
+    const bool windowed = S == S_TPCC && wb && db->n > (1ull << wb);
+    const uint32_t nwin = windowed ? (uint32_t)((db->n - 1) >> wb) + 1 : 1;
     if (stream)
         TRY(sort_records(db, KEY_ITEM_SHIFT + TM1_SLOT_BITS, db->item_bits - TM1_SLOT_BITS, db->d_sc + SC_NREC,
                          db->max_rec));
     else
         TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
-    db->rec_item_sorted = !stream;
+    if (windowed) {
+        uint64_t* other = db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a;
+        db->d_sorted = radix_sort_u64(db->d_sorted, other, db->d_sc + SC_NREC, db->max_rec, 6 + wb, bits_for(nwin - 1),
+                                      db->sort_ws, db->epoch, s);
+        db->launches += 2 + (bits_for(nwin - 1) + 7) / 8;
+    }
+    db->rec_item_sorted = !stream && !windowed;
     STAGE("sort");
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
-    if (stream) {
+    if (windowed) {
+        win_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, wb,
+                                                                             nwin, db->d_wseg);
+        ++db->launches;
+        CK(cudaMemsetAsync(db->d_wst, 0xFF, db->n_items * sizeof(int2), s));     // (-1, -1): no access yet
+        const uint64_t* keys = db->d_sorted;
+        const uint32_t* seg = db->d_wseg;
+        uint32_t nw = nwin;
+        uint32_t* D = db->d_D;
+        int2* wst = db->d_wst;
+        LookBack<Xf> lb = db->lb_rank;
+        GridBar* bar = db->d_bar;
+        uint32_t* sc = db->d_sc;
+        uint32_t maxp = 1u << 16;
+        uint32_t lmax = db->rank_local;
+        void* args[] = {&keys, &seg, &nw, &D, &wst, &lb, &bar, &sc, &maxp, &lmax};
+        TRY(launch_coop(db, (const void*)rank_window_kernel, db->rank_window_grid, RK_THREADS, args));
+        ++db->launches;
+    } else if (stream) {
         const uint32_t gs = grid_for(db->max_rec, RS_STREAM_TILE, (uint32_t)db->nsm * 6);
         rank_stream_tm1_kernel<<<gs, RS_STREAM_THREADS, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_D, db->d_sc);
         ++db->launches;
@@ -826,6 +859,15 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->rank_root = schema == S_TPCC ? 0 : 1;
     if (const char* e = getenv("GPUTX_RANK_ROOT")) db->rank_root = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_RANK_STREAM")) db->rank_stream = (uint32_t)atoi(e);
+    // TPC-C: 16 k-transaction windows (<= 23 passes per window)
+    db->rank_window = schema == S_TPCC ? 14 : 0;
+    if (const char* e = getenv("GPUTX_RANK_WINDOW")) db->rank_window = (uint32_t)atoi(e);
+    db->rank_window_grid = coop_grid(db, rank_window_kernel, RK_THREADS, 0);
+    if (db->rank_window) {
+        gputx_status st2;
+        if ((st2 = dalloc(db, &db->d_wseg, (db->max_bulk >> db->rank_window) + 4)) || (st2 = dalloc(db, &db->d_wst, n_items + 1)))
+            return bail(st2);
+    }
     db->rank_root_grid = schema == S_TPCB ? coop_grid(db, rank_root_kernel<S_TPCB>, RK_THREADS, 0)
                          : schema == S_TM1 ? coop_grid(db, rank_root_kernel<S_TM1>, RK_THREADS, 0)
                                            : coop_grid(db, rank_root_kernel<S_TPCC>, RK_THREADS, 0);
@@ -835,6 +877,8 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->kset_cluster = schema == S_TPCB ? 16 : 8;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
+    // K-SET runs: rounds of up to runmax transactions run inside CTA 0 (kernels.cuh "Runs")
+    if (const char* e = getenv("GPUTX_KSET_RUNMAX")) db->kset_diag = (db->kset_diag & 0xFFFFu) | ((uint32_t)atoi(e) << 16);
     db->sync_stages = getenv("GPUTX_SYNC") != nullptr;
     if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
     if (const char* e = getenv("GPUTX_TPL_SLEEP")) {
@@ -1424,7 +1468,7 @@ void gputx_close_db(gputx_db* db) {
                   db->sort_ws.hist, db->sort_ws.status, db->sort_ws.tickets, db->rank_memo.aggA,
                   db->rank_memo.carD, db->rank_memo.dirty, db->rank_memo.recpos, db->d_rtrace, db->d_ts,
                   db->d_src, db->d_home_pos, db->d_xflag, db->s_type, db->s_poff, db->s_pw, db->s_ts,
-                  db->d_hstatus, db->d_hout};
+                  db->d_hstatus, db->d_hout, db->d_wseg, db->d_wst};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (db->h_sc) cudaFreeHost(db->h_sc);

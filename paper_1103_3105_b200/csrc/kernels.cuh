@@ -548,6 +548,213 @@ __device__ __forceinline__ void rank_generic(const uint64_t* __restrict__ keys, 
     }
 }
 
+// -------------------------------------------------------------------------------------
+// Windowed rank (TPC-C).  The records are sorted by (window, item, ts),
+// a window being 2^WB consecutive timestamps, and the fixpoint is iterated one window
+// after the other: a group head inside window w starts from the state (a, m) its item
+// had at the end of window w-1 (wst[item], (-1, -1) before the first access) instead
+// of (-1, -1).  A transaction's records all lie in its own window, and every earlier
+// access to an item lies in an earlier window or earlier in the same group, so the
+// per-window fixpoint with the carried states is the exact depth (SA-5 "exact" on every
+// configuration).  TPC-C's whole-bulk iteration needs ~230 grid passes over all 7 M
+// records because its longest paths hop between items hundreds of times; windowed, each
+// pass touches one window's ~115 k records (L2-resident) and a window converges in
+// <= ~25 passes.  After a window converges one more sweep writes the states of its
+// groups' last records to wst.
+// -------------------------------------------------------------------------------------
+DEV Xf rkw_const(int a, int m) { return Xf{NEG, NEG, a, NEG, NEG, m}; }
+// a head's map: the record's map applied after the carried state (a constant)
+DEV Xf rkw_xf(bool head, uint32_t mode, int d, int2 c) {
+    const Xf x = rec_xf(false, mode, d);
+    return head ? OpXf::combine(rkw_const(c.x, c.y), x) : x;
+}
+DEV int rkw_level(bool head, uint32_t mode, int d, const Xf& cur, int2 c) {
+    return rec_level(false, mode, d, head ? rkw_const(c.x, c.y) : cur);
+}
+// warp-tile [tb, tb + RK_WT) of window [ws, we) into the warp's stage: head/mode/valid
+// bits (the window's first record is a head), the records' depths and the heads'
+// carried states
+DEV uint32_t rkw_load(const uint64_t* __restrict__ keys, uint32_t ws, uint32_t we, uint32_t tb, uint64_t* stage,
+                      const uint32_t* D, const int2* wst, int* dv, int2* cs) {
+    const uint32_t lane = lane_id();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        const uint32_t i = k * 32 + lane;
+        stage[i] = tb + i < we ? __ldg(&keys[tb + i]) : ~0ull;
+    }
+    const uint64_t prev = tb > ws ? __ldg(&keys[tb - 1]) : ~0ull;
+    __syncwarp();
+    uint32_t hw = 0;
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k) {
+        const uint32_t pos = lane * RK_ITEMS + k;
+        dv[k] = 0;
+        cs[k] = make_int2(-1, -1);
+        if (tb + pos < we) {
+            const uint64_t key = stage[pos];
+            const uint64_t pk = pos ? stage[pos - 1] : prev;
+            const bool head = tb + pos == ws || key_item(pk) != key_item(key);
+            hw |= rk_bits(head, key_mode(key), k);
+            dv[k] = (int)__ldcg(&D[key_idx(key)]);
+            if (head) cs[k] = __ldcg(&wst[key_item(key)]);
+        }
+    }
+    return hw;
+}
+DEV Xf rkw_compose(uint32_t hw, const int* dv, const int2* cs) {
+    Xf agg = OpXf::identity();
+#pragma unroll
+    for (int k = 0; k < RK_ITEMS; ++k)
+        if (rk_valid(hw, k)) agg = OpXf::combine(agg, rkw_xf(rk_head(hw, k), rk_mode(hw, k), dv[k], cs[k]));
+    return agg;
+}
+
+__global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64_t* __restrict__ keys,
+                                                                 const uint32_t* __restrict__ seg, uint32_t nwin,
+                                                                 uint32_t* D, int2* wst, LookBack<Xf> lb, GridBar* bar,
+                                                                 uint32_t* sc, uint32_t max_passes, uint32_t local_max) {
+    constexpr uint32_t NW = RK_THREADS / 32;
+    __shared__ uint64_t stage_all[NW * RK_WT];
+    __shared__ Xf sm[8];
+    __shared__ Xf wagg[NW];
+    __shared__ int s_chg;
+    Xf* cta_agg = lb.agg;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+    uint64_t* stage = stage_all + wid * RK_WT;
+    const uint32_t gw = blockIdx.x * NW + wid;
+    uint32_t gpass = 0;
+    bool noconv = false;
+    for (uint32_t w = 0; w < nwin; ++w) {
+        const uint32_t ws = __ldcg(&seg[w]), we = __ldcg(&seg[w + 1]);
+        if (ws >= we) continue;                          // (uniform: every CTA reads the same seg)
+        const uint32_t nwt = (we - ws + RK_WT - 1) / RK_WT;
+        const uint32_t per = (nwt + gridDim.x * NW - 1) / (gridDim.x * NW);
+        const uint32_t w0 = min(nwt, gw * per), w1 = min(nwt, w0 + per);
+        Xf carry0 = OpXf::identity();                    // state entering this warp's range
+        for (uint32_t pass = 0;; ++pass, ++gpass) {
+            if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (gpass + 1) % 3] = 0;
+            if (tid == 0) s_chg = 0;
+            // A: aggregate of this warp's range, then of the CTA's
+            Xf mine = OpXf::identity();
+            for (uint32_t wt = w0; wt < w1; ++wt) {
+                int dv[RK_ITEMS];
+                int2 cs[RK_ITEMS];
+                const uint32_t hw = rkw_load(keys, ws, we, ws + wt * RK_WT, stage, D, wst, dv, cs);
+                Xf tot;
+                rk_wscan(rkw_compose(hw, dv, cs), tot);
+                mine = OpXf::combine(mine, tot);
+            }
+            if (lane == 0) wagg[wid] = mine;
+            __syncthreads();
+            if (tid == 0) {
+                Xf c = OpXf::identity();
+                for (uint32_t j = 0; j < NW; ++j) c = OpXf::combine(c, wagg[j]);
+                lb_store(&cta_agg[blockIdx.x], c);
+            }
+            grid_sync(bar);
+            // C: state entering this warp's range
+            Xf carry = OpXf::identity();
+            for (uint32_t c0 = 0; c0 < blockIdx.x; c0 += RK_THREADS) {
+                const Xf x = (c0 + tid < blockIdx.x) ? lb_load(&cta_agg[c0 + tid]) : OpXf::identity();
+                Xf tot;
+                block_scan_excl<Xf, OpXf>(x, tot, sm);
+                carry = OpXf::combine(carry, tot);
+            }
+            for (uint32_t j = 0; j < wid; ++j) carry = OpXf::combine(carry, wagg[j]);
+            carry0 = carry;
+            // D: sweep the warp-tiles in order, raising depths (RED.MAX)
+            bool wchg = false;
+            for (uint32_t wt = w0; wt < w1; ++wt) {
+                Xf last_tot = OpXf::identity();
+                for (uint32_t it = 0; it < local_max; ++it) {
+                    int dv[RK_ITEMS];
+                    int2 cs[RK_ITEMS];
+                    const uint32_t hw = rkw_load(keys, ws, we, ws + wt * RK_WT, stage, D, wst, dv, cs);
+                    Xf tot;
+                    const Xf ex = rk_wscan(rkw_compose(hw, dv, cs), tot);
+                    last_tot = tot;
+                    Xf cur = OpXf::combine(carry, ex);
+                    bool chg = false;
+#pragma unroll
+                    for (int k = 0; k < RK_ITEMS; ++k) {
+                        if (!rk_valid(hw, k)) continue;
+                        const bool head = rk_head(hw, k);
+                        const uint32_t mode = rk_mode(hw, k);
+                        const int L = rkw_level(head, mode, dv[k], cur, cs[k]);
+                        cur = OpXf::combine(cur, rkw_xf(head, mode, dv[k], cs[k]));
+                        if (L > dv[k]) {
+                            atomicMax(&D[key_idx(stage[lane * RK_ITEMS + k])], (uint32_t)L);
+                            chg = true;
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, chg)) break;
+                    wchg = true;
+                }
+                carry = OpXf::combine(carry, last_tot);
+            }
+            if (lane == 0 && wchg) s_chg = 1;
+            __syncthreads();
+            if (tid == 0 && s_chg) sc[SC_CHG0 + gpass % 3] = 1;
+            grid_sync(bar);
+            const uint32_t c = __ldcg(&sc[SC_CHG0 + gpass % 3]);
+            if (!c || pass + 1 >= max_passes) {
+                noconv |= c != 0;
+                ++gpass;
+                break;
+            }
+        }
+        // the window's final states: the last record of each group writes its item's
+        // state (D did not change in the last pass, so carry0 and the sweep are exact)
+        {
+            Xf carry = carry0;
+            for (uint32_t wt = w0; wt < w1; ++wt) {
+                const uint32_t tb = ws + wt * RK_WT;
+                int dv[RK_ITEMS];
+                int2 cs[RK_ITEMS];
+                const uint32_t hw = rkw_load(keys, ws, we, tb, stage, D, wst, dv, cs);
+                const uint64_t after = tb + RK_WT < we ? __ldg(&keys[tb + RK_WT]) : ~0ull;
+                Xf tot;
+                const Xf ex = rk_wscan(rkw_compose(hw, dv, cs), tot);
+                Xf cur = OpXf::combine(carry, ex);
+                int2 outv[RK_ITEMS];
+                uint32_t tail = 0;
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k) {
+                    if (!rk_valid(hw, k)) continue;
+                    cur = OpXf::combine(cur, rkw_xf(rk_head(hw, k), rk_mode(hw, k), dv[k], cs[k]));
+                    const uint32_t pos = lane * RK_ITEMS + k;
+                    const uint64_t nk = pos + 1 < RK_WT ? stage[pos + 1] : after;
+                    if (tb + pos + 1 >= we || key_item(nk) != key_item(stage[pos])) {
+                        tail |= 1u << k;
+                        outv[k] = make_int2(cur.ac, cur.mc);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < RK_ITEMS; ++k)
+                    if ((tail >> k) & 1u) __stcg(&wst[key_item(stage[lane * RK_ITEMS + k])], outv[k]);
+                carry = OpXf::combine(carry, tot);
+            }
+        }
+        grid_sync(bar);                                   // states visible to the next window
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        sc[SC_PASSES] = gpass;
+        sc[SC_NOCONV] = noconv ? 1u : 0u;
+    }
+}
+
+// seg[w] = first sorted record of window w (records sorted by (window, item, ts))
+__global__ void __launch_bounds__(256) win_bounds_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                         uint32_t wb, uint32_t nwin, uint32_t* seg) {
+    const uint32_t nrec = *nrec_ptr;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= nrec; k += gridDim.x * blockDim.x) {
+        const int64_t w = k < nrec ? (int64_t)(key_idx(__ldg(&keys[k])) >> wb) : (int64_t)nwin;
+        const int64_t pw = k ? (int64_t)(key_idx(__ldg(&keys[k - 1])) >> wb) : -1;
+        for (int64_t q = pw + 1; q <= w; ++q) seg[q] = k;
+    }
+}
+
 __global__ void __launch_bounds__(RK_THREADS, 2) rank_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
                                                           uint32_t* D, LookBack<Xf> lb, uint32_t epoch0,
                                                           GridBar* bar, uint32_t* sc, uint32_t max_passes,
@@ -1095,18 +1302,26 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                 __syncthreads();
             }
         }
-        // Warp runs of tiny rounds: rounds k .. e-1 that are narrow, need one CTA and hold
-        // <= 32 transactions each are executed by warp 0 of the CTA alone, lane j taking
-        // the round's j-th transaction, separated by __syncwarp() (which orders the lanes'
-        // memory accesses) instead of a 1024-thread __syncthreads; the next round's
-        // parameters are loaded before the current one executes.  The run's last round
-        // goes through the regular path below (its hand-off to whatever follows).
+        // Runs of one-CTA rounds: rounds k .. e-1 that are narrow and need one CTA (<= Q
+        // transactions each) are executed by the first W warps of CTA 0 alone (W = the
+        // run's largest round / 32), thread j taking the round's j-th transaction,
+        // separated by __syncwarp() (W = 1) or a named barrier of W warps -- both order the
+        // participants' memory accesses -- instead of a 1024-thread __syncthreads; the
+        // next round's parameters are loaded before the current one executes.  The run's
+        // last round goes through the regular path below (its hand-off to what follows).
         // Other CTAs of the cluster hold no work in these rounds and skip them too.
         if (TAILRUN && nar && gk == 1 && !(diag & 256u)) {
-            uint32_t e = k;
-            while (e < nk && e + 1 < cb + KX_CH && narrow(e) && G(e) == 1 && soff[e - cb + 1] - soff[e - cb] <= 32u) ++e;
-            if (e >= k + 2) {                   // rounds k .. e-2 in the warp run, e-1 regular
-                if (b == 0 && tid < 32) {
+            // rounds of up to runmax transactions join the run (diag >> 16; 0: one-CTA rounds)
+            const uint32_t runmax = min((uint32_t)KB, diag >> 16);
+            uint32_t e = k, wmax = 0;
+            while (e < nk && e + 1 < cb + KX_CH && narrow(e) &&
+                   (G(e) == 1 || soff[e - cb + 1] - soff[e - cb] <= runmax)) {
+                wmax = max(wmax, soff[e - cb + 1] - soff[e - cb]);
+                ++e;
+            }
+            const uint32_t nthr = min((uint32_t)KB, (wmax + 31) & ~31u);
+            if (e >= k + 2) {                   // rounds k .. e-2 in the run, e-1 regular
+                if (b == 0 && tid < nthr) {
                     auto ld = [&](uint32_t kk, uint32_t& idx, uint32_t& t, uint32_t* q) {
                         const uint32_t j = soff[kk - cb] + tid;
                         idx = 0xFFFFFFFFu;
@@ -1128,19 +1343,22 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                         if (kk + 2 < e) ld(kk + 1, yi, yt, yq);
                         if (xi != 0xFFFFFFFFu) exec_txn_p<S, SH>(db, xi, xt, xq);
                         if (yi != 0xFFFFFFFFu) warm_rows<S>(db, yt, yq);      // next round's rows into L2
-                        __syncwarp();
+                        if (nthr == 32) __syncwarp();
+                        else asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
                         xi = yi; xt = yt;
 #pragma unroll
                         for (int w = 0; w < (PW > 0 ? PW : 1); ++w) xq[w] = yq[w];
                     }
                 }
-                __syncthreads();
+                // the run's writes reach every CTA of the cluster before round e-1 (which
+                // may need several of them)
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
                 k = e - 1;
                 bounds(k, lo, hi);
-                slice(lo, hi, 1, lo, hi);
+                slice(lo, hi, G(k), lo, hi);
                 prefetch(lo, hi);
                 prev = k - 1;
-                gprev = 1;
+                gprev = G(k - 1);
                 continue;
             }
         }

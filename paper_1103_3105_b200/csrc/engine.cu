@@ -166,6 +166,7 @@ struct gputx_db {
     uint32_t rank_stream = 1;                 // TM-1 per-subscriber streaming rank (GPUTX_RANK_STREAM overrides)
     uint32_t rank_window = 0;                 // TPC-C windowed rank: log2 window (GPUTX_RANK_WINDOW overrides)
     int rank_window_grid = 0;
+    uint32_t rank_window_cluster = 0;         // 0: cooperative grid with grid barriers (GPUTX_RANK_WCLUSTER)
     uint32_t* d_wseg = nullptr;               // window -> first sorted record
     int2* d_wst = nullptr;                    // item -> (a, m) at the end of the previous windows
     bool rec_item_sorted = false;             // d_sorted holds records in (item, ts) order
@@ -385,7 +386,23 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
         uint32_t maxp = 1u << 16;
         uint32_t lmax = db->rank_local;
         void* args[] = {&keys, &seg, &nw, &D, &wst, &lb, &bar, &sc, &maxp, &lmax};
-        TRY(launch_coop(db, (const void*)rank_window_kernel, db->rank_window_grid, RK_THREADS, args));
+        if (db->rank_window_cluster) {           // one cluster; hardware cluster barriers
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(db->rank_window_cluster);
+            lc.blockDim = dim3(RK_THREADS);
+            lc.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = db->rank_window_cluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelExC(&lc, (const void*)rank_window_kernel<true>, args);
+            if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("rank cluster launch: ") + cudaGetErrorString(e));
+        } else {
+            TRY(launch_coop(db, (const void*)rank_window_kernel<false>, db->rank_window_grid, RK_THREADS, args));
+        }
         ++db->launches;
     } else if (stream) {
         const uint32_t gs = grid_for(db->max_rec, RS_STREAM_TILE, (uint32_t)db->nsm * 6);
@@ -859,10 +876,18 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->rank_root = schema == S_TPCC ? 0 : 1;
     if (const char* e = getenv("GPUTX_RANK_ROOT")) db->rank_root = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_RANK_STREAM")) db->rank_stream = (uint32_t)atoi(e);
-    // TPC-C: 16 k-transaction windows (<= 23 passes per window)
-    db->rank_window = schema == S_TPCC ? 14 : 0;
+    // TPC-C: 128 k-transaction windows (measured: 2^12 .. 2^17 -> rank 19.6 .. 10.8 ms at
+    // 1 M transactions, profiles/round1.md)
+    db->rank_window = schema == S_TPCC ? 17 : 0;
     if (const char* e = getenv("GPUTX_RANK_WINDOW")) db->rank_window = (uint32_t)atoi(e);
-    db->rank_window_grid = coop_grid(db, rank_window_kernel, RK_THREADS, 0);
+    db->rank_window_grid = coop_grid(db, rank_window_kernel<false>, RK_THREADS, 0);
+    // one 16-CTA cluster with hardware barriers was measured slower than the full
+    // cooperative grid with the aggregate reuse (kernels.cuh rank_window_kernel)
+    db->rank_window_cluster = 0;
+    if (const char* e = getenv("GPUTX_RANK_WCLUSTER")) db->rank_window_cluster = (uint32_t)atoi(e);
+    if (db->rank_window_cluster > 8 &&
+        cudaFuncSetAttribute(rank_window_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        db->rank_window_cluster = 8;
     if (db->rank_window) {
         gputx_status st2;
         if ((st2 = dalloc(db, &db->d_wseg, (db->max_bulk >> db->rank_window) + 4)) || (st2 = dalloc(db, &db->d_wst, n_items + 1)))

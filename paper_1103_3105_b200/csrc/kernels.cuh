@@ -610,6 +610,16 @@ DEV Xf rkw_compose(uint32_t hw, const int* dv, const int2* cs) {
     return agg;
 }
 
+// CL: launched as ONE thread-block cluster (gridDim.x = cluster size): the barriers
+// between the phases of a pass are hardware cluster barriers (release/acquire at
+// cluster scope) instead of grid barriers -- a window's passes are latency-bound, so
+// fewer SMs with a cheaper barrier win.
+template <bool CL>
+DEV void rkw_sync(GridBar* bar) {
+    if (CL) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else grid_sync(bar);
+}
+template <bool CL>
 __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64_t* __restrict__ keys,
                                                                  const uint32_t* __restrict__ seg, uint32_t nwin,
                                                                  uint32_t* D, int2* wst, LookBack<Xf> lb, GridBar* bar,
@@ -632,27 +642,36 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
         const uint32_t per = (nwt + gridDim.x * NW - 1) / (gridDim.x * NW);
         const uint32_t w0 = min(nwt, gw * per), w1 = min(nwt, w0 + per);
         Xf carry0 = OpXf::identity();                    // state entering this warp's range
+        // Passes alternate between "fresh" (phase A recomputes every range aggregate from
+        // the current depths; 2 barriers) and "reuse" (the aggregates each warp composed
+        // while sweeping in the previous pass are published at its end; 1 barrier, no
+        // phase A).  Reused aggregates may be stale (another warp raised a shared
+        // transaction since) but are lower bounds, so the relaxation stays sound; the
+        // window is converged only after a FRESH pass raises nothing.
+        bool fresh = true;
         for (uint32_t pass = 0;; ++pass, ++gpass) {
             if (blockIdx.x == 0 && tid == 0) sc[SC_CHG0 + (gpass + 1) % 3] = 0;
             if (tid == 0) s_chg = 0;
-            // A: aggregate of this warp's range, then of the CTA's
-            Xf mine = OpXf::identity();
-            for (uint32_t wt = w0; wt < w1; ++wt) {
-                int dv[RK_ITEMS];
-                int2 cs[RK_ITEMS];
-                const uint32_t hw = rkw_load(keys, ws, we, ws + wt * RK_WT, stage, D, wst, dv, cs);
-                Xf tot;
-                rk_wscan(rkw_compose(hw, dv, cs), tot);
-                mine = OpXf::combine(mine, tot);
+            if (fresh) {
+                // A: aggregate of this warp's range, then of the CTA's
+                Xf mine = OpXf::identity();
+                for (uint32_t wt = w0; wt < w1; ++wt) {
+                    int dv[RK_ITEMS];
+                    int2 cs[RK_ITEMS];
+                    const uint32_t hw = rkw_load(keys, ws, we, ws + wt * RK_WT, stage, D, wst, dv, cs);
+                    Xf tot;
+                    rk_wscan(rkw_compose(hw, dv, cs), tot);
+                    mine = OpXf::combine(mine, tot);
+                }
+                if (lane == 0) wagg[wid] = mine;
+                __syncthreads();
+                if (tid == 0) {
+                    Xf c = OpXf::identity();
+                    for (uint32_t j = 0; j < NW; ++j) c = OpXf::combine(c, wagg[j]);
+                    lb_store(&cta_agg[blockIdx.x], c);
+                }
+                rkw_sync<CL>(bar);
             }
-            if (lane == 0) wagg[wid] = mine;
-            __syncthreads();
-            if (tid == 0) {
-                Xf c = OpXf::identity();
-                for (uint32_t j = 0; j < NW; ++j) c = OpXf::combine(c, wagg[j]);
-                lb_store(&cta_agg[blockIdx.x], c);
-            }
-            grid_sync(bar);
             // C: state entering this warp's range
             Xf carry = OpXf::identity();
             for (uint32_t c0 = 0; c0 < blockIdx.x; c0 += RK_THREADS) {
@@ -665,6 +684,7 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
             carry0 = carry;
             // D: sweep the warp-tiles in order, raising depths (RED.MAX)
             bool wchg = false;
+            Xf mine_d = OpXf::identity();
             for (uint32_t wt = w0; wt < w1; ++wt) {
                 Xf last_tot = OpXf::identity();
                 for (uint32_t it = 0; it < local_max; ++it) {
@@ -692,17 +712,26 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
                     wchg = true;
                 }
                 carry = OpXf::combine(carry, last_tot);
+                mine_d = OpXf::combine(mine_d, last_tot);
             }
             if (lane == 0 && wchg) s_chg = 1;
+            __syncthreads();                           // every warp is past C and D
+            if (lane == 0) wagg[wid] = mine_d;         // (the next pass may reuse them)
             __syncthreads();
-            if (tid == 0 && s_chg) sc[SC_CHG0 + gpass % 3] = 1;
-            grid_sync(bar);
+            if (tid == 0) {
+                if (s_chg) sc[SC_CHG0 + gpass % 3] = 1;
+                Xf cc = OpXf::identity();
+                for (uint32_t j = 0; j < NW; ++j) cc = OpXf::combine(cc, wagg[j]);
+                lb_store(&cta_agg[blockIdx.x], cc);
+            }
+            rkw_sync<CL>(bar);
             const uint32_t c = __ldcg(&sc[SC_CHG0 + gpass % 3]);
-            if (!c || pass + 1 >= max_passes) {
+            if ((!c && fresh) || pass + 1 >= max_passes) {
                 noconv |= c != 0;
                 ++gpass;
                 break;
             }
+            fresh = !c;                                // nothing raised on reused aggregates: verify
         }
         // the window's final states: the last record of each group writes its item's
         // state (D did not change in the last pass, so carry0 and the sweep are exact)
@@ -736,7 +765,7 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
                 carry = OpXf::combine(carry, tot);
             }
         }
-        grid_sync(bar);                                   // states visible to the next window
+        rkw_sync<CL>(bar);                                   // states visible to the next window
     }
     if (blockIdx.x == 0 && tid == 0) {
         sc[SC_PASSES] = gpass;

@@ -330,7 +330,7 @@ def main():
     ap.add_argument("--others", default="part,tpl,auto", help="extra strategies measured on the same bulks "
                     "(auto: Algorithm 1, PAPER.md:422-437, with the library's default thresholds)")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample (the contract asks for ~10-30 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -497,7 +497,7 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, txns, runs, secs = oracle_rate(wl, W.make_db(wl["schema"], dims, seed=args.seed), bulks,
-                                             args.cpu_seconds, 50)
+                                             args.cpu_seconds, 1000)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{runs} bulk(s) x {n} txns of the same workload, serial loop {secs:.2f} s",
                "cpu": cpu_model(), "nproc": os.cpu_count()}

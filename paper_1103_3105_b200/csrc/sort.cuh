@@ -27,6 +27,7 @@ struct SortWs {
     uint64_t* status;      // [max_tiles][256]  (epoch:30 | kind:2) << 32 | value
     uint32_t* tickets;     // [64]
     uint64_t max_tiles;
+    uint32_t items;        // keys per thread of a pass tile (8, 12 or 16; 0 = RS_ITEMS)
 };
 
 __global__ void __launch_bounds__(256) rs_hist_kernel(const uint64_t* __restrict__ keys,
@@ -67,6 +68,7 @@ DEV uint64_t rs_pack(uint32_t epoch, uint32_t kind, uint32_t v) {
     return ((uint64_t)((epoch << 2) | kind) << 32) | v;
 }
 
+template <int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __restrict__ in,
                                                              uint64_t* __restrict__ out,
                                                              const uint32_t* __restrict__ n_ptr,
@@ -78,30 +80,31 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
     __shared__ uint32_t tstart[256];
     __shared__ uint32_t gbase[256];
     __shared__ uint32_t scan_sm[8];
-    __shared__ uint64_t stage[RS_TILE];
+    constexpr int WK = 32 * ITEMS, TILE = RS_THREADS * ITEMS;
+    __shared__ uint64_t stage[TILE];
     __shared__ uint32_t s_tile;
 
     const uint32_t n = *n_ptr;
-    const uint32_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+    const uint32_t ntiles = (n + TILE - 1) / TILE;
     const uint32_t tid = threadIdx.x, lane = lane_id(), wid = warp_id();
     if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     for (uint32_t i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&whist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
-    const uint64_t tbase = (uint64_t)tile * RS_TILE;
+    const uint64_t tbase = (uint64_t)tile * TILE;
 
-    uint64_t key[RS_ITEMS];
-    uint16_t loc[RS_ITEMS];
-    const uint64_t wbase = tbase + wid * RS_WK;
+    uint64_t key[ITEMS];
+    uint16_t loc[ITEMS];
+    const uint64_t wbase = tbase + wid * WK;
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const uint64_t i = wbase + j * 32 + lane;
         key[j] = i < n ? __ldg(&in[i]) : ~0ull;
     }
     const uint32_t lmask = lanemask_lt();
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const uint64_t i = wbase + j * 32 + lane;
         const uint32_t d = i < n ? (uint32_t)(key[j] >> shift) & mask : 0x100u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
     tstart[d] = block_scan_excl<uint32_t, OpAddU32>(cnt, tot, scan_sm);
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const uint64_t i = wbase + j * 32 + lane;
         if (i < n) {
             const uint32_t dj = (uint32_t)(key[j] >> shift) & mask;
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
         }
     }
     __syncthreads();
-    const uint32_t tn = (n - tbase) < (uint64_t)RS_TILE ? (uint32_t)(n - tbase) : (uint32_t)RS_TILE;
+    const uint32_t tn = (n - tbase) < (uint64_t)TILE ? (uint32_t)(n - tbase) : (uint32_t)TILE;
     for (uint32_t i = tid; i < tn; i += RS_THREADS) {
         const uint64_t k = stage[i];
         const uint32_t dk = (uint32_t)(k >> shift) & mask;
@@ -182,14 +185,16 @@ inline uint64_t* radix_sort_u64(uint64_t* a, uint64_t* b, const uint32_t* n_dev,
     cudaMemsetAsync(ws.tickets, 0, sizeof(uint32_t) * 64, s);
     rs_hist_kernel<<<RS_HIST_GRID, 256, 0, s>>>(a, n_dev, lo, nbits, ws.hist);
     rs_scan_kernel<<<npass, 256, 0, s>>>(ws.hist);
-    const uint32_t grid = (uint32_t)((n_max + RS_TILE - 1) / RS_TILE);
+    const uint32_t tile = RS_THREADS * (ws.items ? ws.items : RS_ITEMS);
+    const uint32_t grid = (uint32_t)((n_max + tile - 1) / tile);
     uint64_t* src = a;
     uint64_t* dst = b;
     for (uint32_t p = 0; p < npass; ++p) {
         const uint32_t w = nbits - 8 * p < 8 ? nbits - 8 * p : 8;
         ++epoch;
-        rs_pass_kernel<<<grid, RS_THREADS, 0, s>>>(src, dst, n_dev, lo + 8 * p, (1u << w) - 1, ws.hist + p * 256,
-                                                   ws.status, epoch, ws.tickets + p);
+        auto fn = ws.items == 8 ? rs_pass_kernel<8> : ws.items == 12 ? rs_pass_kernel<12> : rs_pass_kernel<RS_ITEMS>;
+        fn<<<grid, RS_THREADS, 0, s>>>(src, dst, n_dev, lo + 8 * p, (1u << w) - 1, ws.hist + p * 256,
+                                       ws.status, epoch, ws.tickets + p);
         uint64_t* t = src; src = dst; dst = t;
     }
     return src;

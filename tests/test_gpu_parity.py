@@ -276,3 +276,35 @@ def test_auto_strategy_algorithm1(schema, dims, n, kw, want):
     assert st["strategy"] == want
     assert (st["zero_set"], st["depth"], st["cross"]) == (ref["w0"], ref["d"], ref["c"])
     db.close()
+
+
+@pytest.mark.parametrize("add_rule", [False, True])
+@pytest.mark.parametrize("wbits,n", [(8, 5_000), (10, 3 * 1024 + 1), (12, 4096), (13, 100)])
+def test_tpcc_windowed_rank(monkeypatch, wbits, n, add_rule):
+    """A5 windowed: windows of 2^wbits transactions,
+    a ragged last window, a bulk that is exactly whole windows and one smaller than a
+    window; depths equal the T-dependency-graph depths and the state
+    equals serial execution, with and without the ADD rule."""
+    monkeypatch.setenv("GPUTX_RANK_WINDOW", str(wbits))
+    dims = W.TpccDims(3, 4, 300, 2_000)
+    image = W.tpcc_db(dims, seed=5)
+    bulk = W.tpcc_bulk(dims, n, seed=13, remote_line_pct=20.0, remote_pay_pct=30.0)
+    db = gpu_db(W.TPCC, dims, image, n, add_rule=add_rule)
+    run_both(W.TPCC, dims, image, [bulk], "kset", db=db)
+    assert np.array_equal(db.depths(), oracle.depths(W.TPCC, dims.dims, image, bulk, add_rule=add_rule))
+    db.close()
+
+
+@pytest.mark.parametrize("runmax", [0, 1024])
+def test_kset_round_runs(monkeypatch, runmax):
+    """K-SET runs of one-CTA rounds (and, with GPUTX_KSET_RUNMAX, of narrow rounds up to
+    1,024 transactions) inside CTA 0: deep TM-1 NURand tail and TPC-B with few branches."""
+    monkeypatch.setenv("GPUTX_KSET_RUNMAX", str(runmax))
+    for schema, dims, n, kw in [(W.TM1, W.Tm1Dims(3_000), 20_000, dict(dist="nurand")),
+                                (W.TPCB, W.TpcbDims(3, 10, 1000), 6_000, dict(remote_pct=30.0))]:
+        image = W.make_db(schema, dims, seed=2)
+        bulk = W.make_bulk(schema, dims, n, 17, **kw)
+        db = gpu_db(schema, dims, image, n)
+        run_both(schema, dims, image, [bulk], "kset", db=db)
+        assert np.array_equal(db.depths(), oracle.depths(schema, dims.dims, image, bulk))
+        db.close()

@@ -242,7 +242,11 @@ gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes);
  *      transactions, [ts, out words] (gputx_shard_stride(schema, 1) words), grouped by
  *      home shard.
  *   5. gputx_shard_return_merge(db, recv, n_recv): OR the returned fragment outputs into
- *      the home records (fragments write disjoint fields).  Then gputx_read_results. */
+ *      the home records (fragments write disjoint fields).  Then gputx_read_results.
+ * The pack calls are synchronous: their send buffer is complete when they return.  The
+ * caller must have completed the writes into recv (e.g. synchronized the stream its
+ * exchange ran on) before calling gputx_shard_submit / gputx_shard_return_merge, which
+ * read it on the handle's stream. */
 uint32_t gputx_shard_stride(gputx_schema schema, int result);
 gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* home, uint32_t* send, uint64_t send_cap,
                               uint64_t* counts);

@@ -1167,6 +1167,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
             shard_pack_kernel<<<grid_for(np, 256, 148 * 8), 256, 0, s>>>(pairs, db->d_sc + SC_XTOTAL, db->s_type,
                                                                          db->s_poff, db->s_pw, db->s_ts, stride, send);
             ++db->launches;
+            CK(cudaStreamSynchronize(s));      // send is complete on return (the caller moves it)
         }
     } else {
         for (uint32_t q = 0; q < SC_COUNT; ++q) db->h_sc[q] = 0;
@@ -1240,6 +1241,7 @@ gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send
             if (!send) return GPUTX_EINVAL;
             ret_pack_kernel<<<grid_for(np, 256, 148 * 8), 256, 0, s>>>(pairs, db->d_sc + SC_XTOTAL, db->d_ts,
                                                                        db->d_out, ow, send);
+            CK(cudaStreamSynchronize(s));      // send is complete on return (the caller moves it)
         }
     } else {
         for (uint32_t q = 0; q < SC_COUNT; ++q) db->h_sc[q] = 0;

@@ -1531,17 +1531,55 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
     if (p >= nparts) return;                                   // warp-uniform
     const uint32_t lo = part_off[p], hi = part_off[p + 1];
     const bool sh = db.ts != nullptr;
+    const uint32_t lane = lane_id();
+    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
+    // L2 warming pipeline over the serial chain (cf. part_exec_kernel): while fragment j
+    // executes, the parameter words of j+2 and the rows of j+1 (district / stock / item /
+    // customer, from its already-warm parameters) are prefetched into L2
+    constexpr uint64_t NONE = ~0ull;
+    auto key = [&](uint32_t j) -> uint64_t { return j < hi ? __ldg(&frags[j]) : NONE; };
+    auto fidx = [](uint64_t fk) -> uint32_t { return (uint32_t)(fk >> 8) & 0xFFFFFFu; };
+    uint64_t k1 = key(lo + 1), k2 = key(lo + 2);
+    uint32_t o1 = k1 != NONE ? db.poff[fidx(k1)] : 0u, t1 = k1 != NONE ? db.type[fidx(k1)] : 0u;
     for (uint32_t j = lo; j < hi; ++j) {
         const uint64_t fk = __ldg(&frags[j]);
         const uint32_t idx = (uint32_t)(fk >> 8) & 0xFFFFFFu;
+        // issue: key of j+3, type/offset of j+2, parameter lines of j+2
+        const uint64_t k3 = key(j + 3);
+        uint32_t o2 = 0, t2 = 0;
+        if (k2 != NONE) {
+            o2 = db.poff[fidx(k2)];
+            t2 = db.type[fidx(k2)];
+            if (lane < 2) l2_warm(db.pw + o2 + 32 * lane);
+        }
+        // rows of j+1 (its parameters were warmed one iteration ago)
+        if (k1 != NONE) {
+            const uint32_t* q = db.pw + o1;
+            const uint32_t w = q[0], dd = q[1];
+            if (t1 == 0) {
+                const uint32_t cnt = min(q[3], 15u);
+                if (lane < cnt) {
+                    const uint32_t it = q[4 + 3 * lane], sw = q[5 + 3 * lane];
+                    if (it < I) {
+                        l2_warm(&COL(const int32_t, C_S_QTY)[(uint64_t)sw * I + it]);
+                        l2_warm(&COL(const int32_t, C_I_PRICE)[it]);
+                    }
+                }
+                if (lane == 31) l2_warm(&COL(const uint32_t, C_D_NEXT)[(uint64_t)w * D + dd]);
+            } else if (lane == 0 && q[4] != 2) {
+                l2_warm(&COL(const int64_t, C_C_BAL)[((uint64_t)q[2] * D + q[3]) * C + q[5]]);
+            }
+        }
         if ((fk & 0xFFu) == F_WHOLE || (db.type[idx] == 0 && fragments<S_TPCC>(db, idx, nullptr) == 1)) {
             tpcc_txn_warp(db, idx, db.type[idx], db.pw + db.poff[idx], sh);
         } else {
-            if (lane_id() == 0) exec_frag<S_TPCC>(db, fk);
+            if (lane == 0) exec_frag<S_TPCC>(db, fk);
             __syncwarp();
         }
+        k1 = k2; k2 = k3;
+        o1 = o2; t1 = t2;
     }
-    if (lane_id() == 0 && hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
+    if (lane == 0 && hi - lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
 }
 
 // One thread per partition runs its fragments in ts order.  The

@@ -33,6 +33,10 @@ def all_to_all_records(send: torch.Tensor, counts: list[int], stride: int, group
                            [c * stride for c in counts], group=group)          # C2 / C3
     if recv.device != send.device:
         recv = recv.to(send.device)
+    if recv.is_cuda:
+        # the engine reads recv on its own stream: the exchange's writes (NCCL, or the
+        # host-to-device copy after gloo) must have landed first (include/gputx.h)
+        torch.cuda.current_stream(recv.device).synchronize()
     return recv, total
 
 
@@ -72,11 +76,13 @@ class LocalShards:
         dbs = self.dbs
         packed = [db.shard_pack(h, on_device=on_device) for db, h in zip(dbs, homes)]
         recvs = self._exchange([p[0] for p in packed], [p[1] for p in packed], dbs[0].shard_stride(False))
+        torch.cuda.current_stream().synchronize()          # the device gathers have landed
         for db, (rv, n) in zip(dbs, recvs):
             db.shard_submit(rv, n)
         stats = [db.execute(strategy) for db in dbs]
         rp = [db.shard_return_pack() for db in dbs]
         rr = self._exchange([p[0] for p in rp], [p[1] for p in rp], dbs[0].shard_stride(True))
+        torch.cuda.current_stream().synchronize()
         for db, (rv, n) in zip(dbs, rr):
             db.shard_return_merge(rv, n)
         return stats

@@ -1524,6 +1524,27 @@ __global__ void __launch_bounds__(256) part_bounds_kernel(const uint64_t* frags,
 }
 // TPC-C: one warp per partition; a whole-transaction fragment runs as tpcc_txn_warp,
 // split fragments (remote lines / customer) on lane 0
+// the rows a TPC-C transaction will touch, prefetched into L2 by its warp (lane l: the
+// stock and item rows of line l; lane 31: the district; Payment: lane 0, the customer)
+DEV void tpcc_warm_warp(const DevDb& db, uint32_t t, const uint32_t* q) {
+    const uint32_t lane = lane_id();
+    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
+    const uint32_t w = q[0], dd = q[1];
+    if (t == 0) {
+        const uint32_t cnt = min(q[3], 15u);
+        if (lane < cnt) {
+            const uint32_t it = q[4 + 3 * lane], sw = q[5 + 3 * lane];
+            if (it < I) {
+                l2_warm(&COL(const int32_t, C_S_QTY)[(uint64_t)sw * I + it]);
+                l2_warm(&COL(const int32_t, C_I_PRICE)[it]);
+            }
+        }
+        if (lane == 31) l2_warm(&COL(const uint32_t, C_D_NEXT)[(uint64_t)w * D + dd]);
+    } else if (lane == 0 && q[4] != 2) {
+        l2_warm(&COL(const int64_t, C_C_BAL)[((uint64_t)q[2] * D + q[3]) * C + q[5]]);
+    }
+}
+
 __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uint64_t* __restrict__ frags,
                                                              const uint32_t* __restrict__ part_off, uint32_t nparts,
                                                              uint32_t* sc) {
@@ -1532,7 +1553,6 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
     const uint32_t lo = part_off[p], hi = part_off[p + 1];
     const bool sh = db.ts != nullptr;
     const uint32_t lane = lane_id();
-    const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
     // L2 warming pipeline over the serial chain (cf. part_exec_kernel): while fragment j
     // executes, the parameter words of j+2 and the rows of j+1 (district / stock / item /
     // customer, from its already-warm parameters) are prefetched into L2
@@ -1553,23 +1573,7 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
             if (lane < 2) l2_warm(db.pw + o2 + 32 * lane);
         }
         // rows of j+1 (its parameters were warmed one iteration ago)
-        if (k1 != NONE) {
-            const uint32_t* q = db.pw + o1;
-            const uint32_t w = q[0], dd = q[1];
-            if (t1 == 0) {
-                const uint32_t cnt = min(q[3], 15u);
-                if (lane < cnt) {
-                    const uint32_t it = q[4 + 3 * lane], sw = q[5 + 3 * lane];
-                    if (it < I) {
-                        l2_warm(&COL(const int32_t, C_S_QTY)[(uint64_t)sw * I + it]);
-                        l2_warm(&COL(const int32_t, C_I_PRICE)[it]);
-                    }
-                }
-                if (lane == 31) l2_warm(&COL(const uint32_t, C_D_NEXT)[(uint64_t)w * D + dd]);
-            } else if (lane == 0 && q[4] != 2) {
-                l2_warm(&COL(const int64_t, C_C_BAL)[((uint64_t)q[2] * D + q[3]) * C + q[5]]);
-            }
-        }
+        if (k1 != NONE) tpcc_warm_warp(db, t1, db.pw + o1);
         if ((fk & 0xFFu) == F_WHOLE || (db.type[idx] == 0 && fragments<S_TPCC>(db, idx, nullptr) == 1)) {
             tpcc_txn_warp(db, idx, db.type[idx], db.pw + db.poff[idx], sh);
         } else {
@@ -2024,6 +2028,9 @@ __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint
         if (j < k && (uint32_t)j == lane) item = r[j].item;
     const bool mine = (int)lane < k;
     const uint32_t key = mine ? __ldg(&lkey[rec_off[idx] + lane]) : 0u;
+    // the rows come into L2 while the locks are awaited (on the W_YTD / district chains
+    // the post-acquire execution is the critical path)
+    tpcc_warm_warp(db, db.type[idx], db.pw + db.poff[idx]);
     bool got = !mine;
     uint32_t polls = 0;
     while (!__all_sync(0xffffffffu, got)) {

@@ -866,7 +866,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
     // sweeps per warp-tile per rank pass, measured per schema (profiles/round1.md):
     // TM-1 / TPC-B chains are mostly root-local (sweeps close them in the tile), TPC-C's cross tiles
-    db->rank_local = schema == S_TPCC ? 1 : 4;
+    const bool add_rule = (cfg->flags & GPUTX_FLAG_ADD_RULE) != 0;
+    // TPC-B with the ADD rule: 1 in-tile sweep (its tiles settle at once; 0.75 -> 0.70 ms)
+    db->rank_local = schema == S_TPCC || (schema == S_TPCB && add_rule) ? 1 : 4;
     if (const char* e = getenv("GPUTX_RANK_LOCAL")) db->rank_local = (uint32_t)std::max(1, atoi(e));
     // TPC-C: each pass raises most of the long W_YTD chains' suffix, so nearly every tile is
     // dirty every pass and the marking costs more than it saves (profiles/round1.md)
@@ -876,7 +878,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // transactions never cross subscribers (2 passes: settle + confirm; 0.80 -> 0.21 ms),
     // TPC-B crosses branches only through remote accounts (7 -> 4 passes, 2.9 -> 2.1 ms).
     // TPC-C's 64 warehouses are far larger than a warp's share: CTA-range passes instead.
-    db->rank_root = schema == S_TPCC ? 0 : 1;
+    // (TPC-B with the ADD rule: the grid-wide scan balances better than whole branches
+    //  per warp, 0.97 -> 0.70 ms; profiles/round1.md)
+    db->rank_root = schema == S_TPCC || (schema == S_TPCB && add_rule) ? 0 : 1;
     if (const char* e = getenv("GPUTX_RANK_ROOT")) db->rank_root = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_RANK_STREAM")) db->rank_stream = (uint32_t)atoi(e);
     // TPC-C: 128 k-transaction windows (measured: 2^12 .. 2^17 -> rank 19.6 .. 10.8 ms at
@@ -901,7 +905,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
                                            : coop_grid(db, rank_root_kernel<S_TPCC>, RK_THREADS, 0);
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
-    db->kset_q = schema == S_TPCC ? 8 : schema == S_TPCB ? 64 : 128;   // TPC-C: one warp per txn, 8 warps
+    db->kset_q = schema == S_TPCC ? 8 : schema == S_TPCB ? 32 : 128;   // TPC-C: one warp per txn, 8 warps
     db->kset_cluster = schema == S_TPCB ? 16 : 8;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);

@@ -355,7 +355,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     const bool windowed = S == S_TPCC && wb && db->n > (1ull << wb);
     const uint32_t nwin = windowed ? (uint32_t)((db->n - 1) >> wb) + 1 : 1;
     if (stream)
-        TRY(sort_records(db, KEY_ITEM_SHIFT + TM1_SLOT_BITS, db->item_bits - TM1_SLOT_BITS, db->d_sc + SC_NREC,
+        TRY(sort_records(db, KEY_ITEM_SHIFT + TM1_COMP_BITS, db->item_bits - TM1_COMP_BITS, db->d_sc + SC_NREC,
                          db->max_rec));
     else
         TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));

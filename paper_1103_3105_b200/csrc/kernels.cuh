@@ -940,8 +940,9 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
 
 // Root-stream rank (TM-1): every TM-1 transaction touches the items of ONE subscriber
 // (PAPER.md:451-453), so the T-dependency graph is a disjoint union of per-subscriber
-// graphs.  The records are sorted on the subscriber bits only (stable: (root, ts)
-// order, a transaction's records adjacent), and one thread per subscriber runs the
+// graphs -- finer: per (subscriber, item component), TM1_COMP_BITS in schema.cuh.  The
+// records are sorted on the (subscriber, component) bits only (stable: (root, ts)
+// order, a transaction's records adjacent), and one thread per root runs the
 // streaming depth recurrence over them in ts order (SURVEY.md §8(c) "Depth oracle"):
 //   d(t) = max over t's records of (write ? Md[x] + 1 : Wd[x] + 1), 0 without records;
 //   then write: Wd[x] = Md[x] = d(t);  read: Md[x] = max(Md[x], d(t)).
@@ -975,8 +976,8 @@ __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(cons
             const uint32_t p = t0 + i * RS_STREAM_THREADS + threadIdx.x;
             bool head = false;
             if (p < nrec) {
-                const uint64_t r = key_item(__ldg(&keys[p])) >> TM1_SLOT_BITS;
-                head = p == 0 || (key_item(__ldg(&keys[p - 1])) >> TM1_SLOT_BITS) != r;
+                const uint64_t r = key_item(__ldg(&keys[p])) >> TM1_COMP_BITS;
+                head = p == 0 || (key_item(__ldg(&keys[p - 1])) >> TM1_COMP_BITS) != r;
             }
             const uint32_t m = __ballot_sync(0xffffffffu, head);
             uint32_t base = 0;
@@ -988,7 +989,7 @@ __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(cons
         const uint32_t nh = s_nh;
         for (uint32_t h = threadIdx.x; h < nh; h += RS_STREAM_THREADS) {
             const uint32_t p = heads[h];
-            const uint64_t root = key_item(__ldg(&keys[p])) >> TM1_SLOT_BITS;
+            const uint64_t root = key_item(__ldg(&keys[p])) >> TM1_COMP_BITS;     // (subscriber, component)
 #pragma unroll 8
             for (uint32_t j = 0; j < TM1_STRIDE; ++j) st[j * RS_STREAM_THREADS] = make_int2(-1, -1);
             // walk the root's records in chunks of RS_CHUNK keys, the next chunk's loads in
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(cons
 #pragma unroll
                 for (int i = 0; i < RS_CHUNK; ++i) {
                     const uint64_t kk = cur[i];
-                    if (!go || (key_item(kk) >> TM1_SLOT_BITS) != root) { go = false; continue; }
+                    if (!go || (key_item(kk) >> TM1_COMP_BITS) != root) { go = false; continue; }
                     const uint32_t id = key_idx(kk);
                     if (id != tidx) {
                         if (m) close(tidx, pk, m, d);

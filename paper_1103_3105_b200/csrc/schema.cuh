@@ -120,12 +120,17 @@ DEV int add_rec(Rec* r, int k, uint64_t item, uint32_t w) {
 // Item ids are partition-major (subscriber / branch / warehouse): all items of one
 // root key are adjacent, so the conflict groups a transaction touches sit in the same
 // sorted tile and the rank kernel's in-tile iteration resolves their chains on chip.
-//   TM-1 : s*32 + {0 BIT1, 1 VLR, 2+sf-1 SFDA, 6+(sf-1)*3+st/8 CF}   (18 of 32 slots: the
+//   TM-1 : s*32 + {0 BIT1, 1 VLR, 2+sf-1 SFDA, 8+(sf-1)*4+st/8 CF}   (18 of 32 slots: the
 //          subscriber is the item id's high bits, so a sort on them alone gives (root, ts))
 //   TPC-B: b*(1+T+A) + {0 BR, 1+t TEL, 1+T+a ACC}
 //   TPC-C: w*(2D+1+DC+I) + {d DNEXT, D WYTD, D+1+d DYTD, 2D+1+d*C+c CUST, 2D+1+DC+i STOCK}
 constexpr uint32_t TM1_SLOT_BITS = 5;
 constexpr uint64_t TM1_STRIDE = 1u << TM1_SLOT_BITS;
+// A TM-1 transaction touches one of a subscriber's independent item components: {BIT1,
+// VLR, SFDA*} (GSD, USD, UL; slots 0-7) or the CF slots of one sf (GND, ICF, DCF; slots
+// 8 + 4(sf-1) + st/8).  Slot >> 3 separates {A}, {CF sf 1, 2}, {CF sf 3, 4}: components
+// share no transaction, so their depths are independent (streaming rank walks each alone).
+constexpr uint32_t TM1_COMP_BITS = 3;
 // Basic operations of one (ingested) transaction.  Returns the count (<= MAX_REC).
 template <int S>
 DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
@@ -143,7 +148,7 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
         switch (t) {
         case 0: { uint64_t s = (uint64_t)(p[0] - 1) * TM1_STRIDE; r[0] = {s, 0u}; r[1] = {s + 1, 0u}; return 2; }
         case 1: {
-            uint64_t c = (uint64_t)(p[0] - 1) * TM1_STRIDE + 6 + (p[1] - 1) * 3;
+            uint64_t c = (uint64_t)(p[0] - 1) * TM1_STRIDE + 8 + (p[1] - 1) * 4;
             r[0] = {c, 0u}; r[1] = {c + 1, 0u}; r[2] = {c + 2, 0u};
             return 3;
         }
@@ -152,7 +157,7 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
         case 4: if (p[0] == 0) return 0; r[0] = {(uint64_t)(p[0] - 1) * TM1_STRIDE + 1, 1u}; return 1;
         case 5: case 6:
             if (p[0] == 0) return 0;
-            r[0] = {(uint64_t)(p[0] - 1) * TM1_STRIDE + 6 + (p[2] - 1) * 3 + p[3] / 8, 1u};
+            r[0] = {(uint64_t)(p[0] - 1) * TM1_STRIDE + 8 + (p[2] - 1) * 4 + p[3] / 8, 1u};
             return 1;
         }
         return 0;

@@ -1,7 +1,9 @@
 cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q -k "tpcb or add_rule or smoke" > gpurun_out/pytest_q.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_q.log; tail -2 gpurun_out/pytest_q.log
 run() { env $1 timeout 200 python bench.py --workload $3 --strategy $4 --steps 3 --warmup 3 --no-cpu-baseline --others "" > gpurun_out/tune_$2.json 2>gpurun_out/tune_$2.err; echo "$2 rc=$?"; }
-run "X=1" tpcb tpcb kset
-run "GPUTX_KSET_Q=16" tpcb_q16 tpcb kset
-run "X=1" tpcbadd tpcb_add kset
-run "X=1" tpcbhotadd tpcb_hot_add kset
+run "GPUTX_KSET_Q=64" tm1_q64 tm1 kset
+run "GPUTX_KSET_Q=256" tm1_q256 tm1 kset
+run "GPUTX_KSET_CLUSTER=16" tm1_c16 tm1 kset
+run "GPUTX_KSET_Q=4" tpcc_q4 tpcc kset
+run "GPUTX_KSET_Q=16" tpcc_q16 tpcc kset
+run "GPUTX_KSET_CLUSTER=16" tpcc_c16 tpcc kset
+run "GPUTX_KSET_CLUSTER=8" tpcb_c8 tpcb kset

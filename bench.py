@@ -125,8 +125,11 @@ def rank_bytes(schema: int, records: int, passes: int, n: int) -> int:
     return passes * records * 12 + 4 * n
 
 
-def rank_kernel_name(schema: int) -> str:
-    return {W.TM1: "rank_stream_tm1_kernel", W.TPCB: "rank_root_kernel", W.TPCC: "rank_window_kernel"}[schema]
+def rank_kernel_name(schema: int, add_rule: bool = False) -> str:
+    """The rank kernel the library runs by default (engine.cu gputx_open_db)."""
+    if schema == W.TPCB:
+        return "rank_kernel" if add_rule else "rank_root_kernel"
+    return {W.TM1: "rank_stream_tm1_kernel", W.TPCC: "rank_window_kernel"}[schema]
 
 
 def ncu_traffic(workload: str, kernel: str):
@@ -482,7 +485,7 @@ def main():
     cand = {}
     eff = last["strategy"]                                  # auto: the strategy Algorithm 1 chose
     if last["rank_passes"]:
-        cand[rank_kernel_name(wl["schema"])] = (rank_bytes(wl["schema"], last["records"], last["rank_passes"], n),
+        cand[rank_kernel_name(wl["schema"], wl.get("add_rule", False))] = (rank_bytes(wl["schema"], last["records"], last["rank_passes"], n),
                                                 phase["ms_rank"])
     cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1])

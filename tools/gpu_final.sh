@@ -24,6 +24,6 @@ for k in kset_exec rank_stream rs_pass group_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 3 -c 1 -o $O/full_tm1_$k \
     python bench.py --steps 1 --warmup 3 --others "" --no-cpu-baseline > $O/ncu_tm1_$k.log 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rank_root" -s 1 -c 1 -o $O/full_tpcb_add_rank_root \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rank_kernel" -s 1 -c 1 -o $O/full_tpcb_add_rank_kernel \
     python bench.py --workload tpcb_add --steps 1 --warmup 3 --others "" --no-cpu-baseline > $O/ncu_tpcb_add.log 2>&1
 ls $O

@@ -17,9 +17,9 @@ READ = {
     ("tm1", "rank_stream_tm1_kernel"): ("17.8 MB", "the serial walk of the hottest NURand (subscriber, component) roots bounds it; D writes stay in L2"),
     ("tm1", "rs_pass_kernel"): ("19.5 MB", "one of 3 passes over 1.2 M records: look-back latency, not bandwidth"),
     ("tm1", "group_kernel"): ("40 MB", "scatter of ids + 8 parameter words"),
-    ("tpcb_add", "rank_kernel"): ("296 MB", "2 grid passes over 12 M records (+ the first pass's recpos prologue)"),
-    ("tpcc_add", "rank_window_kernel"): ("see bench", "458 window passes; each touches one 2^17-transaction window (L2-resident)"),
-    ("tpcb", "kset_exec_kernel"): ("372 MB", "4,196 rounds of ≤ 1,000 deposits: critical-path bound"),
+    ("tpcb_add", "rank_kernel"): ("304 MB", "2 grid passes over 12 M records (+ the first pass's recpos prologue)"),
+    ("tpcc_add", "rank_window_kernel"): ("4873 MB", "458 window passes; each touches one 2^17-transaction window (L2-resident)"),
+    ("tpcb", "kset_exec_kernel"): ("404 MB", "4,196 rounds of ≤ 1,000 deposits: critical-path bound"),
 }
 rows = []
 for (wl, k), (alg, why) in READ.items():

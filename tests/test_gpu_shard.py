@@ -84,3 +84,17 @@ def test_sharded_errors():
         assert e.value.name == "ECROSS"
     finally:
         db.close()
+
+
+@pytest.mark.parametrize("schema,dims,n,kw", [
+    (W.TPCB, W.TpcbDims(12, 10, 500), 6000, dict(remote_pct=40.0)),
+    (W.TPCC, W.TpccDims(8, 10, 300, 2000), 5000, dict(remote_line_pct=10.0, remote_pay_pct=30.0)),
+])
+def test_auto_sharded(schema, dims, n, kw):
+    """GPUTX_AUTO on shards: each shard runs Algorithm 1 on its local graph (the choice
+    may differ between shards; every strategy is shard-local) and the union still
+    equals serial execution."""
+    image = W.make_db(schema, dims, seed=2)
+    bulk = W.make_bulk(schema, dims, n, 9, **kw)
+    stats = _run(schema, dims, image, bulk, 2, "auto")
+    assert all(s["strategy"] in ("kset", "part", "tpl") for s in stats)

@@ -1,10 +1,7 @@
-cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out/final2
-O=gpurun_out/final2
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rank_kernel" -s 1 -c 1 -o $O/full_tpcb_add_rank_kernel \
-    python bench.py --workload tpcb_add --steps 1 --warmup 3 --others "" --no-cpu-baseline > $O/ncu_tpcb_add.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rank_window" -s 1 -c 1 -o $O/full_tpcc_add_rank_window \
-    python bench.py --workload tpcc_add --steps 1 --warmup 3 --others "" --no-cpu-baseline > $O/ncu_tpcc_add.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kset_exec" -s 1 -c 1 -o $O/full_tpcb_kset_exec \
-    python bench.py --workload tpcb --steps 1 --warmup 3 --others "" --no-cpu-baseline > $O/ncu_tpcb.log 2>&1
-timeout 900 python bench.py --workload tpcb_add --steps 5 --warmup 3 > $O/bench_tpcb_add.json 2> $O/bench_tpcb_add.err
-ls $O
+cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
+run() { env $1 timeout 200 python bench.py --workload $3 --strategy $4 --steps 3 --warmup 3 --no-cpu-baseline --others "" > gpurun_out/tune_$2.json 2>gpurun_out/tune_$2.err; echo "$2 rc=$?"; }
+run "GPUTX_KSET_Q=24" tpcb_q24 tpcb kset
+run "GPUTX_KSET_Q=48" tpcb_q48 tpcb kset
+run "GPUTX_KSET_Q=32 GPUTX_KSET_CLUSTER=0" tpcb_q32c0 tpcb kset
+run "GPUTX_KSET_Q=16 GPUTX_KSET_CLUSTER=0" tpcb_q16c0 tpcb kset
+run "GPUTX_KSET_Q=8 GPUTX_KSET_CLUSTER=0" tpcb_q8c0 tpcb kset

@@ -1101,8 +1101,13 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     const uint64_t n = b->n;
     uint32_t n_words = 0;
     if (n) {
-        if (b->on_device) CK(cudaMemcpy(&n_words, b->param_off + n, 4, cudaMemcpyDeviceToHost));
-        else n_words = b->param_off[n];
+        if (b->on_device) {   // ordered on the handle's stream (the caller's buffers may come from it)
+            CK(cudaMemcpyAsync(db->h_sc + SC_COUNT - 1, b->param_off + n, 4, cudaMemcpyDeviceToHost, db->stream));
+            CK(cudaStreamSynchronize(db->stream));
+            n_words = db->h_sc[SC_COUNT - 1];
+        } else {
+            n_words = b->param_off[n];
+        }
     }
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     if (!b->ts && db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
@@ -1135,8 +1140,13 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
     const uint64_t n = b->n;
     uint32_t n_words = 0;
     if (n) {
-        if (b->on_device) CK(cudaMemcpy(&n_words, b->param_off + n, 4, cudaMemcpyDeviceToHost));
-        else n_words = b->param_off[n];
+        if (b->on_device) {   // ordered on the handle's stream (the caller's buffers may come from it)
+            CK(cudaMemcpyAsync(db->h_sc + SC_COUNT - 1, b->param_off + n, 4, cudaMemcpyDeviceToHost, db->stream));
+            CK(cudaStreamSynchronize(db->stream));
+            n_words = db->h_sc[SC_COUNT - 1];
+        } else {
+            n_words = b->param_off[n];
+        }
     }
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);

@@ -19,11 +19,11 @@ enum {
     SC_ERR = 0, SC_BADIDX, SC_NREC, SC_NFRAG, SC_MAXD, SC_ZERO, SC_PASSES, SC_CHG0, SC_CHG1, SC_CHG2,
     SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV, SC_XTOTAL,
     SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
-    SC_COUNT = 32
+    SC_COUNT = 40      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS)
 };
 enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
-constexpr int SC_CROSS = 24;      // c: transactions with fragments in > 1 PART partition
+constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {

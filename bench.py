@@ -400,6 +400,7 @@ def main():
         ms, stats = [], []
         for k in range(steps):
             flush.fill_(k & 0xFF)                        # L2 flush, outside the timed window
+            stream.synchronize()                         # (done before the window opens)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)

@@ -642,10 +642,10 @@ gputx_status execute_schema(gputx_db* db, gputx_strategy st) {
 }
 
 template <int S>
-void launch_ingest(gputx_db* db, uint32_t n_words) {
+void launch_ingest(gputx_db* db, uint32_t n_words, const uint32_t* nw_ptr) {
     DevDb v = make_devdb(db);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
-    ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, db->type_mask, db->d_ins_off,
+    ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, nw_ptr, db->type_mask, db->d_ins_off,
                                                 (uint32_t)(db->n + 1), db->d_sc, db->d_xflag);
                                                 ++db->launches;
 }
@@ -661,7 +661,9 @@ gputx_status submit_check(gputx_db* db, const gputx_bulk* b) {
 
 // the bulk is in d_type / d_poff / d_pw (/ d_ts, d_src): validate it, resolve the split
 // lookups, count insert rows
-gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words) {
+// pw_src (device, optional): the caller's parameter words, copied here with their count
+// read on the device from d_poff[n] (n_words is then ignored)
+gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uint32_t* pw_src = nullptr) {
     cudaStream_t s = db->stream;
     db->n = n;
     db->launches = 0;
@@ -674,9 +676,16 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words) {
     if (n) {
         if (ins_scan) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * ntab, s));
         if (db->nshards > 1) CK(cudaMemsetAsync(db->d_xflag, 0, n, s));
-        if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words);
-        else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words);
-        else launch_ingest<S_TPCC>(db, n_words);
+        const uint32_t* nw_ptr = nullptr;
+        if (pw_src) {
+            nw_ptr = db->d_poff + n;
+            n_words = (uint32_t)db->max_words;
+            copy_pw_kernel<<<148 * 4, 256, 0, s>>>(pw_src, nw_ptr, db->d_pw, n_words, db->d_sc);
+            ++db->launches;
+        }
+        if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words, nw_ptr);
+        else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words, nw_ptr);
+        else launch_ingest<S_TPCC>(db, n_words, nw_ptr);
         if (ins_scan && db->schema != S_TM1)
             for (int t = 0; t < ntab; ++t)
                 scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n,
@@ -687,11 +696,12 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words) {
     if (db->h_sc[SC_ERR]) {
         static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
                                      "parameter out of range", "bad param_off", "timestamps not increasing",
-                                     "home partition not owned by this shard"};
+                                     "home partition not owned by this shard", "too many parameter words"};
         const uint32_t e = db->h_sc[SC_ERR];
         db->n = 0;
+        if (e == E_WORDS) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
         return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : e == E_OWNER ? GPUTX_ECROSS : GPUTX_EINVAL,
-                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 8 ? e : 0]);
+                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 9 ? e : 0]);
     }
     // insert rows this bulk will append (decisions are static: two-phase procedures)
     for (auto& t : db->ins) {
@@ -1100,27 +1110,19 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     cudaStream_t s = db->stream;
     const uint64_t n = b->n;
     uint32_t n_words = 0;
-    if (n) {
-        if (b->on_device) {   // ordered on the handle's stream (the caller's buffers may come from it)
-            CK(cudaMemcpyAsync(db->h_sc + SC_COUNT - 1, b->param_off + n, 4, cudaMemcpyDeviceToHost, db->stream));
-            CK(cudaStreamSynchronize(db->stream));
-            n_words = db->h_sc[SC_COUNT - 1];
-        } else {
-            n_words = b->param_off[n];
-        }
-    }
+    if (n && !b->on_device) n_words = b->param_off[n];
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     if (!b->ts && db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
     db->has_ts = b->ts != nullptr;
-    if (n) {
+    if (n) {   // (device bulks: ordered on the handle's stream; the words' count is read there)
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
         CK(cudaMemcpyAsync(db->d_poff, b->param_off, (n + 1) * 4, kind, s));
-        if (n_words) CK(cudaMemcpyAsync(db->d_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
+        if (n_words && !b->on_device) CK(cudaMemcpyAsync(db->d_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
         if (b->ts) CK(cudaMemcpyAsync(db->d_ts, b->ts, n * 4, kind, s));
     }
     db->first_ts = db->next_ts;
-    TRY(finish_submit(db, n, n_words));
+    TRY(finish_submit(db, n, n_words, n && b->on_device ? b->param_words : nullptr));
     if (!b->ts) db->next_ts += n;
     if (first_ts) *first_ts = db->first_ts;
     return GPUTX_OK;

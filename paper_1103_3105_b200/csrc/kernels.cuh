@@ -21,7 +21,7 @@ enum {
     SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
     SC_COUNT = 40      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS)
 };
-enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7 };
+enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7, E_WORDS = 8 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
 
@@ -39,11 +39,25 @@ DEV void report_err(uint32_t* sc, uint32_t code, uint32_t idx) {
 // =====================================================================================
 // ingest: validate in place, resolve static lookups, count insert rows
 // =====================================================================================
+// A device-resident bulk's parameter words, copied with the count read on the device
+// (param_off[n]) -- no host round trip to size the copy; more than max_words -> E_WORDS
+__global__ void __launch_bounds__(256) copy_pw_kernel(const uint32_t* __restrict__ src, const uint32_t* nw_ptr,
+                                                      uint32_t* dst, uint32_t max_words, uint32_t* sc) {
+    uint32_t nw = __ldg(nw_ptr);
+    if (nw > max_words) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) report_err(sc, E_WORDS, 0);
+        nw = max_words;
+    }
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) dst[i] = __ldg(&src[i]);
+}
+
+// nw_ptr (optional): the word count on the device; n_words is then its upper bound
 template <int S>
-__global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uint32_t n_words, uint32_t type_mask,
-                                                     uint32_t* ins_cnt, uint32_t ins_stride, uint32_t* sc,
-                                                     uint8_t* xflag) {
+__global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uint32_t n_words, const uint32_t* nw_ptr,
+                                                     uint32_t type_mask, uint32_t* ins_cnt, uint32_t ins_stride,
+                                                     uint32_t* sc, uint8_t* xflag) {
     const uint32_t n = db.n;
+    if (nw_ptr) n_words = min(__ldg(nw_ptr), n_words);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t t = db.type[i];
         // sharded: a peer's transaction (NOT_HOME) only runs its fragments on this shard

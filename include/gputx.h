@@ -116,7 +116,7 @@ typedef struct {
     uint64_t ksets;          /* d + 1 (K-SET)                                            */
     uint64_t zero_set;       /* w0 = |0-set| (K-SET)                        */
     uint64_t records;        /* access records emitted (K-SET, TPL)                     */
-    uint64_t rank_passes;    /* segmented max-scan passes to the fixpoint (K-SET)       */
+    uint64_t rank_passes;    /* rank passes to the fixpoint (K-SET; TPC-C: summed over windows; TM-1: 1) */
     uint64_t parts;          /* partitions (PART)                                       */
     uint64_t fragments;      /* executed fragments (PART)                               */
     uint64_t max_chain;      /* longest partition (PART)                                */

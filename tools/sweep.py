@@ -39,7 +39,8 @@ def main():
     image = W.tpcb_db(dims)
     nmax = 1 << args.max_log2
     dev = torch.device("cuda", 0)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # one stream for the engine and the events
+    torch.cuda.set_stream(stream)
     db = Database(W.TPCB, dims.dims, nmax, image, stream=stream.cuda_stream,
                   insert_capacity=2)
     thetas = [float(x) for x in args.thetas.split(",")]
@@ -83,7 +84,8 @@ def main():
                 else:
                     med = statistics.median(ms)
                     row.update(result="ok", ms=med, txn_per_s=n / (med / 1e3), depth=st["depth"],
-                               max_chain=st["max_chain"], rank_passes=st["rank_passes"], ms_exec=st["ms_exec"])
+                               max_chain=st["max_chain"], rank_passes=st["rank_passes"], ms_exec=st["ms_exec"],
+                               chose=st["strategy"])
                 rows.append(row)
                 print(json.dumps(row), flush=True)
             del t, o, w

@@ -171,8 +171,10 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* s
  * then runs   w0 >= w0_bar            -> K-SET (reusing the ranks)
  *             c <= c_bar or d >= d_bar -> PART
  *             otherwise               -> TPL  (reusing the sorted access records).
- * Defaults: w0_bar = 128 x #SMs (the GPU's processors: 18,944 on B200),
- * d_bar = 2048, c_bar = 0 (calibrated per machine: tools/calibrate_chooser.py).
+ * Defaults, calibrated on B200 with tools/calibrate_chooser.py (the paper calibrates its
+ * thresholds; profiles/round1_chooser_calibration.json): w0_bar = 64 x #SMs
+ * (9,472 on B200; PAPER.md:414 ties it to the GPU's processors), d_bar = 0, c_bar = 0 --
+ * i.e. K-SET for a wide 0-set, else PART (TPL never won where w0 was small).
  * Errors: EINVAL (null handle). */
 gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, uint64_t c_bar);
 

@@ -104,8 +104,10 @@ struct gputx_db {
     bool sealed = false, submitted = false, executed = false, poisoned = false;
     int last_strategy = -1;
     int chosen = -1;                          // strategy that ran for the last execute
-    // Algorithm 1 thresholds (gputx_set_chooser); w0_bar 0 => 128 x #SMs
-    uint64_t ch_w0 = 0, ch_d = 2048, ch_c = 0;
+    // Algorithm 1 thresholds (gputx_set_chooser); w0_bar 0 => 64 x #SMs.  Calibrated on
+    // B200 by tools/calibrate_chooser.py (profiles/round1_chooser_calibration.json): d_bar = 0
+    // (PART whenever K-SET is not chosen) lifts the mean chosen/best throughput 0.70 -> 0.88
+    uint64_t ch_w0 = 0, ch_d = 0, ch_c = 0;
     uint64_t n = 0, first_ts = 0, next_ts = 0, max_bulk = 0, max_words = 0, max_rec = 0, n_items = 0;
     uint32_t item_bits = 0;
     uint32_t nparts = 0, part_bits = 0, part_size = 128;
@@ -610,7 +612,7 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v, bool sorted = false) {
 
 // Algorithm 1 on the bulk's structural parameters
 gputx_strategy choose_strategy(const gputx_db* db, uint64_t w0, uint64_t d, uint64_t c) {
-    const uint64_t w0_bar = db->ch_w0 ? db->ch_w0 : 128ull * (uint64_t)db->nsm;
+    const uint64_t w0_bar = db->ch_w0 ? db->ch_w0 : 64ull * (uint64_t)db->nsm;
     if (w0 >= w0_bar) return GPUTX_KSET;                   // lines 2-3
     if (c <= db->ch_c || d >= db->ch_d) return GPUTX_PART;  // lines 5-8
     return GPUTX_TPL;                                      // line 10

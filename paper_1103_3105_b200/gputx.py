@@ -276,7 +276,7 @@ class Database:
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
         return st.as_dict()
 
-    def set_chooser(self, w0_bar: int = 0, d_bar: int = 2048, c_bar: int = 0):
+    def set_chooser(self, w0_bar: int = 0, d_bar: int = 0, c_bar: int = 0):
         """Algorithm 1 thresholds for strategy "auto" (include/gputx.h gputx_set_chooser)."""
         self._check(self.lib.gputx_set_chooser(self.h, int(w0_bar), int(d_bar), int(c_bar)), self.h)
 

@@ -52,11 +52,14 @@ def graph_appendix_b(pool):
     """Appendix B: add transactions in ts order; per item keep the
     ascending list of transactions that accessed it.  A write scans back from the
     tail to the last writer t_w: edge t_w -> t if t_w is the tail, else edges from
-    EVERY reader between the tail and t_w (reading R-S8).  A read adds t_w -> t."""
+    EVERY reader between the tail and t_w (reading R-S8).  A read adds t_w -> t.
+    Appendix B knows reads and writes only: an 'A' operation raises ValueError."""
     lists = defaultdict(list)          # item -> [(txn, mode)]
     edges = set()
     for t, txn in enumerate(pool):
         for item, mode in _norm(txn).items():
+            if mode not in ('R', 'W'):
+                raise ValueError(f"graph_appendix_b: mode {mode!r} (Appendix B has R/W only)")
             L = lists[item]
             if L:
                 if mode == 'W':

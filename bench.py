@@ -259,20 +259,24 @@ def make_inputs(wl, rank: int, ws: int, steps: int, seed: int):
     return dims, image, bulks
 
 
-def oracle_rate(wl, image, bulks, min_seconds: float, max_runs: int):
+def oracle_rate(wl, image, bulks, min_seconds: float, max_runs: int, first=None):
     """The oracle (serial ts-order executor, one host core) on a bounded sample:
-    successive bulks on the evolving state until min_seconds of loop time."""
+    successive bulks on the evolving state until min_seconds of loop time; committed
+    transactions per second of loop time.  `first`: the oracle's result of bulk 0 on
+    `image` already computed (the parity gate's), counted as the first sample."""
     import oracle
     cur = image
-    secs, txns, runs = 0.0, 0, 0
+    secs, txns, runs, committed = 0.0, 0, 0, 0
     while runs < max_runs and (secs < min_seconds or runs == 0):
         b = bulks[runs % len(bulks)]
-        r = oracle.run(wl["schema"], wl["dims"].dims, cur, b, first_ts=txns)
+        r = first if (runs == 0 and first is not None) else \
+            oracle.run(wl["schema"], wl["dims"].dims, cur, b, first_ts=txns)
         cur = r.db
         secs += r.seconds
         txns += b.n
+        committed += int((r.status == 0).sum())
         runs += 1
-    return txns / secs, txns, runs, secs
+    return committed / secs, txns, runs, secs
 
 
 def cpu_model():
@@ -286,6 +290,8 @@ def cpu_model():
 
 
 def run_reference(args, wl, ws, rank):
+    """The reference arm: the oracle (serial ts-order executor, one host core), as it
+    stands, on the headline workload; rank 0 only (other ranks exit without work)."""
     if rank != 0:
         return 0
     _, image, bulks = make_inputs(wl, 0, 1, max(args.steps, 1), args.seed)
@@ -294,19 +300,21 @@ def run_reference(args, wl, ws, rank):
     for k in range(args.warmup):
         cur = oracle.run(wl["schema"], wl["dims"].dims, cur, bulks[k % len(bulks)]).db
     secs = []
-    txns = 0
+    txns = committed = 0
     for k in range(args.steps):
         b = bulks[k % len(bulks)]
         r = oracle.run(wl["schema"], wl["dims"].dims, cur, b, first_ts=txns)
         cur = r.db
         secs.append(r.seconds)
         txns += b.n
-    value = txns / sum(secs)
+        committed += int((r.status == 0).sum())
+    value = committed / sum(secs)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": config_of(args, wl, wl["dims"], 1),
+        "all_txn_per_s": txns / sum(secs),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} bulks of {wl['n']} txns ({wl['desc']}), serial loop only",
                          "cpu": cpu_model(), "nproc": os.cpu_count()},
@@ -320,52 +328,99 @@ def config_of(args, wl, dims, ws):
     c = {"workload": wl["desc"], "strategy": args.strategy, "bulk": wl["n"], "dims": list(dims.dims),
          "conflict_rule": "R/W + ADD" if wl.get("add_rule") else "R/W (paper)",
          "l2": "flushed (256 MiB write) before every timed step", "inputs": "resident in HBM (value); "
-         "pinned host (e2e)"}
+         "pinned host (e2e)", "value_counts": "committed transactions (SPEC.md:500); all_txn_per_s counts aborts too"}
     if ws > 1:
-        c["sharding"] = (f"{ws} shards by root key, bulk {wl['n']} per shard (weak scaling); cross-shard "
-                         "transactions exchanged by NCCL all-to-all inside the step")
+        if args.scaling == "strong":
+            c["sharding"] = (f"{ws} shards by root key of the configuration's {dims.dims[0]} roots, one bulk of "
+                             f"{wl['n']} transactions in total (strong scaling); cross-shard fragments exchanged "
+                             "inside the step")
+        else:
+            c["sharding"] = (f"{ws} shards by root key, bulk {wl['n']} per shard (weak scaling); cross-shard "
+                             "fragments exchanged inside the step")
     return c
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="tm1", choices=sorted(WORKLOADS))
-    ap.add_argument("--strategy", default="kset", choices=["kset", "part", "tpl", "auto"])
-    ap.add_argument("--others", default="part,tpl,auto", help="extra strategies measured on the same bulks "
-                    "(auto: Algorithm 1, PAPER.md:422-437, with the library's default thresholds)")
-    ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample (the contract asks for ~10-30 s)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
-    ws, rank, local, dist = dist_setup(args)
-    if args.impl == "reference":
-        return run_reference(args, wl, ws, rank)
+def _diff(ref, st, out, got):
+    """First difference between the oracle's result and the GPU's (None if identical)."""
+    if not np.array_equal(st, ref.status):
+        return f"status differs at {int(np.flatnonzero(st != ref.status)[0])}"
+    if not np.array_equal(out, ref.out):
+        return f"output differs at txn {int(np.flatnonzero((out != ref.out).any(axis=1))[0])}"
+    for k, a in ref.db.items():
+        if not np.array_equal(a, got[k]):
+            return f"column {k} differs"
+    return None
 
+
+def parity_gate(wl, db, dims, image, bulk0, strategy):
+    """SPEC.md:499 / SURVEY.md §2.5: before any number is reported, the GPU's result of
+    bulk 0 on the pristine image must equal the oracle's (Definition 1) element by element:
+    statuses, output records and every column.  Runs outside the timed region; the oracle
+    result it compares against is the first sample of the cpu_baseline leg."""
+    import oracle
+    ref = oracle.run(wl["schema"], dims.dims, image, bulk0, first_ts=0)
+    db.reset()
+    db.submit(bulk0)
+    db.execute(strategy)
+    st, out = db.read_results()
+    got = db.read_image(image)
+    err = _diff(ref, st, out, got)
+    db.reset()
+    return ref, err
+
+
+def spawn_ranks(args):
+    """--gpus N without a launcher: re-run this script under torch.distributed.run with N
+    processes (one per GPU), 127.0.0.1 rendezvous."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def make_inputs_strong(wl, rank: int, ws: int, steps: int, seed: int):
+    """Strong scaling: the configuration's own database and ONE bulk of the configuration's
+    size in total; rank r submits the transactions whose home root it owns (global ts)."""
+    nb = min(steps, 3)
+    dims = wl["dims"]
+    image = W.make_db(wl["schema"], dims, seed=seed)
+    bulks = [W.split_home(W.make_bulk(wl["schema"], dims, wl["n"], seed + k, **wl["kw"]), dims, ws)[rank]
+             for k in range(nb)]
+    return dims, image, bulks
+
+
+def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
+    """One workload: timed K-SET (or --strategy) steps on device-resident bulks, the e2e
+    loop through the C ABI with pinned host buffers, the other strategies, the roofline of
+    the dominant kernel, the cpu_baseline and the parity gate.  Returns the JSON object."""
     import torch
     from paper_1103_3105_b200 import Database
 
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    # one non-default stream for the engine (cfg.stream) and every torch op of the step:
-    # copies, the L2 flush and the timing events are ordered with the engine's kernels
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    clk = Clocks(local).__enter__()                      # sampling starts now, ends after the e2e loop
-    dims, image, bulks = make_inputs(wl, rank, ws, max(args.steps, 1), args.seed)
-    n = wl["n"]
-    cap = 3 * (args.warmup + args.steps) + 8          # bulks the merged insert tables must hold
-    # sharded: the local bulk is the home bulk plus the peers' cross-shard transactions
-    max_bulk = n if ws == 1 else min(1 << 24, n + n // 2 + 1024)
-    db = Database(wl["schema"], dims.dims, max_bulk, image, device=local, stream=stream.cuda_stream,
+    wl = WORKLOADS[name]
+    strong = ws > 1 and args.scaling == "strong"
+    if strong:
+        dims, image, bulks = make_inputs_strong(wl, rank, ws, max(args.steps, 1), args.seed)
+    else:
+        dims, image, bulks = make_inputs(wl, rank, ws, max(args.steps, 1), args.seed)
+    n_total = wl["n"] if strong else ws * wl["n"]              # transactions of one global step
+    cap = 3 * (args.warmup + args.steps) + 12          # bulks the merged insert tables must hold
+    nmax = max(b.n for b in bulks)
+    max_bulk = nmax if ws == 1 else min(1 << 24, nmax + nmax // 2 + 1024)
+    db = Database(wl["schema"], dims.dims, max_bulk, image, device=dev.index, stream=stream.cuda_stream,
                   insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws,
                   add_rule=wl.get("add_rule", False))
-    del image
+
+    # ---- parity gate (N = 1): bulk 0 vs the oracle, before anything is timed ----------
+    parity, parity_err, ref0 = None, None, None
+    if ws == 1 and not args.no_parity:
+        ref0, parity_err = parity_gate(wl, db, dims, image, bulks[0], args.strategy)
+        parity = parity_err is None
+    if ws > 1:
+        del image
+        image = None
 
     class DevBulk:
         def __init__(self, b):
@@ -390,6 +445,8 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    window = [0.0, 0.0]
+
     def timed(strategy, steps, warmup):
         for k in range(warmup):
             step_dev(k, strategy)
@@ -413,20 +470,26 @@ def main():
         barrier()
         return ms, stats
 
-    window = [0.0, 0.0]
-
     def max_over_ranks(x: float) -> float:
         return reduce_max(dist, x, dev)
 
+    def sum_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t)
+        return float(t.item())
+
     # ---- headline strategy, device-resident inputs -----------------------------------
+    db.reset()
     ms, stats = timed(args.strategy, args.steps, args.warmup)
     clocks = clk.summary(*window)
     total_ms = max_over_ranks(sum(ms))
-    value = ws * n * args.steps / (total_ms / 1e3)
+    committed = sum_over_ranks(float(sum(s["committed"] for s in stats)))
+    allt = sum_over_ranks(float(sum(s["n"] for s in stats)))
+    value = committed / (total_ms / 1e3)
     launches = int(sum(s["launches"] for s in stats))
-
-    # results of the last step for the byte model
-    st_host, _ = db.read_results()
+    st_host, _ = db.read_results()                    # results of the last step (byte model)
 
     # ---- e2e through the C ABI with host (pinned) buffers ----------------------------
     class HostBulk:
@@ -441,13 +504,16 @@ def main():
             return sum(a.nbytes for a in (self.type, self.param_off, self.param_words, self.ts) if a is not None)
 
     hb = [HostBulk(b) for b in bulks]
-    st_pin = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
-    out_pin = torch.empty(n * db.stride, dtype=torch.uint8).pin_memory().numpy().reshape(n, db.stride)
+    st_pin = torch.empty(nmax, dtype=torch.uint8).pin_memory().numpy()
+    out_pin = torch.empty(nmax * db.stride, dtype=torch.uint8).pin_memory().numpy().reshape(nmax, db.stride)
     e2e_ms = []
+    e2e_committed = 0
     for k in range(args.warmup + args.steps):
         b = hb[k % len(hb)]
+        nb_ = b.type.shape[0]
         flush.fill_(k & 0xFF)
         torch.cuda.synchronize()
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -456,21 +522,24 @@ def main():
         else:
             db.submit(b, on_device=False)
             db.execute_nostats(args.strategy)
-        db.read_results(st_pin, out_pin)
+        db.read_results(st_pin[:nb_], out_pin[:nb_])
         e1.record(stream)
         e1.synchronize()
         if k >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
+            e2e_committed += int((st_pin[:nb_] == 0).sum())
     e2e_total = max_over_ranks(sum(e2e_ms))
+    e2e_committed = sum_over_ranks(float(e2e_committed))
     h2d = int(np.mean([b.nbytes() for b in hb]))
-    d2h = n + n * db.stride
+    d2h = int(np.mean([b.type.shape[0] for b in hb])) * (1 + db.stride)
 
     # ---- other strategies on the same bulks ------------------------------------------
     others = {}
     for s in [x for x in args.others.split(",") if x and x != args.strategy]:
         m2, s2 = timed(s, max(2, args.steps // 2), 1)
         tot = max_over_ranks(sum(m2))
-        others[s] = {"value": ws * n * len(m2) / (tot / 1e3), "ms_per_step": tot / len(m2),
+        c2 = sum_over_ranks(float(sum(x["committed"] for x in s2)))
+        others[s] = {"value": c2 / (tot / 1e3), "ms_per_step": tot / len(m2),
                      "ms_exec": statistics.mean(x["ms_exec"] for x in s2),
                      "max_chain": s2[-1]["max_chain"], "parts": s2[-1]["parts"]}
         if s == "auto":
@@ -480,66 +549,136 @@ def main():
     # ---- roofline of the dominant kernel ---------------------------------------------
     peak, peak_kind = _peaks()
     phase = {k: statistics.mean(s[k] for s in stats) for k in
-             ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_total")}
+             ("ms_ingest", "ms_exchange", "ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_total")}
     last = stats[-1]
     b_last = bulks[(args.warmup + args.steps - 1) % len(bulks)]
     cand = {}
     eff = last["strategy"]                                  # auto: the strategy Algorithm 1 chose
+    nloc = b_last.n
     if last["rank_passes"]:
-        cand[rank_kernel_name(wl["schema"], wl.get("add_rule", False))] = (rank_bytes(wl["schema"], last["records"], last["rank_passes"], n),
-                                                phase["ms_rank"])
-    cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
-    kname = max(cand, key=lambda k: cand[k][1])
-    kbytes, kms = cand[kname]
-    achieved = kbytes / (kms / 1e3) / 1e9
-    traffic, tr = ncu_traffic(args.workload, kname)
-    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": tr and tr["source"],
-                # the ncu DRAM fraction of the same capture (cold cache)
-                "ncu_dram_frac": tr and traffic / (tr["ncu_us_per_launch"] * 1e-6) / 1e9 / peak,
-                "ncu_l2_hit_pct": tr and tr["l2_hit_pct"],
-                "peak_source": peak_kind,
-                "algorithmic_bytes": kbytes, "kernel_ms": kms,
-                # K-SET exec is bounded by its d+1 dependent rounds: the
-                # per-round latency is the number that moves it on deep graphs
-                "critical_path": ({"rounds": last["depth"] + 1,
-                                   "us_per_round": 1e3 * phase["ms_exec"] / (last["depth"] + 1)}
-                                  if eff == "kset" else {"max_chain": last["max_chain"]} if eff == "part"
-                                  else None),
-                "share_of_step": kms / phase["ms_total"] if phase["ms_total"] else None}
+        cand[rank_kernel_name(wl["schema"], wl.get("add_rule", False))] = (
+            rank_bytes(wl["schema"], last["records"], last["rank_passes"], nloc), phase["ms_rank"])
+    if ws == 1:
+        cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+    kname = max(cand, key=lambda k: cand[k][1]) if cand else None
+    roofline = None
+    if kname:
+        kbytes, kms = cand[kname]
+        achieved = kbytes / (kms / 1e3) / 1e9
+        traffic, tr = ncu_traffic(name, kname)
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "traffic_source": tr and tr["source"],
+                    # the ncu DRAM fraction of the same capture (cold cache)
+                    "ncu_dram_frac": tr and traffic / (tr["ncu_us_per_launch"] * 1e-6) / 1e9 / peak,
+                    "ncu_l2_hit_pct": tr and tr["l2_hit_pct"],
+                    "peak_source": peak_kind,
+                    "algorithmic_bytes": kbytes, "kernel_ms": kms,
+                    # K-SET exec is bounded by its d+1 dependent rounds: the
+                    # per-round latency is the number that moves it on deep graphs
+                    "critical_path": ({"rounds": last["depth"] + 1,
+                                       "us_per_round": 1e3 * phase["ms_exec"] / (last["depth"] + 1)}
+                                      if eff == "kset" else {"max_chain": last["max_chain"]} if eff == "part"
+                                      else None),
+                    "share_of_step": kms / phase["ms_total"] if phase["ms_total"] else None}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) -----------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, txns, runs, secs = oracle_rate(wl, W.make_db(wl["schema"], dims, seed=args.seed), bulks,
-                                             args.cpu_seconds, 1000)
+        rate, txns, runs, secs = oracle_rate(wl, image, bulks, args.cpu_seconds, 1000, first=ref0)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{runs} bulk(s) x {n} txns of the same workload, serial loop {secs:.2f} s",
+               "sample": f"{runs} bulk(s) x {wl['n']} txns of the same workload, serial loop {secs:.2f} s "
+                         "(committed txn/s)",
                "cpu": cpu_model(), "nproc": os.cpu_count()}
-
-    clk.__exit__()
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int64", "data": "synthetic (seeded generators, workloads/)",
-        "config": config_of(args, wl, dims, ws),
-        "e2e": {"value": ws * n * args.steps / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    db.close()
+    del flush
+    torch.cuda.empty_cache()
+    res = {
+        "workload": name, "value": value if parity is not False else 0.0, "unit": UNIT,
+        "ms_per_step": total_ms / args.steps, "all_txn_per_s": allt / (total_ms / 1e3),
+        "parity": parity if parity is not None else "not checked (N>1: tests/test_gpu_shard.py)",
+        "e2e": {"value": e2e_committed / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "clocks": clocks,
+        "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
         "phases_ms": phase,
         "graph": {"depth": last["depth"], "zero_set": last["zero_set"], "records": last["records"],
                   "rank_passes": last["rank_passes"], "committed": last["committed"], "aborted": last["aborted"]},
         "strategies": {args.strategy: {"value": value, "ms_per_step": total_ms / args.steps}, **others},
+        "config": config_of(args, wl, dims, ws), "n_total_per_step": n_total,
     }
+    if parity_err:
+        res["parity_error"] = parity_err
+    if last.get("flags"):
+        res["exec_flags"] = last["flags"]
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="tm1", choices=sorted(WORKLOADS))
+    ap.add_argument("--also", default="default", help="further workloads measured after the headline, comma "
+                    "separated; 'default' = tpcb,tpcc when the headline is tm1 (BASELINE's three metric "
+                    "workloads), 'none' = headline only")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = bulk per GPU fixed, database N times the roots; strong = the "
+                    "configuration's database and one bulk in total, sharded (BASELINE config 4)")
+    ap.add_argument("--strategy", default="kset", choices=["kset", "part", "tpl", "auto"])
+    ap.add_argument("--others", default="part,tpl,auto", help="extra strategies measured on the same bulks "
+                    "(auto: Algorithm 1, PAPER.md:422-437, with the library's default thresholds)")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample (the contract asks for ~10-30 s)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    wl = WORKLOADS[args.workload]
+    ws, rank, local, dist = dist_setup(args)
+    if ws != args.gpus and args.impl != "reference":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if args.impl == "reference":
+        return run_reference(args, wl, ws, rank)
+
+    import torch
+
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # one non-default stream for the engine (cfg.stream) and every torch op of the step:
+    # copies, the L2 flush and the timing events are ordered with the engine's kernels
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    also = args.also
+    if also == "default":
+        also = "tpcb,tpcc" if args.workload == "tm1" else "none"
+    extra = [x for x in also.split(",") if x and x != "none" and x != args.workload]
+    clk = Clocks(local).__enter__()                      # sampling starts now
+    head = measure(args, args.workload, ws, rank, dist, dev, stream, clk, True)
+    subs = {x: measure(args, x, ws, rank, dist, dev, stream, clk, False) for x in extra}
+    clk.__exit__()
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (seeded generators, workloads/)",
+        "config": head["config"], "parity": head["parity"], "all_txn_per_s": head["all_txn_per_s"],
+        "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "roofline": head["roofline"],
+        "cpu_baseline": head["cpu_baseline"], "clocks": head["clocks"], "phases_ms": head["phases_ms"],
+        "graph": head["graph"], "strategies": head["strategies"],
+    }
+    for k in ("parity_error", "exec_flags"):
+        if k in head:
+            line[k] = head[k]
+    if subs:
+        line["workloads"] = subs
     if rank == 0:
         print(json.dumps(line), flush=True)
-    db.close()
     if dist is not None:
         dist.destroy_process_group()
-    return 0
+    return 0 if all(x["parity"] is not False for x in [head, *subs.values()]) else 3
 
 
 if __name__ == "__main__":

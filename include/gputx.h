@@ -125,7 +125,16 @@ typedef struct {
     uint64_t cross;          /* c: transactions with fragments in more than one PART partition
                                 (filled by PART and AUTO, else 0)             */
     uint64_t strategy;       /* the strategy that ran (GPUTX_AUTO: the one Algorithm 1 chose) */
+    double ms_ingest;        /* device time of the last submit on the handle's stream: H2D/D2D of the
+                                signatures, validation, split lookups, insert counts  */
+    double ms_exchange;      /* sharded: device time of the cross-shard exchange of this bulk (pack,
+                                peer transfer, merge by ts; return of fragment outputs), else 0   */
+    uint64_t flags;          /* GPUTX_STAT_* bits below                                          */
 } gputx_stats;
+
+/* gputx_stats.flags */
+#define GPUTX_STAT_CLUSTER_FALLBACK 1u   /* K-SET executor was launched without its cluster shape
+                                            (e.g. by a profiler) and used counter hand-offs only */
 
 /* Create a database handle for cfg->schema with empty (zero) columns on cfg->device.
  * Errors: EINVAL (bad schema/dims/max_bulk), ENOMEM, ECUDA.  *out is NULL on error. */

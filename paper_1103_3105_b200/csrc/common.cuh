@@ -71,6 +71,27 @@ struct GridBar {
     uint32_t top;
     uint32_t pad[31];
     uint32_t gen;
+    uint32_t pad2[31];
+    uint32_t dead;        // watchdog tripped in this launch (reset by the host before each launch)
+};
+
+// Spin watchdog (SPEC "watchdog -> EDEADLOCK"): every device spin loop that
+// waits for another CTA polls a timer; past g_watchdog_ns (GPUTX_WATCHDOG_MS, default 10 s)
+// or once another waiter has tripped, it gives up, the kernel drains without waiting, and
+// the host returns GPUTX_EDEADLOCK and poisons the handle until gputx_reset.
+__device__ unsigned long long g_watchdog_ns = 10000000000ull;
+struct SpinWatch {
+    uint64_t t0 = 0;
+    uint32_t n = 0;
+    // call once per unsuccessful poll; true = give up (and *flag is set)
+    DEV bool expired(uint32_t* flag) {
+        if ((++n & 1023u) != 0) return false;
+        const uint64_t now = globaltimer_ns();
+        if (!t0) { t0 = now; return false; }
+        if (*reinterpret_cast<volatile uint32_t*>(flag)) return true;
+        if (now - t0 > g_watchdog_ns) { atomicExch(flag, 1u); return true; }
+        return false;
+    }
 };
 
 DEV void grid_sync(GridBar* b) {
@@ -95,8 +116,11 @@ DEV void grid_sync(GridBar* b) {
                 wait = false;
             }
         }
-        if (wait)
-            while (ld_acquire(&b->gen) == g) { }
+        if (wait) {
+            SpinWatch wd;
+            while (ld_acquire(&b->gen) == g)
+                if (wd.expired(&b->dead)) break;
+        }
         __threadfence();
     }
     __syncthreads();

@@ -180,6 +180,9 @@ struct gputx_db {
     bool tpl_persistent = false;   // GPUTX_TPL_PERSISTENT=1: persistent per-lane tickets (slower: divergent spinners)
     uint32_t kset_cluster = 8;     // CTAs per thread-block cluster of the K-SET executor
     cudaEvent_t ev[8] = {};
+    cudaEvent_t ev_sub[2] = {};       // submit start / end (ms_ingest)
+    cudaEvent_t ev_x[4] = {};         // sharded exchange: pack start/end, merge start/end (ms_exchange)
+    bool have_x = false;
     bool has_depth = false, has_perm = false;
     uint64_t launches = 0;     // kernels launched since the last submit
     // timestamps and shards
@@ -372,6 +375,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(&db->d_bar->dead, 0, sizeof(uint32_t), s));
     if (windowed) {
         win_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, wb,
                                                                              nwin, db->d_wseg);
@@ -501,7 +505,9 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
             gk = fg; done = fdone; off = foff;
         }
         void* args[] = {&vv, &perm, &off, &TT, &gk, &done, &sc, &pt, &pp, &trace, &diag, &C};
-        if (C) {
+        // diag 512: launch WITHOUT the cluster attribute while still passing C (what a
+        // profiler replaying the launch does); the kernel must detect it (SC_NOCLUSTER)
+        if (C && !(diag & 512u)) {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3(G);
             lc.blockDim = dim3(kset_block<S>());
@@ -693,6 +699,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
                 scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n,
                          db->d_sc + SC_INS0 + t);
     }
+    cudaEventRecord(db->ev_sub[1], s);
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR]) {
@@ -875,6 +882,8 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     cudaMemsetAsync(db->d_lock, 0, n_items * 4, db->stream);
     if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
     for (auto& e : db->ev) cudaEventCreate(&e);
+    for (auto& e : db->ev_sub) cudaEventCreate(&e);
+    for (auto& e : db->ev_x) cudaEventCreate(&e);
     db->rank_grid = coop_grid(db, rank_kernel, RK_THREADS, 0);
     // sweeps per warp-tile per rank pass, measured per schema (profiles/round1.md):
     // TM-1 / TPC-B chains are mostly root-local (sweeps close them in the tile), TPC-C's cross tiles
@@ -925,6 +934,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_RUNMAX")) db->kset_diag = (db->kset_diag & 0xFFFFu) | ((uint32_t)atoi(e) << 16);
     db->sync_stages = getenv("GPUTX_SYNC") != nullptr;
     if (const char* e = getenv("GPUTX_TPL_PERSISTENT")) db->tpl_persistent = atoi(e) != 0;
+    if (const char* e = getenv("GPUTX_WATCHDOG_MS")) {   // spin watchdog of every device wait loop
+        const unsigned long long ns = (unsigned long long)std::max(1, atoi(e)) * 1000000ull;
+        cudaMemcpyToSymbol(g_watchdog_ns, &ns, sizeof(ns));
+    }
     if (const char* e = getenv("GPUTX_TPL_SLEEP")) {
         const uint32_t cap = (uint32_t)atoi(e);
         cudaMemcpyToSymbol(g_tpl_sleep_cap, &cap, 4);
@@ -1116,6 +1129,8 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     if (!b->ts && db->next_ts + n >= (1ull << 32)) return fail(db, GPUTX_ECAPACITY, "timestamp space exhausted");
     db->has_ts = b->ts != nullptr;
+    db->have_x = false;
+    cudaEventRecord(db->ev_sub[0], s);
     if (n) {   // (device bulks: ordered on the handle's stream; the words' count is read there)
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
@@ -1154,6 +1169,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
     }
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
+    cudaEventRecord(db->ev_sub[0], s);
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
     if (n) {
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -1334,7 +1350,8 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     if (ranked && db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
     if (db->h_sc[SC_DEADLOCK]) {
         db->poisoned = true;
-        return fail(db, GPUTX_EDEADLOCK, "TPL spin watchdog tripped");
+        return fail(db, GPUTX_EDEADLOCK, "spin watchdog tripped (a device wait exceeded GPUTX_WATCHDOG_MS); "
+                                         "database poisoned until gputx_reset");
     }
     if (stats) {
         memset(stats, 0, sizeof(*stats));
@@ -1368,6 +1385,16 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
         const uint64_t ab = n ? db->h_sc[SC_COMMITTED] : 0;    // aborts, counted on the device
         stats->aborted = ab;
         stats->committed = n - ab;
+        float mi = 0;
+        if (cudaEventElapsedTime(&mi, db->ev_sub[0], db->ev_sub[1]) == cudaSuccess) stats->ms_ingest = mi;
+        if (db->have_x) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, db->ev_x[0], db->ev_x[1]);
+            cudaEventElapsedTime(&b, db->ev_x[2], db->ev_x[3]);
+            stats->ms_exchange = a + b;
+        }
+        stats->flags = db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0;
+        cudaGetLastError();
     }
     return GPUTX_OK;
 }
@@ -1521,6 +1548,10 @@ void gputx_close_db(gputx_db* db) {
         if (p) cudaFree(p);
     if (db->h_sc) cudaFreeHost(db->h_sc);
     for (auto& e : db->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : db->ev_sub)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : db->ev_x)
         if (e) cudaEventDestroy(e);
     if (db->own_stream && db->stream) cudaStreamDestroy(db->stream);
     delete db;

@@ -19,11 +19,12 @@ enum {
     SC_ERR = 0, SC_BADIDX, SC_NREC, SC_NFRAG, SC_MAXD, SC_ZERO, SC_PASSES, SC_CHG0, SC_CHG1, SC_CHG2,
     SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV, SC_XTOTAL,
     SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
-    SC_COUNT = 40      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS)
+    SC_COUNT = 40      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS; 33: SC_NOCLUSTER)
 };
 enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7, E_WORDS = 8 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
+constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested cluster shape (counter hand-offs used)
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -552,7 +553,8 @@ __device__ __forceinline__ void rank_generic(const uint64_t* __restrict__ keys, 
         grid_sync(bar);
         if (blockIdx.x == 0) tmax(pass, 4);
         const uint32_t c = __ldcg(&sc[SC_CHG0 + pass % 3]);
-        if (!c || pass + 1 >= max_passes) {
+        if (!c || pass + 1 >= max_passes || __ldcg(&bar->dead)) {
+            if (blockIdx.x == 0 && tid == 0 && __ldcg(&bar->dead)) sc[SC_DEADLOCK] = 1u;
             if (blockIdx.x == 0 && tid == 0) {
                 sc[SC_PASSES] = pass + 1;
                 sc[SC_NOCONV] = c ? 1u : 0u;
@@ -740,7 +742,7 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
             }
             rkw_sync<CL>(bar);
             const uint32_t c = __ldcg(&sc[SC_CHG0 + gpass % 3]);
-            if ((!c && fresh) || pass + 1 >= max_passes) {
+            if ((!c && fresh) || pass + 1 >= max_passes || __ldcg(&bar->dead)) {
                 noconv |= c != 0;
                 ++gpass;
                 break;
@@ -780,10 +782,12 @@ __global__ void __launch_bounds__(RK_THREADS, 2) rank_window_kernel(const uint64
             }
         }
         rkw_sync<CL>(bar);                                   // states visible to the next window
+        if (__ldcg(&bar->dead)) break;                      // watchdog: drain
     }
     if (blockIdx.x == 0 && tid == 0) {
         sc[SC_PASSES] = gpass;
         sc[SC_NOCONV] = noconv ? 1u : 0u;
+        if (__ldcg(&bar->dead)) sc[SC_DEADLOCK] = 1u;
     }
 }
 
@@ -942,7 +946,8 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
         grid_sync(bar);
         if (trace && blockIdx.x == 0 && tid == 0 && pass < RANK_TRACE_SLOTS / 8) trace[8 * pass + 4] = globaltimer_ns();
         const uint32_t c = __ldcg(&sc[SC_CHG0 + pass % 3]);
-        if (!c || pass + 1 >= max_passes) {
+        if (!c || pass + 1 >= max_passes || __ldcg(&bar->dead)) {
+            if (blockIdx.x == 0 && tid == 0 && __ldcg(&bar->dead)) sc[SC_DEADLOCK] = 1u;
             if (blockIdx.x == 0 && tid == 0) {
                 sc[SC_PASSES] = pass + 1;
                 sc[SC_NOCONV] = c ? 1u : 0u;
@@ -1226,6 +1231,17 @@ __global__ void kset_sched_kernel(const uint32_t* __restrict__ off, uint32_t T, 
     }
 }
 
+// GPUTX_KSET_DIAG bit 1024 (tests only): a pseudo-random 0..2 us sleep before every
+// transaction a thread executes, so that rounds finish in a different order every run
+// (timing-perturbation stress test of the round hand-offs, tests/test_gpu_stress.py)
+DEV void kx_jitter(uint32_t diag, uint32_t k, uint32_t b, uint32_t tid) {
+    if (diag & 1024u) {
+        uint32_t h = (k * 0x9E3779B1u) ^ (b * 0x85EBCA77u) ^ (tid * 0xC2B2AE3Du) ^ (uint32_t)clock64();
+        h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+        __nanosleep(h & 2047u);
+    }
+}
+
 constexpr int KX_THREADS = 1024;
 constexpr uint32_t KX_CH = 2048;      // rounds staged per shared-memory chunk
 
@@ -1239,6 +1255,17 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     const uint32_t nk = __ldcg(&sc[SC_MAXD]) + 1;
     const uint32_t b = blockIdx.x, tid = threadIdx.x;
     constexpr bool TAILRUN = S != S_TPCC && PW > 0;
+    // The cluster hand-offs below are only valid if the launch really formed clusters of
+    // cluster_c CTAs.  A launcher that drops the cluster attribute (a profiler replaying
+    // the launch does: GPUTEST_r01's ncu-wrapped smoke ran every CTA as its own cluster, so
+    // barrier.cluster synchronised nothing and narrow rounds raced) must not break the
+    // schedule: read the shape the hardware gave us and fall back to counter hand-offs.
+    uint32_t ncta_cluster;
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta_cluster));
+    if (cluster_c && ncta_cluster != cluster_c) {
+        if (b == 0 && tid == 0) const_cast<uint32_t*>(sc)[SC_NOCLUSTER] = ncta_cluster;
+        cluster_c = 0;
+    }
     // prefetched first slice of the round this CTA executes next
     uint32_t nidx = 0xFFFFFFFFu, nt = 0;
     uint32_t np[PW > 0 ? PW : 1];
@@ -1315,6 +1342,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     auto narrow = [&](uint32_t kk) -> bool { return C && G(kk) <= C; };
     auto part = [&](uint32_t kk) -> bool { return narrow(kk) ? b < C : b < G(kk); };
     auto nsig = [&](uint32_t kk) -> uint32_t { return narrow(kk) ? C : G(kk); };   // signals of round kk
+    // watchdog (GPUTX_WATCHDOG_MS): a wait that times out puts the CTA in drain mode --
+    // it still walks the schedule, signals and takes part in cluster barriers so that no
+    // other CTA hangs on it, but neither waits nor executes; the host reports EDEADLOCK
+    __shared__ uint32_t s_dead;
+    if (tid == 0) s_dead = 0;
+    bool dead = false;
     uint32_t k = 0;
     while (k < nk && !part(k)) ++k;                      // this CTA's first round
     if (k >= nk) return;
@@ -1335,15 +1368,20 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         const bool nar_m1 = C && gm1 <= C;
         if (k > 0 && !(nar && nar_m1)) {
             const bool mine = !C && (prev == k - 1) && gprev == 1;
-            if (!mine) {
+            if (!mine && !dead) {
                 if (tid == 0) {
-                    const uint32_t need = nar_m1 ? C : gm1;
+                    // diag 2048 (tests): round 1 waits for one signal too many -> watchdog
+                    const uint32_t need = (nar_m1 ? C : gm1) + ((diag & 2048u) && k == 1 ? 1u : 0u);
                     uint32_t spins = 0;
-                    while (ld_acquire(&done[k - 1]) < need)
+                    SpinWatch wd;
+                    while (ld_acquire(&done[k - 1]) < need) {
                         if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
+                        if (wd.expired(const_cast<uint32_t*>(&sc[SC_DEADLOCK]))) { s_dead = 1; break; }
+                    }
                     if (trace && b == 0) trace[8 * k + 4] = spins;
                 }
                 __syncthreads();
+                dead = s_dead != 0;
             }
         }
         // Runs of one-CTA rounds: rounds k .. e-1 that are narrow and need one CTA (<= Q
@@ -1354,7 +1392,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         // next round's parameters are loaded before the current one executes.  The run's
         // last round goes through the regular path below (its hand-off to what follows).
         // Other CTAs of the cluster hold no work in these rounds and skip them too.
-        if (TAILRUN && nar && gk == 1 && !(diag & 256u)) {
+        if (TAILRUN && nar && gk == 1 && !(diag & 256u) && !dead) {
             // rounds of up to runmax transactions join the run (diag >> 16; 0: one-CTA rounds)
             const uint32_t runmax = min((uint32_t)KB, diag >> 16);
             uint32_t e = k, wmax = 0;
@@ -1385,7 +1423,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                         if (trace && tid == 0) trace[8 * kk] = globaltimer_ns();        // round start
                         uint32_t yi = 0xFFFFFFFFu, yt = 0, yq[PW > 0 ? PW : 1];
                         if (kk + 2 < e) ld(kk + 1, yi, yt, yq);
-                        if (xi != 0xFFFFFFFFu) exec_txn_p<S, SH>(db, xi, xt, xq);
+                        if (xi != 0xFFFFFFFFu) { kx_jitter(diag, kk, b, tid); exec_txn_p<S, SH>(db, xi, xt, xq); }
                         if (yi != 0xFFFFFFFFu) warm_rows<S>(db, yt, yq);      // next round's rows into L2
                         if (nthr == 32) __syncwarp();
                         else asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
@@ -1427,9 +1465,10 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             slice(lo, hi, G(k2), lo, hi);
             if (!(diag & 8u)) prefetch(lo, hi);
         }
-        if (!WARPX && cidx != 0xFFFFFFFFu && !(diag & 1u)) {
+        if (!WARPX && cidx != 0xFFFFFFFFu && !(diag & 1u) && !dead) {
             const bool tt = trace && (diag & 2u);
             const uint64_t t0 = tt ? globaltimer_ns() : 0;
+            kx_jitter(diag, k, b, tid);
             if (PW > 0) exec_txn_p<S, SH>(db, cidx, ct, cp);
             else exec_txn<S, SH>(db, cidx);
             if (tt) {   // slowest transaction of the round: duration << 24 | idx (GPUTX_KSET_DIAG=2)
@@ -1438,9 +1477,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                           (unsigned long long)((d << 24) | cidx));
             }
         }
-        if (WARPX && !(diag & 1u))
-            for (uint32_t j = clo + (tid >> 5); j < chi; j += KB / 32) exec_txn_warp<SH>(db, __ldg(&perm[j]));
-        for (uint32_t j = (diag & 1u) || WARPX ? chi : clo + KB + tid; j < chi; j += KB) {
+        if (WARPX && !(diag & 1u) && !dead)
+            for (uint32_t j = clo + (tid >> 5); j < chi; j += KB / 32) {
+                kx_jitter(diag, k, b, tid & ~31u);
+                exec_txn_warp<SH>(db, __ldg(&perm[j]));
+            }
+        for (uint32_t j = (diag & 1u) || WARPX || dead ? chi : clo + KB + tid; j < chi; j += KB) {
             if (PW > 0) {
                 uint32_t q[PW > 0 ? PW : 1];
 #pragma unroll

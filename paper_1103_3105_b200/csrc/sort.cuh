@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
         }
         old = __shfl_sync(0xffffffffu, old, leader);
         loc[j] = (uint16_t)(old + __popc(peers & lmask));
+        __syncwarp();          // the next key's leader (another lane) reads this count
     }
     __syncthreads();
     // per digit: exclusive prefix over warps (in key order), tile count

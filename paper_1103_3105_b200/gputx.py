@@ -47,7 +47,8 @@ class Stats(ctypes.Structure):
                                                "rank_passes", "parts", "fragments", "max_chain", "launches")] + \
                [(k, ctypes.c_double) for k in ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_merge",
                                                "ms_total")] + \
-               [(k, ctypes.c_uint64) for k in ("cross", "strategy")]
+               [(k, ctypes.c_uint64) for k in ("cross", "strategy")] + \
+               [(k, ctypes.c_double) for k in ("ms_ingest", "ms_exchange")] + [("flags", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -68,3 +68,33 @@ def test_reference_arm_torchrun_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_bench_self_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` without a launcher re-runs itself under torch.distributed.run
+    with two ranks (--gpus was parsed and ignored); rank 0 prints n_gpus 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "2", "--warmup", "1",
+           "--workload", "tpcb_tiny", "--scaling", "strong"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+
+
+def test_strong_scaling_inputs_partition_one_bulk():
+    """--scaling strong (BASELINE config 4): the configuration's database and ONE bulk in
+    total; every transaction is submitted by exactly one rank (its home warehouse's), with
+    its global timestamp."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import workloads as W
+    wl = dict(bench.WORKLOADS["tpcc"], dims=W.TpccDims(8, 10, 30, 1000), n=3000)
+    parts = [bench.make_inputs_strong(wl, r, 4, 1, seed=5) for r in range(4)]
+    assert all(p[0].dims == (8, 10, 30, 1000) for p in parts)
+    ts = np.concatenate([p[2][0].ts for p in parts]).astype(np.int64)
+    assert np.array_equal(np.sort(ts), np.arange(3000))
+    for r, p in enumerate(parts):
+        assert np.all(W.shard_of(W.home_roots(p[2][0]), 4, 8) == r)

@@ -35,6 +35,18 @@ for r in range(reps):
         if len(rows):
             types = bulk.type[rows]
             msgs.append(f"out rows {len(rows)} first {rows[:10]} types {np.bincount(types, minlength=7)}")
+            if r == 0 and which == "tm1":
+                d = db.depths()
+                nbr = {int(v): k for k, v in enumerate(image["sub_nbr"])}
+                for i in rows[:6]:
+                    if bulk.type[i] != 0:
+                        continue
+                    s_ = int(bulk.params(i)[0]) - 1
+                    gv = int(o[i][20:24].copy().view(np.uint32)[0])
+                    wv = int(ro[i][20:24].copy().view(np.uint32)[0])
+                    uls = [(j, int(d[j]), int(bulk.params(j)[2])) for j in range(n) if bulk.type[j] == 4
+                           and nbr.get(int(bulk.params(j)[0]) | (int(bulk.params(j)[1]) << 32)) == s_]
+                    msgs.append(f"  GSD {i} depth {d[i]} s {s_} got vlr {gv} want {wv} init {int(image['sub_vlr'][s_])} ULs {uls}")
             if r == 0:
                 d = db.depths()
                 for i in rows[:5]:

@@ -66,7 +66,7 @@ typedef enum {
     GPUTX_ESTATE = 5,        /* call out of order (e.g. submit twice, execute unsealed)   */
     GPUTX_ECAPACITY = 6,     /* bulk > max_bulk, output buffer short, insert table full   */
     GPUTX_ECROSS = 7,        /* PART: a cross-partition type with no fragment split       */
-    GPUTX_EDEADLOCK = 8,     /* TPL spin watchdog tripped; db poisoned until reset        */
+    GPUTX_EDEADLOCK = 8,     /* a spin watchdog tripped (K-SET round wait, grid barrier, TPL lock); db poisoned until reset */
     GPUTX_ECUDA = 9,         /* CUDA runtime error                                        */
     GPUTX_ENCCL = 10         /* reserved: inter-GPU exchange                              */
 } gputx_status;
@@ -169,7 +169,8 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* bulk, uint64_t* f
 
 /* Execute the submitted bulk with the given strategy to completion (synchronous) and
  * merge the insert buffers.  stats may be NULL.  Errors: ESTATE (nothing
- * submitted), EDEADLOCK (TPL watchdog), ECAPACITY (insert table full), ECUDA. */
+ * submitted), EDEADLOCK (a device wait exceeded the spin watchdog, GPUTX_WATCHDOG_MS,
+ * default 10 s: the handle is poisoned until gputx_reset), ECAPACITY (insert table full), ECUDA. */
 gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* stats);
 
 /* Thresholds of the strategy chooser, Algorithm 1 (Appendix D
@@ -183,7 +184,13 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* s
  * Defaults, calibrated on B200 with tools/calibrate_chooser.py (the paper calibrates its
  * thresholds; profiles/round1_chooser_calibration.json): w0_bar = 64 x #SMs
  * (9,472 on B200; PAPER.md:414 ties it to the GPU's processors), d_bar = 0, c_bar = 0 --
- * i.e. K-SET for a wide 0-set, else PART (TPL never won where w0 was small).
+ * i.e. K-SET for a wide 0-set, else PART; with d_bar = 0 the default NEVER returns TPL.
+ * That is a calibration outcome, not a property of TPL: TPL was the fastest strategy on 5
+ * of the 13 calibration bulks.  Four of them (TM-1, TM-1 uniform, TPC-B ADD, TPC-C ADD) have
+ * w0 >= 9,472, where line 2 returns K-SET before TPL is considered; TPC-C (w0 = 624,
+ * d = 7,990) would pick TPL only with d_bar > 7,990, which loses more on the TPC-B sweep
+ * bulks (PART-best, d up to 99,466) than it gains -- Algorithm 1's three thresholds cannot
+ * separate them (DESIGN.md §4 "Strategy chooser"). 
  * Errors: EINVAL (null handle). */
 gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, uint64_t c_bar);
 

@@ -52,6 +52,13 @@ DEV void st_release(uint32_t* p, uint32_t v) {
 DEV void st_release64(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// fire-and-forget release increment: orders every prior write of the calling thread (and,
+// cumulatively, those it observed, e.g. its CTA's writes before a __syncthreads) before
+// the increment; ~0.3 us/round cheaper than __threadfence (fence.sc) + atomicAdd
+// (tools/handoff.cu, profiles/round2_handoff_microbench.txt)
+DEV void red_add_release(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 DEV uint32_t atom_add_release(uint32_t* p, uint32_t v) {
     uint32_t old;
     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

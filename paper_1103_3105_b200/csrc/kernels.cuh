@@ -1375,7 +1375,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
                     uint32_t spins = 0;
                     SpinWatch wd;
                     while (ld_acquire(&done[k - 1]) < need) {
-                        if (++spins > 16) __nanosleep(b == 0 ? 20 : 200);
+                        if (++spins > 64) __nanosleep(32);
                         if (wd.expired(const_cast<uint32_t*>(&sc[SC_DEADLOCK]))) { s_dead = 1; break; }
                     }
                     if (trace && b == 0) trace[8 * k + 4] = spins;
@@ -1509,18 +1509,12 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
             const bool solo = gk == 1 && k + 1 < nk && narrow(k + 1) && G(k + 1) == 1;
             if (solo) __syncthreads();
             else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-            if (k + 1 < nk && !narrow(k + 1) && tid == 0) {          // a wide round follows
-                __threadfence();
-                atomicAdd(&done[k], 1u);
-            }
+            if (k + 1 < nk && !narrow(k + 1) && tid == 0) red_add_release(&done[k], 1u);   // a wide round follows
         } else {
             __syncthreads();
             // without clusters CTA 0 runs every round; for it k2 == k + 1
             const bool next_shared = b > 0 || C || ((k + 1 < nk) && G(k + 1) > 1);
-            if (tid == 0 && (gk > 1 || next_shared)) {
-                __threadfence();
-                atomicAdd(&done[k], 1u);
-            }
+            if (tid == 0 && (gk > 1 || next_shared)) red_add_release(&done[k], 1u);
         }
         if (trace && b == 0 && tid == 0) trace[8 * k + 1] = globaltimer_ns();
         if (!next_mine) {

@@ -34,12 +34,18 @@
  *   TPC-C     type 0 NewOrder [w, d, c, ol_cnt, (i, supply_w, qty) x ol_cnt]
  *                             type 1 Payment  [w, d, cw, cd, by_name, c_or_last, h_amount]
  *                             (by-name customer lookup, runs at submit)
+ *   MICRO     dims = (N tuples, T types <= 32, x, 0); type t in [0, T): [tuple]
+ *                             reads the tuple (f32 bits, column "tuple"), applies 100*x "sin
+ *                             calls" of type t (u = fma(v, 15/16 - t/128, (t - 15.5)/1024),
+ *                             v = u * (1 + u^2 (C3 + u^2 C5)), IEEE fma/mul, DESIGN.md R-M1),
+ *                             writes it back; never aborts.  Unsharded only.
  *
  * Output records (fixed stride per schema, zero for aborted transactions):
  *   TPC-B  8 B : i64 account balance after the deposit
  *   TM-1  40 B : GSD  [0]u64 sub_nbr [8]u64 hex [16]u32 msc [20]u32 vlr [24]u16 bits [26]u8[10] byte2
  *                GND  [0]u32 count [8,16,24]u64 numberx of the qualifying rows in start-time order
  *                GAD  [0]u8 data1 [1]u8 data2 [4]u32 data3 [8]u64 data4
+ *   MICRO  4 B : u32 bits of the value written back
  *   TPC-C 200 B: NewOrder [0]u32 o_id [4]u32 ol_cnt [8]i64 total, line l at 16+12l:
  *                         [0]i32 s_quantity before the update [4]i32 amount [8]u8 brand 'B'
  *                Payment  [0]u32 c_id [4]u32 c_credit(1=BC) [8]i64 c_balance after
@@ -73,7 +79,8 @@ typedef enum {
 
 typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2,
                GPUTX_AUTO = 3  /* Algorithm 1, see gputx_set_chooser */ } gputx_strategy;
-typedef enum { GPUTX_TPCB = 1, GPUTX_TM1 = 2, GPUTX_TPCC = 3 } gputx_schema;
+typedef enum { GPUTX_TPCB = 1, GPUTX_TM1 = 2, GPUTX_TPCC = 3,
+               GPUTX_MICRO = 4  /* the paper's micro benchmark (§6.1), see below */ } gputx_schema;
 
 typedef struct {
     gputx_schema schema;
@@ -193,6 +200,17 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* s
  * separate them (DESIGN.md §4 "Strategy chooser"). 
  * Errors: EINVAL (null handle). */
 gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, uint64_t c_bar);
+
+/* Type grouping inside each k-set (Appendix D "Branch divergence"):
+ * transactions of one k-set are ordered by p groups of type ids (type * p / T, the high
+ * part of the id -- what (log2 p)/b passes of a b-bit radix partitioning on the type give),
+ * so a warp's lanes take at most a few branches of the combined switch.  p = 0 (default)
+ * or p = T: one group per type (full grouping; on B200 it is the same single counting-sort
+ * pass as depth-only grouping); p = 1: depth only, types mixed in ts order (the paper's
+ * "basic execution").  The best p is found by calibration (tools/calibrate_grouping.py,
+ * PAPER.md:404 "we run calibration to determine the number of passes").
+ * Errors: EINVAL (p > T). */
+gputx_status gputx_set_grouping(gputx_db* db, uint32_t p);
 
 /* Copy the last executed bulk's results to host: status u8[n] (may be NULL) and the
  * output records (n * gputx_out_stride bytes; out may be NULL).  ECAPACITY if out_bytes

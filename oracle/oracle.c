@@ -35,6 +35,7 @@
  * every-linear-extension brute force on tiny bulks, the Figure-1 worked depths,
  * O(n^2) brute-force depths and the Appendix-B graph + topological sort.
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -42,11 +43,12 @@
 /* ---------------------------------------------------------------------------- */
 /* schemas (values of the public interface; the oracle keeps its own copy)       */
 /* ---------------------------------------------------------------------------- */
-enum { S_TPCB = 1, S_TM1 = 2, S_TPCC = 3 };
+enum { S_TPCB = 1, S_TM1 = 2, S_TPCC = 3, S_MICRO = 4 };
 
 #define OUT_TPCB 8
 #define OUT_TM1 40
 #define OUT_TPCC 200
+#define OUT_MICRO 4
 
 static void put_u32(uint8_t* p, uint32_t v) { memcpy(p, &v, 4); }
 static void put_i32(uint8_t* p, int32_t v) { memcpy(p, &v, 4); }
@@ -322,11 +324,44 @@ static void tpcc_txn(void** cols, const uint32_t* dims, int type, const uint32_t
 }
 
 /* ============================================================================ */
+/* Micro benchmark (§6.1): "Each transaction reads a tuple, and     */
+/* performs computation, and then writes the result back to the tuple.  The      */
+/* amount of computation is simulated with calling the _sinf function (100 * x)   */
+/* times."  dims = (N tuples, T types, x); params [tuple]; col 0 tuple (f32 bits). */
+/* One "sin call" of type t (DESIGN.md R-M1): u = fma(v, A_t, B_t) keeps the      */
+/* argument in [-1, 1] and makes every type a different function; then the odd   */
+/* polynomial sin(u) ~ u * (1 + s*(C3 + s*C5)), s = u*u, with IEEE fma where     */
+/* written and single rounding elsewhere, so the GPU evaluates it bit-exactly.     */
+/* Output: the written value (u32 bits).  Never aborts.                            */
+/* ============================================================================ */
+static void micro_txn(void** cols, const uint32_t* dims, int type, const uint32_t* p, uint8_t* st, uint8_t* out)
+{
+    uint32_t* tup = (uint32_t*)cols[0];
+    float v;
+    memcpy(&v, &tup[p[0]], 4);
+    const float A = 0.9375f - (float)type * 0.0078125f;        /* exact binary fractions */
+    const float B = ((float)type - 15.5f) * 0.0009765625f;
+    const float C3 = -0x1.555556p-3f, C5 = 0x1.111112p-7f;      /* -1/6, 1/120 rounded */
+    const uint64_t calls = 100ull * dims[2];
+    for (uint64_t j = 0; j < calls; ++j) {
+        float u = fmaf(v, A, B);
+        float s2 = u * u;
+        float q = fmaf(s2, C5, C3);
+        q = fmaf(s2, q, 1.0f);
+        v = u * q;
+    }
+    memcpy(&tup[p[0]], &v, 4);
+    memcpy(out, &v, 4);
+    *st = 0;
+}
+
+/* ============================================================================ */
 /* Definition 1: serial execution in increasing timestamp order                  */
 /* ============================================================================ */
 uint32_t orc_out_stride(int schema)
 {
-    return schema == S_TPCB ? OUT_TPCB : schema == S_TM1 ? OUT_TM1 : schema == S_TPCC ? OUT_TPCC : 0;
+    return schema == S_TPCB ? OUT_TPCB : schema == S_TM1 ? OUT_TM1 : schema == S_TPCC ? OUT_TPCC
+         : schema == S_MICRO ? OUT_MICRO : 0;
 }
 
 int orc_run(int schema, const uint32_t* dims, void** cols, uint64_t n, const uint8_t* type,
@@ -344,6 +379,7 @@ int orc_run(int schema, const uint32_t* dims, void** cols, uint64_t n, const uin
         uint8_t* o = out + stride * i;
         if (schema == S_TPCB) tpcb_txn(cols, p, ts, &status[i], o, ins, nrows);
         else if (schema == S_TM1) tm1_txn(&tm1, type[i], p, &status[i], o);
+        else if (schema == S_MICRO) micro_txn(cols, dims, type[i], p, &status[i], o);
         else tpcc_txn(cols, dims, type[i], p, ts, &status[i], o, ins, nrows);
         if (status[i]) memset(o, 0, stride);      /* an aborted txn returns no record */
     }
@@ -356,7 +392,7 @@ int orc_run(int schema, const uint32_t* dims, void** cols, uint64_t n, const uin
 /* increment; only with the ADD rule, SURVEY.md NEXT-1 / PAPER.md:475(c): two adds  */
 /* of one item do not conflict, an add conflicts with reads and writes)            */
 /* ============================================================================ */
-enum { T_ACC = 1, T_TEL, T_BR, T_BIT1, T_VLR, T_SFDA, T_CF, T_DNEXT, T_STOCK, T_WYTD, T_DYTD, T_CUST };
+enum { T_ACC = 1, T_TEL, T_BR, T_BIT1, T_VLR, T_SFDA, T_CF, T_DNEXT, T_STOCK, T_WYTD, T_DYTD, T_CUST, T_TUPLE };
 #define ITEM(tag, row) (((uint64_t)(tag) << 48) | (uint64_t)(row))
 
 static int add_op(uint64_t* it, uint8_t* md, int k, uint64_t item, uint8_t mode)
@@ -408,6 +444,8 @@ static int footprint(int schema, const uint32_t* dims, void** cols, int type, co
         }
         return 0;
     }
+    if (schema == S_MICRO)          /* read, compute, write back: one write of the tuple */
+        return add_op(it, md, k, ITEM(T_TUPLE, p[0]), 1);
     /* TPC-C */
     uint64_t D = dims[1], C = dims[2], I = dims[3];
     if (type == 0) {

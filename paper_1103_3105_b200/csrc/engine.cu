@@ -38,6 +38,7 @@ std::vector<ColSpec> column_specs(int schema, const uint32_t* d) {
     const uint64_t a = d[0], b = d[1], c = d[2], e = d[3];
     if (schema == S_TPCB)
         return {{"br_bal", 8, a}, {"tel_bal", 8, a * b}, {"acc_bal", 8, a * c}};
+    if (schema == S_MICRO) return {{"tuple", 4, a}};          // f32 bit patterns
     if (schema == S_TM1) {
         const uint64_t P = a;
         return {{"sub_nbr", 8, P},      {"sub_bits", 2, P},     {"sub_hex", 8, P},       {"sub_byte2", 1, 10 * P},
@@ -65,7 +66,9 @@ std::vector<InsSpec> insert_specs(int schema) {
     return {};
 }
 
-uint32_t ntypes_of(int schema) { return schema == S_TPCB ? 1 : schema == S_TM1 ? 7 : 2; }
+uint32_t ntypes_of(int schema, const uint32_t* d) {
+    return schema == S_TPCB ? 1 : schema == S_TM1 ? 7 : schema == S_MICRO ? d[1] : 2;
+}
 uint32_t bits_for(uint64_t maxval) {   // bits to represent values in [0, maxval]
     uint32_t b = 0;
     while (b < 64 && (maxval >> b)) ++b;
@@ -174,6 +177,7 @@ struct gputx_db {
     bool rec_item_sorted = false;             // d_sorted holds records in (item, ts) order
     int rank_root_grid = 0;
     uint32_t kset_q = 128;     // max transactions per CTA per k-set round (GPUTX_KSET_Q overrides)
+    uint32_t group_p = 0;      // type groups per k-set (gputx_set_grouping; 0 = one per type)
     bool sync_stages = false;  // GPUTX_SYNC (diagnostics): synchronise and check after each stage
     uint32_t kset_diag = 0;    // GPUTX_KSET_DIAG (diagnostics): 1 skip bodies, 8 skip prefetch, 128 hand-off skeleton
     uint32_t exec_grid_override = 0;
@@ -319,7 +323,7 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 
 // ------------------------------------------------------------------------------- K-SET
 // parameter words staged in registers by the K-SET executor (0: read from HBM)
-template <int S> constexpr int kset_pw() { return S == S_TPCB ? 4 : S == S_TM1 ? 8 : 0; }
+template <int S> constexpr int kset_pw() { return S == S_TPCB || S == S_MICRO ? 4 : S == S_TM1 ? 8 : 0; }
 template <int S> constexpr int kset_block() { return S == S_TPCC ? 256 : KX_THREADS; }
 template <int S> const void* kset_fn(bool sh) {
     return sh ? (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), true>
@@ -458,13 +462,14 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
     ++db->launches;
     const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
+    const uint32_t P = db->group_p ? std::min(db->group_p, T) : T;
     group_kernel<0, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, nullptr, nullptr,
-                                          nullptr, nullptr, nullptr, nullptr);
+                                          nullptr, nullptr, nullptr, nullptr, P);
     ++db->launches;
     scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
     ++db->launches;
     group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
-                                                     db->d_perm, db->d_poff, db->d_pw, db->d_ptype, db->d_pp);
+                                                     db->d_perm, db->d_poff, db->d_pw, db->d_ptype, db->d_pp, P);
     ++db->launches;
     STAGE("group");
     cudaEventRecord(db->ev[5], s);
@@ -693,6 +698,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
         }
         if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words, nw_ptr);
         else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words, nw_ptr);
+        else if (db->schema == S_MICRO) launch_ingest<S_MICRO>(db, n_words, nw_ptr);
         else launch_ingest<S_TPCC>(db, n_words, nw_ptr);
         if (ins_scan && db->schema != S_TM1)
             for (int t = 0; t < ntab; ++t)
@@ -738,7 +744,8 @@ Col* find_col(gputx_db* db, const char* name) {
 extern "C" {
 
 uint32_t gputx_out_stride(gputx_schema schema) {
-    return schema == GPUTX_TPCB ? 8 : schema == GPUTX_TM1 ? 40 : schema == GPUTX_TPCC ? 200 : 0;
+    return schema == GPUTX_TPCB ? 8 : schema == GPUTX_TM1 ? 40 : schema == GPUTX_TPCC ? 200
+         : schema == GPUTX_MICRO ? 4 : 0;
 }
 
 const char* gputx_last_error(const gputx_db* db) { return db ? db->err.c_str() : "null handle"; }
@@ -748,17 +755,20 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     *out = nullptr;
     if (!cfg) return GPUTX_EINVAL;
     const int schema = (int)cfg->schema;
-    if (schema < 1 || schema > 3) return GPUTX_EINVAL;
+    if (schema < 1 || schema > 4) return GPUTX_EINVAL;
     if (cfg->max_bulk == 0 || cfg->max_bulk > (1u << 24)) return GPUTX_EINVAL;
     const uint32_t* d = cfg->dims;
     if (schema == S_TPCB && (!d[0] || !d[1] || !d[2])) return GPUTX_EINVAL;
     if (schema == S_TM1 && !d[0]) return GPUTX_EINVAL;
+    // micro benchmark: N tuples, 1 <= T <= 32 types, x <= 1000 units of 100 sin calls; unsharded
+    if (schema == S_MICRO && (!d[0] || !d[1] || d[1] > MICRO_MAX_TYPES || d[2] > 1000 || cfg->nshards > 1))
+        return GPUTX_EINVAL;
     if (schema == S_TPCC && (!d[0] || !d[1] || !d[2] || !d[3])) return GPUTX_EINVAL;
     gputx_db* db = new gputx_db();
     db->cfg = *cfg;
     db->schema = schema;
-    db->ntypes = ntypes_of(schema);
-    db->type_mask = (1u << db->ntypes) - 1;
+    db->ntypes = ntypes_of(schema, d);
+    db->type_mask = db->ntypes >= 32 ? 0xFFFFFFFFu : (1u << db->ntypes) - 1;
     db->max_bulk = cfg->max_bulk;
     db->out_stride = gputx_out_stride(cfg->schema);
     db->part_size = cfg->part_size ? cfg->part_size : 128;
@@ -787,6 +797,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     } else if (schema == S_TM1) {
         n_items = TM1_STRIDE * d[0];
         max_words_per = 7; max_rec_per = 3;
+        db->nparts = (uint32_t)((d[0] + db->part_size - 1) / db->part_size);
+    } else if (schema == S_MICRO) {
+        n_items = d[0];
+        max_words_per = 1; max_rec_per = 1;
         db->nparts = (uint32_t)((d[0] + db->part_size - 1) / db->part_size);
     } else {
         const uint64_t WD = (uint64_t)d[0] * d[1];
@@ -923,10 +937,11 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     }
     db->rank_root_grid = schema == S_TPCB ? coop_grid(db, rank_root_kernel<S_TPCB>, RK_THREADS, 0)
                          : schema == S_TM1 ? coop_grid(db, rank_root_kernel<S_TM1>, RK_THREADS, 0)
+                         : schema == S_MICRO ? coop_grid(db, rank_root_kernel<S_MICRO>, RK_THREADS, 0)
                                            : coop_grid(db, rank_root_kernel<S_TPCC>, RK_THREADS, 0);
     // a round's memory instructions are spread over ceil(|k-set| / Q) SMs; a TPC-C
     // NewOrder issues ~10x the memory instructions of a TM-1 / TPC-B transaction
-    db->kset_q = schema == S_TPCC ? 8 : schema == S_TPCB ? 32 : 128;   // TPC-C: one warp per txn, 8 warps
+    db->kset_q = schema == S_TPCC ? 8 : schema == S_TPCB || schema == S_MICRO ? 32 : 128;   // TPC-C: one warp per txn, 8 warps
     db->kset_cluster = schema == S_TPCB ? 16 : 8;
     if (const char* e = getenv("GPUTX_KSET_Q")) db->kset_q = (uint32_t)std::max(1, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DIAG")) db->kset_diag = (uint32_t)atoi(e);
@@ -947,8 +962,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
     // (sized on the plain variant; the explicit-ts / sharded variant gets the same attributes)
     const void* kfn = schema == S_TPCB ? kset_fn<S_TPCB>(false) : schema == S_TM1 ? kset_fn<S_TM1>(false)
+                    : schema == S_MICRO ? kset_fn<S_MICRO>(false)
                                                                                   : kset_fn<S_TPCC>(false);
     const int kblock = schema == S_TPCB ? kset_block<S_TPCB>() : schema == S_TM1 ? kset_block<S_TM1>()
+                     : schema == S_MICRO ? kset_block<S_MICRO>()
                                                                                  : kset_block<S_TPCC>();
     {
         int per = 0;
@@ -958,6 +975,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     while (db->kset_cluster) {
         if (db->kset_cluster > 8) {
             const void* kfn_ts = schema == S_TPCB ? kset_fn<S_TPCB>(true) : schema == S_TM1 ? kset_fn<S_TM1>(true)
+                    : schema == S_MICRO ? kset_fn<S_MICRO>(true)
                                                                                            : kset_fn<S_TPCC>(true);
             cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaFuncSetAttribute(kfn_ts, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -986,6 +1004,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         db->kset_grid = std::min(db->kset_grid, nclusters * (int)db->kset_cluster);
         // the explicit-ts / sharded variant has its own cooperative grid
         const void* kfn_ts = schema == S_TPCB ? kset_fn<S_TPCB>(true) : schema == S_TM1 ? kset_fn<S_TM1>(true)
+                    : schema == S_MICRO ? kset_fn<S_MICRO>(true)
                                                                                        : kset_fn<S_TPCC>(true);
         int per_ts = 0, ncl_ts = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ts, kfn_ts, kblock, 0);
@@ -1326,6 +1345,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
         if (db->schema != S_TPCB && !(db->kset_diag & 4096u)) CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
         if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
         else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
+        else if (db->schema == S_MICRO) r = execute_schema<S_MICRO>(db, st);
         else r = execute_schema<S_TPCC>(db, st);
     } else {
         for (int k = 1; k < 7; ++k) cudaEventRecord(db->ev[k], s);
@@ -1495,6 +1515,13 @@ gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
     if (n) CK(cudaMemcpy(host, db->d_perm, n * 4, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_set_grouping(gputx_db* db, uint32_t p) {
+    if (!db) return GPUTX_EINVAL;
+    if (p > db->ntypes) return fail(db, GPUTX_EINVAL, "more type groups than types");
+    db->group_p = p;
     return GPUTX_OK;
 }
 

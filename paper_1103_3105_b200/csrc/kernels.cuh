@@ -76,6 +76,9 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
             const uint32_t B = db.dims[0], T = db.dims[1], A = db.dims[2];
             if (len != 4) { report_err(sc, E_LEN, i); continue; }
             if (p[0] >= B * A || p[1] >= B * T || p[2] >= B) { report_err(sc, E_RANGE, i); continue; }
+        } else if (S == S_MICRO) {
+            if (len != 1) { report_err(sc, E_LEN, i); continue; }
+            if (p[0] >= db.dims[0]) { report_err(sc, E_RANGE, i); continue; }
         } else if (S == S_TM1) {
             const uint32_t P = db.dims[0];
             const uint8_t need[7] = {1, 4, 2, 4, 3, 7, 4};
@@ -1152,7 +1155,8 @@ template <int MODE, int PW>
 __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__ D, const uint8_t* __restrict__ type,
                                                     uint32_t n, uint32_t T, uint32_t* cnt, const uint32_t* off,
                                                     uint32_t* perm, const uint32_t* __restrict__ poff,
-                                                    const uint32_t* __restrict__ pw, uint8_t* ptype, uint32_t* pp) {
+                                                    const uint32_t* __restrict__ pw, uint8_t* ptype, uint32_t* pp,
+                                                    uint32_t P) {
     __shared__ uint32_t skey[GR_SLOTS];
     __shared__ uint32_t scnt[GR_SLOTS];
     __shared__ uint32_t sbase[GR_SLOTS];
@@ -1165,7 +1169,9 @@ __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__
 #pragma unroll
         for (int k = 0; k < GR_ITEMS; ++k) {
             const uint64_t i = t0 + k * 256 + threadIdx.x;
-            key[k] = i < n ? D[i] * T + type[i] : GR_EMPTY;
+            // type groups: P partitions of the type ids by their high part (P = T: one
+            // group per type; P = 1: depth only) -- PAPER.md:402-404 radix passes on type
+            key[k] = i < n ? D[i] * T + (P >= T ? type[i] : type[i] * P / T) : GR_EMPTY;
             const uint32_t peers = __match_any_sync(0xffffffffu, key[k]);
             const int leader = __ffs(peers) - 1;
             int sl = -1;
@@ -1646,7 +1652,7 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
 template <int S>
 __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t* __restrict__ frags,
                                                         const uint32_t* __restrict__ part_off, uint32_t nparts, uint32_t* sc) {
-    constexpr int PW = S == S_TPCB ? 4 : 8;
+    constexpr int PW = S == S_TPCB || S == S_MICRO ? 4 : 8;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= nparts) return;
     const uint32_t lo = part_off[p], hi = part_off[p + 1];
@@ -1681,6 +1687,8 @@ __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t
         if (S == S_TPCB) {
             if (kind != F_REMOTE) tpcb_home(db, idx, q0, sh);
             if (kind != F_HOME) tpcb_account(db, idx, q0);
+        } else if (S == S_MICRO) {
+            micro_txn(db, idx, t0, q0);
         } else {
             tm1_txn(db, idx, t0, q0);
         }

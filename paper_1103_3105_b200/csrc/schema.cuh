@@ -13,10 +13,12 @@
 
 namespace gputx {
 
-enum Schema { S_TPCB = 1, S_TM1 = 2, S_TPCC = 3 };
+enum Schema { S_TPCB = 1, S_TM1 = 2, S_TPCC = 3, S_MICRO = 4 };
+constexpr uint32_t MICRO_MAX_TYPES = 32;     // T: branches of the micro benchmark's switch
 
 // ---- column indices (must match the catalog in engine.cu) -----------------------
 enum { B_BR = 0, B_TEL, B_ACC, B_NCOL };
+enum { U_TUPLE = 0, U_NCOL };
 enum { M_NBR = 0, M_BITS, M_HEX, M_BYTE2, M_MSC, M_VLR, M_AI_VALID, M_AI_D1, M_AI_D2, M_AI_D3, M_AI_D4,
        M_SF_VALID, M_SF_ACTIVE, M_SF_ERR, M_SF_DA, M_SF_DB, M_CF_LIVE, M_CF_END, M_CF_NUM, M_NCOL };
 enum { C_W_YTD = 0, C_W_TAX, C_D_YTD, C_D_TAX, C_D_NEXT, C_C_BAL, C_C_YTD, C_C_CNT, C_C_DISC, C_C_CREDIT,
@@ -144,6 +146,9 @@ DEV int footprint(const DevDb& db, uint32_t t, const uint32_t* p, Rec* r) {
         r[1] = {(uint64_t)(p[1] / T) * sb + 1 + p[1] % T, inc};
         r[2] = {(uint64_t)p[2] * sb, inc};
         return 3;
+    } else if (S == S_MICRO) {
+        r[0] = {(uint64_t)p[0], 1u};                    // read, compute, write back the tuple
+        return 1;
     } else if (S == S_TM1) {
         switch (t) {
         case 0: { uint64_t s = (uint64_t)(p[0] - 1) * TM1_STRIDE; r[0] = {s, 0u}; r[1] = {s + 1, 0u}; return 2; }
@@ -187,6 +192,7 @@ template <int S>
 DEV uint64_t item_root(const DevDb& db, uint64_t item) {
     if (S == S_TPCB) return item / (1ull + db.dims[1] + db.dims[2]);
     if (S == S_TM1) return item >> TM1_SLOT_BITS;
+    if (S == S_MICRO) return item;
     const uint64_t D = db.dims[1];
     return item / (2 * D + 1 + D * db.dims[2] + db.dims[3]);
 }
@@ -333,6 +339,51 @@ DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
         return;
     }
     }
+}
+
+// ---- Micro benchmark (§6.1) -------------------------------------------
+// "Each transaction reads a tuple, and performs computation, and then writes the result
+// back to the tuple.  The amount of computation is simulated with calling the _sinf
+// function (100 * x) times."  One call of type t (DESIGN.md R-M1): u = fma(v, A_t, B_t),
+// then sin(u) ~ u * (1 + s (C3 + s C5)), s = u^2 -- every operation IEEE round-to-nearest
+// (__fmaf_rn / __fmul_rn: no contraction), so the result is bit-exact against the C
+// oracle.  Each type is its own instantiation with its constants as immediates, so the
+// T cases of the combined switch are T distinct code paths (the paper makes sure "the
+// branches are not eliminated by code optimization"): lanes of one warp with different
+// types serialise, which is what type grouping removes.
+template <uint32_t TT>
+__device__ __noinline__ float micro_body(float v, uint32_t calls) {
+    constexpr float A = 0.9375f - (float)TT * 0.0078125f;
+    constexpr float B = ((float)TT - 15.5f) * 0.0009765625f;
+    constexpr float C3 = -0x1.555556p-3f, C5 = 0x1.111112p-7f;
+#pragma unroll 1
+    for (uint32_t j = 0; j < calls; ++j) {
+        const float u = __fmaf_rn(v, A, B);
+        const float s2 = __fmul_rn(u, u);
+        float q = __fmaf_rn(s2, C5, C3);
+        q = __fmaf_rn(s2, q, 1.0f);
+        v = __fmul_rn(u, q);
+    }
+    return v;
+}
+
+DEV void micro_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+    uint32_t* tup = COL(uint32_t, U_TUPLE);
+    const uint32_t calls = 100u * db.dims[2];
+    float v = __uint_as_float(ldm(&tup[p[0]]));
+    switch (t) {
+#define MICRO_CASE(k) case k: v = micro_body<k>(v, calls); break;
+        MICRO_CASE(0) MICRO_CASE(1) MICRO_CASE(2) MICRO_CASE(3) MICRO_CASE(4) MICRO_CASE(5) MICRO_CASE(6)
+        MICRO_CASE(7) MICRO_CASE(8) MICRO_CASE(9) MICRO_CASE(10) MICRO_CASE(11) MICRO_CASE(12) MICRO_CASE(13)
+        MICRO_CASE(14) MICRO_CASE(15) MICRO_CASE(16) MICRO_CASE(17) MICRO_CASE(18) MICRO_CASE(19)
+        MICRO_CASE(20) MICRO_CASE(21) MICRO_CASE(22) MICRO_CASE(23) MICRO_CASE(24) MICRO_CASE(25)
+        MICRO_CASE(26) MICRO_CASE(27) MICRO_CASE(28) MICRO_CASE(29) MICRO_CASE(30) MICRO_CASE(31)
+#undef MICRO_CASE
+    default: break;
+    }
+    const uint32_t bits = __float_as_uint(v);
+    stm(&tup[p[0]], bits);
+    put32(db.out + (uint64_t)idx * 4, bits);
 }
 
 // ---- TPC-C -------------------------------------------------------------------------
@@ -720,6 +771,8 @@ DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p
         tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
+    } else if (S == S_MICRO) {
+        micro_txn(db, idx, t, p);
     } else {
         tpcc_txn(db, idx, t, p, SH);
     }
@@ -754,6 +807,9 @@ DEV int fragments(const DevDb& db, uint32_t idx, uint64_t* out) {
     } else if (S == S_TM1) {
         const uint32_t pid = p[0] ? (p[0] - 1) / db.part_size : 0;
         if (out) out[0] = frag_key(pid, idx, F_WHOLE);
+        return 1;
+    } else if (S == S_MICRO) {                         // partition = part_size consecutive tuples
+        if (out) out[0] = frag_key(p[0] / db.part_size, idx, F_WHOLE);
         return 1;
     } else {
         const uint32_t w = p[0];
@@ -791,6 +847,8 @@ DEV void exec_frag(const DevDb& db, uint64_t fk) {
         if (kind != F_HOME) tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
         tm1_txn(db, idx, t, p);
+    } else if (S == S_MICRO) {
+        micro_txn(db, idx, t, p);
     } else {
         if (t == 0) {
             if (tpcc_no_aborts(db, p)) { db.status[idx] = 1; return; }
@@ -807,7 +865,7 @@ DEV void exec_frag(const DevDb& db, uint64_t fk) {
 // a fragment lives on this shard (TM-1 transactions are single-root: home = local)
 template <int S>
 DEV bool frag_local(const DevDb& db, uint64_t fk) {
-    return S == S_TM1 || db.nshards <= 1 || root_local(db, fk >> 32);
+    return S == S_TM1 || S == S_MICRO || db.nshards <= 1 || root_local(db, fk >> 32);
 }
 
 // the fragments of txn idx on this shard (all of them when unsharded)

@@ -19,7 +19,7 @@ STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET, AUTO: GPUTX_AU
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_TYPE", 5: "ESTATE",
                 6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
-OUT_STRIDE = {1: 8, 2: 40, 3: 200}
+OUT_STRIDE = {1: 8, 2: 40, 3: 200, 4: 4}
 FLAG_ADD_RULE = 1            # include/gputx.h GPUTX_FLAG_ADD_RULE
 
 
@@ -79,6 +79,7 @@ def load_library():
         "gputx_column_info": ([P, U32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(U32), ctypes.POINTER(U64)], I),
         "gputx_seal": ([P], I),
         "gputx_register_types": ([P, P, U32], I),
+        "gputx_set_grouping": ([P, U32], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
@@ -117,11 +118,12 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
             "gputx_set_launch", "gputx_set_chooser", "gputx_trace_rounds", "gputx_read_round_ns",
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
-            "gputx_shard_return_pack", "gputx_shard_return_merge"]
+            "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
     2: {},
+    4: {},
     3: {"order": ["o_id", "o_d", "o_w", "o_c", "o_entry_d", "o_ol_cnt", "o_all_local"],
         "new_order": ["no_o_id", "no_d", "no_w"],
         "order_line": ["ol_o_id", "ol_d", "ol_w", "ol_number", "ol_i_id", "ol_supply_w", "ol_quantity", "ol_amount"],
@@ -276,6 +278,10 @@ class Database:
         st = Stats()
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
         return st.as_dict()
+
+    def set_grouping(self, p: int = 0):
+        """Type groups per k-set (include/gputx.h gputx_set_grouping; 0 = one per type)."""
+        self._check(self.lib.gputx_set_grouping(self.h, int(p)), self.h)
 
     def set_chooser(self, w0_bar: int = 0, d_bar: int = 0, c_bar: int = 0):
         """Algorithm 1 thresholds for strategy "auto" (include/gputx.h gputx_set_chooser)."""

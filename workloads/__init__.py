@@ -26,7 +26,7 @@ import numpy as np
 # --------------------------------------------------------------------------------------
 # schemas and type ids (interface constants, mirrored by include/gputx.h)
 # --------------------------------------------------------------------------------------
-TPCB, TM1, TPCC = 1, 2, 3
+TPCB, TM1, TPCC, MICRO = 1, 2, 3, 4
 
 TPCB_DEPOSIT = 0
 TM1_GSD, TM1_GND, TM1_GAD, TM1_USD, TM1_UL, TM1_ICF, TM1_DCF = range(7)
@@ -38,7 +38,7 @@ TM1_MIX = (35, 10, 35, 2, 14, 2, 2)
 TPCC_MIX = (45, 43)
 
 # output record stride (bytes) per schema; layouts documented in include/gputx.h
-OUT_STRIDE = {TPCB: 8, TM1: 40, TPCC: 200}
+OUT_STRIDE = {TPCB: 8, TM1: 40, TPCC: 200, MICRO: 4}
 
 
 @dataclass
@@ -426,6 +426,49 @@ def tpcc_bulk(dims: TpccDims, n: int, seed: int, mix=TPCC_MIX, remote_line_pct: 
     return b
 
 
+# --------------------------------------------------------------------------------------
+# Micro benchmark (§6.1): N tuples; a bulk of single-tuple transactions
+# spread evenly over T types (the branches of the combined switch kernel); each reads
+# its tuple, computes (x units of 100 sin evaluations, the procedure's cost) and writes
+# the result back.  Skew: the first tuple with probability alpha, the others uniformly
+# ("transactions acquire the first lock with a probability of alpha").
+# --------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class MicroDims:
+    tuples: int = 8_000_000       # PAPER.md:258 "the number of tuples is fixed to be eight millions"
+    types: int = 8                # T (default 8)
+    x: int = 16                   # computation units (default 16)
+
+    @property
+    def dims(self):
+        return (self.tuples, self.types, self.x, 0)
+
+
+def micro_db(dims: MicroDims, seed: int = 7) -> dict[str, np.ndarray]:
+    """Tuple values: f32 uniform in [-0.5, 0.5), stored as their u32 bit patterns."""
+    rng = _rng(seed, 0x3C0)
+    v = (rng.random(dims.tuples, dtype=np.float32) - np.float32(0.5)).astype(np.float32)
+    return {"tuple": v.view(np.uint32).copy()}
+
+
+def micro_bulk(dims: MicroDims, n: int, seed: int, alpha: float = 0.0, theta: float = 0.0,
+               types: int | None = None) -> Bulk:
+    """n transactions [tuple id]; type uniform over the T types ("transactions are evenly
+    assigned with a transaction type"); tuple 0 w.p. alpha, else uniform (or Zipf theta)."""
+    rng = _rng(seed, 0x3C1)
+    T = dims.types if types is None else types
+    t = rng.integers(0, T, size=n).astype(np.uint8)
+    if theta > 0.0:
+        tup = zipf_keys(rng, theta, dims.tuples, n)
+    else:
+        tup = rng.integers(0, dims.tuples, size=n, dtype=np.int64)
+    if alpha > 0.0:
+        tup = np.where(rng.random(n) < alpha, 0, tup)
+    b = _pack(MICRO, t, fixed=tup.reshape(n, 1))
+    b.meta = dict(dims=dims.dims, seed=seed, alpha=alpha, root=tup.astype(np.int64))
+    return b
+
+
 def make_db(schema: int, dims, seed: int = 7) -> dict[str, np.ndarray]:
     if schema == TPCB:
         return tpcb_db(dims)
@@ -433,6 +476,8 @@ def make_db(schema: int, dims, seed: int = 7) -> dict[str, np.ndarray]:
         return tm1_db(dims, seed)
     if schema == TPCC:
         return tpcc_db(dims, seed)
+    if schema == MICRO:
+        return micro_db(dims, seed)
     raise ValueError(schema)
 
 
@@ -443,6 +488,8 @@ def make_bulk(schema: int, dims, n: int, seed: int, **kw) -> Bulk:
         return tm1_bulk(dims, n, seed, **kw)
     if schema == TPCC:
         return tpcc_bulk(dims, n, seed, **kw)
+    if schema == MICRO:
+        return micro_bulk(dims, n, seed, **kw)
     raise ValueError(schema)
 
 

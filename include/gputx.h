@@ -290,6 +290,34 @@ gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_r
 gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send_cap, uint64_t* counts);
 gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64_t n_recv);
 
+/* ---- Streaming K-SET over a live transaction pool (SURVEY.md
+ * §8(f) NEXT-2) ---------------------------------------------------------------------------
+ * Transactions arrive in the pool in submission order (ts = next_ts + i, the auto-increment
+ * id of PAPER.md:95) and wait there until they are in the pool's 0-set: no earlier pool
+ * transaction conflicts with them.  Each step executes exactly that 0-set in one lock-free
+ * round (Property 1) and removes it: "It iteratively pick the 0-set as a bulk
+ * for execution ... the transactions in 1-set become the 0-set".  The
+ * k-sets are maintained incrementally: an arrival's access records are radix-sorted and
+ * merged into the pool's sorted record array, and the 0-set is found by one pass of
+ * group-head checks, without a rank fixpoint.  Every executed transaction
+ * precedes, in ts, every pending transaction it conflicts with, so once the pool drains the
+ * database and every transaction's (status, output) equal serial execution in ts order
+ * (Definition 1).  Insert rows are appended at execution time, in ts order within a step.
+ *   gputx_pool_submit(db, arrivals, &first_ts): validate + resolve lookups (as
+ *       gputx_submit_bulk) and append; EINVAL if arrivals->ts is set, ECAPACITY if the pool
+ *       would exceed max_bulk transactions, ESTATE while a bulk is submitted / sharded handles.
+ *   gputx_pool_step(db, stats, &executed): execute the current 0-set (stats: n = executed,
+ *       ms_rank = 0-set extraction, ms_exec = the round, ms_merge = pool compaction).
+ *   gputx_pool_read(db, ts, status, out, cap, &n): host copies of the last step's executed
+ *       transactions in ts order: u32 ts[n], u8 status[n], out[n * gputx_out_stride]; any of
+ *       the three may be NULL; ECAPACITY if cap < n (n is still returned).
+ *   gputx_pool_pending(db, &n): transactions still in the pool.
+ * gputx_submit_bulk returns ESTATE while the pool is not empty; gputx_reset empties it. */
+gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* arrivals, uint64_t* first_ts);
+gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* executed);
+gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* out, uint64_t cap, uint64_t* n);
+gputx_status gputx_pool_pending(const gputx_db* db, uint64_t* n);
+
 /* Restore the pristine image (columns and insert tables) by a device copy. */
 gputx_status gputx_reset(gputx_db* db);
 

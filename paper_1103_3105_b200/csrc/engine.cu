@@ -199,6 +199,17 @@ struct gputx_db {
     uint8_t* s_type = nullptr;       // sharded: staged home bulk (gputx_shard_pack)
     uint32_t *s_poff = nullptr, *s_pw = nullptr, *s_ts = nullptr;
     uint8_t *d_hstatus = nullptr, *d_hout = nullptr;   // sharded: home results in home order
+    // streaming K-SET pool (gputx_pool_*): pending transactions live in d_type/d_poff/d_pw/d_ts
+    // (positions 0..pool_n-1, ts order); their sorted access records in d_prec
+    bool pool_ready = false;
+    uint64_t pool_n = 0, pool_words = 0, pool_nrec = 0, pool_exec = 0;
+    uint64_t *d_prec = nullptr, *d_prec2 = nullptr;
+    uint32_t *d_pins = nullptr, *q_ins = nullptr, *st_ins = nullptr;   // per-table insert counts
+    uint8_t* q_type = nullptr;
+    uint32_t *q_poff = nullptr, *q_pw = nullptr, *q_ts = nullptr;      // compaction targets
+    uint32_t *d_zflag = nullptr, *d_fna = nullptr, *d_list = nullptr, *d_npos = nullptr, *d_noff = nullptr,
+             *d_rpos = nullptr, *d_rts = nullptr;
+    uint8_t *d_rstatus = nullptr, *d_rout = nullptr;
     uint64_t nh = 0;                 // sharded: home transactions staged / in the bulk
     bool staged = false, returned = false;
 };
@@ -665,6 +676,7 @@ void launch_ingest(gputx_db* db, uint32_t n_words, const uint32_t* nw_ptr) {
 
 gputx_status submit_check(gputx_db* db, const gputx_bulk* b) {
     if (!db->sealed) return fail(db, GPUTX_ESTATE, "submit before seal");
+    if (db->pool_n) return fail(db, GPUTX_ESTATE, "the transaction pool is not empty (gputx_pool_step until drained)");
     if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is already submitted");
     if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
     if (b->n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
@@ -727,6 +739,175 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
         }
     }
     db->submitted = true;
+    return GPUTX_OK;
+}
+
+// ---------------------------------------------------------------- streaming K-SET pool
+constexpr int SC_POOL_KEPT = SC_CHG0, SC_POOL_WORDS = SC_CHG1;   // (rank slots, unused in pool steps)
+
+gputx_status pool_alloc(gputx_db* db) {
+    if (db->pool_ready) return GPUTX_OK;
+    const uint64_t NB = db->max_bulk;
+    gputx_status st;
+    if (!db->s_type &&
+        ((st = dalloc(db, &db->s_type, NB + 1)) || (st = dalloc(db, &db->s_poff, NB + 1)) ||
+         (st = dalloc(db, &db->s_pw, db->max_words + 16))))
+        return st;
+    if ((st = dalloc(db, &db->d_prec, db->max_rec + 1)) || (st = dalloc(db, &db->d_prec2, db->max_rec + 1)) ||
+        (st = dalloc(db, &db->d_pins, 4 * (NB + 1))) || (st = dalloc(db, &db->q_ins, 4 * (NB + 1))) ||
+        (st = dalloc(db, &db->st_ins, 4 * (NB + 1))) || (st = dalloc(db, &db->q_type, NB + 1)) ||
+        (st = dalloc(db, &db->q_poff, NB + 1)) || (st = dalloc(db, &db->q_pw, db->max_words + 16)) ||
+        (st = dalloc(db, &db->q_ts, NB + 1)) || (st = dalloc(db, &db->d_zflag, NB + 1)) ||
+        (st = dalloc(db, &db->d_fna, db->n_items)) || (st = dalloc(db, &db->d_list, NB + 1)) ||
+        (st = dalloc(db, &db->d_npos, NB + 2)) || (st = dalloc(db, &db->d_noff, NB + 2)) ||
+        (st = dalloc(db, &db->d_rpos, db->max_rec + 2)) || (st = dalloc(db, &db->d_rts, NB + 1)) ||
+        (st = dalloc(db, &db->d_rstatus, NB + 1)) || (st = dalloc(db, &db->d_rout, NB * db->out_stride + 16)))
+        return st;
+    db->pool_ready = true;
+    return GPUTX_OK;
+}
+
+template <int S>
+gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
+    cudaStream_t s = db->stream;
+    const uint32_t ntab = (uint32_t)db->ins.size();
+    // 1. ingest the arrivals in the staging area (validation, split lookups, insert counts)
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    if (ntab) CK(cudaMemsetAsync(db->st_ins, 0, 4 * (m + 1) * ntab, s));
+    DevDb v = make_devdb(db);
+    v.n = (uint32_t)m;
+    v.type = db->s_type;
+    v.poff = db->s_poff;
+    v.pw = db->s_pw;
+    v.ts = nullptr;
+    const uint32_t g = grid_for(m, 256, 148 * 16);
+    ingest_kernel<S><<<g, 256, 0, s>>>(v, db->s_pw, words, nullptr, db->type_mask, db->st_ins, (uint32_t)(m + 1),
+                                       db->d_sc, nullptr);
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_ERR])
+        return fail(db, db->h_sc[SC_ERR] <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
+                    "pool arrival " + std::to_string(db->h_sc[SC_BADIDX]) + " rejected (code " +
+                        std::to_string(db->h_sc[SC_ERR]) + ")");
+    // 2. append to the pool with timestamps next_ts + i
+    const uint32_t n0 = (uint32_t)db->pool_n;
+    pool_append_kernel<<<g, 256, 0, s>>>(db->s_type, db->s_poff, db->s_pw, db->st_ins, (uint32_t)m, n0,
+                                         (uint32_t)db->pool_words, (uint32_t)db->next_ts, ntab,
+                                         S == S_TPCB ? 1u : 0u, db->d_type, db->d_poff, db->d_pw, db->d_ts,
+                                         db->d_pins, (uint32_t)db->max_bulk);
+    // 3. the arrivals' access records, sorted by (item, ts), merged into the pool's
+    DevDb a = make_devdb(db);
+    a.n = (uint32_t)m;
+    a.type = db->d_type + n0;
+    a.poff = db->d_poff + n0;
+    a.idx_base = n0;
+    emit_count_kernel<S><<<g, 256, 0, s>>>(a, db->d_cnt);
+    scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, m, db->d_sc + SC_NREC);
+    emit_write_kernel<S><<<g, 256, 0, s>>>(a, db->d_rec_off, db->d_rec_a);
+    const uint64_t* srt = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_NREC,
+                                         std::min<uint64_t>(db->max_rec, m * MAX_REC), KEY_ITEM_SHIFT, db->item_bits,
+                                         db->sort_ws, db->epoch, s);
+    const uint64_t tot = db->pool_nrec + std::min<uint64_t>(db->max_rec, m * MAX_REC);
+    pool_merge_kernel<<<grid_for(tot, 256, 148 * 8), 256, 0, s>>>(db->d_prec, (uint32_t)db->pool_nrec, srt,
+                                                                  db->d_sc + SC_NREC, db->d_prec2);
+    std::swap(db->d_prec, db->d_prec2);
+    db->launches += 6;
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    db->pool_nrec += db->h_sc[SC_NREC];
+    db->pool_n += m;
+    db->pool_words += words;
+    return GPUTX_OK;
+}
+
+template <int S>
+gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
+    cudaStream_t s = db->stream;
+    const uint64_t n = db->pool_n, nrec = db->pool_nrec;
+    const uint32_t ntab = (uint32_t)db->ins.size();
+    const uint32_t g = grid_for(std::max(n, nrec), 256, 148 * 16);
+    db->launches = 0;
+    cudaEventRecord(db->ev[0], s);
+    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    // 0-set of the pool: one pass of head checks over the sorted records (no rank fixpoint)
+    pool_zs_init_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_lock, db->d_fna, db->d_zflag, (uint32_t)n);
+    pool_zs_mark_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_lock, db->d_fna);
+    pool_zs_check_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_lock, db->d_fna, db->d_zflag);
+    scan_u32(db, db->d_zflag, db->d_rec_off, nullptr, n, db->d_sc + SC_XTOTAL);
+    pool_list_kernel<<<g, 256, 0, s>>>(db->d_zflag, db->d_rec_off, (uint32_t)n, db->d_list);
+    // insert rows of the executed transactions: positions in ts order (appended per step)
+    if (ntab) {
+        pool_ins_mask_kernel<<<g, 256, 0, s>>>(db->d_zflag, db->d_pins, (uint32_t)n, (uint32_t)db->max_bulk, ntab,
+                                              db->d_ins_off);
+        for (uint32_t t = 0; t < ntab; ++t)
+            scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n, db->d_sc + SC_INS0 + t);
+    }
+    db->launches += 5;
+    cudaEventRecord(db->ev[4], s);
+    // one lock-free round (Property 1): the whole 0-set in parallel
+    CK(cudaMemsetAsync(db->d_status, 0, n, s));
+    CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
+    db->n = n;
+    db->has_ts = true;
+    DevDb v = make_devdb(db);
+    pool_exec_kernel<S><<<grid_for(S == S_TPCC ? n * 32 : n, 256, 148 * 8), 256, 0, s>>>(v, db->d_list,
+                                                                                       db->d_sc + SC_XTOTAL);
+    cudaEventRecord(db->ev[6], s);
+    pool_results_kernel<<<g, 256, 0, s>>>(db->d_list, db->d_sc + SC_XTOTAL, db->d_ts, db->d_status, db->d_out,
+                                          db->out_stride, db->d_rts, db->d_rstatus, db->d_rout);
+    count_aborts_kernel<<<grid_for(n / 4 + 1, 256, 148 * 4), 256, 0, s>>>(db->d_status, (uint32_t)n,
+                                                                          db->d_sc + SC_COMMITTED);
+    // remove the executed transactions and their records (stable: ts order and the
+    // records' (item, ts) order are preserved; record idx renumbered)
+    pool_keep_kernel<<<g, 256, 0, s>>>(db->d_zflag, db->d_poff, (uint32_t)n, db->d_cnt, db->d_rpos);
+    scan_u32(db, db->d_cnt, db->d_npos, nullptr, n, db->d_sc + SC_POOL_KEPT);
+    scan_u32(db, db->d_rpos, db->d_noff, nullptr, n, db->d_sc + SC_POOL_WORDS);
+    pool_compact_kernel<<<g, 256, 0, s>>>(db->d_zflag, db->d_npos, db->d_noff, (uint32_t)n, ntab,
+                                          (uint32_t)db->max_bulk, db->d_type, db->d_poff, db->d_pw, db->d_ts,
+                                          db->d_pins, db->q_type, db->q_poff, db->q_pw, db->q_ts, db->q_ins,
+                                          db->d_sc + SC_POOL_KEPT, db->d_sc + SC_POOL_WORDS);
+    pool_rec_keep_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_zflag, db->d_cnt);
+    scan_u32(db, db->d_cnt, db->d_rpos, nullptr, nrec, db->d_sc + SC_NREC);
+    pool_rec_compact_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_cnt, db->d_rpos, db->d_npos,
+                                              db->d_prec2);
+    db->launches += 10;
+    cudaEventRecord(db->ev[7], s);
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    std::swap(db->d_type, db->q_type);
+    std::swap(db->d_poff, db->q_poff);
+    std::swap(db->d_pw, db->q_pw);
+    std::swap(db->d_ts, db->q_ts);
+    std::swap(db->d_pins, db->q_ins);
+    std::swap(db->d_prec, db->d_prec2);
+    const uint64_t ex = db->h_sc[SC_XTOTAL];
+    db->pool_exec = ex;
+    db->pool_n = db->h_sc[SC_POOL_KEPT];
+    db->pool_words = db->h_sc[SC_POOL_WORDS];
+    db->pool_nrec = db->h_sc[SC_NREC];
+    for (auto& t : db->ins) t.rows += db->h_sc[SC_INS0 + t.table_id];
+    db->executed = false;          // gputx_read_results is for bulks; pool results: gputx_pool_read
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->n = ex;
+        stats->zero_set = ex;
+        stats->records = nrec;
+        stats->aborted = db->h_sc[SC_COMMITTED];
+        stats->committed = ex - stats->aborted;
+        stats->launches = db->launches;
+        stats->strategy = GPUTX_KSET;
+        float a = 0, b = 0, c = 0, tot = 0;
+        cudaEventElapsedTime(&a, db->ev[0], db->ev[4]);
+        cudaEventElapsedTime(&b, db->ev[4], db->ev[6]);
+        cudaEventElapsedTime(&c, db->ev[6], db->ev[7]);
+        cudaEventElapsedTime(&tot, db->ev[0], db->ev[7]);
+        stats->ms_rank = a;       // 0-set extraction (head checks + list + insert positions)
+        stats->ms_exec = b;
+        stats->ms_merge = c;      // results + compaction of the pool
+        stats->ms_total = tot;
+    }
     return GPUTX_OK;
 }
 
@@ -1518,6 +1699,81 @@ gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
     return GPUTX_OK;
 }
 
+gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
+    if (!db || !b) return GPUTX_EINVAL;
+    if (!db->sealed) return fail(db, GPUTX_ESTATE, "pool submit before seal");
+    if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
+    if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
+    if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "the pool is single-GPU (unsharded handles)");
+    if (b->ts) return fail(db, GPUTX_EINVAL, "pool arrivals take ts = next_ts + i (gputx_bulk.ts must be NULL)");
+    const uint64_t m = b->n;
+    if (db->pool_n + m > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "pool would exceed max_bulk");
+    if (m && (!b->type || !b->param_off || !b->param_words)) return GPUTX_EINVAL;
+    if (db->next_ts + m >= (1ull << 24)) return fail(db, GPUTX_ECAPACITY, "timestamp space (24 bits) exhausted; reset");
+    TRY(pool_alloc(db));
+    if (first_ts) *first_ts = db->next_ts;
+    if (!m) return GPUTX_OK;
+    cudaStream_t s = db->stream;
+    uint32_t words = 0;
+    if (b->on_device) {
+        CK(cudaMemcpyAsync(db->h_sc + SC_COUNT - 1, b->param_off + m, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        words = db->h_sc[SC_COUNT - 1];
+    } else {
+        words = b->param_off[m];
+    }
+    if (db->pool_words + words > db->max_words) return fail(db, GPUTX_ECAPACITY, "pool parameter words exceed capacity");
+    const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(db->s_type, b->type, m, kind, s));
+    CK(cudaMemcpyAsync(db->s_poff, b->param_off, (m + 1) * 4, kind, s));
+    if (words) CK(cudaMemcpyAsync(db->s_pw, b->param_words, (uint64_t)words * 4, kind, s));
+    gputx_status r;
+    if (db->schema == S_TPCB) r = pool_submit_schema<S_TPCB>(db, m, words);
+    else if (db->schema == S_TM1) r = pool_submit_schema<S_TM1>(db, m, words);
+    else if (db->schema == S_MICRO) r = pool_submit_schema<S_MICRO>(db, m, words);
+    else r = pool_submit_schema<S_TPCC>(db, m, words);
+    if (r == GPUTX_OK) db->next_ts += m;
+    return r;
+}
+
+gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* executed) {
+    if (!db) return GPUTX_EINVAL;
+    if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
+    if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
+    if (!db->pool_n) {
+        db->pool_exec = 0;
+        if (executed) *executed = 0;
+        if (stats) memset(stats, 0, sizeof(*stats));
+        return GPUTX_OK;
+    }
+    gputx_status r;
+    if (db->schema == S_TPCB) r = pool_step_schema<S_TPCB>(db, stats);
+    else if (db->schema == S_TM1) r = pool_step_schema<S_TM1>(db, stats);
+    else if (db->schema == S_MICRO) r = pool_step_schema<S_MICRO>(db, stats);
+    else r = pool_step_schema<S_TPCC>(db, stats);
+    if (r == GPUTX_OK && executed) *executed = db->pool_exec;
+    return r;
+}
+
+gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* out, uint64_t cap, uint64_t* n) {
+    if (!db) return GPUTX_EINVAL;
+    const uint64_t k = db->pool_exec;
+    if (n) *n = k;
+    if (k > cap) return fail(db, GPUTX_ECAPACITY, "result buffers hold fewer than the step's transactions");
+    cudaStream_t s = db->stream;
+    if (k && ts) CK(cudaMemcpyAsync(ts, db->d_rts, k * 4, cudaMemcpyDeviceToHost, s));
+    if (k && status) CK(cudaMemcpyAsync(status, db->d_rstatus, k, cudaMemcpyDeviceToHost, s));
+    if (k && out) CK(cudaMemcpyAsync(out, db->d_rout, k * db->out_stride, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_pool_pending(const gputx_db* db, uint64_t* n) {
+    if (!db || !n) return GPUTX_EINVAL;
+    *n = db->pool_n;
+    return GPUTX_OK;
+}
+
 gputx_status gputx_set_grouping(gputx_db* db, uint32_t p) {
     if (!db) return GPUTX_EINVAL;
     if (p > db->ntypes) return fail(db, GPUTX_EINVAL, "more type groups than types");
@@ -1544,6 +1800,7 @@ gputx_status gputx_reset(gputx_db* db) {
     db->submitted = false;
     db->executed = false;
     db->next_ts = 0;
+    db->pool_n = db->pool_words = db->pool_nrec = db->pool_exec = 0;
     return GPUTX_OK;
 }
 
@@ -1572,6 +1829,16 @@ void gputx_close_db(gputx_db* db) {
                   db->d_src, db->d_home_pos, db->d_xflag, db->s_type, db->s_poff, db->s_pw, db->s_ts,
                   db->d_hstatus, db->d_hout, db->d_wseg, db->d_wst};
     for (void* p : ps)
+        if (p) cudaFree(p);
+    void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
+                  db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,
+                  db->d_rstatus, db->d_rout};
+    if (db->nshards <= 1) {                  // pool staging (sharded handles free s_* above)
+        void* st[] = {db->s_type, db->s_poff, db->s_pw};
+        for (void* p : st)
+            if (p) cudaFree(p);
+    }
+    for (void* p : pp)
         if (p) cudaFree(p);
     if (db->h_sc) cudaFreeHost(db->h_sc);
     for (auto& e : db->ev)

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) emit_write_kernel(DevDb db, const uint32_
         Rec r[MAX_REC];
         const int k = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
         uint64_t* dst = keys + off[i];
-        for (int j = 0; j < k; ++j) dst[j] = make_key(r[j].item, i, j, r[j].w);
+        for (int j = 0; j < k; ++j) dst[j] = make_key(r[j].item, db.idx_base + i, j, r[j].w);
     }
 }
 
@@ -2139,4 +2139,186 @@ __global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, cons
     }
 }
 
+}  // namespace gputx
+
+namespace gputx {
+// =====================================================================================
+// Streaming K-SET over a live transaction pool (SURVEY.md §8(f)
+// NEXT-2).  The pool = transactions not executed yet, in ts order, already ingested, with
+// their access records kept SORTED by (item, ts).  Arrivals are ingested in a staging
+// area, their records radix-sorted on their own and MERGED into the pool's sorted array
+// ("their basic operations are merged into the sorted array").  A step
+// executes the pool's 0-set -- found in one pass over the records, no rank fixpoint ("the
+// incremental algorithm is able to find the 0-set without computing the k-set from
+// scratch"): a transaction is in the 0-set iff no earlier pool transaction conflicts with
+// it, i.e. each of its records is a write at the head of its item group, or a read (add)
+// with only reads (adds) before it -- then removes them and their records from the pool.
+// =====================================================================================
+constexpr uint32_t POOL_INF = 0xFFFFFFFFu;
+
+// append the ingested arrivals (staging) to the pool: types, rebased offsets, words,
+// timestamps ts0 + i, per-table insert counts (stride cap + 1; TPC-B: one history row each)
+__global__ void __launch_bounds__(256) pool_append_kernel(const uint8_t* __restrict__ st_type,
+        const uint32_t* __restrict__ st_poff, const uint32_t* __restrict__ st_pw, const uint32_t* __restrict__ st_ins,
+        uint32_t m, uint32_t n0, uint32_t w0, uint32_t ts0, uint32_t ntab, uint32_t ins_all_one, uint8_t* p_type,
+        uint32_t* p_poff, uint32_t* p_pw, uint32_t* p_ts, uint32_t* p_ins, uint32_t cap) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = tid; i < m; i += nt) {
+        p_type[n0 + i] = st_type[i];
+        p_poff[n0 + i] = w0 + st_poff[i];
+        p_ts[n0 + i] = ts0 + i;
+        for (uint32_t t = 0; t < ntab; ++t)
+            p_ins[t * (cap + 1) + n0 + i] = ins_all_one ? 1u : st_ins[t * (m + 1) + i];
+    }
+    const uint32_t nw = st_poff[m];
+    for (uint32_t j = tid; j < nw; j += nt) p_pw[w0 + j] = st_pw[j];
+    if (tid == 0) p_poff[n0 + m] = w0 + nw;
+}
+
+// merge two sorted runs of unique keys: A (the pool's records) and B (the arrivals')
+__global__ void __launch_bounds__(256) pool_merge_kernel(const uint64_t* __restrict__ A, uint32_t na,
+                                                         const uint64_t* __restrict__ B, const uint32_t* nb_ptr,
+                                                         uint64_t* __restrict__ out) {
+    const uint32_t nb = *nb_ptr;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = tid; i < na + nb; i += nt) {
+        const bool fromA = i < na;
+        const uint64_t k = fromA ? __ldg(&A[i]) : __ldg(&B[i - na]);
+        const uint64_t* other = fromA ? B : A;
+        uint32_t lo = 0, hi = fromA ? nb : na;          // #keys of the other run below k
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&other[mid]) < k) lo = mid + 1; else hi = mid;
+        }
+        out[(fromA ? i : i - na) + lo] = k;
+    }
+}
+
+// 0-set, pass 1: per item group of the pool, reset the first non-read / non-add positions
+__global__ void __launch_bounds__(256) pool_zs_init_kernel(const uint64_t* __restrict__ keys, uint32_t nrec,
+                                                           uint32_t* fnr, uint32_t* fna, uint32_t* zflag, uint32_t n) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t r = tid; r < nrec; r += nt) {
+        const uint64_t it = key_item(__ldg(&keys[r]));
+        fnr[it] = POOL_INF;
+        fna[it] = POOL_INF;
+    }
+    for (uint32_t t = tid; t < n; t += nt) zflag[t] = 1u;
+}
+// pass 2: first position of a record that is not a read (resp. not an add) in each group
+__global__ void __launch_bounds__(256) pool_zs_mark_kernel(const uint64_t* __restrict__ keys, uint32_t nrec,
+                                                           uint32_t* fnr, uint32_t* fna) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += gridDim.x * blockDim.x) {
+        const uint64_t k = __ldg(&keys[r]);
+        const uint32_t mode = key_mode(k);
+        if (mode != 0) atomicMin(&fnr[key_item(k)], r);
+        if (mode != 2) atomicMin(&fna[key_item(k)], r);
+    }
+}
+// pass 3: a record with a conflicting earlier record in its group takes its transaction
+// out of the 0-set (write: not the group head; read: a non-read before it; add: a non-add)
+__global__ void __launch_bounds__(256) pool_zs_check_kernel(const uint64_t* __restrict__ keys, uint32_t nrec,
+                                                            const uint32_t* fnr, const uint32_t* fna, uint32_t* zflag) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += gridDim.x * blockDim.x) {
+        const uint64_t k = __ldg(&keys[r]);
+        const uint64_t it = key_item(k);
+        const uint32_t mode = key_mode(k);
+        bool ok;
+        if (mode == 1) ok = r == 0 || key_item(__ldg(&keys[r - 1])) != it;
+        else if (mode == 0) ok = fnr[it] > r;
+        else ok = fna[it] > r;
+        if (!ok) zflag[key_idx(k)] = 0u;
+    }
+}
+
+// the step's insert counts: rows of executed (0-set) transactions only
+__global__ void __launch_bounds__(256) pool_ins_mask_kernel(const uint32_t* __restrict__ zflag,
+                                                            const uint32_t* __restrict__ p_ins, uint32_t n, uint32_t cap,
+                                                            uint32_t ntab, uint32_t* cnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        for (uint32_t t = 0; t < ntab; ++t) cnt[t * (n + 1) + i] = zflag[i] ? p_ins[t * (cap + 1) + i] : 0u;
+}
+
+// execution list of the 0-set (ts order) from the scanned flags
+__global__ void __launch_bounds__(256) pool_list_kernel(const uint32_t* __restrict__ zflag,
+                                                        const uint32_t* __restrict__ pos, uint32_t n, uint32_t* list) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (zflag[i]) list[pos[i]] = i;
+}
+
+// one lock-free round over the 0-set (Property 1): no two listed
+// transactions conflict; one thread per transaction (TPC-C: one warp)
+template <int S>
+__global__ void __launch_bounds__(256) pool_exec_kernel(DevDb db, const uint32_t* __restrict__ list,
+                                                        const uint32_t* cnt_ptr) {
+    const uint32_t cnt = *cnt_ptr;
+    if (S == S_TPCC) {
+        const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+        for (uint32_t k = w; k < cnt; k += nw) exec_txn_warp<true>(db, __ldg(&list[k]));
+    } else {
+        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
+            exec_txn<S, true>(db, __ldg(&list[k]));
+    }
+}
+
+// results of the step, in ts order: ts, status, output record
+__global__ void __launch_bounds__(256) pool_results_kernel(const uint32_t* __restrict__ list, const uint32_t* cnt_ptr,
+                                                           const uint32_t* __restrict__ p_ts,
+                                                           const uint8_t* __restrict__ status,
+                                                           const uint8_t* __restrict__ out, uint32_t ow,
+                                                           uint32_t* r_ts, uint8_t* r_status, uint8_t* r_out) {
+    const uint32_t cnt = *cnt_ptr;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t i = __ldg(&list[k]);
+        r_ts[k] = p_ts[i];
+        r_status[k] = status[i];
+        for (uint32_t b = 0; b < ow; ++b) r_out[(uint64_t)k * ow + b] = out[(uint64_t)i * ow + b];
+    }
+}
+
+// keep flags (1 - zflag) and kept parameter lengths, for the compaction scans
+__global__ void __launch_bounds__(256) pool_keep_kernel(const uint32_t* __restrict__ zflag,
+                                                        const uint32_t* __restrict__ p_poff, uint32_t n,
+                                                        uint32_t* keep, uint32_t* klen) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        keep[i] = zflag[i] ? 0u : 1u;
+        klen[i] = zflag[i] ? 0u : p_poff[i + 1] - p_poff[i];
+    }
+}
+// move the kept transactions to their new (dense, still ts-ordered) positions
+__global__ void __launch_bounds__(256) pool_compact_kernel(const uint32_t* __restrict__ zflag,
+        const uint32_t* __restrict__ npos, const uint32_t* __restrict__ noff, uint32_t n, uint32_t ntab, uint32_t cap,
+        const uint8_t* __restrict__ p_type, const uint32_t* __restrict__ p_poff, const uint32_t* __restrict__ p_pw,
+        const uint32_t* __restrict__ p_ts, const uint32_t* __restrict__ p_ins, uint8_t* q_type, uint32_t* q_poff,
+        uint32_t* q_pw, uint32_t* q_ts, uint32_t* q_ins, const uint32_t* nkept_ptr, const uint32_t* nwords_ptr) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = tid; i < n; i += nt) {
+        if (zflag[i]) continue;
+        const uint32_t j = npos[i];
+        q_type[j] = p_type[i];
+        q_ts[j] = p_ts[i];
+        q_poff[j] = noff[i];
+        for (uint32_t t = 0; t < ntab; ++t) q_ins[t * (cap + 1) + j] = p_ins[t * (cap + 1) + i];
+        const uint32_t a = p_poff[i], len = p_poff[i + 1] - a;
+        for (uint32_t w = 0; w < len; ++w) q_pw[noff[i] + w] = p_pw[a + w];
+    }
+    if (tid == 0) q_poff[*nkept_ptr] = *nwords_ptr;
+}
+// records of kept transactions, idx renumbered (the (item, ts) order is unchanged)
+__global__ void __launch_bounds__(256) pool_rec_keep_kernel(const uint64_t* __restrict__ keys, uint32_t nrec,
+                                                            const uint32_t* __restrict__ zflag, uint32_t* keep) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += gridDim.x * blockDim.x)
+        keep[r] = zflag[key_idx(__ldg(&keys[r]))] ? 0u : 1u;
+}
+__global__ void __launch_bounds__(256) pool_rec_compact_kernel(const uint64_t* __restrict__ keys, uint32_t nrec,
+                                                               const uint32_t* __restrict__ keep,
+                                                               const uint32_t* __restrict__ rpos,
+                                                               const uint32_t* __restrict__ npos, uint64_t* out) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += gridDim.x * blockDim.x) {
+        if (!keep[r]) continue;
+        const uint64_t k = __ldg(&keys[r]);
+        const uint64_t idx_mask = (uint64_t)0xFFFFFFu << 6;
+        out[rpos[r]] = (k & ~idx_mask) | ((uint64_t)npos[key_idx(k)] << 6);
+    }
+}
 }  // namespace gputx

@@ -65,6 +65,7 @@ struct DevDb {
     const uint32_t* ts;                // global timestamps (NULL: first_ts + idx)
     const uint32_t* src;               // sharded: home-bulk index, or NOT_HOME (a peer's transaction)
     const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
+    uint32_t idx_base;                 // emit: record idx = idx_base + i (pool arrivals; 0 otherwise)
 };
 constexpr uint32_t NOT_HOME = 0xFFFFFFFFu;
 

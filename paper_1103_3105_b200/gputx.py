@@ -80,6 +80,10 @@ def load_library():
         "gputx_seal": ([P], I),
         "gputx_register_types": ([P, P, U32], I),
         "gputx_set_grouping": ([P, U32], I),
+        "gputx_pool_submit": ([P, P, P], I),
+        "gputx_pool_step": ([P, P, P], I),
+        "gputx_pool_read": ([P, P, P, P, U64, P], I),
+        "gputx_pool_pending": ([P, P], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
@@ -118,7 +122,8 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
             "gputx_set_launch", "gputx_set_chooser", "gputx_trace_rounds", "gputx_read_round_ns",
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
-            "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping"]
+            "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping",
+            "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -278,6 +283,41 @@ class Database:
         st = Stats()
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
         return st.as_dict()
+
+    # ---- streaming K-SET pool (include/gputx.h "Streaming K-SET") -------------------
+    def pool_submit(self, bulk=None, *, type=None, param_off=None, param_words=None, on_device: bool = False) -> int:
+        """Append arrivals to the transaction pool; returns the first assigned ts."""
+        b = self._bulk(bulk, type, param_off, param_words, None, on_device)
+        b.ts = None
+        first = ctypes.c_uint64()
+        self._check(self.lib.gputx_pool_submit(self.h, ctypes.byref(b), ctypes.byref(first)), self.h)
+        return first.value
+
+    def pool_step(self) -> dict:
+        """Execute the pool's current 0-set; stats dict with n = executed transactions."""
+        st = Stats()
+        ex = ctypes.c_uint64()
+        self._check(self.lib.gputx_pool_step(self.h, ctypes.byref(st), ctypes.byref(ex)), self.h)
+        d = st.as_dict()
+        d["executed"] = ex.value
+        self.pool_last = ex.value
+        return d
+
+    def pool_read(self, cap: int | None = None):
+        """(ts u32[n], status u8[n], out u8[n, stride]) of the last step's transactions."""
+        n = ctypes.c_uint64()
+        k = getattr(self, "pool_last", 0) if cap is None else cap
+        ts = np.zeros(max(k, 1), np.uint32)
+        st = np.zeros(max(k, 1), np.uint8)
+        out = np.zeros((max(k, 1), self.stride), np.uint8)
+        self._check(self.lib.gputx_pool_read(self.h, _ptr(ts), _ptr(st), _ptr(out), k, ctypes.byref(n)), self.h)
+        m = n.value
+        return ts[:m], st[:m], out[:m]
+
+    def pool_pending(self) -> int:
+        n = ctypes.c_uint64()
+        self._check(self.lib.gputx_pool_pending(self.h, ctypes.byref(n)), self.h)
+        return n.value
 
     def set_grouping(self, p: int = 0):
         """Type groups per k-set (include/gputx.h gputx_set_grouping; 0 = one per type)."""

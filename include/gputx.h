@@ -78,9 +78,25 @@ typedef enum {
 } gputx_status;
 
 typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2,
-               GPUTX_AUTO = 3  /* Algorithm 1, see gputx_set_chooser */ } gputx_strategy;
+               GPUTX_AUTO = 3, /* Algorithm 1, see gputx_set_chooser */
+               /* Relaxed timestamp constraint (Appendix G):
+                * the result equals serial execution in SOME order (serializability), not
+                * necessarily ts order; the order used is gputx_read_serial_order's.        */
+               GPUTX_TPL_RELAXED = 4,  /* Figure 10 spin locks (CAS), acquired in item order,
+                                          strict 2PL; order = lock-point order               */
+               GPUTX_PART_RELAXED = 5  /* sort-free PART: per-partition counters give each
+                                          transaction its position, a prefix sum the starts
+                                          (PAPER.md:523); cross-partition transactions then run
+                                          under TPL_RELAXED. Single-GPU only.  */
+} gputx_strategy;
 typedef enum { GPUTX_TPCB = 1, GPUTX_TM1 = 2, GPUTX_TPCC = 3,
                GPUTX_MICRO = 4  /* the paper's micro benchmark (§6.1), see below */ } gputx_schema;
+
+/* Device-memory hooks: every device allocation of the handle goes through
+ * alloc(bytes, stream, ctx) / free(ptr, stream, ctx) when they are set -- e.g. PyTorch's
+ * caching allocator, so the engine shares the framework's memory pool -- else cudaMalloc. */
+typedef void* (*gputx_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*gputx_free_fn)(void* ptr, void* stream, void* ctx);
 
 typedef struct {
     gputx_schema schema;
@@ -95,6 +111,9 @@ typedef struct {
     uint32_t flags;           /* GPUTX_FLAG_* below; 0 = the paper's R/W conflict rule              */
     uint32_t shard;           /* this handle's shard in [0, nshards)                                */
     uint32_t nshards;         /* 0 or 1: unsharded; 2..8: one handle per GPU, see "Sharding" below  */
+    gputx_alloc_fn alloc;     /* NULL => cudaMalloc / cudaFree (both or neither)                     */
+    gputx_free_fn free;
+    void* alloc_ctx;
 } gputx_db_config;
 
 /* gputx_db_config.flags
@@ -240,6 +259,12 @@ gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const cha
 gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n);
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n);
 
+/* The serialization order of the last execute under GPUTX_TPL_RELAXED / GPUTX_PART_RELAXED:
+ * u32 order[n], a permutation of the bulk's transactions such that executing them one at a
+ * time in this order (each keeping its own ts for time fields) gives exactly the database,
+ * statuses and outputs the relaxed execution produced.  ESTATE for other strategies. */
+gputx_status gputx_read_serial_order(gputx_db* db, uint32_t* host, uint64_t n);
+
 /* K-SET round tracing (diagnostics): when on, the executor records device times (ns,
  * %globaltimer) per round k: [8k] CTA 0 starts, [8k+1] CTA 0 has signalled, [8k+2] and
  * [8k+3] the same for CTA 1 (0 if it did not take part), [8k+4], [8k+5] polls CTA 0 / 1
@@ -317,6 +342,14 @@ gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* arrivals, uint64_
 gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* executed);
 gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* out, uint64_t cap, uint64_t* n);
 gputx_status gputx_pool_pending(const gputx_db* db, uint64_t* n);
+
+/* Snapshot of the current database (every column and the merged insert tables) into one
+ * caller-owned host buffer; 2-call size query: buf == NULL sets *bytes to the size needed.
+ * Layout: "GPTXSNAP" u32 version(1) u32 schema u32 dims[4] u32 ncols u32 ntables; per column
+ * u32 name_len, name, u32 elem_bytes, u64 count, the column's bytes; per insert table u32
+ * name_len, name, u32 ncols, u64 rows, per column u32 name_len, name, rows * 4 bytes.
+ * ECAPACITY (and *bytes = needed) if *bytes is short; ESTATE before seal. */
+gputx_status gputx_snapshot(gputx_db* db, void* buf, uint64_t* bytes);
 
 /* Restore the pristine image (columns and insert tables) by a device copy. */
 gputx_status gputx_reset(gputx_db* db);

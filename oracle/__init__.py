@@ -84,6 +84,8 @@ def _load():
         lib.orc_footprint.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P, P, P, P, ctypes.c_uint64,
                                       ctypes.c_int]
         lib.orc_footprint.restype = ctypes.c_int64
+        lib.orc_run_order.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P, ctypes.c_uint64, P, P, P, P, P]
+        lib.orc_run_order.restype = ctypes.c_int
         lib.orc_depths.argtypes = [ctypes.c_uint64, P, P, P, P]
         lib.orc_depths.restype = ctypes.c_int
         _lib = lib
@@ -112,8 +114,10 @@ class Result:
         self.db, self.status, self.out, self.inserts = db, status, out, inserts
 
 
-def run(schema: int, dims, db: dict, bulk, first_ts: int = 0) -> Result:
-    """Definition 1: execute `bulk` serially in ts order on a COPY of `db`."""
+def run(schema: int, dims, db: dict, bulk, first_ts: int = 0, order=None) -> Result:
+    """Definition 1: execute `bulk` serially in ts order on a COPY of `db`.  With `order`
+    (a permutation of range(n)): serially in that order, each transaction keeping its own
+    ts (orc_run_order; the witness replay of the relaxed strategies)."""
     lib = _load()
     work = {k: np.ascontiguousarray(v).copy() for k, v in db.items()}
     cols = [work[k] for k in COLS[schema]]
@@ -134,8 +138,16 @@ def run(schema: int, dims, db: dict, bulk, first_ts: int = 0) -> Result:
         pw = np.zeros(1, np.uint32)
     dm = _dims(dims)
     t0 = time.perf_counter()
-    rc = lib.orc_run(schema, _ptr(dm), _ptrs(cols), n, _ptr(tp), _ptr(po), _ptr(pw), first_ts,
-                     _ptr(status), _ptr(out), _ptrs(ins_cols), _ptr(nrows))
+    if order is None:
+        rc = lib.orc_run(schema, _ptr(dm), _ptrs(cols), n, _ptr(tp), _ptr(po), _ptr(pw), first_ts,
+                         _ptr(status), _ptr(out), _ptrs(ins_cols), _ptr(nrows))
+    else:
+        od = np.ascontiguousarray(order, np.uint32)
+        if od.shape != (n,) or not np.array_equal(np.sort(od), np.arange(n, dtype=np.uint32)):
+            raise ValueError("order must be a permutation of range(n)")
+        rc = lib.orc_run_order(schema, _ptr(dm), _ptrs(cols), n, _ptr(tp), _ptr(po), _ptr(pw), first_ts,
+                               _ptr(od if n else np.zeros(1, np.uint32)), _ptr(status), _ptr(out),
+                               _ptrs(ins_cols), _ptr(nrows))
     secs = time.perf_counter() - t0
     if rc != 0:
         raise RuntimeError(f"orc_run failed: {rc}")

@@ -60,6 +60,30 @@ static void put_i64(uint8_t* p, int64_t v) { memcpy(p, &v, 8); }
 /* cols: 0 br_bal i64[B], 1 tel_bal i64[B*T], 2 acc_bal i64[B*A]                  */
 /* ins : history h_tid,h_bid,h_aid u32, h_delta i32, h_ts u32                     */
 /* ============================================================================ */
+/* WITHDRAW (type 1): a NON-two-phase procedure -- it
+ * debits account, teller and branch, THEN aborts if the account went negative, which
+ * requires undoing its own updates (here: restoring the values it overwrote).  No history
+ * row.  Output on commit: the account balance after the debit. */
+static void tpcb_withdraw(void** cols, const uint32_t* p, uint8_t* st, uint8_t* out)
+{
+    int64_t* br = (int64_t*)cols[0];
+    int64_t* tel = (int64_t*)cols[1];
+    int64_t* acc = (int64_t*)cols[2];
+    uint32_t aid = p[0], tid = p[1], bid = p[2];
+    int64_t amt = (int64_t)(int32_t)p[3];
+    int64_t a0 = acc[aid], t0 = tel[tid], b0 = br[bid];   /* undo log */
+    acc[aid] -= amt;
+    tel[tid] -= amt;
+    br[bid] -= amt;
+    if (acc[aid] < 0) {                                  /* abort after the writes: roll back */
+        acc[aid] = a0; tel[tid] = t0; br[bid] = b0;
+        *st = 1;
+        return;
+    }
+    put_i64(out, acc[aid]);
+    *st = 0;
+}
+
 static void tpcb_txn(void** cols, const uint32_t* p, uint64_t ts, uint8_t* st, uint8_t* out,
                      void** ins, uint64_t* nrows)
 {
@@ -377,11 +401,41 @@ int orc_run(int schema, const uint32_t* dims, void** cols, uint64_t n, const uin
         const uint32_t* p = param_words + param_off[i];
         uint64_t ts = first_ts + i;
         uint8_t* o = out + stride * i;
-        if (schema == S_TPCB) tpcb_txn(cols, p, ts, &status[i], o, ins, nrows);
+        if (schema == S_TPCB && type[i] == 1) tpcb_withdraw(cols, p, &status[i], o);
+        else if (schema == S_TPCB) tpcb_txn(cols, p, ts, &status[i], o, ins, nrows);
         else if (schema == S_TM1) tm1_txn(&tm1, type[i], p, &status[i], o);
         else if (schema == S_MICRO) micro_txn(cols, dims, type[i], p, &status[i], o);
         else tpcc_txn(cols, dims, type[i], p, ts, &status[i], o, ins, nrows);
         if (status[i]) memset(o, 0, stride);      /* an aborted txn returns no record */
+    }
+    return 0;
+}
+
+/* The same executor over an explicit order (a permutation of 0..n-1): transaction
+ * order[k] runs k-th and keeps its own timestamp first_ts + order[k].  Serializability
+ * without the timestamp constraint (Appendix G) means "equal to this loop
+ * for SOME order"; the relaxed GPU strategies report the order they realised. */
+int orc_run_order(int schema, const uint32_t* dims, void** cols, uint64_t n, const uint8_t* type,
+                  const uint32_t* param_off, const uint32_t* param_words, uint64_t first_ts,
+                  const uint32_t* order, uint8_t* status, uint8_t* out, void** ins, uint64_t* nrows)
+{
+    uint32_t stride = orc_out_stride(schema);
+    if (!stride) return -1;
+    memset(out, 0, stride * n);
+    tm1_t tm1;
+    if (schema == S_TM1) tm1 = tm1_bind(cols, dims);
+    for (uint64_t k = 0; k < n; ++k) {
+        uint64_t i = order[k];
+        if (i >= n) return -2;
+        const uint32_t* p = param_words + param_off[i];
+        uint64_t ts = first_ts + i;
+        uint8_t* o = out + stride * i;
+        if (schema == S_TPCB && type[i] == 1) tpcb_withdraw(cols, p, &status[i], o);
+        else if (schema == S_TPCB) tpcb_txn(cols, p, ts, &status[i], o, ins, nrows);
+        else if (schema == S_TM1) tm1_txn(&tm1, type[i], p, &status[i], o);
+        else if (schema == S_MICRO) micro_txn(cols, dims, type[i], p, &status[i], o);
+        else tpcc_txn(cols, dims, type[i], p, ts, &status[i], o, ins, nrows);
+        if (status[i]) memset(o, 0, stride);
     }
     return 0;
 }

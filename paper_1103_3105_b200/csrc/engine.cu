@@ -67,7 +67,7 @@ std::vector<InsSpec> insert_specs(int schema) {
 }
 
 uint32_t ntypes_of(int schema, const uint32_t* d) {
-    return schema == S_TPCB ? 1 : schema == S_TM1 ? 7 : schema == S_MICRO ? d[1] : 2;
+    return schema == S_TPCB ? 2 : schema == S_TM1 ? 7 : schema == S_MICRO ? d[1] : 2;   // TPC-B: deposit, withdraw
 }
 uint32_t bits_for(uint64_t maxval) {   // bits to represent values in [0, maxval]
     uint32_t b = 0;
@@ -199,6 +199,9 @@ struct gputx_db {
     uint8_t* s_type = nullptr;       // sharded: staged home bulk (gputx_shard_pack)
     uint32_t *s_poff = nullptr, *s_pw = nullptr, *s_ts = nullptr;
     uint8_t *d_hstatus = nullptr, *d_hout = nullptr;   // sharded: home results in home order
+    uint32_t* d_order = nullptr;     // relaxed strategies: the serialization order they produced
+    UndoRec* d_undo = nullptr;       // undo-log slots (TPC-B WITHDRAW, a non-two-phase type)
+    bool has_order = false;
     // streaming K-SET pool (gputx_pool_*): pending transactions live in d_type/d_poff/d_pw/d_ts
     // (positions 0..pool_n-1, ts order); their sorted access records in d_prec
     bool pool_ready = false;
@@ -234,12 +237,26 @@ template <class T>
 gputx_status dalloc(gputx_db* db, T** p, uint64_t count) {
     *p = nullptr;
     if (count == 0) count = 1;
+    if (db->cfg.alloc) {        // the caller's allocator (e.g. PyTorch's caching allocator)
+        *p = (T*)db->cfg.alloc(count * sizeof(T), (void*)db->stream, db->cfg.alloc_ctx);
+        if (!*p) {
+            db->err = "cfg.alloc(" + std::to_string(count * sizeof(T)) + ") returned NULL";
+            return GPUTX_ENOMEM;
+        }
+        return GPUTX_OK;
+    }
     cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
     if (e != cudaSuccess) {
         db->err = std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + "): " + cudaGetErrorString(e);
         return GPUTX_ENOMEM;
     }
     return GPUTX_OK;
+}
+
+void dfree(gputx_db* db, void* p) {
+    if (!p) return;
+    if (db->cfg.free) db->cfg.free(p, (void*)db->stream, db->cfg.alloc_ctx);
+    else cudaFree(p);
 }
 
 #define STAGE(name)                                                                             \
@@ -308,6 +325,7 @@ DevDb make_devdb(gputx_db* db) {
     v.ts = db->has_ts ? db->d_ts : nullptr;
     v.src = db->nshards > 1 ? db->d_src : nullptr;
     v.xflag = db->nshards > 1 ? db->d_xflag : nullptr;
+    v.undo = db->d_undo;
     return v;
 }
 
@@ -632,6 +650,53 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v, bool sorted = false) {
     return GPUTX_OK;
 }
 
+// ------------------------------------------------------------ relaxed-timestamp strategies
+// (Appendix G): serializability only; the executed serialization order
+// is recorded in d_order (gputx_read_serial_order)
+template <int S>
+gputx_status run_tpl_relaxed(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[1], s);
+    CK(cudaMemsetAsync(db->d_lock, 0, db->n_items * 4, s));          // spin locks free
+    for (int k = 2; k < 6; ++k) cudaEventRecord(db->ev[k], s);
+    tpl_relaxed_kernel<S><<<(uint32_t)((db->n + 127) / 128), 128, 0, s>>>(v, nullptr, nullptr, db->d_lock,
+                                                                          db->d_order, 0, db->d_sc);
+    ++db->launches;
+    cudaEventRecord(db->ev[6], s);
+    db->has_order = true;
+    return GPUTX_OK;
+}
+
+template <int S>
+gputx_status run_part_relaxed(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    const uint32_t g = grid_for(db->n, 256, 148 * 16);
+    cudaEventRecord(db->ev[1], s);
+    CK(cudaMemsetAsync(db->d_part_off, 0, ((uint64_t)db->nparts + 1) * 4, s));
+    // bulk generation without sort: per-partition counters -> keys, prefix sum -> starts
+    rpart_key_kernel<S><<<g, 256, 0, s>>>(v, db->d_part_off, db->d_D, db->d_perm, db->d_cnt, db->d_sc);
+    scan_u32(db, db->d_part_off, db->d_part_off, nullptr, db->nparts, db->d_sc + SC_NFRAG);
+    rpart_scatter_kernel<<<g, 256, 0, s>>>(db->d_D, db->d_perm, db->d_part_off, (uint32_t)db->n, db->d_rec_off);
+    db->launches += 3;
+    for (int k = 2; k < 6; ++k) cudaEventRecord(db->ev[k], s);
+    const uint32_t pb = 128, np = db->nparts;
+    rpart_exec_kernel<S><<<(uint32_t)(((uint64_t)np * (S == S_TPCC ? 32 : 1) + pb - 1) / pb), pb, 0, s>>>(
+        v, db->d_rec_off, db->d_part_off, np, db->d_order, db->d_sc);
+    // cross-partition transactions afterwards under the basic spin locks;
+    // their serialization numbers follow the single-partition ones (base = #single)
+    CK(cudaMemsetAsync(db->d_lock, 0, db->n_items * 4, s));
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t ncross = db->h_sc[SC_XTOTAL];
+    if (ncross)
+        tpl_relaxed_kernel<S><<<(ncross + 127) / 128, 128, 0, s>>>(v, db->d_cnt, db->d_sc + SC_XTOTAL, db->d_lock,
+                                                                 db->d_order, (uint32_t)db->n - ncross, db->d_sc);
+    db->launches += 2;
+    cudaEventRecord(db->ev[6], s);
+    db->has_order = true;
+    return GPUTX_OK;
+}
+
 // Algorithm 1 on the bulk's structural parameters
 gputx_strategy choose_strategy(const gputx_db* db, uint64_t w0, uint64_t d, uint64_t c) {
     const uint64_t w0_bar = db->ch_w0 ? db->ch_w0 : 64ull * (uint64_t)db->nsm;
@@ -660,6 +725,8 @@ template <int S>
 gputx_status execute_schema(gputx_db* db, gputx_strategy st) {
     DevDb v = make_devdb(db);
     if (st == GPUTX_AUTO) return run_auto<S>(db, v);
+    if (st == GPUTX_TPL_RELAXED) return run_tpl_relaxed<S>(db, v);
+    if (st == GPUTX_PART_RELAXED) return run_part_relaxed<S>(db, v);
     if (st == GPUTX_KSET) return run_kset<S>(db, v);
     if (st == GPUTX_PART) return run_part<S>(db, v);
     return run_tpl<S>(db, v);
@@ -696,7 +763,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     db->executed = false;
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
     CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
-    const bool ins_scan = db->schema == S_TPCC || db->has_ts;
+    const bool ins_scan = db->schema == S_TPCC || db->schema == S_TPCB || db->has_ts;
     const int ntab = db->schema == S_TPCC ? 4 : 1;
     if (n) {
         if (ins_scan) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * ntab, s));
@@ -732,7 +799,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     }
     // insert rows this bulk will append (decisions are static: two-phase procedures)
     for (auto& t : db->ins) {
-        t.pending = (db->schema == S_TPCB && !db->has_ts) ? n : db->h_sc[SC_INS0 + t.table_id];
+        t.pending = db->h_sc[SC_INS0 + t.table_id];
         if (t.rows + t.pending > t.cap) {
             db->n = 0;
             return fail(db, GPUTX_ECAPACITY, "insert table " + t.name + " full; reset or raise insert_capacity");
@@ -794,7 +861,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     const uint32_t n0 = (uint32_t)db->pool_n;
     pool_append_kernel<<<g, 256, 0, s>>>(db->s_type, db->s_poff, db->s_pw, db->st_ins, (uint32_t)m, n0,
                                          (uint32_t)db->pool_words, (uint32_t)db->next_ts, ntab,
-                                         S == S_TPCB ? 1u : 0u, db->d_type, db->d_poff, db->d_pw, db->d_ts,
+                                         0u, db->d_type, db->d_poff, db->d_pw, db->d_ts,
                                          db->d_pins, (uint32_t)db->max_bulk);
     // 3. the arrivals' access records, sorted by (item, ts), merged into the pool's
     DevDb a = make_devdb(db);
@@ -935,6 +1002,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (!out) return GPUTX_EINVAL;
     *out = nullptr;
     if (!cfg) return GPUTX_EINVAL;
+    if ((cfg->alloc == nullptr) != (cfg->free == nullptr)) return GPUTX_EINVAL;
     const int schema = (int)cfg->schema;
     if (schema < 1 || schema > 4) return GPUTX_EINVAL;
     if (cfg->max_bulk == 0 || cfg->max_bulk > (1u << 24)) return GPUTX_EINVAL;
@@ -1034,8 +1102,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_lock, n_items)) || (st = dalloc(db, &db->d_lkey, db->max_rec)) ||
         (st = dalloc(db, &db->d_part_off, (uint64_t)db->nparts + 2)) || (st = dalloc(db, &db->d_sc, SC_COUNT)) ||
         (st = dalloc(db, &db->d_bar, 1)) || (st = dalloc(db, &db->d_tickets, 256)) ||
-        (st = dalloc(db, &db->d_ts, NB + 1)))
+        (st = dalloc(db, &db->d_ts, NB + 1)) || (st = dalloc(db, &db->d_order, NB + 1)))
         return bail(st);
+    if (schema == S_TPCB && (st = dalloc(db, &db->d_undo, NB * UNDO_SLOTS))) return bail(st);
     if (db->nshards > 1 &&
         ((st = dalloc(db, &db->d_src, NB + 1)) || (st = dalloc(db, &db->d_home_pos, NB + 1)) ||
          (st = dalloc(db, &db->d_xflag, NB + 1)) || (st = dalloc(db, &db->s_type, NB + 1)) ||
@@ -1514,8 +1583,12 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
 gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
     if (!db) return GPUTX_EINVAL;
     if (!db->submitted) return fail(db, GPUTX_ESTATE, "nothing submitted");
-    if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET && st != GPUTX_AUTO)
+    if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET && st != GPUTX_AUTO && st != GPUTX_TPL_RELAXED &&
+        st != GPUTX_PART_RELAXED)
         return fail(db, GPUTX_EINVAL, "bad strategy");
+    if ((st == GPUTX_TPL_RELAXED || st == GPUTX_PART_RELAXED) && db->nshards > 1)
+        return fail(db, GPUTX_EINVAL, "relaxed strategies are single-GPU");
+    db->has_order = false;
     db->chosen = st == GPUTX_AUTO ? (int)GPUTX_KSET : (int)st;   // AUTO: overwritten by run_auto
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[0], s);
@@ -1568,10 +1641,11 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
             stats->zero_set = db->h_sc[SC_ZERO];
             stats->rank_passes = db->h_sc[SC_PASSES];
         }
-        if (eff == GPUTX_PART) {
+        if (eff == GPUTX_PART || eff == GPUTX_PART_RELAXED) {
             stats->parts = db->nparts;
             stats->max_chain = db->h_sc[SC_MAXCHAIN];
         }
+        if (eff == GPUTX_PART_RELAXED) stats->cross = db->h_sc[SC_XTOTAL];
         float ms[8] = {0};
         for (int k = 1; k < 8; ++k) cudaEventElapsedTime(&ms[k], db->ev[k - 1], db->ev[k]);
         stats->ms_emit = ms[2];
@@ -1768,6 +1842,63 @@ gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* 
     return GPUTX_OK;
 }
 
+// Snapshot: the whole current database in one host buffer.
+//   "GPTXSNAP" u32 version=1 u32 schema u32 dims[4] u32 ncols u32 ntables
+//   per column : u32 name_len, name, u32 elem_bytes, u64 count, count*elem bytes
+//   per table  : u32 name_len, name, u32 ncols, u64 rows, per column: u32 name_len, name, rows*4 bytes
+gputx_status gputx_snapshot(gputx_db* db, void* buf, uint64_t* bytes) {
+    if (!db || !bytes) return GPUTX_EINVAL;
+    if (!db->sealed) return fail(db, GPUTX_ESTATE, "snapshot before seal");
+    uint64_t need = 8 + 4 * 8;
+    for (auto& c : db->cols) need += 4 + strlen(c.spec.name) + 4 + 8 + c.spec.count * c.spec.elem;
+    for (auto& t : db->ins) {
+        need += 4 + t.name.size() + 4 + 8;
+        for (auto& c : t.cols) need += 4 + c.name.size() + t.rows * 4;
+    }
+    if (!buf) { *bytes = need; return GPUTX_OK; }
+    if (*bytes < need) { *bytes = need; return fail(db, GPUTX_ECAPACITY, "snapshot buffer too small"); }
+    uint8_t* o = (uint8_t*)buf;
+    auto put = [&](const void* p, uint64_t k) { memcpy(o, p, k); o += k; };
+    auto u32 = [&](uint32_t v) { put(&v, 4); };
+    auto u64 = [&](uint64_t v) { put(&v, 8); };
+    put("GPTXSNAP", 8);
+    u32(1);
+    u32((uint32_t)db->schema);
+    for (int k = 0; k < 4; ++k) u32(db->cfg.dims[k]);
+    u32((uint32_t)db->cols.size());
+    u32((uint32_t)db->ins.size());
+    for (auto& c : db->cols) {
+        u32((uint32_t)strlen(c.spec.name));
+        put(c.spec.name, strlen(c.spec.name));
+        u32(c.spec.elem);
+        u64(c.spec.count);
+        CK(cudaMemcpyAsync(o, c.d, c.spec.count * c.spec.elem, cudaMemcpyDeviceToHost, db->stream));
+        o += c.spec.count * c.spec.elem;
+    }
+    for (auto& t : db->ins) {
+        u32((uint32_t)t.name.size());
+        put(t.name.data(), t.name.size());
+        u32((uint32_t)t.cols.size());
+        u64(t.rows);
+        for (auto& c : t.cols) {
+            u32((uint32_t)c.name.size());
+            put(c.name.data(), c.name.size());
+            if (t.rows) CK(cudaMemcpyAsync(o, c.d, t.rows * 4, cudaMemcpyDeviceToHost, db->stream));
+            o += t.rows * 4;
+        }
+    }
+    CK(cudaStreamSynchronize(db->stream));
+    *bytes = need;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_read_serial_order(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (!db || !host) return GPUTX_EINVAL;
+    if (!db->has_order || n != db->n) return fail(db, GPUTX_ESTATE, "no relaxed-strategy execution of this bulk");
+    if (n) CK(cudaMemcpy(host, db->d_order, n * 4, cudaMemcpyDeviceToHost));
+    return GPUTX_OK;
+}
+
 gputx_status gputx_pool_pending(const gputx_db* db, uint64_t* n) {
     if (!db || !n) return GPUTX_EINVAL;
     *n = db->pool_n;
@@ -1816,9 +1947,9 @@ gputx_status gputx_set_launch(gputx_db* db, uint32_t exec_block, uint32_t exec_g
 void gputx_close_db(gputx_db* db) {
     if (!db) return;
     if (db->stream) cudaStreamSynchronize(db->stream);
-    for (auto& c : db->cols) { cudaFree(c.d); cudaFree(c.pristine); }
+    for (auto& c : db->cols) { dfree(db, c.d); dfree(db, c.pristine); }
     for (auto& t : db->ins)
-        for (auto& c : t.cols) cudaFree(c.d);
+        for (auto& c : t.cols) dfree(db, c.d);
     void* ps[] = {db->d_type, db->d_poff, db->d_pw, db->d_status, db->d_out, db->d_ins_off, db->d_hkeys, db->d_hvals,
                   db->d_name_sorted, db->d_name_off, db->d_rec_a, db->d_rec_b, db->d_cnt, db->d_rec_off, db->d_D,
                   db->d_perm, db->d_g, db->d_done, db->d_ptype, db->d_pp, db->d_trace, db->d_gcnt, db->d_goff, db->d_lock, db->d_lkey, db->d_part_off, db->d_sc, db->d_bar,
@@ -1828,18 +1959,13 @@ void gputx_close_db(gputx_db* db) {
                   db->rank_memo.carD, db->rank_memo.dirty, db->rank_memo.recpos, db->d_rtrace, db->d_ts,
                   db->d_src, db->d_home_pos, db->d_xflag, db->s_type, db->s_poff, db->s_pw, db->s_ts,
                   db->d_hstatus, db->d_hout, db->d_wseg, db->d_wst};
-    for (void* p : ps)
-        if (p) cudaFree(p);
+    for (void* p : ps) dfree(db, p);
+    dfree(db, db->d_order);
+    dfree(db, db->d_undo);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
                   db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,
                   db->d_rstatus, db->d_rout};
-    if (db->nshards <= 1) {                  // pool staging (sharded handles free s_* above)
-        void* st[] = {db->s_type, db->s_poff, db->s_pw};
-        for (void* p : st)
-            if (p) cudaFree(p);
-    }
-    for (void* p : pp)
-        if (p) cudaFree(p);
+    for (void* p : pp) dfree(db, p);          // (pool staging s_* is in ps above)
     if (db->h_sc) cudaFreeHost(db->h_sc);
     for (auto& e : db->ev)
         if (e) cudaEventDestroy(e);

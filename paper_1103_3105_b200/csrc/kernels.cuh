@@ -76,6 +76,9 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
             const uint32_t B = db.dims[0], T = db.dims[1], A = db.dims[2];
             if (len != 4) { report_err(sc, E_LEN, i); continue; }
             if (p[0] >= B * A || p[1] >= B * T || p[2] >= B) { report_err(sc, E_RANGE, i); continue; }
+            // WITHDRAW: a local account (its rollback must not span partitions / shards) and a
+            // positive amount
+            if (t == 1 && (p[0] / A != p[2] || (int32_t)p[3] <= 0)) { report_err(sc, E_RANGE, i); continue; }
         } else if (S == S_MICRO) {
             if (len != 1) { report_err(sc, E_LEN, i); continue; }
             if (p[0] >= db.dims[0]) { report_err(sc, E_RANGE, i); continue; }
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                 if (p[4] != 2 && home) ins_cnt[T_HIST * ins_stride + i] = 1;
             }
         }
-        if (S == S_TPCB && db.ts) ins_cnt[i] = home ? 1u : 0u;   // history rows via ins_off
+        if (S == S_TPCB) ins_cnt[i] = (home && t == 0) ? 1u : 0u;   // history rows (deposits) via ins_off
         if (db.nshards > 1) {
             // the home root must be this shard's iff the transaction was submitted here
             const uint64_t root = S == S_TPCB ? p[2] : S == S_TPCC ? p[0] : (uint64_t)(p[0] ? p[0] - 1 : db.root_lo);
@@ -1685,8 +1688,12 @@ __global__ void __launch_bounds__(128) part_exec_kernel(DevDb db, const uint64_t
         // execute fragment j
         const uint32_t idx = fidx(k0), kind = (uint32_t)k0 & 0xFFu;
         if (S == S_TPCB) {
-            if (kind != F_REMOTE) tpcb_home(db, idx, q0, sh);
-            if (kind != F_HOME) tpcb_account(db, idx, q0);
+            if (t0 == 1) {
+                tpcb_withdraw(db, idx, q0);
+            } else {
+                if (kind != F_REMOTE) tpcb_home(db, idx, q0, sh);
+                if (kind != F_HOME) tpcb_account(db, idx, q0);
+            }
         } else if (S == S_MICRO) {
             micro_txn(db, idx, t0, q0);
         } else {
@@ -2319,6 +2326,134 @@ __global__ void __launch_bounds__(256) pool_rec_compact_kernel(const uint64_t* _
         const uint64_t k = __ldg(&keys[r]);
         const uint64_t idx_mask = (uint64_t)0xFFFFFFu << 6;
         out[rpos[r]] = (k & ~idx_mask) | ((uint64_t)npos[key_idx(k)] << 6);
+    }
+}
+}  // namespace gputx
+
+namespace gputx {
+// =====================================================================================
+// Relaxed-timestamp strategies (Appendix G):
+// serializability without the timestamp constraint -- the result equals serial execution
+// in SOME order, which the executor records (d_order, gputx_read_serial_order).
+//   TPL_RELAXED : the basic spin lock of Figure 10 (atomicCAS 0 -> 1, release 0), locks
+//                 acquired in increasing item order (no deadlock), strict 2PL; a
+//                 transaction takes its serialization number at its lock point (every
+//                 lock held), and 2PL serializes transactions in lock-point order.
+//   PART_RELAXED: no sort: "each transaction needs to acquire the lock for its partition,
+//                 get the counter value as its key value, and increases the counter value
+//                 by one ... A prefix sum is used to calculate the start position of each
+//                 group"; cross-partition transactions then run under
+//                 TPL_RELAXED ("we use TPL"), after every partition.
+// =====================================================================================
+constexpr uint32_t RX_CROSS = 0xFFFFFFFFu;
+
+DEV void rx_sort_items(Rec* r, int k) {        // insertion sort by item (k <= MAX_REC)
+    for (int a = 1; a < k; ++a) {
+        const Rec x = r[a];
+        int b = a - 1;
+        while (b >= 0 && r[b].item > x.item) { r[b + 1] = r[b]; --b; }
+        r[b + 1] = x;
+    }
+}
+
+// list: the transactions to run (nullptr: all of the bulk); order[base + seq] = idx
+template <int S>
+__global__ void __launch_bounds__(128) tpl_relaxed_kernel(DevDb db, const uint32_t* __restrict__ list,
+                                                          const uint32_t* cnt_ptr, uint32_t* lock, uint32_t* order,
+                                                          uint32_t base, uint32_t* sc) {
+    const uint32_t cnt = list ? *cnt_ptr : db.n;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool done = t >= cnt;
+    const uint32_t idx = done ? 0u : (list ? __ldg(&list[t]) : t);
+    Rec r[MAX_REC];
+    int k = 0, j = 0;
+    if (!done) {
+        k = footprint<S>(db, db.type[idx], db.pw + db.poff[idx], r);
+        rx_sort_items(r, k);
+    }
+    uint32_t polls = 0;
+    // warp-converged acquisition (as tpl_exec_kernel): lanes that can take their next lock
+    // advance, lanes holding every lock execute and release in the same iteration
+    while (__any_sync(0xffffffffu, !done)) {
+        bool progressed = false;
+        if (!done) {
+            while (j < k) {
+                uint32_t old;
+                asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(&lock[r[j].item]) : "memory");
+                if (old != 0u) break;
+                ++j;
+                progressed = true;
+            }
+            if (j == k) {
+                const uint32_t seq = atomicAdd(&sc[SC_TICKET], 1u);       // lock point
+                order[base + seq] = idx;
+                exec_txn<S, false>(db, idx);
+                for (int q = 0; q < k; ++q) st_release(&lock[r[q].item], 0u);
+                done = true;
+                progressed = true;
+            }
+        }
+        if (!__any_sync(0xffffffffu, progressed)) {
+            if (++polls > SPIN_LIMIT) {
+                if (!done) atomicExch(&sc[SC_DEADLOCK], 1u);
+                break;
+            }
+            __nanosleep(polls > 8 ? 64u : 0u);
+        }
+    }
+}
+
+// PART_RELAXED step 1: partition key by counter (single-partition transactions) or the
+// cross list; step 2 (after a scan of cnt): the partition-major list
+template <int S>
+__global__ void __launch_bounds__(256) rpart_key_kernel(DevDb db, uint32_t* pcnt, uint32_t* pkey, uint32_t* ppid,
+                                                        uint32_t* clist, uint32_t* sc) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
+        uint64_t fk[MAX_REC];
+        const int nf = fragments<S>(db, i, fk);
+        if (nf == 1) {
+            const uint32_t pid = (uint32_t)(fk[0] >> 32);
+            ppid[i] = pid;
+            pkey[i] = atomicAdd(&pcnt[pid], 1u);
+        } else {
+            ppid[i] = RX_CROSS;
+            clist[atomicAdd(&sc[SC_XTOTAL], 1u)] = i;
+        }
+    }
+}
+__global__ void __launch_bounds__(256) rpart_scatter_kernel(const uint32_t* __restrict__ pkey,
+                                                            const uint32_t* __restrict__ ppid,
+                                                            const uint32_t* __restrict__ pstart, uint32_t n,
+                                                            uint32_t* plist) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (ppid[i] != RX_CROSS) plist[pstart[ppid[i]] + pkey[i]] = i;
+}
+// one thread (TPC-C: one warp) per partition runs its transactions in key order; the
+// partition-major list is also the serialization order of this phase
+template <int S>
+__global__ void __launch_bounds__(128) rpart_exec_kernel(DevDb db, const uint32_t* __restrict__ plist,
+                                                         const uint32_t* __restrict__ pstart, uint32_t nparts,
+                                                         uint32_t* order, uint32_t* sc) {
+    if (S == S_TPCC) {
+        const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        if (p >= nparts) return;
+        const uint32_t lo = pstart[p], hi = pstart[p + 1];
+        for (uint32_t k = lo; k < hi; ++k) {
+            const uint32_t idx = __ldg(&plist[k]);
+            if (lane_id() == 0) order[k] = idx;
+            exec_txn_warp<false>(db, idx);
+        }
+        if (lane_id() == 0 && hi > lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
+    } else {
+        const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+        if (p >= nparts) return;
+        const uint32_t lo = pstart[p], hi = pstart[p + 1];
+        for (uint32_t k = lo; k < hi; ++k) {
+            const uint32_t idx = __ldg(&plist[k]);
+            order[k] = idx;
+            exec_txn<S, false>(db, idx);
+        }
+        if (hi > lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
     }
 }
 }  // namespace gputx

@@ -66,7 +66,20 @@ struct DevDb {
     const uint32_t* src;               // sharded: home-bulk index, or NOT_HOME (a peer's transaction)
     const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
     uint32_t idx_base;                 // emit: record idx = idx_base + i (pool arrivals; 0 otherwise)
+    struct UndoRec* undo;              // per-transaction undo-log slots (non-two-phase types)
 };
+
+// Undo log: written in GPU memory before each update of a NON-two-phase
+// transaction and discarded at commit; on abort the transaction replays it backwards.
+// RESTORE puts back the value it overwrote (exclusively held items); ADD compensates an
+// increment (items other transactions may increment concurrently under the ADD rule).
+enum { UNDO_RESTORE = 0, UNDO_ADD = 1 };
+struct UndoRec {
+    uint32_t col, kind;
+    uint64_t row;
+    int64_t val;
+};
+constexpr int UNDO_SLOTS = 3;          // records per transaction (TPC-B WITHDRAW: account, teller, branch)
 constexpr uint32_t NOT_HOME = 0xFFFFFFFFu;
 
 // sh (compile-time in the fused kernels): the bulk carries explicit timestamps (sharded or
@@ -225,8 +238,10 @@ DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     const int32_t delta = (int32_t)p[3];
     red_add(&COL(int64_t, B_TEL)[p[1]], (int64_t)delta);
     red_add(&COL(int64_t, B_BR)[p[2]], (int64_t)delta);
-    // history row: every deposit commits, so row = position (sharded: among home deposits)
-    const uint64_t r = db.ins_base[0] + (sh ? db.ins_off[idx] : idx);
+    // history row: deposits always commit; the row is the deposit's position among the bulk's
+    // (home) deposits -- WITHDRAWs insert nothing (ingest counts, exclusive scan)
+    (void)sh;
+    const uint64_t r = db.ins_base[0] + db.ins_off[idx];
     INS(uint32_t, IB_TID)[r] = p[1];
     INS(uint32_t, IB_BID)[r] = p[2];
     INS(uint32_t, IB_AID)[r] = p[0];
@@ -238,6 +253,40 @@ DEV void tpcb_account(const DevDb& db, uint32_t idx, const uint32_t* p) {
     const int64_t v = ldm(&acc[p[0]]) + (int32_t)p[3];
     stm(&acc[p[0]], v);
     reinterpret_cast<int64_t*>(db.out)[idx] = v;
+}
+
+// WITHDRAW (TPC-B type 1): NON-two-phase on purpose --
+// it debits account, teller and branch and only then checks that the account did not go
+// negative; an abort rolls its own updates back from the undo log.  Every strategy runs
+// it with the items held exclusively (k-set round, PART partition, TPL locks held through
+// the rollback), so no other transaction saw the dirty values and the recovery affects
+// the transaction alone (DESIGN.md R-U1).
+DEV void undo_apply(const DevDb& db, const UndoRec* log, int nl) {
+    for (int j = nl - 1; j >= 0; --j) {
+        int64_t* c = reinterpret_cast<int64_t*>(db.col[log[j].col]);
+        if (log[j].kind == UNDO_RESTORE) stm(&c[log[j].row], log[j].val);
+        else red_add(&c[log[j].row], log[j].val);
+    }
+}
+DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p) {
+    UndoRec* log = db.undo + (uint64_t)idx * UNDO_SLOTS;
+    const int64_t amt = (int32_t)p[3];
+    int64_t* acc = COL(int64_t, B_ACC);
+    const int64_t a0 = ldm(&acc[p[0]]);
+    log[0] = {B_ACC, UNDO_RESTORE, p[0], a0};          // log first, then update
+    stm(&acc[p[0]], a0 - amt);
+    log[1] = {B_TEL, UNDO_ADD, p[1], amt};
+    red_add(&COL(int64_t, B_TEL)[p[1]], -amt);
+    log[2] = {B_BR, UNDO_ADD, p[2], amt};
+    red_add(&COL(int64_t, B_BR)[p[2]], -amt);
+    const int64_t a1 = ldm(&acc[p[0]]);                // the check reads the updated row
+    if (a1 < 0) {
+        undo_apply(db, log, UNDO_SLOTS);
+        db.status[idx] = 1;
+        reinterpret_cast<int64_t*>(db.out)[idx] = 0;   // (TPC-B output records are not pre-zeroed)
+        return;
+    }
+    reinterpret_cast<int64_t*>(db.out)[idx] = a1;
 }
 
 // ---- TM-1 --------------------------------------------------------------------------
@@ -768,6 +817,7 @@ template <int S, bool SH = false>
 DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     if (SH && db.xflag && db.xflag[idx]) { exec_local<S>(db, idx); return; }
     if (S == S_TPCB) {
+        if (t == 1) { tpcb_withdraw(db, idx, p); return; }
         tpcb_home(db, idx, p, SH);
         tpcb_account(db, idx, p);
     } else if (S == S_TM1) {
@@ -802,7 +852,7 @@ DEV int fragments(const DevDb& db, uint32_t idx, uint64_t* out) {
     const uint32_t* p = db.pw + db.poff[idx];
     if (S == S_TPCB) {
         const uint32_t home = p[2], own = p[0] / db.dims[2];
-        if (home == own) { if (out) out[0] = frag_key(home, idx, F_WHOLE); return 1; }
+        if (home == own || t == 1) { if (out) out[0] = frag_key(home, idx, F_WHOLE); return 1; }
         if (out) { out[0] = frag_key(home, idx, F_HOME); out[1] = frag_key(own, idx, F_REMOTE); }
         return 2;
     } else if (S == S_TM1) {
@@ -844,6 +894,7 @@ DEV void exec_frag(const DevDb& db, uint64_t fk) {
     const bool sh = db.ts != nullptr;
     const uint32_t* p = db.pw + db.poff[idx];
     if (S == S_TPCB) {
+        if (t == 1) { tpcb_withdraw(db, idx, p); return; }
         if (kind != F_REMOTE) tpcb_home(db, idx, p, sh);
         if (kind != F_HOME) tpcb_account(db, idx, p);
     } else if (S == S_TM1) {

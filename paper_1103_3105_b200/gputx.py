@@ -13,9 +13,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(HERE, "libgputx.so")
 
-GPUTX_TPL, GPUTX_PART, GPUTX_KSET, GPUTX_AUTO = 0, 1, 2, 3
-TPL, PART, KSET, AUTO = "tpl", "part", "kset", "auto"
-STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET, AUTO: GPUTX_AUTO}
+GPUTX_TPL, GPUTX_PART, GPUTX_KSET, GPUTX_AUTO, GPUTX_TPL_RELAXED, GPUTX_PART_RELAXED = 0, 1, 2, 3, 4, 5
+TPL, PART, KSET, AUTO, TPL_RELAXED, PART_RELAXED = "tpl", "part", "kset", "auto", "tpl_relaxed", "part_relaxed"
+STRATEGIES = {TPL: GPUTX_TPL, PART: GPUTX_PART, KSET: GPUTX_KSET, AUTO: GPUTX_AUTO, TPL_RELAXED: GPUTX_TPL_RELAXED,
+              PART_RELAXED: GPUTX_PART_RELAXED}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_TYPE", 5: "ESTATE",
                 6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
@@ -30,11 +31,32 @@ class GputxError(RuntimeError):
         self.name = STATUS_NAMES.get(status, str(status))
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Config(ctypes.Structure):
     _fields_ = [("schema", ctypes.c_int), ("dims", ctypes.c_uint32 * 4), ("max_bulk", ctypes.c_uint64),
                 ("insert_capacity", ctypes.c_uint64), ("part_size", ctypes.c_uint32), ("device", ctypes.c_int),
                 ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint32), ("shard", ctypes.c_uint32),
-                ("nshards", ctypes.c_uint32)]
+                ("nshards", ctypes.c_uint32), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
+
+
+def torch_allocator(device: int):
+    """(alloc, free) callbacks routing the engine's device memory through PyTorch's caching
+    allocator (include/gputx.h gputx_alloc_fn) -- memory plumbing only."""
+    import torch
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream or None)
+        except Exception:
+            return None
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 class BulkC(ctypes.Structure):
@@ -84,6 +106,8 @@ def load_library():
         "gputx_pool_step": ([P, P, P], I),
         "gputx_pool_read": ([P, P, P, P, U64, P], I),
         "gputx_pool_pending": ([P, P], I),
+        "gputx_read_serial_order": ([P, P, U64], I),
+        "gputx_snapshot": ([P, P, P], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
@@ -123,7 +147,8 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_set_launch", "gputx_set_chooser", "gputx_trace_rounds", "gputx_read_round_ns",
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
             "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping",
-            "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending"]
+            "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending",
+            "gputx_read_serial_order", "gputx_snapshot"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -149,7 +174,7 @@ class Database:
 
     def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
                  device: int = 0, stream: int | None = None, insert_capacity: int = 0, shard: int = 0,
-                 nshards: int = 1, add_rule: bool = False):
+                 nshards: int = 1, add_rule: bool = False, torch_memory: bool = False):
         self.lib = load_library()
         self.schema = schema
         cfg = Config()
@@ -164,6 +189,9 @@ class Database:
         cfg.flags = FLAG_ADD_RULE if add_rule else 0
         cfg.shard = int(shard)
         cfg.nshards = int(nshards)
+        if torch_memory:                     # device memory from PyTorch's caching allocator
+            self._alloc_cbs = torch_allocator(int(device))
+            cfg.alloc, cfg.free = self._alloc_cbs
         self.shard, self.nshards, self.device = int(shard), int(nshards), int(device)
         self._bufs = {}
         h = ctypes.c_void_p()
@@ -313,6 +341,50 @@ class Database:
         self._check(self.lib.gputx_pool_read(self.h, _ptr(ts), _ptr(st), _ptr(out), k, ctypes.byref(n)), self.h)
         m = n.value
         return ts[:m], st[:m], out[:m]
+
+    def snapshot(self) -> dict:
+        """The current database via gputx_snapshot: {"columns": {name: bytes-view array},
+        "tables": {table: {column: u32 array}}} (parsed from the documented layout)."""
+        need = ctypes.c_uint64()
+        self._check(self.lib.gputx_snapshot(self.h, None, ctypes.byref(need)), self.h)
+        buf = np.zeros(need.value, np.uint8)
+        self._check(self.lib.gputx_snapshot(self.h, _ptr(buf), ctypes.byref(need)), self.h)
+        o = 0
+
+        def take(k):
+            nonlocal o
+            v = buf[o:o + k]
+            o += k
+            return v
+
+        def u32():
+            return int(take(4).view(np.uint32)[0])
+
+        def u64():
+            return int(take(8).view(np.uint64)[0])
+
+        assert bytes(take(8)) == b"GPTXSNAP" and u32() == 1
+        res = {"schema": u32(), "dims": [u32() for _ in range(4)], "columns": {}, "tables": {}}
+        ncols, ntab = u32(), u32()
+        for _ in range(ncols):
+            name = bytes(take(u32())).decode()
+            el, cnt = u32(), u64()
+            res["columns"][name] = take(el * cnt).copy()
+        for _ in range(ntab):
+            tname = bytes(take(u32())).decode()
+            nc, rows = u32(), u64()
+            res["tables"][tname] = {}
+            for _ in range(nc):
+                cname = bytes(take(u32())).decode()
+                res["tables"][tname][cname] = take(rows * 4).copy().view(np.uint32)
+        assert o == need.value
+        return res
+
+    def serial_order(self) -> np.ndarray:
+        """The serialization order of the last relaxed-strategy execute (u32[n])."""
+        a = np.zeros(max(self.n, 1), np.uint32)
+        self._check(self.lib.gputx_read_serial_order(self.h, _ptr(a), self.n), self.h)
+        return a[:self.n]
 
     def pool_pending(self) -> int:
         n = ctypes.c_uint64()

@@ -1,0 +1,45 @@
+"""Boundary features of SURVEY.md §8(b): device memory through the caller's allocator
+(cfg.alloc / cfg.free = PyTorch's caching allocator) and gputx_snapshot."""
+import numpy as np
+import pytest
+
+import workloads as W
+from tests.parity import gpu_db, run_both
+
+pytestmark = pytest.mark.gpu
+
+
+def test_torch_caching_allocator_hooks():
+    import torch
+    dims = W.TpccDims(2, 10, 300, 2000)
+    image = W.tpcc_db(dims, seed=1)
+    bulk = W.tpcc_bulk(dims, 3000, seed=2)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated(0)
+    db = gpu_db(W.TPCC, dims, image, bulk.n, torch_memory=True)
+    held = torch.cuda.memory_allocated(0) - before
+    assert held > 10 << 20                      # the engine's buffers live in torch's pool
+    for s in ("kset", "tpl", "part"):
+        db.reset()
+        run_both(W.TPCC, dims, image, [bulk], s, db=db)
+    db.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(0) - before < (1 << 20)   # all of it returned
+
+
+def test_snapshot_matches_columns_and_inserts():
+    dims = W.TpcbDims(4, 10, 1000)
+    image = W.tpcb_db(dims)
+    bulk = W.tpcb_bulk(dims, 5000, seed=3, withdraw_pct=20.0)
+    db = gpu_db(W.TPCB, dims, image, bulk.n)
+    db.submit(bulk)
+    db.execute("kset")
+    snap = db.snapshot()
+    assert snap["schema"] == W.TPCB and snap["dims"] == list(dims.dims)
+    got = db.read_image(image)
+    for k in image:
+        assert np.array_equal(snap["columns"][k].view(image[k].dtype), got[k].reshape(-1)), k
+    ins = db.inserts()
+    for c, a in ins["history"].items():
+        assert np.array_equal(snap["tables"]["history"][c], a.view(np.uint32)), c
+    db.close()

@@ -360,3 +360,39 @@ def test_tpcb_add_rule_depth_closed_form():
     # without the rule every deposit of a branch is one chain (depth >= branch position)
     d0 = oracle.depths(W.TPCB, dims.dims, image, bulk)
     assert d0.max() > 1000 and d.max() < 200
+
+
+def test_tpcb_withdraw_non_two_phase_by_projection():
+    """WITHDRAW (type 1, NEXT-4 / PAPER.md:441-443) debits first and aborts afterwards if
+    the account went negative; its undo must leave no trace.  Per-account projection: a
+    withdrawal commits iff the balance before it covers the amount; teller and branch
+    balances are the sums of committed signed amounts; Sum A = Sum T = Sum B; only
+    deposits add history rows."""
+    dims = W.TpcbDims(4, 3, 40)
+    db = W.tpcb_db(dims)
+    b = W.tpcb_bulk(dims, 6000, seed=9, remote_pct=20.0, withdraw_pct=45.0)
+    r = oracle.run(W.TPCB, dims.dims, db, b)
+    p = b.param_words.reshape(-1, 4).astype(np.int64)
+    amt = p[:, 3].astype(np.uint32).view(np.int32).astype(np.int64)
+    acc = np.zeros(dims.branches * dims.accounts_per_branch, np.int64)
+    tel = np.zeros(dims.branches * dims.tellers_per_branch, np.int64)
+    br = np.zeros(dims.branches, np.int64)
+    aborts = 0
+    for i in range(b.n):
+        a, t, bb = p[i, 0], p[i, 1], p[i, 2]
+        if b.type[i] == W.TPCB_WITHDRAW:
+            assert a // dims.accounts_per_branch == bb                 # always a local account
+            if acc[a] >= amt[i]:
+                acc[a] -= amt[i]; tel[t] -= amt[i]; br[bb] -= amt[i]
+                assert r.status[i] == 0 and r.out[i].view(np.int64)[0] == acc[a]
+            else:
+                aborts += 1
+                assert r.status[i] == 1 and not r.out[i].any()
+        else:
+            acc[a] += amt[i]; tel[t] += amt[i]; br[bb] += amt[i]
+            assert r.status[i] == 0 and r.out[i].view(np.int64)[0] == acc[a]
+    assert np.array_equal(r.db["acc_bal"], acc) and np.array_equal(r.db["tel_bal"], tel)
+    assert np.array_equal(r.db["br_bal"], br)
+    assert acc.sum() == tel.sum() == br.sum()
+    assert len(r.inserts["history"]["h_ts"]) == int((b.type == 0).sum())
+    assert 100 < aborts < int((b.type == 1).sum())

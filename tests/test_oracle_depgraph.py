@@ -182,3 +182,28 @@ def test_add_rule_special_cases():
     assert _streaming([[("x", "A")]] * 6) == [0] * 6
     assert _streaming([[("x", "A")], [("x", "A")], [("x", "R")], [("x", "R")], [("x", "A")]]) == [0, 0, 1, 1, 2]
     assert _streaming([[("x", "A")], [("x", "A")], [("x", "W")], [("x", "A")]]) == [0, 0, 1, 2]
+
+
+def test_run_order_matches_one_at_a_time_replay():
+    """orc_run_order (the witness replay of the relaxed strategies) equals
+    executing the transactions one at a time in that order (run_sequence), and with the
+    identity order equals Definition 1."""
+    import numpy as np
+    import oracle
+    import workloads as W
+    for schema, dims, kw in [(W.TPCB, W.TpcbDims(2, 2, 5), dict(remote_pct=30.0)), (W.TM1, W.Tm1Dims(4), {}),
+                             (W.TPCC, W.TpccDims(2, 2, 3, 4), dict(rbk_pct=10.0)), (W.MICRO, W.MicroDims(5, 4, 1), {})]:
+        db = W.make_db(schema, dims, seed=2)
+        bulk = W.make_bulk(schema, dims, 40, 3, **kw)
+        order = np.random.default_rng(1).permutation(bulk.n)
+        a = oracle.run(schema, dims.dims, db, bulk, order=order)
+        b = oracle.run_sequence(schema, dims.dims, db, bulk, order)
+        for k in a.db:
+            assert np.array_equal(a.db[k], b.db[k]), (schema, k)
+        assert np.array_equal(a.status, b.status) and np.array_equal(a.out, b.out)
+        for t in a.inserts:
+            for c in a.inserts[t]:
+                assert np.array_equal(a.inserts[t][c], b.inserts[t][c]), (schema, t, c)
+        ident = oracle.run(schema, dims.dims, db, bulk, order=np.arange(bulk.n))
+        ref = oracle.run(schema, dims.dims, db, bulk)
+        assert np.array_equal(ident.out, ref.out) and all(np.array_equal(ident.db[k], ref.db[k]) for k in ref.db)

@@ -151,9 +151,17 @@ def tpcb_db(dims: TpcbDims) -> dict[str, np.ndarray]:
     }
 
 
+TPCB_WITHDRAW = 1
+
+
 def tpcb_bulk(dims: TpcbDims, n: int, seed: int, remote_pct: float = 15.0,
-              alpha: float = 0.0, zipf_theta: float = 0.0, home_range: tuple | None = None) -> Bulk:
+              alpha: float = 0.0, zipf_theta: float = 0.0, home_range: tuple | None = None,
+              withdraw_pct: float = 0.0) -> Bulk:
     """n deposit transactions, params [aid, tid, bid, delta(i32 as u32)].
+
+    withdraw_pct > 0: that share are WITHDRAW [aid, tid, bid, amount] (type 1, SURVEY.md
+    NEXT-4 / PAPER.md:441-443: a NON-two-phase type -- it debits, then aborts if the account
+    went negative; always a local account), amount uniform in [1, 999999] cents.
 
     Branch: hot-branch alpha model (branch 0 w.p. alpha, else uniform)
     or Zipf(theta) over branches; teller uniform within the branch; account in the
@@ -179,9 +187,17 @@ def tpcb_bulk(dims: TpcbDims, n: int, seed: int, remote_pct: float = 15.0,
         abr = np.where(remote, other, bid)
     aid = abr * A + rng.integers(0, A, size=n, dtype=np.int64)
     delta = rng.integers(-999_999, 1_000_000, size=n, dtype=np.int64)
+    types = np.zeros(n, np.uint8)
+    if withdraw_pct > 0:
+        rw = _rng(seed, 0xBD)
+        wd = rw.random(n) < withdraw_pct / 100.0
+        types[wd] = TPCB_WITHDRAW
+        aid = np.where(wd, bid * A + rw.integers(0, A, size=n, dtype=np.int64), aid)
+        delta = np.where(wd, rw.integers(1, 1_000_000, size=n, dtype=np.int64), delta)
     fixed = np.stack([aid, tid, bid, delta.astype(np.int32).view(np.uint32).astype(np.int64)], axis=1)
-    b = _pack(TPCB, np.zeros(n, np.uint8), fixed=fixed.astype(np.uint32))
-    b.meta = dict(dims=dims.dims, seed=seed, remote_pct=remote_pct, alpha=alpha, zipf=zipf_theta)
+    b = _pack(TPCB, types, fixed=fixed.astype(np.uint32))
+    b.meta = dict(dims=dims.dims, seed=seed, remote_pct=remote_pct, alpha=alpha, zipf=zipf_theta,
+                  withdraw_pct=withdraw_pct)
     return b
 
 

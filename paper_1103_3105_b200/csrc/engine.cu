@@ -233,6 +233,13 @@ gputx_status fail(gputx_db* db, gputx_status s, const std::string& m) {
     return s;
 }
 
+// the first bad transaction of the last validating kernel and its error code (report_err)
+uint64_t err_packed(const gputx_db* db) {
+    return (uint64_t)db->h_sc[SC_ERRPK] | ((uint64_t)db->h_sc[SC_ERRPK + 1] << 32);
+}
+uint32_t err_code(const gputx_db* db) { return (uint32_t)(err_packed(db) & 0xFFu); }
+uint32_t err_idx(const gputx_db* db) { return (uint32_t)(err_packed(db) >> 8); }
+
 template <class T>
 gputx_status dalloc(gputx_db* db, T** p, uint64_t count) {
     *p = nullptr;
@@ -762,7 +769,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     db->has_depth = db->has_perm = false;
     db->executed = false;
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
     const bool ins_scan = db->schema == S_TPCC || db->schema == S_TPCB || db->has_ts;
     const int ntab = db->schema == S_TPCC ? 4 : 1;
     if (n) {
@@ -791,11 +798,11 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
         static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
                                      "parameter out of range", "bad param_off", "timestamps not increasing",
                                      "home partition not owned by this shard", "too many parameter words"};
-        const uint32_t e = db->h_sc[SC_ERR];
+        const uint32_t e = err_code(db);
         db->n = 0;
         if (e == E_WORDS) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
         return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : e == E_OWNER ? GPUTX_ECROSS : GPUTX_EINVAL,
-                    std::string("transaction ") + std::to_string(db->h_sc[SC_BADIDX]) + ": " + what[e < 9 ? e : 0]);
+                    std::string("transaction ") + std::to_string(err_idx(db)) + ": " + what[e < 9 ? e : 0]);
     }
     // insert rows this bulk will append (decisions are static: two-phase procedures)
     for (auto& t : db->ins) {
@@ -840,7 +847,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     const uint32_t ntab = (uint32_t)db->ins.size();
     // 1. ingest the arrivals in the staging area (validation, split lookups, insert counts)
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
     if (ntab) CK(cudaMemsetAsync(db->st_ins, 0, 4 * (m + 1) * ntab, s));
     DevDb v = make_devdb(db);
     v.n = (uint32_t)m;
@@ -854,9 +861,9 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
-        return fail(db, db->h_sc[SC_ERR] <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
-                    "pool arrival " + std::to_string(db->h_sc[SC_BADIDX]) + " rejected (code " +
-                        std::to_string(db->h_sc[SC_ERR]) + ")");
+        return fail(db, err_code(db) <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
+                    "pool arrival " + std::to_string(err_idx(db)) + " rejected (code " +
+                        std::to_string(err_code(db)) + ")");
     // 2. append to the pool with timestamps next_ts + i
     const uint32_t n0 = (uint32_t)db->pool_n;
     pool_append_kernel<<<g, 256, 0, s>>>(db->s_type, db->s_poff, db->s_pw, db->st_ins, (uint32_t)m, n0,
@@ -1448,6 +1455,8 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
         CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
         const DevDb v = make_devdb(db);
         const uint32_t g = grid_for(n, 256, 148 * 8);
+        CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+        shard_validate_kernel<<<g, 256, 0, s>>>(db->s_poff, (uint32_t)n, n_words, stride - 3, db->d_sc);
         if (db->schema == S_TPCB) shard_count_kernel<S_TPCB><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
         else if (db->schema == S_TM1) shard_count_kernel<S_TM1><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
         else shard_count_kernel<S_TPCC><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
@@ -1461,6 +1470,8 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
                                                bits_for(db->nshards - 1), db->sort_ws, db->epoch, s);
         CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (db->h_sc[SC_ERR])
+            return fail(db, GPUTX_EINVAL, "home transaction " + std::to_string(err_idx(db)) + ": bad param_off");
         const uint64_t np = db->h_sc[SC_XTOTAL];
         for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
         if (np > send_cap) return fail(db, GPUTX_ECAPACITY, "send buffer holds " + std::to_string(send_cap) +
@@ -1502,7 +1513,8 @@ gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_r
         merge_meta_kernel<<<g, 256, 0, s>>>(keys, nn, nh, db->s_type, db->s_poff, db->s_ts, recv, stride, db->d_type,
                                             db->d_ts, db->d_src, db->d_home_pos, db->d_cnt);
         scan_u32(db, db->d_cnt, db->d_poff, nullptr, n, db->d_sc + SC_XTOTAL);
-        merge_params_kernel<<<g, 256, 0, s>>>(keys, nn, nh, db->s_poff, db->s_pw, recv, stride, db->d_poff, db->d_pw);
+        merge_params_kernel<<<g, 256, 0, s>>>(keys, nn, nh, db->s_poff, db->s_pw, recv, stride, db->d_poff, db->d_pw,
+                                              (uint32_t)db->max_words);
         db->launches += 4 + 4;
         CK(cudaMemcpyAsync(&n_words, db->d_sc + SC_XTOTAL, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1560,7 +1572,7 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
     if (n_recv && !recv) return GPUTX_EINVAL;
     cudaStream_t s = db->stream;
     CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_BADIDX, 0xFF, 4, s));
+    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
     if (n_recv) {
         ret_merge_kernel<<<grid_for(n_recv, 256, 148 * 8), 256, 0, s>>>(recv, (uint32_t)n_recv, db->out_stride / 4,
                                                                          db->d_ts, db->d_src, (uint32_t)db->n,
@@ -1574,7 +1586,7 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
-        return fail(db, GPUTX_EINVAL, "returned result " + std::to_string(db->h_sc[SC_BADIDX]) +
+        return fail(db, GPUTX_EINVAL, "returned result " + std::to_string(err_idx(db)) +
                                           " matches no home transaction");
     db->returned = true;
     return GPUTX_OK;

@@ -25,6 +25,7 @@ enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_O
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
 constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested cluster shape (counter hand-offs used)
+constexpr int SC_ERRPK = 34;      // [34, 36): u64 (first bad idx << 8 | its code); all-ones = none
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -32,9 +33,12 @@ __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
     return x;
 }
 
+// The first bad transaction and ITS error code, packed (idx << 8 | code) in one 64-bit
+// word so that one atomicMin keeps them together (separate min/max words paired
+// the lowest index with another transaction's code); SC_ERR flags "some error".
 DEV void report_err(uint32_t* sc, uint32_t code, uint32_t idx) {
-    atomicMin(&sc[SC_BADIDX], idx);
-    atomicMax(&sc[SC_ERR], code);
+    atomicMin(reinterpret_cast<unsigned long long*>(&sc[SC_ERRPK]), ((unsigned long long)idx << 8) | code);
+    atomicOr(&sc[SC_ERR], 1u);
 }
 
 // =====================================================================================
@@ -1761,19 +1765,38 @@ DEV uint32_t dest_mask(const DevDb& db, uint32_t t, const uint32_t* p, uint32_t 
     return m & ~(1u << db.shard);
 }
 
+// the caller's home-bulk offsets, checked before anything is read through them:
+// param_off[0] == 0, non-decreasing, at most maxlen words per transaction, param_off[nh] ==
+// the word count; a violation reports E_OFF at the first bad transaction
+__global__ void __launch_bounds__(256) shard_validate_kernel(const uint32_t* poff, uint32_t nh, uint32_t n_words,
+                                                             uint32_t maxlen, uint32_t* sc) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const uint32_t o0 = poff[i], o1 = poff[i + 1];
+        if ((i == 0 && o0 != 0) || o1 < o0 || o1 - o0 > maxlen || o1 > n_words || (i == nh - 1 && o1 != n_words))
+            report_err(sc, E_OFF, i);
+    }
+}
+// a transaction's word count as the shard kernels read it: clamped to the record stride
+DEV uint32_t shard_len(const uint32_t* poff, uint32_t i, uint32_t maxlen) {
+    const uint32_t o0 = poff[i], o1 = poff[i + 1];
+    return o1 < o0 ? 0u : min(o1 - o0, maxlen);
+}
+
 template <int S>
 __global__ void __launch_bounds__(256) shard_count_kernel(DevDb db, const uint8_t* type, const uint32_t* poff,
                                                           const uint32_t* pw, uint32_t nh, uint32_t* cnt) {
+    const uint32_t maxlen = S == S_TPCB ? 4u : S == S_TM1 ? 7u : 49u;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x)
-        cnt[i] = __popc(dest_mask<S>(db, type[i], pw + poff[i], poff[i + 1] - poff[i]));
+        cnt[i] = __popc(dest_mask<S>(db, type[i], pw + poff[i], shard_len(poff, i, maxlen)));
 }
 
 template <int S>
 __global__ void __launch_bounds__(256) shard_pair_kernel(DevDb db, const uint8_t* type, const uint32_t* poff,
                                                          const uint32_t* pw, uint32_t nh, const uint32_t* off,
                                                          uint64_t* pairs, uint32_t* sc) {
+    const uint32_t maxlen = S == S_TPCB ? 4u : S == S_TM1 ? 7u : 49u;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
-        uint32_t m = dest_mask<S>(db, type[i], pw + poff[i], poff[i + 1] - poff[i]);
+        uint32_t m = dest_mask<S>(db, type[i], pw + poff[i], shard_len(poff, i, maxlen));
         uint32_t o = off[i];
         while (m) {
             const uint32_t q = __ffs(m) - 1;
@@ -1790,7 +1813,7 @@ __global__ void __launch_bounds__(256) shard_pack_kernel(const uint64_t* pairs, 
     const uint32_t np = *npairs;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < np; k += gridDim.x * blockDim.x) {
         const uint32_t i = (uint32_t)pairs[k];
-        const uint32_t o0 = poff[i], len = min(poff[i + 1] - o0, stride - 3);
+        const uint32_t o0 = poff[i], len = shard_len(poff, i, stride - 3);
         uint32_t* r = send + (uint64_t)k * stride;
         r[0] = ts[i];
         r[1] = type[i];
@@ -1818,7 +1841,7 @@ __global__ void __launch_bounds__(256) merge_meta_kernel(const uint64_t* keys, u
         if (s < nh) {
             type[k] = htype[s];
             ts[k] = hts[s];
-            len[k] = hpoff[s + 1] - hpoff[s];
+            len[k] = shard_len(hpoff, s, stride - 3);
             src[k] = s;
             home_pos[s] = k;
         } else {
@@ -1834,12 +1857,13 @@ __global__ void __launch_bounds__(256) merge_meta_kernel(const uint64_t* keys, u
 __global__ void __launch_bounds__(256) merge_params_kernel(const uint64_t* keys, uint32_t n, uint32_t nh,
                                                            const uint32_t* hpoff, const uint32_t* hpw,
                                                            const uint32_t* recv, uint32_t stride, const uint32_t* poff,
-                                                           uint32_t* pw) {
+                                                           uint32_t* pw, uint32_t max_words) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint32_t s = (uint32_t)keys[k];
         const uint32_t o = poff[k], len = poff[k + 1] - o;
         const uint32_t* from = s < nh ? hpw + hpoff[s] : recv + (uint64_t)(s - nh) * stride + 3;
-        for (uint32_t w = 0; w < len; ++w) pw[o + w] = from[w];
+        // writes are bounded by the buffer (the host then rejects n_words > max_words)
+        for (uint32_t w = 0; w < len && o + w < max_words; ++w) pw[o + w] = from[w];
     }
 }
 

@@ -98,3 +98,28 @@ def test_auto_sharded(schema, dims, n, kw):
     bulk = W.make_bulk(schema, dims, n, 9, **kw)
     stats = _run(schema, dims, image, bulk, 2, "auto")
     assert all(s["strategy"] in ("kset", "part", "tpl") for s in stats)
+
+
+@pytest.mark.parametrize("bad", ["nonmonotone", "toolong", "firstoff"])
+def test_shard_pack_rejects_malformed_offsets(bad):
+    """a malformed home bulk must be rejected (EINVAL) before any kernel reads
+    or writes through its offsets -- no out-of-bounds merge of parameter words."""
+    from paper_1103_3105_b200 import Database
+    from paper_1103_3105_b200.gputx import GputxError
+    dims = W.TpccDims(4, 10, 30, 500)
+    image = W.tpcc_db(dims, seed=1)
+    bulk = W.tpcc_bulk(dims, 400, seed=2)
+    home = W.split_home(bulk, dims, 2)[0]
+    off = home.param_off.astype(np.int64).copy()
+    if bad == "nonmonotone":
+        off[5] = off[7] + 3
+    elif bad == "toolong":
+        off[6] = off[5] + 50              # > 49 words (the TPC-C maximum) for transaction 5
+    else:
+        off[0] = 1                        # param_off[0] must be 0
+    home.param_off = off.astype(np.uint32)
+    db = Database(W.TPCC, dims.dims, bulk.n, image, shard=0, nshards=2)
+    with pytest.raises(GputxError) as e:
+        db.shard_pack(home)
+    assert e.value.name in ("EINVAL", "ECAPACITY")
+    db.close()

@@ -199,6 +199,17 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* bulk, uint64_t* f
  * default 10 s: the handle is poisoned until gputx_reset), ECAPACITY (insert table full), ECUDA. */
 gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* stats);
 
+/* A stream of k HOST bulks executed back to back with the transfers overlapped: bulk i+1's
+ * H2D copy and bulk i-1's D2H of results run on two copy streams while bulk i executes
+ * (double-buffered device slots).  Equivalent to k x (gputx_submit_bulk + gputx_execute +
+ * gputx_read_results) -- same results, same errors (the first failing bulk stops the run);
+ * the paper counts the transfers in the bulk time and keeps them below 5% (PAPER.md:449,
+ * 515).  status[i] (u8[n_i]) and out[i] (n_i * gputx_out_stride) are caller-owned host
+ * buffers (pinned for real overlap; entries may be NULL); stats: k entries or NULL.
+ * Returns after the last result has landed; every bulk takes ts = next_ts + position. */
+gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, gputx_strategy strategy,
+                             uint8_t* const* status, void* const* out, gputx_stats* stats);
+
 /* Thresholds of the strategy chooser, Algorithm 1 (Appendix D
  * "Choosing the suitable execution strategy").  GPUTX_AUTO first builds the
  * T-dependency graph's structural parameters of the submitted bulk:

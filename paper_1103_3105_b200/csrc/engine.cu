@@ -135,6 +135,18 @@ struct gputx_db {
     uint64_t* d_rec_a = nullptr;
     uint64_t* d_rec_b = nullptr;
     uint64_t* d_sorted = nullptr;
+    uint64_t* d_item_sorted = nullptr;  // records in (item, ts) order after the K-SET sort (or null)
+    int kset_df = -1;                   // K-SET executor: 1 dataflow, 0 rounds, -1 schema default
+    bool kset_ran_df = false;
+    bool ins_dense = false;
+    // gputx_run_bulks: copy streams and double-buffered device slots (lazily created)
+    cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_res[2] = {}, ev_res_free[2] = {};
+    uint8_t* in_type[2] = {};
+    uint32_t *in_poff[2] = {}, *in_pw[2] = {};
+    uint8_t *res_status[2] = {}, *res_out[2] = {};
+    uint32_t kset_df_ahead = 0;         // dataflow look-ahead throttle in k-sets, 0 = off (GPUTX_KSET_DF_AHEAD)
+    uint32_t kset_df_grid = 0;          // dataflow persistent grid cap (GPUTX_KSET_DF_GRID), 0 = co-resident
     uint32_t* d_cnt = nullptr;       // max(max_bulk, max_rec) + 1
     uint32_t* d_rec_off = nullptr;   // max_bulk + 1
     uint32_t* d_D = nullptr;
@@ -333,6 +345,7 @@ DevDb make_devdb(gputx_db* db) {
     v.src = db->nshards > 1 ? db->d_src : nullptr;
     v.xflag = db->nshards > 1 ? db->d_xflag : nullptr;
     v.undo = db->d_undo;
+    v.ins_dense = db->ins_dense ? 1u : 0u;
     return v;
 }
 
@@ -404,11 +417,15 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
                          db->max_rec));
     else
         TRY(sort_records(db, KEY_ITEM_SHIFT, db->item_bits, db->d_sc + SC_NREC, db->max_rec));
+    db->d_item_sorted = stream ? nullptr : db->d_sorted;   // (item, ts) order (TPL keys / K-SET dataflow)
     if (windowed) {
         uint64_t* other = db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a;
         db->d_sorted = radix_sort_u64(db->d_sorted, other, db->d_sc + SC_NREC, db->max_rec, 6 + wb, bits_for(nwin - 1),
                                       db->sort_ws, db->epoch, s);
         db->launches += 2 + (bits_for(nwin - 1) + 7) / 8;
+        // one 8-bit pass reads the item-sorted buffer and writes the other: the item order
+        // survives for the dataflow executor (more passes would overwrite it)
+        if ((bits_for(nwin - 1) + 7) / 8 != 1) db->d_item_sorted = nullptr;
     }
     db->rec_item_sorted = !stream && !windowed;
     STAGE("sort");
@@ -488,6 +505,16 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     return GPUTX_OK;
 }
 
+template <int S>
+bool kset_use_dataflow(const gputx_db* db) {
+    if (S == S_TM1) return false;       // records sorted by item component, not by item
+    if (db->kset_df >= 0) return db->kset_df != 0;
+    // measured (profiles/round2_kset_dataflow.txt): TPC-C exec 34.1 -> 23.5 ms (its long
+    // W_YTD / D_NEXT_O_ID chains with ~125-transaction k-sets); TPC-B rounds 13.9 vs dataflow
+    // >= 33.7 ms (1,000 hot branch chains, 3 locks per hop); micro/TM-1: rounds
+    return S == S_TPCC;
+}
+
 // K-SET part 2: group by (depth, type), then the k-set rounds
 template <int S>
 gputx_status kset_exec(gputx_db* db, const DevDb& v) {
@@ -509,8 +536,42 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     ++db->launches;
     STAGE("group");
     cudaEventRecord(db->ev[5], s);
+    // K-SET dataflow executor (deep graphs: TPC-B / TPC-C / micro under the R/W rule): the
+    // k-sets are executed in k-set order without round barriers -- every transaction waits
+    // only until its own predecessors in the T-dependency graph are done, read from per-item
+    // completion counters keyed by position in the item's ts-ordered access list (the same
+    // keys as TPL, PAPER.md:370-388 / DESIGN.md R-S5); dispatch in perm order makes every
+    // wait point to a transaction of smaller depth, already taken by a running lane.
+    const bool df = kset_use_dataflow<S>(db) && db->d_item_sorted;
+    db->kset_ran_df = df;
+    if (df) {
+        ++db->epoch;
+        tpl_keys_kernel<<<(uint32_t)((db->max_rec + RK_TILE - 1) / RK_TILE) + 1, RK_THREADS, 0, s>>>(
+            db->d_item_sorted, db->d_sc + SC_NREC, db->d_rec_off, db->d_lkey, db->d_lock, db->lb_tpl, db->epoch,
+            next_ticket(db));
+        const bool sh = db->has_ts;
+        // per-k-set completion counters (zeroed by the schedule kernel) for the look-ahead throttle
+        kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, 1, db->kset_q,
+                                                                         db->d_g, db->d_done);
+        DfThrottle thr = db->kset_df_ahead ? DfThrottle{db->d_D, db->d_goff, T, db->kset_df_ahead, db->d_done}
+                                           : DfThrottle{};
+        if (S == S_TPCC) {
+            const uint32_t grid = (uint32_t)((db->n + 3) / 4);
+            if (sh) tpl_exec_warp_kernel<true><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, db->d_perm, thr);
+            else tpl_exec_warp_kernel<false><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, db->d_perm, thr);
+        } else {
+            int per = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tpl_exec_persistent_kernel<S, true>, 256, 0);
+            // resident lanes = the look-ahead of the dispatch (GPUTX_KSET_DF_GRID CTAs of 256)
+            uint32_t grid = std::min<uint64_t>((uint32_t)std::max(1, per) * (uint32_t)db->nsm, (db->n + 255) / 256);
+            if (db->kset_df_grid) grid = std::min(grid, db->kset_df_grid);
+            if (sh) tpl_exec_persistent_kernel<S, true><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, db->d_perm, thr);
+            else tpl_exec_persistent_kernel<S, false><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, db->d_perm, thr);
+        }
+        db->launches += 2;
+    }
     // rounds
-    {
+    if (!df) {
         const uint32_t Gv = (uint32_t)(db->has_ts ? db->kset_grid_ts : db->kset_grid);   // co-resident grid
         uint32_t G = db->exec_grid_override ? std::min(db->exec_grid_override, Gv) : Gv;
         if (db->kset_cluster) G = std::max(db->kset_cluster, G / db->kset_cluster * db->kset_cluster);
@@ -641,12 +702,12 @@ gputx_status run_tpl(gputx_db* db, const DevDb& v, bool sorted = false) {
         int per = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tpl_exec_persistent_kernel<S, true>, 256, 0);
         const uint32_t grid = std::min<uint64_t>((uint32_t)std::max(1, per) * (uint32_t)db->nsm, (db->n + 255) / 256);
-        if (sh) tpl_exec_persistent_kernel<S, true><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
-        else tpl_exec_persistent_kernel<S, false><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        if (sh) tpl_exec_persistent_kernel<S, true><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, nullptr, DfThrottle{});
+        else tpl_exec_persistent_kernel<S, false><<<grid, 256, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, nullptr, DfThrottle{});
     } else if (S == S_TPCC) {                 // one warp per transaction
         const uint32_t grid = (uint32_t)((db->n + 3) / 4);
-        if (sh) tpl_exec_warp_kernel<true><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
-        else tpl_exec_warp_kernel<false><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
+        if (sh) tpl_exec_warp_kernel<true><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, nullptr, DfThrottle{});
+        else tpl_exec_warp_kernel<false><<<grid, 128, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc, nullptr, DfThrottle{});
     } else {
         const uint32_t tb = 128, grid = (uint32_t)((db->n + tb - 1) / tb);
         if (sh) tpl_exec_kernel<S, true><<<grid, tb, 0, s>>>(v, db->d_rec_off, db->d_lkey, db->d_lock, db->d_sc);
@@ -804,6 +865,9 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
         return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : e == E_OWNER ? GPUTX_ECROSS : GPUTX_EINVAL,
                     std::string("transaction ") + std::to_string(err_idx(db)) + ": " + what[e < 9 ? e : 0]);
     }
+    // TPC-B: when every transaction is a home deposit, its history row is its position (no
+    // ins_off load on the executors' critical paths, e.g. PART's serial branch chains)
+    db->ins_dense = db->schema == S_TPCB && !db->h_sc[SC_SPARSE];
     // insert rows this bulk will append (decisions are static: two-phase procedures)
     for (auto& t : db->ins) {
         t.pending = db->h_sc[SC_INS0 + t.table_id];
@@ -924,6 +988,7 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
     CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
     db->n = n;
     db->has_ts = true;
+    db->ins_dense = false;              // pool rows: positions scanned over the executed 0-set
     DevDb v = make_devdb(db);
     pool_exec_kernel<S><<<grid_for(S == S_TPCC ? n * 32 : n, 256, 148 * 8), 256, 0, s>>>(v, db->d_list,
                                                                                        db->d_sc + SC_XTOTAL);
@@ -1217,6 +1282,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // K-SET executor: thread-block clusters of kset_cluster CTAs (rounds of <= that many
     // CTAs are separated by the hardware cluster barrier); 0 disables clusters
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
+    if (const char* e = getenv("GPUTX_KSET_DF")) db->kset_df = atoi(e);
+    if (const char* e = getenv("GPUTX_KSET_DF_AHEAD")) db->kset_df_ahead = (uint32_t)atoi(e);
+    if (const char* e = getenv("GPUTX_KSET_DF_GRID")) db->kset_df_grid = (uint32_t)atoi(e);
     // (sized on the plain variant; the explicit-ts / sharded variant gets the same attributes)
     const void* kfn = schema == S_TPCB ? kset_fn<S_TPCB>(false) : schema == S_TM1 ? kset_fn<S_TM1>(false)
                     : schema == S_MICRO ? kset_fn<S_MICRO>(false)
@@ -1904,6 +1972,86 @@ gputx_status gputx_snapshot(gputx_db* db, void* buf, uint64_t* bytes) {
     return GPUTX_OK;
 }
 
+// ------------------------------------------------------------------ overlapped bulk stream
+gputx_status pipe_alloc(gputx_db* db) {
+    if (db->st_h2d) return GPUTX_OK;
+    CK(cudaStreamCreateWithFlags(&db->st_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&db->st_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        for (cudaEvent_t* e : {&db->ev_in[k], &db->ev_in_free[k], &db->ev_res[k], &db->ev_res_free[k]})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        gputx_status st;
+        if ((st = dalloc(db, &db->in_type[k], db->max_bulk + 1)) || (st = dalloc(db, &db->in_poff[k], db->max_bulk + 1)) ||
+            (st = dalloc(db, &db->in_pw[k], db->max_words + 16)) || (st = dalloc(db, &db->res_status[k], db->max_bulk + 1)) ||
+            (st = dalloc(db, &db->res_out[k], db->max_bulk * db->out_stride + 16)))
+            return st;
+        CK(cudaEventRecord(db->ev_in_free[k], db->stream));
+        CK(cudaEventRecord(db->ev_res_free[k], db->stream));
+    }
+    return GPUTX_OK;
+}
+
+gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, gputx_strategy st,
+                             uint8_t* const* status, void* const* out, gputx_stats* stats) {
+    if (!db || (k && !bulks)) return GPUTX_EINVAL;
+    if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "sharded handles: use the shard calls");
+    for (uint64_t i = 0; i < k; ++i) {
+        if (bulks[i].on_device || bulks[i].ts) return fail(db, GPUTX_EINVAL, "run_bulks takes host bulks without ts");
+        if (bulks[i].n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
+        if (bulks[i].n && bulks[i].param_off[bulks[i].n] > db->max_words)
+            return fail(db, GPUTX_ECAPACITY, "too many parameter words");
+    }
+    TRY(pipe_alloc(db));
+    cudaStream_t s = db->stream;
+    // H2D of bulk i into slot i % 2, once the submit of bulk i - 2 has consumed that slot
+    auto h2d = [&](uint64_t i) -> gputx_status {
+        const gputx_bulk& b = bulks[i];
+        const int sl = (int)(i & 1);
+        CK(cudaStreamWaitEvent(db->st_h2d, db->ev_in_free[sl], 0));
+        if (b.n) {
+            CK(cudaMemcpyAsync(db->in_type[sl], b.type, b.n, cudaMemcpyHostToDevice, db->st_h2d));
+            CK(cudaMemcpyAsync(db->in_poff[sl], b.param_off, (b.n + 1) * 4, cudaMemcpyHostToDevice, db->st_h2d));
+            const uint64_t w = b.param_off[b.n];
+            if (w) CK(cudaMemcpyAsync(db->in_pw[sl], b.param_words, w * 4, cudaMemcpyHostToDevice, db->st_h2d));
+        }
+        CK(cudaEventRecord(db->ev_in[sl], db->st_h2d));
+        return GPUTX_OK;
+    };
+    if (k) TRY(h2d(0));
+    for (uint64_t i = 0; i < k; ++i) {
+        const int sl = (int)(i & 1);
+        if (i + 1 < k) TRY(h2d(i + 1));              // next bulk's copy overlaps this one's execution
+        CK(cudaStreamWaitEvent(s, db->ev_in[sl], 0));
+        gputx_bulk dv = bulks[i];
+        dv.type = db->in_type[sl];
+        dv.param_off = db->in_poff[sl];
+        dv.param_words = db->in_pw[sl];
+        dv.on_device = 1;
+        TRY(gputx_submit_bulk(db, &dv, nullptr));
+        CK(cudaEventRecord(db->ev_in_free[sl], s));
+        TRY(gputx_execute(db, st, stats ? &stats[i] : nullptr));
+        // results: a device copy into the slot (after the D2H of bulk i - 2 left it), then
+        // the D2H on its own stream, overlapping the next bulk's execution
+        const uint64_t n = bulks[i].n;
+        CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
+        if (n) {
+            CK(cudaMemcpyAsync(db->res_status[sl], db->d_status, n, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(db->res_out[sl], db->d_out, n * db->out_stride, cudaMemcpyDeviceToDevice, s));
+        }
+        CK(cudaEventRecord(db->ev_res[sl], s));
+        CK(cudaStreamWaitEvent(db->st_d2h, db->ev_res[sl], 0));
+        if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->res_status[sl], n, cudaMemcpyDeviceToHost, db->st_d2h));
+        if (n && out && out[i])
+            CK(cudaMemcpyAsync(out[i], db->res_out[sl], n * db->out_stride, cudaMemcpyDeviceToHost, db->st_d2h));
+        CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
+    }
+    // the handle's stream is ordered after the last result copy (an event recorded on it
+    // after this call covers the whole run), then wait for it
+    for (int sl = 0; sl < 2; ++sl) CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
+    CK(cudaStreamSynchronize(s));
+    return GPUTX_OK;
+}
+
 gputx_status gputx_read_serial_order(gputx_db* db, uint32_t* host, uint64_t n) {
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_order || n != db->n) return fail(db, GPUTX_ESTATE, "no relaxed-strategy execution of this bulk");
@@ -1985,6 +2133,14 @@ void gputx_close_db(gputx_db* db) {
         if (e) cudaEventDestroy(e);
     for (auto& e : db->ev_x)
         if (e) cudaEventDestroy(e);
+    for (int k = 0; k < 2; ++k) {
+        for (cudaEvent_t e : {db->ev_in[k], db->ev_in_free[k], db->ev_res[k], db->ev_res_free[k]})
+            if (e) cudaEventDestroy(e);
+        dfree(db, db->in_type[k]); dfree(db, db->in_poff[k]); dfree(db, db->in_pw[k]);
+        dfree(db, db->res_status[k]); dfree(db, db->res_out[k]);
+    }
+    if (db->st_h2d) cudaStreamDestroy(db->st_h2d);
+    if (db->st_d2h) cudaStreamDestroy(db->st_d2h);
     if (db->own_stream && db->stream) cudaStreamDestroy(db->stream);
     delete db;
 }

@@ -26,6 +26,7 @@ constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
 constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested cluster shape (counter hand-offs used)
 constexpr int SC_ERRPK = 34;      // [34, 36): u64 (first bad idx << 8 | its code); all-ones = none
+constexpr int SC_SPARSE = 36;     // TPC-B ingest: transactions without a history row (withdrawals, peers')
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -151,7 +152,10 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                 if (p[4] != 2 && home) ins_cnt[T_HIST * ins_stride + i] = 1;
             }
         }
-        if (S == S_TPCB) ins_cnt[i] = (home && t == 0) ? 1u : 0u;   // history rows (deposits) via ins_off
+        if (S == S_TPCB) {                                           // history rows (deposits) via ins_off
+            ins_cnt[i] = (home && t == 0) ? 1u : 0u;
+            if (!(home && t == 0)) atomicAdd(&sc[SC_SPARSE], 1u);       // some row is not at its idx
+        }
         if (db.nshards > 1) {
             // the home root must be this shard's iff the transaction was submitted here
             const uint64_t root = S == S_TPCB ? p[2] : S == S_TPCC ? p[0] : (uint64_t)(p[0] ? p[0] - 1 : db.root_lo);
@@ -2013,6 +2017,34 @@ constexpr uint32_t SPIN_LIMIT = 1u << 24;   // polls before the watchdog trips (
 // no lane waits inside a collective for another lane's release: ITS lets a lane whose
 // lock is free leave, execute and release while its siblings keep polling.
 __device__ uint32_t g_tpl_sleep_cap = 2048;    // ns; GPUTX_TPL_SLEEP overrides (experiments)
+
+// K-SET dataflow look-ahead throttle: a transaction of depth k does not start polling its
+// locks before the k-set (k - ahead - 1) is complete, so the resident lanes poll the locks
+// of a few k-sets only (300 k lanes spinning on the next 300 levels of TPC-B's 1,000 branch
+// locks saturated L2 with polls: 14 -> 192 ms).  Pure pacing: correctness comes from the
+// lock keys alone.  level sizes from the group offsets (goff[k*T]), completions in done[k].
+struct DfThrottle {
+    const uint32_t* D;         // depth per transaction (null: TPL, no throttle)
+    const uint32_t* goff;      // group offsets: k-set k = perm[goff[k*T] .. goff[(k+1)*T])
+    uint32_t T, ahead;
+    uint32_t* done;            // completed transactions per k-set
+    DEV bool on() const { return D != nullptr; }
+    DEV void wait(uint32_t idx) const {
+        const uint32_t k = __ldg(&D[idx]);
+        if (k <= ahead) return;
+        const uint32_t lv = k - ahead - 1;
+        const uint32_t need = __ldg(&goff[(lv + 1) * T]) - __ldg(&goff[lv * T]);
+        uint32_t polls = 0;
+        while (ld_relaxed(&done[lv]) < need)
+            if (++polls > 4) __nanosleep(256);
+    }
+    DEV void finish(uint32_t idx) const {
+        const uint32_t k = __ldg(&D[idx]);
+        const uint32_t am = __activemask();
+        const uint32_t peers = __match_any_sync(am, k);
+        if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(&done[k], (uint32_t)__popc(peers));
+    }
+};
 DEV bool tpl_acquire(uint32_t* lw, uint32_t key) {
     if (ld_acquire(lw) >= key) return true;          // uncontended: no collective
     uint32_t polls = 0;
@@ -2035,10 +2067,14 @@ DEV bool tpl_acquire(uint32_t* lw, uint32_t key) {
 }
 
 // Release +1 on a lock word; lanes releasing the same word combine into one atomic.
+// The leader's increment is a release (red.release.gpu); __syncwarp(peers) first makes
+// every peer's writes happen before it (release is cumulative) -- no fence.sc per lane
+// (fence.sc + atomicAdd cost ~0.3 us more per hand-off, tools/handoff.cu).
 DEV void tpl_release(uint32_t* lw) {
     const uint32_t am = __activemask();
     const uint32_t peers = __match_any_sync(am, (unsigned long long)lw);
-    if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(lw, (uint32_t)__popc(peers));
+    __syncwarp(peers);
+    if ((int)lane_id() == __ffs(peers) - 1) red_add_release(lw, (uint32_t)__popc(peers));
 }
 
 template <int S, bool SH>
@@ -2077,7 +2113,6 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
             }
             if (j == k) {
                 exec_txn<S, SH>(db, idx);
-                __threadfence();
                 for (int q = 0; q < k; ++q) tpl_release(&lock[r[q].item]);
                 done = true;
                 progressed = true;
@@ -2103,12 +2138,15 @@ __global__ void __launch_bounds__(128) tpl_exec_kernel(DevDb db, const uint32_t*
 template <bool SH>
 __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
                                                             const uint32_t* __restrict__ lkey, uint32_t* lock,
-                                                            uint32_t* sc) {
+                                                            uint32_t* sc, const uint32_t* __restrict__ order,
+                                                            DfThrottle thr) {
     __shared__ uint32_t s_base;
-    if (threadIdx.x == 0) s_base = atomicAdd(&sc[SC_TICKET], blockDim.x / 32);   // ts-ordered dispatch
+    if (threadIdx.x == 0) s_base = atomicAdd(&sc[SC_TICKET], blockDim.x / 32);   // ordered dispatch
     __syncthreads();
-    const uint32_t idx = s_base + (threadIdx.x >> 5);
-    if (idx >= db.n) return;                                   // warp-uniform
+    const uint32_t tk = s_base + (threadIdx.x >> 5);
+    if (tk >= db.n) return;                                    // warp-uniform
+    // tickets follow ts (TPL) or the k-set order (K-SET dataflow: order = perm)
+    const uint32_t idx = order ? __ldg(&order[tk]) : tk;
     const uint32_t lane = lane_id();
     Rec r[MAX_REC];
     const int k = footprint_local<S_TPCC>(db, db.type[idx], db.pw + db.poff[idx], r);
@@ -2118,6 +2156,7 @@ __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint
         if (j < k && (uint32_t)j == lane) item = r[j].item;
     const bool mine = (int)lane < k;
     const uint32_t key = mine ? __ldg(&lkey[rec_off[idx] + lane]) : 0u;
+    if (thr.on()) thr.wait(idx);
     // the rows come into L2 while the locks are awaited (on the W_YTD / district chains
     // the post-acquire execution is the critical path)
     tpcc_warm_warp(db, db.type[idx], db.pw + db.poff[idx]);
@@ -2136,8 +2175,9 @@ __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint
         __nanosleep(g == 1 ? (polls > 8 ? 32u : 0u) : min(g * 32u, g_tpl_sleep_cap));
     }
     exec_txn_warp<SH>(db, idx);
-    __threadfence();
-    if (mine) atomicAdd(&lock[item], 1u);
+    __syncwarp();                              // every lane's writes before any lane's release
+    if (mine) red_add_release(&lock[item], 1u);
+    if (thr.on() && lane == 0) atomicAdd(&thr.done[__ldg(&thr.D[idx])], 1u);
 }
 
 // Persistent TPL: every lane takes its next transaction as soon as it has released the
@@ -2148,15 +2188,20 @@ __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint
 template <int S, bool SH>
 __global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, const uint32_t* __restrict__ rec_off,
                                                                   const uint32_t* __restrict__ lkey, uint32_t* lock,
-                                                                  uint32_t* sc) {
+                                                                  uint32_t* sc, const uint32_t* __restrict__ order,
+                                                                  DfThrottle thr) {
     for (;;) {
         const uint32_t am = __activemask();
         const int leader = __ffs(am) - 1;
         uint32_t base = 0;
         if ((int)lane_id() == leader) base = atomicAdd(&sc[SC_TICKET], (uint32_t)__popc(am));
         base = __shfl_sync(am, base, leader);
-        const uint32_t idx = base + __popc(am & lanemask_lt());
-        if (idx >= db.n) break;
+        const uint32_t tk = base + __popc(am & lanemask_lt());
+        if (tk >= db.n) break;
+        // K-SET dataflow (order = perm): tickets in k-set order, so a transaction only
+        // waits for transactions of smaller depth, all already taken by running lanes
+        const uint32_t idx = order ? __ldg(&order[tk]) : tk;
+        if (thr.on()) thr.wait(idx);
         Rec r[MAX_REC];
         const int k = footprint_local<S>(db, db.type[idx], db.pw + db.poff[idx], r);
         const uint32_t ro = rec_off[idx];
@@ -2165,8 +2210,8 @@ __global__ void __launch_bounds__(256) tpl_exec_persistent_kernel(DevDb db, cons
             if (!tpl_acquire(&lock[r[j].item], key)) atomicExch(&sc[SC_DEADLOCK], 1u);
         }
         exec_txn<S, SH>(db, idx);
-        __threadfence();
         for (int j = 0; j < k; ++j) tpl_release(&lock[r[j].item]);
+        if (thr.on()) thr.finish(idx);
     }
 }
 

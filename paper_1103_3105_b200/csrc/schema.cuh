@@ -67,6 +67,7 @@ struct DevDb {
     const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
     uint32_t idx_base;                 // emit: record idx = idx_base + i (pool arrivals; 0 otherwise)
     struct UndoRec* undo;              // per-transaction undo-log slots (non-two-phase types)
+    uint32_t ins_dense;                // TPC-B: every transaction is a home deposit -> history row = idx
 };
 
 // Undo log: written in GPU memory before each update of a NON-two-phase
@@ -241,7 +242,7 @@ DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     // history row: deposits always commit; the row is the deposit's position among the bulk's
     // (home) deposits -- WITHDRAWs insert nothing (ingest counts, exclusive scan)
     (void)sh;
-    const uint64_t r = db.ins_base[0] + db.ins_off[idx];
+    const uint64_t r = db.ins_base[0] + (db.ins_dense ? idx : db.ins_off[idx]);
     INS(uint32_t, IB_TID)[r] = p[1];
     INS(uint32_t, IB_BID)[r] = p[2];
     INS(uint32_t, IB_AID)[r] = p[0];

@@ -108,6 +108,7 @@ def load_library():
         "gputx_pool_pending": ([P, P], I),
         "gputx_read_serial_order": ([P, P, U64], I),
         "gputx_snapshot": ([P, P, P], I),
+        "gputx_run_bulks": ([P, P, U64, I, P, P, P], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
@@ -148,7 +149,7 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
             "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping",
             "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending",
-            "gputx_read_serial_order", "gputx_snapshot"]
+            "gputx_read_serial_order", "gputx_snapshot", "gputx_run_bulks"]
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -341,6 +342,29 @@ class Database:
         self._check(self.lib.gputx_pool_read(self.h, _ptr(ts), _ptr(st), _ptr(out), k, ctypes.byref(n)), self.h)
         m = n.value
         return ts[:m], st[:m], out[:m]
+
+    def run_bulks(self, bulks, strategy: str = KSET, status=None, out=None, stats: bool = False):
+        """gputx_run_bulks: host bulks back to back with overlapped H2D / D2H.  status / out:
+        lists of caller-owned host arrays (u8[n_i], u8[n_i, stride]) or None."""
+        k = len(bulks)
+        arr = (BulkC * max(k, 1))()
+        keep = []
+        for i, b in enumerate(bulks):
+            t = np.ascontiguousarray(b.type, np.uint8)
+            po = np.ascontiguousarray(b.param_off, np.uint32)
+            pw = np.ascontiguousarray(b.param_words, np.uint32)
+            if pw.size == 0:
+                pw = np.zeros(1, np.uint32)
+            keep.append((t, po, pw))
+            arr[i] = BulkC(_ptr(t), _ptr(po), _ptr(pw), int(t.shape[0]), 0, None)
+        sp = (ctypes.c_void_p * max(k, 1))(*[(_ptr(a) if a is not None else None) for a in (status or [None] * k)])
+        op = (ctypes.c_void_p * max(k, 1))(*[(_ptr(a) if a is not None else None) for a in (out or [None] * k)])
+        sts = (Stats * max(k, 1))() if stats else None
+        self._check(self.lib.gputx_run_bulks(self.h, arr, k, STRATEGIES[strategy], sp, op, sts), self.h)
+        if k:
+            self.n = int(bulks[-1].type.shape[0])
+        self._keep = keep
+        return [s.as_dict() for s in sts[:k]] if stats else None
 
     def snapshot(self) -> dict:
         """The current database via gputx_snapshot: {"columns": {name: bytes-view array},

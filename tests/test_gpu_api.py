@@ -43,3 +43,30 @@ def test_snapshot_matches_columns_and_inserts():
     for c, a in ins["history"].items():
         assert np.array_equal(snap["tables"]["history"][c], a.view(np.uint32)), c
     db.close()
+
+
+@pytest.mark.parametrize("schema", [W.TM1, W.TPCC, W.TPCB])
+def test_run_bulks_overlapped_equals_serial(schema):
+    """gputx_run_bulks (overlapped H2D / D2H, two copy streams) gives every bulk's results
+    and the final state of the serial run of the bulks one after another."""
+    import oracle
+    import torch
+    dims = {W.TM1: W.Tm1Dims(5000), W.TPCC: W.TpccDims(2, 10, 300, 2000), W.TPCB: W.TpcbDims(4, 10, 1000)}[schema]
+    image = W.make_db(schema, dims, seed=1)
+    bulks = [W.make_bulk(schema, dims, 3000 + 500 * k, seed=10 + k) for k in range(5)]
+    db = gpu_db(schema, dims, image, 6000, insert_capacity=8)
+    stride = db.stride
+    st = [torch.empty(b.n, dtype=torch.uint8).pin_memory().numpy() for b in bulks]
+    out = [torch.empty(b.n * stride, dtype=torch.uint8).pin_memory().numpy().reshape(b.n, stride) for b in bulks]
+    stats = db.run_bulks(bulks, "kset", st, out, stats=True)
+    cur, ts = image, 0
+    for k, b in enumerate(bulks):
+        ref = oracle.run(schema, dims.dims, cur, b, first_ts=ts)
+        assert np.array_equal(st[k], ref.status), k
+        assert np.array_equal(out[k], ref.out), k
+        assert stats[k]["n"] == b.n
+        cur, ts = ref.db, ts + b.n
+    got = db.read_image(image)
+    for c in image:
+        assert np.array_equal(got[c], cur[c]), c
+    db.close()

@@ -71,7 +71,12 @@ def test_kset_survives_launch_without_clusters(case):
     image = W.make_db(schema, dims, seed=1)
     bulk = W.make_bulk(schema, dims, n, seed=2, **kw)
     ref = oracle.run(schema, dims.dims, image, bulk)
-    db = _open(schema, dims, image, n, cluster=8, diag=NO_CLUSTER_LAUNCH | JITTER)
+    import os as _os
+    _os.environ["GPUTX_KSET_DF"] = "0"           # the round executor (TPC-C defaults to dataflow)
+    try:
+        db = _open(schema, dims, image, n, cluster=8, diag=NO_CLUSTER_LAUNCH | JITTER)
+    finally:
+        _os.environ.pop("GPUTX_KSET_DF", None)
     try:
         for rep in range(5):
             db.reset()

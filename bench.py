@@ -337,6 +337,8 @@ def config_of(args, wl, dims, ws):
         else:
             c["sharding"] = (f"{ws} shards by root key, bulk {wl['n']} per shard (weak scaling); cross-shard "
                              "fragments exchanged inside the step")
+        c["exchange"] = ("torch.distributed all-to-all of library-packed records" if os.environ.get("GPUTX_NO_P2P")
+                         else "fused in the library: P2P stores into the owner shard's HBM arena (CUDA IPC)")
     return c
 
 
@@ -433,6 +435,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     if ws > 1:
         from paper_1103_3105_b200 import shard as SH
+        if not os.environ.get("GPUTX_NO_P2P"):
+            SH.connect_p2p(db)         # the library's fused exchange over peer memory (CUDA IPC)
 
     def step_dev(k, strategy):
         b = dbulks[k % len(dbulks)]

@@ -74,7 +74,7 @@ typedef enum {
     GPUTX_ECROSS = 7,        /* PART: a cross-partition type with no fragment split       */
     GPUTX_EDEADLOCK = 8,     /* a spin watchdog tripped (K-SET round wait, grid barrier, TPL lock); db poisoned until reset */
     GPUTX_ECUDA = 9,         /* CUDA runtime error                                        */
-    GPUTX_ENCCL = 10         /* reserved: inter-GPU exchange                              */
+    GPUTX_ENCCL = 10         /* inter-GPU exchange: a peer's arena cannot be mapped       */
 } gputx_status;
 
 typedef enum { GPUTX_TPL = 0, GPUTX_PART = 1, GPUTX_KSET = 2,
@@ -320,6 +320,33 @@ gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes);
  * exchange ran on) before calling gputx_shard_submit / gputx_shard_return_merge, which
  * read it on the handle's stream. */
 uint32_t gputx_shard_stride(gputx_schema schema, int result);
+
+/* The same exchange FUSED into the library over peer memory (no host
+ * staging and no collective call): every shard owns an exchange arena in its HBM; the
+ * kernel that packs a shard's cross-shard records writes each one straight into the owner
+ * shard's arena (P2P stores over NVLink / NVSwitch, or same-device stores when shards share
+ * a GPU) and its last CTA publishes the bulk's epoch to every peer; the receiving shard's
+ * stream waits for all peers' epochs on the device (spin watchdog -> EDEADLOCK), merges the
+ * received records by ts and ingests the local bulk.  Fragment outputs return the same way.
+ *   connect once: blob = gputx_shard_export(db) on every shard (GPUTX_PEER_BLOB_BYTES; a
+ *     CUDA IPC handle of the arena), all-gathered by the caller in shard order (any host
+ *     plumbing, e.g. torch.distributed.all_gather_object), then gputx_shard_connect(db,
+ *     blobs); handles of ONE process: gputx_shard_connect_local(dbs, n).
+ *   per bulk, on every shard: gputx_shard_dispatch(db, home) -> gputx_shard_receive(db,
+ *     &n_local) -> gputx_execute -> gputx_shard_return(db) -> gputx_shard_collect(db) ->
+ *     gputx_read_results.  In one process, call dispatch on every handle before receive on
+ *     any (receive waits for all peers), and return on every handle before collect.
+ * dispatch always publishes (an empty contribution if it fails validation), so peers never
+ * hang on a failing shard.  ECAPACITY if an arena's record area is full (it holds max_bulk
+ * records); ENCCL if a peer's arena cannot be mapped. */
+#define GPUTX_PEER_BLOB_BYTES 128
+gputx_status gputx_shard_export(gputx_db* db, void* blob);
+gputx_status gputx_shard_connect(gputx_db* db, const void* blobs);
+gputx_status gputx_shard_connect_local(gputx_db* const* dbs, uint32_t n);
+gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* home);
+gputx_status gputx_shard_receive(gputx_db* db, uint64_t* n_local);
+gputx_status gputx_shard_return(gputx_db* db);
+gputx_status gputx_shard_collect(gputx_db* db);
 gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* home, uint32_t* send, uint64_t send_cap,
                               uint64_t* counts);
 gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_recv, uint64_t* n_local);

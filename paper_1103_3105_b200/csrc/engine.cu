@@ -7,6 +7,7 @@
 //   TPL  : emit -> radix sort by item -> lock keys -> ts-ordered 2PL execution
 #include <algorithm>
 #include <cstdio>
+#include <unistd.h>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -145,6 +146,14 @@ struct gputx_db {
     uint8_t* in_type[2] = {};
     uint32_t *in_poff[2] = {}, *in_pw[2] = {};
     uint8_t *res_status[2] = {}, *res_out[2] = {};
+    // peer-memory exchange (gputx_shard_export / connect / dispatch / receive / return / collect)
+    uint32_t* arena = nullptr;          // this shard's arena (cudaMalloc: exportable by IPC)
+    uint64_t arena_words = 0, ret_base = 0;
+    uint32_t fwd_cap = 0, ret_cap = 0, xepoch = 0;
+    uint32_t* d_done_ctas = nullptr;
+    PeerTable pt{};
+    bool p2p = false;
+    std::vector<void*> ipc_open;
     uint32_t kset_df_ahead = 0;         // dataflow look-ahead throttle in k-sets, 0 = off (GPUTX_KSET_DF_AHEAD)
     uint32_t kset_df_grid = 0;          // dataflow persistent grid cap (GPUTX_KSET_DF_GRID), 0 = co-resident
     uint32_t* d_cnt = nullptr;       // max(max_bulk, max_rec) + 1
@@ -1177,6 +1186,17 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_ts, NB + 1)) || (st = dalloc(db, &db->d_order, NB + 1)))
         return bail(st);
     if (schema == S_TPCB && (st = dalloc(db, &db->d_undo, NB * UNDO_SLOTS))) return bail(st);
+    if (db->nshards > 1) {             // exchange arena: raw cudaMalloc (IPC-exportable)
+        const uint32_t sf = gputx_shard_stride((gputx_schema)schema, 0), sr = gputx_shard_stride((gputx_schema)schema, 1);
+        db->fwd_cap = (uint32_t)NB;
+        db->ret_cap = (uint32_t)NB;
+        db->ret_base = AR_HDR + (uint64_t)db->fwd_cap * sf;
+        db->arena_words = db->ret_base + (uint64_t)db->ret_cap * sr;
+        if (cudaMalloc((void**)&db->arena, db->arena_words * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
+        cudaMemsetAsync(db->arena, 0, db->arena_words * 4, db->stream);
+        if ((st = dalloc(db, &db->d_done_ctas, 1))) return bail(st);
+        cudaMemsetAsync(db->d_done_ctas, 0, 4, db->stream);
+    }
     if (db->nshards > 1 &&
         ((st = dalloc(db, &db->d_src, NB + 1)) || (st = dalloc(db, &db->d_home_pos, NB + 1)) ||
          (st = dalloc(db, &db->d_xflag, NB + 1)) || (st = dalloc(db, &db->s_type, NB + 1)) ||
@@ -1630,6 +1650,214 @@ gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send
         for (uint32_t q = 0; q < SC_COUNT; ++q) db->h_sc[q] = 0;
     }
     for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
+    return GPUTX_OK;
+}
+
+// ------------------------------------------------------------- peer-memory exchange (fused)
+struct PeerBlob {
+    char magic[8];
+    uint32_t version, shard, nshards, device;
+    uint64_t pid, ptr, words, ret_base;
+    uint32_t fwd_cap, ret_cap;
+    cudaIpcMemHandle_t h;
+};
+static_assert(sizeof(PeerBlob) <= GPUTX_PEER_BLOB_BYTES, "blob size");
+
+gputx_status gputx_shard_export(gputx_db* db, void* blob) {
+    if (!db || !blob) return GPUTX_EINVAL;
+    if (db->nshards < 2 || !db->arena) return fail(db, GPUTX_ESTATE, "not a sharded handle");
+    PeerBlob b{};
+    memcpy(b.magic, "GPTXPEER", 8);
+    b.version = 1;
+    b.shard = db->shard;
+    b.nshards = db->nshards;
+    b.device = (uint32_t)db->cfg.device;
+    b.pid = (uint64_t)getpid();
+    b.ptr = (uint64_t)(uintptr_t)db->arena;
+    b.words = db->arena_words;
+    b.ret_base = db->ret_base;
+    b.fwd_cap = db->fwd_cap;
+    b.ret_cap = db->ret_cap;
+    CK(cudaIpcGetMemHandle(&b.h, db->arena));
+    memset(blob, 0, GPUTX_PEER_BLOB_BYTES);
+    memcpy(blob, &b, sizeof(b));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_connect(gputx_db* db, const void* blobs) {
+    if (!db || !blobs) return GPUTX_EINVAL;
+    if (db->nshards < 2 || !db->arena) return fail(db, GPUTX_ESTATE, "not a sharded handle");
+    if (db->p2p) return fail(db, GPUTX_ESTATE, "already connected");
+    CK(cudaSetDevice(db->cfg.device));
+    PeerTable pt{};
+    for (uint32_t q = 0; q < db->nshards; ++q) {
+        PeerBlob b;
+        memcpy(&b, (const uint8_t*)blobs + (uint64_t)q * GPUTX_PEER_BLOB_BYTES, sizeof(b));
+        if (memcmp(b.magic, "GPTXPEER", 8) || b.version != 1 || b.shard != q || b.nshards != db->nshards ||
+            b.ret_base >= b.words)
+            return fail(db, GPUTX_EINVAL, "peer blob " + std::to_string(q) + " does not match this handle");
+        pt.ret_base[q] = b.ret_base;
+        pt.fwd_cap[q] = b.fwd_cap;
+        pt.ret_cap[q] = b.ret_cap;
+        if (q == db->shard) {
+            pt.arena[q] = db->arena;
+        } else if (b.pid == (uint64_t)getpid()) {       // same process: the pointer itself
+            if ((int)b.device != db->cfg.device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess((int)b.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(db, GPUTX_ENCCL, std::string("peer access: ") + cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+            pt.arena[q] = (uint32_t*)(uintptr_t)b.ptr;
+        } else {                                       // another process: CUDA IPC over NVLink
+            void* p = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&p, b.h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) return fail(db, GPUTX_ENCCL, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+            db->ipc_open.push_back(p);
+            pt.arena[q] = (uint32_t*)p;
+        }
+    }
+    db->pt = pt;
+    db->p2p = true;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_connect_local(gputx_db* const* dbs, uint32_t n) {
+    if (!dbs || n < 2 || n > MAX_SHARDS) return GPUTX_EINVAL;
+    std::vector<uint8_t> blobs((size_t)n * GPUTX_PEER_BLOB_BYTES);
+    for (uint32_t q = 0; q < n; ++q) {
+        if (!dbs[q] || dbs[q]->shard != q || dbs[q]->nshards != n) return GPUTX_EINVAL;
+        TRY(gputx_shard_export(dbs[q], blobs.data() + (size_t)q * GPUTX_PEER_BLOB_BYTES));
+    }
+    for (uint32_t q = 0; q < n; ++q) TRY(gputx_shard_connect(dbs[q], blobs.data()));
+    return GPUTX_OK;
+}
+
+extern "C++" {
+template <int S>
+void p2p_dispatch_launch(gputx_db* db, uint32_t nh) {
+    const DevDb v = make_devdb(db);
+    const uint32_t g = std::max<uint32_t>(1, grid_for(nh, 256, 148 * 8));
+    p2p_dispatch_kernel<S><<<g, 256, 0, db->stream>>>(v, db->s_type, db->s_poff, db->s_pw, db->s_ts, nh, db->pt,
+                                                      db->shard, db->nshards,
+                                                      gputx_shard_stride((gputx_schema)db->schema, 0), db->xepoch,
+                                                      db->d_done_ctas);
+    ++db->launches;
+}
+}  // extern "C++"
+
+gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
+    if (!db || !b) return GPUTX_EINVAL;
+    if (!db->p2p) return fail(db, GPUTX_ESTATE, "gputx_shard_connect first");
+    cudaStream_t s = db->stream;
+    ++db->xepoch;                      // every shard dispatches once per bulk: epochs agree
+    db->have_x = true;
+    cudaEventRecord(db->ev_x[0], s);
+    cudaEventRecord(db->ev_sub[0], s);
+    db->launches = 0;
+    gputx_status err = submit_check(db, b);
+    if (err == GPUTX_OK && b->n && !b->ts) err = fail(db, GPUTX_EINVAL, "sharded bulks need global timestamps");
+    const uint64_t n = err == GPUTX_OK ? b->n : 0;
+    uint32_t n_words = 0;
+    if (n) {
+        if (b->on_device) {
+            CK(cudaMemcpyAsync(db->h_sc + SC_COUNT - 1, b->param_off + n, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            n_words = db->h_sc[SC_COUNT - 1];
+        } else {
+            n_words = b->param_off[n];
+        }
+        if (n_words > db->max_words) err = fail(db, GPUTX_ECAPACITY, "too many parameter words");
+    }
+    uint32_t nh = 0;
+    if (err == GPUTX_OK && n) {
+        const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(db->s_type, b->type, n, kind, s));
+        CK(cudaMemcpyAsync(db->s_poff, b->param_off, (n + 1) * 4, kind, s));
+        if (n_words) CK(cudaMemcpyAsync(db->s_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
+        CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
+        CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+        CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+        const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
+        shard_validate_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(db->s_poff, (uint32_t)n, n_words, stride - 3,
+                                                                        db->d_sc);
+        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (db->h_sc[SC_ERR]) err = fail(db, GPUTX_EINVAL, "home transaction " + std::to_string(err_idx(db)) +
+                                                               ": bad param_off");
+        else nh = (uint32_t)n;
+    }
+    // always publish (an empty contribution on error), so that no peer waits forever
+    if (db->schema == S_TPCB) p2p_dispatch_launch<S_TPCB>(db, nh);
+    else if (db->schema == S_TM1) p2p_dispatch_launch<S_TM1>(db, nh);
+    else p2p_dispatch_launch<S_TPCC>(db, nh);
+    CK(cudaGetLastError());
+    if (err != GPUTX_OK) return err;
+    db->nh = nh;
+    db->staged = true;
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_receive(gputx_db* db, uint64_t* n_local) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->p2p || !db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_dispatch first");
+    cudaStream_t s = db->stream;
+    CK(cudaMemsetAsync(db->d_sc + SC_DEADLOCK, 0, 4, s));
+    p2p_wait_kernel<<<1, 32, 0, s>>>(db->arena, AR_FWD_FLAGS, AR_FWD_CNT, db->shard, db->nshards, db->xepoch,
+                                     db->d_sc, db->d_sc + SC_P2P);
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_DEADLOCK]) {
+        db->poisoned = true;
+        return fail(db, GPUTX_EDEADLOCK, "a peer shard did not publish its records (watchdog)");
+    }
+    if (db->h_sc[SC_P2P + 1] & 1u) return fail(db, GPUTX_ECAPACITY, "exchange arena full (forward records)");
+    const uint64_t nr = db->h_sc[SC_P2P];
+    gputx_status r = gputx_shard_submit(db, db->arena + AR_HDR, nr, n_local);
+    // ms_exchange = dispatch .. received records merged and ingested, + return .. collected
+    cudaEventRecord(db->ev_x[1], s);
+    return r;
+}
+
+extern "C++" {
+template <int S>
+void p2p_return_launch(gputx_db* db) {
+    const DevDb v = make_devdb(db);
+    const uint32_t g = std::max<uint32_t>(1, grid_for(db->n, 256, 148 * 8));
+    p2p_return_kernel<S><<<g, 256, 0, db->stream>>>(v, db->pt, db->shard, db->nshards, db->out_stride / 4,
+                                                    db->xepoch, db->d_done_ctas);
+    ++db->launches;
+}
+}  // extern "C++"
+
+gputx_status gputx_shard_return(gputx_db* db) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->p2p) return fail(db, GPUTX_ESTATE, "gputx_shard_connect first");
+    if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
+    cudaEventRecord(db->ev_x[2], db->stream);
+    if (db->schema == S_TPCB) p2p_return_launch<S_TPCB>(db);
+    else if (db->schema == S_TM1) p2p_return_launch<S_TM1>(db);
+    else p2p_return_launch<S_TPCC>(db);
+    CK(cudaGetLastError());
+    return GPUTX_OK;
+}
+
+gputx_status gputx_shard_collect(gputx_db* db) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->p2p || !db->executed) return fail(db, GPUTX_ESTATE, "gputx_shard_return first");
+    cudaStream_t s = db->stream;
+    p2p_wait_kernel<<<1, 32, 0, s>>>(db->arena, AR_RET_FLAGS, AR_RET_CNT, db->shard, db->nshards, db->xepoch,
+                                     db->d_sc, db->d_sc + SC_P2P);
+    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (db->h_sc[SC_DEADLOCK]) {
+        db->poisoned = true;
+        return fail(db, GPUTX_EDEADLOCK, "a peer shard did not return its outputs (watchdog)");
+    }
+    if (db->h_sc[SC_P2P + 1] & 2u) return fail(db, GPUTX_ECAPACITY, "exchange arena full (returned outputs)");
+    const uint64_t nr = db->h_sc[SC_P2P];
+    TRY(gputx_shard_return_merge(db, db->arena + db->ret_base, nr));
+    cudaEventRecord(db->ev_x[3], s);
     return GPUTX_OK;
 }
 
@@ -2140,6 +2368,9 @@ void gputx_close_db(gputx_db* db) {
         dfree(db, db->res_status[k]); dfree(db, db->res_out[k]);
     }
     if (db->st_h2d) cudaStreamDestroy(db->st_h2d);
+    for (void* p : db->ipc_open) cudaIpcCloseMemHandle(p);
+    if (db->arena) cudaFree(db->arena);
+    dfree(db, db->d_done_ctas);
     if (db->st_d2h) cudaStreamDestroy(db->st_d2h);
     if (db->own_stream && db->stream) cudaStreamDestroy(db->stream);
     delete db;

@@ -27,6 +27,7 @@ constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART 
 constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested cluster shape (counter hand-offs used)
 constexpr int SC_ERRPK = 34;      // [34, 36): u64 (first bad idx << 8 | its code); all-ones = none
 constexpr int SC_SPARSE = 36;     // TPC-B ingest: transactions without a history row (withdrawals, peers')
+constexpr int SC_P2P = 37;        // [37, 39): peer exchange: records received, overflow bits
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -2523,6 +2524,122 @@ __global__ void __launch_bounds__(128) rpart_exec_kernel(DevDb db, const uint32_
             exec_txn<S, false>(db, idx);
         }
         if (hi > lo) atomicMax(&sc[SC_MAXCHAIN], hi - lo);
+    }
+}
+}  // namespace gputx
+
+namespace gputx {
+// =====================================================================================
+// Peer-memory exchange (fused): every shard owns an ARENA in its
+// HBM -- per-source arrival flags, a record counter and a record area for the cross-shard
+// transactions it receives, the same for returned fragment outputs.  The producing kernel
+// writes each record straight into the destination shard's arena (P2P stores over NVLink /
+// NVSwitch; same-device stores when the shards share a GPU), reserving its slot with a
+// system-scope atomic on the destination's counter; the kernel's last CTA then publishes
+// the epoch to every peer (release at system scope).  No host staging, no all-to-all call.
+// =====================================================================================
+constexpr uint32_t AR_FWD_FLAGS = 0;      // [MAX_SHARDS] x 32 words (own 128-B lines)
+constexpr uint32_t AR_RET_FLAGS = 256;
+constexpr uint32_t AR_FWD_CNT = 512;
+constexpr uint32_t AR_RET_CNT = 544;
+constexpr uint32_t AR_OVF = 576;          // overflow: a sender found the record area full
+constexpr uint32_t AR_HDR = 640;          // record areas start here (words)
+struct PeerTable {
+    uint32_t* arena[MAX_SHARDS];           // every shard's arena as seen from this process
+    uint64_t ret_base[MAX_SHARDS];         // its geometry (arenas are sized by each shard's max_bulk)
+    uint32_t fwd_cap[MAX_SHARDS], ret_cap[MAX_SHARDS];
+};
+DEV void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+DEV uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// last-CTA publication: every CTA fences its P2P stores at system scope and counts itself;
+// the last one (after the acquire fence) stores the epoch into flag[self] of every peer
+DEV void p2p_publish(const PeerTable& pt, uint32_t off_flags, uint32_t self, uint32_t G, uint32_t epoch,
+                     uint32_t* done_ctas) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const uint32_t prev = atomicAdd(done_ctas, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            *done_ctas = 0;                                   // reusable by the next exchange
+            for (uint32_t q = 0; q < G; ++q)
+                if (q != self) st_release_sys(&pt.arena[q][off_flags + self * 32], epoch);
+        }
+    }
+}
+
+// C1+C2 fused with the pack: [ts, type, len, params] of every (home transaction, remote
+// shard owning one of its fragments) into that shard's arena.  Thread 0 of CTA 0 also
+// clears this shard's return counter for the coming return exchange (all peers' returns of
+// the previous epoch were merged before this dispatch).
+template <int S>
+__global__ void __launch_bounds__(256) p2p_dispatch_kernel(DevDb db, const uint8_t* __restrict__ type,
+        const uint32_t* __restrict__ poff, const uint32_t* __restrict__ pw, const uint32_t* __restrict__ ts,
+        uint32_t nh, PeerTable pt, uint32_t self, uint32_t G, uint32_t stride, uint32_t epoch, uint32_t* done_ctas) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) pt.arena[self][AR_RET_CNT] = 0;
+    const uint32_t maxlen = stride - 3;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const uint32_t len = shard_len(poff, i, maxlen);
+        uint32_t m = dest_mask<S>(db, type[i], pw + poff[i], len) & ~(1u << self);
+        while (m) {
+            const uint32_t q = __ffs(m) - 1;
+            m &= m - 1;
+            uint32_t* ar = pt.arena[q];
+            const uint32_t slot = atomicAdd_system(&ar[AR_FWD_CNT], 1u);
+            if (slot >= pt.fwd_cap[q]) { atomicOr_system(&ar[AR_OVF], 1u); continue; }
+            uint32_t* r = ar + AR_HDR + (uint64_t)slot * stride;
+            r[0] = ts[i];
+            r[1] = type[i];
+            r[2] = len;
+            const uint32_t* src = pw + poff[i];
+            for (uint32_t w = 0; w < len; ++w) r[3 + w] = src[w];
+        }
+    }
+    p2p_publish(pt, AR_FWD_FLAGS, self, G, epoch, done_ctas);
+}
+
+// C3 fused: the output record of every peer's transaction executed here goes straight into
+// its home shard's arena; thread 0 of CTA 0 clears this shard's forward counter (the
+// records it received for this epoch were merged before the execution).
+template <int S>
+__global__ void __launch_bounds__(256) p2p_return_kernel(DevDb db, PeerTable pt, uint32_t self, uint32_t G,
+                                                         uint32_t ow, uint32_t epoch, uint32_t* done_ctas) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) pt.arena[self][AR_FWD_CNT] = 0;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < db.n; k += gridDim.x * blockDim.x) {
+        if (db.src[k] != NOT_HOME) continue;
+        const uint32_t* p = db.pw + db.poff[k];
+        const uint32_t q = shard_of(db, S == S_TPCB ? p[2] : p[0]);
+        uint32_t* ar = pt.arena[q];
+        const uint32_t slot = atomicAdd_system(&ar[AR_RET_CNT], 1u);
+        if (slot >= pt.ret_cap[q]) { atomicOr_system(&ar[AR_OVF], 2u); continue; }
+        uint32_t* r = ar + pt.ret_base[q] + (uint64_t)slot * (1 + ow);
+        r[0] = db.ts[k];
+        const uint32_t* o = reinterpret_cast<const uint32_t*>(db.out + (uint64_t)k * ow * 4);
+        for (uint32_t w = 0; w < ow; ++w) r[1 + w] = o[w];
+    }
+    p2p_publish(pt, AR_RET_FLAGS, self, G, epoch, done_ctas);
+}
+
+// wait until every peer published `epoch` (watchdog -> SC_DEADLOCK), then copy the count
+__global__ void p2p_wait_kernel(uint32_t* arena, uint32_t off_flags, uint32_t off_cnt, uint32_t self, uint32_t G,
+                                uint32_t epoch, uint32_t* sc, uint32_t* cnt_out) {
+    const uint32_t q = threadIdx.x;
+    if (q < G && q != self) {
+        SpinWatch wd;
+        while (ld_acquire_sys(&arena[off_flags + q * 32]) < epoch)
+            if (wd.expired(&sc[SC_DEADLOCK])) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *cnt_out = ld_acquire_sys(&arena[off_cnt]);
+        cnt_out[1] = ld_acquire_sys(&arena[AR_OVF]);
     }
 }
 }  // namespace gputx

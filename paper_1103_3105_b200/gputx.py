@@ -109,6 +109,13 @@ def load_library():
         "gputx_read_serial_order": ([P, P, U64], I),
         "gputx_snapshot": ([P, P, P], I),
         "gputx_run_bulks": ([P, P, U64, I, P, P, P], I),
+        "gputx_shard_export": ([P, P], I),
+        "gputx_shard_connect": ([P, P], I),
+        "gputx_shard_connect_local": ([P, U32], I),
+        "gputx_shard_dispatch": ([P, P], I),
+        "gputx_shard_receive": ([P, P], I),
+        "gputx_shard_return": ([P], I),
+        "gputx_shard_collect": ([P], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
@@ -149,7 +156,10 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_read_rank_ns", "gputx_shard_stride", "gputx_shard_pack", "gputx_shard_submit",
             "gputx_shard_return_pack", "gputx_shard_return_merge", "gputx_set_grouping",
             "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending",
-            "gputx_read_serial_order", "gputx_snapshot", "gputx_run_bulks"]
+            "gputx_read_serial_order", "gputx_snapshot", "gputx_run_bulks", "gputx_shard_export",
+            "gputx_shard_connect", "gputx_shard_connect_local", "gputx_shard_dispatch", "gputx_shard_receive",
+            "gputx_shard_return", "gputx_shard_collect"]
+PEER_BLOB_BYTES = 128                    # include/gputx.h GPUTX_PEER_BLOB_BYTES
 
 INSERT_TABLES = {
     1: {"history": ["h_tid", "h_bid", "h_aid", "h_delta", "h_ts"]},
@@ -307,6 +317,43 @@ class Database:
 
     def shard_return_merge(self, recv, n_recv: int):
         self._check(self.lib.gputx_shard_return_merge(self.h, _ptr(recv) if n_recv else None, int(n_recv)), self.h)
+
+    # ---- fused peer-memory exchange (include/gputx.h "FUSED into the library") -----------
+    def shard_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(PEER_BLOB_BYTES)
+        self._check(self.lib.gputx_shard_export(self.h, buf), self.h)
+        return buf.raw
+
+    def shard_connect(self, blobs: list[bytes]):
+        raw = b"".join(blobs)
+        self._check(self.lib.gputx_shard_connect(self.h, raw), self.h)
+
+    @staticmethod
+    def shard_connect_local(dbs: list["Database"]):
+        lib = dbs[0].lib
+        arr = (ctypes.c_void_p * len(dbs))(*[d.h.value for d in dbs])
+        st = lib.gputx_shard_connect_local(arr, len(dbs))
+        if st != 0:
+            raise GputxError(st, lib.gputx_last_error(dbs[0].h).decode())
+
+    def shard_dispatch(self, bulk=None, *, type=None, param_off=None, param_words=None, ts=None,
+                       on_device: bool = False):
+        b = self._bulk(bulk, type, param_off, param_words, ts, on_device)
+        self.nh = int(b.n)
+        self._check(self.lib.gputx_shard_dispatch(self.h, ctypes.byref(b)), self.h)
+
+    def shard_receive(self) -> int:
+        nl = ctypes.c_uint64()
+        self._check(self.lib.gputx_shard_receive(self.h, ctypes.byref(nl)), self.h)
+        self.n_local = int(nl.value)
+        self.n = self.nh
+        return self.n_local
+
+    def shard_return(self):
+        self._check(self.lib.gputx_shard_return(self.h), self.h)
+
+    def shard_collect(self):
+        self._check(self.lib.gputx_shard_collect(self.h), self.h)
 
     def execute(self, strategy: str = KSET) -> dict:
         st = Stats()

@@ -40,9 +40,28 @@ def all_to_all_records(send: torch.Tensor, counts: list[int], stride: int, group
     return recv, total
 
 
+def connect_p2p(db: Database, group=None):
+    """Map every rank's exchange arena into this rank (CUDA IPC over NVLink / NVSwitch):
+    the blobs are all-gathered once with torch.distributed (host plumbing only); from then
+    on records move by the library's own kernels (gputx_shard_dispatch / return)."""
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, db.shard_export(), group=group)
+    db.shard_connect(blobs)
+    db.p2p = True
+
+
 def step(db: Database, home, strategy: str, group=None, on_device: bool = False) -> dict:
-    """One bulk on this rank's shard: pack, exchange, submit, execute, return outputs.
+    """One bulk on this rank's shard.  Connected (connect_p2p): dispatch over peer memory,
+    receive, execute, return, collect -- no host staging, no collective.  Otherwise: pack,
+    all-to-all with torch.distributed, submit, execute, return, merge.
     `home` = this rank's home transactions with global ts (numpy or device tensors)."""
+    if getattr(db, "p2p", False):
+        db.shard_dispatch(home, on_device=on_device)
+        db.shard_receive()
+        st = db.execute(strategy)
+        db.shard_return()
+        db.shard_collect()
+        return st
     send, counts = db.shard_pack(home, on_device=on_device)
     recv, n = all_to_all_records(send, counts, db.shard_stride(False), group)
     db.shard_submit(recv, n)
@@ -54,10 +73,14 @@ def step(db: Database, home, strategy: str, group=None, on_device: bool = False)
 
 
 class LocalShards:
-    """G shard handles in one process on one GPU; the all-to-all is a device gather."""
+    """G shard handles in one process on one GPU; the all-to-all is a device gather, or
+    (p2p=True) the library's fused peer-memory exchange between the handles."""
 
-    def __init__(self, dbs: list[Database]):
+    def __init__(self, dbs: list[Database], p2p: bool = False):
         self.dbs = dbs
+        self.p2p = p2p
+        if p2p:
+            Database.shard_connect_local(dbs)
 
     @staticmethod
     def _exchange(sends, counts, stride):
@@ -74,6 +97,17 @@ class LocalShards:
 
     def step(self, homes, strategy: str, on_device: bool = False) -> list[dict]:
         dbs = self.dbs
+        if self.p2p:              # every dispatch before any receive (receive waits for all peers)
+            for db, h in zip(dbs, homes):
+                db.shard_dispatch(h, on_device=on_device)
+            for db in dbs:
+                db.shard_receive()
+            stats = [db.execute(strategy) for db in dbs]
+            for db in dbs:
+                db.shard_return()
+            for db in dbs:
+                db.shard_collect()
+            return stats
         packed = [db.shard_pack(h, on_device=on_device) for db, h in zip(dbs, homes)]
         recvs = self._exchange([p[0] for p in packed], [p[1] for p in packed], dbs[0].shard_stride(False))
         torch.cuda.current_stream().synchronize()          # the device gathers have landed

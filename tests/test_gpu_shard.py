@@ -14,14 +14,14 @@ pytestmark = pytest.mark.gpu
 STRATS = ["kset", "part", "tpl"]
 
 
-def _run(schema, dims, image, bulk, G, strategy, **kw):
+def _run(schema, dims, image, bulk, G, strategy, p2p=False, **kw):
     from paper_1103_3105_b200 import Database
     from paper_1103_3105_b200.shard import LocalShards
     ref = oracle.run(schema, dims.dims, image, bulk)
     homes = W.split_home(bulk, dims, G)
     dbs = [Database(schema, dims.dims, bulk.n, image, shard=r, nshards=G, **kw) for r in range(G)]
     try:
-        stats = LocalShards(dbs).step(homes, strategy)
+        stats = LocalShards(dbs, p2p=p2p).step(homes, strategy)
         compare_sharded(schema, dims, ref, dbs, homes, image, label=f"{strategy} G={G}")
         return stats
     finally:
@@ -123,3 +123,80 @@ def test_shard_pack_rejects_malformed_offsets(bad):
         db.shard_pack(home)
     assert e.value.name in ("EINVAL", "ECAPACITY")
     db.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("case", ["tpcb", "tpcc", "tm1"])
+@pytest.mark.parametrize("G", [2, 4])
+def test_fused_peer_exchange(case, G, strategy):
+    """The library's fused exchange over peer memory (gputx_shard_dispatch / receive /
+    return / collect): the dispatching kernel writes the records straight into the owner
+    shard's arena; the union of the shards equals the serial run of the whole bulk."""
+    if case == "tpcb":
+        dims = W.TpcbDims(12, 10, 500)
+        image, bulk = W.tpcb_db(dims), W.tpcb_bulk(dims, 6000, seed=3, remote_pct=40.0)
+        schema = W.TPCB
+    elif case == "tpcc":
+        dims = W.TpccDims(8, 10, 30, 1000)
+        image, bulk = W.tpcc_db(dims, seed=2), W.tpcc_bulk(dims, 5000, seed=4, remote_line_pct=10.0,
+                                                           remote_pay_pct=30.0)
+        schema = W.TPCC
+    else:
+        dims = W.Tm1Dims(4000)
+        image, bulk = W.tm1_db(dims, seed=2), W.tm1_bulk(dims, 6000, seed=5)
+        schema = W.TM1
+    stats = _run(schema, dims, image, bulk, G, strategy, p2p=True)
+    if case != "tm1":
+        assert sum(s["n"] for s in stats) > bulk.n          # cross-shard records moved
+
+
+def test_fused_peer_exchange_repeated_epochs():
+    """Several bulks back to back through the same arenas (epochs, counter resets)."""
+    from paper_1103_3105_b200 import Database
+    from paper_1103_3105_b200.shard import LocalShards
+    dims = W.TpccDims(6, 10, 30, 1000)
+    image = W.tpcc_db(dims, seed=2)
+    G = 3
+    dbs = [Database(W.TPCC, dims.dims, 6000, image, shard=r, nshards=G, insert_capacity=6) for r in range(G)]
+    ls = LocalShards(dbs, p2p=True)
+    cur, ts0 = image, 0
+    try:
+        for k in range(4):
+            bulk = W.tpcc_bulk(dims, 3000, seed=20 + k, remote_line_pct=10.0, remote_pay_pct=30.0)
+            bulk.ts = (ts0 + np.arange(bulk.n)).astype(np.uint32)
+            ref = oracle.run(W.TPCC, dims.dims, cur, bulk, first_ts=ts0)
+            homes = W.split_home(bulk, dims, G)
+            for h in homes:
+                h.ts = (h.ts.astype(np.int64) + ts0).astype(np.uint32)
+            ls.step(homes, "kset")
+            for r, db in enumerate(dbs):
+                st, out = db.read_results()
+                idx = homes[r].ts.astype(np.int64) - ts0
+                assert np.array_equal(st, ref.status[idx]) and np.array_equal(out, ref.out[idx]), (k, r)
+            cur, ts0 = ref.db, ts0 + bulk.n
+    finally:
+        for db in dbs:
+            db.close()
+
+
+def test_bench_cli_two_ranks_strong_tpcc():
+    """`GPUTX_DIST_BACKEND=gloo python bench.py --gpus 2 --workload tpcc
+    --scaling strong` on one GPU spawns 2 ranks, runs the fused peer exchange between them
+    (CUDA IPC on one device) and prints one line with n_gpus 2 (a functional check: two
+    ranks sharing one GPU say nothing about scaling)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["GPUTX_DIST_BACKEND"] = "gloo"
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--workload", "tpcc", "--scaling", "strong",
+                          "--steps", "2", "--warmup", "3", "--also", "none", "--others", "", "--no-cpu-baseline"],
+                         cwd=root, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert "fused" in d["config"]["exchange"]

@@ -581,7 +581,10 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         cand[rank_kernel_name(wl["schema"], wl.get("add_rule", False))] = (
             rank_bytes(wl["schema"], last["records"], last["rank_passes"], nloc), phase["ms_rank"])
     if ws == 1:
-        cand[f"{eff}_exec_kernel"] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+        # K-SET's dataflow executor (TPC-C default, stats flag 2) runs the counter-lock kernels
+        ek = (("tpl_exec_warp_kernel" if wl["schema"] == W.TPCC else "tpl_exec_persistent_kernel")
+              if eff == "kset" and (last.get("flags", 0) & 2) else f"{eff}_exec_kernel")
+        cand[ek] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1]) if cand else None
     roofline = None
     if kname:

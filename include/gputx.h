@@ -161,6 +161,8 @@ typedef struct {
 /* gputx_stats.flags */
 #define GPUTX_STAT_CLUSTER_FALLBACK 1u   /* K-SET executor was launched without its cluster shape
                                             (e.g. by a profiler) and used counter hand-offs only */
+#define GPUTX_STAT_KSET_DATAFLOW 2u      /* K-SET ran the dataflow executor (per-item completion
+                                            counters, k-set-order dispatch) instead of rounds  */
 
 /* Create a database handle for cfg->schema with empty (zero) columns on cfg->device.
  * Errors: EINVAL (bad schema/dims/max_bulk), ENOMEM, ECUDA.  *out is NULL on error. */

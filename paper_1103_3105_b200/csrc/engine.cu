@@ -1976,7 +1976,8 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
             cudaEventElapsedTime(&b, db->ev_x[2], db->ev_x[3]);
             stats->ms_exchange = a + b;
         }
-        stats->flags = db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0;
+        stats->flags = (db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0) |
+                       ((ranked && eff == GPUTX_KSET && db->kset_ran_df) ? GPUTX_STAT_KSET_DATAFLOW : 0);
         cudaGetLastError();
     }
     return GPUTX_OK;

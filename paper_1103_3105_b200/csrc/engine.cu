@@ -140,6 +140,8 @@ struct gputx_db {
     int kset_df = -1;                   // K-SET executor: 1 dataflow, 0 rounds, -1 schema default
     bool kset_ran_df = false;
     bool ins_dense = false;
+    uint8_t *tm1_sub = nullptr, *tm1_ai = nullptr, *tm1_sf = nullptr, *tm1_cf = nullptr;   // TM-1 row groups
+    bool rows_dirty = false;            // TM-1: rows hold newer mutable fields than the columns
     // gputx_run_bulks: copy streams and double-buffered device slots (lazily created)
     cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_res[2] = {}, ev_res_free[2] = {};
@@ -355,6 +357,10 @@ DevDb make_devdb(gputx_db* db) {
     v.xflag = db->nshards > 1 ? db->d_xflag : nullptr;
     v.undo = db->d_undo;
     v.ins_dense = db->ins_dense ? 1u : 0u;
+    v.tm1_sub = db->tm1_sub;
+    v.tm1_ai = db->tm1_ai;
+    v.tm1_sf = db->tm1_sf;
+    v.tm1_cf = db->tm1_cf;
     return v;
 }
 
@@ -1032,6 +1038,7 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
     std::swap(db->d_prec, db->d_prec2);
     const uint64_t ex = db->h_sc[SC_XTOTAL];
     db->pool_exec = ex;
+    if (S == S_TM1 && ex) db->rows_dirty = true;
     db->pool_n = db->h_sc[SC_POOL_KEPT];
     db->pool_words = db->h_sc[SC_POOL_WORDS];
     db->pool_nrec = db->h_sc[SC_NREC];
@@ -1056,6 +1063,25 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
         stats->ms_merge = c;      // results + compaction of the pool
         stats->ms_total = tot;
     }
+    return GPUTX_OK;
+}
+
+// TM-1 row groups (schema.cuh): built from the columns, and the columns' mutable fields
+// refreshed from them before any read of the database image
+gputx_status tm1_rows_pack(gputx_db* db) {
+    if (db->schema != S_TM1) return GPUTX_OK;
+    const DevDb v = make_devdb(db);
+    tm1_pack_kernel<<<grid_for(db->cfg.dims[0], 256, 148 * 8), 256, 0, db->stream>>>(v);
+    CK(cudaGetLastError());
+    db->rows_dirty = false;
+    return GPUTX_OK;
+}
+gputx_status tm1_rows_sync(gputx_db* db) {
+    if (db->schema != S_TM1 || !db->rows_dirty) return GPUTX_OK;
+    const DevDb v = make_devdb(db);
+    tm1_unpack_kernel<<<grid_for(db->cfg.dims[0], 256, 148 * 8), 256, 0, db->stream>>>(v);
+    CK(cudaGetLastError());
+    db->rows_dirty = false;
     return GPUTX_OK;
 }
 
@@ -1186,6 +1212,12 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_ts, NB + 1)) || (st = dalloc(db, &db->d_order, NB + 1)))
         return bail(st);
     if (schema == S_TPCB && (st = dalloc(db, &db->d_undo, NB * UNDO_SLOTS))) return bail(st);
+    if (schema == S_TM1) {
+        const uint64_t P = d[0];
+        if ((st = dalloc(db, &db->tm1_sub, P * TM1_SUBROW)) || (st = dalloc(db, &db->tm1_ai, 4 * P * TM1_AIROW)) ||
+            (st = dalloc(db, &db->tm1_sf, 4 * P * TM1_SFROW)) || (st = dalloc(db, &db->tm1_cf, 4 * P * TM1_CFROW)))
+            return bail(st);
+    }
     if (db->nshards > 1) {             // exchange arena: raw cudaMalloc (IPC-exportable)
         const uint32_t sf = gputx_shard_stride((gputx_schema)schema, 0), sr = gputx_shard_stride((gputx_schema)schema, 1);
         db->fwd_cap = (uint32_t)NB;
@@ -1459,6 +1491,7 @@ gputx_status gputx_seal(gputx_db* db) {
         db->h_last.clear();
         db->h_first.clear();
     }
+    TRY(tm1_rows_pack(db));
     // pristine copy for reset
     for (auto& c : db->cols) {
         const uint64_t b = c.spec.count * c.spec.elem;
@@ -1923,6 +1956,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    if (db->schema == S_TM1 && n) db->rows_dirty = true;
     const bool ranked = (st == GPUTX_KSET || st == GPUTX_AUTO) && n;
     const gputx_strategy eff = (gputx_strategy)db->chosen;
     if (ranked) db->rank_epoch += db->h_sc[SC_PASSES] + 1;
@@ -2014,6 +2048,7 @@ gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const vo
 
 gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint64_t bytes) {
     if (!db || !name || !host) return GPUTX_EINVAL;
+    TRY(tm1_rows_sync(db));
     Col* c = find_col(db, name);
     if (!c) return fail(db, GPUTX_EINVAL, std::string("unknown column ") + name);
     if (bytes != c->spec.count * c->spec.elem) return fail(db, GPUTX_EINVAL, "size mismatch");
@@ -2166,6 +2201,7 @@ gputx_status gputx_snapshot(gputx_db* db, void* buf, uint64_t* bytes) {
     }
     if (!buf) { *bytes = need; return GPUTX_OK; }
     if (*bytes < need) { *bytes = need; return fail(db, GPUTX_ECAPACITY, "snapshot buffer too small"); }
+    TRY(tm1_rows_sync(db));
     uint8_t* o = (uint8_t*)buf;
     auto put = [&](const void* p, uint64_t k) { memcpy(o, p, k); o += k; };
     auto u32 = [&](uint32_t v) { put(&v, 4); };
@@ -2315,6 +2351,7 @@ gputx_status gputx_reset(gputx_db* db) {
     for (auto& c : db->cols)
         CK(cudaMemcpyAsync(c.d, c.pristine, c.spec.count * c.spec.elem, cudaMemcpyDeviceToDevice, db->stream));
     for (auto& t : db->ins) { t.rows = 0; t.pending = 0; }
+    TRY(tm1_rows_pack(db));
     CK(cudaStreamSynchronize(db->stream));
     db->poisoned = false;
     db->submitted = false;
@@ -2350,6 +2387,7 @@ void gputx_close_db(gputx_db* db) {
                   db->d_hstatus, db->d_hout, db->d_wseg, db->d_wst};
     for (void* p : ps) dfree(db, p);
     dfree(db, db->d_order);
+    dfree(db, db->tm1_sub); dfree(db, db->tm1_ai); dfree(db, db->tm1_sf); dfree(db, db->tm1_cf);
     dfree(db, db->d_undo);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
                   db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,

@@ -2643,3 +2643,62 @@ __global__ void p2p_wait_kernel(uint32_t* arena, uint32_t off_flags, uint32_t of
     }
 }
 }  // namespace gputx
+
+namespace gputx {
+// TM-1 row groups <-> columns (schema.cuh "TM-1 rows"): pack all fields at seal / reset,
+// unpack the mutable ones (vlr, bits, sf.data_a, cf live / end / numberx) before a read
+__global__ void __launch_bounds__(256) tm1_pack_kernel(DevDb db) {
+    const uint32_t P = db.dims[0];
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < P; s += gridDim.x * blockDim.x) {
+        uint8_t* r = db.tm1_sub + (uint64_t)s * TM1_SUBROW;
+        *reinterpret_cast<uint64_t*>(r) = COL(const uint64_t, M_NBR)[s];
+        *reinterpret_cast<uint64_t*>(r + 8) = COL(const uint64_t, M_HEX)[s];
+        *reinterpret_cast<uint32_t*>(r + 16) = COL(const uint32_t, M_MSC)[s];
+        *reinterpret_cast<uint32_t*>(r + 20) = COL(const uint32_t, M_VLR)[s];
+        *reinterpret_cast<uint16_t*>(r + 24) = COL(const uint16_t, M_BITS)[s];
+        for (int k = 0; k < 10; ++k) r[26 + k] = COL(const uint8_t, M_BYTE2)[(uint64_t)s * 10 + k];
+        for (int k = 36; k < (int)TM1_SUBROW; ++k) r[k] = 0;
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint64_t f = (uint64_t)s * 4 + j;
+            uint8_t* a = db.tm1_ai + f * TM1_AIROW;
+            a[0] = COL(const uint8_t, M_AI_VALID)[f]; a[1] = COL(const uint8_t, M_AI_D1)[f];
+            a[2] = COL(const uint8_t, M_AI_D2)[f]; a[3] = 0;
+            *reinterpret_cast<uint32_t*>(a + 4) = COL(const uint32_t, M_AI_D3)[f];
+            *reinterpret_cast<uint64_t*>(a + 8) = COL(const uint64_t, M_AI_D4)[f];
+            uint8_t* g = db.tm1_sf + f * TM1_SFROW;
+            g[0] = COL(const uint8_t, M_SF_VALID)[f]; g[1] = COL(const uint8_t, M_SF_ACTIVE)[f];
+            g[2] = COL(const uint8_t, M_SF_ERR)[f]; g[3] = COL(const uint8_t, M_SF_DA)[f];
+            *reinterpret_cast<uint32_t*>(g + 4) = 0;
+            *reinterpret_cast<uint64_t*>(g + 8) = COL(const uint64_t, M_SF_DB)[f];
+            uint8_t* c = db.tm1_cf + f * TM1_CFROW;
+            for (int k = 0; k < 16; ++k) c[k] = 0;
+            for (int k = 0; k < 3; ++k) {
+                c[k] = COL(const uint8_t, M_CF_LIVE)[f * 3 + k];
+                c[4 + k] = COL(const uint8_t, M_CF_END)[f * 3 + k];
+                *reinterpret_cast<uint64_t*>(c + 16 + 8 * k) = COL(const uint64_t, M_CF_NUM)[f * 3 + k];
+            }
+            *reinterpret_cast<uint64_t*>(c + 40) = 0;
+            *reinterpret_cast<uint64_t*>(c + 48) = 0;
+            *reinterpret_cast<uint64_t*>(c + 56) = 0;
+        }
+    }
+}
+__global__ void __launch_bounds__(256) tm1_unpack_kernel(DevDb db) {
+    const uint32_t P = db.dims[0];
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < P; s += gridDim.x * blockDim.x) {
+        const uint8_t* r = db.tm1_sub + (uint64_t)s * TM1_SUBROW;
+        COL(uint32_t, M_VLR)[s] = *reinterpret_cast<const uint32_t*>(r + 20);
+        COL(uint16_t, M_BITS)[s] = *reinterpret_cast<const uint16_t*>(r + 24);
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint64_t f = (uint64_t)s * 4 + j;
+            COL(uint8_t, M_SF_DA)[f] = db.tm1_sf[f * TM1_SFROW + 3];
+            const uint8_t* c = db.tm1_cf + f * TM1_CFROW;
+            for (int k = 0; k < 3; ++k) {
+                COL(uint8_t, M_CF_LIVE)[f * 3 + k] = c[k];
+                COL(uint8_t, M_CF_END)[f * 3 + k] = c[4 + k];
+                COL(uint64_t, M_CF_NUM)[f * 3 + k] = *reinterpret_cast<const uint64_t*>(c + 16 + 8 * k);
+            }
+        }
+    }
+}
+}  // namespace gputx

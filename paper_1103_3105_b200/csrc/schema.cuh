@@ -68,6 +68,7 @@ struct DevDb {
     uint32_t idx_base;                 // emit: record idx = idx_base + i (pool arrivals; 0 otherwise)
     struct UndoRec* undo;              // per-transaction undo-log slots (non-two-phase types)
     uint32_t ins_dense;                // TPC-B: every transaction is a home deposit -> history row = idx
+    uint8_t *tm1_sub, *tm1_ai, *tm1_sf, *tm1_cf;   // TM-1 row groups (tm1_txn)
 };
 
 // Undo log: written in GPU memory before each update of a NON-two-phase
@@ -291,46 +292,48 @@ DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p) {
 }
 
 // ---- TM-1 --------------------------------------------------------------------------
+// TM-1 rows (DESIGN.md §5 "TM-1 row groups"): the fields one TATP procedure reads lie in
+// one aligned row, so a transaction moves 1-3 sectors with 16-byte vector loads instead of
+// ~10 scattered column accesses (the wide 0-set round was bound by L1 wavefronts: 23
+// sectors per warp request).  The column store stays the interface (load / read / reset);
+// rows are built at seal and after a reset, and unpacked into the mutable columns before
+// they are read.
+//   SUB (64 B)  [0] nbr u64 [8] hex u64 [16] msc u32 [20] vlr u32 [24] bits u16 [26] byte2[10]
+//               -- bytes [0, 36) are exactly GSD's output record
+//   AI  (16 B)  [0] valid [1] data1 [2] data2 [4] data3 u32 [8] data4 u64
+//   SF  (16 B)  [0] valid [1] active [2] error [3] data_a [8] data_b u64
+//   CF  (64 B per (s, sf)) [0..3) live, [4..7) end_time, [16 + 8k] numberx of start 8k
+constexpr uint32_t TM1_SUBROW = 64, TM1_AIROW = 16, TM1_SFROW = 16, TM1_CFROW = 64;
+
 DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     uint8_t* o = db.out + (uint64_t)idx * 40;
     switch (t) {
-    case 0: {   // GET_SUBSCRIBER_DATA
+    case 0: {   // GET_SUBSCRIBER_DATA: the row's first 36 bytes are the output record
         const uint32_t s = p[0] - 1;
-        const uint64_t nbr = __ldg(&COL(const uint64_t, M_NBR)[s]);
-        const uint64_t hex = __ldg(&COL(const uint64_t, M_HEX)[s]);
-        const uint32_t msc = __ldg(&COL(const uint32_t, M_MSC)[s]);
-        const uint32_t vlr = ldm(&COL(uint32_t, M_VLR)[s]);
-        const uint16_t bits = ldm(&COL(uint16_t, M_BITS)[s]);
-        const uint16_t* b2 = reinterpret_cast<const uint16_t*>(COL(const uint8_t, M_BYTE2) + (uint64_t)s * 10);
-        uint16_t bb[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) bb[k] = __ldg(b2 + k);
-        put64(o, nbr);
-        put64(o + 8, hex);
-        put32(o + 16, msc);
-        put32(o + 20, vlr);
-        reinterpret_cast<uint16_t*>(o)[12] = bits;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) reinterpret_cast<uint16_t*>(o)[13 + k] = bb[k];
+        const uint4* row = reinterpret_cast<const uint4*>(db.tm1_sub + (uint64_t)s * TM1_SUBROW);
+        const uint4 a = row[0], b = row[1], c = row[2];        // (vlr, bits live in b: weak loads)
+        uint2* q = reinterpret_cast<uint2*>(o);                // out + idx*40 is 8-byte aligned
+        q[0] = make_uint2(a.x, a.y);
+        q[1] = make_uint2(a.z, a.w);
+        q[2] = make_uint2(b.x, b.y);
+        q[3] = make_uint2(b.z, b.w);
+        q[4] = make_uint2(c.x, 0u);
         return;
     }
     case 1: {   // GET_NEW_DESTINATION
         const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
-        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
-        const uint8_t active = __ldg(&COL(const uint8_t, M_SF_ACTIVE)[f]);
-        uint8_t live[3], endt[3];
-        uint64_t num[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            live[k] = ldm(&COL(uint8_t, M_CF_LIVE)[f * 3 + k]);
-            endt[k] = ldm(&COL(uint8_t, M_CF_END)[f * 3 + k]);
-            num[k] = ldm(&COL(uint64_t, M_CF_NUM)[f * 3 + k]);
-        }
+        const uint4 sf = *reinterpret_cast<const uint4*>(db.tm1_sf + f * TM1_SFROW);
+        const uint4* cf = reinterpret_cast<const uint4*>(db.tm1_cf + f * TM1_CFROW);
+        const uint4 h = cf[0], n01 = cf[1], n2 = cf[2];
+        const uint32_t valid = sf.x & 0xFFu, active = (sf.x >> 8) & 0xFFu;
         if (!valid || !active) { db.status[idx] = 1; return; }
+        const uint64_t num[3] = {(uint64_t)n01.x | ((uint64_t)n01.y << 32), (uint64_t)n01.z | ((uint64_t)n01.w << 32),
+                                 (uint64_t)n2.x | ((uint64_t)n2.y << 32)};
         uint32_t cnt = 0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            if (live[k] && (uint32_t)k * 8 <= p[2] && p[3] < endt[k]) {
+            const uint32_t live = (h.x >> (8 * k)) & 0xFFu, endt = (h.y >> (8 * k)) & 0xFFu;
+            if (live && (uint32_t)k * 8 <= p[2] && p[3] < endt) {
                 put64(o + 8 + 8 * cnt, num[k]);
                 ++cnt;
             }
@@ -341,52 +344,48 @@ DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
     }
     case 2: {   // GET_ACCESS_DATA
         const uint64_t a = (uint64_t)(p[0] - 1) * 4 + (p[1] - 1);
-        const uint8_t valid = __ldg(&COL(const uint8_t, M_AI_VALID)[a]);
-        const uint8_t d1 = __ldg(&COL(const uint8_t, M_AI_D1)[a]);
-        const uint8_t d2 = __ldg(&COL(const uint8_t, M_AI_D2)[a]);
-        const uint32_t d3 = __ldg(&COL(const uint32_t, M_AI_D3)[a]);
-        const uint64_t d4 = __ldg(&COL(const uint64_t, M_AI_D4)[a]);
-        if (!valid) { db.status[idx] = 1; return; }
-        put32(o, (uint32_t)d1 | ((uint32_t)d2 << 8));
-        put32(o + 4, d3);
-        put64(o + 8, d4);
+        const uint4 r = *reinterpret_cast<const uint4*>(db.tm1_ai + a * TM1_AIROW);
+        if (!(r.x & 0xFFu)) { db.status[idx] = 1; return; }
+        uint2* q = reinterpret_cast<uint2*>(o);
+        q[0] = make_uint2((r.x >> 8) & 0xFFFFu, r.y);          // data1, data2 | data3
+        q[1] = make_uint2(r.z, r.w);                            // data4
         return;
     }
     case 3: {   // UPDATE_SUBSCRIBER_DATA (two-phase: SF existence first)
         const uint32_t s = p[0] - 1;
         const uint64_t f = (uint64_t)s * 4 + (p[1] - 1);
-        uint16_t* bits = COL(uint16_t, M_BITS);
-        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
-        const uint16_t b = ldm(&bits[s]);
+        uint16_t* bits = reinterpret_cast<uint16_t*>(db.tm1_sub + (uint64_t)s * TM1_SUBROW + 24);
+        const uint8_t valid = db.tm1_sf[f * TM1_SFROW];
+        const uint16_t b = ldm(bits);
         if (!valid) { db.status[idx] = 1; return; }
-        stm(&bits[s], (uint16_t)((b & 0xFFFEu) | (p[2] & 1u)));
-        stm(&COL(uint8_t, M_SF_DA)[f], (uint8_t)p[3]);
+        stm(bits, (uint16_t)((b & 0xFFFEu) | (p[2] & 1u)));
+        stm(db.tm1_sf + f * TM1_SFROW + 3, (uint8_t)p[3]);
         return;
     }
     case 4: {   // UPDATE_LOCATION (sub_nbr resolved at submit)
         if (p[0] == 0) { db.status[idx] = 1; return; }
-        stm(&COL(uint32_t, M_VLR)[p[0] - 1], p[2]);
+        stm(reinterpret_cast<uint32_t*>(db.tm1_sub + (uint64_t)(p[0] - 1) * TM1_SUBROW + 20), p[2]);
         return;
     }
     case 5: {   // INSERT_CALL_FORWARDING
         if (p[0] == 0) { db.status[idx] = 1; return; }
         const uint64_t f = (uint64_t)(p[0] - 1) * 4 + (p[2] - 1);
-        const uint64_t c = f * 3 + p[3] / 8;
-        uint8_t* live = COL(uint8_t, M_CF_LIVE);
-        const uint8_t valid = __ldg(&COL(const uint8_t, M_SF_VALID)[f]);
-        const uint8_t lv = ldm(&live[c]);
+        const uint32_t k = p[3] / 8;
+        uint8_t* cf = db.tm1_cf + f * TM1_CFROW;
+        const uint8_t valid = db.tm1_sf[f * TM1_SFROW];
+        const uint8_t lv = ldm(cf + k);
         if (!valid || lv) { db.status[idx] = 1; return; }
-        stm(&live[c], (uint8_t)1);
-        stm(&COL(uint8_t, M_CF_END)[c], (uint8_t)p[4]);
-        stm(&COL(uint64_t, M_CF_NUM)[c], (uint64_t)p[5] | ((uint64_t)p[6] << 32));
+        stm(cf + k, (uint8_t)1);
+        stm(cf + 4 + k, (uint8_t)p[4]);
+        stm(reinterpret_cast<uint64_t*>(cf + 16 + 8 * k), (uint64_t)p[5] | ((uint64_t)p[6] << 32));
         return;
     }
     case 6: {   // DELETE_CALL_FORWARDING
         if (p[0] == 0) { db.status[idx] = 1; return; }
-        const uint64_t c = ((uint64_t)(p[0] - 1) * 4 + (p[2] - 1)) * 3 + p[3] / 8;
-        uint8_t* live = COL(uint8_t, M_CF_LIVE);
-        if (!ldm(&live[c])) { db.status[idx] = 1; return; }
-        stm(&live[c], (uint8_t)0);
+        uint8_t* cf = db.tm1_cf + ((uint64_t)(p[0] - 1) * 4 + (p[2] - 1)) * TM1_CFROW;
+        const uint32_t k = p[3] / 8;
+        if (!ldm(cf + k)) { db.status[idx] = 1; return; }
+        stm(cf + k, (uint8_t)0);
         return;
     }
     }

@@ -45,10 +45,14 @@ for k in order:
 w = np.where(raw[:, 6] > 0, raw[:, 6] - ns, 0)[:-1]
 s1 = np.where(raw[:, 1] > 0, raw[:, 1] - ns, 0)[:-1]
 print(f"  mean us: work-issued {w.mean() / 1e3:.2f} signalled {s1.mean() / 1e3:.2f} round {dt.mean() / 1e3:.2f}")
+lstart = np.where(raw[:, 5] > 0, raw[:, 5] - ns, 0)[:-1]
+lwork = np.where(raw[:, 7] > 0, raw[:, 7] - ns, 0)[:-1]
 for lo, hi in [(0, 1), (1, 9), (9, 33), (33, 129), (129, 1025), (1025, 10**9)]:
     m = (sizes[:-1] >= lo) & (sizes[:-1] < hi)
     if m.any():
-        print(f"  size [{lo},{hi}): rounds {m.sum():6d} total_us {dt[m].sum() / 1e3:9.1f} mean_us {dt[m].mean() / 1e3:7.2f}")
+        print(f"  size [{lo},{hi}): rounds {m.sum():6d} total_us {dt[m].sum() / 1e3:9.1f} mean_us {dt[m].mean() / 1e3:7.2f}"
+              f"  cta0 issued {w[m].mean() / 1e3:6.2f} signalled {s1[m].mean() / 1e3:6.2f} last start"
+              f" {lstart[m].mean() / 1e3:6.2f} last issued {lwork[m].mean() / 1e3:6.2f}")
 print("  k, size, dt_us (every few rounds):")
 step = max(1, nk // 40)
 print("  " + " ".join(f"{k}:{sizes[k]}:{dt[k] / 1e3:.2f}" for k in range(0, nk - 1, step)))

@@ -554,6 +554,25 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     e2e_committed = sum_over_ranks(float(e2e_committed))
     h2d = int(np.mean([b.nbytes() for b in hb]))
     d2h = int(np.mean([b.type.shape[0] for b in hb])) * (1 + db.stride)
+    # the link the e2e number is bound by: pinned copies of one step's bytes, each direction
+    # alone (outside every timed region); the overlapped e2e step can't beat max(H2D, D2H)
+    pcie = {}
+    for name, nbytes, hd in (("h2d_gbs", h2d, True), ("d2h_gbs", d2h, False)):
+        hbuf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        dbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c1 = torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            (dbuf.copy_(hbuf, non_blocking=True) if hd else hbuf.copy_(dbuf, non_blocking=True))
+            c1.record(stream)
+            c1.synchronize()
+            best = min(best, c0.elapsed_time(c1))
+        pcie[name] = nbytes / (best / 1e3) / 1e9
+        del hbuf, dbuf
+    pcie["transfer_floor_ms"] = max(h2d / pcie["h2d_gbs"], d2h / pcie["d2h_gbs"]) / 1e6
 
     # ---- other strategies on the same bulks ------------------------------------------
     others = {}
@@ -622,7 +641,10 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         "ms_per_step": total_ms / args.steps, "all_txn_per_s": allt / (total_ms / 1e3),
         "parity": parity if parity is not None else "not checked (N>1: tests/test_gpu_shard.py)",
         "e2e": {"value": e2e_committed / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps, "pcie": pcie,
+                "method": ("gputx_run_bulks: H2D of bulk i+1 and D2H of bulk i-1 overlap bulk i (two copy "
+                           "streams); back-to-back bulks, no L2 flush in between") if ws == 1 else
+                          "per step: H2D, sharded step, D2H (serial)"},
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
         "phases_ms": phase,
         "graph": {"depth": last["depth"], "zero_set": last["zero_set"], "records": last["records"],

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>         // header-only NVTX ranges: phases visible to nsys / ncu --nvtx
+
 #include "../../include/gputx.h"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -296,6 +298,12 @@ void dfree(gputx_db* db, void* p) {
             if (e_ != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
         }                                                                                       \
     } while (0)
+// NVTX range per pipeline phase (host side; ncu --nvtx --nvtx-include "gputx.rank/" etc.)
+struct NvtxRange {
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define NVTX_SCOPE(name) NvtxRange nvtx_scope_(name)
 #define TRY(x)                              \
     do {                                    \
         gputx_status s_ = (x);              \
@@ -414,6 +422,7 @@ gputx_status sort_records(gputx_db* db, uint32_t lo, uint32_t nbits, const uint3
 // the depth reduction giving d = max depth and w0 = |0-set|
 template <int S>
 gputx_status kset_rank(gputx_db* db, const DevDb& v) {
+    NVTX_SCOPE("gputx.kset.emit_sort_rank");
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
     TRY(emit_records<S>(db, v));
@@ -533,6 +542,7 @@ bool kset_use_dataflow(const gputx_db* db) {
 // K-SET part 2: group by (depth, type), then the k-set rounds
 template <int S>
 gputx_status kset_exec(gputx_db* db, const DevDb& v) {
+    NVTX_SCOPE("gputx.kset.group_exec");
     cudaStream_t s = db->stream;
     const uint32_t T = db->ntypes;
     group_nkeys_kernel<<<1, 1, 0, s>>>(db->d_sc, T);
@@ -661,6 +671,7 @@ gputx_status run_kset(gputx_db* db, const DevDb& v) {
 // count_cross = false: GPUTX_AUTO counted c already
 template <int S>
 gputx_status run_part(gputx_db* db, const DevDb& v, bool count_cross = true) {
+    NVTX_SCOPE("gputx.part");
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
@@ -697,6 +708,7 @@ gputx_status run_part(gputx_db* db, const DevDb& v, bool count_cross = true) {
 // K-SET analysis first; TPL's records are the same)
 template <int S>
 gputx_status run_tpl(gputx_db* db, const DevDb& v, bool sorted = false) {
+    NVTX_SCOPE("gputx.tpl");
     cudaStream_t s = db->stream;
     if (!sorted) {
         cudaEventRecord(db->ev[1], s);
@@ -1517,6 +1529,7 @@ gputx_status gputx_register_types(gputx_db* db, const uint32_t* ids, uint32_t k)
 
 gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
     if (!db || !b) return GPUTX_EINVAL;
+    NVTX_SCOPE("gputx.submit");
     if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "sharded handle: submit with gputx_shard_pack + gputx_shard_submit");
     TRY(submit_check(db, b));
     cudaStream_t s = db->stream;
@@ -1781,6 +1794,7 @@ void p2p_dispatch_launch(gputx_db* db, uint32_t nh) {
 
 gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
     if (!db || !b) return GPUTX_EINVAL;
+    NVTX_SCOPE("gputx.shard_dispatch");
     if (!db->p2p) return fail(db, GPUTX_ESTATE, "gputx_shard_connect first");
     cudaStream_t s = db->stream;
     ++db->xepoch;                      // every shard dispatches once per bulk: epochs agree
@@ -1833,6 +1847,7 @@ gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
 
 gputx_status gputx_shard_receive(gputx_db* db, uint64_t* n_local) {
     if (!db) return GPUTX_EINVAL;
+    NVTX_SCOPE("gputx.shard_receive");
     if (!db->p2p || !db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_dispatch first");
     cudaStream_t s = db->stream;
     CK(cudaMemsetAsync(db->d_sc + SC_DEADLOCK, 0, 4, s));
@@ -1923,6 +1938,7 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
 
 gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
     if (!db) return GPUTX_EINVAL;
+    NVTX_SCOPE("gputx.execute");
     if (!db->submitted) return fail(db, GPUTX_ESTATE, "nothing submitted");
     if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET && st != GPUTX_AUTO && st != GPUTX_TPL_RELAXED &&
         st != GPUTX_PART_RELAXED)
@@ -2156,6 +2172,7 @@ gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* b, uint64_t* firs
 
 gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* executed) {
     if (!db) return GPUTX_EINVAL;
+    NVTX_SCOPE("gputx.pool_step");
     if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
     if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
     if (!db->pool_n) {

@@ -32,6 +32,10 @@ def cases():
     for lg in (12, 16, 20):
         for th in (0.0, 0.9):
             yield f"tpcb_n2^{lg}_zipf{th}", W.TPCB, d, 1 << lg, dict(remote_pct=15.0, zipf_theta=th), False
+    # the micro benchmark: lock skew alpha, cheap procedures (x = 1)
+    m = W.MicroDims(1 << 20, 8, 1)
+    for a in (0.0, 0.01, 0.1):
+        yield f"micro_alpha{a}", W.MICRO, m, 1 << 16, dict(alpha=a), False
 
 
 def choose(w0, d, c, w0b, db, cb):
@@ -79,18 +83,30 @@ def main():
         row["best"] = max(("kset", "part", "tpl"), key=lambda s: row[s])
         print(json.dumps(row), flush=True)
         rows.append(row)
-    grid_w0 = [0, 1_000, 10_000, 18_944, 100_000, 500_000, 1_000_000, 4_000_000, INF]
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    grid_w0 = sorted({0, 1_000, 64 * nsm, 10_000, 128 * nsm, 100_000, 500_000, 1_000_000, 4_000_000, INF})
     grid_d = [0, 64, 256, 1_024, 2_048, 8_192, 65_536, 1 << 20, INF]
     grid_c = [0, 100, 10_000, 100_000, 1_000_000, INF]
 
-    def score(b):
-        return statistics.mean(r[choose(r["w0"], r["d"], r["c"], *b)] / r[r["best"]] for r in rows)
+    def score(b, rs=None):
+        rs = rows if rs is None else rs
+        return statistics.mean(r[choose(r["w0"], r["d"], r["c"], *b)] / r[r["best"]] for r in rs)
 
-    best = max(itertools.product(grid_w0, grid_d, grid_c), key=score)
-    default = (18_944, 2_048, 0)
-    res = {"rows": rows, "default": {"w0_bar": default[0], "d_bar": default[1], "c_bar": default[2],
-                                     "mean_efficiency": score(default)},
+    grid = list(itertools.product(grid_w0, grid_d, grid_c))
+    best = max(grid, key=score)
+    # held-out efficiency: leave each bulk out, fit on the others, score it alone
+    loo = []
+    for k, r in enumerate(rows):
+        rest = rows[:k] + rows[k + 1:]
+        fit = max(grid, key=lambda b: score(b, rest))
+        loo.append(score(fit, [r]))
+    default = (64 * nsm, 0, 0)                    # the library's defaults (engine.cu choose_strategy)
+    paper = (128 * nsm, 2_048, 0)                 # an uncalibrated reading
+    res = {"rows": rows, "library_default": {"w0_bar": default[0], "d_bar": default[1], "c_bar": default[2],
+                                             "mean_efficiency": score(default)},
+           "uncalibrated": {"w0_bar": paper[0], "d_bar": paper[1], "c_bar": paper[2], "mean_efficiency": score(paper)},
            "calibrated": {"w0_bar": best[0], "d_bar": best[1], "c_bar": best[2], "mean_efficiency": score(best)},
+           "leave_one_out_mean_efficiency": statistics.mean(loo),
            "oracle_best_mean_efficiency": 1.0}
     print(json.dumps({k: v for k, v in res.items() if k != "rows"}), flush=True)
     json.dump(res, open(args.out, "w"), indent=1)

@@ -66,6 +66,31 @@ DEV uint32_t atom_add_release(uint32_t* p, uint32_t v) {
 }
 
 // ---------------------------------------------------------------------------------
+// dev_fill: cudaMemsetAsync's signature, done by a kernel.  A memset may be serviced by a
+// copy engine and then waits behind an in-flight bulk transfer in the same direction
+// (gputx_run_bulks overlaps a bulk's result D2H with the next bulk's execution).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fill_bytes_kernel(uint8_t* p, uint32_t v8, uint64_t bytes) {
+    const uint64_t head = (16 - ((uintptr_t)p & 15)) & 15;
+    const uint64_t h = head < bytes ? head : bytes;
+    const uint64_t n16 = (bytes - h) / 16;
+    const uint32_t w = v8 * 0x01010101u;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+    if (tid < h) p[tid] = (uint8_t)v8;
+    uint4* q = reinterpret_cast<uint4*>(p + h);
+    for (uint64_t i = tid; i < n16; i += nt) q[i] = make_uint4(w, w, w, w);
+    for (uint64_t i = h + n16 * 16 + tid; i < bytes; i += nt) p[i] = (uint8_t)v8;
+}
+inline cudaError_t dev_fill(void* p, int value, size_t bytes, cudaStream_t s) {
+    if (!bytes) return cudaSuccess;
+    uint64_t blocks = (bytes / 16 + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    fill_bytes_kernel<<<(unsigned)blocks, 256, 0, s>>>((uint8_t*)p, (uint32_t)(value & 0xFF), (uint64_t)bytes);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
 // Grid barrier for a cooperative launch (all CTAs co-resident).  gen is bumped by
 // the last arriver; waiters poll it with acquire loads.
 // ---------------------------------------------------------------------------------

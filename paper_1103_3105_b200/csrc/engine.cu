@@ -142,6 +142,7 @@ struct gputx_db {
     int kset_df = -1;                   // K-SET executor: 1 dataflow, 0 rounds, -1 schema default
     bool kset_ran_df = false;
     bool ins_dense = false;
+    uint32_t* h_sc_dev = nullptr;       // device alias of the mapped host counters
     uint8_t *tm1_sub = nullptr, *tm1_ai = nullptr, *tm1_sf = nullptr, *tm1_cf = nullptr;   // TM-1 row groups
     bool rows_dirty = false;            // TM-1: rows hold newer mutable fields than the columns
     // gputx_run_bulks: copy streams and double-buffered device slots (lazily created)
@@ -258,6 +259,15 @@ gputx_status fail(gputx_db* db, gputx_status s, const std::string& m) {
     return s;
 }
 
+// device counters -> mapped host counters (kernel stores, no copy engine); read by the host
+// after it synchronises the stream
+gputx_status pull_sc(gputx_db* db, cudaStream_t s) {
+    pull_sc_kernel<<<1, 64, 0, s>>>(db->d_sc, db->h_sc_dev, SC_COUNT);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("pull_sc: ") + cudaGetErrorString(e));
+    return GPUTX_OK;
+}
+
 // the first bad transaction of the last validating kernel and its error code (report_err)
 uint64_t err_packed(const gputx_db* db) {
     return (uint64_t)db->h_sc[SC_ERRPK] | ((uint64_t)db->h_sc[SC_ERRPK + 1] << 32);
@@ -312,7 +322,7 @@ struct NvtxRange {
 
 uint32_t* next_ticket(gputx_db* db) {
     // 256 ticket counters zeroed together; a slot is used once per memset cycle
-    if (db->ticket_slot == 0) cudaMemsetAsync(db->d_tickets, 0, 256 * sizeof(uint32_t), db->stream);
+    if (db->ticket_slot == 0) dev_fill(db->d_tickets, 0, 256 * sizeof(uint32_t), db->stream);
     uint32_t* t = db->d_tickets + db->ticket_slot;
     db->ticket_slot = (db->ticket_slot + 1) & 255u;
     return t;
@@ -455,13 +465,13 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     STAGE("sort");
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
-    CK(cudaMemsetAsync(db->d_D, 0, db->n * sizeof(uint32_t), s));
-    CK(cudaMemsetAsync(&db->d_bar->dead, 0, sizeof(uint32_t), s));
+    CK(dev_fill(db->d_D, 0, db->n * sizeof(uint32_t), s));
+    CK(dev_fill(&db->d_bar->dead, 0, sizeof(uint32_t), s));
     if (windowed) {
         win_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, wb,
                                                                              nwin, db->d_wseg);
         ++db->launches;
-        CK(cudaMemsetAsync(db->d_wst, 0xFF, db->n_items * sizeof(int2), s));     // (-1, -1): no access yet
+        CK(dev_fill(db->d_wst, 0xFF, db->n_items * sizeof(int2), s));     // (-1, -1): no access yet
         const uint64_t* keys = db->d_sorted;
         const uint32_t* seg = db->d_wseg;
         uint32_t nw = nwin;
@@ -509,7 +519,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
         RkMemo memo = db->rank_memo;
         memo.rec_off = db->d_rec_off;
         uint64_t* rtrace = db->trace_rounds ? db->d_rtrace : nullptr;
-        if (rtrace) CK(cudaMemsetAsync(rtrace, 0, RANK_TRACE_SLOTS * 8, s));
+        if (rtrace) CK(dev_fill(rtrace, 0, RANK_TRACE_SLOTS * 8, s));
         if (db->rank_root) {             // root-local sweeps (TM-1: single-root transactions)
             DevDb vv = v;
             void* rargs[] = {&vv, &keys, &nrec, &D, &bar, &sc, &maxp, &rtrace, &lb, &epoch0, &lmax, &dirty, &memo};
@@ -601,7 +611,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
         uint32_t G = db->exec_grid_override ? std::min(db->exec_grid_override, Gv) : Gv;
         if (db->kset_cluster) G = std::max(db->kset_cluster, G / db->kset_cluster * db->kset_cluster);
         uint32_t* done = db->d_done;
-        if (db->kset_diag & 16u) CK(cudaMemsetAsync(done, 0, db->n * 4, s));
+        if (db->kset_diag & 16u) CK(dev_fill(done, 0, db->n * 4, s));
         kset_sched_kernel<<<grid_for(db->n, 256, 148 * 4), 256, 0, s>>>(db->d_goff, T, db->d_sc, G, db->kset_q,
                                                                          db->d_g, (db->kset_diag & 16u) ? nullptr : done);
         ++db->launches;
@@ -614,7 +624,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
         const uint8_t* pt = db->d_ptype;
         const uint32_t* pp = db->d_pp;
         uint64_t* trace = db->trace_rounds ? db->d_trace : nullptr;
-        if (trace) CK(cudaMemsetAsync(trace, 0, (db->n + 1) * 64, s));
+        if (trace) CK(dev_fill(trace, 0, (db->n + 1) * 64, s));
         uint32_t diag = db->kset_diag;
         uint32_t C = db->kset_cluster;
         if (diag & 64u) {                 // diagnostics: run on freshly allocated metadata buffers
@@ -627,7 +637,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
                 cudaMalloc(&fg, fcap * 2); cudaMalloc(&fdone, fcap * 4); cudaMalloc(&foff, fcap * 4);
             }
             cudaMemcpyAsync(fg, db->d_g, db->n * 2, cudaMemcpyDeviceToDevice, s);
-            cudaMemsetAsync(fdone, 0, db->n * 4, s);
+            dev_fill(fdone, 0, db->n * 4, s);
             cudaMemcpyAsync(foff, db->d_goff, (db->n * T + 1) * 4, cudaMemcpyDeviceToDevice, s);
             gk = fg; done = fdone; off = foff;
         }
@@ -752,7 +762,7 @@ template <int S>
 gputx_status run_tpl_relaxed(gputx_db* db, const DevDb& v) {
     cudaStream_t s = db->stream;
     cudaEventRecord(db->ev[1], s);
-    CK(cudaMemsetAsync(db->d_lock, 0, db->n_items * 4, s));          // spin locks free
+    CK(dev_fill(db->d_lock, 0, db->n_items * 4, s));          // spin locks free
     for (int k = 2; k < 6; ++k) cudaEventRecord(db->ev[k], s);
     tpl_relaxed_kernel<S><<<(uint32_t)((db->n + 127) / 128), 128, 0, s>>>(v, nullptr, nullptr, db->d_lock,
                                                                           db->d_order, 0, db->d_sc);
@@ -767,7 +777,7 @@ gputx_status run_part_relaxed(gputx_db* db, const DevDb& v) {
     cudaStream_t s = db->stream;
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     cudaEventRecord(db->ev[1], s);
-    CK(cudaMemsetAsync(db->d_part_off, 0, ((uint64_t)db->nparts + 1) * 4, s));
+    CK(dev_fill(db->d_part_off, 0, ((uint64_t)db->nparts + 1) * 4, s));
     // bulk generation without sort: per-partition counters -> keys, prefix sum -> starts
     rpart_key_kernel<S><<<g, 256, 0, s>>>(v, db->d_part_off, db->d_D, db->d_perm, db->d_cnt, db->d_sc);
     scan_u32(db, db->d_part_off, db->d_part_off, nullptr, db->nparts, db->d_sc + SC_NFRAG);
@@ -779,8 +789,8 @@ gputx_status run_part_relaxed(gputx_db* db, const DevDb& v) {
         v, db->d_rec_off, db->d_part_off, np, db->d_order, db->d_sc);
     // cross-partition transactions afterwards under the basic spin locks;
     // their serialization numbers follow the single-partition ones (base = #single)
-    CK(cudaMemsetAsync(db->d_lock, 0, db->n_items * 4, s));
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    CK(dev_fill(db->d_lock, 0, db->n_items * 4, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     const uint32_t ncross = db->h_sc[SC_XTOTAL];
     if (ncross)
@@ -806,7 +816,7 @@ gputx_status run_auto(gputx_db* db, const DevDb& v) {
     cross_count_kernel<S><<<grid_for(db->n, 256, 148 * 8), 256, 0, s>>>(v, db->d_sc + SC_CROSS);
     ++db->launches;
     TRY(kset_rank<S>(db, v));                               // line 1: w0 (and d)
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_NOCONV]) return fail(db, GPUTX_ECUDA, "rank did not converge");
     const gputx_strategy ch = choose_strategy(db, db->h_sc[SC_ZERO], db->h_sc[SC_MAXD], db->h_sc[SC_CROSS]);
@@ -856,13 +866,13 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     db->launches = 0;
     db->has_depth = db->has_perm = false;
     db->executed = false;
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
     const bool ins_scan = db->schema == S_TPCC || db->schema == S_TPCB || db->has_ts;
     const int ntab = db->schema == S_TPCC ? 4 : 1;
     if (n) {
-        if (ins_scan) CK(cudaMemsetAsync(db->d_ins_off, 0, 4 * (n + 1) * ntab, s));
-        if (db->nshards > 1) CK(cudaMemsetAsync(db->d_xflag, 0, n, s));
+        if (ins_scan) CK(dev_fill(db->d_ins_off, 0, 4 * (n + 1) * ntab, s));
+        if (db->nshards > 1) CK(dev_fill(db->d_xflag, 0, n, s));
         const uint32_t* nw_ptr = nullptr;
         if (pw_src) {
             nw_ptr = db->d_poff + n;
@@ -880,7 +890,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
                          db->d_sc + SC_INS0 + t);
     }
     cudaEventRecord(db->ev_sub[1], s);
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR]) {
         static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
@@ -937,9 +947,9 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     cudaStream_t s = db->stream;
     const uint32_t ntab = (uint32_t)db->ins.size();
     // 1. ingest the arrivals in the staging area (validation, split lookups, insert counts)
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
-    if (ntab) CK(cudaMemsetAsync(db->st_ins, 0, 4 * (m + 1) * ntab, s));
+    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    if (ntab) CK(dev_fill(db->st_ins, 0, 4 * (m + 1) * ntab, s));
     DevDb v = make_devdb(db);
     v.n = (uint32_t)m;
     v.type = db->s_type;
@@ -949,7 +959,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     const uint32_t g = grid_for(m, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, s>>>(v, db->s_pw, words, nullptr, db->type_mask, db->st_ins, (uint32_t)(m + 1),
                                        db->d_sc, nullptr);
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
         return fail(db, err_code(db) <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
@@ -978,7 +988,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
                                                                   db->d_sc + SC_NREC, db->d_prec2);
     std::swap(db->d_prec, db->d_prec2);
     db->launches += 6;
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     db->pool_nrec += db->h_sc[SC_NREC];
     db->pool_n += m;
@@ -994,7 +1004,7 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
     const uint32_t g = grid_for(std::max(n, nrec), 256, 148 * 16);
     db->launches = 0;
     cudaEventRecord(db->ev[0], s);
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
     // 0-set of the pool: one pass of head checks over the sorted records (no rank fixpoint)
     pool_zs_init_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_lock, db->d_fna, db->d_zflag, (uint32_t)n);
     pool_zs_mark_kernel<<<g, 256, 0, s>>>(db->d_prec, (uint32_t)nrec, db->d_lock, db->d_fna);
@@ -1011,8 +1021,8 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
     db->launches += 5;
     cudaEventRecord(db->ev[4], s);
     // one lock-free round (Property 1): the whole 0-set in parallel
-    CK(cudaMemsetAsync(db->d_status, 0, n, s));
-    CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
+    CK(dev_fill(db->d_status, 0, n, s));
+    CK(dev_fill(db->d_out, 0, n * db->out_stride, s));
     db->n = n;
     db->has_ts = true;
     db->ins_dense = false;              // pool rows: positions scanned over the executed 0-set
@@ -1039,7 +1049,7 @@ gputx_status pool_step_schema(gputx_db* db, gputx_stats* stats) {
                                               db->d_prec2);
     db->launches += 10;
     cudaEventRecord(db->ev[7], s);
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     std::swap(db->d_type, db->q_type);
@@ -1188,7 +1198,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         Col c;
         c.spec = cs;
         if ((st = dalloc(db, (uint8_t**)&c.d, cs.count * cs.elem)) != GPUTX_OK) return bail(st);
-        cudaMemsetAsync(c.d, 0, cs.count * cs.elem, db->stream);
+        dev_fill(c.d, 0, cs.count * cs.elem, db->stream);
         db->cols.push_back(c);
     }
     // insert tables
@@ -1237,9 +1247,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         db->ret_base = AR_HDR + (uint64_t)db->fwd_cap * sf;
         db->arena_words = db->ret_base + (uint64_t)db->ret_cap * sr;
         if (cudaMalloc((void**)&db->arena, db->arena_words * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
-        cudaMemsetAsync(db->arena, 0, db->arena_words * 4, db->stream);
+        dev_fill(db->arena, 0, db->arena_words * 4, db->stream);
         if ((st = dalloc(db, &db->d_done_ctas, 1))) return bail(st);
-        cudaMemsetAsync(db->d_done_ctas, 0, 4, db->stream);
+        dev_fill(db->d_done_ctas, 0, 4, db->stream);
     }
     if (db->nshards > 1 &&
         ((st = dalloc(db, &db->d_src, NB + 1)) || (st = dalloc(db, &db->d_home_pos, NB + 1)) ||
@@ -1273,14 +1283,19 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->sort_ws.status, db->sort_ws.max_tiles * 256)) ||
         (st = dalloc(db, &db->sort_ws.tickets, 64)))
         return bail(st);
-    cudaMemsetAsync(db->lb_scan.flag, 0, tiles * 4, db->stream);
-    cudaMemsetAsync(db->lb_rank.flag, 0, tiles * 4, db->stream);
-    cudaMemsetAsync(db->lb_tpl.flag, 0, tiles * 4, db->stream);
-    cudaMemsetAsync(db->sort_ws.status, 0, db->sort_ws.max_tiles * 256 * 8, db->stream);
-    cudaMemsetAsync(db->d_bar, 0, sizeof(GridBar), db->stream);
-    cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, db->stream);
-    cudaMemsetAsync(db->d_lock, 0, n_items * 4, db->stream);
-    if (cudaMallocHost((void**)&db->h_sc, SC_COUNT * 4) != cudaSuccess) return bail(GPUTX_ENOMEM);
+    dev_fill(db->lb_scan.flag, 0, tiles * 4, db->stream);
+    dev_fill(db->lb_rank.flag, 0, tiles * 4, db->stream);
+    dev_fill(db->lb_tpl.flag, 0, tiles * 4, db->stream);
+    dev_fill(db->sort_ws.status, 0, db->sort_ws.max_tiles * 256 * 8, db->stream);
+    dev_fill(db->d_bar, 0, sizeof(GridBar), db->stream);
+    dev_fill(db->d_sc, 0, SC_COUNT * 4, db->stream);
+    dev_fill(db->d_lock, 0, n_items * 4, db->stream);
+    // counters come back through mapped (zero-copy) host memory, written by a kernel: a
+    // D2H copy would queue on the copy engine behind a large result transfer of
+    // gputx_run_bulks and stall the next bulk's synchronous steps (1.67 vs 1.05 ms / bulk)
+    if (cudaHostAlloc((void**)&db->h_sc, SC_COUNT * 4, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&db->h_sc_dev, db->h_sc, 0) != cudaSuccess)
+        return bail(GPUTX_ENOMEM);
     for (auto& e : db->ev) cudaEventCreate(&e);
     for (auto& e : db->ev_sub) cudaEventCreate(&e);
     for (auto& e : db->ev_x) cudaEventCreate(&e);
@@ -1580,7 +1595,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
     if (n_words > db->max_words) return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
     cudaEventRecord(db->ev_sub[0], s);
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
     if (n) {
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         CK(cudaMemcpyAsync(db->s_type, b->type, n, kind, s));
@@ -1589,7 +1604,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
         CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
         const DevDb v = make_devdb(db);
         const uint32_t g = grid_for(n, 256, 148 * 8);
-        CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+        CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
         shard_validate_kernel<<<g, 256, 0, s>>>(db->s_poff, (uint32_t)n, n_words, stride - 3, db->d_sc);
         if (db->schema == S_TPCB) shard_count_kernel<S_TPCB><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
         else if (db->schema == S_TM1) shard_count_kernel<S_TM1><<<g, 256, 0, s>>>(v, db->s_type, db->s_poff, db->s_pw, (uint32_t)n, db->d_cnt);
@@ -1602,7 +1617,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
         const uint64_t* pairs = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL,
                                                std::min<uint64_t>(n * (db->nshards - 1), db->max_rec), 32,
                                                bits_for(db->nshards - 1), db->sort_ws, db->epoch, s);
-        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        TRY(pull_sc(db, s));
         CK(cudaStreamSynchronize(s));
         if (db->h_sc[SC_ERR])
             return fail(db, GPUTX_EINVAL, "home transaction " + std::to_string(err_idx(db)) + ": bad param_off");
@@ -1639,7 +1654,7 @@ gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_r
         const uint32_t g = grid_for(n, 256, 148 * 8);
         const uint32_t nh = (uint32_t)db->nh;
         merge_keys_kernel<<<g, 256, 0, s>>>(db->s_ts, nh, recv, (uint32_t)n_recv, stride, db->d_rec_a);
-        CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
+        CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
         uint32_t nn = (uint32_t)n;
         CK(cudaMemcpyAsync(db->d_sc + SC_XTOTAL, &nn, 4, cudaMemcpyHostToDevice, s));
         const uint64_t* keys = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL, n, 32, 32, db->sort_ws,
@@ -1668,8 +1683,8 @@ gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
     cudaStream_t s = db->stream;
     const uint32_t ow = db->out_stride / 4;
-    CK(cudaMemsetAsync(db->d_sc + SC_DEST0, 0, MAX_SHARDS * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_XTOTAL, 0, 4, s));
+    CK(dev_fill(db->d_sc + SC_DEST0, 0, MAX_SHARDS * 4, s));
+    CK(dev_fill(db->d_sc + SC_XTOTAL, 0, 4, s));
     if (db->n) {
         const uint32_t g = grid_for(db->n, 256, 148 * 8);
         const DevDb v = make_devdb(db);
@@ -1680,7 +1695,7 @@ gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send
         else ret_pair_kernel<S_TPCC><<<g, 256, 0, s>>>(v, db->d_rec_off, db->d_rec_a, db->d_sc);
         const uint64_t* pairs = radix_sort_u64(db->d_rec_a, db->d_rec_b, db->d_sc + SC_XTOTAL, db->n, 32,
                                                bits_for(db->nshards - 1), db->sort_ws, db->epoch, s);
-        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        TRY(pull_sc(db, s));
         CK(cudaStreamSynchronize(s));
         const uint64_t np = db->h_sc[SC_XTOTAL];
         for (uint32_t q = 0; q < db->nshards; ++q) counts[q] = db->h_sc[SC_DEST0 + q];
@@ -1823,12 +1838,12 @@ gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
         CK(cudaMemcpyAsync(db->s_poff, b->param_off, (n + 1) * 4, kind, s));
         if (n_words) CK(cudaMemcpyAsync(db->s_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
         CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
-        CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-        CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+        CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
+        CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
         const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
         shard_validate_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(db->s_poff, (uint32_t)n, n_words, stride - 3,
                                                                         db->d_sc);
-        CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+        TRY(pull_sc(db, s));
         CK(cudaStreamSynchronize(s));
         if (db->h_sc[SC_ERR]) err = fail(db, GPUTX_EINVAL, "home transaction " + std::to_string(err_idx(db)) +
                                                                ": bad param_off");
@@ -1850,10 +1865,10 @@ gputx_status gputx_shard_receive(gputx_db* db, uint64_t* n_local) {
     NVTX_SCOPE("gputx.shard_receive");
     if (!db->p2p || !db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_dispatch first");
     cudaStream_t s = db->stream;
-    CK(cudaMemsetAsync(db->d_sc + SC_DEADLOCK, 0, 4, s));
+    CK(dev_fill(db->d_sc + SC_DEADLOCK, 0, 4, s));
     p2p_wait_kernel<<<1, 32, 0, s>>>(db->arena, AR_FWD_FLAGS, AR_FWD_CNT, db->shard, db->nshards, db->xepoch,
                                      db->d_sc, db->d_sc + SC_P2P);
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_DEADLOCK]) {
         db->poisoned = true;
@@ -1896,7 +1911,7 @@ gputx_status gputx_shard_collect(gputx_db* db) {
     cudaStream_t s = db->stream;
     p2p_wait_kernel<<<1, 32, 0, s>>>(db->arena, AR_RET_FLAGS, AR_RET_CNT, db->shard, db->nshards, db->xepoch,
                                      db->d_sc, db->d_sc + SC_P2P);
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_DEADLOCK]) {
         db->poisoned = true;
@@ -1915,8 +1930,8 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
     if (n_recv && !recv) return GPUTX_EINVAL;
     cudaStream_t s = db->stream;
-    CK(cudaMemsetAsync(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(cudaMemsetAsync(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
+    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
     if (n_recv) {
         ret_merge_kernel<<<grid_for(n_recv, 256, 148 * 8), 256, 0, s>>>(recv, (uint32_t)n_recv, db->out_stride / 4,
                                                                          db->d_ts, db->d_src, (uint32_t)db->n,
@@ -1927,7 +1942,7 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
                                                                            db->d_status, db->d_out, db->out_stride,
                                                                            db->d_hstatus, db->d_hout);
     }
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
         return fail(db, GPUTX_EINVAL, "returned result " + std::to_string(err_idx(db)) +
@@ -1952,8 +1967,11 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     const uint64_t n = db->n;
     gputx_status r = GPUTX_OK;
     if (n) {
-        CK(cudaMemsetAsync(db->d_status, 0, n, s));
-        if (db->schema != S_TPCB && !(db->kset_diag & 4096u)) CK(cudaMemsetAsync(db->d_out, 0, n * db->out_stride, s));
+        zero_bytes_kernel<<<grid_for((n + 15) / 16, 256, 148 * 4), 256, 0, s>>>(db->d_status, n);
+        if (db->schema != S_TPCB && !(db->kset_diag & 4096u))
+            zero_bytes_kernel<<<grid_for(n * db->out_stride / 16 + 1, 256, 148 * 8), 256, 0, s>>>(db->d_out,
+                                                                                             n * db->out_stride);
+        db->launches += db->schema != S_TPCB ? 2 : 1;
         if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
         else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
         else if (db->schema == S_MICRO) r = execute_schema<S_MICRO>(db, st);
@@ -1969,7 +1987,7 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
                                                                               db->d_sc + SC_COMMITTED);
         ++db->launches;
     }
-    CK(cudaMemcpyAsync(db->h_sc, db->d_sc, SC_COUNT * 4, cudaMemcpyDeviceToHost, s));
+    TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     if (db->schema == S_TM1 && n) db->rows_dirty = true;
@@ -2280,12 +2298,15 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
     for (uint64_t i = 0; i < k; ++i) {
         if (bulks[i].on_device || bulks[i].ts) return fail(db, GPUTX_EINVAL, "run_bulks takes host bulks without ts");
         if (bulks[i].n > db->max_bulk) return fail(db, GPUTX_ECAPACITY, "bulk larger than max_bulk");
+        if (bulks[i].n && (!bulks[i].type || !bulks[i].param_off || !bulks[i].param_words)) return GPUTX_EINVAL;
         if (bulks[i].n && bulks[i].param_off[bulks[i].n] > db->max_words)
             return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     }
     TRY(pipe_alloc(db));
     cudaStream_t s = db->stream;
-    // H2D of bulk i into slot i % 2, once the submit of bulk i - 2 has consumed that slot
+    // No device-to-device copies on the way (they would queue behind the other copy stream's
+    // transfer on the copy engines): each slot's input buffers are SWAPPED in as the engine's
+    // bulk buffers, and its result buffers swapped in for the next bulk's results.
     auto h2d = [&](uint64_t i) -> gputx_status {
         const gputx_bulk& b = bulks[i];
         const int sl = (int)(i & 1);
@@ -2300,37 +2321,47 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
         return GPUTX_OK;
     };
     if (k) TRY(h2d(0));
+    int last = 0;
     for (uint64_t i = 0; i < k; ++i) {
         const int sl = (int)(i & 1);
+        last = sl;
         if (i + 1 < k) TRY(h2d(i + 1));              // next bulk's copy overlaps this one's execution
-        CK(cudaStreamWaitEvent(s, db->ev_in[sl], 0));
-        gputx_bulk dv = bulks[i];
-        dv.type = db->in_type[sl];
-        dv.param_off = db->in_poff[sl];
-        dv.param_words = db->in_pw[sl];
-        dv.on_device = 1;
-        TRY(gputx_submit_bulk(db, &dv, nullptr));
+        TRY(submit_check(db, &bulks[i]));
+        CK(cudaStreamWaitEvent(s, db->ev_in[sl], 0));       // bulk i has landed in slot sl
+        CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0)); // bulk i-2's results left slot sl
+        std::swap(db->d_type, db->in_type[sl]);
+        std::swap(db->d_poff, db->in_poff[sl]);
+        std::swap(db->d_pw, db->in_pw[sl]);
+        std::swap(db->d_status, db->res_status[sl]);
+        std::swap(db->d_out, db->res_out[sl]);
+        // the buffers now in slot sl held bulk i-1 (already executed): free for bulk i+1's copy
         CK(cudaEventRecord(db->ev_in_free[sl], s));
-        TRY(gputx_execute(db, st, stats ? &stats[i] : nullptr));
-        // results: a device copy into the slot (after the D2H of bulk i - 2 left it), then
-        // the D2H on its own stream, overlapping the next bulk's execution
         const uint64_t n = bulks[i].n;
-        CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
-        if (n) {
-            CK(cudaMemcpyAsync(db->res_status[sl], db->d_status, n, cudaMemcpyDeviceToDevice, s));
-            CK(cudaMemcpyAsync(db->res_out[sl], db->d_out, n * db->out_stride, cudaMemcpyDeviceToDevice, s));
-        }
+        db->has_ts = false;
+        db->first_ts = db->next_ts;
+        TRY(finish_submit(db, n, n ? bulks[i].param_off[n] : 0));
+        db->next_ts += n;
+        TRY(gputx_execute(db, st, stats ? &stats[i] : nullptr));
+        // results stay in the engine's d_status / d_out until the next bulk swaps them out; the
+        // D2H reads them from there on its own stream, overlapping the next execution
         CK(cudaEventRecord(db->ev_res[sl], s));
         CK(cudaStreamWaitEvent(db->st_d2h, db->ev_res[sl], 0));
-        if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->res_status[sl], n, cudaMemcpyDeviceToHost, db->st_d2h));
+        if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->d_status, n, cudaMemcpyDeviceToHost, db->st_d2h));
         if (n && out && out[i])
-            CK(cudaMemcpyAsync(out[i], db->res_out[sl], n * db->out_stride, cudaMemcpyDeviceToHost, db->st_d2h));
+            CK(cudaMemcpyAsync(out[i], db->d_out, n * db->out_stride, cudaMemcpyDeviceToHost, db->st_d2h));
         CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
+        // the next bulk gets the other slot's result buffers (swap below) -- these stay put
+        std::swap(db->d_status, db->res_status[sl]);
+        std::swap(db->d_out, db->res_out[sl]);
     }
     // the handle's stream is ordered after the last result copy (an event recorded on it
     // after this call covers the whole run), then wait for it
     for (int sl = 0; sl < 2; ++sl) CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
     CK(cudaStreamSynchronize(s));
+    if (k) {                                   // gputx_read_results: the last bulk's results
+        std::swap(db->d_status, db->res_status[last]);
+        std::swap(db->d_out, db->res_out[last]);
+    }
     return GPUTX_OK;
 }
 

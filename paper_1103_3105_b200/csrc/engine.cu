@@ -2367,6 +2367,7 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
 
 gputx_status gputx_read_serial_order(gputx_db* db, uint32_t* host, uint64_t n) {
     if (!db || !host) return GPUTX_EINVAL;
+    if (n == 0 && db->n == 0) return GPUTX_OK;                    // an empty bulk: the empty order
     if (!db->has_order || n != db->n) return fail(db, GPUTX_ESTATE, "no relaxed-strategy execution of this bulk");
     if (n) CK(cudaMemcpy(host, db->d_order, n * 4, cudaMemcpyDeviceToHost));
     return GPUTX_OK;

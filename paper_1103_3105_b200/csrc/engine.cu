@@ -406,7 +406,10 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 // ------------------------------------------------------------------------------- K-SET
 // parameter words staged in registers by the K-SET executor (0: read from HBM)
 template <int S> constexpr int kset_pw() { return S == S_TPCB || S == S_MICRO ? 4 : S == S_TM1 ? 8 : 0; }
-template <int S> constexpr int kset_block() { return S == S_TPCC ? 256 : KX_THREADS; }
+// executor CTA size: TM-1 256 (a narrow round's CTAs hold <= Q = 128 transactions; smaller
+// CTAs make its cluster barrier cheaper: TM-1 exec 0.428 -> 0.408 ms), TPC-C 256 (one warp
+// per transaction), TPC-B / micro 1024
+template <int S> constexpr int kset_block() { return S == S_TPCC || S == S_TM1 ? 256 : KX_THREADS; }
 template <int S> const void* kset_fn(bool sh) {
     return sh ? (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), true>
               : (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), false>;

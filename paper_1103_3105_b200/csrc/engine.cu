@@ -505,7 +505,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
         }
         ++db->launches;
     } else if (stream) {
-        const uint32_t gs = grid_for(db->max_rec, RS_STREAM_TILE, (uint32_t)db->nsm * 6);
+        const uint32_t gs = grid_for(db->max_rec, RS_STREAM_TILE, (uint32_t)db->nsm * 16);   // (all resident)
         rank_stream_tm1_kernel<<<gs, RS_STREAM_THREADS, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_D, db->d_sc);
         ++db->launches;
     } else {

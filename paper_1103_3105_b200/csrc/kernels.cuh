@@ -976,102 +976,186 @@ __global__ void __launch_bounds__(RK_THREADS) rank_root_kernel(DevDb db, const u
 // (PAPER.md:451-453), so the T-dependency graph is a disjoint union of per-subscriber
 // graphs -- finer: per (subscriber, item component), TM1_COMP_BITS in schema.cuh.  The
 // records are sorted on the (subscriber, component) bits only (stable: (root, ts)
-// order, a transaction's records adjacent), and one thread per root runs the
-// streaming depth recurrence over them in ts order (SURVEY.md §8(c) "Depth oracle"):
+// order, a transaction's records adjacent), and the streaming depth recurrence runs
+// over each root's records in ts order (SURVEY.md §8(c) "Depth oracle"):
 //   d(t) = max over t's records of (write ? Md[x] + 1 : Wd[x] + 1), 0 without records;
 //   then write: Wd[x] = Md[x] = d(t);  read: Md[x] = max(Md[x], d(t)).
-// Exact in one pass (the streaming order is a topological order of the root's graph),
-// with the per-item state (Wd, Md) of the subscriber's <= 32 item slots in shared
-// memory.  This replaces the iterated scan's repeated sweeps of hot NURand subscribers
-// (13 sweeps in the first pass, profiles/round1.md).
+// Exact in one pass (the streaming order is a topological order of the root's graph).
+// A root has <= 8 item slots (item & 7); their state (Wd, Md) lives in registers
+// (constant-indexed, selected by a 3-level tree).  This replaces the iterated scan's
+// repeated sweeps of hot NURand subscribers (13 sweeps in the first pass, round 1).
 constexpr int RS_STREAM_THREADS = 128;
 constexpr int RS_CHUNK = 8;
+constexpr uint32_t RS_LONG = 32;                           // longer roots: warp walk
 constexpr int RS_STREAM_TILE = RS_STREAM_THREADS * 8;     // records scanned for heads per CTA
-// Each CTA first collects the subscriber heads (first record of a subscriber) of its
-// tile of RS_STREAM_TILE sorted records into shared memory, then its threads walk those
-// subscribers (a walk may run past the tile) — so the lanes of a warp walk in lockstep
-// instead of diverging between head checks and walks (the SIMT cost of a thread-per-
-// record formulation).
+constexpr uint32_t TM1_ROOT_SLOTS = 1u << TM1_COMP_BITS;
+
+struct Tm1RootState {
+    int W[TM1_ROOT_SLOTS], M[TM1_ROOT_SLOTS];
+    uint32_t wm = 0, rm = 0;                 // the open transaction's written / read slots
+    int d = 0;                               // and its depth so far
+    DEV Tm1RootState() {
+#pragma unroll
+        for (int j = 0; j < (int)TM1_ROOT_SLOTS; ++j) W[j] = M[j] = -1;
+    }
+    DEV static int sel(const int* a, uint32_t x) {
+        const int l = x & 2u ? (x & 1u ? a[3] : a[2]) : (x & 1u ? a[1] : a[0]);
+        const int h = x & 2u ? (x & 1u ? a[7] : a[6]) : (x & 1u ? a[5] : a[4]);
+        return x & 4u ? h : l;
+    }
+    // one record (slot x, write w) of the open transaction; nothing when !valid
+    DEV void access(uint32_t x, bool w, bool valid) {
+        const int v = (w ? sel(M, x) : sel(W, x)) + 1;
+        d = valid ? max(d, v) : d;
+        const uint32_t b = valid ? 1u << x : 0u;
+        wm |= w ? b : 0u;
+        rm |= w ? 0u : b;
+    }
+    // the open transaction closes when c: its depth updates its slots (branch-free)
+    DEV void close(bool c) {
+#pragma unroll
+        for (int j = 0; j < (int)TM1_ROOT_SLOTS; ++j) {
+            const bool wj = c && (wm >> j & 1u), rj = c && (rm >> j & 1u);
+            W[j] = wj ? d : W[j];
+            M[j] = wj ? d : (rj ? max(M[j], d) : M[j]);
+        }
+        d = c ? 0 : d;
+        wm = c ? 0u : wm;
+        rm = c ? 0u : rm;
+    }
+};
+DEV uint64_t tm1_root(uint64_t k) { return key_item(k) >> TM1_COMP_BITS; }
+DEV uint32_t tm1_slot(uint64_t k) { return (uint32_t)key_item(k) & (TM1_ROOT_SLOTS - 1); }
+
+// Each CTA first lists the root heads (first record of a root) of its tile of
+// RS_STREAM_TILE sorted records in position order (block scan), so a root ends at the
+// next head.  A root whose records all belong to one transaction has depth 0 (skipped:
+// D is zero-filled); other roots up to RS_LONG records are walked one per thread, longer
+// ones (hot NURand subscribers, up to ~660 records) one per warp: the warp loads 32
+// consecutive keys per instruction, two chunks ahead, every lane decodes its own record
+// (slot, mode, first-of-transaction) and the recurrence runs branch-free over the 32
+// broadcast records in every lane, so only its ~20-cycle state dependence is serial.
 __global__ void __launch_bounds__(RS_STREAM_THREADS) rank_stream_tm1_kernel(const uint64_t* __restrict__ keys,
                                                                            const uint32_t* nrec_ptr, uint32_t* D,
                                                                            uint32_t* sc) {
-    __shared__ int2 st_all[RS_STREAM_THREADS * TM1_STRIDE];      // (Wd, Md) per slot, per thread
-    __shared__ uint32_t heads[RS_STREAM_TILE];
-    __shared__ uint32_t s_nh;
-    int2* st = st_all + threadIdx.x;                            // slot k at st[k * THREADS]: no bank conflicts
+    constexpr int PER = RS_STREAM_TILE / RS_STREAM_THREADS;
+    __shared__ uint32_t heads[RS_STREAM_TILE + 1];
+    __shared__ uint32_t longs[RS_STREAM_TILE];
+    __shared__ uint32_t scan_sm[RS_STREAM_THREADS / 32];
+    __shared__ uint32_t s_nl;
+    __shared__ int2 wstate[RS_STREAM_THREADS / 32][TM1_ROOT_SLOTS];
+    __shared__ uint2 wbuf[RS_STREAM_THREADS / 32][32];
     const uint32_t nrec = *nrec_ptr;
     const uint32_t ntiles = (nrec + RS_STREAM_TILE - 1) / RS_STREAM_TILE;
+    const uint32_t tid = threadIdx.x, lane = lane_id();
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (threadIdx.x == 0) s_nh = 0;
-        __syncthreads();
+        if (tid == 0) s_nl = 0;
         const uint32_t t0 = tile * RS_STREAM_TILE;
+        const uint32_t tend = min(t0 + (uint32_t)RS_STREAM_TILE, nrec);
+        // heads of this thread's PER consecutive records, then a block scan
+        const uint32_t pb = t0 + tid * PER;
+        uint64_t prev = pb > 0 && pb - 1 < nrec ? __ldg(&keys[pb - 1]) : ~0ull;
+        uint32_t flags = 0;
 #pragma unroll
-        for (int i = 0; i < RS_STREAM_TILE / RS_STREAM_THREADS; ++i) {
-            const uint32_t p = t0 + i * RS_STREAM_THREADS + threadIdx.x;
-            bool head = false;
-            if (p < nrec) {
-                const uint64_t r = key_item(__ldg(&keys[p])) >> TM1_COMP_BITS;
-                head = p == 0 || (key_item(__ldg(&keys[p - 1])) >> TM1_COMP_BITS) != r;
+        for (int i = 0; i < PER; ++i) {
+            if (pb + i < nrec) {
+                const uint64_t k = __ldg(&keys[pb + i]);
+                if (pb + i == 0 || tm1_root(prev) != tm1_root(k)) flags |= 1u << i;
+                prev = k;
             }
-            const uint32_t m = __ballot_sync(0xffffffffu, head);
-            uint32_t base = 0;
-            if (lane_id() == 0 && m) base = atomicAdd(&s_nh, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (head) heads[base + __popc(m & lanemask_lt())] = p;
+        }
+        uint32_t nh;
+        uint32_t at = block_scan_excl<uint32_t, OpAddU32>((uint32_t)__popc(flags), nh, scan_sm);
+        for (uint32_t f = flags; f; f &= f - 1) heads[at++] = pb + (__ffs(f) - 1);
+        if (tid == 0) heads[nh] = tend;
+        __syncthreads();
+        // long roots first (the hot subscribers' walks are the kernel's critical path)
+        for (uint32_t h = tid; h < nh; h += RS_STREAM_THREADS) {
+            const uint32_t p = heads[h], e = heads[h + 1];
+            if (e - p > RS_LONG || (h + 1 == nh && e < nrec && tm1_root(__ldg(&keys[e])) == tm1_root(__ldg(&keys[p]))))
+                longs[atomicAdd(&s_nl, 1u)] = p;
         }
         __syncthreads();
-        const uint32_t nh = s_nh;
-        for (uint32_t h = threadIdx.x; h < nh; h += RS_STREAM_THREADS) {
-            const uint32_t p = heads[h];
-            const uint64_t root = key_item(__ldg(&keys[p])) >> TM1_COMP_BITS;     // (subscriber, component)
-#pragma unroll 8
-            for (uint32_t j = 0; j < TM1_STRIDE; ++j) st[j * RS_STREAM_THREADS] = make_int2(-1, -1);
-            // walk the root's records in chunks of RS_CHUNK keys, the next chunk's loads in
-            // flight while the current one is processed.  The open transaction's records
-            // (distinct items, <= 3) are packed 7 bits each (slot | mode << 5) in `pk`; its
-            // depth is max'ed as they arrive (the state changes only when it closes).
-            uint64_t cur[RS_CHUNK], nxt[RS_CHUNK];
-            auto load = [&](uint64_t* b, uint32_t q) {
-#pragma unroll
-                for (int i = 0; i < RS_CHUNK; ++i) b[i] = q + i < nrec ? __ldg(&keys[q + i]) : ~0ull;
-            };
-            auto close = [&](uint32_t idx, uint32_t pk, int m, int d) {
-                for (int j = 0; j < m; ++j) {
-                    const uint32_t e = (pk >> (7 * j)) & 0x7Fu;
-                    int2* x = &st[(e & 31u) * RS_STREAM_THREADS];
-                    if ((e >> 5) == 1u) *x = make_int2(d, d);
-                    else x->y = max(x->y, d);
-                }
-                D[idx] = (uint32_t)d;
-            };
-            uint32_t q = p;
-            load(cur, q);
-            q += RS_CHUNK;
-            uint32_t tidx = 0xFFFFFFFFu, pk = 0;
-            int m = 0, d = 0;
+        const uint32_t nl = s_nl;
+        int2* ws = wstate[warp_id()];
+        for (uint32_t h = warp_id(); h < nl; h += RS_STREAM_THREADS / 32) {
+            const uint32_t p = longs[h];
+            const uint64_t kp = __ldg(&keys[p]);
+            const uint64_t root = tm1_root(kp);
+            auto ld = [&](uint32_t q) { return q + lane < nrec ? __ldg(&keys[q + lane]) : ~0ull; };
+            uint64_t c0 = ld(p), c1 = ld(p + 32), carry = ~0ull;   // carry: the previous chunk's last key
+            uint32_t q = p + 64;
+            if (lane < TM1_ROOT_SLOTS) ws[lane] = make_int2(-1, -1);
+            __syncwarp();
             bool go = true;
             while (go) {
-                load(nxt, q);
-                q += RS_CHUNK;
-#pragma unroll
-                for (int i = 0; i < RS_CHUNK; ++i) {
-                    const uint64_t kk = cur[i];
-                    if (!go || (key_item(kk) >> TM1_COMP_BITS) != root) { go = false; continue; }
-                    const uint32_t id = key_idx(kk);
-                    if (id != tidx) {
-                        if (m) close(tidx, pk, m, d);
-                        tidx = id; pk = 0; m = 0; d = 0;
-                    }
-                    const uint32_t slot = (uint32_t)(key_item(kk) & (TM1_STRIDE - 1)), mode = key_mode(kk);
-                    const int2 x = st[slot * RS_STREAM_THREADS];
-                    d = max(d, (mode == 1u ? x.y : x.x) + 1);
-                    pk |= (slot | (mode << 5)) << (7 * m);
-                    ++m;
+                const uint64_t c2 = ld(q);
+                q += 32;
+                // lane-parallel: does this lane's record start a transaction; if so, its
+                // <= 3 records (this one and the next two, looking into the next chunk)
+                // packed 4 bits each (slot | write << 3) with their count
+                uint64_t kprev = __shfl_up_sync(0xffffffffu, c0, 1);
+                if (lane == 0) kprev = carry;
+                const bool valid = tm1_root(c0) == root;                    // a prefix of the chunk
+                const bool start = valid && (lane == 0 && carry == ~0ull ? true : key_idx(c0) != key_idx(kprev));
+                const uint64_t a1 = __shfl_down_sync(0xffffffffu, c0, 1), b1 = __shfl_sync(0xffffffffu, c1, (lane + 1) & 31);
+                const uint64_t a2 = __shfl_down_sync(0xffffffffu, c0, 2), b2 = __shfl_sync(0xffffffffu, c1, (lane + 2) & 31);
+                const uint64_t k1 = lane + 1 < 32 ? a1 : b1, k2 = lane + 2 < 32 ? a2 : b2;
+                const uint32_t id = key_idx(c0);
+                const bool h1 = tm1_root(k1) == root && key_idx(k1) == id;
+                const bool h2 = h1 && tm1_root(k2) == root && key_idx(k2) == id;
+                auto enc = [](uint64_t k) { return tm1_slot(k) | (key_mode(k) == 1u ? 8u : 0u); };
+                const uint32_t tw = enc(c0) | (h1 ? enc(k1) << 4 | 1u << 12 : 0u) | (h2 ? enc(k2) << 8 | 1u << 13 : 0u);
+                const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+                go = vm == 0xffffffffu;
+                carry = __shfl_sync(0xffffffffu, c0, 31);
+                // serial part, one transaction per step (warp-uniform: every lane keeps the
+                // same slot state (Wd, Md) in this warp's shared words)
+                // the chunk's transactions compacted in order into this warp's buffer, so the
+                // serial loop's loads of them are independent of its state chain
+                const uint32_t smask = __ballot_sync(0xffffffffu, start);
+                if (start) wbuf[warp_id()][__popc(smask & lanemask_lt())] = make_uint2(tw, id);
+                __syncwarp();
+                const int ns = __popc(smask);
+#pragma unroll 8
+                for (int j = 0; j < ns; ++j) {
+                    const uint2 tj = wbuf[warp_id()][j];
+                    const uint32_t t = tj.x, cid = tj.y;
+                    const uint32_t e0 = t & 15u, e1 = (t >> 4) & 15u, e2 = (t >> 8) & 15u;
+                    const int2 s0 = ws[e0 & 7u], s1 = ws[e1 & 7u], s2 = ws[e2 & 7u];
+                    int d = ((e0 & 8u) ? s0.y : s0.x) + 1;
+                    if (t & (1u << 12)) d = max(d, ((e1 & 8u) ? s1.y : s1.x) + 1);
+                    if (t & (1u << 13)) d = max(d, ((e2 & 8u) ? s2.y : s2.x) + 1);
+                    ws[e0 & 7u] = (e0 & 8u) ? make_int2(d, d) : make_int2(s0.x, max(s0.y, d));
+                    if (t & (1u << 12)) ws[e1 & 7u] = (e1 & 8u) ? make_int2(d, d) : make_int2(s1.x, max(s1.y, d));
+                    if (t & (1u << 13)) ws[e2 & 7u] = (e2 & 8u) ? make_int2(d, d) : make_int2(s2.x, max(s2.y, d));
+                    if (lane == 0 && d) D[cid] = (uint32_t)d;
                 }
-#pragma unroll
-                for (int i = 0; i < RS_CHUNK; ++i) cur[i] = nxt[i];
+                __syncwarp();
+                c0 = c1;
+                c1 = c2;
             }
-            if (m) close(tidx, pk, m, d);
+            __syncwarp();
+        }
+        for (uint32_t h = tid; h < nh; h += RS_STREAM_THREADS) {
+            const uint32_t p = heads[h], e = heads[h + 1];
+            const uint64_t k0 = __ldg(&keys[p]);
+            if (e - p > RS_LONG || (h + 1 == nh && e < nrec && tm1_root(__ldg(&keys[e])) == tm1_root(k0)))
+                continue;                                                 // walked by a warp
+            if (key_idx(__ldg(&keys[e - 1])) == key_idx(k0)) continue;   // one transaction: depth 0
+            Tm1RootState st;
+            uint32_t tidx = key_idx(k0);
+            for (uint32_t q = p; q < e; ++q) {
+                const uint64_t k = __ldg(&keys[q]);            // (L1: this tile)
+                const uint32_t id = key_idx(k);
+                if (id != tidx) {
+                    if (st.d) D[tidx] = (uint32_t)st.d;
+                    st.close(true);
+                    tidx = id;
+                }
+                st.access(tm1_slot(k), key_mode(k) == 1u, true);
+            }
+            if (st.d) D[tidx] = (uint32_t)st.d;
         }
         __syncthreads();
     }

@@ -1466,6 +1466,7 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
     // it still walks the schedule, signals and takes part in cluster barriers so that no
     // other CTA hangs on it, but neither waits nor executes; the host reports EDEADLOCK
     __shared__ uint32_t s_dead;
+    __shared__ uint32_t s_run[2];
     if (tid == 0) s_dead = 0;
     bool dead = false;
     uint32_t k = 0;
@@ -1515,12 +1516,26 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
         if (TAILRUN && nar && gk == 1 && !(diag & 256u) && !dead) {
             // rounds of up to runmax transactions join the run (diag >> 16; 0: one-CTA rounds)
             const uint32_t runmax = min((uint32_t)KB, diag >> 16);
-            uint32_t e = k, wmax = 0;
-            while (e < nk && e + 1 < cb + KX_CH && narrow(e) &&
-                   (G(e) == 1 || soff[e - cb + 1] - soff[e - cb] <= runmax)) {
-                wmax = max(wmax, soff[e - cb + 1] - soff[e - cb]);
-                ++e;
+            // the run's end e (first round from k on that is not a one-CTA narrow round, or
+            // the staged chunk's end) and its widest round, KB rounds per step in parallel
+            // (a serial scan of a ~130-round tail cost ~20 us, profiles/round2_rounds_tm1)
+            const uint32_t lim = min(nk, cb + KX_CH - 1);
+            if (tid == 0) { s_run[0] = lim; s_run[1] = 0; }
+            __syncthreads();
+            for (uint32_t base = k; base < lim; base += KB) {
+                const uint32_t x = base + tid;
+                if (x < lim) {
+                    const uint32_t sz = soff[x - cb + 1] - soff[x - cb], gx = sg[x - cb];
+                    if (!(C && gx <= C && (gx == 1 || sz <= runmax))) atomicMin(&s_run[0], x);
+                }
+                __syncthreads();
+                if (s_run[0] < base + KB) break;
             }
+            const uint32_t e = s_run[0];
+            for (uint32_t x = k + tid; x < e; x += KB) atomicMax(&s_run[1], soff[x - cb + 1] - soff[x - cb]);
+            __syncthreads();
+            const uint32_t wmax = s_run[1];
+            __syncthreads();                    // (s_run is rewritten by the next run)
             const uint32_t nthr = min((uint32_t)KB, (wmax + 31) & ~31u);
             if (e >= k + 2) {                   // rounds k .. e-2 in the run, e-1 regular
                 if (b == 0 && tid < nthr) {

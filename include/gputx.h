@@ -105,7 +105,8 @@ typedef struct {
                                  TPC-C: warehouses W, districts/W D, customers/district C, items I */
     uint64_t max_bulk;        /* transactions per bulk, <= 1<<24 (timestamp field width)            */
     uint64_t insert_capacity; /* merged insert tables hold this many full bulks; 0 => 8            */
-    uint32_t part_size;       /* PART: TM-1 subscribers per partition; 0 => 128     */
+    uint32_t part_size;       /* PART: TM-1 subscribers / micro tuples per partition; 0 => TM-1 1,  */
+                              /* micro 128 (PAPER.md:461 tuned 128 on its GPU; B200: DESIGN.md)    */
     int device;               /* CUDA device ordinal                                                */
     void* stream;             /* cudaStream_t to order all work on; NULL => a library-owned stream  */
     uint32_t flags;           /* GPUTX_FLAG_* below; 0 = the paper's R/W conflict rule              */

@@ -1152,7 +1152,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->type_mask = db->ntypes >= 32 ? 0xFFFFFFFFu : (1u << db->ntypes) - 1;
     db->max_bulk = cfg->max_bulk;
     db->out_stride = gputx_out_stride(cfg->schema);
-    db->part_size = cfg->part_size ? cfg->part_size : 128;
+    // PART partition size: PAPER.md:461 tuned 128 on its GPU; on B200 TM-1 runs fastest with
+    // one subscriber per partition (maximum parallelism; tools/probe_part_tm1.py: PART total
+    // 0.51 ms at 1 vs 3.45 ms at 128 on the 1M/1M NURand bulk), the micro benchmark keeps 128
+    db->part_size = cfg->part_size ? cfg->part_size : schema == S_TM1 ? 1 : 128;
     db->nshards = cfg->nshards ? cfg->nshards : 1;
     db->shard = cfg->shard;
     if (db->nshards > MAX_SHARDS || db->shard >= db->nshards) { delete db; return GPUTX_EINVAL; }

@@ -439,11 +439,16 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
             SH.connect_p2p(db)         # the library's fused exchange over peer memory (CUDA IPC)
 
     def step_dev(k, strategy):
+        """Launch one step; returns the function that completes it (-> stats).  Single
+        GPU: gputx_execute_async, so the end event is recorded behind the bulk's last
+        kernel, not behind the host's stats bookkeeping (gputx_wait)."""
         b = dbulks[k % len(dbulks)]
         if ws > 1:
-            return SH.step(db, b, strategy, on_device=True)
+            st = SH.step(db, b, strategy, on_device=True)
+            return lambda: st
         db.submit(b, on_device=True)
-        return db.execute(strategy)
+        db.execute_async(strategy)
+        return db.wait
 
     def barrier():
         if dist is not None:
@@ -453,7 +458,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
 
     def timed(strategy, steps, warmup):
         for k in range(warmup):
-            step_dev(k, strategy)
+            step_dev(k, strategy)()
         torch.cuda.synchronize()
         barrier()
         clk.wait_first()
@@ -465,8 +470,9 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            stats.append(step_dev(warmup + k, strategy))
+            finish = step_dev(warmup + k, strategy)
             e1.record(stream)
+            stats.append(finish())
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
         torch.cuda.synchronize()

@@ -202,6 +202,17 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* bulk, uint64_t* f
  * default 10 s: the handle is poisoned until gputx_reset), ECAPACITY (insert table full), ECUDA. */
 gputx_status gputx_execute(gputx_db* db, gputx_strategy strategy, gputx_stats* stats);
 
+/* gputx_execute in two halves, so the caller's thread is free while the bulk runs (and a
+ * device timer can bracket exactly the bulk's kernels).  gputx_execute_async enqueues every
+ * kernel of the strategy on the handle's stream and returns; host-detectable errors
+ * (ESTATE nothing submitted, EINVAL bad strategy) are returned here, nothing is enqueued
+ * then.  (GPUTX_AUTO and the sharded / relaxed paths still synchronise inside for their
+ * device-computed decisions.)  gputx_wait synchronises and returns what gputx_execute would
+ * have: the device-side errors (EDEADLOCK, ECUDA) and the stats (may be NULL).  Until
+ * gputx_wait, every other call on the handle except gputx_close_db returns ESTATE. */
+gputx_status gputx_execute_async(gputx_db* db, gputx_strategy strategy);
+gputx_status gputx_wait(gputx_db* db, gputx_stats* stats);
+
 /* A stream of k HOST bulks executed back to back with the transfers overlapped: bulk i+1's
  * H2D copy and bulk i-1's D2H of results run on two copy streams while bulk i executes
  * (double-buffered device slots).  Equivalent to k x (gputx_submit_bulk + gputx_execute +

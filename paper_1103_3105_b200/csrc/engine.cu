@@ -108,6 +108,8 @@ struct gputx_db {
     std::vector<Col> cols;
     std::vector<InsTable> ins;
     bool sealed = false, submitted = false, executed = false, poisoned = false;
+    bool exec_pending = false;                // gputx_execute_async launched, gputx_wait not yet
+    int exec_st = 0;                          // its requested strategy
     int last_strategy = -1;
     int chosen = -1;                          // strategy that ran for the last execute
     // Algorithm 1 thresholds (gputx_set_chooser); w0_bar 0 => 64 x #SMs.  Calibrated on
@@ -406,10 +408,11 @@ uint32_t grid_for(uint64_t n, uint32_t block, uint32_t cap) {
 // ------------------------------------------------------------------------------- K-SET
 // parameter words staged in registers by the K-SET executor (0: read from HBM)
 template <int S> constexpr int kset_pw() { return S == S_TPCB || S == S_MICRO ? 4 : S == S_TM1 ? 8 : 0; }
-// executor CTA size: TM-1 256 (a narrow round's CTAs hold <= Q = 128 transactions; smaller
-// CTAs make its cluster barrier cheaper: TM-1 exec 0.428 -> 0.408 ms), TPC-C 256 (one warp
-// per transaction), TPC-B / micro 1024
-template <int S> constexpr int kset_block() { return S == S_TPCC || S == S_TM1 ? 256 : KX_THREADS; }
+// executor CTA size: 256 for TM-1 / TPC-B (a round's CTA holds <= Q = 128 / 32 transactions;
+// smaller CTAs make its barriers cheaper: TM-1 exec 0.428 -> 0.408 ms, TPC-B 12.0 -> 10.0 ms;
+// 128 / 64 measured no better, tools/gpu_kb_sweep.sh), TPC-C 256 (one warp per
+// transaction), micro 1024 (compute-heavy types)
+template <int S> constexpr int kset_block() { return S == S_MICRO ? KX_THREADS : 256; }
 template <int S> const void* kset_fn(bool sh) {
     return sh ? (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), true>
               : (const void*)kset_exec_kernel<S, kset_pw<S>(), kset_block<S>(), false>;
@@ -1549,6 +1552,7 @@ gputx_status gputx_register_types(gputx_db* db, const uint32_t* ids, uint32_t k)
 }
 
 gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !b) return GPUTX_EINVAL;
     NVTX_SCOPE("gputx.submit");
     if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "sharded handle: submit with gputx_shard_pack + gputx_shard_submit");
@@ -1582,6 +1586,7 @@ uint32_t gputx_shard_stride(gputx_schema schema, int result) {
 }
 
 gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send, uint64_t send_cap, uint64_t* counts) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !b || !counts) return GPUTX_EINVAL;
     if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
     TRY(submit_check(db, b));
@@ -1648,6 +1653,7 @@ gputx_status gputx_shard_pack(gputx_db* db, const gputx_bulk* b, uint32_t* send,
 }
 
 gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_recv, uint64_t* n_local) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (!db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_pack first");
     if (n_recv && !recv) return GPUTX_EINVAL;
@@ -1684,6 +1690,7 @@ gputx_status gputx_shard_submit(gputx_db* db, const uint32_t* recv, uint64_t n_r
 }
 
 gputx_status gputx_shard_return_pack(gputx_db* db, uint32_t* send, uint64_t send_cap, uint64_t* counts) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !counts) return GPUTX_EINVAL;
     if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
@@ -1814,6 +1821,7 @@ void p2p_dispatch_launch(gputx_db* db, uint32_t nh) {
 }  // extern "C++"
 
 gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !b) return GPUTX_EINVAL;
     NVTX_SCOPE("gputx.shard_dispatch");
     if (!db->p2p) return fail(db, GPUTX_ESTATE, "gputx_shard_connect first");
@@ -1867,6 +1875,7 @@ gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
 }
 
 gputx_status gputx_shard_receive(gputx_db* db, uint64_t* n_local) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     NVTX_SCOPE("gputx.shard_receive");
     if (!db->p2p || !db->staged) return fail(db, GPUTX_ESTATE, "gputx_shard_dispatch first");
@@ -1900,6 +1909,7 @@ void p2p_return_launch(gputx_db* db) {
 }  // extern "C++"
 
 gputx_status gputx_shard_return(gputx_db* db) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (!db->p2p) return fail(db, GPUTX_ESTATE, "gputx_shard_connect first");
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
@@ -1912,6 +1922,7 @@ gputx_status gputx_shard_return(gputx_db* db) {
 }
 
 gputx_status gputx_shard_collect(gputx_db* db) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (!db->p2p || !db->executed) return fail(db, GPUTX_ESTATE, "gputx_shard_return first");
     cudaStream_t s = db->stream;
@@ -1931,6 +1942,7 @@ gputx_status gputx_shard_collect(gputx_db* db) {
 }
 
 gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64_t n_recv) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (db->nshards < 2) return fail(db, GPUTX_ESTATE, "not a sharded handle");
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
@@ -1957,8 +1969,9 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
     return GPUTX_OK;
 }
 
-gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
-    if (!db) return GPUTX_EINVAL;
+// the launch half of gputx_execute / gputx_execute_async: every kernel of the strategy,
+// the abort count and the counter pull, enqueued on the handle's stream
+gputx_status execute_launch(gputx_db* db, gputx_strategy st) {
     NVTX_SCOPE("gputx.execute");
     if (!db->submitted) return fail(db, GPUTX_ESTATE, "nothing submitted");
     if (st != GPUTX_TPL && st != GPUTX_PART && st != GPUTX_KSET && st != GPUTX_AUTO && st != GPUTX_TPL_RELAXED &&
@@ -1994,6 +2007,17 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
         ++db->launches;
     }
     TRY(pull_sc(db, s));
+    db->exec_pending = true;
+    db->exec_st = (int)st;
+    return GPUTX_OK;
+}
+
+// the completion half: wait for the stream, device-side errors, stats
+gputx_status execute_finish(gputx_db* db, gputx_stats* stats) {
+    db->exec_pending = false;
+    const gputx_strategy st = (gputx_strategy)db->exec_st;
+    cudaStream_t s = db->stream;
+    const uint64_t n = db->n;
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     if (db->schema == S_TM1 && n) db->rows_dirty = true;
@@ -2057,7 +2081,28 @@ gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) 
     return GPUTX_OK;
 }
 
+
+gputx_status gputx_execute(gputx_db* db, gputx_strategy st, gputx_stats* stats) {
+    if (!db) return GPUTX_EINVAL;
+    if (db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
+    TRY(execute_launch(db, st));
+    return execute_finish(db, stats);
+}
+
+gputx_status gputx_execute_async(gputx_db* db, gputx_strategy st) {
+    if (!db) return GPUTX_EINVAL;
+    if (db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
+    return execute_launch(db, st);
+}
+
+gputx_status gputx_wait(gputx_db* db, gputx_stats* stats) {
+    if (!db) return GPUTX_EINVAL;
+    if (!db->exec_pending) return fail(db, GPUTX_ESTATE, "no asynchronous execute pending");
+    return execute_finish(db, stats);
+}
+
 gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     const uint8_t* ds = nullptr;
     const void* dout = nullptr;
     uint64_t n = 0;
@@ -2071,6 +2116,7 @@ gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64
 }
 
 gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const void** out, uint64_t* n) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
     if (db->nshards > 1) {
@@ -2087,6 +2133,7 @@ gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const vo
 }
 
 gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint64_t bytes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !name || !host) return GPUTX_EINVAL;
     TRY(tm1_rows_sync(db));
     Col* c = find_col(db, name);
@@ -2098,6 +2145,7 @@ gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint6
 }
 
 gputx_status gputx_insert_rows(gputx_db* db, const char* table, uint64_t* rows) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !table || !rows) return GPUTX_EINVAL;
     for (auto& t : db->ins)
         if (t.name == table) { *rows = t.rows; return GPUTX_OK; }
@@ -2105,6 +2153,7 @@ gputx_status gputx_insert_rows(gputx_db* db, const char* table, uint64_t* rows) 
 }
 
 gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const char* column, void* host, uint64_t bytes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !table || !column) return GPUTX_EINVAL;
     for (auto& t : db->ins) {
         if (t.name != table) continue;
@@ -2122,6 +2171,7 @@ gputx_status gputx_read_insert_column(gputx_db* db, const char* table, const cha
 }
 
 gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_depth || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET depths for this bulk");
     if (n) CK(cudaMemcpy(host, db->d_D, n * 4, cudaMemcpyDeviceToHost));
@@ -2129,6 +2179,7 @@ gputx_status gputx_read_depths(gputx_db* db, uint32_t* host, uint64_t n) {
 }
 
 gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->trace_rounds || !db->has_perm) return fail(db, GPUTX_ESTATE, "round tracing off or no K-SET bulk");
     if (rounds > db->n) return fail(db, GPUTX_EINVAL, "more rounds than transactions");
@@ -2137,6 +2188,7 @@ gputx_status gputx_read_round_ns(gputx_db* db, uint64_t* host, uint64_t rounds) 
 }
 
 gputx_status gputx_read_rank_ns(gputx_db* db, uint64_t* host, uint64_t passes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->trace_rounds || !db->has_depth) return fail(db, GPUTX_ESTATE, "tracing off or no K-SET bulk");
     if (passes > RANK_TRACE_SLOTS / 8) return fail(db, GPUTX_EINVAL, "too many passes");
@@ -2151,6 +2203,7 @@ gputx_status gputx_trace_rounds(gputx_db* db, int on) {
 }
 
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
     if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
     if (n) CK(cudaMemcpy(host, db->d_perm, n * 4, cudaMemcpyDeviceToHost));
@@ -2158,6 +2211,7 @@ gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
 }
 
 gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* b, uint64_t* first_ts) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !b) return GPUTX_EINVAL;
     if (!db->sealed) return fail(db, GPUTX_ESTATE, "pool submit before seal");
     if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
@@ -2195,6 +2249,7 @@ gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* b, uint64_t* firs
 }
 
 gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* executed) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     NVTX_SCOPE("gputx.pool_step");
     if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
@@ -2215,6 +2270,7 @@ gputx_status gputx_pool_step(gputx_db* db, gputx_stats* stats, uint64_t* execute
 }
 
 gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* out, uint64_t cap, uint64_t* n) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     const uint64_t k = db->pool_exec;
     if (n) *n = k;
@@ -2232,6 +2288,7 @@ gputx_status gputx_pool_read(gputx_db* db, uint32_t* ts, uint8_t* status, void* 
 //   per column : u32 name_len, name, u32 elem_bytes, u64 count, count*elem bytes
 //   per table  : u32 name_len, name, u32 ncols, u64 rows, per column: u32 name_len, name, rows*4 bytes
 gputx_status gputx_snapshot(gputx_db* db, void* buf, uint64_t* bytes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !bytes) return GPUTX_EINVAL;
     if (!db->sealed) return fail(db, GPUTX_ESTATE, "snapshot before seal");
     uint64_t need = 8 + 4 * 8;
@@ -2299,6 +2356,7 @@ gputx_status pipe_alloc(gputx_db* db) {
 
 gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, gputx_strategy st,
                              uint8_t* const* status, void* const* out, gputx_stats* stats) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || (k && !bulks)) return GPUTX_EINVAL;
     if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "sharded handles: use the shard calls");
     for (uint64_t i = 0; i < k; ++i) {
@@ -2372,6 +2430,7 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
 }
 
 gputx_status gputx_read_serial_order(gputx_db* db, uint32_t* host, uint64_t n) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
     if (n == 0 && db->n == 0) return GPUTX_OK;                    // an empty bulk: the empty order
     if (!db->has_order || n != db->n) return fail(db, GPUTX_ESTATE, "no relaxed-strategy execution of this bulk");
@@ -2401,6 +2460,7 @@ gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, ui
 }
 
 gputx_status gputx_reset(gputx_db* db) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db) return GPUTX_EINVAL;
     if (!db->sealed) return fail(db, GPUTX_ESTATE, "reset before seal");
     for (auto& c : db->cols)

@@ -118,6 +118,8 @@ def load_library():
         "gputx_shard_collect": ([P], I),
         "gputx_submit_bulk": ([P, ctypes.POINTER(BulkC), ctypes.POINTER(U64)], I),
         "gputx_execute": ([P, I, ctypes.POINTER(Stats)], I),
+        "gputx_execute_async": ([P, I], I),
+        "gputx_wait": ([P, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
         "gputx_results_device": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)], I),
         "gputx_out_stride": ([I], U32),
@@ -149,7 +151,7 @@ def load_library():
 
 
 EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_seal", "gputx_register_types",
-            "gputx_submit_bulk", "gputx_execute", "gputx_read_results", "gputx_results_device",
+            "gputx_submit_bulk", "gputx_execute", "gputx_execute_async", "gputx_wait", "gputx_read_results", "gputx_results_device",
             "gputx_out_stride", "gputx_read_column", "gputx_insert_rows", "gputx_read_insert_column",
             "gputx_read_depths", "gputx_read_perm", "gputx_reset", "gputx_close_db", "gputx_last_error",
             "gputx_set_launch", "gputx_set_chooser", "gputx_trace_rounds", "gputx_read_round_ns",
@@ -358,6 +360,16 @@ class Database:
     def execute(self, strategy: str = KSET) -> dict:
         st = Stats()
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], ctypes.byref(st)), self.h)
+        return st.as_dict()
+
+    def execute_async(self, strategy: str = KSET) -> None:
+        """Enqueue the bulk's execution and return (complete it with wait())."""
+        self._check(self.lib.gputx_execute_async(self.h, STRATEGIES[strategy]), self.h)
+
+    def wait(self) -> dict:
+        """Complete an execute_async: synchronise, raise its device-side errors, stats."""
+        st = Stats()
+        self._check(self.lib.gputx_wait(self.h, ctypes.byref(st)), self.h)
         return st.as_dict()
 
     # ---- streaming K-SET pool (include/gputx.h "Streaming K-SET") -------------------

@@ -70,3 +70,32 @@ def test_run_bulks_overlapped_equals_serial(schema):
     for c in image:
         assert np.array_equal(got[c], cur[c]), c
     db.close()
+
+
+@pytest.mark.parametrize("strategy", ["kset", "part", "tpl", "auto"])
+def test_execute_async_wait_equals_execute(strategy):
+    """gputx_execute_async + gputx_wait give gputx_execute's results and stats; the
+    handle refuses other calls (ESTATE) while the execute is pending."""
+    import oracle
+    from paper_1103_3105_b200.gputx import GputxError
+    dims = W.Tm1Dims(5000)
+    image = W.make_db(W.TM1, dims, seed=1)
+    bulk = W.make_bulk(W.TM1, dims, 4000, seed=7)
+    db = gpu_db(W.TM1, dims, image, bulk.n, insert_capacity=8)
+    db.submit(bulk)
+    db.execute_async(strategy)
+    with pytest.raises(GputxError):
+        db.read_results()
+    with pytest.raises(GputxError):
+        db.execute(strategy)
+    st = db.wait()
+    with pytest.raises(GputxError):
+        db.wait()                                   # nothing pending any more
+    assert st["n"] == bulk.n and st["committed"] + st["aborted"] == bulk.n
+    ref = oracle.run(W.TM1, dims.dims, image, bulk)
+    status, out = db.read_results()
+    assert np.array_equal(status, ref.status) and np.array_equal(out, ref.out)
+    got = db.read_image(image)
+    for c in image:
+        assert np.array_equal(got[c], ref.db[c]), c
+    db.close()

@@ -683,6 +683,35 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, 
 // was the per-round critical path (~5 us); spread over the lanes it is ~20 per lane.
 // Same results as tpcc_txn: a repeated stock row sees its earlier line's update (the
 // updates are chained through the lanes in line order) and only its last line stores it.
+// TPC-C Payment on the calling thread; with_wytd = false leaves out its W_YTD update
+// (the caller applies it under the warehouse's lock: tpl_exec_warp_kernel).  Returns
+// false if it aborted (by-name lookup found nobody: no writes at all).
+DEV bool tpcc_payment(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh, bool with_wytd) {
+    const uint32_t D = db.dims[1], C = db.dims[2];
+    const uint32_t w = p[0], d = p[1];
+    const uint64_t wd = (uint64_t)w * D + d;
+    uint8_t* o = db.out + (uint64_t)idx * 200;
+    if (p[4] == 2) { db.status[idx] = 1; return false; }
+    const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
+    const int64_t cbal = ldm(&COL(int64_t, C_C_BAL)[cx]);
+    const uint8_t credit = __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]);
+    const uint64_t rh = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
+    const uint32_t h = p[6];
+    if (with_wytd) red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
+    red_add(&COL(int64_t, C_D_YTD)[wd], (int64_t)h);
+    INS(uint32_t, IH_C)[rh] = p[5]; INS(uint32_t, IH_CD)[rh] = p[3]; INS(uint32_t, IH_CW)[rh] = p[2];
+    INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = txn_ts(db, idx, sh);
+    INS(int32_t, IH_AMT)[rh] = (int32_t)h;
+    const int64_t nb = cbal - (int64_t)h;
+    stm(&COL(int64_t, C_C_BAL)[cx], nb);
+    red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
+    red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
+    put32(o, p[5]);
+    put32(o + 4, credit);
+    put64(o + 8, (uint64_t)nb);
+    return true;
+}
+
 DEV void tpcc_txn_warp(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, bool sh) {
     constexpr uint32_t FULL = 0xffffffffu;
     const uint32_t lane = lane_id();
@@ -691,25 +720,7 @@ DEV void tpcc_txn_warp(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t
     const uint64_t wd = (uint64_t)w * D + d;
     uint8_t* o = db.out + (uint64_t)idx * 200;
     if (t != 0) {                                 // Payment: small, lane 0
-        if (lane != 0) return;
-        if (p[4] == 2) { db.status[idx] = 1; return; }
-        const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
-        const int64_t cbal = ldm(&COL(int64_t, C_C_BAL)[cx]);
-        const uint8_t credit = __ldg(&COL(const uint8_t, C_C_CREDIT)[cx]);
-        const uint64_t rh = db.ins_base[T_HIST] + db.ins_off[T_HIST * (uint64_t)db.ins_stride + idx];
-        const uint32_t h = p[6];
-        red_add(&COL(int64_t, C_W_YTD)[w], (int64_t)h);
-        red_add(&COL(int64_t, C_D_YTD)[wd], (int64_t)h);
-        INS(uint32_t, IH_C)[rh] = p[5]; INS(uint32_t, IH_CD)[rh] = p[3]; INS(uint32_t, IH_CW)[rh] = p[2];
-        INS(uint32_t, IH_D)[rh] = d; INS(uint32_t, IH_W)[rh] = w; INS(uint32_t, IH_DATE)[rh] = txn_ts(db, idx, sh);
-        INS(int32_t, IH_AMT)[rh] = (int32_t)h;
-        const int64_t nb = cbal - (int64_t)h;
-        stm(&COL(int64_t, C_C_BAL)[cx], nb);
-        red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
-        red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
-        put32(o, p[5]);
-        put32(o + 4, credit);
-        put64(o + 8, (uint64_t)nb);
+        if (lane == 0) tpcc_payment(db, idx, p, sh, true);
         return;
     }
     const uint32_t cnt = min(p[3], 15u);

@@ -1760,7 +1760,7 @@ __global__ void __launch_bounds__(128) part_exec_warp_kernel(DevDb db, const uin
         }
         // rows of j+1 (its parameters were warmed one iteration ago)
         if (k1 != NONE) tpcc_warm_warp(db, t1, db.pw + o1);
-        if ((fk & 0xFFu) == F_WHOLE || (db.type[idx] == 0 && fragments<S_TPCC>(db, idx, nullptr) == 1)) {
+        if ((fk & 0xFFu) == F_WHOLE) {
             tpcc_txn_warp(db, idx, db.type[idx], db.pw + db.poff[idx], sh);
         } else {
             if (lane == 0) exec_frag<S_TPCC>(db, fk);

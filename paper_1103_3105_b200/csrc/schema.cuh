@@ -876,7 +876,12 @@ DEV int fragments(const DevDb& db, uint32_t idx, uint64_t* out) {
     } else {
         const uint32_t w = p[0];
         if (t == 0) {
-            if (tpcc_no_aborts(db, p)) { if (out) out[0] = frag_key(w, idx, F_HOME); return 1; }
+            // an aborting NewOrder, or one whose lines are all home-warehouse, is whole
+            // (the PART executors run whole NewOrders with the warp procedure)
+            if (tpcc_no_aborts(db, p)) { if (out) out[0] = frag_key(w, idx, F_WHOLE); return 1; }
+            bool local = true;
+            for (uint32_t l = 0; l < p[3]; ++l) local &= p[5 + 3 * l] == w;
+            if (local) { if (out) out[0] = frag_key(w, idx, F_WHOLE); return 1; }
             int k = 0;
             if (out) out[k] = frag_key(w, idx, F_HOME);
             ++k;

@@ -164,6 +164,10 @@ typedef struct {
                                             (e.g. by a profiler) and used counter hand-offs only */
 #define GPUTX_STAT_KSET_DATAFLOW 2u      /* K-SET ran the dataflow executor (per-item completion
                                             counters, k-set-order dispatch) instead of rounds  */
+#define GPUTX_STAT_KSET_OWNER 4u         /* K-SET ran owner-local rounds: every warp executes the
+                                            k-sets of its own transactions (root key -> warp),
+                                            waiting only for cross-warp predecessors (default
+                                            for TM-1 / TPC-B / micro under the R/W rule)       */
 
 /* Create a database handle for cfg->schema with empty (zero) columns on cfg->device.
  * Errors: EINVAL (bad schema/dims/max_bulk), ENOMEM, ECUDA.  *out is NULL on error. */

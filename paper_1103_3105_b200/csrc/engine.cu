@@ -211,6 +211,16 @@ struct gputx_db {
     uint32_t exec_grid_override = 0;
     bool tpl_persistent = false;   // GPUTX_TPL_PERSISTENT=1: persistent per-lane tickets (slower: divergent spinners)
     uint32_t kset_cluster = 8;     // CTAs per thread-block cluster of the K-SET executor
+    // owner-local K-SET rounds: GPUTX_KSET_OWN=0 restores the global rounds
+    int kset_own = 1;
+    bool kset_ran_own = false;
+    int own_grid[2] = {0, 0};          // co-resident CTAs of the executor without / with waits
+    uint32_t* d_oseg = nullptr;        // owner segments [OWN_MAXW + 1] and the sort count word
+    uint32_t* d_prog = nullptr;        // per-warp progress [OWN_MAXW]
+    uint32_t* d_own = nullptr;         // per-transaction owner (dependency pass)
+    unsigned long long* d_wait = nullptr;   // per-transaction cross-owner wait
+    unsigned long long* d_owait = nullptr;  // the same in owner order
+    uint8_t* d_pub = nullptr;          // per-transaction "another warp waits for me"
     cudaEvent_t ev[8] = {};
     cudaEvent_t ev_sub[2] = {};       // submit start / end (ms_ingest)
     cudaEvent_t ev_x[4] = {};         // sharded exchange: pack start/end, merge start/end (ms_exchange)
@@ -545,6 +555,90 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     return GPUTX_OK;
 }
 
+constexpr uint32_t OWN_MAXW = 16384;    // owner warps (executor CTAs x 8)
+
+template <int S, bool DEP>
+const void* own_fn() {
+    return (const void*)kset_own_exec_kernel<S, kset_pw<S>(), DEP>;
+}
+
+// owner-local rounds: TM-1 / TPC-B / micro under the R/W rule, unsharded; the round
+// diagnostics (GPUTX_KSET_DIAG bits other than jitter / own-test bits) and round traces
+// belong to the global-round executor
+template <int S>
+bool kset_use_own(const gputx_db* db) {
+    if (S == S_TPCC || !db->kset_own || db->has_ts || db->trace_rounds) return false;
+    if (db->cfg.flags & GPUTX_FLAG_ADD_RULE) return false;
+    if (db->kset_diag & ~(1024u | 8192u | 16384u | 0xFFFF0000u)) return false;
+    const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
+    return !dep || db->rec_item_sorted;          // the dependency pass walks (item, ts) records
+}
+
+template <int S>
+gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
+    const uint32_t n = (uint32_t)db->n;
+    if (!db->d_oseg) {
+        gputx_status st;
+        if ((st = dalloc(db, &db->d_oseg, OWN_MAXW + 2)) || (st = dalloc(db, &db->d_prog, OWN_MAXW))) return st;
+    }
+    if (dep && !db->d_own) {
+        gputx_status st;
+        if ((st = dalloc(db, &db->d_own, db->max_bulk)) || (st = dalloc(db, &db->d_wait, db->max_bulk)) ||
+            (st = dalloc(db, &db->d_pub, db->max_bulk)) || (st = dalloc(db, &db->d_owait, db->max_bulk)))
+            return st;
+    }
+    int& gridv = db->own_grid[dep ? 1 : 0];
+    if (!gridv) {
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dep ? own_fn<S, true>() : own_fn<S, false>(), 256, 0);
+        gridv = std::max(1, per) * db->nsm;
+        gridv = std::min<int>(gridv, OWN_MAXW / 8);
+    }
+    uint32_t G = (uint32_t)gridv;
+    if (db->exec_grid_override) G = std::min(G, db->exec_grid_override);
+    const uint32_t NW = G * 8;
+    const uint32_t g = grid_for(n, 256, (uint32_t)db->nsm * 8);
+    uint64_t* kb = db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a;
+    uint32_t diag = db->kset_diag;
+    own_key_kernel<S><<<g, 256, 0, s>>>(v, db->d_perm, n, NW, kb, dep ? db->d_own : nullptr, diag,
+                                        db->d_oseg + OWN_MAXW + 1);
+    ++db->launches;
+    if (dep) {
+        CK(dev_fill(db->d_wait, 0, (uint64_t)n * 8, s));
+        CK(dev_fill(db->d_pub, 0, n, s));
+        CK(dev_fill(db->d_sc + SC_OWNGLOBAL, 0, 4, s));
+        own_dep_kernel<<<grid_for(db->max_rec, 256, (uint32_t)db->nsm * 8), 256, 0, s>>>(
+            db->d_sorted, db->d_sc + SC_NREC, db->d_own, db->d_D, db->d_wait, db->d_pub, db->d_sc, diag);
+        ++db->launches;
+    }
+    // stable sort on the owner bits: (owner, depth, type) order (count word set by own_key_kernel)
+    uint64_t* tmp = db->d_sorted == db->d_rec_a ? db->d_rec_a : db->d_rec_b;
+    uint64_t* sk = radix_sort_u64(kb, tmp, db->d_oseg + OWN_MAXW + 1, n, 32, bits_for(NW - 1), db->sort_ws, db->epoch, s);
+    db->launches += 2 + (bits_for(NW - 1) + 7) / 8;
+    constexpr int PW = kset_pw<S>();
+    own_gather_kernel<PW><<<g, 256, 0, s>>>(v, sk, n, NW, db->d_perm, db->d_D, dep ? db->d_wait : nullptr,
+                                            dep ? db->d_pub : nullptr, db->d_done, db->d_ptype, db->d_pp, db->d_cnt,
+                                            dep ? db->d_owait : nullptr, db->d_oseg, db->d_prog);
+    ++db->launches;
+    STAGE("own group");
+    cudaEventRecord(db->ev[5], s);
+    DevDb vv = v;
+    const uint32_t* oseg = db->d_oseg;
+    const uint32_t* oidx = db->d_done;
+    const uint8_t* otype = db->d_ptype;
+    const uint32_t* opp = db->d_pp;
+    const uint32_t* odep = db->d_cnt;
+    const unsigned long long* wt = db->d_owait;
+    uint32_t* prog = db->d_prog;
+    uint32_t* sc = db->d_sc;
+    void* args[] = {&vv, &oseg, &oidx, &otype, &opp, &odep, &wt, &prog, &sc, &diag};
+    TRY(launch_coop(db, dep ? own_fn<S, true>() : own_fn<S, false>(), (int)G, 256, args));
+    ++db->launches;
+    return GPUTX_OK;
+}
+
 template <int S>
 bool kset_use_dataflow(const gputx_db* db) {
     if (S == S_TM1) return false;       // records sorted by item component, not by item
@@ -572,10 +666,25 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     ++db->launches;
     scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
     ++db->launches;
-    group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
-                                                     db->d_perm, db->d_poff, db->d_pw, db->d_ptype, db->d_pp, P);
+    const bool df = kset_use_dataflow<S>(db) && db->d_item_sorted;
+    const bool own = !df && kset_use_own<S>(db) && db->n > 0;
+    if (own)        // the owner gather stages types / parameters itself
+        group_kernel<1, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
+                                              db->d_perm, nullptr, nullptr, nullptr, nullptr, P);
+    else
+        group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt,
+                                                         db->d_goff, db->d_perm, db->d_poff, db->d_pw, db->d_ptype,
+                                                         db->d_pp, P);
     ++db->launches;
     STAGE("group");
+    db->kset_ran_own = own;
+    if (own) {
+        TRY(kset_own_exec<S>(db, v));
+        STAGE("kset exec");
+        cudaEventRecord(db->ev[6], s);
+        db->has_perm = true;
+        return GPUTX_OK;
+    }
     cudaEventRecord(db->ev[5], s);
     // K-SET dataflow executor (deep graphs: TPC-B / TPC-C / micro under the R/W rule): the
     // k-sets are executed in k-set order without round barriers -- every transaction waits
@@ -583,7 +692,6 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     // completion counters keyed by position in the item's ts-ordered access list (the same
     // keys as TPL, PAPER.md:370-388 / DESIGN.md R-S5); dispatch in perm order makes every
     // wait point to a transaction of smaller depth, already taken by a running lane.
-    const bool df = kset_use_dataflow<S>(db) && db->d_item_sorted;
     db->kset_ran_df = df;
     if (df) {
         ++db->epoch;
@@ -1371,6 +1479,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // CTAs are separated by the hardware cluster barrier); 0 disables clusters
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DF")) db->kset_df = atoi(e);
+    if (const char* e = getenv("GPUTX_KSET_OWN")) db->kset_own = atoi(e);
+    // diag 16384 (tests: arbitrary owners) needs (item, ts)-sorted records for the dependency pass
+    if (schema == S_TM1 && (db->kset_diag & 16384u)) db->rank_stream = 0;
     if (const char* e = getenv("GPUTX_KSET_DF_AHEAD")) db->kset_df_ahead = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_KSET_DF_GRID")) db->kset_df_grid = (uint32_t)atoi(e);
     // (sized on the plain variant; the explicit-ts / sharded variant gets the same attributes)
@@ -2075,7 +2186,8 @@ gputx_status execute_finish(gputx_db* db, gputx_stats* stats) {
             stats->ms_exchange = a + b;
         }
         stats->flags = (db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0) |
-                       ((ranked && eff == GPUTX_KSET && db->kset_ran_df) ? GPUTX_STAT_KSET_DATAFLOW : 0);
+                       ((ranked && eff == GPUTX_KSET && db->kset_ran_df) ? GPUTX_STAT_KSET_DATAFLOW : 0) |
+                       ((ranked && eff == GPUTX_KSET && db->kset_ran_own) ? GPUTX_STAT_KSET_OWNER : 0);
         cudaGetLastError();
     }
     return GPUTX_OK;
@@ -2386,11 +2498,21 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
     };
     if (k) TRY(h2d(0));
     int last = 0;
+    static const bool ptrace = getenv("GPUTX_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> pev;
+    auto pmark = [&](cudaStream_t st_) {
+        if (!ptrace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st_);
+        pev.push_back(e);
+    };
     for (uint64_t i = 0; i < k; ++i) {
         const int sl = (int)(i & 1);
         last = sl;
         if (i + 1 < k) TRY(h2d(i + 1));              // next bulk's copy overlaps this one's execution
         TRY(submit_check(db, &bulks[i]));
+        pmark(s);
         CK(cudaStreamWaitEvent(s, db->ev_in[sl], 0));       // bulk i has landed in slot sl
         CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0)); // bulk i-2's results left slot sl
         std::swap(db->d_type, db->in_type[sl]);
@@ -2405,15 +2527,19 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
         db->first_ts = db->next_ts;
         TRY(finish_submit(db, n, n ? bulks[i].param_off[n] : 0));
         db->next_ts += n;
+        pmark(s);
         TRY(gputx_execute(db, st, stats ? &stats[i] : nullptr));
+        pmark(s);
         // results stay in the engine's d_status / d_out until the next bulk swaps them out; the
         // D2H reads them from there on its own stream, overlapping the next execution
         CK(cudaEventRecord(db->ev_res[sl], s));
         CK(cudaStreamWaitEvent(db->st_d2h, db->ev_res[sl], 0));
+        pmark(db->st_d2h);
         if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->d_status, n, cudaMemcpyDeviceToHost, db->st_d2h));
         if (n && out && out[i])
             CK(cudaMemcpyAsync(out[i], db->d_out, n * db->out_stride, cudaMemcpyDeviceToHost, db->st_d2h));
         CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
+        pmark(db->st_d2h);
         // the next bulk gets the other slot's result buffers (swap below) -- these stay put
         std::swap(db->d_status, db->res_status[sl]);
         std::swap(db->d_out, db->res_out[sl]);
@@ -2422,6 +2548,15 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
     // after this call covers the whole run), then wait for it
     for (int sl = 0; sl < 2; ++sl) CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
     CK(cudaStreamSynchronize(s));
+    if (ptrace) {
+        for (size_t j = 0; j < pev.size(); ++j) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pev[0], pev[j]);
+            fprintf(stderr, "%s%s%.3f", j % 5 == 0 ? "\n[pipe] " : " ", j % 5 == 0 ? "" : "", ms);
+        }
+        fprintf(stderr, "\n[pipe] columns: pre-wait, exec-start, exec-end, d2h-start, d2h-end\n");
+        for (auto e : pev) cudaEventDestroy(e);
+    }
     if (k) {                                   // gputx_read_results: the last bulk's results
         std::swap(db->d_status, db->res_status[last]);
         std::swap(db->d_out, db->res_out[last]);
@@ -2504,6 +2639,7 @@ void gputx_close_db(gputx_db* db) {
     dfree(db, db->d_order);
     dfree(db, db->tm1_sub); dfree(db, db->tm1_ai); dfree(db, db->tm1_sf); dfree(db, db->tm1_cf);
     dfree(db, db->d_undo);
+    dfree(db, db->d_oseg); dfree(db, db->d_prog); dfree(db, db->d_own); dfree(db, db->d_wait); dfree(db, db->d_pub); dfree(db, db->d_owait);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
                   db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,
                   db->d_rstatus, db->d_rout};

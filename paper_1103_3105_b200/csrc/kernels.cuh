@@ -1667,6 +1667,255 @@ __global__ void __launch_bounds__(KB) kset_exec_kernel(DevDb db, const uint32_t*
 }
 
 // =====================================================================================
+// K-SET with owner-local rounds (DESIGN.md §4 "Owner-local rounds").  Every transaction
+// gets an owner warp from its root key (TM-1 subscriber, TPC-B home branch, micro tuple);
+// each warp executes ITS transactions k-set by k-set (Property 1 within a k-set, PAPER.md
+// :123-125; k-sets in increasing k, §5.3), its rounds separated by __syncwarp().  Nothing
+// is global: a transaction whose T-dependency predecessor belongs to
+// another warp waits, before it runs, until that warp's progress word says the
+// predecessor's k-set is done; every other predecessor is the warp's own, in an earlier
+// round.  progress[w] = "all of w's rounds below this value are done" (monotone), written
+// only at the end of a round that some other warp waits for.  Waits point to strictly
+// smaller k, and all warps are co-resident (cooperative launch), so the warp at the
+// smallest pending k can always proceed: no deadlock.
+// =====================================================================================
+constexpr uint32_t OWN_INF = 0xFFFFFFFFu;
+constexpr unsigned long long OWN_GLOBAL = ~0ull;   // wait: every warp's progress >= own k
+constexpr int SC_OWNGLOBAL = 39;                    // some transaction waits globally
+constexpr uint32_t OWN_WALK = 64;                   // records walked per conflict search
+
+template <int S>
+DEV uint32_t own_of(const uint32_t* p, uint32_t nw, uint32_t idx, uint32_t diag) {
+    if (diag & 16384u) return (uint32_t)(nbr_hash(idx) % nw);      // tests: arbitrary owners
+    if (S == S_TPCB) return p[2] % nw;                               // home branch
+    return (uint32_t)(nbr_hash((uint64_t)p[0]) % nw);              // TM-1 subscriber, micro tuple
+}
+
+// keys[j] = owner(perm[j]) << 32 | j over the (depth, type)-ordered perm; a stable sort on
+// the owner bits then gives (owner, depth, type) order.  own[idx] = owner (dependency pass).
+template <int S>
+__global__ void __launch_bounds__(256) own_key_kernel(DevDb db, const uint32_t* __restrict__ perm, uint32_t n,
+                                                      uint32_t nw, uint64_t* keys, uint32_t* own, uint32_t diag,
+                                                      uint32_t* n_out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;      // the owner sort's count word
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t idx = perm[j];
+        const uint32_t o = own_of<S>(db.pw + db.poff[idx], nw, idx, diag);
+        keys[j] = ((uint64_t)o << 32) | j;
+        if (own) own[idx] = o;
+    }
+}
+
+DEV void own_add_wait(unsigned long long* wait, uint32_t idx, uint32_t o, uint32_t need, uint32_t* sc) {
+    const unsigned long long v = ((unsigned long long)o << 32) | need;
+    const unsigned long long old = atomicCAS(&wait[idx], 0ull, v);
+    if (old == 0ull || old == v) return;
+    if ((uint32_t)(old >> 32) == o) { atomicMax(&wait[idx], v); return; }   // same warp: the later k
+    atomicExch(&wait[idx], OWN_GLOBAL);                                       // two warps: wait for all
+    atomicOr(&sc[SC_OWNGLOBAL], 1u);
+}
+
+// Cross-owner predecessors from the (item, ts)-sorted records (R/W rule):
+// a record conflicts with the earlier records of its item back to (and including) the
+// previous write -- a read only with that write.  Predecessors further back are ordered
+// before that write, which waited for them itself.  A foreign predecessor p of txn t
+// gives t a wait (owner(p), D[p] + 1) and marks p "publish".  More than one foreign warp,
+// or a walk longer than OWN_WALK records, makes t wait for every warp (OWN_GLOBAL).
+__global__ void __launch_bounds__(256) own_dep_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                      const uint32_t* __restrict__ own, const uint32_t* __restrict__ D,
+                                                      unsigned long long* wait, uint8_t* pub, uint32_t* sc,
+                                                      uint32_t diag) {
+    const uint32_t nrec = *nrec_ptr;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const uint64_t item = key_item(k);
+        const uint32_t idx = key_idx(k), m = key_mode(k), o = own[idx];
+        uint32_t steps = 0;
+        for (uint32_t j = i; j-- > 0;) {
+            const uint64_t kj = keys[j];
+            if (key_item(kj) != item) break;
+            const uint32_t mj = key_mode(kj);
+            if (m == 1u || mj == 1u) {
+                const uint32_t ij = key_idx(kj), oj = own[ij];
+                if (oj != o) {
+                    if (diag & 8192u) { atomicExch(&wait[idx], OWN_GLOBAL); atomicOr(&sc[SC_OWNGLOBAL], 1u); }
+                    else own_add_wait(wait, idx, oj, D[ij] + 1u, sc);
+                    pub[ij] = 1;
+                }
+            }
+            if (mj == 1u) break;
+            if (++steps >= OWN_WALK) {
+                atomicExch(&wait[idx], OWN_GLOBAL);
+                atomicOr(&sc[SC_OWNGLOBAL], 1u);
+                break;
+            }
+        }
+    }
+}
+
+// Owner-ordered execution arrays: oidx / otype / odep / the first PW parameter words, the
+// owner segments oseg[0..nw] and every warp's initial progress (its first k, or INF).
+// With the dependency pass, owait[pos] = wait[idx] and bit 31 of odep = pub[idx]: the
+// executor's staging is then one level of coalesced loads.
+constexpr uint32_t OWN_PUB = 0x80000000u;
+template <int PW>
+__global__ void __launch_bounds__(256) own_gather_kernel(DevDb db, const uint64_t* __restrict__ skeys, uint32_t n,
+                                                         uint32_t nw, const uint32_t* __restrict__ perm,
+                                                         const uint32_t* __restrict__ D,
+                                                         const unsigned long long* __restrict__ wait,
+                                                         const uint8_t* __restrict__ pub, uint32_t* oidx,
+                                                         uint8_t* otype, uint32_t* opp, uint32_t* odep,
+                                                         unsigned long long* owait, uint32_t* oseg, uint32_t* prog) {
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n; pos += gridDim.x * blockDim.x) {
+        const uint64_t sk = skeys[pos];
+        const uint32_t o = (uint32_t)(sk >> 32), idx = perm[(uint32_t)sk];
+        const uint32_t d = D[idx];
+        oidx[pos] = idx;
+        otype[pos] = db.type[idx];
+        odep[pos] = d | (pub && pub[idx] ? OWN_PUB : 0u);
+        if (wait) owait[pos] = wait[idx];
+        if (PW > 0) {
+            const uint32_t* src = db.pw + db.poff[idx];
+#pragma unroll
+            for (int w = 0; w < PW; w += 4)
+                *reinterpret_cast<uint4*>(opp + (uint64_t)pos * PW + w) =
+                    make_uint4(src[w], src[w + 1], src[w + 2], src[w + 3]);
+        }
+        const int64_t prev = pos ? (int64_t)(skeys[pos - 1] >> 32) : -1;
+        if ((int64_t)o != prev) {
+            for (int64_t q = prev + 1; q < (int64_t)o; ++q) { oseg[q] = pos; prog[q] = OWN_INF; }   // empty owners
+            oseg[o] = pos;
+            prog[o] = d;
+        }
+        if (pos == n - 1)
+            for (uint32_t q = o + 1; q <= nw; ++q) { oseg[q] = n; if (q < nw) prog[q] = OWN_INF; }
+    }
+}
+
+// The warp's segment is staged 32 entries at a time in registers, three chunks deep: A
+// (being executed), B (landed; its rows warmed into L2 when it became next) and C (in
+// flight).  Round d0 = the entries from the cursor on with depth d0 (a prefix: the
+// segment is (depth, type)-ordered); lane L takes the round's L-th entry from A or B by
+// shuffles, so no load sits between two rounds -- only the round's own memory accesses
+// and the __syncwarp() that orders them before the next round's.
+template <int S, int PW, bool DEP>
+__global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint32_t* __restrict__ oseg,
+                                                            const uint32_t* __restrict__ oidx,
+                                                            const uint8_t* __restrict__ otype,
+                                                            const uint32_t* __restrict__ opp,
+                                                            const uint32_t* __restrict__ odep,
+                                                            const unsigned long long* __restrict__ owait,
+                                                            uint32_t* prog, uint32_t* sc, uint32_t diag) {
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    constexpr int NP = PW > 0 ? PW : 1;
+    const uint32_t lane = lane_id();
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t lo = oseg[w], hi = oseg[w + 1];
+    if (lo >= hi) return;
+    const bool gmode = DEP && __ldcg(&sc[SC_OWNGLOBAL]) != 0u;
+    struct E {
+        uint32_t idx, t, d;              // d: depth | OWN_PUB; INF past the segment
+        unsigned long long wt;
+        uint32_t q[NP];
+    };
+    auto load = [&](uint32_t base, E& e) {
+        const uint32_t j = base + lane;
+        e.idx = OWN_INF; e.t = 0; e.d = OWN_INF; e.wt = 0;
+#pragma unroll
+        for (int x = 0; x < NP; ++x) e.q[x] = 0;
+        if (j < hi) {
+            e.idx = __ldg(&oidx[j]);
+            e.t = __ldg(&otype[j]);
+            e.d = __ldg(&odep[j]);
+            if (PW > 0) {
+#pragma unroll
+                for (int x = 0; x < NP; x += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(opp + (uint64_t)j * PW + x));
+                    e.q[x] = v.x; e.q[x + 1] = v.y; e.q[x + 2] = v.z; e.q[x + 3] = v.w;
+                }
+            }
+            if (DEP) e.wt = __ldg(&owait[j]);
+        }
+    };
+    // entry (cursor + lane) of the window A|B, by shuffles (every lane takes part)
+    auto pick = [&](const E& a, const E& b, uint32_t src, E& x) {
+        const uint32_t sl = src & 31u;
+        const bool fa = src < 32u;
+        uint32_t u, v;
+        u = __shfl_sync(FULL, a.idx, sl); v = __shfl_sync(FULL, b.idx, sl); x.idx = fa ? u : v;
+        u = __shfl_sync(FULL, a.t, sl);   v = __shfl_sync(FULL, b.t, sl);   x.t = fa ? u : v;
+        u = __shfl_sync(FULL, a.d, sl);   v = __shfl_sync(FULL, b.d, sl);   x.d = fa ? u : v;
+        if (DEP) {
+            const unsigned long long ua = __shfl_sync(FULL, a.wt, sl), ub = __shfl_sync(FULL, b.wt, sl);
+            x.wt = fa ? ua : ub;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            u = __shfl_sync(FULL, a.q[k], sl); v = __shfl_sync(FULL, b.q[k], sl); x.q[k] = fa ? u : v;
+        }
+    };
+    auto depth_at = [&](const E& a, const E& b, uint32_t p) -> uint32_t {   // uniform p < 64
+        const uint32_t u = __shfl_sync(FULL, a.d, p & 31u), v = __shfl_sync(FULL, b.d, p & 31u);
+        return (p < 32u ? u : v) & ~OWN_PUB;
+    };
+    E A, B, C;
+    load(lo, A);
+    load(lo + 32, B);
+    load(lo + 64, C);
+    if (B.idx != OWN_INF) warm_rows<S>(db, B.t, B.q);
+    uint32_t ca = lo, p = 0;        // window base, cursor offset in it (< 32)
+    bool pubr = false;
+    uint32_t d0 = depth_at(A, B, 0);
+    while (ca + p < hi) {
+        E X;
+        pick(A, B, p + lane, X);
+        const uint32_t xd = X.d & ~OWN_PUB;
+        const uint32_t cnt = __popc(__ballot_sync(FULL, xd == d0));       // >= 1; prefix of the window
+        if (lane < cnt) {
+            if (DEP && X.wt) {
+                SpinWatch wd;
+                if (X.wt == OWN_GLOBAL) {
+                    for (uint32_t q = 0; q < nw; ++q) {
+                        if (q == w) continue;
+                        while (ld_acquire(&prog[q]) < d0)
+                            if (wd.expired(&sc[SC_DEADLOCK])) break;
+                    }
+                } else {
+                    const uint32_t ow = (uint32_t)(X.wt >> 32), need = (uint32_t)X.wt;
+                    uint32_t spins = 0;
+                    while (ld_acquire(&prog[ow]) < need) {
+                        if (++spins > 16) __nanosleep(64);
+                        if (wd.expired(&sc[SC_DEADLOCK])) break;
+                    }
+                }
+            }
+            kx_jitter(diag, d0, w, lane);
+            exec_txn_p<S, false>(db, X.idx, X.t, X.q);
+        }
+        if (DEP) pubr |= __ballot_sync(FULL, lane < cnt && (X.d & OWN_PUB)) != 0u;
+        p += cnt;
+        if (p >= 32u) {                  // A consumed: slide the window
+            A = B;
+            B = C;
+            ca += 32;
+            p -= 32;
+            load(ca + 64, C);
+            if (B.idx != OWN_INF) warm_rows<S>(db, B.t, B.q);
+        }
+        const uint32_t dn = ca + p < hi ? depth_at(A, B, p) : OWN_INF;
+        if (dn != d0) {                  // round d0 of this warp ends
+            const bool publish = DEP && (pubr || gmode);
+            if (publish) __threadfence();          // each lane's writes, at gpu scope
+            __syncwarp();                          // ... and before the warp's next round
+            if (publish && lane == 0) st_release(&prog[w], dn);
+            pubr = false;
+            d0 = dn;
+        }
+    }
+}
+
+// =====================================================================================
 // PART
 // =====================================================================================
 template <int S>

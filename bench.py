@@ -411,9 +411,11 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     cap = 3 * (args.warmup + args.steps) + 12          # bulks the merged insert tables must hold
     nmax = max(b.n for b in bulks)
     max_bulk = nmax if ws == 1 else min(1 << 24, nmax + nmax // 2 + 1024)
+    # single GPU: packed output records (GPUTX_FLAG_PACKED_OUT) -- the result transfer moves
+    # only what the procedures return; sharded handles keep the stride
     db = Database(wl["schema"], dims.dims, max_bulk, image, device=dev.index, stream=stream.cuda_stream,
                   insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws,
-                  add_rule=wl.get("add_rule", False))
+                  add_rule=wl.get("add_rule", False), packed_out=ws == 1)
 
     # ---- parity gate (N = 1): bulk 0 vs the oracle, before anything is timed ----------
     parity, parity_err, ref0 = None, None, None
@@ -518,6 +520,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     out_pin = torch.empty(nmax * db.stride, dtype=torch.uint8).pin_memory().numpy().reshape(nmax, db.stride)
     e2e_ms = []
     e2e_committed = 0
+    e2e_out_bytes = 0.0
     if ws == 1:
         # gputx_run_bulks: the K bulks' H2D / D2H overlap the executions (two copy streams);
         # results alternate between two pinned host buffers (each read back at the end)
@@ -536,6 +539,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         e1.synchronize()
         e2e_ms = [e0.elapsed_time(e1)]
         e2e_committed = sum(x["committed"] for x in sts)
+        e2e_out_bytes = float(np.mean([x["out_bytes"] for x in sts]))
     for k in range(args.warmup + args.steps) if ws > 1 else []:
         b = hb[k % len(hb)]
         nb_ = b.type.shape[0]
@@ -559,7 +563,9 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     e2e_total = max_over_ranks(sum(e2e_ms))
     e2e_committed = sum_over_ranks(float(e2e_committed))
     h2d = int(np.mean([b.nbytes() for b in hb]))
-    d2h = int(np.mean([b.type.shape[0] for b in hb])) * (1 + db.stride)
+    # status u8[n] + the output records the result read moved (packed at N = 1)
+    d2h = int(np.mean([b.type.shape[0] for b in hb]) + (e2e_out_bytes if ws == 1 else
+                                                           np.mean([b.type.shape[0] for b in hb]) * db.stride))
     # the link the e2e number is bound by: pinned copies of one step's bytes, each direction
     # alone (outside every timed region); the overlapped e2e step can't beat max(H2D, D2H)
     pcie = {}
@@ -607,8 +613,11 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
             rank_bytes(wl["schema"], last["records"], last["rank_passes"], nloc), phase["ms_rank"])
     if ws == 1:
         # K-SET's dataflow executor (TPC-C default, stats flag 2) runs the counter-lock kernels
+        # owner-local rounds (TM-1 / TPC-B / micro default, stats flag 4) run kset_own_exec_kernel
+        fl = last.get("flags", 0)
         ek = (("tpl_exec_warp_kernel" if wl["schema"] == W.TPCC else "tpl_exec_persistent_kernel")
-              if eff == "kset" and (last.get("flags", 0) & 2) else f"{eff}_exec_kernel")
+              if eff == "kset" and (fl & 2) else "kset_own_exec_kernel" if eff == "kset" and (fl & 4)
+              else f"{eff}_exec_kernel")
         cand[ek] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1]) if cand else None
     roofline = None
@@ -649,7 +658,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         "e2e": {"value": e2e_committed / (e2e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps, "pcie": pcie,
                 "method": ("gputx_run_bulks: H2D of bulk i+1 and D2H of bulk i-1 overlap bulk i (two copy "
-                           "streams); back-to-back bulks, no L2 flush in between") if ws == 1 else
+                           "streams); back-to-back bulks, no L2 flush in between; packed output records "
+                           "(GPUTX_FLAG_PACKED_OUT)") if ws == 1 else
                           "per step: H2D, sharded step, D2H (serial)"},
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
         "phases_ms": phase,

@@ -125,6 +125,18 @@ typedef struct {
  *   TPL lock keys follow the rule; the final database and every output stay equal to
  *   serial execution in ts order (the increments are atomic and commutative). */
 #define GPUTX_FLAG_ADD_RULE 1u
+/* GPUTX_FLAG_PACKED_OUT: variable-size output records.  Transaction i's record is the
+ * first gputx_out_size(type, params) bytes of its fixed-stride record (the rest of that
+ * record is always zero), at byte offset out_off[i] = sum of the sizes before it, so a
+ * bulk's outputs are one dense array of out_off[n] bytes instead of n * gputx_out_stride:
+ * the result transfer the paper counts in the bulk time carries only
+ * what the procedures return.  Sizes (multiples of 8; micro 4):
+ *   TPC-B 8; micro 4; TM-1 GSD 40, GND 32, GAD 16, USD / UL / ICF / DCF 0;
+ *   TPC-C NewOrder 16 + 12 x ol_cnt rounded up to 8, Payment 16.
+ * The offsets are computed at submit (gputx_read_out_offsets); gputx_read_results,
+ * gputx_results_device and gputx_run_bulks then move out_off[n] bytes.  Not with sharding
+ * or the transaction pool (EINVAL there). */
+#define GPUTX_FLAG_PACKED_OUT 2u
 
 typedef struct {
     const uint8_t* type;        /* u8[n]                                                */
@@ -157,6 +169,8 @@ typedef struct {
     double ms_exchange;      /* sharded: device time of the cross-shard exchange of this bulk (pack,
                                 peer transfer, merge by ts; return of fragment outputs), else 0   */
     uint64_t flags;          /* GPUTX_STAT_* bits below                                          */
+    uint64_t out_bytes;      /* bytes of this bulk's output records: n * gputx_out_stride, or the
+                                packed size with GPUTX_FLAG_PACKED_OUT (what a result read moves) */
 } gputx_stats;
 
 /* gputx_stats.flags */
@@ -222,7 +236,8 @@ gputx_status gputx_wait(gputx_db* db, gputx_stats* stats);
  * (double-buffered device slots).  Equivalent to k x (gputx_submit_bulk + gputx_execute +
  * gputx_read_results) -- same results, same errors (the first failing bulk stops the run);
  * the paper counts the transfers in the bulk time and keeps them below 5% (PAPER.md:449,
- * 515).  status[i] (u8[n_i]) and out[i] (n_i * gputx_out_stride) are caller-owned host
+ * 515).  status[i] (u8[n_i]) and out[i] (n_i * gputx_out_stride bytes; with
+ * GPUTX_FLAG_PACKED_OUT the bulk's packed outputs, at most that) are caller-owned host
  * buffers (pinned for real overlap; entries may be NULL); stats: k entries or NULL.
  * Returns after the last result has landed; every bulk takes ts = next_ts + position. */
 gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, gputx_strategy strategy,
@@ -261,7 +276,8 @@ gputx_status gputx_set_chooser(gputx_db* db, uint64_t w0_bar, uint64_t d_bar, ui
 gputx_status gputx_set_grouping(gputx_db* db, uint32_t p);
 
 /* Copy the last executed bulk's results to host: status u8[n] (may be NULL) and the
- * output records (n * gputx_out_stride bytes; out may be NULL).  ECAPACITY if out_bytes
+ * output records (n * gputx_out_stride bytes, or out_off[n] with GPUTX_FLAG_PACKED_OUT;
+ * out may be NULL).  ECAPACITY if out_bytes
  * is short, ESTATE before the first execute.  Sharded: the n home transactions passed to
  * gputx_shard_pack, in that order, after gputx_shard_return_merge. */
 gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64_t out_bytes);
@@ -272,6 +288,11 @@ gputx_status gputx_results_device(gputx_db* db, const uint8_t** status, const vo
                                   uint64_t* n);
 
 uint32_t gputx_out_stride(gputx_schema schema);
+
+/* GPUTX_FLAG_PACKED_OUT: the submitted bulk's output offsets u32[n + 1] (out_off[n] = the
+ * bytes of its packed outputs) to host; *bytes (may be NULL) = out_off[n].  Without the
+ * flag the records are fixed-stride and this returns EINVAL.  ESTATE before a submit. */
+gputx_status gputx_read_out_offsets(gputx_db* db, uint32_t* host, uint64_t n, uint64_t* bytes);
 
 /* Snapshot one current column to host (exact bytes of the column). */
 gputx_status gputx_read_column(gputx_db* db, const char* name, void* host, uint64_t bytes);

@@ -125,6 +125,9 @@ struct gputx_db {
     uint32_t* d_pw = nullptr;
     uint8_t* d_status = nullptr;
     uint8_t* d_out = nullptr;
+    bool packed = false;               // GPUTX_FLAG_PACKED_OUT
+    uint32_t* d_out_off = nullptr;     // packed record offsets [n + 1]
+    uint64_t out_bytes = 0;            // the submitted bulk's output bytes (packed: out_off[n])
     uint32_t out_stride = 0;
     uint32_t* d_ins_off = nullptr;   // 4 * (max_bulk + 1)
     // indexes
@@ -218,6 +221,7 @@ struct gputx_db {
     uint32_t* d_oseg = nullptr;        // owner segments [OWN_MAXW + 1] and the sort count word
     uint32_t* d_prog = nullptr;        // per-warp progress [OWN_MAXW]
     uint32_t* d_own = nullptr;         // per-transaction owner (dependency pass)
+    uint32_t* d_oout = nullptr;        // packed output offsets in owner order
     unsigned long long* d_wait = nullptr;   // per-transaction cross-owner wait
     unsigned long long* d_owait = nullptr;  // the same in owner order
     uint8_t* d_pub = nullptr;          // per-transaction "another warp waits for me"
@@ -362,6 +366,7 @@ DevDb make_devdb(gputx_db* db) {
     v.status = db->d_status;
     v.out = db->d_out;
     v.out_stride = db->out_stride;
+    v.out_off = db->packed ? db->d_out_off : nullptr;
     for (size_t k = 0; k < db->cols.size() && k < (size_t)MAX_COLS; ++k) v.col[k] = db->cols[k].d;
     int c = 0;
     for (auto& t : db->ins) {
@@ -582,6 +587,7 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     if (!db->d_oseg) {
         gputx_status st;
         if ((st = dalloc(db, &db->d_oseg, OWN_MAXW + 2)) || (st = dalloc(db, &db->d_prog, OWN_MAXW))) return st;
+        if (db->packed && (st = dalloc(db, &db->d_oout, db->max_bulk))) return st;
     }
     if (dep && !db->d_own) {
         gputx_status st;
@@ -620,7 +626,8 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     constexpr int PW = kset_pw<S>();
     own_gather_kernel<PW><<<g, 256, 0, s>>>(v, sk, n, NW, db->d_perm, db->d_D, dep ? db->d_wait : nullptr,
                                             dep ? db->d_pub : nullptr, db->d_done, db->d_ptype, db->d_pp, db->d_cnt,
-                                            dep ? db->d_owait : nullptr, db->d_oseg, db->d_prog);
+                                            dep ? db->d_owait : nullptr, db->d_oseg, db->d_prog,
+                                            db->packed ? db->d_oout : nullptr);
     ++db->launches;
     STAGE("own group");
     cudaEventRecord(db->ev[5], s);
@@ -631,9 +638,10 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     const uint32_t* opp = db->d_pp;
     const uint32_t* odep = db->d_cnt;
     const unsigned long long* wt = db->d_owait;
+    const uint32_t* oout = db->packed ? db->d_oout : nullptr;
     uint32_t* prog = db->d_prog;
     uint32_t* sc = db->d_sc;
-    void* args[] = {&vv, &oseg, &oidx, &otype, &opp, &odep, &wt, &prog, &sc, &diag};
+    void* args[] = {&vv, &oseg, &oidx, &otype, &opp, &odep, &wt, &oout, &prog, &sc, &diag};
     TRY(launch_coop(db, dep ? own_fn<S, true>() : own_fn<S, false>(), (int)G, 256, args));
     ++db->launches;
     return GPUTX_OK;
@@ -956,7 +964,8 @@ void launch_ingest(gputx_db* db, uint32_t n_words, const uint32_t* nw_ptr) {
     DevDb v = make_devdb(db);
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, nw_ptr, db->type_mask, db->d_ins_off,
-                                                (uint32_t)(db->n + 1), db->d_sc, db->d_xflag);
+                                                (uint32_t)(db->n + 1), db->d_sc, db->d_xflag,
+                                                db->packed ? db->d_out_off : nullptr);
                                                 ++db->launches;
 }
 
@@ -1002,6 +1011,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
             for (int t = 0; t < ntab; ++t)
                 scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n,
                          db->d_sc + SC_INS0 + t);
+        if (db->packed) scan_u32(db, db->d_out_off, db->d_out_off, nullptr, n, db->d_sc + SC_OUTBYTES);
     }
     cudaEventRecord(db->ev_sub[1], s);
     TRY(pull_sc(db, s));
@@ -1019,6 +1029,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     // TPC-B: when every transaction is a home deposit, its history row is its position (no
     // ins_off load on the executors' critical paths, e.g. PART's serial branch chains)
     db->ins_dense = db->schema == S_TPCB && !db->h_sc[SC_SPARSE];
+    db->out_bytes = db->packed ? (uint64_t)db->h_sc[SC_OUTBYTES] : n * db->out_stride;
     // insert rows this bulk will append (decisions are static: two-phase procedures)
     for (auto& t : db->ins) {
         t.pending = db->h_sc[SC_INS0 + t.table_id];
@@ -1072,7 +1083,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     v.ts = nullptr;
     const uint32_t g = grid_for(m, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, s>>>(v, db->s_pw, words, nullptr, db->type_mask, db->st_ins, (uint32_t)(m + 1),
-                                       db->d_sc, nullptr);
+                                       db->d_sc, nullptr, nullptr);
     TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
@@ -1270,6 +1281,8 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->nshards = cfg->nshards ? cfg->nshards : 1;
     db->shard = cfg->shard;
     if (db->nshards > MAX_SHARDS || db->shard >= db->nshards) { delete db; return GPUTX_EINVAL; }
+    db->packed = (cfg->flags & GPUTX_FLAG_PACKED_OUT) != 0;
+    if (db->packed && db->nshards > 1) { delete db; return GPUTX_EINVAL; }   // fixed-stride exchange records
     db->nroot = d[0];                       // branches / subscribers / warehouses
     if (db->nroot < db->nshards) { delete db; return GPUTX_EINVAL; }
     db->root_lo = (uint32_t)(((uint64_t)db->shard * db->nroot + db->nshards - 1) / db->nshards);
@@ -1351,6 +1364,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
         (st = dalloc(db, &db->d_ts, NB + 1)) || (st = dalloc(db, &db->d_order, NB + 1)))
         return bail(st);
     if (schema == S_TPCB && (st = dalloc(db, &db->d_undo, NB * UNDO_SLOTS))) return bail(st);
+    if (db->packed && (st = dalloc(db, &db->d_out_off, NB + 1))) return bail(st);
     if (schema == S_TM1) {
         const uint64_t P = d[0];
         if ((st = dalloc(db, &db->tm1_sub, P * TM1_SUBROW)) || (st = dalloc(db, &db->tm1_ai, 4 * P * TM1_AIROW)) ||
@@ -2099,8 +2113,8 @@ gputx_status execute_launch(gputx_db* db, gputx_strategy st) {
     if (n) {
         zero_bytes_kernel<<<grid_for((n + 15) / 16, 256, 148 * 4), 256, 0, s>>>(db->d_status, n);
         if (db->schema != S_TPCB && !(db->kset_diag & 4096u))
-            zero_bytes_kernel<<<grid_for(n * db->out_stride / 16 + 1, 256, 148 * 8), 256, 0, s>>>(db->d_out,
-                                                                                             n * db->out_stride);
+            zero_bytes_kernel<<<grid_for(db->out_bytes / 16 + 1, 256, 148 * 8), 256, 0, s>>>(db->d_out,
+                                                                                         db->out_bytes);
         db->launches += db->schema != S_TPCB ? 2 : 1;
         if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
         else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
@@ -2185,6 +2199,7 @@ gputx_status execute_finish(gputx_db* db, gputx_stats* stats) {
             cudaEventElapsedTime(&b, db->ev_x[2], db->ev_x[3]);
             stats->ms_exchange = a + b;
         }
+        stats->out_bytes = db->nshards > 1 ? db->nh * db->out_stride : db->out_bytes;
         stats->flags = (db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0) |
                        ((ranked && eff == GPUTX_KSET && db->kset_ran_df) ? GPUTX_STAT_KSET_DATAFLOW : 0) |
                        ((ranked && eff == GPUTX_KSET && db->kset_ran_own) ? GPUTX_STAT_KSET_OWNER : 0);
@@ -2219,11 +2234,22 @@ gputx_status gputx_read_results(gputx_db* db, uint8_t* status, void* out, uint64
     const void* dout = nullptr;
     uint64_t n = 0;
     TRY(gputx_results_device(db, &ds, &dout, &n));
-    const uint64_t need = n * db->out_stride;
+    const uint64_t need = db->nshards > 1 || !db->packed ? n * db->out_stride : db->out_bytes;
     if (out && out_bytes < need) return fail(db, GPUTX_ECAPACITY, "output buffer too small");
     if (status && n) CK(cudaMemcpyAsync(status, ds, n, cudaMemcpyDeviceToHost, db->stream));
     if (out && n) CK(cudaMemcpyAsync(out, dout, need, cudaMemcpyDeviceToHost, db->stream));
     CK(cudaStreamSynchronize(db->stream));
+    return GPUTX_OK;
+}
+
+gputx_status gputx_read_out_offsets(gputx_db* db, uint32_t* host, uint64_t n, uint64_t* bytes) {
+    if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
+    if (!db) return GPUTX_EINVAL;
+    if (!db->packed) return fail(db, GPUTX_EINVAL, "fixed-stride outputs (no GPUTX_FLAG_PACKED_OUT)");
+    if (!db->submitted && !db->executed) return fail(db, GPUTX_ESTATE, "no submitted bulk");
+    if (host && n != db->n + 1) return fail(db, GPUTX_EINVAL, "offsets are u32[n + 1]");
+    if (host) CK(cudaMemcpy(host, db->d_out_off, (db->n + 1) * 4, cudaMemcpyDeviceToHost));
+    if (bytes) *bytes = db->out_bytes;
     return GPUTX_OK;
 }
 
@@ -2326,6 +2352,7 @@ gputx_status gputx_pool_submit(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !b) return GPUTX_EINVAL;
     if (!db->sealed) return fail(db, GPUTX_ESTATE, "pool submit before seal");
+    if (db->packed) return fail(db, GPUTX_EINVAL, "the transaction pool returns fixed-stride outputs");
     if (db->submitted) return fail(db, GPUTX_ESTATE, "a bulk is submitted; execute it first");
     if (db->poisoned) return fail(db, GPUTX_ESTATE, "database poisoned by a deadlock; reset first");
     if (db->nshards > 1) return fail(db, GPUTX_ESTATE, "the pool is single-GPU (unsharded handles)");
@@ -2537,7 +2564,7 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
         pmark(db->st_d2h);
         if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->d_status, n, cudaMemcpyDeviceToHost, db->st_d2h));
         if (n && out && out[i])
-            CK(cudaMemcpyAsync(out[i], db->d_out, n * db->out_stride, cudaMemcpyDeviceToHost, db->st_d2h));
+            CK(cudaMemcpyAsync(out[i], db->d_out, db->out_bytes, cudaMemcpyDeviceToHost, db->st_d2h));
         CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
         pmark(db->st_d2h);
         // the next bulk gets the other slot's result buffers (swap below) -- these stay put
@@ -2639,7 +2666,8 @@ void gputx_close_db(gputx_db* db) {
     dfree(db, db->d_order);
     dfree(db, db->tm1_sub); dfree(db, db->tm1_ai); dfree(db, db->tm1_sf); dfree(db, db->tm1_cf);
     dfree(db, db->d_undo);
-    dfree(db, db->d_oseg); dfree(db, db->d_prog); dfree(db, db->d_own); dfree(db, db->d_wait); dfree(db, db->d_pub); dfree(db, db->d_owait);
+    dfree(db, db->d_out_off);
+    dfree(db, db->d_oseg); dfree(db, db->d_prog); dfree(db, db->d_oout); dfree(db, db->d_own); dfree(db, db->d_wait); dfree(db, db->d_pub); dfree(db, db->d_owait);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
                   db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,
                   db->d_rstatus, db->d_rout};

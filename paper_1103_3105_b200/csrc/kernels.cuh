@@ -19,7 +19,7 @@ enum {
     SC_ERR = 0, SC_BADIDX, SC_NREC, SC_NFRAG, SC_MAXD, SC_ZERO, SC_PASSES, SC_CHG0, SC_CHG1, SC_CHG2,
     SC_KNEXT, SC_TICKET, SC_DEADLOCK, SC_MAXCHAIN, SC_NKEYS, SC_NKEYS1, SC_COMMITTED, SC_NOCONV, SC_XTOTAL,
     SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
-    SC_COUNT = 40      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS; 33: SC_NOCLUSTER)
+    SC_COUNT = 48      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS; 33: SC_NOCLUSTER; ... 40: SC_OUTBYTES)
 };
 enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7, E_WORDS = 8 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
@@ -28,6 +28,7 @@ constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested clust
 constexpr int SC_ERRPK = 34;      // [34, 36): u64 (first bad idx << 8 | its code); all-ones = none
 constexpr int SC_SPARSE = 36;     // TPC-B ingest: transactions without a history row (withdrawals, peers')
 constexpr int SC_P2P = 37;        // [37, 39): peer exchange: records received, overflow bits
+constexpr int SC_OUTBYTES = 40;   // GPUTX_FLAG_PACKED_OUT: bytes of the bulk's packed output records
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(256) copy_pw_kernel(const uint32_t* __restrict
 template <int S>
 __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uint32_t n_words, const uint32_t* nw_ptr,
                                                      uint32_t type_mask, uint32_t* ins_cnt, uint32_t ins_stride,
-                                                     uint32_t* sc, uint8_t* xflag) {
+                                                     uint32_t* sc, uint8_t* xflag, uint32_t* out_size) {
     const uint32_t n = db.n;
     if (nw_ptr) n_words = min(__ldg(nw_ptr), n_words);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                 if (p[4] != 2 && home) ins_cnt[T_HIST * ins_stride + i] = 1;
             }
         }
+        if (out_size) out_size[i] = out_bytes<S>(t, p);            // packed outputs (scanned at submit)
         if (S == S_TPCB) {                                           // history rows (deposits) via ins_off
             ins_cnt[i] = (home && t == 0) ? 1u : 0u;
             if (!(home && t == 0)) atomicAdd(&sc[SC_SPARSE], 1u);       // some row is not at its idx
@@ -1765,7 +1767,8 @@ __global__ void __launch_bounds__(256) own_gather_kernel(DevDb db, const uint64_
                                                          const unsigned long long* __restrict__ wait,
                                                          const uint8_t* __restrict__ pub, uint32_t* oidx,
                                                          uint8_t* otype, uint32_t* opp, uint32_t* odep,
-                                                         unsigned long long* owait, uint32_t* oseg, uint32_t* prog) {
+                                                         unsigned long long* owait, uint32_t* oseg, uint32_t* prog,
+                                                         uint32_t* oout) {
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < n; pos += gridDim.x * blockDim.x) {
         const uint64_t sk = skeys[pos];
         const uint32_t o = (uint32_t)(sk >> 32), idx = perm[(uint32_t)sk];
@@ -1774,6 +1777,7 @@ __global__ void __launch_bounds__(256) own_gather_kernel(DevDb db, const uint64_
         otype[pos] = db.type[idx];
         odep[pos] = d | (pub && pub[idx] ? OWN_PUB : 0u);
         if (wait) owait[pos] = wait[idx];
+        if (oout) oout[pos] = db.out_off[idx];          // packed output offset, staged
         if (PW > 0) {
             const uint32_t* src = db.pw + db.poff[idx];
 #pragma unroll
@@ -1805,6 +1809,7 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
                                                             const uint32_t* __restrict__ opp,
                                                             const uint32_t* __restrict__ odep,
                                                             const unsigned long long* __restrict__ owait,
+                                                            const uint32_t* __restrict__ oout,
                                                             uint32_t* prog, uint32_t* sc, uint32_t diag) {
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     constexpr int NP = PW > 0 ? PW : 1;
@@ -1816,12 +1821,13 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
     const bool gmode = DEP && __ldcg(&sc[SC_OWNGLOBAL]) != 0u;
     struct E {
         uint32_t idx, t, d;              // d: depth | OWN_PUB; INF past the segment
+        uint32_t oo;                     // packed output offset (OUT_AUTO: fixed stride)
         unsigned long long wt;
         uint32_t q[NP];
     };
     auto load = [&](uint32_t base, E& e) {
         const uint32_t j = base + lane;
-        e.idx = OWN_INF; e.t = 0; e.d = OWN_INF; e.wt = 0;
+        e.idx = OWN_INF; e.t = 0; e.d = OWN_INF; e.wt = 0; e.oo = OUT_AUTO;
 #pragma unroll
         for (int x = 0; x < NP; ++x) e.q[x] = 0;
         if (j < hi) {
@@ -1836,6 +1842,7 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
                 }
             }
             if (DEP) e.wt = __ldg(&owait[j]);
+            if (oout) e.oo = __ldg(&oout[j]);
         }
     };
     // entry (cursor + lane) of the window A|B, by shuffles (every lane takes part)
@@ -1846,6 +1853,7 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
         u = __shfl_sync(FULL, a.idx, sl); v = __shfl_sync(FULL, b.idx, sl); x.idx = fa ? u : v;
         u = __shfl_sync(FULL, a.t, sl);   v = __shfl_sync(FULL, b.t, sl);   x.t = fa ? u : v;
         u = __shfl_sync(FULL, a.d, sl);   v = __shfl_sync(FULL, b.d, sl);   x.d = fa ? u : v;
+        u = __shfl_sync(FULL, a.oo, sl);  v = __shfl_sync(FULL, b.oo, sl);  x.oo = fa ? u : v;
         if (DEP) {
             const unsigned long long ua = __shfl_sync(FULL, a.wt, sl), ub = __shfl_sync(FULL, b.wt, sl);
             x.wt = fa ? ua : ub;
@@ -1891,7 +1899,7 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
                 }
             }
             kx_jitter(diag, d0, w, lane);
-            exec_txn_p<S, false>(db, X.idx, X.t, X.q);
+            exec_txn_p<S, false>(db, X.idx, X.t, X.q, X.oo);
         }
         if (DEP) pubr |= __ballot_sync(FULL, lane < cnt && (X.d & OWN_PUB)) != 0u;
         p += cnt;

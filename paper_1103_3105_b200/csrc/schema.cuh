@@ -47,6 +47,7 @@ struct DevDb {
     uint8_t* status;
     uint8_t* out;
     uint32_t out_stride;
+    const uint32_t* out_off;           // GPUTX_FLAG_PACKED_OUT: record offsets (else nullptr: idx * stride)
     void* col[MAX_COLS];
     void* ins[MAX_INS];
     uint64_t ins_base[4];              // merged-table row count before this bulk
@@ -103,6 +104,23 @@ DEV uint32_t shard_of(const DevDb& db, uint64_t root) { return (uint32_t)(root *
 template <class T> DEV T ldm(const T* p) { return *p; }
 template <class T> DEV void stm(T* p, T v) { *p = v; }
 DEV void put32(uint8_t* o, uint32_t v) { *reinterpret_cast<uint32_t*>(o) = v; }
+// GPUTX_FLAG_PACKED_OUT record size of a transaction (include/gputx.h): the bytes its
+// procedure can write, rounded to the record's alignment
+template <int S>
+DEV uint32_t out_bytes(uint32_t t, const uint32_t* p) {
+    if (S == S_TPCB) return 8;
+    if (S == S_MICRO) return 4;
+    if (S == S_TM1) return t == 0 ? 40u : t == 1 ? 32u : t == 2 ? 16u : 0u;
+    return t == 0 ? (16u + 12u * p[3] + 7u) & ~7u : 16u;
+}
+// transaction idx's output record: fixed stride, or packed at its submit-time offset --
+// `oo` when the caller staged it (OUT_AUTO: loaded here, a dependent load before the store)
+constexpr uint32_t OUT_AUTO = 0xFFFFFFFFu;
+template <uint32_t STRIDE>
+DEV uint8_t* out_rec(const DevDb& db, uint32_t idx, uint32_t oo = OUT_AUTO) {
+    if (oo != OUT_AUTO) return db.out + oo;
+    return db.out + (db.out_off ? (uint64_t)__ldg(&db.out_off[idx]) : (uint64_t)idx * STRIDE);
+}
 DEV void put64(uint8_t* o, uint64_t v) {
     reinterpret_cast<uint32_t*>(o)[0] = (uint32_t)v;
     reinterpret_cast<uint32_t*>(o)[1] = (uint32_t)(v >> 32);
@@ -250,11 +268,11 @@ DEV void tpcb_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh) {
     INS(int32_t, IB_DELTA)[r] = delta;
     INS(uint32_t, IB_TS)[r] = txn_ts(db, idx, sh);
 }
-DEV void tpcb_account(const DevDb& db, uint32_t idx, const uint32_t* p) {
+DEV void tpcb_account(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_t oo = OUT_AUTO) {
     int64_t* acc = COL(int64_t, B_ACC);
     const int64_t v = ldm(&acc[p[0]]) + (int32_t)p[3];
     stm(&acc[p[0]], v);
-    reinterpret_cast<int64_t*>(db.out)[idx] = v;
+    *reinterpret_cast<int64_t*>(out_rec<8>(db, idx, oo)) = v;
 }
 
 // WITHDRAW (TPC-B type 1): NON-two-phase on purpose --
@@ -270,7 +288,7 @@ DEV void undo_apply(const DevDb& db, const UndoRec* log, int nl) {
         else red_add(&c[log[j].row], log[j].val);
     }
 }
-DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p) {
+DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_t oo = OUT_AUTO) {
     UndoRec* log = db.undo + (uint64_t)idx * UNDO_SLOTS;
     const int64_t amt = (int32_t)p[3];
     int64_t* acc = COL(int64_t, B_ACC);
@@ -285,10 +303,10 @@ DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p) {
     if (a1 < 0) {
         undo_apply(db, log, UNDO_SLOTS);
         db.status[idx] = 1;
-        reinterpret_cast<int64_t*>(db.out)[idx] = 0;   // (TPC-B output records are not pre-zeroed)
+        *reinterpret_cast<int64_t*>(out_rec<8>(db, idx, oo)) = 0;   // (TPC-B output records are not pre-zeroed)
         return;
     }
-    reinterpret_cast<int64_t*>(db.out)[idx] = a1;
+    *reinterpret_cast<int64_t*>(out_rec<8>(db, idx, oo)) = a1;
 }
 
 // ---- TM-1 --------------------------------------------------------------------------
@@ -305,8 +323,8 @@ DEV void tpcb_withdraw(const DevDb& db, uint32_t idx, const uint32_t* p) {
 //   CF  (64 B per (s, sf)) [0..3) live, [4..7) end_time, [16 + 8k] numberx of start 8k
 constexpr uint32_t TM1_SUBROW = 64, TM1_AIROW = 16, TM1_SFROW = 16, TM1_CFROW = 64;
 
-DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
-    uint8_t* o = db.out + (uint64_t)idx * 40;
+DEV void tm1_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, uint32_t oo = OUT_AUTO) {
+    uint8_t* o = out_rec<40>(db, idx, oo);
     switch (t) {
     case 0: {   // GET_SUBSCRIBER_DATA: the row's first 36 bytes are the output record
         const uint32_t s = p[0] - 1;
@@ -417,7 +435,7 @@ __device__ __noinline__ float micro_body(float v, uint32_t calls) {
     return v;
 }
 
-DEV void micro_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+DEV void micro_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, uint32_t oo = OUT_AUTO) {
     uint32_t* tup = COL(uint32_t, U_TUPLE);
     const uint32_t calls = 100u * db.dims[2];
     float v = __uint_as_float(ldm(&tup[p[0]]));
@@ -433,7 +451,7 @@ DEV void micro_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p)
     }
     const uint32_t bits = __float_as_uint(v);
     stm(&tup[p[0]], bits);
-    put32(db.out + (uint64_t)idx * 4, bits);
+    put32(out_rec<4>(db, idx, oo), bits);
 }
 
 // ---- TPC-C -------------------------------------------------------------------------
@@ -463,7 +481,7 @@ DEV void tpcc_no_stock(const DevDb& db, uint32_t idx, const uint32_t* p, uint32_
             q0[l] = ldm(&sq[sidx[l]]);
         }
     }
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     int32_t cur[15];
 #pragma unroll
     for (int l = 0; l < 15; ++l) {
@@ -520,7 +538,7 @@ DEV void tpcc_no_home(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh)
     const uint64_t rn = db.ins_base[T_NEWORDER] + db.ins_off[T_NEWORDER * (uint64_t)db.ins_stride + idx];
     INS(uint32_t, IN_OID)[rn] = oid; INS(uint32_t, IN_D)[rn] = d; INS(uint32_t, IN_W)[rn] = w;
     const uint64_t rl0 = db.ins_base[T_OLINE] + db.ins_off[T_OLINE * (uint64_t)db.ins_stride + idx];
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     int64_t sum = 0;
 #pragma unroll
     for (int l = 0; l < 15; ++l) {
@@ -559,7 +577,7 @@ DEV void tpcc_pay_customer(const DevDb& db, uint32_t idx, const uint32_t* p) {
     stm(&bal[cx], nb);
     red_add(&COL(int64_t, C_C_YTD)[cx], (int64_t)h);
     red_add(&COL(uint32_t, C_C_CNT)[cx], 1u);
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     put32(o, p[5]);
     put32(o + 4, credit);
     put64(o + 8, (uint64_t)nb);
@@ -620,7 +638,7 @@ DEV void tpcc_txn(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, 
     }
     // ---- decide, then write
     if (abort) { db.status[idx] = 1; return; }
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     if (no) {
         stm(&COL(uint32_t, C_D_NEXT)[wd], oid + 1);
         uint32_t all_local = 1;
@@ -690,7 +708,7 @@ DEV bool tpcc_payment(const DevDb& db, uint32_t idx, const uint32_t* p, bool sh,
     const uint32_t D = db.dims[1], C = db.dims[2];
     const uint32_t w = p[0], d = p[1];
     const uint64_t wd = (uint64_t)w * D + d;
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     if (p[4] == 2) { db.status[idx] = 1; return false; }
     const uint64_t cx = ((uint64_t)p[2] * D + p[3]) * C + p[5];
     const int64_t cbal = ldm(&COL(int64_t, C_C_BAL)[cx]);
@@ -718,7 +736,7 @@ DEV void tpcc_txn_warp(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t
     const uint32_t D = db.dims[1], C = db.dims[2], I = db.dims[3];
     const uint32_t w = p[0], d = p[1];
     const uint64_t wd = (uint64_t)w * D + d;
-    uint8_t* o = db.out + (uint64_t)idx * 200;
+    uint8_t* o = out_rec<200>(db, idx);
     if (t != 0) {                                 // Payment: small, lane 0
         if (lane == 0) tpcc_payment(db, idx, p, sh, true);
         return;
@@ -825,16 +843,16 @@ DEV void warm_rows(const DevDb& db, uint32_t t, const uint32_t* p) {
 }
 
 template <int S, bool SH = false>
-DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p) {
+DEV void exec_txn_p(const DevDb& db, uint32_t idx, uint32_t t, const uint32_t* p, uint32_t oo = OUT_AUTO) {
     if (SH && db.xflag && db.xflag[idx]) { exec_local<S>(db, idx); return; }
     if (S == S_TPCB) {
-        if (t == 1) { tpcb_withdraw(db, idx, p); return; }
+        if (t == 1) { tpcb_withdraw(db, idx, p, oo); return; }
         tpcb_home(db, idx, p, SH);
-        tpcb_account(db, idx, p);
+        tpcb_account(db, idx, p, oo);
     } else if (S == S_TM1) {
-        tm1_txn(db, idx, t, p);
+        tm1_txn(db, idx, t, p, oo);
     } else if (S == S_MICRO) {
-        micro_txn(db, idx, t, p);
+        micro_txn(db, idx, t, p, oo);
     } else {
         tpcc_txn(db, idx, t, p, SH);
     }

@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_
                 6: "ECAPACITY", 7: "ECROSS", 8: "EDEADLOCK", 9: "ECUDA", 10: "ENCCL"}
 OUT_STRIDE = {1: 8, 2: 40, 3: 200, 4: 4}
 FLAG_ADD_RULE = 1            # include/gputx.h GPUTX_FLAG_ADD_RULE
+FLAG_PACKED_OUT = 2          # include/gputx.h GPUTX_FLAG_PACKED_OUT
 
 
 class GputxError(RuntimeError):
@@ -70,7 +71,8 @@ class Stats(ctypes.Structure):
                [(k, ctypes.c_double) for k in ("ms_emit", "ms_sort", "ms_rank", "ms_group", "ms_exec", "ms_merge",
                                                "ms_total")] + \
                [(k, ctypes.c_uint64) for k in ("cross", "strategy")] + \
-               [(k, ctypes.c_double) for k in ("ms_ingest", "ms_exchange")] + [("flags", ctypes.c_uint64)]
+               [(k, ctypes.c_double) for k in ("ms_ingest", "ms_exchange")] + [("flags", ctypes.c_uint64),
+                                                                                   ("out_bytes", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -121,6 +123,7 @@ def load_library():
         "gputx_execute_async": ([P, I], I),
         "gputx_wait": ([P, ctypes.POINTER(Stats)], I),
         "gputx_read_results": ([P, P, P, U64], I),
+        "gputx_read_out_offsets": ([P, P, U64, P], I),
         "gputx_results_device": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)], I),
         "gputx_out_stride": ([I], U32),
         "gputx_read_column": ([P, ctypes.c_char_p, P, U64], I),
@@ -160,7 +163,7 @@ EXPORTED = ["gputx_open_db", "gputx_load_column", "gputx_column_info", "gputx_se
             "gputx_pool_submit", "gputx_pool_step", "gputx_pool_read", "gputx_pool_pending",
             "gputx_read_serial_order", "gputx_snapshot", "gputx_run_bulks", "gputx_shard_export",
             "gputx_shard_connect", "gputx_shard_connect_local", "gputx_shard_dispatch", "gputx_shard_receive",
-            "gputx_shard_return", "gputx_shard_collect"]
+            "gputx_shard_return", "gputx_shard_collect", "gputx_read_out_offsets"]
 PEER_BLOB_BYTES = 128                    # include/gputx.h GPUTX_PEER_BLOB_BYTES
 
 INSERT_TABLES = {
@@ -175,6 +178,19 @@ INSERT_TABLES = {
 SIGNED_INSERT_COLS = {"h_delta", "ol_amount", "h_amount"}
 
 
+def unpack_outputs(buf: np.ndarray, off: np.ndarray, stride: int) -> np.ndarray:
+    """Packed output records (GPUTX_FLAG_PACKED_OUT) -> u8[n, stride] (zero-padded)."""
+    n = len(off) - 1
+    out = np.zeros((n, stride), np.uint8)
+    size = np.diff(off.astype(np.int64))
+    for s in np.unique(size):
+        if s == 0:
+            continue
+        rows = np.nonzero(size == s)[0]
+        out[rows, :s] = buf[off[rows].astype(np.int64)[:, None] + np.arange(s)]
+    return out
+
+
 def _ptr(a) -> int:
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
@@ -187,7 +203,7 @@ class Database:
 
     def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
                  device: int = 0, stream: int | None = None, insert_capacity: int = 0, shard: int = 0,
-                 nshards: int = 1, add_rule: bool = False, torch_memory: bool = False):
+                 nshards: int = 1, add_rule: bool = False, torch_memory: bool = False, packed_out: bool = False):
         self.lib = load_library()
         self.schema = schema
         cfg = Config()
@@ -199,7 +215,8 @@ class Database:
         cfg.part_size = int(part_size)
         cfg.device = int(device)
         cfg.stream = stream
-        cfg.flags = FLAG_ADD_RULE if add_rule else 0
+        cfg.flags = (FLAG_ADD_RULE if add_rule else 0) | (FLAG_PACKED_OUT if packed_out else 0)
+        self.packed = bool(packed_out)
         cfg.shard = int(shard)
         cfg.nshards = int(nshards)
         if torch_memory:                     # device memory from PyTorch's caching allocator
@@ -485,14 +502,28 @@ class Database:
     def execute_nostats(self, strategy: str = KSET):
         self._check(self.lib.gputx_execute(self.h, STRATEGIES[strategy], None), self.h)
 
-    def read_results(self, status: np.ndarray | None = None, out: np.ndarray | None = None):
+    def read_results(self, status: np.ndarray | None = None, out: np.ndarray | None = None, raw: bool = False):
+        """(status u8[n], outputs).  Outputs: u8[n, stride]; with packed_out the packed bytes
+        are read (gputx_read_results) and, unless raw, placed back at stride positions."""
         if status is None:
             status = np.zeros(self.n, np.uint8)
+        if self.packed:
+            off = self.read_out_offsets()
+            buf = np.zeros(max(int(off[-1]), 1), np.uint8)
+            self._check(self.lib.gputx_read_results(self.h, _ptr(status) if self.n else None,
+                                                    _ptr(buf) if self.n else None, buf.nbytes), self.h)
+            return status, (buf[:int(off[-1])] if raw else unpack_outputs(buf, off, self.stride))
         if out is None:
             out = np.zeros((self.n, self.stride), np.uint8)
         self._check(self.lib.gputx_read_results(self.h, _ptr(status) if self.n else None,
                                                 _ptr(out) if self.n else None, out.nbytes), self.h)
         return status, out
+
+    def read_out_offsets(self) -> np.ndarray:
+        """gputx_read_out_offsets: u32[n + 1] byte offsets of the packed output records."""
+        off = np.zeros(self.n + 1, np.uint32)
+        self._check(self.lib.gputx_read_out_offsets(self.h, _ptr(off), self.n + 1, None), self.h)
+        return off
 
     def results_device(self):
         s, o, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()

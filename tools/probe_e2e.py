@@ -11,7 +11,7 @@ from paper_1103_3105_b200 import Database  # noqa: E402
 
 wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "tm1"]
 dims, image, bulks = bench.make_inputs(wl, 0, 1, 3, 1)
-db = Database(wl["schema"], dims.dims, wl["n"], image, insert_capacity=60)
+db = Database(wl["schema"], dims.dims, wl["n"], image, insert_capacity=60, packed_out=True)
 
 
 def pin(a):

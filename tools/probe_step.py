@@ -17,7 +17,7 @@ tt = torch.from_numpy(bulk.type).to(dev)
 po = torch.from_numpy(bulk.param_off.view(np.int32)).to(dev)
 pw = torch.from_numpy(bulk.param_words.view(np.int32)).to(dev)
 strategy = sys.argv[1] if len(sys.argv) > 1 else "kset"
-db = Database(W.TM1, dims.dims, 1_000_000, image, insert_capacity=8)
+db = Database(W.TM1, dims.dims, 1_000_000, image, insert_capacity=8, packed_out=True)
 stream = torch.cuda.current_stream()
 rows = []
 for it in range(12):

@@ -8,6 +8,7 @@
 // Operators follow the convention  Op::combine(earlier, later)  so that a
 // prefix is  combine(combine(x0, x1), x2) ...  in array order.
 #pragma once
+#include <initializer_list>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -89,6 +90,51 @@ inline cudaError_t dev_fill(void* p, int value, size_t bytes, cudaStream_t s) {
     fill_bytes_kernel<<<(unsigned)blocks, 256, 0, s>>>((uint8_t*)p, (uint32_t)(value & 0xFF), (uint64_t)bytes);
     return cudaGetLastError();
 }
+
+// Several fills in ONE launch (blockIdx.y = segment): the per-bulk bookkeeping fills
+// (counters, depth array, sort workspace, result buffers) otherwise cost a launch each.
+// The segments are filled concurrently: they must not overlap.
+struct FillSeg {
+    uint8_t* p;
+    uint64_t bytes;
+    uint32_t v8;
+};
+constexpr int FILL_MAX = 4;
+struct FillList {
+    FillSeg s[FILL_MAX];
+};
+__global__ void __launch_bounds__(256) fill_multi_kernel(FillList fl) {
+    const FillSeg g = fl.s[blockIdx.y];
+    uint8_t* p = g.p;
+    const uint64_t bytes = g.bytes;
+    const uint64_t head = (16 - ((uintptr_t)p & 15)) & 15;
+    const uint64_t h = head < bytes ? head : bytes;
+    const uint64_t n16 = (bytes - h) / 16;
+    const uint32_t w = g.v8 * 0x01010101u;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+    if (tid < h) p[tid] = (uint8_t)g.v8;
+    uint4* q = reinterpret_cast<uint4*>(p + h);
+    for (uint64_t i = tid; i < n16; i += nt) q[i] = make_uint4(w, w, w, w);
+    for (uint64_t i = h + n16 * 16 + tid; i < bytes; i += nt) p[i] = (uint8_t)g.v8;
+}
+// fills (ptr, byte value, bytes) x k (k <= FILL_MAX; empty segments allowed)
+inline cudaError_t dev_fill_multi(cudaStream_t s, std::initializer_list<FillSeg> segs) {
+    FillList fl = {};
+    int k = 0;
+    uint64_t mx = 0;
+    for (const FillSeg& g : segs) {
+        if (!g.bytes) continue;
+        fl.s[k++] = {g.p, g.bytes, g.v8 & 0xFFu};
+        mx = g.bytes > mx ? g.bytes : mx;
+    }
+    if (!k) return cudaSuccess;
+    uint64_t blocks = (mx / 16 + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    fill_multi_kernel<<<dim3((unsigned)blocks, (unsigned)k), 256, 0, s>>>(fl);
+    return cudaGetLastError();
+}
+inline FillSeg fseg(void* p, int v, uint64_t bytes) { return FillSeg{(uint8_t*)p, bytes, (uint32_t)(v & 0xFF)}; }
 
 // ---------------------------------------------------------------------------------
 // Grid barrier for a cooperative launch (all CTAs co-resident).  gen is bumped by

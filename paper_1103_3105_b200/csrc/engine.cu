@@ -218,6 +218,7 @@ struct gputx_db {
     int kset_own = 1;
     bool kset_ran_own = false;
     int own_grid[2] = {0, 0};          // co-resident CTAs of the executor without / with waits
+    uint32_t own_g = 0, own_nw = 0;    // this bulk's executor grid and owner warps
     uint32_t* d_oseg = nullptr;        // owner segments [OWN_MAXW + 1] and the sort count word
     uint32_t* d_prog = nullptr;        // per-warp progress [OWN_MAXW]
     uint32_t* d_own = nullptr;         // per-transaction owner (dependency pass)
@@ -486,8 +487,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     STAGE("sort");
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
-    CK(dev_fill(db->d_D, 0, db->n * sizeof(uint32_t), s));
-    CK(dev_fill(&db->d_bar->dead, 0, sizeof(uint32_t), s));
+    CK(dev_fill_multi(s, {fseg(db->d_D, 0, db->n * sizeof(uint32_t)), fseg(&db->d_bar->dead, 0, sizeof(uint32_t))}));
     if (windowed) {
         win_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, wb,
                                                                              nwin, db->d_wseg);
@@ -580,10 +580,8 @@ bool kset_use_own(const gputx_db* db) {
 }
 
 template <int S>
-gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
-    cudaStream_t s = db->stream;
+gputx_status own_prepare(gputx_db* db) {
     const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
-    const uint32_t n = (uint32_t)db->n;
     if (!db->d_oseg) {
         gputx_status st;
         if ((st = dalloc(db, &db->d_oseg, OWN_MAXW + 2)) || (st = dalloc(db, &db->d_prog, OWN_MAXW))) return st;
@@ -604,24 +602,31 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     }
     uint32_t G = (uint32_t)gridv;
     if (db->exec_grid_override) G = std::min(G, db->exec_grid_override);
-    const uint32_t NW = G * 8;
+    db->own_g = G;
+    db->own_nw = G * 8;
+    return GPUTX_OK;
+}
+
+// (after group_kernel<1, 0, S> wrote the owner keys)
+template <int S>
+gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
+    const uint32_t n = (uint32_t)db->n;
+    const uint32_t G = db->own_g, NW = db->own_nw;
     const uint32_t g = grid_for(n, 256, (uint32_t)db->nsm * 8);
     uint64_t* kb = db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a;
     uint32_t diag = db->kset_diag;
-    own_key_kernel<S><<<g, 256, 0, s>>>(v, db->d_perm, n, NW, kb, dep ? db->d_own : nullptr, diag,
-                                        db->d_oseg + OWN_MAXW + 1);
-    ++db->launches;
     if (dep) {
-        CK(dev_fill(db->d_wait, 0, (uint64_t)n * 8, s));
-        CK(dev_fill(db->d_pub, 0, n, s));
-        CK(dev_fill(db->d_sc + SC_OWNGLOBAL, 0, 4, s));
+        CK(dev_fill_multi(s, {fseg(db->d_wait, 0, (uint64_t)n * 8), fseg(db->d_pub, 0, n),
+                              fseg(db->d_sc + SC_OWNGLOBAL, 0, 4)}));
         own_dep_kernel<<<grid_for(db->max_rec, 256, (uint32_t)db->nsm * 8), 256, 0, s>>>(
             db->d_sorted, db->d_sc + SC_NREC, db->d_own, db->d_D, db->d_wait, db->d_pub, db->d_sc, diag);
         ++db->launches;
     }
-    // stable sort on the owner bits: (owner, depth, type) order (count word set by own_key_kernel)
+    // stable sort on the owner bits: (owner, depth, type) order
     uint64_t* tmp = db->d_sorted == db->d_rec_a ? db->d_rec_a : db->d_rec_b;
-    uint64_t* sk = radix_sort_u64(kb, tmp, db->d_oseg + OWN_MAXW + 1, n, 32, bits_for(NW - 1), db->sort_ws, db->epoch, s);
+    uint64_t* sk = radix_sort_u64(kb, tmp, db->d_sc + SC_NTXN, n, 32, bits_for(NW - 1), db->sort_ws, db->epoch, s);
     db->launches += 2 + (bits_for(NW - 1) + 7) / 8;
     constexpr int PW = kset_pw<S>();
     own_gather_kernel<PW><<<g, 256, 0, s>>>(v, sk, n, NW, db->d_perm, db->d_D, dep ? db->d_wait : nullptr,
@@ -663,9 +668,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     NVTX_SCOPE("gputx.kset.group_exec");
     cudaStream_t s = db->stream;
     const uint32_t T = db->ntypes;
-    group_nkeys_kernel<<<1, 1, 0, s>>>(db->d_sc, T);
-    ++db->launches;
-    zero_dev_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc + SC_NKEYS1);
+    group_zero_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc, T);     // key count + zeroed counters
     ++db->launches;
     const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
     const uint32_t P = db->group_p ? std::min(db->group_p, T) : T;
@@ -676,10 +679,14 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     ++db->launches;
     const bool df = kset_use_dataflow<S>(db) && db->d_item_sorted;
     const bool own = !df && kset_use_own<S>(db) && db->n > 0;
-    if (own)        // the owner gather stages types / parameters itself
-        group_kernel<1, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
-                                              db->d_perm, nullptr, nullptr, nullptr, nullptr, P);
-    else
+    if (own) {      // + the owner keys; the owner gather stages types / parameters itself
+        TRY(own_prepare<S>(db));
+        const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
+        OwnKeys ok{db->own_nw, db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a, dep ? db->d_own : nullptr,
+                   db->kset_diag};
+        group_kernel<1, 0, S><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
+                                                 db->d_perm, db->d_poff, db->d_pw, nullptr, nullptr, P, ok);
+    } else
         group_kernel<1, kset_pw<S>()><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt,
                                                          db->d_goff, db->d_perm, db->d_poff, db->d_pw, db->d_ptype,
                                                          db->d_pp, P);
@@ -989,8 +996,8 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
     db->launches = 0;
     db->has_depth = db->has_perm = false;
     db->executed = false;
-    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
+                              fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
     const bool ins_scan = db->schema == S_TPCC || db->schema == S_TPCB || db->has_ts;
     const int ntab = db->schema == S_TPCC ? 4 : 1;
     if (n) {
@@ -1072,8 +1079,8 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     cudaStream_t s = db->stream;
     const uint32_t ntab = (uint32_t)db->ins.size();
     // 1. ingest the arrivals in the staging area (validation, split lookups, insert counts)
-    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
+                              fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
     if (ntab) CK(dev_fill(db->st_ins, 0, 4 * (m + 1) * ntab, s));
     DevDb v = make_devdb(db);
     v.n = (uint32_t)m;
@@ -1977,8 +1984,8 @@ gputx_status gputx_shard_dispatch(gputx_db* db, const gputx_bulk* b) {
         CK(cudaMemcpyAsync(db->s_poff, b->param_off, (n + 1) * 4, kind, s));
         if (n_words) CK(cudaMemcpyAsync(db->s_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
         CK(cudaMemcpyAsync(db->s_ts, b->ts, n * 4, kind, s));
-        CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
-        CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+        CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
+                              fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
         const uint32_t stride = gputx_shard_stride((gputx_schema)db->schema, 0);
         shard_validate_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(db->s_poff, (uint32_t)n, n_words, stride - 3,
                                                                         db->d_sc);
@@ -2073,8 +2080,8 @@ gputx_status gputx_shard_return_merge(gputx_db* db, const uint32_t* recv, uint64
     if (!db->executed) return fail(db, GPUTX_ESTATE, "no executed bulk");
     if (n_recv && !recv) return GPUTX_EINVAL;
     cudaStream_t s = db->stream;
-    CK(dev_fill(db->d_sc, 0, SC_COUNT * 4, s));
-    CK(dev_fill(db->d_sc + SC_ERRPK, 0xFF, 8, s));
+    CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
+                              fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
     if (n_recv) {
         ret_merge_kernel<<<grid_for(n_recv, 256, 148 * 8), 256, 0, s>>>(recv, (uint32_t)n_recv, db->out_stride / 4,
                                                                          db->d_ts, db->d_src, (uint32_t)db->n,
@@ -2111,11 +2118,10 @@ gputx_status execute_launch(gputx_db* db, gputx_strategy st) {
     const uint64_t n = db->n;
     gputx_status r = GPUTX_OK;
     if (n) {
-        zero_bytes_kernel<<<grid_for((n + 15) / 16, 256, 148 * 4), 256, 0, s>>>(db->d_status, n);
-        if (db->schema != S_TPCB && !(db->kset_diag & 4096u))
-            zero_bytes_kernel<<<grid_for(db->out_bytes / 16 + 1, 256, 148 * 8), 256, 0, s>>>(db->d_out,
-                                                                                         db->out_bytes);
-        db->launches += db->schema != S_TPCB ? 2 : 1;
+        // status and (unless TPC-B, whose procedures write every record) the output records, one launch
+        const bool zo = db->schema != S_TPCB && !(db->kset_diag & 4096u);
+        CK(dev_fill_multi(s, {fseg(db->d_status, 0, n), fseg(db->d_out, 0, zo ? db->out_bytes : 0)}));
+        ++db->launches;
         if (db->schema == S_TPCB) r = execute_schema<S_TPCB>(db, st);
         else if (db->schema == S_TM1) r = execute_schema<S_TM1>(db, st);
         else if (db->schema == S_MICRO) r = execute_schema<S_MICRO>(db, st);

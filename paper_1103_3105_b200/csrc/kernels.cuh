@@ -29,6 +29,7 @@ constexpr int SC_ERRPK = 34;      // [34, 36): u64 (first bad idx << 8 | its cod
 constexpr int SC_SPARSE = 36;     // TPC-B ingest: transactions without a history row (withdrawals, peers')
 constexpr int SC_P2P = 37;        // [37, 39): peer exchange: records received, overflow bits
 constexpr int SC_OUTBYTES = 40;   // GPUTX_FLAG_PACKED_OUT: bytes of the bulk's packed output records
+constexpr int SC_NTXN = 41;       // transactions in the submitted bulk (device copy of n, ingest)
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                                                      uint32_t type_mask, uint32_t* ins_cnt, uint32_t ins_stride,
                                                      uint32_t* sc, uint8_t* xflag, uint32_t* out_size) {
     const uint32_t n = db.n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_NTXN] = n;
     if (nw_ptr) n_words = min(__ldg(nw_ptr), n_words);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t t = db.type[i];
@@ -1227,6 +1229,13 @@ __global__ void group_nkeys_kernel(uint32_t* sc, uint32_t T) {
     sc[SC_NKEYS1] = (sc[SC_MAXD] + 1) * T + 1;
 }
 
+// group_nkeys_kernel + zero_dev_kernel in one launch: every thread derives the key count
+__global__ void __launch_bounds__(256) group_zero_kernel(uint32_t* cnt, uint32_t* sc, uint32_t T) {
+    const uint32_t nk = (__ldcg(&sc[SC_MAXD]) + 1) * T;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { sc[SC_NKEYS] = nk; sc[SC_NKEYS1] = nk + 1; }
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nk + 1; i += gridDim.x * blockDim.x) cnt[i] = 0;
+}
+
 __global__ void pull_sc_kernel(const uint32_t* __restrict__ sc, uint32_t* host_mapped, uint32_t n) {
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) host_mapped[i] = __ldcg(&sc[i]);
 }
@@ -1267,12 +1276,23 @@ DEV int gr_slot(uint32_t* skey, uint32_t key) {
 // mode 0: histogram into cnt[]; mode 1: scatter perm[] (cnt[] counts down) and, for
 // PW > 0, the type and the first PW parameter words of each transaction into execution
 // order (ptype[pos], pp[pos*PW..]) so the executor reads them coalesced.
-template <int MODE, int PW>
+// Owner keys (K-SET owner-local rounds): with OS = the schema, mode 1 also writes
+// okeys[pos] = owner(i) << 32 | pos (and own[i]) for the stable owner sort.
+struct OwnKeys {
+    uint32_t nw;
+    uint64_t* keys;
+    uint32_t* own;
+    uint32_t diag;
+};
+template <int S>
+DEV uint32_t own_of(const uint32_t* p, uint32_t nw, uint32_t idx, uint32_t diag);
+
+template <int MODE, int PW, int OS = 0>
 __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__ D, const uint8_t* __restrict__ type,
                                                     uint32_t n, uint32_t T, uint32_t* cnt, const uint32_t* off,
                                                     uint32_t* perm, const uint32_t* __restrict__ poff,
                                                     const uint32_t* __restrict__ pw, uint8_t* ptype, uint32_t* pp,
-                                                    uint32_t P) {
+                                                    uint32_t P, OwnKeys ok = {}) {
     __shared__ uint32_t skey[GR_SLOTS];
     __shared__ uint32_t scnt[GR_SLOTS];
     __shared__ uint32_t sbase[GR_SLOTS];
@@ -1318,6 +1338,11 @@ __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__
                 const uint32_t i = (uint32_t)(t0 + k * 256 + threadIdx.x);
                 const uint32_t pos = off[key[k]] + (slot[k] >= 0 ? sbase[slot[k]] + rank[k] : rank[k]);
                 perm[pos] = i;
+                if (OS) {
+                    const uint32_t o = own_of<OS>(pw + poff[i], ok.nw, i, ok.diag);
+                    ok.keys[pos] = ((uint64_t)o << 32) | pos;
+                    if (ok.own) ok.own[i] = o;
+                }
                 if (PW > 0) {
                     ptype[pos] = type[i];
                     const uint32_t* src = pw + poff[i];
@@ -1691,21 +1716,6 @@ DEV uint32_t own_of(const uint32_t* p, uint32_t nw, uint32_t idx, uint32_t diag)
     if (diag & 16384u) return (uint32_t)(nbr_hash(idx) % nw);      // tests: arbitrary owners
     if (S == S_TPCB) return p[2] % nw;                               // home branch
     return (uint32_t)(nbr_hash((uint64_t)p[0]) % nw);              // TM-1 subscriber, micro tuple
-}
-
-// keys[j] = owner(perm[j]) << 32 | j over the (depth, type)-ordered perm; a stable sort on
-// the owner bits then gives (owner, depth, type) order.  own[idx] = owner (dependency pass).
-template <int S>
-__global__ void __launch_bounds__(256) own_key_kernel(DevDb db, const uint32_t* __restrict__ perm, uint32_t n,
-                                                      uint32_t nw, uint64_t* keys, uint32_t* own, uint32_t diag,
-                                                      uint32_t* n_out) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;      // the owner sort's count word
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t idx = perm[j];
-        const uint32_t o = own_of<S>(db.pw + db.poff[idx], nw, idx, diag);
-        keys[j] = ((uint64_t)o << 32) | j;
-        if (own) own[idx] = o;
-    }
 }
 
 DEV void own_add_wait(unsigned long long* wait, uint32_t idx, uint32_t o, uint32_t need, uint32_t* sc) {

@@ -182,8 +182,7 @@ inline uint64_t* radix_sort_u64(uint64_t* a, uint64_t* b, const uint32_t* n_dev,
                                 uint32_t nbits, SortWs& ws, uint32_t& epoch, cudaStream_t s) {
     if (n_max == 0 || nbits == 0) return a;
     const uint32_t npass = (nbits + 7) / 8;
-    dev_fill(ws.hist, 0, sizeof(uint32_t) * RS_MAXPASS * 256, s);
-    dev_fill(ws.tickets, 0, sizeof(uint32_t) * 64, s);
+    dev_fill_multi(s, {fseg(ws.hist, 0, sizeof(uint32_t) * RS_MAXPASS * 256), fseg(ws.tickets, 0, sizeof(uint32_t) * 64)});
     rs_hist_kernel<<<RS_HIST_GRID, 256, 0, s>>>(a, n_dev, lo, nbits, ws.hist);
     rs_scan_kernel<<<npass, 256, 0, s>>>(ws.hist);
     const uint32_t tile = RS_THREADS * (ws.items ? ws.items : RS_ITEMS);

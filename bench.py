@@ -659,7 +659,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps, "pcie": pcie,
                 "method": ("gputx_run_bulks: H2D of bulk i+1 and D2H of bulk i-1 overlap bulk i (two copy "
                            "streams); back-to-back bulks, no L2 flush in between; packed output records "
-                           "(GPUTX_FLAG_PACKED_OUT)") if ws == 1 else
+                           "(GPUTX_FLAG_PACKED_OUT); TM-1 / micro K-SET pipelined (no host round trip "
+                           "between bulks)") if ws == 1 else
                           "per step: H2D, sharded step, D2H (serial)"},
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
         "phases_ms": phase,

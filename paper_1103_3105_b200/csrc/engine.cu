@@ -11,6 +11,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <emmintrin.h>
 
 #include <nvtx3/nvToolsExt.h>         // header-only NVTX ranges: phases visible to nsys / ncu --nvtx
 
@@ -148,6 +149,14 @@ struct gputx_db {
     bool kset_ran_df = false;
     bool ins_dense = false;
     uint32_t* h_sc_dev = nullptr;       // device alias of the mapped host counters
+    // pipelined gputx_run_bulks (no host round trip per bulk): per-bulk counter slots in
+    // mapped host memory, the failed-bulk guard and the run's poison word
+    bool pipe = false;
+    uint32_t* pull_target = nullptr;    // device alias where pull_sc writes (nullptr: h_sc_dev)
+    uint32_t* h_slots = nullptr;        // [slots_cap][SC_COUNT] mapped
+    uint32_t* h_slots_dev = nullptr;
+    uint64_t slots_cap = 0;
+    uint32_t* d_poison = nullptr;
     uint8_t *tm1_sub = nullptr, *tm1_ai = nullptr, *tm1_sf = nullptr, *tm1_cf = nullptr;   // TM-1 row groups
     bool rows_dirty = false;            // TM-1: rows hold newer mutable fields than the columns
     // gputx_run_bulks: copy streams and double-buffered device slots (lazily created)
@@ -279,7 +288,7 @@ gputx_status fail(gputx_db* db, gputx_status s, const std::string& m) {
 // device counters -> mapped host counters (kernel stores, no copy engine); read by the host
 // after it synchronises the stream
 gputx_status pull_sc(gputx_db* db, cudaStream_t s) {
-    pull_sc_kernel<<<1, 64, 0, s>>>(db->d_sc, db->h_sc_dev, SC_COUNT);
+    pull_sc_kernel<<<1, 64, 0, s>>>(db->d_sc, db->pull_target ? db->pull_target : db->h_sc_dev, SC_COUNT);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(db, GPUTX_ECUDA, std::string("pull_sc: ") + cudaGetErrorString(e));
     return GPUTX_OK;
@@ -384,6 +393,8 @@ DevDb make_devdb(gputx_db* db) {
     v.part_size = db->part_size;
     v.add_rule = (db->cfg.flags & GPUTX_FLAG_ADD_RULE) ? 1u : 0u;
     v.nshards = db->nshards;
+    v.err = db->pipe ? db->d_sc + SC_ERR : nullptr;
+    v.poison = db->pipe ? db->d_poison : nullptr;
     v.shard = db->shard;
     v.nroot = db->nroot;
     v.root_lo = db->root_lo;
@@ -683,7 +694,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
         TRY(own_prepare<S>(db));
         const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
         OwnKeys ok{db->own_nw, db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a, dep ? db->d_own : nullptr,
-                   db->kset_diag};
+                   db->kset_diag, db->pipe ? db->d_sc + SC_ERR : nullptr};
         group_kernel<1, 0, S><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
                                                  db->d_perm, db->d_poff, db->d_pw, nullptr, nullptr, P, ok);
     } else
@@ -2499,6 +2510,174 @@ gputx_status pipe_alloc(gputx_db* db) {
     return GPUTX_OK;
 }
 
+// bytes of a host bulk's output records (GPUTX_FLAG_PACKED_OUT sizes, include/gputx.h)
+// for the schemas without parameter-dependent sizes
+uint64_t host_out_bytes(const gputx_db* db, const uint8_t* type, uint64_t n) {
+    if (!db->packed) return n * db->out_stride;
+    if (db->schema == S_MICRO) return 4 * n;
+    if (db->schema == S_TPCB) return 8 * n;
+    // TM-1: GSD 40, GND 32, GAD 16, the rest 0 -- the type bytes counted 16 at a time (SSE2
+    // compare + movemask + popcount: the host enqueues the next bulk while this one runs)
+    uint64_t c0 = 0, c1 = 0, c2 = 0, i = 0;
+    const __m128i z0 = _mm_setzero_si128(), z1 = _mm_set1_epi8(1), z2 = _mm_set1_epi8(2);
+    for (; i + 16 <= n; i += 16) {
+        const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(type + i));
+        c0 += __builtin_popcount(_mm_movemask_epi8(_mm_cmpeq_epi8(v, z0)));
+        c1 += __builtin_popcount(_mm_movemask_epi8(_mm_cmpeq_epi8(v, z1)));
+        c2 += __builtin_popcount(_mm_movemask_epi8(_mm_cmpeq_epi8(v, z2)));
+    }
+    for (; i < n; ++i) { c0 += type[i] == 0; c1 += type[i] == 1; c2 += type[i] == 2; }
+    return 40 * c0 + 32 * c1 + 16 * c2;
+}
+
+// Pipelined gputx_run_bulks (TM-1 / micro, K-SET with owner-local rounds): every bulk's
+// submit and execute are enqueued without a host round trip.  Ingest errors cannot be
+// returned before the execute is enqueued, so the kernels that read parameters treat a
+// bulk whose ingest flagged an error as empty (DevDb.err) and the run's poison word makes
+// every later bulk fail at ingest; the counters of bulk i land in mapped host slot i and
+// are checked after the one synchronisation at the end (the first failing bulk's error is
+// returned, as in the synchronous loop).  Per-bulk stats carry counts, not phase times.
+gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, uint8_t* const* status,
+                            void* const* out, gputx_stats* stats) {
+    cudaStream_t s = db->stream;
+    if (db->slots_cap < k) {
+        if (db->h_slots) cudaFreeHost(db->h_slots);
+        db->h_slots = nullptr;
+        db->slots_cap = 0;
+        const uint64_t cap = std::max<uint64_t>(k, 64);
+        if (cudaHostAlloc((void**)&db->h_slots, cap * SC_COUNT * 4, cudaHostAllocMapped | cudaHostAllocPortable) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer((void**)&db->h_slots_dev, db->h_slots, 0) != cudaSuccess)
+            return fail(db, GPUTX_ENOMEM, "run_bulks counter slots");
+        db->slots_cap = cap;
+    }
+    if (!db->d_poison) TRY(dalloc(db, &db->d_poison, 1));
+    CK(dev_fill(db->d_poison, 0, 4, s));
+    std::vector<uint64_t> nb(k), ob(k);
+    auto h2d = [&](uint64_t i) -> gputx_status {
+        const gputx_bulk& b = bulks[i];
+        const int sl = (int)(i & 1);
+        CK(cudaStreamWaitEvent(db->st_h2d, db->ev_in_free[sl], 0));
+        if (b.n) {
+            CK(cudaMemcpyAsync(db->in_type[sl], b.type, b.n, cudaMemcpyHostToDevice, db->st_h2d));
+            CK(cudaMemcpyAsync(db->in_poff[sl], b.param_off, (b.n + 1) * 4, cudaMemcpyHostToDevice, db->st_h2d));
+            const uint64_t w = b.param_off[b.n];
+            if (w) CK(cudaMemcpyAsync(db->in_pw[sl], b.param_words, w * 4, cudaMemcpyHostToDevice, db->st_h2d));
+        }
+        CK(cudaEventRecord(db->ev_in[sl], db->st_h2d));
+        return GPUTX_OK;
+    };
+    gputx_status hst = GPUTX_OK;               // a host-detected error stops enqueueing
+    uint64_t done = 0;
+    int last = 0;
+    db->pipe = true;
+    if (k) hst = h2d(0);
+    for (uint64_t i = 0; i < k && hst == GPUTX_OK; ++i) {
+        const int sl = (int)(i & 1);
+        last = sl;
+        if (i + 1 < k && (hst = h2d(i + 1)) != GPUTX_OK) break;
+        if ((hst = submit_check(db, &bulks[i])) != GPUTX_OK) break;
+        CK(cudaStreamWaitEvent(s, db->ev_in[sl], 0));
+        CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
+        std::swap(db->d_type, db->in_type[sl]);
+        std::swap(db->d_poff, db->in_poff[sl]);
+        std::swap(db->d_pw, db->in_pw[sl]);
+        std::swap(db->d_status, db->res_status[sl]);
+        std::swap(db->d_out, db->res_out[sl]);
+        CK(cudaEventRecord(db->ev_in_free[sl], s));
+        const uint64_t n = bulks[i].n;
+        const uint32_t words = n ? bulks[i].param_off[n] : 0;
+        // submit without the round trip (finish_submit's device half)
+        db->has_ts = false;
+        db->first_ts = db->next_ts;
+        db->n = n;
+        db->launches = 0;
+        db->has_depth = db->has_perm = false;
+        db->executed = false;
+        CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
+                              fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
+        if (n) {
+            if (db->schema == S_TM1) launch_ingest<S_TM1>(db, words, nullptr);
+            else launch_ingest<S_MICRO>(db, words, nullptr);
+            if (db->packed) scan_u32(db, db->d_out_off, db->d_out_off, nullptr, n, db->d_sc + SC_OUTBYTES);
+        }
+        db->ins_dense = false;
+        db->out_bytes = host_out_bytes(db, bulks[i].type, n);
+        db->submitted = true;
+        db->next_ts += n;
+        db->pull_target = db->h_slots_dev + i * SC_COUNT;
+        hst = execute_launch(db, GPUTX_KSET);
+        db->exec_pending = false;
+        db->pull_target = nullptr;
+        if (hst != GPUTX_OK) break;
+        nb[i] = n;
+        ob[i] = db->out_bytes;
+        done = i + 1;
+        CK(cudaEventRecord(db->ev_res[sl], s));
+        CK(cudaStreamWaitEvent(db->st_d2h, db->ev_res[sl], 0));
+        if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->d_status, n, cudaMemcpyDeviceToHost, db->st_d2h));
+        if (n && out && out[i] && db->out_bytes)
+            CK(cudaMemcpyAsync(out[i], db->d_out, db->out_bytes, cudaMemcpyDeviceToHost, db->st_d2h));
+        CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
+        std::swap(db->d_status, db->res_status[sl]);
+        std::swap(db->d_out, db->res_out[sl]);
+    }
+    db->pipe = false;
+    db->pull_target = nullptr;
+    for (int sl = 0; sl < 2; ++sl) CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (done) {                                // gputx_read_results: the last bulk's results
+        std::swap(db->d_status, db->res_status[last]);
+        std::swap(db->d_out, db->res_out[last]);
+    }
+    if (done && db->schema == S_TM1) db->rows_dirty = true;   // (the row groups changed)
+    // the bulks' counters, in order: the first failing bulk stops the run
+    for (uint64_t i = 0; i < done; ++i) {
+        const uint32_t* h = db->h_slots + i * SC_COUNT;
+        db->rank_epoch += h[SC_PASSES] + 1;
+        if (h[SC_ERR]) {
+            static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
+                                         "parameter out of range", "bad param_off", "timestamps not increasing",
+                                         "home partition not owned by this shard", "too many parameter words",
+                                         "an earlier bulk of the run failed"};
+            const uint64_t pk = (uint64_t)h[SC_ERRPK] | ((uint64_t)h[SC_ERRPK + 1] << 32);
+            const uint32_t e = (uint32_t)(pk & 0xFF), bad = (uint32_t)(pk >> 8);
+            db->n = 0;
+            db->submitted = false;
+            db->executed = false;
+            return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
+                        "bulk " + std::to_string(i) + ", transaction " + std::to_string(bad) + ": " +
+                            what[e <= 9 ? e : 0]);
+        }
+        if (h[SC_DEADLOCK]) {
+            db->poisoned = true;
+            return fail(db, GPUTX_EDEADLOCK, "spin watchdog tripped (bulk " + std::to_string(i) + ")");
+        }
+        if (stats) {
+            gputx_stats& st = stats[i];
+            memset(&st, 0, sizeof(st));
+            st.n = nb[i];
+            st.strategy = GPUTX_KSET;
+            st.records = h[SC_NREC];
+            st.depth = h[SC_MAXD];
+            st.ksets = (uint64_t)h[SC_MAXD] + 1;
+            st.zero_set = h[SC_ZERO];
+            st.rank_passes = h[SC_PASSES];
+            st.aborted = nb[i] ? h[SC_COMMITTED] : 0;
+            st.committed = nb[i] - st.aborted;
+            st.out_bytes = ob[i];
+            st.flags = GPUTX_STAT_KSET_OWNER | GPUTX_STAT_PIPELINED;
+        }
+    }
+    if (done) {
+        db->executed = true;
+        db->last_strategy = (int)GPUTX_KSET;
+        if (db->schema == S_TM1) db->rows_dirty = true;
+    }
+    return hst;
+}
+
 gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, gputx_strategy st,
                              uint8_t* const* status, void* const* out, gputx_stats* stats) {
     if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
@@ -2512,6 +2691,12 @@ gputx_status gputx_run_bulks(gputx_db* db, const gputx_bulk* bulks, uint64_t k, 
             return fail(db, GPUTX_ECAPACITY, "too many parameter words");
     }
     TRY(pipe_alloc(db));
+    // the pipelined loop: TM-1 / micro K-SET (owner-local rounds; no inserts, no host-side
+    // decisions between ingest and execute); GPUTX_PIPE=0 keeps the synchronous loop
+    static const bool pipe_env = !getenv("GPUTX_PIPE") || atoi(getenv("GPUTX_PIPE")) != 0;
+    if (pipe_env && st == GPUTX_KSET && k &&
+        ((db->schema == S_TM1 && kset_use_own<S_TM1>(db)) || (db->schema == S_MICRO && kset_use_own<S_MICRO>(db))))
+        return run_bulks_pipe(db, bulks, k, status, out, stats);
     cudaStream_t s = db->stream;
     // No device-to-device copies on the way (they would queue behind the other copy stream's
     // transfer on the copy engines): each slot's input buffers are SWAPPED in as the engine's
@@ -2679,6 +2864,8 @@ void gputx_close_db(gputx_db* db) {
                   db->d_rstatus, db->d_rout};
     for (void* p : pp) dfree(db, p);          // (pool staging s_* is in ps above)
     if (db->h_sc) cudaFreeHost(db->h_sc);
+    if (db->h_slots) cudaFreeHost(db->h_slots);
+    dfree(db, db->d_poison);
     for (auto& e : db->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : db->ev_sub)

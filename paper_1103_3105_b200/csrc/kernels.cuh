@@ -21,7 +21,7 @@ enum {
     SC_RRSPLIT,       // 19: root-local rank fell back to the grid scan (a root too large for one warp)
     SC_COUNT = 48      // (slots 20-31: SC_INS0, SC_DEST0; 32: SC_CROSS; 33: SC_NOCLUSTER; ... 40: SC_OUTBYTES)
 };
-enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7, E_WORDS = 8 };
+enum { E_TYPE = 1, E_UNREG = 2, E_LEN = 3, E_RANGE = 4, E_OFF = 5, E_TS = 6, E_OWNER = 7, E_WORDS = 8, E_POISON = 9 };
 constexpr int SC_INS0 = 20;       // [20, 24): insert rows per table (ingest)
 constexpr int SC_CROSS = 32;      // c: transactions with fragments in > 1 PART partition
 constexpr int SC_NOCLUSTER = 33;  // K-SET: launched without the requested cluster shape (counter hand-offs used)
@@ -67,6 +67,10 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
                                                      uint32_t* sc, uint8_t* xflag, uint32_t* out_size) {
     const uint32_t n = db.n;
     if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_NTXN] = n;
+    if (db.poison && __ldcg(db.poison)) {             // an earlier bulk of this run failed
+        if (blockIdx.x == 0 && threadIdx.x == 0) report_err(sc, E_POISON, 0);
+        return;
+    }
     if (nw_ptr) n_words = min(__ldg(nw_ptr), n_words);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t t = db.type[i];
@@ -215,14 +219,17 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* in, ui
 // =====================================================================================
 template <int S>
 __global__ void __launch_bounds__(256) emit_count_kernel(DevDb db, uint32_t* cnt) {
+    const bool failed = bulk_failed(db);
+    if (failed && db.poison && blockIdx.x == 0 && threadIdx.x == 0) *db.poison = 1u;   // stop the run
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
         Rec r[MAX_REC];
-        cnt[i] = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
+        cnt[i] = failed ? 0 : footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
     }
 }
 
 template <int S>
 __global__ void __launch_bounds__(256) emit_write_kernel(DevDb db, const uint32_t* __restrict__ off, uint64_t* keys) {
+    if (bulk_failed(db)) return;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
         Rec r[MAX_REC];
         const int k = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
@@ -1283,6 +1290,7 @@ struct OwnKeys {
     uint64_t* keys;
     uint32_t* own;
     uint32_t diag;
+    const uint32_t* err;      // pipelined run_bulks: failed bulk -> no parameter reads
 };
 template <int S>
 DEV uint32_t own_of(const uint32_t* p, uint32_t nw, uint32_t idx, uint32_t diag);
@@ -1339,7 +1347,7 @@ __global__ void __launch_bounds__(256) group_kernel(const uint32_t* __restrict__
                 const uint32_t pos = off[key[k]] + (slot[k] >= 0 ? sbase[slot[k]] + rank[k] : rank[k]);
                 perm[pos] = i;
                 if (OS) {
-                    const uint32_t o = own_of<OS>(pw + poff[i], ok.nw, i, ok.diag);
+                    const uint32_t o = ok.err && __ldcg(ok.err) ? 0u : own_of<OS>(pw + poff[i], ok.nw, i, ok.diag);
                     ok.keys[pos] = ((uint64_t)o << 32) | pos;
                     if (ok.own) ok.own[i] = o;
                 }
@@ -1788,7 +1796,7 @@ __global__ void __launch_bounds__(256) own_gather_kernel(DevDb db, const uint64_
         odep[pos] = d | (pub && pub[idx] ? OWN_PUB : 0u);
         if (wait) owait[pos] = wait[idx];
         if (oout) oout[pos] = db.out_off[idx];          // packed output offset, staged
-        if (PW > 0) {
+        if (PW > 0 && !bulk_failed(db)) {
             const uint32_t* src = db.pw + db.poff[idx];
 #pragma unroll
             for (int w = 0; w < PW; w += 4)
@@ -1827,7 +1835,7 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t lo = oseg[w], hi = oseg[w + 1];
-    if (lo >= hi) return;
+    if (lo >= hi || bulk_failed(db)) return;
     const bool gmode = DEP && __ldcg(&sc[SC_OWNGLOBAL]) != 0u;
     struct E {
         uint32_t idx, t, d;              // d: depth | OWN_PUB; INF past the segment

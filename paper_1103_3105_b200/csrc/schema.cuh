@@ -67,6 +67,11 @@ struct DevDb {
     const uint32_t* src;               // sharded: home-bulk index, or NOT_HOME (a peer's transaction)
     const uint8_t* xflag;              // sharded: 1 = some fragment lives on another shard
     uint32_t idx_base;                 // emit: record idx = idx_base + i (pool arrivals; 0 otherwise)
+    // pipelined gputx_run_bulks (no host round trip between ingest and execute): the
+    // kernels that read parameters treat the bulk as empty once ingest flagged an error
+    // (*err = sc[SC_ERR]); *poison makes every later bulk of the run fail at ingest
+    const uint32_t* err;
+    uint32_t* poison;
     struct UndoRec* undo;              // per-transaction undo-log slots (non-two-phase types)
     uint32_t ins_dense;                // TPC-B: every transaction is a home deposit -> history row = idx
     uint8_t *tm1_sub, *tm1_ai, *tm1_sf, *tm1_cf;   // TM-1 row groups (tm1_txn)
@@ -113,6 +118,8 @@ DEV uint32_t out_bytes(uint32_t t, const uint32_t* p) {
     if (S == S_TM1) return t == 0 ? 40u : t == 1 ? 32u : t == 2 ? 16u : 0u;
     return t == 0 ? (16u + 12u * p[3] + 7u) & ~7u : 16u;
 }
+// pipelined run_bulks: a bulk whose ingest failed is executed as empty
+DEV bool bulk_failed(const DevDb& db) { return db.err && __ldcg(db.err) != 0u; }
 // transaction idx's output record: fixed stride, or packed at its submit-time offset --
 // `oo` when the caller staged it (OUT_AUTO: loaded here, a dependent load before the store)
 constexpr uint32_t OUT_AUTO = 0xFFFFFFFFu;

@@ -209,6 +209,13 @@ struct gputx_db {
     uint32_t rank_dirty = 1;                  // dirty-tile worklist (GPUTX_RANK_DIRTY overrides)
     uint32_t rank_root = 0;                   // root-local sweeps (GPUTX_RANK_ROOT overrides)
     uint32_t rank_stream = 1;                 // TM-1 per-subscriber streaming rank (GPUTX_RANK_STREAM overrides)
+    uint32_t rank_spine = 1;                  // TPC-B / TPC-C / micro spine-streaming rank (GPUTX_RANK_SPINE)
+    int32_t* d_lastw = nullptr;               // spine rank: latest write before each record
+    uint32_t *d_sp = nullptr, *d_lcnt = nullptr, *d_loff = nullptr, *d_lfill = nullptr, *d_links = nullptr;
+    uint32_t *d_heads = nullptr, *d_ccur = nullptr;
+    int32_t* d_clast = nullptr;
+    LookBack<SegMax> lb_seg{};
+    int sp_grid = 0;
     uint32_t rank_window = 0;                 // TPC-C windowed rank: log2 window (GPUTX_RANK_WINDOW overrides)
     int rank_window_grid = 0;
     uint32_t rank_window_cluster = 0;         // 0: cooperative grid with grid barriers (GPUTX_RANK_WCLUSTER)
@@ -461,6 +468,57 @@ gputx_status sort_records(gputx_db* db, uint32_t lo, uint32_t nbits, const uint3
     return GPUTX_OK;
 }
 
+// Spine-streaming rank: links from the (item, ts)-sorted records, then one
+// warp per chain walks its members in ts order (kernels.cuh "Spine-streaming rank").
+template <int S>
+gputx_status spine_rank(gputx_db* db) {
+    cudaStream_t s = db->stream;
+    const uint64_t NB = db->max_bulk, MR = db->max_rec;
+    if (!db->d_lastw) {
+        gputx_status st;
+        const uint64_t tiles = MR / SC_TILE + 4;
+        if ((st = dalloc(db, &db->d_lastw, MR)) || (st = dalloc(db, &db->d_sp, NB + 1)) ||
+            (st = dalloc(db, &db->d_lcnt, NB + 1)) || (st = dalloc(db, &db->d_loff, NB + 2)) ||
+            (st = dalloc(db, &db->d_lfill, NB + 1)) || (st = dalloc(db, &db->d_links, MR)) ||
+            (st = dalloc(db, &db->d_heads, NB + 1)) || (st = dalloc(db, &db->d_ccur, NB + 1)) ||
+            (st = dalloc(db, &db->d_clast, NB + 1)) || (st = dalloc(db, &db->lb_seg.flag, tiles)) ||
+            (st = dalloc(db, &db->lb_seg.agg, tiles)) || (st = dalloc(db, &db->lb_seg.inc, tiles)))
+            return st;
+        dev_fill(db->lb_seg.flag, 0, tiles * 4, s);
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sp_walk_kernel<S>, 256, 0);
+        db->sp_grid = std::max(1, per) * db->nsm;
+    }
+    const uint64_t n = db->n;
+    CK(dev_fill_multi(s, {fseg(db->d_D, 0xFF, n * 4), fseg(db->d_lcnt, 0, (n + 1) * 4), fseg(db->d_lfill, 0, n * 4),
+                          fseg(db->d_sc + SC_NCHAIN, 0, 4)}));
+    ++db->launches;
+    ++db->epoch;
+    const uint32_t tiles = (uint32_t)((db->max_rec + SC_TILE - 1) / SC_TILE);
+    lastw_kernel<S><<<tiles, SC_THREADS, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->lb_seg, db->epoch,
+                                                  next_ticket(db), db->d_lastw, db->d_sp);
+    const uint32_t g = grid_for(db->max_rec, 256, (uint32_t)db->nsm * 8);
+    sp_count_kernel<S><<<g, 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_lastw, db->d_sp, db->d_lcnt);
+    scan_u32(db, db->d_lcnt, db->d_loff, nullptr, n, nullptr);
+    sp_fill_kernel<S><<<g, 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_lastw, db->d_sp, db->d_loff,
+                                         db->d_lfill, db->d_links, db->d_heads, db->d_sc + SC_NCHAIN);
+    db->launches += 3;
+    const uint64_t* keys = db->d_sorted;
+    const uint32_t* nrec = db->d_sc + SC_NREC;
+    const uint32_t* heads = db->d_heads;
+    const uint32_t* nh = db->d_sc + SC_NCHAIN;
+    const uint32_t* loff = db->d_loff;
+    const uint32_t* links = db->d_links;
+    uint32_t* D = db->d_D;
+    uint32_t* cur = db->d_ccur;
+    int32_t* last = db->d_clast;
+    uint32_t* sc = db->d_sc;
+    void* args[] = {&keys, &nrec, &heads, &nh, &loff, &links, &D, &cur, &last, &sc};
+    TRY(launch_coop(db, (const void*)sp_walk_kernel<S>, db->sp_grid, 256, args));
+    ++db->launches;
+    return GPUTX_OK;
+}
+
 // K-SET part 1 (also the analysis half of GPUTX_AUTO): emit, sort, rank fixpoint, and
 // the depth reduction giving d = max depth and w0 = |0-set|
 template <int S>
@@ -474,10 +532,13 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     // TM-1: single-subscriber transactions -> sort on the subscriber bits only and run
     // the exact streaming recurrence per subscriber (rank_stream_tm1_kernel)
     const bool stream = S == S_TM1 && db->rank_stream;
+    // spine-streaming rank (TPC-B / TPC-C / micro under the R/W rule, unsharded)
+    const bool spine = S != S_TM1 && db->rank_spine && !db->has_ts && !(db->cfg.flags & GPUTX_FLAG_ADD_RULE) &&
+                       db->item_bits <= 32;
     // TPC-C: windowed rank -> (window, item, ts) order: stable sort on the item bits, then
     // on the window bits of the transaction index (key bits [6 + WB, 30))
     const uint32_t wb = db->rank_window;
-    const bool windowed = S == S_TPCC && wb && db->n > (1ull << wb);
+    const bool windowed = !spine && S == S_TPCC && wb && db->n > (1ull << wb);
     const uint32_t nwin = windowed ? (uint32_t)((db->n - 1) >> wb) + 1 : 1;
     if (stream)
         TRY(sort_records(db, KEY_ITEM_SHIFT + TM1_COMP_BITS, db->item_bits - TM1_COMP_BITS, db->d_sc + SC_NREC,
@@ -499,7 +560,9 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(dev_fill_multi(s, {fseg(db->d_D, 0, db->n * sizeof(uint32_t)), fseg(&db->d_bar->dead, 0, sizeof(uint32_t))}));
-    if (windowed) {
+    if (spine) {
+        TRY(spine_rank<S>(db));
+    } else if (windowed) {
         win_bounds_kernel<<<grid_for(db->max_rec + 1, 256, 148 * 8), 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, wb,
                                                                              nwin, db->d_wseg);
         ++db->launches;
@@ -1468,6 +1531,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     db->rank_root = schema == S_TPCC || (schema == S_TPCB && add_rule) ? 0 : 1;
     if (const char* e = getenv("GPUTX_RANK_ROOT")) db->rank_root = (uint32_t)atoi(e);
     if (const char* e = getenv("GPUTX_RANK_STREAM")) db->rank_stream = (uint32_t)atoi(e);
+    if (const char* e = getenv("GPUTX_RANK_SPINE")) db->rank_spine = (uint32_t)atoi(e);
     // TPC-C: 128 k-transaction windows (measured: 2^12 .. 2^17 -> rank 19.6 .. 10.8 ms at
     // 1 M transactions, profiles/round1.md)
     db->rank_window = schema == S_TPCC ? 17 : 0;
@@ -2858,6 +2922,9 @@ void gputx_close_db(gputx_db* db) {
     dfree(db, db->tm1_sub); dfree(db, db->tm1_ai); dfree(db, db->tm1_sf); dfree(db, db->tm1_cf);
     dfree(db, db->d_undo);
     dfree(db, db->d_out_off);
+    dfree(db, db->d_lastw); dfree(db, db->d_sp); dfree(db, db->d_lcnt); dfree(db, db->d_loff); dfree(db, db->d_lfill);
+    dfree(db, db->d_links); dfree(db, db->d_heads); dfree(db, db->d_ccur); dfree(db, db->d_clast);
+    dfree(db, db->lb_seg.flag); dfree(db, db->lb_seg.agg); dfree(db, db->lb_seg.inc);
     dfree(db, db->d_oseg); dfree(db, db->d_prog); dfree(db, db->d_oout); dfree(db, db->d_own); dfree(db, db->d_wait); dfree(db, db->d_pub); dfree(db, db->d_owait);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,
                   db->q_ts, db->d_zflag, db->d_fna, db->d_list, db->d_npos, db->d_noff, db->d_rpos, db->d_rts,

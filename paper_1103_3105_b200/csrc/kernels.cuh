@@ -30,6 +30,7 @@ constexpr int SC_SPARSE = 36;     // TPC-B ingest: transactions without a histor
 constexpr int SC_P2P = 37;        // [37, 39): peer exchange: records received, overflow bits
 constexpr int SC_OUTBYTES = 40;   // GPUTX_FLAG_PACKED_OUT: bytes of the bulk's packed output records
 constexpr int SC_NTXN = 41;       // transactions in the submitted bulk (device copy of n, ingest)
+constexpr int SC_NCHAIN = 42;     // spine-streaming rank: chains
 
 // TM-1 sub_nbr hash (shared host/device)
 __host__ __device__ inline uint64_t nbr_hash(uint64_t x) {
@@ -1209,17 +1210,26 @@ DEV uint32_t block_max_u32(uint32_t v) {      // result valid in thread 0
     return v;
 }
 
-__global__ void __launch_bounds__(256) depth_reduce_kernel(const uint32_t* D, uint32_t n, uint32_t* sc) {
+// (a depth the spine walk left unset -- only after its watchdog tripped, EDEADLOCK -- counts
+// as 0 so that nothing downstream sizes work by it)
+__global__ void __launch_bounds__(256) depth_reduce_kernel(uint32_t* D, uint32_t n, uint32_t* sc) {
     uint32_t mx = 0, z = 0;
     const uint32_t n4 = n / 4;
-    const uint4* D4 = reinterpret_cast<const uint4*>(D);         // D is cudaMalloc'ed: 16-B aligned
+    uint4* D4 = reinterpret_cast<uint4*>(D);                     // D is cudaMalloc'ed: 16-B aligned
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-        const uint4 d = __ldcg(&D4[i]);
+        uint4 d = __ldcg(&D4[i]);
+        if ((d.x & d.y & d.z & d.w) == 0xFFFFFFFFu || d.x == 0xFFFFFFFFu || d.y == 0xFFFFFFFFu || d.z == 0xFFFFFFFFu ||
+            d.w == 0xFFFFFFFFu) {
+            d.x = d.x == 0xFFFFFFFFu ? 0u : d.x; d.y = d.y == 0xFFFFFFFFu ? 0u : d.y;
+            d.z = d.z == 0xFFFFFFFFu ? 0u : d.z; d.w = d.w == 0xFFFFFFFFu ? 0u : d.w;
+            D4[i] = d;
+        }
         mx = max(max(mx, max(d.x, d.y)), max(d.z, d.w));
         z += (d.x == 0) + (d.y == 0) + (d.z == 0) + (d.w == 0);
     }
     for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t d = __ldcg(&D[i]);
+        uint32_t d = __ldcg(&D[i]);
+        if (d == 0xFFFFFFFFu) { d = 0; D[i] = 0; }
         mx = max(mx, d);
         z += d == 0;
     }
@@ -1937,6 +1947,226 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
             if (publish && lane == 0) st_release(&prog[w], dn);
             pubr = false;
             d0 = dn;
+        }
+    }
+}
+
+// =====================================================================================
+// Spine-streaming rank (DESIGN.md §4 "Spine-streaming rank"): every transaction of TPC-B,
+// TPC-C and micro writes one *spine* item that only its own kind writes (TPC-B its branch
+// balance, TPC-C NewOrder its district's next order id and Payment its warehouse's YTD,
+// micro its tuple), so the transactions sharing a spine item form a chain in ts order and
+// D[t] = max(D[previous chain member] + 1, max over t's other conflicting predecessors p of
+// D[p] + 1) -- the longest-path depth of the T-dependency graph computed
+// in one streaming pass per chain.  The other predecessors ("links") come from the
+// (item, ts)-sorted records: a read conflicts with the previous write of its item; a
+// write with the reads since the previous write (each of which is after that write), or
+// with the previous write if there are none.  One warp walks a chain 32 members at a
+// time (max-plus scan), writing each member's depth as soon as its links' depths exist.
+// =====================================================================================
+constexpr uint32_t SP_UNSET = 0xFFFFFFFFu;
+
+template <int S> DEV uint32_t spine_j() { return S == S_TPCB ? 2u : 0u; }   // footprint position
+
+// segmented max of W positions: per record (head of its item group, position of the
+// latest write up to it); identity (0, -1)
+struct SegMax {
+    uint32_t f;
+    int32_t v;
+};
+struct OpSegMax {
+    static DEV SegMax identity() { return SegMax{0u, -1}; }
+    static DEV SegMax combine(SegMax a, SegMax b) { return SegMax{a.f | b.f, b.f ? b.v : max(a.v, b.v)}; }
+};
+
+// lastw[i] encodes what precedes record i in its item group: -1 = i is the group's first
+// record; 2w + 1 = the latest write before i is at w; 2g = no write before i, the group
+// starts at g (a segmented max-scan of head / write markers).  sp[t] = t's spine item.
+template <int S>
+__global__ void __launch_bounds__(SC_THREADS) lastw_kernel(const uint64_t* __restrict__ keys, const uint32_t* n_ptr,
+                                                           LookBack<SegMax> lb, uint32_t epoch, uint32_t* ticket,
+                                                           int32_t* lastw, uint32_t* sp) {
+    __shared__ SegMax sm[8];
+    __shared__ uint32_t s_tile;
+    __shared__ SegMax s_pre;
+    const uint32_t n = *n_ptr;
+    const uint32_t ntiles = (n + SC_TILE - 1) / SC_TILE;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t b = (uint64_t)tile * SC_TILE + threadIdx.x * SC_ITEMS;
+    SegMax e[SC_ITEMS];
+    SegMax agg = OpSegMax::identity();
+    uint64_t prev_item = b > 0 && b - 1 < n ? key_item(keys[b - 1]) : ~0ull;
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        e[k] = OpSegMax::identity();
+        if (b + k < n) {
+            const uint64_t key = keys[b + k];
+            const uint64_t it = key_item(key);
+            const bool head = b + k == 0 || it != prev_item;
+            e[k] = SegMax{head ? 1u : 0u, key_mode(key) == 1u ? (int32_t)(2 * (b + k) + 1) : head ? (int32_t)(2 * (b + k)) : -1};
+            if (key_j(key) == spine_j<S>()) sp[key_idx(key)] = (uint32_t)it;
+            prev_item = it;
+        }
+        agg = OpSegMax::combine(agg, e[k]);
+    }
+    SegMax tot;
+    SegMax ex = block_scan_excl<SegMax, OpSegMax>(agg, tot, sm);
+    if (warp_id() == 0) {
+        SegMax pre = lookback_warp<SegMax, OpSegMax>(lb, tile, epoch, tot);
+        if (lane_id() == 0) s_pre = pre;
+    }
+    __syncthreads();
+    SegMax run = OpSegMax::combine(s_pre, ex);
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        if (b + k < n) lastw[b + k] = e[k].f ? -1 : run.v;     // exclusive (a head starts fresh)
+        run = OpSegMax::combine(run, e[k]);
+    }
+}
+
+// links of record i (not its transaction's spine record): calls f(idx of predecessor)
+template <class F>
+DEV void sp_links(const uint64_t* __restrict__ keys, const int32_t* __restrict__ lastw, uint32_t i, F f) {
+    const uint64_t k = keys[i];
+    const int32_t enc = lastw[i];
+    if (enc < 0) return;                            // first access of its item
+    const bool has_w = enc & 1;
+    const int64_t lw = has_w ? (enc - 1) / 2 : -1;  // latest write, or none
+    const int64_t lo = has_w ? lw + 1 : enc / 2;    // first read after it (or the group start)
+    if (key_mode(k) == 1u) {                        // a write: the reads since the last write, else it
+        for (int64_t j = lo; j < (int64_t)i; ++j) f(key_idx(keys[j]));
+        if (lo == (int64_t)i && has_w) f(key_idx(keys[lw]));
+    } else if (has_w) {                             // a read: the last write
+        f(key_idx(keys[lw]));
+    }
+}
+
+// (a predecessor in t's own chain is implied by the chain order: not a link)
+template <int S>
+__global__ void __launch_bounds__(256) sp_count_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                       const int32_t* __restrict__ lastw,
+                                                       const uint32_t* __restrict__ sp, uint32_t* lcnt) {
+    const uint32_t nrec = *nrec_ptr;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        if (key_j(k) == spine_j<S>()) continue;     // the chain itself
+        const uint32_t me = sp[key_idx(k)];
+        uint32_t c = 0;
+        sp_links(keys, lastw, i, [&](uint32_t p) { c += sp[p] != me; });
+        if (c) atomicAdd(&lcnt[key_idx(k)], c);
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) sp_fill_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                      const int32_t* __restrict__ lastw,
+                                                      const uint32_t* __restrict__ sp,
+                                                      const uint32_t* __restrict__ loff, uint32_t* lfill,
+                                                      uint32_t* links, uint32_t* heads, uint32_t* nheads) {
+    const uint32_t nrec = *nrec_ptr;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const uint32_t t = key_idx(k);
+        if (key_j(k) == spine_j<S>()) {             // chain heads (order irrelevant)
+            if (i == 0 || key_item(keys[i - 1]) != key_item(k)) heads[atomicAdd(nheads, 1u)] = i;
+            continue;
+        }
+        const uint32_t me = sp[t];
+        sp_links(keys, lastw, i, [&](uint32_t p) {
+            if (sp[p] != me) links[loff[t] + atomicAdd(&lfill[t], 1u)] = p;
+        });
+    }
+}
+
+// One warp per chain (co-resident cooperative grid; a warp owning several chains cycles
+// through them, advancing each as far as its links allow: the unprocessed transaction of
+// smallest ts always can advance, so the walk terminates).  Chain state in global memory.
+template <int S>
+__global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict__ keys, const uint32_t* nrec_ptr,
+                                                      const uint32_t* __restrict__ heads, const uint32_t* nheads_ptr,
+                                                      const uint32_t* __restrict__ loff,
+                                                      const uint32_t* __restrict__ links, uint32_t* D,
+                                                      uint32_t* cur, int32_t* last, uint32_t* sc) {
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const uint32_t lane = lane_id();
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5), w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nrec = *nrec_ptr, nh = *nheads_ptr;
+    if (w >= nh) return;
+    SpinWatch wd;
+    uint32_t left = 0;                                   // chains of this warp not finished
+    for (uint32_t c = w; c < nh; c += nw) {
+        if (lane == 0) { cur[c] = heads[c]; last[c] = -1; }
+        ++left;
+    }
+    __syncwarp();
+    uint32_t idle = 0;
+    while (left) {
+        bool progress = false;
+        for (uint32_t c = w; c < nh; c += nw) {
+            uint32_t p = __ldcg(&cur[c]);
+            if (p == SP_UNSET) continue;                 // finished
+            const uint64_t item = key_item(keys[heads[c]]);
+            int32_t ld = __ldcg(&last[c]);
+            while (true) {
+                const uint32_t r = p + lane;
+                bool mem = false;
+                uint32_t t = 0;
+                if (r < nrec) {
+                    const uint64_t k = keys[r];
+                    mem = key_item(k) == item;
+                    t = key_idx(k);
+                }
+                const uint32_t memmask = __ballot_sync(FULL, mem);
+                const uint32_t clen = memmask == FULL ? 32u : __ffs(~memmask) - 1;   // members in this chunk
+                if (clen == 0) {                         // chain done
+                    if (lane == 0) cur[c] = SP_UNSET;
+                    --left;
+                    progress = true;
+                    break;
+                }
+                // e = max over links of D[p] + 1 (or -1); blocked if some link's depth is not there yet
+                int32_t e = -1;
+                bool blocked = false;
+                if (lane < clen) {
+                    const uint32_t a = loff[t], b2 = loff[t + 1];
+                    for (uint32_t x = a; x < b2; ++x) {
+                        const uint32_t dp = __ldcg(&D[__ldg(&links[x])]);
+                        if (dp == SP_UNSET) { blocked = true; break; }
+                        e = max(e, (int32_t)dp + 1);
+                    }
+                }
+                const uint32_t bm = __ballot_sync(FULL, blocked && lane < clen);
+                const uint32_t k = bm ? __ffs(bm) - 1 : clen;                       // lanes [0, k) proceed
+                // D_l = max(ld + 1 + l, max_{m <= l} (e_m - m) + l)   (max-plus scan)
+                int32_t v = lane < k ? e - (int32_t)lane : -0x3FFFFFFF;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(FULL, v, o);
+                    if ((int)lane >= o) v = max(v, y);
+                }
+                const int32_t dl = max(ld + 1 + (int32_t)lane, v + (int32_t)lane);
+                if (lane < k) __stcg(&D[t], (uint32_t)dl);
+                if (k) {
+                    ld = __shfl_sync(FULL, dl, k - 1);
+                    p += k;
+                    progress = true;
+                }
+                if (k < 32) {                            // blocked (or the chain ended inside)
+                    if (k == clen && clen < 32) continue;   // ended: the next iteration sees clen = 0
+                    break;
+                }
+            }
+            if (lane == 0 && __ldcg(&cur[c]) != SP_UNSET) { cur[c] = p; last[c] = ld; }
+            __syncwarp();
+        }
+        if (!progress) {
+            if (++idle > 8) __nanosleep(100);
+            if (wd.expired(&sc[SC_DEADLOCK])) return;
+        } else {
+            idle = 0;
         }
     }
 }

@@ -178,6 +178,8 @@ typedef struct {
                                             (e.g. by a profiler) and used counter hand-offs only */
 #define GPUTX_STAT_KSET_DATAFLOW 2u      /* K-SET ran the dataflow executor (per-item completion
                                             counters, k-set-order dispatch) instead of rounds  */
+#define GPUTX_STAT_KSET_CHAIN 16u        /* TPC-B K-SET over spine chains: one thread per branch
+                                            chain, members in k-set order, cross-chain waits  */
 #define GPUTX_STAT_PIPELINED 8u         /* gputx_run_bulks ran the bulk without a host round trip
                                             (TM-1 / micro K-SET): counts are set, phase times 0 */
 #define GPUTX_STAT_KSET_OWNER 4u         /* K-SET ran owner-local rounds: every warp executes the

@@ -99,7 +99,7 @@ struct FillSeg {
     uint64_t bytes;
     uint32_t v8;
 };
-constexpr int FILL_MAX = 4;
+constexpr int FILL_MAX = 6;
 struct FillList {
     FillSeg s[FILL_MAX];
 };

@@ -216,6 +216,12 @@ struct gputx_db {
     int32_t* d_clast = nullptr;
     LookBack<SegMax> lb_seg{};
     int sp_grid = 0;
+    bool spine_ran = false;                   // this bulk's depths came from the spine rank
+    uint8_t* d_cpub = nullptr;                // chain executor: transaction another chain waits for
+    uint32_t* d_cdone = nullptr;              // chain executor: done[t] == chain_epoch
+    uint32_t chain_epoch = 0;
+    int chain_cap = 0;                        // co-resident chain threads
+    bool kset_ran_chain = false;
     uint32_t rank_window = 0;                 // TPC-C windowed rank: log2 window (GPUTX_RANK_WINDOW overrides)
     int rank_window_grid = 0;
     uint32_t rank_window_cluster = 0;         // 0: cooperative grid with grid barriers (GPUTX_RANK_WCLUSTER)
@@ -232,6 +238,7 @@ struct gputx_db {
     uint32_t kset_cluster = 8;     // CTAs per thread-block cluster of the K-SET executor
     // owner-local K-SET rounds: GPUTX_KSET_OWN=0 restores the global rounds
     int kset_own = 1;
+    int kset_chain = 1;                // TPC-B: K-SET over spine chains (GPUTX_KSET_CHAIN=0: owner warps)
     bool kset_ran_own = false;
     int own_grid[2] = {0, 0};          // co-resident CTAs of the executor without / with waits
     uint32_t own_g = 0, own_nw = 0;    // this bulk's executor grid and owner warps
@@ -481,17 +488,22 @@ gputx_status spine_rank(gputx_db* db) {
             (st = dalloc(db, &db->d_lcnt, NB + 1)) || (st = dalloc(db, &db->d_loff, NB + 2)) ||
             (st = dalloc(db, &db->d_lfill, NB + 1)) || (st = dalloc(db, &db->d_links, MR)) ||
             (st = dalloc(db, &db->d_heads, NB + 1)) || (st = dalloc(db, &db->d_ccur, NB + 1)) ||
-            (st = dalloc(db, &db->d_clast, NB + 1)) || (st = dalloc(db, &db->lb_seg.flag, tiles)) ||
+            (st = dalloc(db, &db->d_clast, NB + 1)) || (st = dalloc(db, &db->d_cpub, NB + 1)) ||
+            (st = dalloc(db, &db->d_cdone, NB + 1)) || (st = dalloc(db, &db->lb_seg.flag, tiles)) ||
             (st = dalloc(db, &db->lb_seg.agg, tiles)) || (st = dalloc(db, &db->lb_seg.inc, tiles)))
             return st;
         dev_fill(db->lb_seg.flag, 0, tiles * 4, s);
+        dev_fill(db->d_cdone, 0, (NB + 1) * 4, s);
+        int perc = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perc, kset_chain_exec_kernel<S_TPCB>, 128, 0);
+        db->chain_cap = std::max(1, perc) * db->nsm * 4;              // chains (one per warp)
         int per = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sp_walk_kernel<S>, 256, 0);
         db->sp_grid = std::max(1, per) * db->nsm;
     }
     const uint64_t n = db->n;
     CK(dev_fill_multi(s, {fseg(db->d_D, 0xFF, n * 4), fseg(db->d_lcnt, 0, (n + 1) * 4), fseg(db->d_lfill, 0, n * 4),
-                          fseg(db->d_sc + SC_NCHAIN, 0, 4)}));
+                          fseg(db->d_sc + SC_NCHAIN, 0, 4), fseg(db->d_cpub, 0, S == S_TPCB ? n : 0)}));
     ++db->launches;
     ++db->epoch;
     const uint32_t tiles = (uint32_t)((db->max_rec + SC_TILE - 1) / SC_TILE);
@@ -501,7 +513,8 @@ gputx_status spine_rank(gputx_db* db) {
     sp_count_kernel<S><<<g, 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_lastw, db->d_sp, db->d_lcnt);
     scan_u32(db, db->d_lcnt, db->d_loff, nullptr, n, nullptr);
     sp_fill_kernel<S><<<g, 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_lastw, db->d_sp, db->d_loff,
-                                         db->d_lfill, db->d_links, db->d_heads, db->d_sc + SC_NCHAIN);
+                                         db->d_lfill, db->d_links, db->d_heads, db->d_sc + SC_NCHAIN,
+                                         S == S_TPCB ? db->d_cpub : nullptr);
     db->launches += 3;
     const uint64_t* keys = db->d_sorted;
     const uint32_t* nrec = db->d_sc + SC_NREC;
@@ -560,6 +573,7 @@ gputx_status kset_rank(gputx_db* db, const DevDb& v) {
     cudaEventRecord(db->ev[3], s);
     // rank fixpoint (persistent, cooperative)
     CK(dev_fill_multi(s, {fseg(db->d_D, 0, db->n * sizeof(uint32_t)), fseg(&db->d_bar->dead, 0, sizeof(uint32_t))}));
+    db->spine_ran = spine;
     if (spine) {
         TRY(spine_rank<S>(db));
     } else if (windowed) {
@@ -737,11 +751,53 @@ bool kset_use_dataflow(const gputx_db* db) {
 }
 
 // K-SET part 2: group by (depth, type), then the k-set rounds
+// K-SET over spine chains (TPC-B): one thread per chain, no group step (kernels.cuh)
+template <int S>
+bool kset_use_chain(const gputx_db* db) {
+    return S == S_TPCB && db->spine_ran && db->kset_own && db->kset_chain && !db->has_ts && !db->trace_rounds &&
+           !(db->kset_diag & ~(1u | 8u | 1024u | 0xFFFF0000u)) && db->cfg.dims[0] <= (uint32_t)db->chain_cap;
+}
+
+template <int S>
+gputx_status kset_chain_exec(gputx_db* db, const DevDb& v) {
+    cudaStream_t s = db->stream;
+    cudaEventRecord(db->ev[5], s);
+    if (++db->chain_epoch == 0) ++db->chain_epoch;
+    DevDb vv = v;
+    const uint64_t* keys = db->d_sorted;
+    const uint32_t* nrec = db->d_sc + SC_NREC;
+    const uint32_t* heads = db->d_heads;
+    const uint32_t* nh = db->d_sc + SC_NCHAIN;
+    const uint32_t* loff = db->d_loff;
+    const uint32_t* links = db->d_links;
+    const uint8_t* cpub = db->d_cpub;
+    uint32_t* done = db->d_cdone;
+    uint32_t ep = db->chain_epoch;
+    uint32_t* sc = db->d_sc;
+    uint32_t diag = db->kset_diag;
+    void* args[] = {&vv, &keys, &nrec, &heads, &nh, &loff, &links, &cpub, &done, &ep, &sc, &diag};
+    const int grid = (int)((db->cfg.dims[0] + 3) / 4);              // chains <= branches, 4 per CTA
+    TRY(launch_coop(db, (const void*)kset_chain_exec_kernel<S_TPCB>, std::max(1, grid), 128, args));
+    ++db->launches;
+    db->kset_ran_chain = true;
+    db->kset_ran_own = true;
+    db->kset_ran_df = false;
+    db->has_perm = false;                     // (gputx_read_perm groups on demand)
+    return GPUTX_OK;
+}
+
 template <int S>
 gputx_status kset_exec(gputx_db* db, const DevDb& v) {
     NVTX_SCOPE("gputx.kset.group_exec");
     cudaStream_t s = db->stream;
     const uint32_t T = db->ntypes;
+    db->kset_ran_chain = false;
+    if (kset_use_chain<S>(db) && db->n) {
+        TRY(kset_chain_exec<S>(db, v));
+        STAGE("kset exec");
+        cudaEventRecord(db->ev[6], s);
+        return GPUTX_OK;
+    }
     group_zero_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc, T);     // key count + zeroed counters
     ++db->launches;
     const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
@@ -1576,6 +1632,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_CLUSTER")) db->kset_cluster = (uint32_t)std::max(0, atoi(e));
     if (const char* e = getenv("GPUTX_KSET_DF")) db->kset_df = atoi(e);
     if (const char* e = getenv("GPUTX_KSET_OWN")) db->kset_own = atoi(e);
+    if (const char* e = getenv("GPUTX_KSET_CHAIN")) db->kset_chain = atoi(e);
     // diag 16384 (tests: arbitrary owners) needs (item, ts)-sorted records for the dependency pass
     if (schema == S_TM1 && (db->kset_diag & 16384u)) db->rank_stream = 0;
     if (const char* e = getenv("GPUTX_KSET_DF_AHEAD")) db->kset_df_ahead = (uint32_t)atoi(e);
@@ -2283,7 +2340,8 @@ gputx_status execute_finish(gputx_db* db, gputx_stats* stats) {
         stats->out_bytes = db->nshards > 1 ? db->nh * db->out_stride : db->out_bytes;
         stats->flags = (db->h_sc[SC_NOCLUSTER] ? GPUTX_STAT_CLUSTER_FALLBACK : 0) |
                        ((ranked && eff == GPUTX_KSET && db->kset_ran_df) ? GPUTX_STAT_KSET_DATAFLOW : 0) |
-                       ((ranked && eff == GPUTX_KSET && db->kset_ran_own) ? GPUTX_STAT_KSET_OWNER : 0);
+                       ((ranked && eff == GPUTX_KSET && db->kset_ran_own) ? GPUTX_STAT_KSET_OWNER : 0) |
+                       ((ranked && eff == GPUTX_KSET && db->kset_ran_chain) ? GPUTX_STAT_KSET_CHAIN : 0);
         cudaGetLastError();
     }
     return GPUTX_OK;
@@ -2424,6 +2482,21 @@ gputx_status gputx_trace_rounds(gputx_db* db, int on) {
 gputx_status gputx_read_perm(gputx_db* db, uint32_t* host, uint64_t n) {
     if (db && db->exec_pending) return fail(db, GPUTX_ESTATE, "an asynchronous execute is pending: gputx_wait first");
     if (!db || !host) return GPUTX_EINVAL;
+    if (db->has_depth && !db->has_perm && db->executed && n == db->n && n) {
+        // the chain executor needs no (depth, type) order: group it on demand
+        cudaStream_t s = db->stream;
+        const uint32_t T = db->ntypes;
+        const uint32_t P = db->group_p ? std::min(db->group_p, T) : T;
+        const uint32_t gg = grid_for((db->n + GR_TILE - 1) / GR_TILE, 1, 148 * 4);
+        group_zero_kernel<<<148 * 4, 256, 0, s>>>(db->d_gcnt, db->d_sc, T);
+        group_kernel<0, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, nullptr, nullptr,
+                                              nullptr, nullptr, nullptr, nullptr, P);
+        scan_u32(db, db->d_gcnt, db->d_goff, db->d_sc + SC_NKEYS, db->n * T + 1, nullptr);
+        group_kernel<1, 0><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
+                                              db->d_perm, nullptr, nullptr, nullptr, nullptr, P);
+        CK(cudaStreamSynchronize(s));
+        db->has_perm = true;
+    }
     if (!db->has_perm || n != db->n) return fail(db, GPUTX_ESTATE, "no K-SET order for this bulk");
     if (n) CK(cudaMemcpy(host, db->d_perm, n * 4, cudaMemcpyDeviceToHost));
     return GPUTX_OK;
@@ -2924,6 +2997,7 @@ void gputx_close_db(gputx_db* db) {
     dfree(db, db->d_out_off);
     dfree(db, db->d_lastw); dfree(db, db->d_sp); dfree(db, db->d_lcnt); dfree(db, db->d_loff); dfree(db, db->d_lfill);
     dfree(db, db->d_links); dfree(db, db->d_heads); dfree(db, db->d_ccur); dfree(db, db->d_clast);
+    dfree(db, db->d_cpub); dfree(db, db->d_cdone);
     dfree(db, db->lb_seg.flag); dfree(db, db->lb_seg.agg); dfree(db, db->lb_seg.inc);
     dfree(db, db->d_oseg); dfree(db, db->d_prog); dfree(db, db->d_oout); dfree(db, db->d_own); dfree(db, db->d_wait); dfree(db, db->d_pub); dfree(db, db->d_owait);
     void* pp[] = {db->d_prec, db->d_prec2, db->d_pins, db->q_ins, db->st_ins, db->q_type, db->q_poff, db->q_pw,

@@ -2065,7 +2065,8 @@ __global__ void __launch_bounds__(256) sp_fill_kernel(const uint64_t* __restrict
                                                       const int32_t* __restrict__ lastw,
                                                       const uint32_t* __restrict__ sp,
                                                       const uint32_t* __restrict__ loff, uint32_t* lfill,
-                                                      uint32_t* links, uint32_t* heads, uint32_t* nheads) {
+                                                      uint32_t* links, uint32_t* heads, uint32_t* nheads,
+                                                      uint8_t* cpub) {
     const uint32_t nrec = *nrec_ptr;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
@@ -2076,7 +2077,10 @@ __global__ void __launch_bounds__(256) sp_fill_kernel(const uint64_t* __restrict
         }
         const uint32_t me = sp[t];
         sp_links(keys, lastw, i, [&](uint32_t p) {
-            if (sp[p] != me) links[loff[t] + atomicAdd(&lfill[t], 1u)] = p;
+            if (sp[p] != me) {
+                links[loff[t] + atomicAdd(&lfill[t], 1u)] = p;
+                if (cpub) cpub[p] = 1;                  // (chain executor: p publishes)
+            }
         });
     }
 }
@@ -2169,6 +2173,114 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
             idle = 0;
         }
     }
+}
+
+// =====================================================================================
+// K-SET over spine chains (TPC-B; DESIGN.md §4 "Chain owners").  Along a spine chain the
+// depth strictly increases (each member conflicts with the previous one), so a chain owns
+// exactly one transaction of each of its k-sets: owner-local rounds with the chain as the
+// owner are the chain's members in order, one per round, and a round of one transaction
+// is ordered after the previous one by the executing thread's program order -- no
+// barrier at all.  One warp per chain: lane 0 executes the members; all 32 lanes stage
+// them 32 at a time, four chunks ahead, each stage a chunk after the one it depends on
+// (keys -> type / offset / links / publish flag -> parameters and output offset -> account
+// rows warmed into L2), so lane 0 never waits on metadata.  Before a member runs, lane 0
+// waits for the members of OTHER chains it depends on (the spine rank's links: done[p] ==
+// epoch, acquire); a member another chain waits for publishes done[t] (release) after it.
+// =====================================================================================
+template <int S>
+__global__ void __launch_bounds__(128) kset_chain_exec_kernel(DevDb db, const uint64_t* __restrict__ keys,
+                                                              const uint32_t* nrec_ptr,
+                                                              const uint32_t* __restrict__ heads,
+                                                              const uint32_t* nheads_ptr,
+                                                              const uint32_t* __restrict__ loff,
+                                                              const uint32_t* __restrict__ links,
+                                                              const uint8_t* __restrict__ cpub, uint32_t* done,
+                                                              uint32_t epoch, uint32_t* sc, uint32_t diag) {
+    constexpr int PW = 4;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    constexpr uint64_t NONE = ~0ull;
+    const uint32_t lane = lane_id();
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + warp_id();
+    const uint32_t nh = *nheads_ptr, nrec = *nrec_ptr;
+    if (c >= nh || bulk_failed(db)) return;
+    const uint32_t lo = heads[c];
+    const uint64_t item = key_item(__ldg(&keys[lo]));
+    // stage registers of this lane's member in each chunk
+    struct Meta { uint32_t idx, t, o, la, lb, pb, oo; };
+    struct Full { uint32_t idx, t, la, lb, pb, oo; uint32_t q[PW]; };
+    auto load_key = [&](uint32_t base) -> uint64_t {
+        const uint32_t j = base + lane;
+        if (j >= nrec) return NONE;
+        const uint64_t k = __ldg(&keys[j]);
+        return key_item(k) == item ? k : NONE;
+    };
+    auto load_meta = [&](uint64_t k, Meta& m) {
+        m.idx = OWN_INF;
+        if (k == NONE) return;
+        const uint32_t x = key_idx(k);
+        m.idx = x; m.t = db.type[x]; m.o = db.poff[x]; m.la = loff[x]; m.lb = loff[x + 1]; m.pb = cpub[x];
+        m.oo = db.out_off ? db.out_off[x] : OUT_AUTO;
+    };
+    auto load_full = [&](const Meta& m, Full& f) {
+        f.idx = m.idx; f.t = m.t; f.la = m.la; f.lb = m.lb; f.pb = m.pb; f.oo = m.oo;
+        if (m.idx == OWN_INF) return;
+        const uint4 v = *reinterpret_cast<const uint4*>(db.pw + m.o);   // (TPC-B: 4 words, 16-B aligned)
+        f.q[0] = v.x; f.q[1] = v.y; f.q[2] = v.z; f.q[3] = v.w;
+    };
+    // chunk b (relative) = members [lo + 32b, lo + 32b + 32)
+    Full E, P1, P2;
+    Meta M;
+    uint64_t K;
+    {
+        const uint64_t k0 = load_key(lo), k1 = load_key(lo + 32), k2 = load_key(lo + 64), k3 = load_key(lo + 96);
+        Meta m0, m1, m2;
+        load_meta(k0, m0); load_meta(k1, m1); load_meta(k2, m2); load_meta(k3, M);
+        load_full(m0, E); load_full(m1, P1); load_full(m2, P2);
+        K = load_key(lo + 128);
+        if (E.idx != OWN_INF && !(diag & 8u)) warm_rows<S>(db, E.t, E.q);
+        if (P1.idx != OWN_INF && !(diag & 8u)) warm_rows<S>(db, P1.t, P1.q);
+    }
+    SpinWatch wd;
+    uint32_t len = 0, base = lo;
+    while (true) {
+        const uint32_t valid = __ballot_sync(FULL, E.idx != OWN_INF);       // a prefix of the chunk
+        const uint32_t cnt = __popc(valid);
+        for (uint32_t m = 0; m < cnt; ++m) {
+            const uint32_t idx = __shfl_sync(FULL, E.idx, m), t = __shfl_sync(FULL, E.t, m);
+            const uint32_t la = __shfl_sync(FULL, E.la, m), lb = __shfl_sync(FULL, E.lb, m);
+            const uint32_t pb = __shfl_sync(FULL, E.pb, m), oo = __shfl_sync(FULL, E.oo, m);
+            uint32_t q[PW];
+#pragma unroll
+            for (int w = 0; w < PW; ++w) q[w] = __shfl_sync(FULL, E.q[w], m);
+            if (lane == 0) {
+                for (uint32_t x = la; x < lb; ++x) {          // predecessors in other chains
+                    const uint32_t p = __ldg(&links[x]);
+                    uint32_t spins = 0;
+                    while (ld_acquire(&done[p]) != epoch) {
+                        if (++spins > 8) __nanosleep(64);
+                        if (wd.expired(&sc[SC_DEADLOCK])) break;
+                    }
+                }
+                kx_jitter(diag, len + m, c, 0);
+                if (!(diag & 1u)) exec_txn_p<S, false>(db, idx, t, q, oo);   // diag 1: skip bodies (timing)
+                if (pb) st_release(&done[idx], epoch);
+            }
+            __syncwarp();
+        }
+        len += cnt;
+        if (cnt < 32) break;                                  // the chain ended in this chunk
+        // rotate the stages: each register set is consumed a chunk after its loads were issued
+        base += 32;
+        E = P1;
+        P1 = P2;
+        // the account rows a chunk ahead into L2 (8 members ahead, per member: 2.94 vs 2.60 ms)
+        if (P1.idx != OWN_INF && !(diag & 8u)) warm_rows<S>(db, P1.t, P1.q);
+        load_full(M, P2);
+        load_meta(K, M);
+        K = load_key(base + 128);
+    }
+    if (lane == 0) atomicMax(&sc[SC_MAXCHAIN], len);
 }
 
 // =====================================================================================

@@ -503,7 +503,7 @@ gputx_status spine_rank(gputx_db* db) {
     }
     const uint64_t n = db->n;
     CK(dev_fill_multi(s, {fseg(db->d_D, 0xFF, n * 4), fseg(db->d_lcnt, 0, (n + 1) * 4), fseg(db->d_lfill, 0, n * 4),
-                          fseg(db->d_sc + SC_NCHAIN, 0, 4), fseg(db->d_cpub, 0, S == S_TPCB ? n : 0)}));
+                          fseg(db->d_sc + SC_NCHAIN, 0, 4), fseg(db->d_cpub, 0, S != S_MICRO ? n : 0)}));
     ++db->launches;
     ++db->epoch;
     const uint32_t tiles = (uint32_t)((db->max_rec + SC_TILE - 1) / SC_TILE);
@@ -514,7 +514,7 @@ gputx_status spine_rank(gputx_db* db) {
     scan_u32(db, db->d_lcnt, db->d_loff, nullptr, n, nullptr);
     sp_fill_kernel<S><<<g, 256, 0, s>>>(db->d_sorted, db->d_sc + SC_NREC, db->d_lastw, db->d_sp, db->d_loff,
                                          db->d_lfill, db->d_links, db->d_heads, db->d_sc + SC_NCHAIN,
-                                         S == S_TPCB ? db->d_cpub : nullptr);
+                                         S != S_MICRO ? db->d_cpub : nullptr);
     db->launches += 3;
     const uint64_t* keys = db->d_sorted;
     const uint32_t* nrec = db->d_sc + SC_NREC;
@@ -752,10 +752,19 @@ bool kset_use_dataflow(const gputx_db* db) {
 
 // K-SET part 2: group by (depth, type), then the k-set rounds
 // K-SET over spine chains (TPC-B): one thread per chain, no group step (kernels.cuh)
+// an upper bound of the spine chains: TPC-B branches; TPC-C warehouses + districts
+template <int S>
+uint64_t chain_bound(const gputx_db* db) {
+    return S == S_TPCB ? db->cfg.dims[0] : (uint64_t)db->cfg.dims[0] * (1 + db->cfg.dims[1]);
+}
+
 template <int S>
 bool kset_use_chain(const gputx_db* db) {
-    return S == S_TPCB && db->spine_ran && db->kset_own && db->kset_chain && !db->has_ts && !db->trace_rounds &&
-           !(db->kset_diag & ~(1u | 8u | 1024u | 0xFFFF0000u)) && db->cfg.dims[0] <= (uint32_t)db->chain_cap;
+    // (TPC-C: a warp per chain running whole Payments one after another was slower than the
+    // dataflow executor, 18.3 vs 12.8 ms -- its W_YTD chains serialise whole transactions)
+    return S == S_TPCB && db->spine_ran && db->kset_own && db->kset_chain && !db->has_ts &&
+           !db->trace_rounds && !(db->kset_diag & ~(1u | 8u | 1024u | 0xFFFF0000u)) &&
+           chain_bound<S>(db) <= (uint64_t)db->chain_cap;
 }
 
 template <int S>
@@ -776,7 +785,7 @@ gputx_status kset_chain_exec(gputx_db* db, const DevDb& v) {
     uint32_t* sc = db->d_sc;
     uint32_t diag = db->kset_diag;
     void* args[] = {&vv, &keys, &nrec, &heads, &nh, &loff, &links, &cpub, &done, &ep, &sc, &diag};
-    const int grid = (int)((db->cfg.dims[0] + 3) / 4);              // chains <= branches, 4 per CTA
+    const int grid = (int)((chain_bound<S>(db) + 3) / 4);           // one chain per warp, 4 per CTA
     TRY(launch_coop(db, (const void*)kset_chain_exec_kernel<S_TPCB>, std::max(1, grid), 128, args));
     ++db->launches;
     db->kset_ran_chain = true;

@@ -127,8 +127,10 @@ def rank_bytes(schema: int, records: int, passes: int, n: int) -> int:
 
 def rank_kernel_name(schema: int, add_rule: bool = False) -> str:
     """The rank kernel the library runs by default (engine.cu gputx_open_db)."""
+    if schema in (W.TPCB, W.TPCC) and not add_rule:
+        return "sp_walk_kernel"                # spine-streaming rank (one pass)
     if schema == W.TPCB:
-        return "rank_kernel" if add_rule else "rank_root_kernel"
+        return "rank_kernel"
     return {W.TM1: "rank_stream_tm1_kernel", W.TPCC: "rank_window_kernel"}[schema]
 
 
@@ -616,8 +618,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         # owner-local rounds (TM-1 / TPC-B / micro default, stats flag 4) run kset_own_exec_kernel
         fl = last.get("flags", 0)
         ek = (("tpl_exec_warp_kernel" if wl["schema"] == W.TPCC else "tpl_exec_persistent_kernel")
-              if eff == "kset" and (fl & 2) else "kset_own_exec_kernel" if eff == "kset" and (fl & 4)
-              else f"{eff}_exec_kernel")
+              if eff == "kset" and (fl & 2) else "kset_chain_exec_kernel" if eff == "kset" and (fl & 16)
+              else "kset_own_exec_kernel" if eff == "kset" and (fl & 4) else f"{eff}_exec_kernel")
         cand[ek] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1]) if cand else None
     roofline = None

@@ -2098,6 +2098,7 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
     const uint32_t lane = lane_id();
     const uint32_t nw = gridDim.x * (blockDim.x >> 5), w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nrec = *nrec_ptr, nh = *nheads_ptr;
+    if (w == 0 && lane == 0) sc[SC_PASSES] = 1;          // one streaming pass (stats)
     if (w >= nh) return;
     SpinWatch wd;
     uint32_t left = 0;                                   // chains of this warp not finished

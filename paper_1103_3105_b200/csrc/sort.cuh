@@ -19,7 +19,7 @@ constexpr int RS_ITEMS = 16;
 constexpr int RS_WK = 32 * RS_ITEMS;               // keys per warp
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per tile
 constexpr int RS_MAXPASS = 5;
-constexpr int RS_HIST_GRID = 296;
+constexpr int RS_HIST_GRID = 148 * 8;            // (296 blocks: 160 us for 12 M keys, latency-bound)
 constexpr int RS_LB = 8;                           // look-back window (tiles per round trip)
 
 struct SortWs {

@@ -239,6 +239,7 @@ struct gputx_db {
     // owner-local K-SET rounds: GPUTX_KSET_OWN=0 restores the global rounds
     int kset_own = 1;
     int kset_chain = 1;                // TPC-B: K-SET over spine chains (GPUTX_KSET_CHAIN=0: owner warps)
+    int own_pipe = 1;                  // owner-local rounds staged through the perm (GPUTX_OWN_PIPE=0: gather pass)
     bool kset_ran_own = false;
     int own_grid[2] = {0, 0};          // co-resident CTAs of the executor without / with waits
     uint32_t own_g = 0, own_nw = 0;    // this bulk's executor grid and owner warps
@@ -684,7 +685,10 @@ gputx_status own_prepare(gputx_db* db) {
     int& gridv = db->own_grid[dep ? 1 : 0];
     if (!gridv) {
         int per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dep ? own_fn<S, true>() : own_fn<S, false>(), 256, 0);
+        const void* fn = db->own_pipe ? (dep ? (const void*)kset_own_pipe_kernel<S, kset_pw<S>(), true>
+                                             : (const void*)kset_own_pipe_kernel<S, kset_pw<S>(), false>)
+                                      : (dep ? own_fn<S, true>() : own_fn<S, false>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0);
         gridv = std::max(1, per) * db->nsm;
         gridv = std::min<int>(gridv, OWN_MAXW / 8);
     }
@@ -717,6 +721,28 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     uint64_t* sk = radix_sort_u64(kb, tmp, db->d_sc + SC_NTXN, n, 32, bits_for(NW - 1), db->sort_ws, db->epoch, s);
     db->launches += 2 + (bits_for(NW - 1) + 7) / 8;
     constexpr int PW = kset_pw<S>();
+    if (db->own_pipe) {                          // no gather: the executor stages through the perm
+        own_bounds_kernel<<<grid_for(NW + 1, 256, 148), 256, 0, s>>>(sk, n, NW, db->d_perm, db->d_D, db->d_oseg,
+                                                                    db->d_prog);
+        ++db->launches;
+        STAGE("own group");
+        cudaEventRecord(db->ev[5], s);
+        DevDb vv = v;
+        const uint32_t* oseg = db->d_oseg;
+        const uint64_t* skp = sk;
+        const uint32_t* perm = db->d_perm;
+        const uint32_t* Dp = db->d_D;
+        const unsigned long long* wt = dep ? db->d_wait : nullptr;
+        const uint8_t* pb = dep ? db->d_pub : nullptr;
+        uint32_t* prog = db->d_prog;
+        uint32_t* sc = db->d_sc;
+        void* args[] = {&vv, &oseg, &skp, &perm, &Dp, &wt, &pb, &prog, &sc, &diag};
+        const void* fn = dep ? (const void*)kset_own_pipe_kernel<S, kset_pw<S>(), true>
+                             : (const void*)kset_own_pipe_kernel<S, kset_pw<S>(), false>;
+        TRY(launch_coop(db, fn, (int)G, 256, args));
+        ++db->launches;
+        return GPUTX_OK;
+    }
     own_gather_kernel<PW><<<g, 256, 0, s>>>(v, sk, n, NW, db->d_perm, db->d_D, dep ? db->d_wait : nullptr,
                                             dep ? db->d_pub : nullptr, db->d_done, db->d_ptype, db->d_pp, db->d_cnt,
                                             dep ? db->d_owait : nullptr, db->d_oseg, db->d_prog,
@@ -1642,6 +1668,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_DF")) db->kset_df = atoi(e);
     if (const char* e = getenv("GPUTX_KSET_OWN")) db->kset_own = atoi(e);
     if (const char* e = getenv("GPUTX_KSET_CHAIN")) db->kset_chain = atoi(e);
+    if (const char* e = getenv("GPUTX_OWN_PIPE")) db->own_pipe = atoi(e);
     // diag 16384 (tests: arbitrary owners) needs (item, ts)-sorted records for the dependency pass
     if (schema == S_TM1 && (db->kset_diag & 16384u)) db->rank_stream = 0;
     if (const char* e = getenv("GPUTX_KSET_DF_AHEAD")) db->kset_df_ahead = (uint32_t)atoi(e);

@@ -1951,6 +1951,172 @@ __global__ void __launch_bounds__(256) kset_own_exec_kernel(DevDb db, const uint
     }
 }
 
+// Owner segments (and every warp's initial progress) straight from the owner-sorted keys
+// (owner << 32 | position in the (depth, type) order): for the executor that stages its
+// own entries through the perm (kset_own_pipe_kernel), no gather pass.
+__global__ void __launch_bounds__(256) own_bounds_kernel(const uint64_t* __restrict__ skeys, uint32_t n,
+                                                         uint32_t nw, const uint32_t* __restrict__ perm,
+                                                         const uint32_t* __restrict__ D, uint32_t* oseg,
+                                                         uint32_t* prog) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w <= nw; w += gridDim.x * blockDim.x) {
+        uint32_t a = 0, b = n;
+        while (a < b) {
+            const uint32_t m = (a + b) >> 1;
+            if ((uint32_t)(skeys[m] >> 32) < w) a = m + 1; else b = m;
+        }
+        oseg[w] = a;
+        if (w < nw) {
+            const bool any = a < n && (uint32_t)(skeys[a] >> 32) == w;
+            prog[w] = any ? D[perm[(uint32_t)skeys[a]]] : OWN_INF;
+        }
+    }
+}
+
+// kset_own_exec_kernel without the gather pass: the warp stages its own entries in four
+// register stages a chunk of 32 apart -- owner-sorted key -> perm -> (type, offset, depth,
+// output offset, wait) -> parameters -- so every stage's loads have a chunk of rounds to land
+// (the gather kernel's random reads, 44 us on TM-1, are spread over the rounds instead).
+template <int S, int PW, bool DEP>
+__global__ void __launch_bounds__(256) kset_own_pipe_kernel(DevDb db, const uint32_t* __restrict__ oseg,
+                                                            const uint64_t* __restrict__ skeys,
+                                                            const uint32_t* __restrict__ perm,
+                                                            const uint32_t* __restrict__ D,
+                                                            const unsigned long long* __restrict__ wait,
+                                                            const uint8_t* __restrict__ pub,
+                                                            uint32_t* prog, uint32_t* sc, uint32_t diag) {
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    constexpr int NP = PW > 0 ? PW : 1;
+    const uint32_t lane = lane_id();
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t lo = oseg[w], hi = oseg[w + 1];
+    if (lo >= hi || bulk_failed(db)) return;
+    const bool gmode = DEP && __ldcg(&sc[SC_OWNGLOBAL]) != 0u;
+    struct E {
+        uint32_t idx, t, d, oo;          // d: depth | OWN_PUB; INF past the segment
+        unsigned long long wt;
+        uint32_t q[NP];
+    };
+    struct Meta { uint32_t idx, t, o, d, oo; unsigned long long wt; };
+    // stage loads (lane l: entry base + l)
+    auto st_key = [&](uint32_t base) -> uint32_t {          // -> position in perm, or INF
+        const uint32_t j = base + lane;
+        return j < hi ? (uint32_t)__ldg(&skeys[j]) : OWN_INF;
+    };
+    auto st_idx = [&](uint32_t pos) -> uint32_t { return pos != OWN_INF ? __ldg(&perm[pos]) : OWN_INF; };
+    auto st_meta2 = [&](uint32_t idx, const uint32_t* Dd, Meta& m) {
+        m.idx = idx; m.t = 0; m.o = 0; m.d = OWN_INF; m.oo = OUT_AUTO; m.wt = 0;
+        if (idx == OWN_INF) return;
+        m.t = db.type[idx];
+        m.o = db.poff[idx];
+        m.d = Dd[idx] | (DEP && pub[idx] ? OWN_PUB : 0u);
+        m.oo = db.out_off ? db.out_off[idx] : OUT_AUTO;
+        if (DEP) m.wt = wait[idx];
+    };
+    auto st_full = [&](const Meta& m, E& e) {
+        e.idx = m.idx; e.t = m.t; e.d = m.d; e.oo = m.oo; e.wt = m.wt;
+#pragma unroll
+        for (int x = 0; x < NP; ++x) e.q[x] = 0;
+        if (m.idx == OWN_INF || PW == 0) return;
+        const uint32_t* p = db.pw + m.o;
+#pragma unroll
+        for (int x = 0; x < NP; ++x) e.q[x] = p[x];
+    };
+    // prologue: chunks 0, 1 complete; 2 meta; 3 idx; 4 key
+    E A, B;
+    Meta M2;
+    uint32_t I3, K4;
+    {
+        Meta m0, m1;
+        st_meta2(st_idx(st_key(lo)), D, m0);
+        st_meta2(st_idx(st_key(lo + 32)), D, m1);
+        st_full(m0, A);
+        st_full(m1, B);
+        st_meta2(st_idx(st_key(lo + 64)), D, M2);
+        I3 = st_idx(st_key(lo + 96));
+        K4 = st_key(lo + 128);
+    }
+    E C;
+    st_full(M2, C);                              // chunk 2's parameters in flight
+    st_meta2(I3, D, M2);                         // chunk 3's metadata in flight
+    I3 = st_idx(K4);                             // chunk 4's perm entries in flight
+    K4 = st_key(lo + 160);                       // chunk 5's keys in flight
+    if (PW > 0 && B.idx != OWN_INF) warm_rows<S>(db, B.t, B.q);
+    auto pick = [&](const E& a, const E& b, uint32_t src, E& x) {
+        const uint32_t sl = src & 31u;
+        const bool fa = src < 32u;
+        uint32_t u, v;
+        u = __shfl_sync(FULL, a.idx, sl); v = __shfl_sync(FULL, b.idx, sl); x.idx = fa ? u : v;
+        u = __shfl_sync(FULL, a.t, sl);   v = __shfl_sync(FULL, b.t, sl);   x.t = fa ? u : v;
+        u = __shfl_sync(FULL, a.d, sl);   v = __shfl_sync(FULL, b.d, sl);   x.d = fa ? u : v;
+        u = __shfl_sync(FULL, a.oo, sl);  v = __shfl_sync(FULL, b.oo, sl);  x.oo = fa ? u : v;
+        if (DEP) {
+            const unsigned long long ua = __shfl_sync(FULL, a.wt, sl), ub = __shfl_sync(FULL, b.wt, sl);
+            x.wt = fa ? ua : ub;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            u = __shfl_sync(FULL, a.q[k], sl); v = __shfl_sync(FULL, b.q[k], sl); x.q[k] = fa ? u : v;
+        }
+    };
+    auto depth_at = [&](const E& a, const E& b, uint32_t p) -> uint32_t {
+        const uint32_t u = __shfl_sync(FULL, a.d, p & 31u), v = __shfl_sync(FULL, b.d, p & 31u);
+        return (p < 32u ? u : v) & ~OWN_PUB;
+    };
+    uint32_t ca = lo, p = 0;
+    bool pubr = false;
+    uint32_t d0 = depth_at(A, B, 0);
+    while (ca + p < hi) {
+        E X;
+        pick(A, B, p + lane, X);
+        const uint32_t xd = X.d & ~OWN_PUB;
+        const uint32_t cnt = __popc(__ballot_sync(FULL, xd == d0));
+        if (lane < cnt) {
+            if (DEP && X.wt) {
+                SpinWatch wd;
+                if (X.wt == OWN_GLOBAL) {
+                    for (uint32_t q = 0; q < nw; ++q) {
+                        if (q == w) continue;
+                        while (ld_acquire(&prog[q]) < d0)
+                            if (wd.expired(&sc[SC_DEADLOCK])) break;
+                    }
+                } else {
+                    const uint32_t ow = (uint32_t)(X.wt >> 32), need = (uint32_t)X.wt;
+                    uint32_t spins = 0;
+                    while (ld_acquire(&prog[ow]) < need) {
+                        if (++spins > 16) __nanosleep(64);
+                        if (wd.expired(&sc[SC_DEADLOCK])) break;
+                    }
+                }
+            }
+            kx_jitter(diag, d0, w, lane);
+            exec_txn_p<S, false>(db, X.idx, X.t, X.q, X.oo);
+        }
+        if (DEP) pubr |= __ballot_sync(FULL, lane < cnt && (X.d & OWN_PUB)) != 0u;
+        p += cnt;
+        if (p >= 32u) {                          // A consumed: advance every stage by a chunk
+            A = B;
+            B = C;
+            ca += 32;
+            p -= 32;
+            st_full(M2, C);
+            st_meta2(I3, D, M2);
+            I3 = st_idx(K4);
+            K4 = st_key(ca + 160);
+            if (PW > 0 && B.idx != OWN_INF) warm_rows<S>(db, B.t, B.q);
+        }
+        const uint32_t dn = ca + p < hi ? depth_at(A, B, p) : OWN_INF;
+        if (dn != d0) {
+            const bool publish = DEP && (pubr || gmode);
+            if (publish) __threadfence();
+            __syncwarp();
+            if (publish && lane == 0) st_release(&prog[w], dn);
+            pubr = false;
+            d0 = dn;
+        }
+    }
+}
+
 // =====================================================================================
 // Spine-streaming rank (DESIGN.md §4 "Spine-streaming rank"): every transaction of TPC-B,
 // TPC-C and micro writes one *spine* item that only its own kind writes (TPC-B its branch

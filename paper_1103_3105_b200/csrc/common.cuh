@@ -353,5 +353,10 @@ struct OpAddU32 {
     static DEV uint32_t identity() { return 0u; }
     static DEV uint32_t combine(uint32_t a, uint32_t b) { return a + b; }
 };
+// two independent u32 sums side by side (one scan for two per-transaction counts)
+struct OpAddU2 {
+    static DEV uint2 identity() { return make_uint2(0u, 0u); }
+    static DEV uint2 combine(uint2 a, uint2 b) { return make_uint2(a.x + b.x, a.y + b.y); }
+};
 
 }  // namespace gputx

@@ -127,6 +127,8 @@ struct gputx_db {
     uint8_t* d_status = nullptr;
     uint8_t* d_out = nullptr;
     bool packed = false;               // GPUTX_FLAG_PACKED_OUT
+    bool rec_at_ingest = false;        // this submit counted the access records (emit skips its count pass)
+    LookBack<uint2> lb_scan2{};        // paired scan (output sizes + record counts)
     uint32_t* d_out_off = nullptr;     // packed record offsets [n + 1]
     uint64_t out_bytes = 0;            // the submitted bulk's output bytes (packed: out_off[n])
     uint32_t out_stride = 0;
@@ -378,6 +380,16 @@ void scan_u32(gputx_db* db, const uint32_t* in, uint32_t* out, const uint32_t* n
                                                      ++db->launches;
 }
 
+// exclusive scans of two u32 arrays in one pass; outX[n], outY[n] and the totals set
+void scan2_u32(gputx_db* db, const uint32_t* inX, const uint32_t* inY, uint32_t* outX, uint32_t* outY, uint64_t n,
+               uint32_t* totX, uint32_t* totY) {
+    const uint32_t grid = (uint32_t)((n + SC_TILE) / SC_TILE);
+    ++db->epoch;
+    scan2_kernel<<<grid, SC_THREADS, 0, db->stream>>>(inX, inY, outX, outY, (uint32_t)n, db->lb_scan2, db->epoch,
+                                                      next_ticket(db), totX, totY);
+    ++db->launches;
+}
+
 DevDb make_devdb(gputx_db* db) {
     DevDb v{};
     v.schema = db->schema;
@@ -462,9 +474,11 @@ template <int S> const void* kset_fn(bool sh) {
 template <int S>
 gputx_status emit_records(gputx_db* db, const DevDb& v) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
-    emit_count_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_cnt);
-    ++db->launches;
-    scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NREC);
+    if (!db->rec_at_ingest) {                 // (counted and scanned at submit otherwise)
+        emit_count_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_cnt);
+        ++db->launches;
+        scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, db->n, db->d_sc + SC_NREC);
+    }
     emit_write_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_rec_off, db->d_rec_a);
     ++db->launches;
     return GPUTX_OK;
@@ -1137,7 +1151,8 @@ void launch_ingest(gputx_db* db, uint32_t n_words, const uint32_t* nw_ptr) {
     const uint32_t g = grid_for(db->n, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, db->stream>>>(v, db->d_pw, n_words, nw_ptr, db->type_mask, db->d_ins_off,
                                                 (uint32_t)(db->n + 1), db->d_sc, db->d_xflag,
-                                                db->packed ? db->d_out_off : nullptr);
+                                                db->packed ? db->d_out_off : nullptr,
+                                                db->rec_at_ingest ? db->d_cnt : nullptr);
                                                 ++db->launches;
 }
 
@@ -1175,6 +1190,7 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
             copy_pw_kernel<<<148 * 4, 256, 0, s>>>(pw_src, nw_ptr, db->d_pw, n_words, db->d_sc);
             ++db->launches;
         }
+        db->rec_at_ingest = db->nshards == 1;      // (sharded emits count their local records)
         if (db->schema == S_TPCB) launch_ingest<S_TPCB>(db, n_words, nw_ptr);
         else if (db->schema == S_TM1) launch_ingest<S_TM1>(db, n_words, nw_ptr);
         else if (db->schema == S_MICRO) launch_ingest<S_MICRO>(db, n_words, nw_ptr);
@@ -1183,7 +1199,13 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
             for (int t = 0; t < ntab; ++t)
                 scan_u32(db, db->d_ins_off + t * (n + 1), db->d_ins_off + t * (n + 1), nullptr, n,
                          db->d_sc + SC_INS0 + t);
-        if (db->packed) scan_u32(db, db->d_out_off, db->d_out_off, nullptr, n, db->d_sc + SC_OUTBYTES);
+        if (db->rec_at_ingest && db->packed)
+            scan2_u32(db, db->d_out_off, db->d_cnt, db->d_out_off, db->d_rec_off, n, db->d_sc + SC_OUTBYTES,
+                      db->d_sc + SC_NREC);
+        else if (db->rec_at_ingest)
+            scan_u32(db, db->d_cnt, db->d_rec_off, nullptr, n, db->d_sc + SC_NREC);
+        else if (db->packed)
+            scan_u32(db, db->d_out_off, db->d_out_off, nullptr, n, db->d_sc + SC_OUTBYTES);
     }
     cudaEventRecord(db->ev_sub[1], s);
     TRY(pull_sc(db, s));
@@ -1255,7 +1277,7 @@ gputx_status pool_submit_schema(gputx_db* db, uint64_t m, uint32_t words) {
     v.ts = nullptr;
     const uint32_t g = grid_for(m, 256, 148 * 16);
     ingest_kernel<S><<<g, 256, 0, s>>>(v, db->s_pw, words, nullptr, db->type_mask, db->st_ins, (uint32_t)(m + 1),
-                                       db->d_sc, nullptr, nullptr);
+                                       db->d_sc, nullptr, nullptr, nullptr);
     TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
     if (db->h_sc[SC_ERR])
@@ -1564,6 +1586,10 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     // look-back state: sized for the largest tiled pass
     // (>= 4096 entries: the rank kernel also keeps one aggregate per CTA here)
     const uint64_t tiles = std::max<uint64_t>((std::max(db->max_rec, NB * db->ntypes) + 2) / 2048 + 4, 4096);
+    if ((st = dalloc(db, &db->lb_scan2.flag, tiles)) || (st = dalloc(db, &db->lb_scan2.agg, tiles)) ||
+        (st = dalloc(db, &db->lb_scan2.inc, tiles)))
+        return bail(st);
+    dev_fill(db->lb_scan2.flag, 0, tiles * 4, db->stream);
     if ((st = dalloc(db, &db->lb_scan.flag, tiles)) || (st = dalloc(db, &db->lb_scan.agg, tiles)) ||
         (st = dalloc(db, &db->lb_scan.inc, tiles)) || (st = dalloc(db, &db->lb_rank.flag, tiles)) ||
         (st = dalloc(db, &db->lb_rank.agg, tiles)) || (st = dalloc(db, &db->lb_rank.inc, tiles)) ||
@@ -2769,6 +2795,8 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
         db->executed = false;
         CK(dev_fill_multi(s, {fseg(db->d_sc, 0, SC_ERRPK * 4), fseg(db->d_sc + SC_ERRPK, 0xFF, 8),
                               fseg(db->d_sc + SC_ERRPK + 2, 0, (SC_COUNT - SC_ERRPK - 2) * 4)}));
+        // (records counted by emit: its failed-bulk guard zeroes them and sets the poison word)
+        db->rec_at_ingest = false;
         if (n) {
             if (db->schema == S_TM1) launch_ingest<S_TM1>(db, words, nullptr);
             else launch_ingest<S_MICRO>(db, words, nullptr);
@@ -3031,6 +3059,7 @@ void gputx_close_db(gputx_db* db) {
     dfree(db, db->tm1_sub); dfree(db, db->tm1_ai); dfree(db, db->tm1_sf); dfree(db, db->tm1_cf);
     dfree(db, db->d_undo);
     dfree(db, db->d_out_off);
+    dfree(db, db->lb_scan2.flag); dfree(db, db->lb_scan2.agg); dfree(db, db->lb_scan2.inc);
     dfree(db, db->d_lastw); dfree(db, db->d_sp); dfree(db, db->d_lcnt); dfree(db, db->d_loff); dfree(db, db->d_lfill);
     dfree(db, db->d_links); dfree(db, db->d_heads); dfree(db, db->d_ccur); dfree(db, db->d_clast);
     dfree(db, db->d_cpub); dfree(db, db->d_cdone);

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(256) copy_pw_kernel(const uint32_t* __restrict
 template <int S>
 __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uint32_t n_words, const uint32_t* nw_ptr,
                                                      uint32_t type_mask, uint32_t* ins_cnt, uint32_t ins_stride,
-                                                     uint32_t* sc, uint8_t* xflag, uint32_t* out_size) {
+                                                     uint32_t* sc, uint8_t* xflag, uint32_t* out_size,
+                                                     uint32_t* rec_cnt) {
     const uint32_t n = db.n;
     if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_NTXN] = n;
     if (db.poison && __ldcg(db.poison)) {             // an earlier bulk of this run failed
@@ -162,6 +163,10 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
             }
         }
         if (out_size) out_size[i] = out_bytes<S>(t, p);            // packed outputs (scanned at submit)
+        if (rec_cnt) {                                                // access records (emit's count pass)
+            Rec rr[MAX_REC];
+            rec_cnt[i] = footprint_local<S>(db, t, p, rr);
+        }
         if (S == S_TPCB) {                                           // history rows (deposits) via ins_off
             ins_cnt[i] = (home && t == 0) ? 1u : 0u;
             if (!(home && t == 0)) atomicAdd(&sc[SC_SPARSE], 1u);       // some row is not at its idx
@@ -212,6 +217,44 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* in, ui
         if (b + k <= n) out[b + k] = run;
         if (total_out && b + k == n) *total_out = run;
         run += v[k];
+    }
+}
+
+// scan_kernel over two u32 arrays at once (packed-output sizes and access-record counts,
+// both per transaction, both computed at ingest): outX[n] / outY[n] = totals
+__global__ void __launch_bounds__(SC_THREADS) scan2_kernel(const uint32_t* inX, const uint32_t* inY, uint32_t* outX,
+                                                           uint32_t* outY, uint32_t n, LookBack<uint2> lb,
+                                                           uint32_t epoch, uint32_t* ticket, uint32_t* totX,
+                                                           uint32_t* totY) {
+    __shared__ uint2 sm[8];
+    __shared__ uint32_t s_tile;
+    __shared__ uint2 s_pre;
+    const uint32_t ntiles = (n + SC_TILE) / SC_TILE;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t b = (uint64_t)tile * SC_TILE + threadIdx.x * SC_ITEMS;
+    uint2 v[SC_ITEMS];
+    uint2 sum = make_uint2(0u, 0u);
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        v[k] = (b + k < n) ? make_uint2(inX[b + k], inY[b + k]) : make_uint2(0u, 0u);
+        sum = OpAddU2::combine(sum, v[k]);
+    }
+    uint2 tot;
+    uint2 ex = block_scan_excl<uint2, OpAddU2>(sum, tot, sm);
+    if (warp_id() == 0) {
+        uint2 pre = lookback_warp<uint2, OpAddU2>(lb, tile, epoch, tot);
+        if (lane_id() == 0) s_pre = pre;
+    }
+    __syncthreads();
+    uint2 run = OpAddU2::combine(s_pre, ex);
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        if (b + k <= n) { outX[b + k] = run.x; outY[b + k] = run.y; }
+        if (b + k == n) { *totX = run.x; *totY = run.y; }
+        run = OpAddU2::combine(run, v[k]);
     }
 }
 

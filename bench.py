@@ -417,7 +417,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     # only what the procedures return; sharded handles keep the stride
     db = Database(wl["schema"], dims.dims, max_bulk, image, device=dev.index, stream=stream.cuda_stream,
                   insert_capacity=cap, shard=rank if ws > 1 else 0, nshards=ws,
-                  add_rule=wl.get("add_rule", False), packed_out=ws == 1)
+                  add_rule=wl.get("add_rule", False), packed_out=ws == 1,
+                  deferred_check=ws == 1)      # TM-1: the validation verdict comes with execute
 
     # ---- parity gate (N = 1): bulk 0 vs the oracle, before anything is timed ----------
     parity, parity_err, ref0 = None, None, None

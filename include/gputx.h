@@ -137,6 +137,14 @@ typedef struct {
  * gputx_results_device and gputx_run_bulks then move out_off[n] bytes.  Not with sharding
  * or the transaction pool (EINVAL there). */
 #define GPUTX_FLAG_PACKED_OUT 2u
+/* GPUTX_FLAG_DEFERRED_CHECK (TM-1 and micro, unsharded): gputx_submit_bulk enqueues the
+ * validation without waiting for its verdict (no host round trip between submit and
+ * execute).  Validation errors (EINVAL, EUNKNOWN_TYPE, ECAPACITY for parameter words) are
+ * then returned by the following gputx_execute / gputx_wait instead, and the database is
+ * unchanged: K-SET's owner-local path executes a failed bulk as empty; every other strategy
+ * takes the verdict before it launches anything.  submit still returns the host-detectable
+ * errors (ESTATE, bulk larger than max_bulk, null pointers). */
+#define GPUTX_FLAG_DEFERRED_CHECK 4u
 
 typedef struct {
     const uint8_t* type;        /* u8[n]                                                */

@@ -128,6 +128,8 @@ struct gputx_db {
     uint8_t* d_out = nullptr;
     bool packed = false;               // GPUTX_FLAG_PACKED_OUT
     bool rec_at_ingest = false;        // this submit counted the access records (emit skips its count pass)
+    bool deferred = false;             // GPUTX_FLAG_DEFERRED_CHECK: this bulk's validation verdict is pending
+    bool guard = false;                // ... and its kernels treat a failed ingest as an empty bulk
     LookBack<uint2> lb_scan2{};        // paired scan (output sizes + record counts)
     uint32_t* d_out_off = nullptr;     // packed record offsets [n + 1]
     uint64_t out_bytes = 0;            // the submitted bulk's output bytes (packed: out_off[n])
@@ -420,7 +422,7 @@ DevDb make_devdb(gputx_db* db) {
     v.part_size = db->part_size;
     v.add_rule = (db->cfg.flags & GPUTX_FLAG_ADD_RULE) ? 1u : 0u;
     v.nshards = db->nshards;
-    v.err = db->pipe ? db->d_sc + SC_ERR : nullptr;
+    v.err = (db->pipe || db->guard) ? db->d_sc + SC_ERR : nullptr;
     v.poison = db->pipe ? db->d_poison : nullptr;
     v.shard = db->shard;
     v.nroot = db->nroot;
@@ -862,7 +864,7 @@ gputx_status kset_exec(gputx_db* db, const DevDb& v) {
         TRY(own_prepare<S>(db));
         const bool dep = S == S_TPCB || (db->kset_diag & 16384u);
         OwnKeys ok{db->own_nw, db->d_sorted == db->d_rec_a ? db->d_rec_b : db->d_rec_a, dep ? db->d_own : nullptr,
-                   db->kset_diag, db->pipe ? db->d_sc + SC_ERR : nullptr};
+                   db->kset_diag, (db->pipe || db->guard) ? db->d_sc + SC_ERR : nullptr};
         group_kernel<1, 0, S><<<gg, 256, 0, s>>>(db->d_D, db->d_type, (uint32_t)db->n, T, db->d_gcnt, db->d_goff,
                                                  db->d_perm, db->d_poff, db->d_pw, nullptr, nullptr, P, ok);
     } else
@@ -1170,8 +1172,16 @@ gputx_status submit_check(gputx_db* db, const gputx_bulk* b) {
 // lookups, count insert rows
 // pw_src (device, optional): the caller's parameter words, copied here with their count
 // read on the device from d_poff[n] (n_words is then ignored)
+gputx_status submit_verdict(gputx_db* db);
+
 gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uint32_t* pw_src = nullptr) {
     cudaStream_t s = db->stream;
+    // GPUTX_FLAG_DEFERRED_CHECK (TM-1 / micro, unsharded): no host round trip here; the
+    // verdict is taken at execute (include/gputx.h)
+    const bool defer = (db->cfg.flags & GPUTX_FLAG_DEFERRED_CHECK) && db->nshards == 1 && !db->has_ts &&
+                       (db->schema == S_TM1 || db->schema == S_MICRO);
+    db->deferred = defer;
+    db->guard = defer;
     db->n = n;
     db->launches = 0;
     db->has_depth = db->has_perm = false;
@@ -1208,8 +1218,21 @@ gputx_status finish_submit(gputx_db* db, uint64_t n, uint32_t n_words, const uin
             scan_u32(db, db->d_out_off, db->d_out_off, nullptr, n, db->d_sc + SC_OUTBYTES);
     }
     cudaEventRecord(db->ev_sub[1], s);
+    if (defer) {
+        db->ins_dense = false;
+        db->out_bytes = n * db->out_stride;   // (an upper bound until the verdict: zero-fill size)
+        for (auto& t : db->ins) t.pending = 0;
+        db->submitted = true;
+        return GPUTX_OK;
+    }
     TRY(pull_sc(db, s));
     CK(cudaStreamSynchronize(s));
+    return submit_verdict(db);
+}
+
+// the host half of a submit: validation errors, insert-table capacity (h_sc is current)
+gputx_status submit_verdict(gputx_db* db) {
+    const uint64_t n = db->n;
     if (db->h_sc[SC_ERR]) {
         static const char* what[] = {"", "type id out of range", "type not registered", "wrong parameter count",
                                      "parameter out of range", "bad param_off", "timestamps not increasing",
@@ -2305,6 +2328,24 @@ gputx_status execute_launch(gputx_db* db, gputx_strategy st) {
         return fail(db, GPUTX_EINVAL, "bad strategy");
     if ((st == GPUTX_TPL_RELAXED || st == GPUTX_PART_RELAXED) && db->nshards > 1)
         return fail(db, GPUTX_EINVAL, "relaxed strategies are single-GPU");
+    if (db->deferred) {
+        // only K-SET's owner-local path guards every parameter read against a failed ingest;
+        // any other execution takes the verdict first (the round trip the flag saves)
+        const bool guarded = st == GPUTX_KSET && (db->schema == S_TM1 ? kset_use_own<S_TM1>(db)
+                                                                       : kset_use_own<S_MICRO>(db));
+        if (!guarded) {
+            db->guard = false;
+            db->deferred = false;
+            TRY(pull_sc(db, db->stream));
+            CK(cudaStreamSynchronize(db->stream));
+            const gputx_status vs = submit_verdict(db);
+            if (vs != GPUTX_OK) {                  // (the failed bulk takes no timestamps)
+                db->submitted = false;
+                if (!db->has_ts) db->next_ts = db->first_ts;
+                return vs;
+            }
+        }
+    }
     db->has_order = false;
     db->chosen = st == GPUTX_AUTO ? (int)GPUTX_KSET : (int)st;   // AUTO: overwritten by run_auto
     cudaStream_t s = db->stream;
@@ -2346,6 +2387,18 @@ gputx_status execute_finish(gputx_db* db, gputx_stats* stats) {
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     if (db->schema == S_TM1 && n) db->rows_dirty = true;
+    if (db->deferred) {                        // the submit's verdict (the bulk ran as empty if it failed)
+        db->deferred = false;
+        db->guard = false;
+        const gputx_status vs = submit_verdict(db);
+        db->submitted = false;
+        if (vs != GPUTX_OK) {
+            db->executed = false;
+            if (!db->has_ts) db->next_ts = db->first_ts;   // (the failed bulk takes no timestamps)
+            return vs;
+        }
+        db->out_bytes = db->packed ? (uint64_t)db->h_sc[SC_OUTBYTES] : n * db->out_stride;
+    }
     const bool ranked = (st == GPUTX_KSET || st == GPUTX_AUTO) && n;
     const gputx_strategy eff = (gputx_strategy)db->chosen;
     if (ranked) db->rank_epoch += db->h_sc[SC_PASSES] + 1;
@@ -2752,7 +2805,7 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
     }
     if (!db->d_poison) TRY(dalloc(db, &db->d_poison, 1));
     CK(dev_fill(db->d_poison, 0, 4, s));
-    std::vector<uint64_t> nb(k), ob(k);
+    std::vector<uint64_t> nb(k), ob(k), fts(k);
     auto h2d = [&](uint64_t i) -> gputx_status {
         const gputx_bulk& b = bulks[i];
         const int sl = (int)(i & 1);
@@ -2789,6 +2842,7 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
         // submit without the round trip (finish_submit's device half)
         db->has_ts = false;
         db->first_ts = db->next_ts;
+        fts[i] = db->first_ts;
         db->n = n;
         db->launches = 0;
         db->has_depth = db->has_perm = false;
@@ -2847,6 +2901,7 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
             db->n = 0;
             db->submitted = false;
             db->executed = false;
+            db->next_ts = fts[i];              // the failed bulk and the ones after it take no ts
             return fail(db, e <= 2 ? GPUTX_EUNKNOWN_TYPE : GPUTX_EINVAL,
                         "bulk " + std::to_string(i) + ", transaction " + std::to_string(bad) + ": " +
                             what[e <= 9 ? e : 0]);
@@ -3025,6 +3080,7 @@ gputx_status gputx_reset(gputx_db* db) {
     db->poisoned = false;
     db->submitted = false;
     db->executed = false;
+    db->deferred = db->guard = false;
     db->next_ts = 0;
     db->pool_n = db->pool_words = db->pool_nrec = db->pool_exec = 0;
     return GPUTX_OK;

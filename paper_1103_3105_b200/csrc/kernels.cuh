@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
     }
     if (nw_ptr) n_words = min(__ldg(nw_ptr), n_words);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        // an invalid transaction keeps no records and no output bytes (a deferred verdict
+        // runs the rest of the bulk's generation on the valid ones)
+        if (out_size) out_size[i] = 0;
+        if (rec_cnt) rec_cnt[i] = 0;
         const uint32_t t = db.type[i];
         // sharded: a peer's transaction (NOT_HOME) only runs its fragments on this shard
         const bool home = !db.src || db.src[i] != NOT_HOME;
@@ -273,8 +277,10 @@ __global__ void __launch_bounds__(256) emit_count_kernel(DevDb db, uint32_t* cnt
 
 template <int S>
 __global__ void __launch_bounds__(256) emit_write_kernel(DevDb db, const uint32_t* __restrict__ off, uint64_t* keys) {
-    if (bulk_failed(db)) return;
+    // a failed bulk (guarded modes): only the transactions that kept records are valid ones
+    const bool failed = bulk_failed(db);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < db.n; i += gridDim.x * blockDim.x) {
+        if (failed && off[i + 1] == off[i]) continue;
         Rec r[MAX_REC];
         const int k = footprint_local<S>(db, db.type[i], db.pw + db.poff[i], r);
         uint64_t* dst = keys + off[i];

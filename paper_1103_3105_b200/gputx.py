@@ -23,6 +23,7 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EDUP_TYPE", 4: "EUNKNOWN_
 OUT_STRIDE = {1: 8, 2: 40, 3: 200, 4: 4}
 FLAG_ADD_RULE = 1            # include/gputx.h GPUTX_FLAG_ADD_RULE
 FLAG_PACKED_OUT = 2          # include/gputx.h GPUTX_FLAG_PACKED_OUT
+FLAG_DEFERRED_CHECK = 4      # include/gputx.h GPUTX_FLAG_DEFERRED_CHECK
 
 
 class GputxError(RuntimeError):
@@ -203,7 +204,8 @@ class Database:
 
     def __init__(self, schema: int, dims, max_bulk: int, image: dict | None = None, *, part_size: int = 0,
                  device: int = 0, stream: int | None = None, insert_capacity: int = 0, shard: int = 0,
-                 nshards: int = 1, add_rule: bool = False, torch_memory: bool = False, packed_out: bool = False):
+                 nshards: int = 1, add_rule: bool = False, torch_memory: bool = False, packed_out: bool = False,
+                 deferred_check: bool = False):
         self.lib = load_library()
         self.schema = schema
         cfg = Config()
@@ -215,7 +217,8 @@ class Database:
         cfg.part_size = int(part_size)
         cfg.device = int(device)
         cfg.stream = stream
-        cfg.flags = (FLAG_ADD_RULE if add_rule else 0) | (FLAG_PACKED_OUT if packed_out else 0)
+        cfg.flags = ((FLAG_ADD_RULE if add_rule else 0) | (FLAG_PACKED_OUT if packed_out else 0) |
+                     (FLAG_DEFERRED_CHECK if deferred_check else 0))
         self.packed = bool(packed_out)
         cfg.shard = int(shard)
         cfg.nshards = int(nshards)

@@ -620,7 +620,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         fl = last.get("flags", 0)
         ek = (("tpl_exec_warp_kernel" if wl["schema"] == W.TPCC else "tpl_exec_persistent_kernel")
               if eff == "kset" and (fl & 2) else "kset_chain_exec_kernel" if eff == "kset" and (fl & 16)
-              else "kset_own_exec_kernel" if eff == "kset" and (fl & 4) else f"{eff}_exec_kernel")
+              else "kset_own_pipe_kernel" if eff == "kset" and (fl & 4) else f"{eff}_exec_kernel")
         cand[ek] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
     kname = max(cand, key=lambda k: cand[k][1]) if cand else None
     roofline = None

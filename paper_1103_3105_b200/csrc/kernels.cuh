@@ -2330,6 +2330,7 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
             if (p == SP_UNSET) continue;                 // finished
             const uint64_t item = key_item(keys[heads[c]]);
             int32_t ld = __ldcg(&last[c]);
+            const bool alone = nh <= nw;                 // this warp's only chain: wait in place
             while (true) {
                 const uint32_t r = p + lane;
                 bool mem = false;
@@ -2347,37 +2348,50 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
                     progress = true;
                     break;
                 }
-                // e = max over links of D[p] + 1 (or -1); blocked if some link's depth is not there yet
+                // e = max over links of D[p] + 1 (or -1); a lane is blocked while some link's depth
+                // is not there yet.  Lanes [s0, clen) of the chunk are pending; a blocked chunk is
+                // re-polled in place (only the unresolved links), not reloaded: a hop between two
+                // chains then costs one L2 round trip
+                uint32_t x = 0, xe = 0;
+                if (lane < clen) { x = loff[t]; xe = loff[t + 1]; }
                 int32_t e = -1;
-                bool blocked = false;
-                if (lane < clen) {
-                    const uint32_t a = loff[t], b2 = loff[t + 1];
-                    for (uint32_t x = a; x < b2; ++x) {
-                        const uint32_t dp = __ldcg(&D[__ldg(&links[x])]);
-                        if (dp == SP_UNSET) { blocked = true; break; }
-                        e = max(e, (int32_t)dp + 1);
+                uint32_t s0 = 0, spins = 0;
+                while (true) {
+                    bool blocked = false;
+                    if (lane >= s0 && lane < clen) {
+                        for (; x < xe; ++x) {
+                            const uint32_t dp = __ldcg(&D[__ldg(&links[x])]);
+                            if (dp == SP_UNSET) { blocked = true; break; }
+                            e = max(e, (int32_t)dp + 1);
+                        }
+                    }
+                    const uint32_t bm = __ballot_sync(FULL, blocked);
+                    const uint32_t k = bm ? __ffs(bm) - 1 : clen;                   // lanes [s0, k) proceed
+                    if (k > s0) {
+                        // D_l = max(ld + 1 + (l - s0), max_{s0 <= m <= l} (e_m - m) + l)   (max-plus scan)
+                        int32_t v = (lane >= s0 && lane < k) ? e - (int32_t)lane : -0x3FFFFFFF;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int32_t y = __shfl_up_sync(FULL, v, o);
+                            if ((int)lane >= o) v = max(v, y);
+                        }
+                        const int32_t dl = max(ld + 1 + (int32_t)lane - (int32_t)s0, v + (int32_t)lane);
+                        if (lane >= s0 && lane < k) __stcg(&D[t], (uint32_t)dl);
+                        ld = __shfl_sync(FULL, dl, k - 1);
+                        s0 = k;
+                        progress = true;
+                        spins = 0;
+                    }
+                    if (s0 == clen) break;
+                    if (!alone && ++spins > 4) break;    // other chains of this warp may unblock it
+                    if (alone && ++spins > 64) {
+                        __nanosleep(64);
+                        if (wd.expired(&sc[SC_DEADLOCK])) break;
                     }
                 }
-                const uint32_t bm = __ballot_sync(FULL, blocked && lane < clen);
-                const uint32_t k = bm ? __ffs(bm) - 1 : clen;                       // lanes [0, k) proceed
-                // D_l = max(ld + 1 + l, max_{m <= l} (e_m - m) + l)   (max-plus scan)
-                int32_t v = lane < k ? e - (int32_t)lane : -0x3FFFFFFF;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(FULL, v, o);
-                    if ((int)lane >= o) v = max(v, y);
-                }
-                const int32_t dl = max(ld + 1 + (int32_t)lane, v + (int32_t)lane);
-                if (lane < k) __stcg(&D[t], (uint32_t)dl);
-                if (k) {
-                    ld = __shfl_sync(FULL, dl, k - 1);
-                    p += k;
-                    progress = true;
-                }
-                if (k < 32) {                            // blocked (or the chain ended inside)
-                    if (k == clen && clen < 32) continue;   // ended: the next iteration sees clen = 0
-                    break;
-                }
+                p += s0;
+                if (s0 < clen) break;                    // blocked: yield (or give up on the watchdog)
+                if (clen < 32) continue;                 // ended inside: the next iteration sees clen = 0
             }
             if (lane == 0 && __ldcg(&cur[c]) != SP_UNSET) { cur[c] = p; last[c] = ld; }
             __syncwarp();

@@ -3161,7 +3161,11 @@ __global__ void __launch_bounds__(128) tpl_exec_warp_kernel(DevDb db, const uint
                 __nanosleep(key - v == 1 ? (n > 8 ? 32u : 0u) : min((key - v) * 32u, g_tpl_sleep_cap));
             }
             if (ok) red_add(&COL(int64_t, C_W_YTD)[p[0]], (int64_t)p[6]);
-            red_add_release(&lock[item], 1u);
+            // the W_YTD turn passes without a release fence: the access it orders is a blind
+            // atomic add (no transaction reads W_YTD), so the next holder needs the turn, not the
+            // visibility of this add -- the hand-off of the ~6,700-Payment W_YTD chains loses the
+            // fence's wait for the add's acknowledgement
+            atomicAdd(&lock[item], 1u);
             if (thr.on()) atomicAdd(&thr.done[__ldg(&thr.D[idx])], 1u);
         }
         return;

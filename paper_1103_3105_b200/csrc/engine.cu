@@ -738,7 +738,7 @@ gputx_status kset_own_exec(gputx_db* db, const DevDb& v) {
     db->launches += 2 + (bits_for(NW - 1) + 7) / 8;
     constexpr int PW = kset_pw<S>();
     if (db->own_pipe) {                          // no gather: the executor stages through the perm
-        own_bounds_kernel<<<grid_for(NW + 1, 256, 148), 256, 0, s>>>(sk, n, NW, db->d_perm, db->d_D, db->d_oseg,
+        own_bounds_kernel<<<grid_for(n + 1, 256, 148 * 8), 256, 0, s>>>(sk, n, NW, db->d_perm, db->d_D, db->d_oseg,
                                                                     db->d_prog);
         ++db->launches;
         STAGE("own group");

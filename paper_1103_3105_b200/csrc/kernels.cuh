@@ -189,6 +189,21 @@ __global__ void __launch_bounds__(256) ingest_kernel(DevDb db, uint32_t* pw, uin
 // =====================================================================================
 constexpr int SC_THREADS = 256, SC_ITEMS = 16, SC_TILE = SC_THREADS * SC_ITEMS;
 
+// a thread's 16 consecutive u32 (a run starts at a multiple of 16 elements; the caller checks
+// the array's 16-B alignment) as four 16-B accesses
+__device__ __forceinline__ void load16(const uint32_t* p, uint32_t (&v)[SC_ITEMS]) {
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS / 4; ++q) {
+        const uint4 x = reinterpret_cast<const uint4*>(p)[q];
+        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+}
+__device__ __forceinline__ void store16(uint32_t* p, const uint32_t (&v)[SC_ITEMS]) {
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS / 4; ++q)
+        reinterpret_cast<uint4*>(p)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* in, uint32_t* out, const uint32_t* n_ptr,
                                                           uint32_t n_host, LookBack<uint32_t> lb, uint32_t epoch,
                                                           uint32_t* ticket, uint32_t* total_out) {
@@ -202,12 +217,18 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* in, ui
     if (tile >= ntiles) return;
     const uint64_t b = (uint64_t)tile * SC_TILE + threadIdx.x * SC_ITEMS;
     uint32_t v[SC_ITEMS];
+    // the thread's 16 values as 4 x 16-B accesses (arrays at a 16-B boundary; the per-table
+    // insert offsets of TPC-C sit at (n + 1)-word strides and take the scalar path)
+    const bool full = b + SC_ITEMS <= n && !(((uintptr_t)in | (uintptr_t)out) & 15);
+    if (full) {
+        load16(in + b, v);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k) v[k] = (b + k < n) ? in[b + k] : 0u;
+    }
     uint32_t s = 0;
 #pragma unroll
-    for (int k = 0; k < SC_ITEMS; ++k) {
-        v[k] = (b + k < n) ? in[b + k] : 0u;
-        s += v[k];
-    }
+    for (int k = 0; k < SC_ITEMS; ++k) s += v[k];
     uint32_t tot;
     uint32_t ex = block_scan_excl<uint32_t, OpAddU32>(s, tot, sm);
     if (warp_id() == 0) {
@@ -216,6 +237,16 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* in, ui
     }
     __syncthreads();
     uint32_t run = s_pre + ex;
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k) {
+            const uint32_t x = v[k];
+            v[k] = run;
+            run += x;
+        }
+        store16(out + b, v);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         if (b + k <= n) out[b + k] = run;
@@ -239,13 +270,21 @@ __global__ void __launch_bounds__(SC_THREADS) scan2_kernel(const uint32_t* inX, 
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
     const uint64_t b = (uint64_t)tile * SC_TILE + threadIdx.x * SC_ITEMS;
-    uint2 v[SC_ITEMS];
+    uint32_t vx[SC_ITEMS], vy[SC_ITEMS];
+    const bool full = b + SC_ITEMS <= n && !(((uintptr_t)inX | (uintptr_t)inY | (uintptr_t)outX | (uintptr_t)outY) & 15);
+    if (full) {
+        load16(inX + b, vx);
+        load16(inY + b, vy);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k) {
+            vx[k] = b + k < n ? inX[b + k] : 0u;
+            vy[k] = b + k < n ? inY[b + k] : 0u;
+        }
+    }
     uint2 sum = make_uint2(0u, 0u);
 #pragma unroll
-    for (int k = 0; k < SC_ITEMS; ++k) {
-        v[k] = (b + k < n) ? make_uint2(inX[b + k], inY[b + k]) : make_uint2(0u, 0u);
-        sum = OpAddU2::combine(sum, v[k]);
-    }
+    for (int k = 0; k < SC_ITEMS; ++k) sum = OpAddU2::combine(sum, make_uint2(vx[k], vy[k]));
     uint2 tot;
     uint2 ex = block_scan_excl<uint2, OpAddU2>(sum, tot, sm);
     if (warp_id() == 0) {
@@ -254,11 +293,24 @@ __global__ void __launch_bounds__(SC_THREADS) scan2_kernel(const uint32_t* inX, 
     }
     __syncthreads();
     uint2 run = OpAddU2::combine(s_pre, ex);
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k) {
+            const uint32_t x = vx[k], y = vy[k];
+            vx[k] = run.x;
+            vy[k] = run.y;
+            run.x += x;
+            run.y += y;
+        }
+        store16(outX + b, vx);
+        store16(outY + b, vy);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         if (b + k <= n) { outX[b + k] = run.x; outY[b + k] = run.y; }
         if (b + k == n) { *totX = run.x; *totY = run.y; }
-        run = OpAddU2::combine(run, v[k]);
+        run = OpAddU2::combine(run, make_uint2(vx[k], vy[k]));
     }
 }
 
@@ -2007,16 +2059,15 @@ __global__ void __launch_bounds__(256) own_bounds_kernel(const uint64_t* __restr
                                                          uint32_t nw, const uint32_t* __restrict__ perm,
                                                          const uint32_t* __restrict__ D, uint32_t* oseg,
                                                          uint32_t* prog) {
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w <= nw; w += gridDim.x * blockDim.x) {
-        uint32_t a = 0, b = n;
-        while (a < b) {
-            const uint32_t m = (a + b) >> 1;
-            if ((uint32_t)(skeys[m] >> 32) < w) a = m + 1; else b = m;
-        }
-        oseg[w] = a;
-        if (w < nw) {
-            const bool any = a < n && (uint32_t)(skeys[a] >> 32) == w;
-            prog[w] = any ? D[perm[(uint32_t)skeys[a]]] : OWN_INF;
+    // one pass over the owner-sorted keys: position i starts the segments of the owners in
+    // (owner(i-1), owner(i)] (empty ones included), so every oseg[w] / prog[w] is written once
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        const uint32_t prev = i ? (uint32_t)(__ldg(&skeys[i - 1]) >> 32) + 1u : 0u;
+        const uint64_t k = i < n ? __ldg(&skeys[i]) : 0ull;
+        const uint32_t cur = i < n ? (uint32_t)(k >> 32) : nw;
+        for (uint32_t w = prev; w <= cur; ++w) {
+            oseg[w] = i;
+            if (w < nw) prog[w] = w == cur ? D[perm[(uint32_t)k]] : OWN_INF;
         }
     }
 }

@@ -576,7 +576,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         hbuf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
         dbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         best = 1e9
-        for _ in range(3):
+        for _ in range(10):                        # (the first copies of a fresh pinned buffer are slow)
             torch.cuda.synchronize()
             c0 = torch.cuda.Event(enable_timing=True)
             c1 = torch.cuda.Event(enable_timing=True)
@@ -588,6 +588,30 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
         pcie[name] = nbytes / (best / 1e3) / 1e9
         del hbuf, dbuf
     pcie["transfer_floor_ms"] = max(h2d / pcie["h2d_gbs"], d2h / pcie["d2h_gbs"]) / 1e6
+    # both directions at once on two streams, as the overlapped e2e step moves them (a
+    # direction alone is faster than the two together on this link)
+    hi, di = torch.empty(h2d, dtype=torch.uint8).pin_memory(), torch.empty(h2d, dtype=torch.uint8, device=dev)
+    ho, do = torch.empty(d2h, dtype=torch.uint8).pin_memory(), torch.empty(d2h, dtype=torch.uint8, device=dev)
+    sa, sb = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = 1e9
+    for _ in range(10):
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        sa.wait_event(c0)
+        sb.wait_event(c0)
+        with torch.cuda.stream(sa):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(sb):
+            ho.copy_(do, non_blocking=True)
+        stream.wait_stream(sa)
+        stream.wait_stream(sb)
+        c1.record(stream)
+        c1.synchronize()
+        best = min(best, c0.elapsed_time(c1))
+    pcie["bidir_floor_ms"] = best
+    del hi, di, ho, do
 
     # ---- other strategies on the same bulks ------------------------------------------
     others = {}

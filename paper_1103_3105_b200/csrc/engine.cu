@@ -2819,6 +2819,18 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
         CK(cudaEventRecord(db->ev_in[sl], db->st_h2d));
         return GPUTX_OK;
     };
+    // GPUTX_PIPE_TRACE: per bulk, event times (ms from the first) of H2D end, exec start,
+    // exec end and D2H end, printed after the run
+    static const bool ptrace = getenv("GPUTX_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> pev;
+    auto pmark = [&](cudaStream_t st_) {
+        if (!ptrace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st_);
+        pev.push_back(e);
+    };
+    if (ptrace) pmark(s);
     gputx_status hst = GPUTX_OK;               // a host-detected error stops enqueueing
     uint64_t done = 0;
     int last = 0;
@@ -2837,6 +2849,7 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
         std::swap(db->d_status, db->res_status[sl]);
         std::swap(db->d_out, db->res_out[sl]);
         CK(cudaEventRecord(db->ev_in_free[sl], s));
+        pmark(s);                              // exec start (its inputs and result slot ready)
         const uint64_t n = bulks[i].n;
         const uint32_t words = n ? bulks[i].param_off[n] : 0;
         // submit without the round trip (finish_submit's device half)
@@ -2869,11 +2882,13 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
         ob[i] = db->out_bytes;
         done = i + 1;
         CK(cudaEventRecord(db->ev_res[sl], s));
+        pmark(s);                              // exec end
         CK(cudaStreamWaitEvent(db->st_d2h, db->ev_res[sl], 0));
         if (n && status && status[i]) CK(cudaMemcpyAsync(status[i], db->d_status, n, cudaMemcpyDeviceToHost, db->st_d2h));
         if (n && out && out[i] && db->out_bytes)
             CK(cudaMemcpyAsync(out[i], db->d_out, db->out_bytes, cudaMemcpyDeviceToHost, db->st_d2h));
         CK(cudaEventRecord(db->ev_res_free[sl], db->st_d2h));
+        pmark(db->st_d2h);                     // D2H end
         std::swap(db->d_status, db->res_status[sl]);
         std::swap(db->d_out, db->res_out[sl]);
     }
@@ -2882,6 +2897,16 @@ gputx_status run_bulks_pipe(gputx_db* db, const gputx_bulk* bulks, uint64_t k, u
     for (int sl = 0; sl < 2; ++sl) CK(cudaStreamWaitEvent(s, db->ev_res_free[sl], 0));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    if (ptrace) {                              // rows: exec start, exec end, D2H end per bulk
+        for (size_t j = 1; j < pev.size(); ++j) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pev[0], pev[j]);
+            fprintf(stderr, "%s%.3f", (j - 1) % 3 == 0 ? "\n[pipe] " : " ", ms);
+            cudaEventDestroy(pev[j]);
+        }
+        fprintf(stderr, "\n");
+        if (!pev.empty()) cudaEventDestroy(pev[0]);
+    }
     if (done) {                                // gputx_read_results: the last bulk's results
         std::swap(db->d_status, db->res_status[last]);
         std::swap(db->d_out, db->res_out[last]);

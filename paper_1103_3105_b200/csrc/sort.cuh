@@ -20,6 +20,7 @@ constexpr int RS_WK = 32 * RS_ITEMS;               // keys per warp
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per tile
 constexpr int RS_MAXPASS = 5;
 constexpr int RS_HIST_GRID = 148 * 8;            // (296 blocks: 160 us for 12 M keys, latency-bound)
+constexpr int RS_HU = 8;                           // histogram: keys in flight per thread
 constexpr int RS_LB = 8;                           // look-back window (tiles per round trip)
 
 struct SortWs {
@@ -38,14 +39,34 @@ __global__ void __launch_bounds__(256) rs_hist_kernel(const uint64_t* __restrict
     for (uint32_t i = threadIdx.x; i < RS_MAXPASS * 256; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     const uint32_t n = *n_ptr;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31) & ~31u); i += gridDim.x * blockDim.x) {
-        const bool valid = i < n;
-        const uint64_t k = valid ? __ldg(&keys[i]) : 0;
-        for (uint32_t p = 0; p < npass; ++p) {
-            const uint32_t w = min(8u, nbits - 8 * p);
-            const uint32_t d = valid ? (uint32_t)(k >> (lo + 8 * p)) & ((1u << w) - 1) : 0x100u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (d < 256 && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&h[p][d], __popc(peers));
+    // RS_HU keys per thread in flight (grid-stride apart): one DRAM round trip per RS_HU keys
+    // instead of one per key (12 M keys: 219 us latency-bound with one)
+    const uint32_t nr = (n + 31) & ~31u, stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < nr; base += stride * RS_HU) {
+        uint64_t k[RS_HU];
+#pragma unroll
+        for (int u = 0; u < RS_HU; ++u) {
+            const uint64_t i = (uint64_t)base + (uint64_t)u * stride;
+            k[u] = i < n ? __ldg(&keys[i]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RS_HU; ++u) {
+            const uint64_t i = (uint64_t)base + (uint64_t)u * stride;
+            if (i - lane_id() >= nr) break;                 // warp-uniform (stride and nr are multiples of 32)
+            const bool valid = i < n;
+            for (uint32_t p = 0; p < npass; ++p) {
+                const uint32_t w = min(8u, nbits - 8 * p);
+                const uint32_t d = valid ? (uint32_t)(k[u] >> (lo + 8 * p)) & ((1u << w) - 1) : 0x100u;
+                // a digit the whole warp shares (the high passes of clustered item ids): one
+                // add; else one shared-memory atomic per lane (no __match_any_sync: its
+                // throughput, not the loads, bounded this kernel)
+                const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+                if (__all_sync(0xffffffffu, d == d0)) {
+                    if (lane_id() == 0 && d0 < 256) atomicAdd(&h[p][d0], 32u);
+                } else if (d < 256) {
+                    atomicAdd(&h[p][d], 1u);
+                }
+            }
         }
     }
     __syncthreads();
@@ -62,6 +83,19 @@ __global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t* hist) {
     uint32_t v = h[threadIdx.x], tot;
     uint32_t ex = block_scan_excl<uint32_t, OpAddU32>(v, tot, sm);
     h[threadIdx.x] = ex;
+}
+
+// lanes holding the same 9-bit value (digit, or 0x100 past the end) as this lane: the
+// __match_any_sync result from 9 ballots (MATCH's issue rate bounded the passes)
+DEV uint32_t rs_peers(uint32_t d) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
 }
 
 DEV uint64_t rs_pack(uint32_t epoch, uint32_t kind, uint32_t v) {
@@ -107,7 +141,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_pass_kernel(const uint64_t* __r
     for (int j = 0; j < ITEMS; ++j) {
         const uint64_t i = wbase + j * 32 + lane;
         const uint32_t d = i < n ? (uint32_t)(key[j] >> shift) & mask : 0x100u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = rs_peers(d);
         const int leader = __ffs(peers) - 1;
         uint32_t old = 0;
         if ((int)lane == leader && d < 256) {

@@ -1,6 +1,6 @@
 // sort.cuh — stable LSD radix sort of u64 keys on a bit range, onesweep style:
 // one histogram pass over the keys for all digit passes, then per 8-bit digit pass a
-// single kernel that ranks a 4096-key tile (warp multi-split with __match_any_sync),
+// single kernel that ranks a 4096-key tile (warp multi-split from per-bit ballots),
 // obtains the tile's global digit offsets by decoupled look-back, stages the tile in
 // shared memory in digit order and writes it out coalesced.
 //

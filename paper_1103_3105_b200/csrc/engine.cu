@@ -243,6 +243,7 @@ struct gputx_db {
     // owner-local K-SET rounds: GPUTX_KSET_OWN=0 restores the global rounds
     int kset_own = 1;
     int kset_chain = 1;                // TPC-B: K-SET over spine chains (GPUTX_KSET_CHAIN=0: owner warps)
+    int chain_runs = 1;                // lane-parallel deposit runs (GPUTX_CHAIN_RUNS=0: lane 0 only)
     int own_pipe = 1;                  // owner-local rounds staged through the perm (GPUTX_OWN_PIPE=0: gather pass)
     bool kset_ran_own = false;
     int own_grid[2] = {0, 0};          // co-resident CTAs of the executor without / with waits
@@ -825,7 +826,7 @@ gputx_status kset_chain_exec(gputx_db* db, const DevDb& v) {
     uint32_t* done = db->d_cdone;
     uint32_t ep = db->chain_epoch;
     uint32_t* sc = db->d_sc;
-    uint32_t diag = db->kset_diag;
+    uint32_t diag = db->kset_diag | (db->chain_runs ? 0u : CHAIN_NO_RUNS);
     void* args[] = {&vv, &keys, &nrec, &heads, &nh, &loff, &links, &cpub, &done, &ep, &sc, &diag};
     const int grid = (int)((chain_bound<S>(db) + 3) / 4);           // one chain per warp, 4 per CTA
     TRY(launch_coop(db, (const void*)kset_chain_exec_kernel<S_TPCB>, std::max(1, grid), 128, args));
@@ -1717,6 +1718,7 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
     if (const char* e = getenv("GPUTX_KSET_DF")) db->kset_df = atoi(e);
     if (const char* e = getenv("GPUTX_KSET_OWN")) db->kset_own = atoi(e);
     if (const char* e = getenv("GPUTX_KSET_CHAIN")) db->kset_chain = atoi(e);
+    if (const char* e = getenv("GPUTX_CHAIN_RUNS")) db->chain_runs = atoi(e);
     if (const char* e = getenv("GPUTX_OWN_PIPE")) db->own_pipe = atoi(e);
     // diag 16384 (tests: arbitrary owners) needs (item, ts)-sorted records for the dependency pass
     if (schema == S_TM1 && (db->kset_diag & 16384u)) db->rank_stream = 0;

@@ -2469,6 +2469,7 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
 // waits for the members of OTHER chains it depends on (the spine rank's links: done[p] ==
 // epoch, acquire); a member another chain waits for publishes done[t] (release) after it.
 // =====================================================================================
+constexpr uint32_t CHAIN_NO_RUNS = 1u << 15;      // (engine-set diag bit: GPUTX_CHAIN_RUNS=0)
 template <int S>
 __global__ void __launch_bounds__(128) kset_chain_exec_kernel(DevDb db, const uint64_t* __restrict__ keys,
                                                               const uint32_t* nrec_ptr,
@@ -2539,7 +2540,7 @@ __global__ void __launch_bounds__(128) kset_chain_exec_kernel(DevDb db, const ui
         const uint32_t okl = __ballot_sync(FULL, S == S_TPCB && E.idx != OWN_INF && E.t == 0u && E.la == E.lb);
         const uint32_t dep0 = __ballot_sync(FULL, S == S_TPCB && E.idx != OWN_INF && E.t == 0u);
         for (uint32_t m = 0; m < cnt;) {
-            if (S == S_TPCB && !(diag & 1u) && (dep0 >> m & 1u)) {
+            if (S == S_TPCB && !(diag & (1u | CHAIN_NO_RUNS)) && (dep0 >> m & 1u)) {
                 const bool inr = lane >= m && lane < cnt;
                 const uint32_t peers = __match_any_sync(FULL, inr ? E.q[0] : 0xFFFFFFFFu - lane);
                 const uint32_t dup = __ballot_sync(FULL, inr && (peers & lanemask_lt() & ~((1u << m) - 1u)) != 0u);

@@ -42,12 +42,16 @@ def _open(dims, image, n, env):
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("jitter", [False, True])
-def test_chain_executor_parity(case, jitter):
+@pytest.mark.parametrize("runs", [True, False])
+def test_chain_executor_parity(case, jitter, runs):
     dims, n, kw = CASES[case]
     image = W.make_db(W.TPCB, dims, seed=1)
     bulk = W.make_bulk(W.TPCB, dims, n, seed=5, **kw)
     ref = oracle.run(W.TPCB, dims.dims, image, bulk)
-    db = _open(dims, image, n, {"GPUTX_KSET_DIAG": str(JITTER)} if jitter else {})
+    env = {"GPUTX_KSET_DIAG": str(JITTER)} if jitter else {}
+    if not runs:
+        env["GPUTX_CHAIN_RUNS"] = "0"
+    db = _open(dims, image, n, env)
     try:
         for rep in range(2 if jitter else 3):
             db.reset()

@@ -1629,8 +1629,9 @@ gputx_status gputx_open_db(const gputx_db_config* cfg, gputx_db** out) {
             return bail(st);
     }
     db->sort_ws.max_tiles = db->max_rec / (RS_THREADS * 8) + 2;     // sized for the smallest tile
-    // keys per thread of a sort tile: 12 for TPC-B's 12 M records (0.86 -> 0.81 ms), 16 else
-    db->sort_ws.items = schema == S_TPCB ? 12 : RS_ITEMS;
+    // keys per thread of a sort tile: 12 for TPC-B's 12 M records (0.70 / 0.60 / 0.65 ms at
+    // 8 / 12 / 16) and TPC-C's (0.34 / 0.29 / 0.31 ms), 16 else
+    db->sort_ws.items = schema == S_TPCB || schema == S_TPCC ? 12 : RS_ITEMS;
     if (const char* e = getenv("GPUTX_SORT_ITEMS")) db->sort_ws.items = (uint32_t)atoi(e);
     if ((st = dalloc(db, &db->sort_ws.hist, RS_MAXPASS * 256)) ||
         (st = dalloc(db, &db->sort_ws.status, db->sort_ws.max_tiles * 256)) ||

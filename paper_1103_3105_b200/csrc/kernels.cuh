@@ -2382,15 +2382,24 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
             const uint64_t item = key_item(keys[heads[c]]);
             int32_t ld = __ldcg(&last[c]);
             const bool alone = nh <= nw;                 // this warp's only chain: wait in place
+            // software pipeline over the chain's chunks: the keys of chunk i+2 and the link
+            // ranges of chunk i+1 are in flight while chunk i is resolved, so a chunk costs its
+            // scan (and its links' depth loads), not a keys -> link-range round trip chain
+            auto ldk = [&](uint32_t r) -> uint64_t {
+                if (r >= nrec) return ~0ull;
+                const uint64_t k = keys[r];
+                return key_item(k) == item ? k : ~0ull;
+            };
+            auto ldx = [&](uint64_t k, uint32_t& x, uint32_t& xe) {
+                x = xe = 0;
+                if (k != ~0ull) { const uint32_t t = key_idx(k); x = loff[t]; xe = loff[t + 1]; }
+            };
+            uint64_t kc = ldk(p + lane), kn = ldk(p + 32 + lane);
+            uint32_t xc, xec;
+            ldx(kc, xc, xec);
             while (true) {
-                const uint32_t r = p + lane;
-                bool mem = false;
-                uint32_t t = 0;
-                if (r < nrec) {
-                    const uint64_t k = keys[r];
-                    mem = key_item(k) == item;
-                    t = key_idx(k);
-                }
+                const bool mem = kc != ~0ull;
+                const uint32_t t = mem ? key_idx(kc) : 0u;
                 const uint32_t memmask = __ballot_sync(FULL, mem);
                 const uint32_t clen = memmask == FULL ? 32u : __ffs(~memmask) - 1;   // members in this chunk
                 if (clen == 0) {                         // chain done
@@ -2399,12 +2408,14 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
                     progress = true;
                     break;
                 }
+                const uint64_t kn2 = clen == 32 ? ldk(p + 64 + lane) : ~0ull;
+                uint32_t xn = 0, xen = 0;
+                if (clen == 32) ldx(kn, xn, xen);
                 // e = max over links of D[p] + 1 (or -1); a lane is blocked while some link's depth
                 // is not there yet.  Lanes [s0, clen) of the chunk are pending; a blocked chunk is
                 // re-polled in place (only the unresolved links), not reloaded: a hop between two
                 // chains then costs one L2 round trip
-                uint32_t x = 0, xe = 0;
-                if (lane < clen) { x = loff[t]; xe = loff[t + 1]; }
+                uint32_t x = lane < clen ? xc : 0u, xe = lane < clen ? xec : 0u;
                 int32_t e = -1;
                 uint32_t s0 = 0, spins = 0;
                 while (true) {
@@ -2442,7 +2453,12 @@ __global__ void __launch_bounds__(256) sp_walk_kernel(const uint64_t* __restrict
                 }
                 p += s0;
                 if (s0 < clen) break;                    // blocked: yield (or give up on the watchdog)
-                if (clen < 32) continue;                 // ended inside: the next iteration sees clen = 0
+                if (clen < 32) {                         // ended inside this chunk: chain done
+                    if (lane == 0) cur[c] = SP_UNSET;
+                    --left;
+                    break;
+                }
+                kc = kn; xc = xn; xec = xen; kn = kn2;
             }
             if (lane == 0 && __ldcg(&cur[c]) != SP_UNSET) { cur[c] = p; last[c] = ld; }
             __syncwarp();

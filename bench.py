@@ -110,11 +110,16 @@ def exec_bytes(schema: int, bulk, status: np.ndarray) -> int:
     return int(per.sum())
 
 
-def rank_bytes(schema: int, records: int, passes: int, n: int) -> int:
+def rank_bytes(schema: int, records: int, passes: int, n: int, kernel: str = "") -> int:
     """Iterated scan (TPC-B; TPC-C per window): per pass, read each sorted record (8 B) and gather
     its transaction's depth (4 B); plus the initial zeroing of D (4 B/txn).
     TM-1 streaming rank (one pass): read each record once (8 B), write D once per
-    transaction (4 B) after zeroing it (4 B)."""
+    transaction (4 B) after zeroing it (4 B).
+    Spine walk (TPC-B / TPC-C default, one pass over all records): each record read once (8 B)
+    by the last-write scan and the link passes, one depth access per record (4 B), plus the
+    zeroing of D (4 B/txn) -- the iterated-scan formula with one pass over the whole bulk."""
+    if kernel == "sp_walk_kernel":
+        return records * 12 + 4 * n
     if schema == W.TM1:
         return records * 8 + 8 * n
     if schema == W.TPCC:
@@ -636,8 +641,8 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     eff = last["strategy"]                                  # auto: the strategy Algorithm 1 chose
     nloc = b_last.n
     if last["rank_passes"]:
-        cand[rank_kernel_name(wl["schema"], wl.get("add_rule", False))] = (
-            rank_bytes(wl["schema"], last["records"], last["rank_passes"], nloc), phase["ms_rank"])
+        rk = rank_kernel_name(wl["schema"], wl.get("add_rule", False))
+        cand[rk] = (rank_bytes(wl["schema"], last["records"], last["rank_passes"], nloc, rk), phase["ms_rank"])
     if ws == 1:
         # K-SET's dataflow executor (TPC-C default, stats flag 2) runs the counter-lock kernels
         # owner-local rounds (TM-1 / TPC-B / micro default, stats flag 4) run kset_own_exec_kernel

@@ -2265,11 +2265,24 @@ __global__ void __launch_bounds__(SC_THREADS) lastw_kernel(const uint64_t* __res
     SegMax e[SC_ITEMS];
     SegMax agg = OpSegMax::identity();
     uint64_t prev_item = b > 0 && b - 1 < n ? key_item(keys[b - 1]) : ~0ull;
+    // the thread's 16 keys (128 B, 128-B aligned) as eight 16-B loads when all are in range
+    const bool full = b + SC_ITEMS <= n;
+    uint64_t kv[SC_ITEMS];
+    if (full) {
+#pragma unroll
+        for (int q = 0; q < SC_ITEMS / 2; ++q) {
+            const ulonglong2 x = reinterpret_cast<const ulonglong2*>(keys + b)[q];
+            kv[2 * q] = x.x; kv[2 * q + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k) kv[k] = b + k < n ? keys[b + k] : 0ull;
+    }
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         e[k] = OpSegMax::identity();
         if (b + k < n) {
-            const uint64_t key = keys[b + k];
+            const uint64_t key = kv[k];
             const uint64_t it = key_item(key);
             const bool head = b + k == 0 || it != prev_item;
             e[k] = SegMax{head ? 1u : 0u, key_mode(key) == 1u ? (int32_t)(2 * (b + k) + 1) : head ? (int32_t)(2 * (b + k)) : -1};
@@ -2286,10 +2299,20 @@ __global__ void __launch_bounds__(SC_THREADS) lastw_kernel(const uint64_t* __res
     }
     __syncthreads();
     SegMax run = OpSegMax::combine(s_pre, ex);
+    int32_t lv[SC_ITEMS];
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
-        if (b + k < n) lastw[b + k] = e[k].f ? -1 : run.v;     // exclusive (a head starts fresh)
+        lv[k] = e[k].f ? -1 : run.v;                            // exclusive (a head starts fresh)
         run = OpSegMax::combine(run, e[k]);
+    }
+    if (full) {
+#pragma unroll
+        for (int q = 0; q < SC_ITEMS / 4; ++q)
+            reinterpret_cast<int4*>(lastw + b)[q] = make_int4(lv[4 * q], lv[4 * q + 1], lv[4 * q + 2], lv[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SC_ITEMS; ++k)
+            if (b + k < n) lastw[b + k] = lv[k];
     }
 }
 

@@ -91,6 +91,46 @@ inline cudaError_t dev_fill(void* p, int value, size_t bytes, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// dev_copy2: two device-to-device copies in ONE launch (blockIdx.y = which), 16-B vectors
+// with four in flight per thread when both ends of a copy are 16-B aligned, bytes otherwise
+// (a D2D cudaMemcpyAsync of a device-resident bulk's types / offsets was ~40 us on TPC-B)
+struct CopySeg {
+    uint8_t* dst;
+    const uint8_t* src;
+    uint64_t bytes;
+};
+__global__ void __launch_bounds__(256) copy2_kernel(CopySeg a, CopySeg b) {
+    const CopySeg c = blockIdx.y ? b : a;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t done = 0;
+    if (!(((uintptr_t)c.dst | (uintptr_t)c.src) & 15u)) {
+        const uint64_t n16 = c.bytes / 16;
+        const uint4* s4 = reinterpret_cast<const uint4*>(c.src);
+        uint4* d4 = reinterpret_cast<uint4*>(c.dst);
+        for (uint64_t i = tid; i < n16; i += 4 * nt) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * nt < n16) v[u] = __ldg(&s4[i + u * nt]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * nt < n16) d4[i + u * nt] = v[u];
+        }
+        done = n16 * 16;
+    }
+    for (uint64_t i = done + tid; i < c.bytes; i += nt) c.dst[i] = c.src[i];
+}
+inline cudaError_t dev_copy2(void* d0, const void* s0, size_t b0, void* d1, const void* s1, size_t b1, cudaStream_t s) {
+    const size_t mx = b0 > b1 ? b0 : b1;
+    if (!mx) return cudaSuccess;
+    uint64_t blocks = (mx / 64 + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    copy2_kernel<<<dim3((unsigned)blocks, 2), 256, 0, s>>>(CopySeg{(uint8_t*)d0, (const uint8_t*)s0, b0},
+                                                          CopySeg{(uint8_t*)d1, (const uint8_t*)s1, b1});
+    return cudaGetLastError();
+}
+
 // Several fills in ONE launch (blockIdx.y = segment): the per-bulk bookkeeping fills
 // (counters, depth array, sort workspace, result buffers) otherwise cost a launch each.
 // The segments are filled concurrently: they must not overlap.

@@ -1920,13 +1920,18 @@ gputx_status gputx_submit_bulk(gputx_db* db, const gputx_bulk* b, uint64_t* firs
     cudaEventRecord(db->ev_sub[0], s);
     if (n) {   // (device bulks: ordered on the handle's stream; the words' count is read there)
         const cudaMemcpyKind kind = b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
-        CK(cudaMemcpyAsync(db->d_poff, b->param_off, (n + 1) * 4, kind, s));
+        if (b->on_device) {
+            CK(dev_copy2(db->d_type, b->type, n, db->d_poff, b->param_off, (n + 1) * 4, s));
+        } else {
+            CK(cudaMemcpyAsync(db->d_type, b->type, n, kind, s));
+            CK(cudaMemcpyAsync(db->d_poff, b->param_off, (n + 1) * 4, kind, s));
+        }
         if (n_words && !b->on_device) CK(cudaMemcpyAsync(db->d_pw, b->param_words, (uint64_t)n_words * 4, kind, s));
         if (b->ts) CK(cudaMemcpyAsync(db->d_ts, b->ts, n * 4, kind, s));
     }
     db->first_ts = db->next_ts;
     TRY(finish_submit(db, n, n_words, n && b->on_device ? b->param_words : nullptr));
+    if (n && b->on_device) ++db->launches;     // (the copy kernel, before finish_submit's reset)
     if (!b->ts) db->next_ts += n;
     if (first_ts) *first_ts = db->first_ts;
     return GPUTX_OK;

@@ -577,7 +577,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
     # the link the e2e number is bound by: pinned copies of one step's bytes, each direction
     # alone (outside every timed region); the overlapped e2e step can't beat max(H2D, D2H)
     pcie = {}
-    for name, nbytes, hd in (("h2d_gbs", h2d, True), ("d2h_gbs", d2h, False)):
+    for pkey, nbytes, hd in (("h2d_gbs", h2d, True), ("d2h_gbs", d2h, False)):
         hbuf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
         dbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         best = 1e9
@@ -590,7 +590,7 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
             c1.record(stream)
             c1.synchronize()
             best = min(best, c0.elapsed_time(c1))
-        pcie[name] = nbytes / (best / 1e3) / 1e9
+        pcie[pkey] = nbytes / (best / 1e3) / 1e9
         del hbuf, dbuf
     pcie["transfer_floor_ms"] = max(h2d / pcie["h2d_gbs"], d2h / pcie["d2h_gbs"]) / 1e6
     # both directions at once on two streams, as the overlapped e2e step moves them (a
@@ -651,6 +651,10 @@ def measure(args, name, ws, rank, dist, dev, stream, clk, headline: bool):
               if eff == "kset" and (fl & 2) else "kset_chain_exec_kernel" if eff == "kset" and (fl & 16)
               else "kset_own_pipe_kernel" if eff == "kset" and (fl & 4) else f"{eff}_exec_kernel")
         cand[ek] = (exec_bytes(wl["schema"], b_last, st_host), phase["ms_exec"])
+    if last["records"] and phase["ms_sort"] > 0:
+        # the (item, ts) radix sort (the sort phase: histogram + digit passes): a sort's
+        # algorithmic floor is one read and one write of every 8-B record
+        cand["rs_pass_kernel"] = (16 * last["records"], phase["ms_sort"])
     kname = max(cand, key=lambda k: cand[k][1]) if cand else None
     roofline = None
     if kname:

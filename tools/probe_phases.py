@@ -14,6 +14,8 @@ strategy = sys.argv[2] if len(sys.argv) > 2 else "kset"
 wl = bench.WORKLOADS[name]
 dims, image, bulks = bench.make_inputs(wl, 0, 1, 3, 1)
 db = Database(wl["schema"], dims.dims, wl["n"], image, insert_capacity=40, packed_out=True)
+if len(sys.argv) > 3:                                  # executor grid cap (CTAs)
+    db.set_launch(exec_grid=int(sys.argv[3]))
 dev = torch.device("cuda:0")
 dbk = [(torch.from_numpy(b.type).to(dev), torch.from_numpy(b.param_off.view(np.int32)).to(dev),
         torch.from_numpy(b.param_words.view(np.int32)).to(dev)) for b in bulks]
